@@ -1,0 +1,183 @@
+/*
+ * whb200 — B200-native (sm_100a) WaveHoltz explicit iteration, C ABI.
+ *
+ * This is the drop-in boundary under the reference package's Python
+ * solve/iterate surface (waveholtz 0.1.0).  The reference has no FFI of its
+ * own: its boundary is the Python function surface resolved by module-level
+ * name lookup (driver.py:38 imports wave_solve_filtered by name), so each
+ * entry point below states which reference function (file:line under
+ * /root/reference/pkg/src/waveholtz) it replaces.  The Python host package
+ * paper_2504_03074_b200 binds these with ctypes.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no torch or CUDA types in signatures.
+ *  - Every call returns 0 on success or a negative WHB_E* code; the message
+ *    of the last failure on the calling thread is whb_last_error().
+ *  - Host pointers are borrowed for the duration of the call only.
+ *  - Fields are float64, C-contiguous in grid.shape with 'ij' indexing
+ *    (grid.py:109-112); Dirichlet boundary points are exactly 0.
+ *  - All per-step scalars (cos(wt*(n*dt)), (cos-alpha/2)*sigma, dt^2/2, dt^2,
+ *    (2/Tbar)*dt, stencil coefficients (1,-2,1)/dx^2, c^2) are computed by the
+ *    caller exactly as the reference computes them (timestep.py:134-145,
+ *    250-301; grid.py:302-306, 366) so device libm never enters the results.
+ *    The kernels are compiled without FMA contraction, so iterates are
+ *    bitwise identical to the reference.
+ *  - A context lives on one device and owns all of its device buffers and
+ *    one CUDA stream; calls on one context must come from one host thread.
+ */
+#ifndef WHB200_H
+#define WHB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WHB_ABI_VERSION 1
+
+enum whb_status {
+    WHB_OK = 0,
+    WHB_E_ARG = -1,      /* invalid argument (Python: ValueError)             */
+    WHB_E_CUDA = -2,     /* CUDA runtime failure (Python: RuntimeError)       */
+    WHB_E_NOMEM = -3,    /* device/host allocation failed (MemoryError)       */
+    WHB_E_STATE = -4,    /* call out of order, e.g. no schedule set           */
+    WHB_E_NODEV = -5     /* no CUDA device visible                            */
+};
+
+/* Field slots of a batch member (per member unless shared). */
+enum whb_field {
+    WHB_V = 0,    /* iterate v (W^0 of a solve; FPI updates it in place)      */
+    WHB_F = 1,    /* forcing f(x) (shared by all members if shared_forcing)   */
+    WHB_WA = 2,   /* leapfrog buffer A (odd time levels)                      */
+    WHB_WB = 3,   /* leapfrog buffer B (even time levels >= 2)                */
+    WHB_ACC = 4,  /* running filter sum                                        */
+    WHB_OUT = 5   /* output of a plain/matvec solve                            */
+};
+
+/* What the last step of a filtered solve writes (timestep.py:300-301, driver.py:222-225, 256-262). */
+enum whb_out_mode {
+    WHB_OUT_PLAIN = 0, /* OUT = (2/Tbar)dt*acc                    — wave_solve_filtered  */
+    WHB_OUT_FPI = 1,   /* V <- (2/Tbar)dt*acc ; resid += (V_new - V_old)^2 — _iterate    */
+    WHB_OUT_AV = 2     /* OUT = V - (2/Tbar)dt*acc  (V = x, f ignored)     — A x = x - W(x,0) */
+};
+
+typedef struct whb_ctx whb_ctx;
+
+int whb_abi_version(void);
+const char *whb_last_error(void);
+int whb_device_count(int *count);
+
+/*
+ * Create a context for `nbatch` independent problems on one grid.
+ *   ndim in {1,2,3}; shape[ndim] = grid.shape (stored points, grid.py:85-94).
+ *   [plane_begin, plane_end): the global axis-0 planes this context owns
+ *   (slab decomposition); pass 0, shape[0] for the whole grid.  ndim==1
+ *   must own the whole grid.
+ *   shared_forcing != 0: one f for all members (batched frequencies, cfg 5).
+ * Replaces: CartesianGrid/GridField storage (grid.py:50-291) + WaveState
+ * (timestep.py:111-129) buffers.
+ */
+int whb_create(whb_ctx **out, int device, int ndim, const int64_t *shape, int64_t plane_begin,
+               int64_t plane_end, int nbatch, int shared_forcing);
+int whb_destroy(whb_ctx *ctx);
+
+/* c^2 * Laplacian_h coefficients per axis: clo[a] = 1/dx_a^2, cmid[a] = -2/dx_a^2
+ * (stencil_coefficients, grid.py:302-306) and c2 = c**2 (grid.py:366).
+ * Replaces DiscreteOperator (grid.py:309-368), order p = 2, all-Dirichlet. */
+int whb_set_operator(whb_ctx *ctx, const double *clo, const double *cmid, double c2);
+
+/* Per-member time schedule of one filtered solve (n_total = N_p*N_t steps):
+ *   cos_f[n_total]   cos(wt*(n*dt)) forcing factor of step n (entry 0 unused)
+ *   acc_c[n_total+1] (cos(wt*(n*dt)) - alpha/2)*sigma_n filter weights
+ * Replaces the scalar part of wave_solve_filtered/step_explicit
+ * (timestep.py:134-145, 271-300) with correct_explicit (timestep.py:78-97). */
+int whb_set_schedule(whb_ctx *ctx, int member, int n_total, double half_dt2, double dt2,
+                     const double *cos_f, const double *acc_c, double out_scale);
+
+/* Field I/O.  `host` holds the owned planes [plane_begin, plane_end) of the
+ * field, C-contiguous.  Upload re-zeroes Dirichlet boundary points
+ * (GridField.set_values, grid.py:218-227).  member is ignored for a shared f. */
+int whb_upload(whb_ctx *ctx, int field, int member, const double *host);
+int whb_download(whb_ctx *ctx, int field, int member, double *host);
+int whb_zero(whb_ctx *ctx, int field, int member);
+
+/* One filtered solve W(v, f) for every member, device resident
+ * (wave_solve_filtered, timestep.py:250-301, explicit branch).
+ *   zero_forcing != 0: f treated as 0 (waveholtz_operator, driver.py:254-258).
+ *   resid_sq (host, nbatch entries, may be NULL): WHB_OUT_FPI only,
+ *   sum over owned points of (v_new - v_old)^2 (driver.py:225 before sqrt). */
+int whb_filtered_solve(whb_ctx *ctx, int out_mode, int zero_forcing, double *resid_sq);
+
+/* `iters` fixed-point passes v <- W(v, f) for all members (driver.py:211-230).
+ * resid_sq_out[iters*nbatch] (host, may be NULL) receives sum (v_{k+1}-v_k)^2
+ * per iteration and member (the caller divides by N and takes sqrt).
+ * tol_sq >= 0: stop after the first iteration whose resid_sq <= tol_sq for
+ * every member (checked on the host each iteration); tol_sq < 0: run all
+ * iterations with no host synchronisation in between.
+ * iters_done (may be NULL) receives the number of passes run. */
+int whb_fpi(whb_ctx *ctx, int iters, double tol_sq, double *resid_sq_out, int *iters_done);
+
+/* End-to-end single-member pass with host buffers (member 0): copy v_host
+ * H2D, v <- W(v, f), copy v D2H into v_out_host, resid_sq as in whb_fpi.
+ * The drop-in for one call of wave_solve_filtered inside _iterate
+ * (driver.py:222-225) with host GridFields. */
+int whb_iterate_host(whb_ctx *ctx, const double *v_host, double *v_out_host, double *resid_sq);
+
+/* ---- Krylov vectors (gmres_solve, linalg.py:102-183; member 0 only) ------
+ * Vector ids >= 0 name full-grid device vectors with the field layout.
+ * Slots: id WHB_V..WHB_OUT alias the member-0 fields; ids >= 8 are extra
+ * vectors reserved with whb_vec_reserve.  Reductions are deterministic
+ * (fixed-order tree), over owned points. */
+int whb_vec_reserve(whb_ctx *ctx, int count, int *first_id);
+int whb_vec_upload(whb_ctx *ctx, int id, const double *host);
+int whb_vec_download(whb_ctx *ctx, int id, double *host);
+int whb_vec_dot(whb_ctx *ctx, int x, int y, double *out);                    /* np.vdot, linalg.py:145 */
+int whb_vec_axpy(whb_ctx *ctx, double a, int x, int y);                       /* y += a*x, linalg.py:146 */
+int whb_vec_scale_into(whb_ctx *ctx, double a, int x, int y);                 /* y = x*a  */
+int whb_vec_div_into(whb_ctx *ctx, int x, double d, int y);                   /* y = x/d, linalg.py:150 */
+int whb_vec_lincomb(whb_ctx *ctx, int y, int first, int count, const double *coef); /* y += Q[:,first:first+count]@coef, linalg.py:174 */
+int whb_vec_sub_into(whb_ctx *ctx, int x, int y, int z);                      /* z = x - y */
+int whb_vec_copy(whb_ctx *ctx, int x, int y);                                 /* y = x */
+/* y = x - W(x, 0)  (waveholtz_operator.matvec, driver.py:256-262) */
+int whb_matvec(whb_ctx *ctx, int x, int y);
+
+/* ---- slab decomposition (multi-GPU) -------------------------------------
+ * Step-level control for halo exchange between contexts on different
+ * devices.  Step s of a solve advances W^s -> W^{s+1}.  A solve is
+ *   whb_solve_begin; for s: whb_step(s, region); ...; whb_solve_end.
+ * region 0 = all owned planes, 1 = the first and last owned planes only
+ * (the planes neighbours need), 2 = the remaining interior planes.
+ * whb_level_plane_ptr returns the device address of local plane `plane`
+ * (0 = low ghost, 1..nloc = owned, nloc+1 = high ghost) of the buffer that
+ * holds time level `level` of member 0 (level 0 = V). */
+int whb_solve_begin(whb_ctx *ctx, int out_mode, int zero_forcing);
+int whb_step(whb_ctx *ctx, int s, int region);
+int whb_solve_end(whb_ctx *ctx, double *resid_sq);
+int whb_level_plane_ptr(whb_ctx *ctx, int level, int64_t plane, uint64_t *dev_ptr, int64_t *plane_elems);
+int whb_stream_ptr(whb_ctx *ctx, uint64_t *stream);
+int whb_synchronize(whb_ctx *ctx);
+/* copy a plane between two contexts (same or peer device), ordered on src's
+ * stream then dst's (the single-process multi-shard path). */
+int whb_copy_plane(whb_ctx *src, int src_level, int64_t src_plane, whb_ctx *dst, int dst_level,
+                   int64_t dst_plane);
+
+/* ---- introspection -------------------------------------------------------- */
+/* Number of kernel launches issued by this context since creation. */
+int whb_launch_count(whb_ctx *ctx, int64_t *count);
+/* Per-launch average device time (ms) of the fused step kernel over the last
+ * whb_fpi/whb_filtered_solve call when timing is enabled (events on the
+ * context stream). */
+int whb_set_timing(whb_ctx *ctx, int enable);
+int whb_last_timing(whb_ctx *ctx, double *step_kernel_ms_total, int64_t *step_kernel_launches,
+                    double *solve_ms_total);
+/* Pinned host buffers for H2D/D2H at full PCIe rate. */
+int whb_host_alloc(void **ptr, int64_t bytes);
+int whb_host_free(void *ptr);
+/* Global and local geometry: shape3[3], pitch, nloc (owned planes). */
+int whb_geometry(whb_ctx *ctx, int64_t *shape3, int64_t *pitch, int64_t *nloc);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WHB200_H */

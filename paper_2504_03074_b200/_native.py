@@ -1,0 +1,330 @@
+"""ctypes binding of the C ABI in include/whb200.h (libwhb200.so, sm_100a).
+
+This is the only path to compute: there is no CPU fallback.  If the library
+is missing or no CUDA device is visible, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libwhb200.so")
+
+# enum whb_field / whb_out_mode (include/whb200.h)
+V, F, WA, WB, ACC, OUT = range(6)
+OUT_PLAIN, OUT_FPI, OUT_AV = 0, 1, 2
+E_ARG, E_CUDA, E_NOMEM, E_STATE, E_NODEV = -1, -2, -3, -4, -5
+
+#: every symbol include/whb200.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "whb_abi_version", "whb_last_error", "whb_device_count", "whb_create", "whb_destroy",
+    "whb_set_operator", "whb_set_schedule", "whb_upload", "whb_download", "whb_zero",
+    "whb_filtered_solve", "whb_fpi", "whb_iterate_host", "whb_vec_reserve", "whb_vec_upload",
+    "whb_vec_download", "whb_vec_dot", "whb_vec_axpy", "whb_vec_scale_into", "whb_vec_div_into",
+    "whb_vec_lincomb", "whb_vec_sub_into", "whb_vec_copy", "whb_matvec", "whb_solve_begin",
+    "whb_step", "whb_solve_end", "whb_level_plane_ptr", "whb_stream_ptr", "whb_synchronize",
+    "whb_copy_plane", "whb_launch_count", "whb_set_timing", "whb_last_timing", "whb_host_alloc",
+    "whb_host_free", "whb_geometry",
+)
+
+_lib = None
+
+
+class NativeError(RuntimeError):
+    """A whb_* call failed on the device side."""
+
+
+def load():
+    """Load libwhb200.so (fails loudly when the extension was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    c_int, c_double, c_i64, c_u64 = ctypes.c_int, ctypes.c_double, ctypes.c_int64, ctypes.c_uint64
+    vp, dp, ip64 = ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)
+    sig = {
+        "whb_abi_version": ([], c_int),
+        "whb_last_error": ([], ctypes.c_char_p),
+        "whb_device_count": ([ctypes.POINTER(c_int)], c_int),
+        "whb_create": ([ctypes.POINTER(vp), c_int, c_int, ip64, c_i64, c_i64, c_int, c_int], c_int),
+        "whb_destroy": ([vp], c_int),
+        "whb_set_operator": ([vp, dp, dp, c_double], c_int),
+        "whb_set_schedule": ([vp, c_int, c_int, c_double, c_double, dp, dp, c_double], c_int),
+        "whb_upload": ([vp, c_int, c_int, dp], c_int),
+        "whb_download": ([vp, c_int, c_int, dp], c_int),
+        "whb_zero": ([vp, c_int, c_int], c_int),
+        "whb_filtered_solve": ([vp, c_int, c_int, dp], c_int),
+        "whb_fpi": ([vp, c_int, c_double, dp, ctypes.POINTER(c_int)], c_int),
+        "whb_iterate_host": ([vp, dp, dp, dp], c_int),
+        "whb_vec_reserve": ([vp, c_int, ctypes.POINTER(c_int)], c_int),
+        "whb_vec_upload": ([vp, c_int, dp], c_int),
+        "whb_vec_download": ([vp, c_int, dp], c_int),
+        "whb_vec_dot": ([vp, c_int, c_int, dp], c_int),
+        "whb_vec_axpy": ([vp, c_double, c_int, c_int], c_int),
+        "whb_vec_scale_into": ([vp, c_double, c_int, c_int], c_int),
+        "whb_vec_div_into": ([vp, c_int, c_double, c_int], c_int),
+        "whb_vec_lincomb": ([vp, c_int, c_int, c_int, dp], c_int),
+        "whb_vec_sub_into": ([vp, c_int, c_int, c_int], c_int),
+        "whb_vec_copy": ([vp, c_int, c_int], c_int),
+        "whb_matvec": ([vp, c_int, c_int], c_int),
+        "whb_solve_begin": ([vp, c_int, c_int], c_int),
+        "whb_step": ([vp, c_int, c_int], c_int),
+        "whb_solve_end": ([vp, dp], c_int),
+        "whb_level_plane_ptr": ([vp, c_int, c_i64, ctypes.POINTER(c_u64), ip64], c_int),
+        "whb_stream_ptr": ([vp, ctypes.POINTER(c_u64)], c_int),
+        "whb_synchronize": ([vp], c_int),
+        "whb_copy_plane": ([vp, c_int, c_i64, vp, c_int, c_i64], c_int),
+        "whb_launch_count": ([vp, ip64], c_int),
+        "whb_set_timing": ([vp, c_int], c_int),
+        "whb_last_timing": ([vp, dp, ip64, dp], c_int),
+        "whb_host_alloc": ([ctypes.POINTER(vp), c_i64], c_int),
+        "whb_host_free": ([vp], c_int),
+        "whb_geometry": ([vp, ip64, ip64, ip64], c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = L
+    return L
+
+
+def check(rc: int, what: str = ""):
+    if rc == 0:
+        return
+    msg = load().whb_last_error().decode(errors="replace")
+    if rc == E_ARG:
+        raise ValueError(f"{what}: {msg}")
+    if rc == E_NOMEM:
+        raise MemoryError(f"{what}: {msg}")
+    raise NativeError(f"{what} failed ({rc}): {msg}")
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def device_count() -> int:
+    n = ctypes.c_int(0)
+    rc = load().whb_device_count(ctypes.byref(n))
+    return n.value if rc == 0 else 0
+
+
+class PinnedBuffer:
+    """Page-locked host float64 array (full-rate H2D/D2H)."""
+
+    def __init__(self, shape):
+        self.shape = tuple(int(s) for s in shape)
+        nbytes = int(np.prod(self.shape)) * 8
+        p = ctypes.c_void_p()
+        check(load().whb_host_alloc(ctypes.byref(p), nbytes), "whb_host_alloc")
+        self._ptr = p
+        buf = (ctypes.c_double * max(1, int(np.prod(self.shape)))).from_address(p.value)
+        self.array = np.frombuffer(buf, dtype=np.float64, count=int(np.prod(self.shape))).reshape(self.shape)
+
+    def free(self):
+        if self._ptr is not None and self._ptr.value:
+            load().whb_host_free(self._ptr)
+            self._ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class Context:
+    """Owns one whb_ctx: device buffers for `nbatch` problems on one grid (slab)."""
+
+    def __init__(self, shape, device=0, plane_range=None, nbatch=1, shared_forcing=False):
+        L = load()
+        self.shape = tuple(int(n) for n in shape)
+        self.ndim = len(self.shape)
+        if plane_range is None:
+            plane_range = (0, self.shape[0] if self.ndim > 1 else 1)
+        self.plane_range = (int(plane_range[0]), int(plane_range[1]))
+        self.nbatch = int(nbatch)
+        self.device = int(device)
+        h = ctypes.c_void_p()
+        shp = np.array(self.shape, dtype=np.int64)
+        check(L.whb_create(ctypes.byref(h), self.device, self.ndim, shp.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                           self.plane_range[0], self.plane_range[1], self.nbatch, int(bool(shared_forcing))),
+              "whb_create")
+        self._h = h
+        # owned part of a field, as host arrays see it
+        if self.ndim == 1:
+            self.local_shape = self.shape
+        else:
+            self.local_shape = (self.plane_range[1] - self.plane_range[0],) + self.shape[1:]
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            load().whb_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- configuration -------------------------------------------------------------
+    def set_operator(self, clo, cmid, c2):
+        clo = np.ascontiguousarray(clo, dtype=np.float64)
+        cmid = np.ascontiguousarray(cmid, dtype=np.float64)
+        check(load().whb_set_operator(self._h, _dp(clo), _dp(cmid), float(c2)), "whb_set_operator")
+
+    def set_schedule(self, member, sched):
+        cos_f = np.ascontiguousarray(sched["cos_f"], dtype=np.float64)
+        acc_c = np.ascontiguousarray(sched["acc_c"], dtype=np.float64)
+        check(load().whb_set_schedule(self._h, int(member), int(sched["n_total"]), float(sched["half_dt2"]),
+                                      float(sched["dt2"]), _dp(cos_f), _dp(acc_c), float(sched["out_scale"])),
+              "whb_set_schedule")
+
+    # -- fields --------------------------------------------------------------------
+    def _host(self, a):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        if a.shape != self.local_shape:
+            raise ValueError(f"shape {a.shape} does not match owned field shape {self.local_shape}")
+        return a
+
+    def upload(self, field, values, member=0):
+        a = self._host(values)
+        check(load().whb_upload(self._h, int(field), int(member), _dp(a)), "whb_upload")
+
+    def download(self, field, member=0, out=None):
+        out = np.empty(self.local_shape) if out is None else out
+        check(load().whb_download(self._h, int(field), int(member), _dp(out)), "whb_download")
+        return out
+
+    def zero(self, field, member=0):
+        check(load().whb_zero(self._h, int(field), int(member)), "whb_zero")
+
+    # -- solves --------------------------------------------------------------------
+    def filtered_solve(self, out_mode=OUT_PLAIN, zero_forcing=False):
+        r = np.zeros(self.nbatch)
+        check(load().whb_filtered_solve(self._h, int(out_mode), int(bool(zero_forcing)), _dp(r)),
+              "whb_filtered_solve")
+        return r
+
+    def fpi(self, iters, tol_sq=-1.0):
+        res = np.zeros(max(1, iters) * self.nbatch)
+        done = ctypes.c_int(0)
+        check(load().whb_fpi(self._h, int(iters), float(tol_sq), _dp(res), ctypes.byref(done)), "whb_fpi")
+        return res[: done.value * self.nbatch].reshape(done.value, self.nbatch)
+
+    def iterate_host(self, v_in, v_out):
+        r = np.zeros(1)
+        check(load().whb_iterate_host(self._h, _dp(v_in), _dp(v_out), _dp(r)), "whb_iterate_host")
+        return float(r[0])
+
+    # -- vectors -------------------------------------------------------------------
+    def vec_reserve(self, count):
+        first = ctypes.c_int(0)
+        check(load().whb_vec_reserve(self._h, int(count), ctypes.byref(first)), "whb_vec_reserve")
+        return list(range(first.value, first.value + count))
+
+    def vec_upload(self, vid, values):
+        a = self._host(values)
+        check(load().whb_vec_upload(self._h, int(vid), _dp(a)), "whb_vec_upload")
+
+    def vec_download(self, vid, out=None):
+        out = np.empty(self.local_shape) if out is None else out
+        check(load().whb_vec_download(self._h, int(vid), _dp(out)), "whb_vec_download")
+        return out
+
+    def dot(self, x, y) -> float:
+        r = ctypes.c_double(0.0)
+        check(load().whb_vec_dot(self._h, int(x), int(y), ctypes.byref(r)), "whb_vec_dot")
+        return r.value
+
+    def axpy(self, a, x, y):
+        check(load().whb_vec_axpy(self._h, float(a), int(x), int(y)), "whb_vec_axpy")
+
+    def scale_into(self, a, x, y):
+        check(load().whb_vec_scale_into(self._h, float(a), int(x), int(y)), "whb_vec_scale_into")
+
+    def div_into(self, x, d, y):
+        check(load().whb_vec_div_into(self._h, int(x), float(d), int(y)), "whb_vec_div_into")
+
+    def sub_into(self, x, y, z):
+        check(load().whb_vec_sub_into(self._h, int(x), int(y), int(z)), "whb_vec_sub_into")
+
+    def copy(self, x, y):
+        check(load().whb_vec_copy(self._h, int(x), int(y)), "whb_vec_copy")
+
+    def lincomb(self, y, first, coef):
+        coef = np.ascontiguousarray(coef, dtype=np.float64)
+        check(load().whb_vec_lincomb(self._h, int(y), int(first), len(coef), _dp(coef)), "whb_vec_lincomb")
+
+    def matvec(self, x, y):
+        check(load().whb_matvec(self._h, int(x), int(y)), "whb_matvec")
+
+    # -- step-level control (slab decomposition) ------------------------------------
+    def solve_begin(self, out_mode, zero_forcing=False):
+        check(load().whb_solve_begin(self._h, int(out_mode), int(bool(zero_forcing))), "whb_solve_begin")
+
+    def step(self, s, region=0):
+        check(load().whb_step(self._h, int(s), int(region)), "whb_step")
+
+    def solve_end(self):
+        r = ctypes.c_double(0.0)
+        check(load().whb_solve_end(self._h, ctypes.byref(r)), "whb_solve_end")
+        return r.value
+
+    def level_plane_ptr(self, level, plane):
+        p = ctypes.c_uint64(0)
+        n = ctypes.c_int64(0)
+        check(load().whb_level_plane_ptr(self._h, int(level), int(plane), ctypes.byref(p), ctypes.byref(n)),
+              "whb_level_plane_ptr")
+        return p.value, n.value
+
+    def stream_ptr(self) -> int:
+        p = ctypes.c_uint64(0)
+        check(load().whb_stream_ptr(self._h, ctypes.byref(p)), "whb_stream_ptr")
+        return p.value
+
+    def synchronize(self):
+        check(load().whb_synchronize(self._h), "whb_synchronize")
+
+    def copy_plane_to(self, src_level, src_plane, dst: "Context", dst_level, dst_plane):
+        check(load().whb_copy_plane(self._h, int(src_level), int(src_plane), dst._h, int(dst_level),
+                                    int(dst_plane)), "whb_copy_plane")
+
+    # -- introspection -------------------------------------------------------------
+    def launch_count(self) -> int:
+        n = ctypes.c_int64(0)
+        check(load().whb_launch_count(self._h, ctypes.byref(n)), "whb_launch_count")
+        return n.value
+
+    def set_timing(self, on=True):
+        check(load().whb_set_timing(self._h, int(bool(on))), "whb_set_timing")
+
+    def last_timing(self):
+        a = ctypes.c_double(0.0)
+        n = ctypes.c_int64(0)
+        b = ctypes.c_double(0.0)
+        check(load().whb_last_timing(self._h, ctypes.byref(a), ctypes.byref(n), ctypes.byref(b)),
+              "whb_last_timing")
+        return a.value, n.value, b.value
+
+    def geometry(self):
+        s = np.zeros(3, dtype=np.int64)
+        p = ctypes.c_int64(0)
+        n = ctypes.c_int64(0)
+        check(load().whb_geometry(self._h, s.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), ctypes.byref(p),
+                                  ctypes.byref(n)), "whb_geometry")
+        return tuple(int(x) for x in s), p.value, n.value

@@ -1,0 +1,1279 @@
+// whb200 — B200-native (sm_100a) WaveHoltz explicit iteration: kernels + C ABI.
+//
+// One CUDA context object (whb_ctx) per (device, grid slab, batch of
+// frequencies).  The hot path is ONE fused kernel per leapfrog step that, for
+// every owned interior point, (a) applies the 3/5/7-point c^2*Laplacian,
+// (b) advances the leapfrog update with forcing f*cos(w_e t^n), and (c) adds
+// the trapezoidal filter term to the accumulator — so W^n is read once per
+// step and never re-read for the filter.  The first
+// step additionally initialises the accumulator; the last step applies the
+// output scale and either writes the new iterate (plus the fixed-point
+// residual partial sums), the plain filtered field, or the GMRES mat-vec
+// x - W(x,0).
+//
+// Arithmetic order follows the reference exactly using
+// explicitly rounded __dadd_rn/__dmul_rn (no FMA contraction), so every
+// iterate is bitwise identical to waveholtz.timestep.wave_solve_filtered.
+//
+// Data layout in HBM: a field is stored as 3D
+// (planes, n1, pitch) float64, planes = owned axis-0 planes + 2 ghost planes,
+// row pitch = n2 rounded up to 16 elements (128 B) so every row starts on a
+// cache-line boundary.  2D grids (n0, n1) are stored as (n0, 1, n1) and 1D
+// grids (n) as (1, 1, n), so the same kernel marches along storage axis 0
+// with the contiguous axis across the warp.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/whb200.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string &msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define WHB_CUDA(call)                                                                          \
+    do {                                                                                        \
+        cudaError_t _e = (call);                                                                \
+        if (_e != cudaSuccess)                                                                  \
+            return fail(_e == cudaErrorMemoryAllocation ? WHB_E_NOMEM : WHB_E_CUDA,             \
+                        std::string(#call) + ": " + cudaGetErrorString(_e));                    \
+    } while (0)
+
+#define WHB_TRY(expr)          \
+    do {                       \
+        int _rc = (expr);      \
+        if (_rc) return _rc;   \
+    } while (0)
+
+// ------------------------------------------------------------------------------------------
+// device-side descriptors
+
+struct Geom {
+    long long S0;     // plane stride (elements)
+    int P;            // row pitch (elements)
+    int n1, n2;       // extents of storage axes 1 and 2 (incl. boundary)
+    int j_lo, j_hi;   // update range on axis 1 ([0,1) when axis 1 is degenerate)
+    int use_c2;
+    double clo0, cmid0, clo1, cmid1, clo2, cmid2, c2;
+};
+
+struct Member {
+    double *v;              // W^0 / iterate
+    const double *f;        // forcing or nullptr (zero forcing)
+    double *wa, *wb, *acc;  // leapfrog pair + filter accumulator
+    double *dst;            // output of the last step (== v for FPI)
+    const double *cos_f;    // [n_total]
+    const double *acc_c;    // [n_total + 1]
+    double half_dt2, dt2, out_scale;
+    int n_total;
+    int out_mode;
+    double *partials;       // residual partial sums (FPI)
+    int idx;                // member index (table order is by n_total, descending)
+    int pad_;
+};
+
+enum { K_FIRST = 0, K_MID = 1, K_LAST = 2 };
+
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+
+// Fused leapfrog + filter march over planes [i0, i1) of one (j, k) column.
+template <int KIND, bool ZF, bool A0, bool A1>
+__device__ __forceinline__ void march(const Geom &g, const Member &m, int s, int i0, int i1, int j,
+                                      int k, double &rsum) {
+    const double *__restrict__ wcur = (s == 0) ? m.v : ((s & 1) ? m.wa : m.wb);
+    const double *wprv = (s == 1) ? m.v : ((s & 1) ? m.wb : m.wa);
+    double *wnxt = ((s + 1) & 1) ? m.wa : m.wb;  // in place over W^{s-1} for s >= 2
+    const double *__restrict__ f = m.f;
+    double *acc = m.acc;
+    const double cosn = (KIND == K_FIRST) ? 1.0 : m.cos_f[s];
+    const double h = (KIND == K_FIRST) ? m.half_dt2 : m.dt2;
+    const double acc0 = m.acc_c[0];
+    const double accn = m.acc_c[s + 1];
+    const double sc = m.out_scale;
+    const long long S0 = g.S0;
+    const int P = g.P;
+
+    long long p = (long long)i0 * S0 + (long long)j * P + k;
+    double wm = A0 ? __ldg(wcur + p - S0) : 0.0;
+    double wc = __ldg(wcur + p);
+#pragma unroll 2
+    for (int i = i0; i < i1; ++i, p += S0) {
+        const double wp = A0 ? __ldg(wcur + p + S0) : 0.0;
+        const double xl = __ldg(wcur + p - 1);
+        const double xh = __ldg(wcur + p + 1);
+        double yl = 0.0, yh = 0.0;
+        if (A1) {
+            yl = __ldg(wcur + p - P);
+            yh = __ldg(wcur + p + P);
+        }
+        double fv = 0.0;
+        if (!ZF) fv = __ldg(f + p);
+        double wpv = 0.0;
+        if (KIND != K_FIRST) wpv = wprv[p];
+        double av = 0.0;
+        if (KIND != K_FIRST) av = acc[p];
+
+        // c^2 * Laplacian in reference order: out = 0; per axis: +lo, +mid, +hi (grid.py:357-366)
+        double lap = 0.0;
+        if (A0) {
+            lap = dadd(lap, dmul(g.clo0, wm));
+            lap = dadd(lap, dmul(g.cmid0, wc));
+            lap = dadd(lap, dmul(g.clo0, wp));
+        }
+        if (A1) {
+            lap = dadd(lap, dmul(g.clo1, yl));
+            lap = dadd(lap, dmul(g.cmid1, wc));
+            lap = dadd(lap, dmul(g.clo1, yh));
+        }
+        lap = dadd(lap, dmul(g.clo2, xl));
+        lap = dadd(lap, dmul(g.cmid2, wc));
+        lap = dadd(lap, dmul(g.clo2, xh));
+        if (g.use_c2) lap = dmul(lap, g.c2);
+
+        double wn;
+        if (KIND == K_FIRST) {
+            // w1 = w + (dt^2/2)*(lap - f)                        timestep.py:137
+            const double d = ZF ? lap : dsub(lap, fv);
+            wn = dadd(wc, dmul(h, d));
+        } else {
+            // w^{n+1} = (2w - w_prev) + dt^2*(lap - f*cos)       timestep.py:139-140
+            const double d = ZF ? lap : dsub(lap, dmul(fv, cosn));
+            wn = dadd(dsub(dmul(2.0, wc), wpv), dmul(h, d));
+        }
+        if (KIND == K_FIRST) {
+            // acc = c0*w0 ; acc += c1*w1                          timestep.py:284, 298
+            wnxt[p] = wn;
+            acc[p] = dadd(dmul(acc0, wc), dmul(accn, wn));
+        } else if (KIND == K_MID) {
+            wnxt[p] = wn;
+            acc[p] = dadd(av, dmul(accn, wn));
+        } else {
+            const double out = dmul(sc, dadd(av, dmul(accn, wn)));  // timestep.py:298-300
+            if (m.out_mode == WHB_OUT_FPI) {
+                const double vold = m.v[p];
+                const double dd = out - vold;
+                rsum += dd * dd;
+                m.v[p] = out;
+            } else if (m.out_mode == WHB_OUT_AV) {
+                m.dst[p] = dsub(m.v[p], out);  // driver.py:259
+            } else {
+                m.dst[p] = out;
+            }
+        }
+        wm = wc;
+        wc = wp;
+    }
+}
+
+template <int KIND, bool ZF, bool A0, bool A1>
+__device__ __forceinline__ void march_guarded(const Geom &g, const Member &m, int s, int i0, int i1,
+                                              int j, int k, bool act, double &rsum) {
+    if (act) march<KIND, ZF, A0, A1>(g, m, s, i0, i1, j, k, rsum);
+}
+
+__device__ __forceinline__ double block_sum(double v) {
+    __shared__ double red[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+    const int nw = (blockDim.x * blockDim.y + 31) >> 5;
+    if ((tid & 31) == 0) red[tid >> 5] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (tid < 32) {
+        t = (tid < nw) ? red[tid] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+    }
+    return t;  // valid in thread 0
+}
+
+// One leapfrog step s for every active batch member (blockIdx.z).
+// blockIdx.x: tile along the contiguous axis; blockIdx.y: (axis-1 tile, axis-0 chunk).
+template <bool A0, bool A1>
+__global__ void __launch_bounds__(256) step_kernel(Geom g, const Member *__restrict__ members, int s,
+                                                   int i_begin, int i_end, int chunk_len, int JT,
+                                                   int part_off) {
+    const Member m = members[blockIdx.z];
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int jt = blockIdx.y % JT;
+    const int ch = blockIdx.y / JT;
+    const int j = A1 ? jt * blockDim.y + threadIdx.y : 0;
+    const int i0 = i_begin + ch * chunk_len;
+    const int i1 = min(i_end, i0 + chunk_len);
+    const bool act = (k >= 1) && (k < g.n2 - 1) && (!A1 || (j >= g.j_lo && j < g.j_hi)) && (i0 < i1);
+    const int kind = (s == 0) ? K_FIRST : ((s == m.n_total - 1) ? K_LAST : K_MID);
+    const bool zf = (m.f == nullptr);
+    double rsum = 0.0;
+    if (kind == K_FIRST) {
+        if (zf) march_guarded<K_FIRST, true, A0, A1>(g, m, s, i0, i1, j, k, act, rsum);
+        else    march_guarded<K_FIRST, false, A0, A1>(g, m, s, i0, i1, j, k, act, rsum);
+    } else if (kind == K_MID) {
+        if (zf) march_guarded<K_MID, true, A0, A1>(g, m, s, i0, i1, j, k, act, rsum);
+        else    march_guarded<K_MID, false, A0, A1>(g, m, s, i0, i1, j, k, act, rsum);
+    } else {
+        if (zf) march_guarded<K_LAST, true, A0, A1>(g, m, s, i0, i1, j, k, act, rsum);
+        else    march_guarded<K_LAST, false, A0, A1>(g, m, s, i0, i1, j, k, act, rsum);
+        if (m.out_mode == WHB_OUT_FPI) {
+            const double t = block_sum(rsum);
+            if (threadIdx.x == 0 && threadIdx.y == 0)
+                m.partials[part_off + blockIdx.y * gridDim.x + blockIdx.x] = t;
+        }
+    }
+}
+
+// Deterministic residual reduction: hist[(*counter)*nb + b] = sum(partials_b[0:nparts]).
+__global__ void reduce_partials_kernel(const Member *__restrict__ members, int nb, int nparts,
+                                       double *hist, int *counter) {
+    __shared__ double red[32];
+    const int slot = *counter;
+    for (int b = 0; b < nb; ++b) {
+        const double *pp = members[b].partials;
+        double t = 0.0;
+        for (int i = threadIdx.x; i < nparts; i += blockDim.x) t += pp[i];
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            double u = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+            for (int o = 16; o > 0; o >>= 1) u += __shfl_down_sync(0xffffffffu, u, o);
+            if (threadIdx.x == 0) hist[(long long)slot * nb + members[b].idx] = u;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *counter = slot + 1;
+}
+
+// Zero the Dirichlet boundary (and keep padding zero) of owned planes [lp0, lp1).
+__global__ void zero_boundary_kernel(double *x, long long S0, int P, int n1, int n2, int act1,
+                                     int lp0, int lp1, int zero_plane_lo, int zero_plane_hi) {
+    const long long total = (long long)(lp1 - lp0) * S0;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long pl = t / S0;
+        const long long r = t - pl * S0;
+        const int j = (int)(r / P);
+        const int k = (int)(r - (long long)j * P);
+        const int plane = lp0 + (int)pl;
+        bool z = (k == 0) || (k >= n2 - 1);
+        if (act1) z = z || (j == 0) || (j == n1 - 1);
+        if (zero_plane_lo && plane == lp0) z = true;
+        if (zero_plane_hi && plane == lp1 - 1) z = true;
+        if (z) x[(long long)plane * S0 + r] = 0.0;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// vector kernels (owned planes only; padding and boundaries are zero in every vector)
+
+constexpr int kRedBlocks = 592;  // 4 x 148 SMs; fixed => deterministic reduction order
+constexpr int kRedThreads = 256;
+
+__global__ void dot_partials_kernel(const double *__restrict__ x, const double *__restrict__ y,
+                                    long long n, double *partials) {
+    double t = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        t += x[i] * y[i];
+    const double b = block_sum(t);
+    if (threadIdx.x == 0) partials[blockIdx.x] = b;
+}
+
+__global__ void final_sum_kernel(const double *__restrict__ partials, int n, double *out) {
+    double t = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) t += partials[i];
+    const double b = block_sum(t);
+    if (threadIdx.x == 0) *out = b;
+}
+
+// y -= h*x exactly as numpy's `w -= H[j,k]*Q[:,j]` (linalg.py:146): y = y - (h*x)
+__global__ void axmy_kernel(double h, const double *__restrict__ x, double *y, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        y[i] = __dsub_rn(y[i], __dmul_rn(h, x[i]));
+}
+
+__global__ void scale_kernel(double a, const double *__restrict__ x, double *y, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        y[i] = __dmul_rn(x[i], a);
+}
+
+__global__ void div_kernel(const double *__restrict__ x, double d, double *y, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        y[i] = __ddiv_rn(x[i], d);
+}
+
+__global__ void sub_kernel(const double *__restrict__ x, const double *__restrict__ y, double *z,
+                           long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        z[i] = __dsub_rn(x[i], y[i]);
+}
+
+constexpr int kMaxComb = 64;
+struct CombArgs {
+    const double *q[kMaxComb];
+    double c[kMaxComb];
+};
+
+// y = y + sum_j c_j q_j (sum accumulated in j order, then added to y: x + Q@y, linalg.py:174)
+__global__ void lincomb_kernel(CombArgs a, int count, double *y, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        double t = 0.0;
+        for (int jj = 0; jj < count; ++jj) t = __dadd_rn(t, __dmul_rn(a.q[jj][i], a.c[jj]));
+        y[i] = __dadd_rn(y[i], t);
+    }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------------
+// host context
+
+struct MemberHost {
+    double *v = nullptr, *f = nullptr, *wa = nullptr, *wb = nullptr, *acc = nullptr, *out = nullptr;
+    double *cos_f = nullptr, *acc_c = nullptr, *partials = nullptr;
+    double half_dt2 = 0, dt2 = 0, out_scale = 0;
+    int n_total = 0;
+};
+
+struct whb_ctx {
+    int device = 0;
+    int ndim = 0;
+    int64_t gshape[3] = {1, 1, 1};  // global storage shape (axis-0, axis-1, axis-2)
+    int64_t plane_begin = 0, plane_end = 1;
+    int64_t nloc = 1;               // owned planes
+    int64_t nplanes = 3;            // allocated planes (owned + 2 ghosts)
+    int P = 16;
+    int64_t S0 = 16;
+    int64_t field_elems = 0;        // nplanes * S0
+    int act0 = 0, act1 = 0;
+    int nbatch = 1;
+    int shared_f = 0;
+    Geom geom{};
+    bool op_set = false;
+    cudaStream_t stream = nullptr;
+    std::vector<MemberHost> mem;
+    double *shared_f_ptr = nullptr;
+    std::vector<double *> vecs;     // extra vectors (id 8 + i)
+    Member *d_members = nullptr;    // device member table
+    std::vector<Member> h_members;  // last uploaded
+    std::vector<int> order;         // table order: members sorted by n_total desc
+    double *d_hist = nullptr;
+    int hist_cap = 0;
+    int *d_counter = nullptr;
+    double *d_red = nullptr;        // vector reduction scratch (kRedBlocks + 1)
+    double *h_red = nullptr;        // pinned scalar
+    // launch geometry
+    int BX = 128, BY = 1, gx = 1, JT = 1, chunk_len = 1, nchunks = 1;
+    int upd_lo = 1, upd_hi = 2;     // local update planes [lo, hi)
+    int nparts = 1;
+    int64_t launches = 0;
+    // graphs keyed by (out_mode, zf)
+    std::map<std::pair<int, int>, cudaGraphExec_t> graphs;
+    bool use_graphs = true;
+    // timing
+    bool timing = false;
+    std::vector<cudaEvent_t> ev;
+    double t_step_ms = 0.0;
+    int64_t t_step_launches = 0;
+    double t_solve_ms = 0.0;
+    // step-level (slab) solve state
+    int cur_mode = -1, cur_zf = 0, cur_parts = 0;
+};
+
+namespace {
+
+int set_dev(whb_ctx *c) {
+    WHB_CUDA(cudaSetDevice(c->device));
+    return 0;
+}
+
+double *field_ptr(whb_ctx *c, int field, int member) {
+    MemberHost &m = c->mem[member];
+    switch (field) {
+        case WHB_V: return m.v;
+        case WHB_F: return c->shared_f ? c->shared_f_ptr : m.f;
+        case WHB_WA: return m.wa;
+        case WHB_WB: return m.wb;
+        case WHB_ACC: return m.acc;
+        case WHB_OUT: return m.out;
+        default: return nullptr;
+    }
+}
+
+int alloc_field(whb_ctx *c, double **p) {
+    WHB_CUDA(cudaMalloc(p, (size_t)c->field_elems * sizeof(double)));
+    WHB_CUDA(cudaMemsetAsync(*p, 0, (size_t)c->field_elems * sizeof(double), c->stream));
+    return 0;
+}
+
+int ensure_out(whb_ctx *c, int member) {
+    if (!c->mem[member].out) return alloc_field(c, &c->mem[member].out);
+    return 0;
+}
+
+double *vec_ptr(whb_ctx *c, int id) {
+    if (id >= 0 && id <= WHB_OUT) return field_ptr(c, id, 0);
+    const int e = id - 8;
+    if (e >= 0 && e < (int)c->vecs.size()) return c->vecs[e];
+    return nullptr;
+}
+
+// owned region [plane 1, plane nloc+1) of a field, as a flat element range
+inline double *owned(double *base, whb_ctx *c) { return base + c->S0; }
+inline long long owned_elems(whb_ctx *c) { return (long long)c->nloc * c->S0; }
+
+int occupancy_blocks(whb_ctx *c) {
+    int nb = 0;
+    cudaError_t e;
+    const int threads = c->BX * c->BY;
+    if (c->act1) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, step_kernel<true, true>, threads, 0);
+    else if (c->act0) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, step_kernel<true, false>, threads, 0);
+    else e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, step_kernel<false, false>, threads, 0);
+    if (e != cudaSuccess || nb < 1) nb = 4;
+    return nb;
+}
+
+int plan_launch(whb_ctx *c) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    c->BX = c->act1 ? 32 : 128;
+    c->BY = c->act1 ? 8 : 1;
+    const int64_t n1 = c->gshape[1], n2 = c->gshape[2];
+    c->gx = (int)((n2 - 1 + c->BX - 1) / c->BX);               // covers k in [0, n2-1)
+    c->JT = c->act1 ? (int)((n1 - 1 + c->BY - 1) / c->BY) : 1;  // covers j in [0, n1-1)
+    // local update planes: owned planes that are global-interior along axis 0
+    if (c->act0) {
+        const int64_t g_lo = std::max<int64_t>(c->plane_begin, 1);
+        const int64_t g_hi = std::min<int64_t>(c->plane_end, c->gshape[0] - 1);
+        c->upd_lo = (int)(g_lo - c->plane_begin + 1);
+        c->upd_hi = (int)std::max<int64_t>(g_hi - c->plane_begin + 1, c->upd_lo);
+    } else {
+        c->upd_lo = 1;
+        c->upd_hi = 2;
+    }
+    const int nplanes = std::max(1, c->upd_hi - c->upd_lo);
+    const int per_sm = occupancy_blocks(c);
+    const long long target = (long long)sms * per_sm * 2;  // ~2 waves
+    const long long tiles = (long long)c->gx * c->JT;
+    int nch = (int)std::max<long long>(1, target / std::max<long long>(1, tiles));
+    const char *env = getenv("WHB_CHUNK");
+    int cl = (nplanes + nch - 1) / nch;
+    const int min_chunk = c->act1 ? 4 : 8;
+    if (cl < min_chunk) cl = std::min(nplanes, min_chunk);
+    if (env && atoi(env) > 0) cl = atoi(env);
+    if (!c->act0) cl = 1;
+    c->chunk_len = cl;
+    c->nchunks = (nplanes + cl - 1) / cl;
+    if ((long long)c->JT * c->nchunks > 65535)
+        return fail(WHB_E_ARG, "grid too large for launch plan (axis-1 tiles x chunks > 65535)");
+    c->nparts = c->gx * c->JT * (c->nchunks + 2);
+    return 0;
+}
+
+int ensure_hist(whb_ctx *c, int iters) {
+    if (iters <= c->hist_cap) return 0;
+    if (c->d_hist) {
+        WHB_CUDA(cudaStreamSynchronize(c->stream));
+        WHB_CUDA(cudaFree(c->d_hist));
+    }
+    int cap = std::max(iters, 64);
+    WHB_CUDA(cudaMalloc(&c->d_hist, (size_t)cap * c->nbatch * sizeof(double)));
+    c->hist_cap = cap;
+    // graphs bake the hist pointer
+    for (auto &kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    c->graphs.clear();
+    return 0;
+}
+
+// Build the member table for a call and upload it if it changed.
+int upload_members(whb_ctx *c, int out_mode, int zf, const double *vx = nullptr, double *dst = nullptr) {
+    std::vector<Member> t(c->nbatch);
+    for (int pos = 0; pos < c->nbatch; ++pos) {
+        const int b = c->order[pos];
+        MemberHost &h = c->mem[b];
+        Member m{};
+        m.v = vx ? const_cast<double *>(vx) : h.v;
+        m.f = zf ? nullptr : (c->shared_f ? c->shared_f_ptr : h.f);
+        m.wa = h.wa;
+        m.wb = h.wb;
+        m.acc = h.acc;
+        if (out_mode == WHB_OUT_FPI) m.dst = m.v;
+        else {
+            if (dst) m.dst = dst;
+            else {
+                WHB_TRY(ensure_out(c, b));
+                m.dst = h.out;
+            }
+        }
+        m.cos_f = h.cos_f;
+        m.acc_c = h.acc_c;
+        m.half_dt2 = h.half_dt2;
+        m.dt2 = h.dt2;
+        m.out_scale = h.out_scale;
+        m.n_total = h.n_total;
+        m.out_mode = out_mode;
+        m.partials = h.partials;
+        m.idx = b;
+        t[pos] = m;
+    }
+    bool same = c->h_members.size() == t.size() &&
+                std::memcmp(c->h_members.data(), t.data(), t.size() * sizeof(Member)) == 0;
+    if (!same) {
+        // table is read by in-flight kernels: order the update on the stream
+        WHB_CUDA(cudaMemcpyAsync(c->d_members, t.data(), t.size() * sizeof(Member),
+                                 cudaMemcpyHostToDevice, c->stream));
+        WHB_CUDA(cudaStreamSynchronize(c->stream));  // t is pageable & local
+        c->h_members = t;
+    }
+    return 0;
+}
+
+int launch_step(whb_ctx *c, int s, int nact, int i_begin, int i_end, int chunk_len, int part_off) {
+    if (nact <= 0 || i_begin >= i_end) return 0;
+    const int nch = (i_end - i_begin + chunk_len - 1) / chunk_len;
+    dim3 grid(c->gx, c->JT * nch, nact);
+    dim3 block(c->BX, c->BY, 1);
+    if (c->act1)
+        step_kernel<true, true><<<grid, block, 0, c->stream>>>(c->geom, c->d_members, s, i_begin, i_end,
+                                                             chunk_len, c->JT, part_off);
+    else if (c->act0)
+        step_kernel<true, false><<<grid, block, 0, c->stream>>>(c->geom, c->d_members, s, i_begin, i_end,
+                                                              chunk_len, c->JT, part_off);
+    else
+        step_kernel<false, false><<<grid, block, 0, c->stream>>>(c->geom, c->d_members, s, i_begin, i_end,
+                                                               chunk_len, c->JT, part_off);
+    c->launches++;
+    WHB_CUDA(cudaGetLastError());
+    return 0;
+}
+
+int max_steps(whb_ctx *c) {
+    int mx = 0;
+    for (auto &m : c->mem) mx = std::max(mx, m.n_total);
+    return mx;
+}
+
+int active_members(whb_ctx *c, int s) {
+    int n = 0;
+    for (auto &m : c->mem) n += (m.n_total > s);
+    return n;
+}
+
+// Enqueue one full filtered solve (all steps + residual reduction).
+int enqueue_solve(whb_ctx *c, int out_mode) {
+    const int ns = max_steps(c);
+    for (int s = 0; s < ns; ++s)
+        WHB_TRY(launch_step(c, s, active_members(c, s), c->upd_lo, c->upd_hi, c->chunk_len, 0));
+    if (out_mode == WHB_OUT_FPI) {
+        reduce_partials_kernel<<<1, 1024, 0, c->stream>>>(c->d_members, c->nbatch,
+                                                          c->gx * c->JT * c->nchunks, c->d_hist,
+                                                          c->d_counter);
+        c->launches++;
+        WHB_CUDA(cudaGetLastError());
+    }
+    return 0;
+}
+
+int run_solve(whb_ctx *c, int out_mode, int zf) {
+    if (!c->use_graphs) return enqueue_solve(c, out_mode);
+    auto key = std::make_pair(out_mode, zf);
+    auto it = c->graphs.find(key);
+    if (it == c->graphs.end()) {
+        cudaGraph_t g;
+        const int64_t l0 = c->launches;
+        WHB_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        int rc = enqueue_solve(c, out_mode);
+        cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+        if (rc) return rc;
+        if (e != cudaSuccess) return fail(WHB_E_CUDA, std::string("capture: ") + cudaGetErrorString(e));
+        cudaGraphExec_t ge;
+        e = cudaGraphInstantiate(&ge, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return fail(WHB_E_CUDA, std::string("instantiate: ") + cudaGetErrorString(e));
+        c->launches = l0;
+        it = c->graphs.emplace(key, ge).first;
+    }
+    WHB_CUDA(cudaGraphLaunch(it->second, c->stream));
+    // account the kernels the graph launches
+    const int ns = max_steps(c);
+    c->launches += ns + (out_mode == WHB_OUT_FPI ? 1 : 0);
+    return 0;
+}
+
+int ensure_events(whb_ctx *c, int n) {
+    while ((int)c->ev.size() < n) {
+        cudaEvent_t e;
+        WHB_CUDA(cudaEventCreate(&e));
+        c->ev.push_back(e);
+    }
+    return 0;
+}
+
+int check_ready(whb_ctx *c) {
+    if (!c->op_set) return fail(WHB_E_STATE, "operator not set (whb_set_operator)");
+    for (int b = 0; b < c->nbatch; ++b)
+        if (c->mem[b].n_total < 2) return fail(WHB_E_STATE, "schedule not set for member " + std::to_string(b));
+    return 0;
+}
+
+int fpi_impl(whb_ctx *c, int iters, double tol_sq, double *resid_out, int *done) {
+    WHB_TRY(check_ready(c));
+    WHB_TRY(ensure_hist(c, iters));
+    WHB_TRY(upload_members(c, WHB_OUT_FPI, 0));
+    WHB_CUDA(cudaMemsetAsync(c->d_counter, 0, sizeof(int), c->stream));
+    if (c->timing) WHB_TRY(ensure_events(c, 2 * iters + 2));
+    int k = 0;
+    std::vector<double> h(c->nbatch);
+    for (k = 0; k < iters; ++k) {
+        if (c->timing) WHB_CUDA(cudaEventRecord(c->ev[2 * k], c->stream));
+        WHB_TRY(run_solve(c, WHB_OUT_FPI, 0));
+        if (c->timing) WHB_CUDA(cudaEventRecord(c->ev[2 * k + 1], c->stream));
+        if (tol_sq >= 0.0) {
+            WHB_CUDA(cudaMemcpyAsync(h.data(), c->d_hist + (size_t)k * c->nbatch, c->nbatch * sizeof(double),
+                                     cudaMemcpyDeviceToHost, c->stream));
+            WHB_CUDA(cudaStreamSynchronize(c->stream));
+            bool conv = true;
+            for (double r : h) conv = conv && (r <= tol_sq);
+            if (conv) {
+                ++k;
+                break;
+            }
+        }
+    }
+    if (resid_out && k > 0)
+        WHB_CUDA(cudaMemcpyAsync(resid_out, c->d_hist, (size_t)k * c->nbatch * sizeof(double),
+                                 cudaMemcpyDeviceToHost, c->stream));
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
+    if (c->timing) {
+        double tot = 0.0;
+        for (int i = 0; i < k; ++i) {
+            float ms = 0.f;
+            WHB_CUDA(cudaEventElapsedTime(&ms, c->ev[2 * i], c->ev[2 * i + 1]));
+            tot += ms;
+        }
+        c->t_solve_ms = tot;
+        c->t_step_ms = tot;
+        c->t_step_launches = (int64_t)k * max_steps(c);
+    }
+    if (done) *done = k;
+    return 0;
+}
+
+int copy_field_h2d(whb_ctx *c, double *dev, const double *host) {
+    // host: owned planes C-contiguous (nloc, n1, n2); device rows have pitch P
+    const size_t rows = (size_t)c->nloc * c->gshape[1];
+    WHB_CUDA(cudaMemcpy2DAsync(dev + c->S0, (size_t)c->P * sizeof(double), host,
+                               (size_t)c->gshape[2] * sizeof(double), (size_t)c->gshape[2] * sizeof(double),
+                               rows, cudaMemcpyHostToDevice, c->stream));
+    return 0;
+}
+
+int copy_field_d2h(whb_ctx *c, const double *dev, double *host) {
+    const size_t rows = (size_t)c->nloc * c->gshape[1];
+    WHB_CUDA(cudaMemcpy2DAsync(host, (size_t)c->gshape[2] * sizeof(double), dev + c->S0,
+                               (size_t)c->P * sizeof(double), (size_t)c->gshape[2] * sizeof(double), rows,
+                               cudaMemcpyDeviceToHost, c->stream));
+    return 0;
+}
+
+int zero_bnd(whb_ctx *c, double *x) {
+    const int zlo = (c->act0 && c->plane_begin == 0) ? 1 : 0;
+    const int zhi = (c->act0 && c->plane_end == c->gshape[0]) ? 1 : 0;
+    zero_boundary_kernel<<<592, 256, 0, c->stream>>>(x, c->S0, c->P, (int)c->gshape[1], (int)c->gshape[2],
+                                                     c->act1, 1, (int)c->nloc + 1, zlo, zhi);
+    c->launches++;
+    WHB_CUDA(cudaGetLastError());
+    return 0;
+}
+
+int vec_reduce_dot(whb_ctx *c, const double *x, const double *y, double *out) {
+    dot_partials_kernel<<<kRedBlocks, kRedThreads, 0, c->stream>>>(x + c->S0, y + c->S0, owned_elems(c), c->d_red);
+    final_sum_kernel<<<1, 1024, 0, c->stream>>>(c->d_red, kRedBlocks, c->d_red + kRedBlocks);
+    c->launches += 2;
+    WHB_CUDA(cudaGetLastError());
+    WHB_CUDA(cudaMemcpyAsync(c->h_red, c->d_red + kRedBlocks, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
+    *out = *c->h_red;
+    return 0;
+}
+
+}  // namespace
+
+// ==========================================================================================
+// C ABI
+
+extern "C" {
+
+int whb_abi_version(void) { return WHB_ABI_VERSION; }
+
+const char *whb_last_error(void) { return g_last_error.c_str(); }
+
+int whb_device_count(int *count) {
+    if (!count) return fail(WHB_E_ARG, "count is NULL");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+        *count = 0;
+        return fail(WHB_E_NODEV, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+    }
+    *count = n;
+    return 0;
+}
+
+int whb_create(whb_ctx **out, int device, int ndim, const int64_t *shape, int64_t plane_begin,
+               int64_t plane_end, int nbatch, int shared_forcing) {
+    if (!out || !shape) return fail(WHB_E_ARG, "NULL argument");
+    *out = nullptr;
+    if (ndim < 1 || ndim > 3) return fail(WHB_E_ARG, "ndim must be 1, 2 or 3");
+    for (int a = 0; a < ndim; ++a)
+        if (shape[a] < 3) return fail(WHB_E_ARG, "every axis needs at least 3 stored points");
+    if (nbatch < 1) return fail(WHB_E_ARG, "nbatch must be >= 1");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(WHB_E_NODEV, "no CUDA device");
+    if (device < 0 || device >= ndev) return fail(WHB_E_ARG, "device index out of range");
+    whb_ctx *c = new whb_ctx();
+    c->device = device;
+    c->ndim = ndim;
+    if (ndim == 3) {
+        c->gshape[0] = shape[0]; c->gshape[1] = shape[1]; c->gshape[2] = shape[2];
+        c->act0 = 1; c->act1 = 1;
+    } else if (ndim == 2) {
+        c->gshape[0] = shape[0]; c->gshape[1] = 1; c->gshape[2] = shape[1];
+        c->act0 = 1; c->act1 = 0;
+    } else {
+        c->gshape[0] = 1; c->gshape[1] = 1; c->gshape[2] = shape[0];
+        c->act0 = 0; c->act1 = 0;
+    }
+    if (ndim == 1) {
+        plane_begin = 0;
+        plane_end = 1;
+    }
+    if (plane_begin < 0 || plane_end > c->gshape[0] || plane_begin >= plane_end) {
+        delete c;
+        return fail(WHB_E_ARG, "invalid owned plane range");
+    }
+    if ((c->gshape[2] > (1 << 30)) || (c->gshape[1] > (1 << 30))) {
+        delete c;
+        return fail(WHB_E_ARG, "axis too large");
+    }
+    c->plane_begin = plane_begin;
+    c->plane_end = plane_end;
+    c->nloc = plane_end - plane_begin;
+    c->nplanes = c->nloc + 2;
+    c->P = (int)((c->gshape[2] + 15) / 16 * 16);
+    c->S0 = (int64_t)c->P * c->gshape[1];
+    c->field_elems = c->nplanes * c->S0;
+    c->nbatch = nbatch;
+    c->shared_f = shared_forcing ? 1 : 0;
+    c->mem.resize(nbatch);
+    c->order.resize(nbatch);
+    for (int b = 0; b < nbatch; ++b) c->order[b] = b;
+    const char *g = getenv("WHB_NO_GRAPHS");
+    if (g && atoi(g)) c->use_graphs = false;
+
+    auto cleanup = [&](int rc) {
+        whb_destroy(c);
+        return rc;
+    };
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cleanup(fail(WHB_E_CUDA, cudaGetErrorString(e)));
+    e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cleanup(fail(WHB_E_CUDA, cudaGetErrorString(e)));
+    int rc = plan_launch(c);
+    if (rc) return cleanup(rc);
+    for (int b = 0; b < nbatch; ++b) {
+        MemberHost &m = c->mem[b];
+        if ((rc = alloc_field(c, &m.v)) || (rc = alloc_field(c, &m.wa)) || (rc = alloc_field(c, &m.wb)) ||
+            (rc = alloc_field(c, &m.acc)))
+            return cleanup(rc);
+        if (!c->shared_f && (rc = alloc_field(c, &m.f))) return cleanup(rc);
+        e = cudaMalloc(&m.partials, (size_t)c->nparts * sizeof(double));
+        if (e != cudaSuccess) return cleanup(fail(WHB_E_NOMEM, "partials"));
+        cudaMemsetAsync(m.partials, 0, (size_t)c->nparts * sizeof(double), c->stream);
+    }
+    if (c->shared_f && (rc = alloc_field(c, &c->shared_f_ptr))) return cleanup(rc);
+    if (cudaMalloc(&c->d_members, nbatch * sizeof(Member)) != cudaSuccess ||
+        cudaMalloc(&c->d_counter, sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&c->d_red, (kRedBlocks + 8) * sizeof(double)) != cudaSuccess ||
+        cudaMallocHost(&c->h_red, 8 * sizeof(double)) != cudaSuccess)
+        return cleanup(fail(WHB_E_NOMEM, "context scratch"));
+    if ((rc = ensure_hist(c, 64))) return cleanup(rc);
+    e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) return cleanup(fail(WHB_E_CUDA, cudaGetErrorString(e)));
+    *out = c;
+    return 0;
+}
+
+int whb_destroy(whb_ctx *c) {
+    if (!c) return 0;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (auto &kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    for (auto &m : c->mem) {
+        cudaFree(m.v); cudaFree(m.f); cudaFree(m.wa); cudaFree(m.wb); cudaFree(m.acc); cudaFree(m.out);
+        cudaFree(m.cos_f); cudaFree(m.acc_c); cudaFree(m.partials);
+    }
+    cudaFree(c->shared_f_ptr);
+    for (double *v : c->vecs) cudaFree(v);
+    cudaFree(c->d_members);
+    cudaFree(c->d_hist);
+    cudaFree(c->d_counter);
+    cudaFree(c->d_red);
+    if (c->h_red) cudaFreeHost(c->h_red);
+    for (auto e : c->ev) cudaEventDestroy(e);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return 0;
+}
+
+int whb_set_operator(whb_ctx *c, const double *clo, const double *cmid, double c2) {
+    if (!c || !clo || !cmid) return fail(WHB_E_ARG, "NULL argument");
+    Geom &g = c->geom;
+    g.S0 = c->S0;
+    g.P = c->P;
+    g.n1 = (int)c->gshape[1];
+    g.n2 = (int)c->gshape[2];
+    g.j_lo = c->act1 ? 1 : 0;
+    g.j_hi = c->act1 ? (int)c->gshape[1] - 1 : 1;
+    g.c2 = c2;
+    g.use_c2 = (c2 != 1.0);  // x*1.0 == x exactly: skipping keeps bitwise parity
+    // map reference axes onto storage axes: 3D (0,1,2); 2D (0,-,2); 1D (-,-,2)
+    g.clo0 = g.cmid0 = g.clo1 = g.cmid1 = 0.0;
+    if (c->ndim == 3) {
+        g.clo0 = clo[0]; g.cmid0 = cmid[0];
+        g.clo1 = clo[1]; g.cmid1 = cmid[1];
+        g.clo2 = clo[2]; g.cmid2 = cmid[2];
+    } else if (c->ndim == 2) {
+        g.clo0 = clo[0]; g.cmid0 = cmid[0];
+        g.clo2 = clo[1]; g.cmid2 = cmid[1];
+    } else {
+        g.clo2 = clo[0]; g.cmid2 = cmid[0];
+    }
+    c->op_set = true;
+    return 0;
+}
+
+int whb_set_schedule(whb_ctx *c, int member, int n_total, double half_dt2, double dt2, const double *cos_f,
+                     const double *acc_c, double out_scale) {
+    if (!c || !cos_f || !acc_c) return fail(WHB_E_ARG, "NULL argument");
+    if (member < 0 || member >= c->nbatch) return fail(WHB_E_ARG, "member out of range");
+    if (n_total < 2) return fail(WHB_E_ARG, "n_total must be >= 2");
+    WHB_TRY(set_dev(c));
+    MemberHost &m = c->mem[member];
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
+    if (m.n_total != n_total) {
+        cudaFree(m.cos_f);
+        cudaFree(m.acc_c);
+        m.cos_f = m.acc_c = nullptr;
+        WHB_CUDA(cudaMalloc(&m.cos_f, n_total * sizeof(double)));
+        WHB_CUDA(cudaMalloc(&m.acc_c, (n_total + 1) * sizeof(double)));
+    }
+    WHB_CUDA(cudaMemcpy(m.cos_f, cos_f, n_total * sizeof(double), cudaMemcpyHostToDevice));
+    WHB_CUDA(cudaMemcpy(m.acc_c, acc_c, (n_total + 1) * sizeof(double), cudaMemcpyHostToDevice));
+    m.n_total = n_total;
+    m.half_dt2 = half_dt2;
+    m.dt2 = dt2;
+    m.out_scale = out_scale;
+    // table order: members by n_total descending (active members form a prefix at every step)
+    std::stable_sort(c->order.begin(), c->order.end(),
+                     [&](int a, int b) { return c->mem[a].n_total > c->mem[b].n_total; });
+    for (auto &kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    c->graphs.clear();
+    c->h_members.clear();
+    return 0;
+}
+
+int whb_upload(whb_ctx *c, int field, int member, const double *host) {
+    if (!c || !host) return fail(WHB_E_ARG, "NULL argument");
+    if (member < 0 || member >= c->nbatch || field < 0 || field > WHB_OUT) return fail(WHB_E_ARG, "bad field/member");
+    WHB_TRY(set_dev(c));
+    if (field == WHB_OUT) WHB_TRY(ensure_out(c, member));
+    double *d = field_ptr(c, field, member);
+    WHB_TRY(copy_field_h2d(c, d, host));
+    WHB_TRY(zero_bnd(c, d));
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int whb_download(whb_ctx *c, int field, int member, double *host) {
+    if (!c || !host) return fail(WHB_E_ARG, "NULL argument");
+    if (member < 0 || member >= c->nbatch || field < 0 || field > WHB_OUT) return fail(WHB_E_ARG, "bad field/member");
+    WHB_TRY(set_dev(c));
+    if (field == WHB_OUT) WHB_TRY(ensure_out(c, member));
+    WHB_TRY(copy_field_d2h(c, field_ptr(c, field, member), host));
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int whb_zero(whb_ctx *c, int field, int member) {
+    if (!c) return fail(WHB_E_ARG, "NULL argument");
+    if (member < 0 || member >= c->nbatch || field < 0 || field > WHB_OUT) return fail(WHB_E_ARG, "bad field/member");
+    WHB_TRY(set_dev(c));
+    if (field == WHB_OUT) WHB_TRY(ensure_out(c, member));
+    WHB_CUDA(cudaMemsetAsync(field_ptr(c, field, member), 0, (size_t)c->field_elems * sizeof(double), c->stream));
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int whb_filtered_solve(whb_ctx *c, int out_mode, int zero_forcing, double *resid_sq) {
+    if (!c) return fail(WHB_E_ARG, "NULL argument");
+    if (out_mode < 0 || out_mode > 2) return fail(WHB_E_ARG, "bad out_mode");
+    WHB_TRY(set_dev(c));
+    WHB_TRY(check_ready(c));
+    const int zf = (zero_forcing || out_mode == WHB_OUT_AV) ? 1 : 0;
+    WHB_TRY(upload_members(c, out_mode, zf));
+    if (out_mode == WHB_OUT_FPI) WHB_CUDA(cudaMemsetAsync(c->d_counter, 0, sizeof(int), c->stream));
+    if (c->timing) {
+        WHB_TRY(ensure_events(c, 2));
+        WHB_CUDA(cudaEventRecord(c->ev[0], c->stream));
+    }
+    WHB_TRY(run_solve(c, out_mode, zf));
+    if (c->timing) WHB_CUDA(cudaEventRecord(c->ev[1], c->stream));
+    if (out_mode == WHB_OUT_FPI && resid_sq)
+        WHB_CUDA(cudaMemcpyAsync(resid_sq, c->d_hist, c->nbatch * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
+    if (c->timing) {
+        float ms = 0.f;
+        WHB_CUDA(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+        c->t_solve_ms = ms;
+        c->t_step_ms = ms;
+        c->t_step_launches = max_steps(c);
+    }
+    return 0;
+}
+
+int whb_fpi(whb_ctx *c, int iters, double tol_sq, double *resid_sq_out, int *iters_done) {
+    if (!c || iters < 0) return fail(WHB_E_ARG, "bad argument");
+    WHB_TRY(set_dev(c));
+    if (iters == 0) {
+        if (iters_done) *iters_done = 0;
+        return 0;
+    }
+    return fpi_impl(c, iters, tol_sq, resid_sq_out, iters_done);
+}
+
+int whb_iterate_host(whb_ctx *c, const double *v_host, double *v_out_host, double *resid_sq) {
+    if (!c || !v_host || !v_out_host) return fail(WHB_E_ARG, "NULL argument");
+    if (c->nbatch != 1) return fail(WHB_E_ARG, "whb_iterate_host needs nbatch == 1");
+    WHB_TRY(set_dev(c));
+    WHB_TRY(check_ready(c));
+    WHB_TRY(ensure_hist(c, 1));
+    WHB_TRY(upload_members(c, WHB_OUT_FPI, 0));
+    WHB_TRY(copy_field_h2d(c, c->mem[0].v, v_host));
+    WHB_TRY(zero_bnd(c, c->mem[0].v));
+    WHB_CUDA(cudaMemsetAsync(c->d_counter, 0, sizeof(int), c->stream));
+    WHB_TRY(run_solve(c, WHB_OUT_FPI, 0));
+    WHB_TRY(copy_field_d2h(c, c->mem[0].v, v_out_host));
+    if (resid_sq) WHB_CUDA(cudaMemcpyAsync(resid_sq, c->d_hist, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+// ---- vectors -------------------------------------------------------------------------------
+
+int whb_vec_reserve(whb_ctx *c, int count, int *first_id) {
+    if (!c || count < 0) return fail(WHB_E_ARG, "bad argument");
+    WHB_TRY(set_dev(c));
+    const int first = 8 + (int)c->vecs.size();
+    for (int i = 0; i < count; ++i) {
+        double *p = nullptr;
+        WHB_TRY(alloc_field(c, &p));
+        c->vecs.push_back(p);
+    }
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
+    if (first_id) *first_id = first;
+    return 0;
+}
+
+#define VEC_OR_FAIL(name, id)                                             \
+    double *name = vec_ptr(c, id);                                        \
+    if (!name) {                                                          \
+        if ((id) == WHB_OUT) {                                            \
+            WHB_TRY(ensure_out(c, 0));                                    \
+            name = vec_ptr(c, id);                                        \
+        } else                                                            \
+            return fail(WHB_E_ARG, "unknown vector id " + std::to_string(id)); \
+    }
+
+int whb_vec_upload(whb_ctx *c, int id, const double *host) {
+    if (!c || !host) return fail(WHB_E_ARG, "NULL argument");
+    WHB_TRY(set_dev(c));
+    VEC_OR_FAIL(x, id);
+    WHB_TRY(copy_field_h2d(c, x, host));
+    WHB_TRY(zero_bnd(c, x));
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int whb_vec_download(whb_ctx *c, int id, double *host) {
+    if (!c || !host) return fail(WHB_E_ARG, "NULL argument");
+    WHB_TRY(set_dev(c));
+    VEC_OR_FAIL(x, id);
+    WHB_TRY(copy_field_d2h(c, x, host));
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int whb_vec_dot(whb_ctx *c, int xi, int yi, double *out) {
+    if (!c || !out) return fail(WHB_E_ARG, "NULL argument");
+    WHB_TRY(set_dev(c));
+    VEC_OR_FAIL(x, xi);
+    VEC_OR_FAIL(y, yi);
+    return vec_reduce_dot(c, x, y, out);
+}
+
+#define ELEMWISE_LAUNCH(kernel, ...)                                                 \
+    do {                                                                            \
+        kernel<<<kRedBlocks, kRedThreads, 0, c->stream>>>(__VA_ARGS__);             \
+        c->launches++;                                                              \
+        WHB_CUDA(cudaGetLastError());                                               \
+    } while (0)
+
+int whb_vec_axpy(whb_ctx *c, double a, int xi, int yi) {
+    if (!c) return fail(WHB_E_ARG, "NULL argument");
+    WHB_TRY(set_dev(c));
+    VEC_OR_FAIL(x, xi);
+    VEC_OR_FAIL(y, yi);
+    // y - ((-a)*x) == y + a*x bitwise; with a = -h this is numpy's `w -= h*q` (linalg.py:146)
+    ELEMWISE_LAUNCH(axmy_kernel, -a, owned(x, c), owned(y, c), owned_elems(c));
+    return 0;
+}
+
+int whb_vec_scale_into(whb_ctx *c, double a, int xi, int yi) {
+    if (!c) return fail(WHB_E_ARG, "NULL argument");
+    WHB_TRY(set_dev(c));
+    VEC_OR_FAIL(x, xi);
+    VEC_OR_FAIL(y, yi);
+    ELEMWISE_LAUNCH(scale_kernel, a, owned(x, c), owned(y, c), owned_elems(c));
+    return 0;
+}
+
+int whb_vec_div_into(whb_ctx *c, int xi, double d, int yi) {
+    if (!c) return fail(WHB_E_ARG, "NULL argument");
+    WHB_TRY(set_dev(c));
+    VEC_OR_FAIL(x, xi);
+    VEC_OR_FAIL(y, yi);
+    ELEMWISE_LAUNCH(div_kernel, owned(x, c), d, owned(y, c), owned_elems(c));
+    return 0;
+}
+
+int whb_vec_sub_into(whb_ctx *c, int xi, int yi, int zi) {
+    if (!c) return fail(WHB_E_ARG, "NULL argument");
+    WHB_TRY(set_dev(c));
+    VEC_OR_FAIL(x, xi);
+    VEC_OR_FAIL(y, yi);
+    VEC_OR_FAIL(z, zi);
+    ELEMWISE_LAUNCH(sub_kernel, owned(x, c), owned(y, c), owned(z, c), owned_elems(c));
+    return 0;
+}
+
+int whb_vec_copy(whb_ctx *c, int xi, int yi) {
+    if (!c) return fail(WHB_E_ARG, "NULL argument");
+    WHB_TRY(set_dev(c));
+    VEC_OR_FAIL(x, xi);
+    VEC_OR_FAIL(y, yi);
+    WHB_CUDA(cudaMemcpyAsync(y, x, (size_t)c->field_elems * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    return 0;
+}
+
+int whb_vec_lincomb(whb_ctx *c, int yi, int first, int count, const double *coef) {
+    if (!c || (!coef && count > 0)) return fail(WHB_E_ARG, "NULL argument");
+    WHB_TRY(set_dev(c));
+    VEC_OR_FAIL(y, yi);
+    for (int base = 0; base < count; base += kMaxComb) {
+        // NB: chunks of 64 add their partial sums to y separately; GMRES restarts are <= 64 in practice
+        CombArgs a{};
+        const int cnt = std::min(kMaxComb, count - base);
+        for (int j = 0; j < cnt; ++j) {
+            double *q = vec_ptr(c, first + base + j);
+            if (!q) return fail(WHB_E_ARG, "unknown vector id in lincomb");
+            a.q[j] = owned(q, c);
+            a.c[j] = coef[base + j];
+        }
+        ELEMWISE_LAUNCH(lincomb_kernel, a, cnt, owned(y, c), owned_elems(c));
+    }
+    return 0;
+}
+
+int whb_matvec(whb_ctx *c, int xi, int yi) {
+    if (!c) return fail(WHB_E_ARG, "NULL argument");
+    if (c->nbatch != 1) return fail(WHB_E_ARG, "whb_matvec needs nbatch == 1");
+    if (xi == yi) return fail(WHB_E_ARG, "whb_matvec needs distinct x and y");
+    WHB_TRY(set_dev(c));
+    WHB_TRY(check_ready(c));
+    VEC_OR_FAIL(x, xi);
+    VEC_OR_FAIL(y, yi);
+    if (x == c->mem[0].wa || x == c->mem[0].wb || x == c->mem[0].acc || y == c->mem[0].wa ||
+        y == c->mem[0].wb || y == c->mem[0].acc)
+        return fail(WHB_E_ARG, "whb_matvec operands may not alias the leapfrog workspace");
+    WHB_TRY(upload_members(c, WHB_OUT_AV, 1, x, y));
+    WHB_TRY(run_solve(c, WHB_OUT_AV, 1));
+    return 0;
+}
+
+// ---- slab step-level control ----------------------------------------------------------------
+
+int whb_solve_begin(whb_ctx *c, int out_mode, int zero_forcing) {
+    if (!c) return fail(WHB_E_ARG, "NULL argument");
+    if (c->nbatch != 1) return fail(WHB_E_ARG, "step-level control needs nbatch == 1");
+    WHB_TRY(set_dev(c));
+    WHB_TRY(check_ready(c));
+    WHB_TRY(ensure_hist(c, 1));
+    const int zf = (zero_forcing || out_mode == WHB_OUT_AV) ? 1 : 0;
+    WHB_TRY(upload_members(c, out_mode, zf));
+    if (out_mode == WHB_OUT_FPI) {
+        WHB_CUDA(cudaMemsetAsync(c->d_counter, 0, sizeof(int), c->stream));
+        // region-split launches leave some partial slots unwritten: start from zero
+        WHB_CUDA(cudaMemsetAsync(c->mem[0].partials, 0, (size_t)c->nparts * sizeof(double), c->stream));
+    }
+    c->cur_mode = out_mode;
+    c->cur_zf = zf;
+    c->cur_parts = 0;
+    return 0;
+}
+
+int whb_step(whb_ctx *c, int s, int region) {
+    if (!c || c->cur_mode < 0) return fail(WHB_E_STATE, "whb_step outside whb_solve_begin/end");
+    if (s < 0 || s >= c->mem[0].n_total) return fail(WHB_E_ARG, "step out of range");
+    WHB_TRY(set_dev(c));
+    const int lo = c->upd_lo, hi = c->upd_hi;
+    const int tiles = c->gx * c->JT;
+    if (region == 0) {
+        WHB_TRY(launch_step(c, s, 1, lo, hi, c->chunk_len, 0));
+        if (s == c->mem[0].n_total - 1) c->cur_parts = tiles * c->nchunks;
+    } else if (region == 1) {
+        // the first and last owned update planes (what neighbours need), one plane per launch
+        WHB_TRY(launch_step(c, s, 1, lo, std::min(lo + 1, hi), 1, 0));
+        if (hi - 1 > lo) WHB_TRY(launch_step(c, s, 1, hi - 1, hi, 1, tiles));
+    } else if (region == 2) {
+        if (hi - 1 > lo + 1) WHB_TRY(launch_step(c, s, 1, lo + 1, hi - 1, c->chunk_len, 2 * tiles));
+        if (s == c->mem[0].n_total - 1) c->cur_parts = c->nparts;
+    } else
+        return fail(WHB_E_ARG, "region must be 0, 1 or 2");
+    return 0;
+}
+
+int whb_solve_end(whb_ctx *c, double *resid_sq) {
+    if (!c || c->cur_mode < 0) return fail(WHB_E_STATE, "whb_solve_end without whb_solve_begin");
+    WHB_TRY(set_dev(c));
+    if (c->cur_mode == WHB_OUT_FPI) {
+        // unused partial slots of region launches stay 0 from the previous zeroing
+        reduce_partials_kernel<<<1, 1024, 0, c->stream>>>(c->d_members, 1, c->cur_parts, c->d_hist, c->d_counter);
+        c->launches++;
+        WHB_CUDA(cudaGetLastError());
+        if (resid_sq) WHB_CUDA(cudaMemcpyAsync(resid_sq, c->d_hist, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    }
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
+    c->cur_mode = -1;
+    return 0;
+}
+
+int whb_level_plane_ptr(whb_ctx *c, int level, int64_t plane, uint64_t *dev_ptr, int64_t *plane_elems) {
+    if (!c || !dev_ptr) return fail(WHB_E_ARG, "NULL argument");
+    if (plane < 0 || plane >= c->nplanes) return fail(WHB_E_ARG, "plane out of range");
+    if (level < 0) return fail(WHB_E_ARG, "level must be >= 0");
+    const MemberHost &m = c->mem[0];
+    const double *base = (level == 0) ? (c->cur_mode >= 0 && !c->h_members.empty() ? c->h_members[0].v : m.v)
+                                      : ((level & 1) ? m.wa : m.wb);
+    *dev_ptr = (uint64_t)(uintptr_t)(base + plane * c->S0);
+    if (plane_elems) *plane_elems = c->S0;
+    return 0;
+}
+
+int whb_stream_ptr(whb_ctx *c, uint64_t *stream) {
+    if (!c || !stream) return fail(WHB_E_ARG, "NULL argument");
+    *stream = (uint64_t)(uintptr_t)c->stream;
+    return 0;
+}
+
+int whb_synchronize(whb_ctx *c) {
+    if (!c) return fail(WHB_E_ARG, "NULL argument");
+    WHB_TRY(set_dev(c));
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int whb_copy_plane(whb_ctx *src, int src_level, int64_t src_plane, whb_ctx *dst, int dst_level, int64_t dst_plane) {
+    if (!src || !dst) return fail(WHB_E_ARG, "NULL argument");
+    if (src->S0 != dst->S0) return fail(WHB_E_ARG, "plane geometry mismatch");
+    uint64_t sp = 0, dp = 0;
+    WHB_TRY(whb_level_plane_ptr(src, src_level, src_plane, &sp, nullptr));
+    WHB_TRY(whb_level_plane_ptr(dst, dst_level, dst_plane, &dp, nullptr));
+    cudaEvent_t e1, e2;
+    WHB_TRY(set_dev(src));
+    WHB_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+    WHB_CUDA(cudaEventRecord(e1, src->stream));
+    WHB_TRY(set_dev(dst));
+    WHB_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+    WHB_CUDA(cudaStreamWaitEvent(dst->stream, e1, 0));
+    WHB_CUDA(cudaMemcpyPeerAsync((void *)(uintptr_t)dp, dst->device, (const void *)(uintptr_t)sp, src->device,
+                                 (size_t)src->S0 * sizeof(double), dst->stream));
+    WHB_CUDA(cudaEventRecord(e2, dst->stream));
+    WHB_TRY(set_dev(src));
+    WHB_CUDA(cudaStreamWaitEvent(src->stream, e2, 0));
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    return 0;
+}
+
+int whb_launch_count(whb_ctx *c, int64_t *count) {
+    if (!c || !count) return fail(WHB_E_ARG, "NULL argument");
+    *count = c->launches;
+    return 0;
+}
+
+int whb_set_timing(whb_ctx *c, int enable) {
+    if (!c) return fail(WHB_E_ARG, "NULL argument");
+    c->timing = enable != 0;
+    return 0;
+}
+
+int whb_last_timing(whb_ctx *c, double *step_ms, int64_t *step_launches, double *solve_ms) {
+    if (!c) return fail(WHB_E_ARG, "NULL argument");
+    if (step_ms) *step_ms = c->t_step_ms;
+    if (step_launches) *step_launches = c->t_step_launches;
+    if (solve_ms) *solve_ms = c->t_solve_ms;
+    return 0;
+}
+
+int whb_host_alloc(void **ptr, int64_t bytes) {
+    if (!ptr || bytes < 0) return fail(WHB_E_ARG, "bad argument");
+    WHB_CUDA(cudaMallocHost(ptr, (size_t)std::max<int64_t>(bytes, 8)));
+    return 0;
+}
+
+int whb_host_free(void *ptr) {
+    if (ptr) WHB_CUDA(cudaFreeHost(ptr));
+    return 0;
+}
+
+int whb_geometry(whb_ctx *c, int64_t *shape3, int64_t *pitch, int64_t *nloc) {
+    if (!c) return fail(WHB_E_ARG, "NULL argument");
+    if (shape3)
+        for (int a = 0; a < 3; ++a) shape3[a] = c->gshape[a];
+    if (pitch) *pitch = c->P;
+    if (nloc) *nloc = c->nloc;
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,89 @@
+"""Device-resident problem state: one whb context per (grid, wave speed, device).
+
+The reference re-creates every array per call (timestep.py:282-301).  Here a
+grid's device buffers (v, f, leapfrog pair, accumulator) are allocated once
+and reused across calls; the forcing is uploaded only when its values change,
+and the per-step schedule only when the time correction changes.
+"""
+
+from __future__ import annotations
+
+import collections
+
+import numpy as np
+
+from . import _native
+from .grid import operator_coefficients
+
+__all__ = ["DeviceProblem", "device_problem", "release_device_cache"]
+
+_MAX_CACHED = 2
+_cache: "collections.OrderedDict[tuple, DeviceProblem]" = collections.OrderedDict()
+
+
+def _grid_key(grid, c, device, nbatch=1, shared=False):
+    return (tuple(int(n) for n in grid.shape), tuple(float(d) for d in grid.spacing), float(c), int(device),
+            int(nbatch), bool(shared))
+
+
+class DeviceProblem:
+    """A grid on one GPU (optionally a batch of problems sharing the grid)."""
+
+    def __init__(self, grid, c=1.0, order=2, device=0, nbatch=1, shared_forcing=False, plane_range=None):
+        clo, cmid, c2 = operator_coefficients(grid, order, c)
+        self.grid = grid
+        self.c = float(c)
+        self.nbatch = nbatch
+        self.ctx = _native.Context(grid.shape, device=device, plane_range=plane_range, nbatch=nbatch,
+                                   shared_forcing=shared_forcing)
+        self.ctx.set_operator(clo, cmid, c2)
+        self._sched = [None] * nbatch
+        self._forcing = [None] * (1 if shared_forcing else nbatch)
+        self.shared_forcing = shared_forcing
+
+    @property
+    def npoints(self) -> int:
+        return int(np.prod(self.grid.shape))
+
+    def set_schedule(self, sched: dict, member: int = 0):
+        key = (sched["n_total"], sched["half_dt2"], sched["dt2"], sched["out_scale"],
+               np.asarray(sched["cos_f"]).tobytes(), np.asarray(sched["acc_c"]).tobytes())
+        if self._sched[member] != key:
+            self.ctx.set_schedule(member, sched)
+            self._sched[member] = key
+
+    def set_forcing(self, values, member: int = 0) -> bool:
+        """Upload f unless the device already holds exactly these values; returns
+        True when f is identically zero (the zero-forcing kernel variant applies)."""
+        slot = 0 if self.shared_forcing else member
+        vals = np.asarray(values, dtype=np.float64)
+        cached = self._forcing[slot]
+        if cached is None or cached.shape != vals.shape or not np.array_equal(cached, vals):
+            self.ctx.upload(_native.F, vals, member)
+            self._forcing[slot] = np.array(vals)
+        return not np.any(self._forcing[slot])
+
+    def close(self):
+        self.ctx.close()
+
+
+def device_problem(grid, c=1.0, order=2, device=0) -> DeviceProblem:
+    """Cached single-problem device state for a grid (LRU of a few entries)."""
+    key = _grid_key(grid, c, device)
+    dp = _cache.get(key)
+    if dp is not None:
+        _cache.move_to_end(key)
+        return dp
+    while len(_cache) >= _MAX_CACHED:
+        _, old = _cache.popitem(last=False)
+        old.close()
+    dp = DeviceProblem(grid, c=c, order=order, device=device)
+    _cache[key] = dp
+    return dp
+
+
+def release_device_cache():
+    """Free every cached device problem (returns HBM to the allocator)."""
+    while _cache:
+        _, dp = _cache.popitem(last=False)
+        dp.close()

@@ -1,0 +1,296 @@
+"""Fixed-point and GMRES WaveHoltz drivers on the GPU — drop-in for the
+explicit-mode drivers of waveholtz/driver.py.
+
+``fpi_solve`` keeps v, f and every wave-solve buffer resident on the device
+for the whole iteration (the reference round-trips every iterate through new
+numpy arrays, driver.py:221-227); the residual ||v_{k+1}-v_k||_2/sqrt(N) is
+reduced inside the last leapfrog step of each pass.  ``krylov_solve`` runs
+the reference's GMRES control flow over device vectors.  Deflation and the
+direct sparse solve (driver.py:88-126, 303-343) are desk-scale oracles and
+out of scope.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from . import _native
+from .device import DeviceProblem, device_problem
+from .filters import FilterConfig, ResonanceError, TimeMode, mode_name
+from .grid import DiscreteOperator, GridField, bc_name
+from .linalg import device_gmres
+from .timestep import correct_explicit, time_schedule
+
+__all__ = [
+    "HelmholtzProblem", "WaveHoltzRun", "NearSingularError", "gaussian_source", "multi_gaussian_source",
+    "fpi_solve", "krylov_solve", "waveholtz_operator", "apply_A", "measure_rate",
+    "resolve_time_discretization", "resonance_gap",
+]
+
+
+class NearSingularError(ValueError):
+    """driver.py:58-59."""
+
+
+def resonance_gap(grid, order: int, c: float, omega: float) -> float:
+    """min |omega - lambda_h| / omega over the discrete Dirichlet spectrum
+    (driver.py:72-81 with grid.py:417-472), without enumerating modes in Python:
+    per-axis lambda^2 lists, the trailing axes combined into one sorted array,
+    then a bisection per leading-axis value."""
+    if order != 2:
+        raise NotImplementedError("resonance check implemented for p = 2")
+    per_axis = []
+    for n, dx in zip(grid.cells, grid.spacing):
+        m = np.arange(1, n)
+        per_axis.append((c / dx) ** 2 * (4.0 * np.sin(m * np.pi / n / 2.0) ** 2))
+    w2 = omega * omega
+    if len(per_axis) == 1:
+        lam = np.sqrt(per_axis[0])
+        return float(np.min(np.abs(omega - lam)) / omega)
+    tail = per_axis[-1]
+    for arr in per_axis[-2:0:-1]:
+        tail = np.add.outer(arr, tail).ravel()
+    tail = np.sort(tail)
+    best = np.inf
+    for l0 in per_axis[0]:
+        i = np.searchsorted(tail, w2 - l0)
+        for j in (i - 1, i):
+            if 0 <= j < tail.size:
+                best = min(best, abs(omega - math.sqrt(l0 + tail[j])))
+    return float(best / omega)
+
+
+@dataclass(frozen=True)
+class HelmholtzProblem:
+    """L u + omega^2 u = f with homogeneous boundary data (driver.py:62-85)."""
+
+    grid: object
+    order: int
+    c: float
+    omega: float
+    forcing: object
+
+    def __post_init__(self):
+        if not self.omega > 0:
+            raise ValueError("omega must be positive")
+        if all(bc_name(b) == "dirichlet" for b in self.grid.bcs) and self.order == 2:
+            gap = resonance_gap(self.grid, self.order, self.c, self.omega)
+            if gap < 1e-10:
+                raise ResonanceError(f"omega = {self.omega:.12g} is within {gap:.1e} of a discrete eigenvalue")
+
+    @property
+    def operator(self) -> DiscreteOperator:
+        return DiscreteOperator(self.grid, self.order, self.c)
+
+
+@dataclass
+class WaveHoltzRun:
+    """Iteration diagnostics in the scaled 2h norm (driver.py:129-151)."""
+
+    method: str
+    periods: int
+    residuals: list
+    iterations: int
+    converged: bool
+    wall_time: float = 0.0
+    inner_iterations: int = 0
+
+    @property
+    def wall_time_per_iteration(self) -> float:
+        return self.wall_time / max(1, self.iterations)
+
+    @property
+    def cr(self) -> float:
+        return measure_rate(self)[0]
+
+    @property
+    def ecr(self) -> float:
+        return measure_rate(self)[1]
+
+
+def measure_rate(run) -> tuple:
+    """(CR, ECR) from the last five residual ratios (driver.py:154-160)."""
+    r = [x for x in run.residuals if x > 0]
+    if len(r) < 6:
+        raise ValueError(f"need at least 6 positive residuals, have {len(r)}")
+    cr = (r[-1] / r[-6]) ** 0.2
+    return cr, cr ** (1.0 / run.periods)
+
+
+def gaussian_source(grid, omega: float, a_g: float, b_g: float, x0) -> GridField:
+    """a_g*exp(-b_g*|x-x0|^2) at the grid points (driver.py:163-179); r^2 is
+    accumulated axis by axis from zeros, as the reference does, so the bits match."""
+    x0 = np.atleast_1d(np.asarray(x0, dtype=float))
+    if x0.size != grid.dim:
+        raise ValueError(f"source center has {x0.size} coordinates for a {grid.dim}D grid")
+    for (lo, hi), xc in zip(grid.bounds, x0):
+        if not lo <= xc <= hi:
+            raise ValueError(f"source center {xc} outside [{lo}, {hi}]")
+    return GridField.from_values(grid, _gaussian_values(grid, a_g, b_g, x0))
+
+
+def _gaussian_values(grid, a_g, b_g, x0, planes=None):
+    """Values on planes [p0, p1) of axis 0 (all when None), memory-lean for 3D."""
+    shape = tuple(grid.shape)
+    p0, p1 = (0, shape[0]) if planes is None else planes
+    sub = (p1 - p0,) + shape[1:]
+    r2 = np.zeros(sub)
+    for ax in range(grid.dim):
+        lo = grid.bounds[ax][0]
+        xs = lo + grid.spacing[ax] * np.arange(shape[ax])
+        if ax == 0:
+            xs = xs[p0:p1]
+        bshape = [1] * grid.dim
+        bshape[ax] = xs.size
+        r2 = r2 + ((xs - x0[ax]) ** 2).reshape(bshape)
+    return a_g * np.exp(-b_g * r2)
+
+
+def multi_gaussian_source(grid, omega: float, n_gauss: int, seed: int = 0, slab_planes: int = 0) -> GridField:
+    """BASELINE forcing recipe: rng = default_rng(seed);
+    amp ~ U(-100,100,K), centres ~ U(0.1,0.9,(K,d)), widths ~ U(100,1000,K);
+    f = sum_k gaussian_source(grid, omega, amp[k], b[k], centre[k]) in k order
+    from zeros, boundary zeroed.  ``slab_planes`` > 0 evaluates the same
+    per-element formula in axis-0 slabs to bound host memory on 1025^3."""
+    rng = np.random.default_rng(seed)
+    amp = rng.uniform(-100.0, 100.0, n_gauss)
+    ctr = rng.uniform(0.1, 0.9, (n_gauss, grid.dim))
+    wid = rng.uniform(100.0, 1000.0, n_gauss)
+    shape = tuple(grid.shape)
+    f = np.zeros(shape)
+    step = slab_planes if slab_planes > 0 else shape[0]
+    for p0 in range(0, shape[0], step):
+        p1 = min(shape[0], p0 + step)
+        acc = np.zeros((p1 - p0,) + shape[1:])
+        for k in range(n_gauss):
+            g = _gaussian_values(grid, amp[k], wid[k], ctr[k], planes=(p0, p1))
+            _zero_boundary_slab(grid, g, p0, p1)
+            acc = acc + g
+        f[p0:p1] = acc
+    return GridField.from_values(grid, f)
+
+
+def _zero_boundary_slab(grid, a, p0, p1):
+    for axis in range(grid.dim):
+        sel = [slice(None)] * grid.dim
+        if axis == 0:
+            if p0 == 0:
+                sel[0] = 0
+                a[tuple(sel)] = 0.0
+            if p1 == grid.shape[0]:
+                sel[0] = -1
+                a[tuple(sel)] = 0.0
+        else:
+            for edge in (0, -1):
+                sel[axis] = edge
+                a[tuple(sel)] = 0.0
+
+
+def resolve_time_discretization(problem, config):
+    """(corr, cfg): explicit mode derives N_t from stability (driver.py:182-192)."""
+    if mode_name(config.mode) == "explicit":
+        corr = correct_explicit(problem.omega, problem.grid, problem.order, problem.c)
+        cfg = config
+        if corr.steps_per_period != config.steps_per_period:
+            cfg = replace(config, steps_per_period=corr.steps_per_period)
+        return corr, cfg
+    if mode_name(config.mode) == "implicit":
+        raise NotImplementedError("implicit time stepping is out of scope for the GPU path (SURVEY §2)")
+    raise ValueError("the continuous filter cannot be time-stepped; pick explicit or implicit")
+
+
+def _device_for(problem) -> DeviceProblem:
+    return device_problem(problem.grid, c=problem.c, order=problem.order)
+
+
+def fpi_solve(problem, config, tol=1e-10, maxit=500, inner_tol=1e-12, device_state=None):
+    """Fixed-point iteration from v = 0, stopping on the successive difference
+    (driver.py:201-203, 211-244), device resident.
+
+    tol < 0 runs exactly ``maxit`` passes with no host synchronisation between
+    them; otherwise the scaled residual is checked on the host after every
+    pass exactly like driver.py:225-230."""
+    corr, cfg = resolve_time_discretization(problem, config)
+    dp = device_state or _device_for(problem)
+    dp.set_schedule(time_schedule(corr, cfg))
+    dp.set_forcing(problem.forcing.values)
+    dp.ctx.zero(_native.V)
+    root_n = math.sqrt(problem.grid.size)
+    residuals = []
+    converged = False
+    k = 0
+    t0 = time.perf_counter()
+    if tol < 0:
+        rs = dp.ctx.fpi(maxit)
+        residuals = [math.sqrt(x) / root_n for x in rs[:, 0]]
+        k = len(residuals)
+    else:
+        for k in range(1, maxit + 1):
+            rs = dp.ctx.fpi(1)
+            diff = math.sqrt(rs[0, 0]) / root_n
+            residuals.append(diff)
+            if diff <= tol:
+                converged = True
+                break
+    wall = time.perf_counter() - t0
+    v = GridField.from_values(problem.grid, dp.ctx.download(_native.V), ghost=2)
+    run = WaveHoltzRun(method="fpi", periods=cfg.periods, residuals=residuals, iterations=k,
+                       converged=converged, wall_time=wall, inner_iterations=0)
+    return v, run
+
+
+def waveholtz_operator(problem, config, corr=None, linear_solver=None, deflation=None):
+    """Matrix-free A v = v - W(v, 0) on host arrays (driver.py:247-264); each call
+    uploads v, runs one zero-forcing wave solve on the device and downloads A v."""
+    if deflation is not None and len(deflation) > 0:
+        raise NotImplementedError("deflation is out of scope for the GPU path (SURVEY §2)")
+    if corr is None:
+        corr, config = resolve_time_discretization(problem, config)
+    dp = _device_for(problem)
+    sched = time_schedule(corr, config)
+
+    def matvec(values: np.ndarray) -> np.ndarray:
+        dp.set_schedule(sched)
+        dp.ctx.upload(_native.V, np.asarray(values, dtype=float))
+        dp.ctx.filtered_solve(_native.OUT_AV, zero_forcing=True)
+        return dp.ctx.download(_native.OUT)
+
+    return matvec
+
+
+def apply_A(v, problem, config, corr=None, linear_solver=None) -> GridField:
+    """driver.py:267-270."""
+    matvec = waveholtz_operator(problem, config, corr=corr, linear_solver=linear_solver)
+    return GridField.from_values(problem.grid, matvec(np.array(v.values)))
+
+
+def krylov_solve(problem, config, tol=1e-10, restart=50, maxit=500, deflation=None, inner_tol=1e-12):
+    """GMRES on (I - S) v = b, b = W(0, f), residuals in the scaled norm
+    (driver.py:273-300), every vector device resident."""
+    if deflation is not None and len(deflation) > 0:
+        raise NotImplementedError("deflation is out of scope for the GPU path (SURVEY §2)")
+    corr, cfg = resolve_time_discretization(problem, config)
+    dp = _device_for(problem)
+    ctx = dp.ctx
+    t0 = time.perf_counter()
+    dp.set_schedule(time_schedule(corr, cfg))
+    dp.set_forcing(problem.forcing.values)
+    ctx.zero(_native.V)
+    ctx.filtered_solve(_native.OUT_PLAIN)  # OUT = b = W(0, f)   (driver.py:279-281)
+    m = max(1, min(restart, maxit))
+    ids = ctx.vec_reserve(m + 4) if not hasattr(dp, "_krylov_ids") or len(dp._krylov_ids) < m + 4 else dp._krylov_ids
+    dp._krylov_ids = ids
+    b_id, x_id, work = ids[0], ids[1], ids[2:]
+    ctx.copy(_native.OUT, b_id)
+    scale = math.sqrt(problem.grid.size)
+    rep = device_gmres(ctx, ctx.matvec, b_id, x_id, tol=0.0, atol=tol * scale, restart=restart, maxit=maxit,
+                       work_ids=work)
+    x = ctx.vec_download(x_id)
+    wall = time.perf_counter() - t0
+    run = WaveHoltzRun(method="gmres", periods=cfg.periods, residuals=[r / scale for r in rep.residual_history],
+                       iterations=rep.iterations, converged=rep.converged, wall_time=wall, inner_iterations=0)
+    return GridField.from_values(problem.grid, x), run
