@@ -1,0 +1,414 @@
+"""Benchmark: explicit WaveHoltz fixed-point iterations on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2] [--impl ours|reference]
+
+A "step" is one WaveHoltz fixed-point iteration v <- W(v, f) (N_t fused
+leapfrog+filter steps over the whole grid + the residual reduction).  The
+default workload is BASELINE config 2 (2D 2049^2, omega = 100.5, 8 seeded
+Gaussians, CFL 0.9, N_t = 202) and the default K = 50 is that config's full
+iteration count: the timed region is the complete 50-iteration solve from
+v = 0.  Inputs are resident in HBM when timing starts; an L2 flush (256 MiB
+scratch write) runs before every timed iteration, outside the timed span.
+
+value      = grid-point updates / s (N stored points x N_t x K / device time), Gpts/s
+e2e        = the same through HostFPIStep (host pinned v in, v_new out, every step)
+roofline   = fused step kernel: 48 algorithmic bytes per point update / average
+             launch duration (CUDA events on the launching stream) vs measured HBM peak
+cpu_baseline = numpy restatement of the reference (1 core), bounded sample
+--impl reference: the C OpenMP restatement of the reference on all host cores
+             (the reference is pure numpy; oracle/ holds its bitwise restatement)
+
+N > 1 (torchrun): every rank solves its own copy of the workload on its GPU
+(independent problems, no data-path collective; "scaling": "weak"); time is the
+max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fused wave-step+filter Gpts/s and WaveHoltz iters/s; % of HBM roofline"
+BYTES_PER_UPDATE = 48  # read W^n, W^{n-1}, f, acc; write W^{n+1}, acc (fp64)
+
+WORKLOADS = {
+    # name: (dim, cells, omega, forcing, iterations)
+    "cfg1": (2, 128, 20.3, ("single", 100.0, 200.0, (0.4, 0.6)), 100),
+    "cfg2": (2, 2048, 100.5, ("multi", 8), 50),
+    "cfg3": (3, 256, 40.7, ("single", 100.0, 300.0, (0.45, 0.5, 0.55)), 30),
+    "cfg4": (3, 1024, 150.3, ("multi", 16), 10),
+}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------------------------------
+# distributed plumbing
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def init_dist(ws):
+    if ws <= 1:
+        return None
+    import torch.distributed as dist
+
+    backend = "nccl"
+    try:
+        import torch
+
+        if not torch.cuda.is_available():
+            backend = "gloo"
+    except Exception:
+        backend = "gloo"
+    dist.init_process_group(backend=backend)
+    return dist
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def max_over_ranks(dist, x: float) -> float:
+    if dist is None:
+        return x
+    import torch
+
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+
+REASONS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+
+class ClockSampler:
+    def __init__(self, gpu_index: int, interval_ms: int = 100):
+        q = "clocks.sm,clocks.max.sm," + ",".join(f"clocks_event_reasons.{r}" for r in REASONS)
+        self.cmd = ["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                    f"-lms", str(interval_ms)]
+        self.proc = None
+        self.lines = []
+        self._t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(self.cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return self
+        self._t = threading.Thread(target=self._read, daemon=True)
+        self._t.start()
+        time.sleep(0.15)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, active = [], [], set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 2 + len(REASONS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for r, v in zip(REASONS, parts[2:]):
+                if v.lower().startswith("active"):
+                    active.add(r)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(active), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------
+# workload construction
+
+
+def build_workload(name):
+    import paper_2504_03074_b200 as wh
+    from paper_2504_03074_b200 import timestep as ts
+
+    dim, n, omega, forcing, iters = WORKLOADS[name]
+    ts._COURANT[2] = 0.9  # BASELINE "CFL 0.9"
+    g = wh.build_grid(dim, [(0.0, 1.0)] * dim, [n] * dim, "dirichlet")
+    if forcing[0] == "single":
+        f = wh.gaussian_source(g, omega, forcing[1], forcing[2], forcing[3])
+    else:
+        f = wh.multi_gaussian_source(g, omega, forcing[1], seed=0, slab_planes=64 if dim == 3 else 0)
+    corr = wh.correct_explicit(omega, g, 2, 1.0)
+    cfg = wh.FilterConfig(omega=omega, periods=1, steps_per_period=corr.steps_per_period, mode="explicit")
+    return g, f, corr, cfg, iters
+
+
+def forcing_desc(name):
+    dim, n, omega, forcing, iters = WORKLOADS[name]
+    if forcing[0] == "single":
+        return f"{forcing[1]}*exp(-{forcing[2]}|x-{forcing[3]}|^2)"
+    return f"sum of {forcing[1]} Gaussians, amp U(-100,100), centre U(0.1,0.9)^{dim}, width U(100,1000), seed 0"
+
+
+# ------------------------------------------------------------------------------------------
+# CPU baseline (numpy restatement = the reference's own numpy call sequence, 1 core)
+
+
+def cpu_baseline_numpy(g, f, corr, target_s=12.0):
+    from oracle import waveholtz_oracle as O
+
+    sc = O.step_scalars(corr.steps_per_period, corr.dt, corr.omega_tilde)
+    fv = np.array(f.values)
+    v = np.zeros_like(fv)
+
+    def run(nsteps):
+        s = dict(sc)
+        s["n_total"] = nsteps
+        t0 = time.perf_counter()
+        O.wave_solve_filtered(v, fv, g.spacing, s)
+        return time.perf_counter() - t0
+
+    t3 = run(3)
+    nsteps = int(max(3, min(corr.steps_per_period, target_s / max(t3 / 3, 1e-6))))
+    dt = run(nsteps)
+    gpts = g.size * nsteps / dt / 1e9
+    return {"value": gpts, "unit": "Gpts/s", "cores": 1, "kind": "port",
+            "sample": f"{nsteps} fused leapfrog+filter steps of the {'x'.join(map(str, g.shape))} grid through "
+                      f"oracle/waveholtz_oracle.py (the reference's numpy ufunc sequence, bitwise identical to it; "
+                      f"numpy elementwise ufuncs run on 1 core); {dt:.2f} s"}
+
+
+# ------------------------------------------------------------------------------------------
+# our arm
+
+
+def load_traffic(workload):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p)).get(workload)
+    return None if d is None else d.get("bytes_per_launch")
+
+
+def run_ours(args, dist, ws, rank, local):
+    import torch
+
+    import paper_2504_03074_b200 as wh
+    from paper_2504_03074_b200 import _native
+    from paper_2504_03074_b200.device import DeviceProblem
+
+    torch.cuda.set_device(local)
+    g, f, corr, cfg, _ = build_workload(args.workload)
+    f_sha = hashlib.sha256(np.ascontiguousarray(f.values).tobytes()).hexdigest()
+    prob = wh.HelmholtzProblem(g, 2, 1.0, cfg.omega, f)
+    sched = wh.time_schedule(corr, cfg)
+    dp = DeviceProblem(g, c=1.0, device=local)
+    dp.set_schedule(sched)
+    dp.set_forcing(f.values)
+    ctx = dp.ctx
+    ctx.set_l2_flush(256 << 20)
+    ctx.set_timing(True)
+    K, W = args.steps, args.warmup
+    n_t = sched["n_total"]
+    npts = g.size
+
+    # warm-up (same code path), then reset to v = 0 so the timed K iterations are the solve itself
+    ctx.zero(_native.V)
+    if W > 0:
+        ctx.fpi(W)
+    ctx.zero(_native.V)
+    torch.cuda.synchronize()
+    barrier(dist)
+    sampler = ClockSampler(local).start()
+    l0 = ctx.launch_count()
+    torch.cuda.synchronize()
+    t_wall0 = time.perf_counter()
+    rs = ctx.fpi(K)  # K passes back-to-back on the context stream, events around each pass
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter() - t_wall0
+    launches = ctx.launch_count() - l0
+    clocks = sampler.stop()
+    step_ms_total, step_launches, solve_ms = ctx.last_timing()
+    barrier(dist)
+    dev_s = max_over_ranks(dist, solve_ms / 1e3)
+    residuals = [math.sqrt(x) / math.sqrt(npts) for x in rs[:, 0]]
+
+    units = npts * n_t * K * ws
+    value = units / dev_s / 1e9
+    ms_per_step = dev_s * 1e3 / K
+    avg_launch_s = (step_ms_total / 1e3) / max(1, step_launches)
+    peak, peak_src = peaks()
+    achieved = BYTES_PER_UPDATE * npts / avg_launch_s / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": load_traffic(args.workload),
+            "kernel": "step_kernel (fused Laplacian + leapfrog + filter accumulate)",
+            "bytes_per_launch": BYTES_PER_UPDATE * npts, "avg_launch_us": avg_launch_s * 1e6,
+            "peak_source": peak_src,
+            "note": "average over all N_t step launches of each pass incl. the first/last-step variants and "
+                    "the per-pass residual reduction (events bracket whole passes)"}
+
+    # e2e: host pinned buffers in and out every step, through the public HostFPIStep call
+    e2e = None
+    if not args.no_e2e:
+        stepper = wh.HostFPIStep(prob, cfg)
+        bufs = [_native.PinnedBuffer(g.shape), _native.PinnedBuffer(g.shape)]
+        bufs[0].array[...] = 0.0
+        for i in range(W):
+            stepper(bufs[i % 2].array, bufs[(i + 1) % 2].array)
+        bufs[0].array[...] = 0.0
+        barrier(dist)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i in range(K):
+            stepper(bufs[i % 2].array, bufs[(i + 1) % 2].array)
+        torch.cuda.synchronize()
+        te = max_over_ranks(dist, time.perf_counter() - t0)
+        final = bufs[K % 2].array
+        if rank == 0 and K <= 500:
+            # the e2e path computes the same iterates as the device-resident one
+            vdev = ctx.download(_native.V)
+            if not np.array_equal(final, vdev):
+                print("WARNING: e2e iterate differs from device-resident iterate", file=sys.stderr)
+        e2e = {"value": units / te / 1e9, "unit": "Gpts/s", "h2d_bytes_per_step": npts * 8,
+               "d2h_bytes_per_step": npts * 8 + 8, "iters_per_s": K * ws / te,
+               "api": "paper_2504_03074_b200.HostFPIStep (C ABI whb_iterate_host), pinned host buffers"}
+        for b in bufs:
+            b.free()
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_numpy(g, f, corr)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "Gpts/s", "n_gpus": ws, "steps": K, "warmup": W,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (BASELINE forcing recipe, SURVEY §8(d)); f sha256 " + f_sha[:16],
+            "config": {"workload": args.workload, "grid": list(g.shape), "omega": cfg.omega,
+                       "N_t": n_t, "iterations": K, "cfl": 0.9, "forcing": forcing_desc(args.workload),
+                       "parallelism": f"independent replicas x{ws}" if ws > 1 else "single GPU",
+                       "l2": f"flushed before every timed iteration (256 MiB write, outside the timed span); "
+                             f"resident set {5 * npts * 8 / 2**20:.0f} MiB"},
+            "iters_per_s": K * ws / dev_s,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": launches,
+            "residuals": {"first": residuals[0], "last": residuals[-1]},
+            "wall_s_timed_region": t_wall, "impl": "ours",
+        }
+        print(json.dumps(line))
+
+
+# ------------------------------------------------------------------------------------------
+# reference arm: C OpenMP restatement of the reference on all host cores
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    from oracle import native as ON
+    from oracle import waveholtz_oracle as O
+
+    g, f, corr, cfg, _ = build_workload(args.workload)
+    sc = O.step_scalars(corr.steps_per_period, corr.dt, corr.omega_tilde)
+    fv = np.array(f.values)
+    threads = ON.max_threads()
+    npts = g.size
+    v = np.zeros_like(fv)
+    # sample size: full iterations when one takes <= ~3 s, else a truncated pass of m steps
+    t0 = time.perf_counter()
+    s5 = dict(sc)
+    s5["n_total"] = 5
+    ON.wave_solve(v, fv, g.spacing, s5, nthreads=threads)
+    per_step = (time.perf_counter() - t0) / 5
+    n_t = sc["n_total"]
+    m = n_t if per_step * n_t <= 3.0 else max(5, int(3.0 / per_step))
+    sm = dict(sc)
+    sm["n_total"] = m
+    for _ in range(args.warmup):
+        v = ON.wave_solve(v, fv, g.spacing, sm, nthreads=threads)
+    v[...] = 0.0
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v = ON.wave_solve(v, fv, g.spacing, sm, nthreads=threads)
+        _ = np.linalg.norm(v)  # the reference's per-iteration residual norm (driver.py:225)
+    dt = time.perf_counter() - t0
+    value = npts * m * args.steps / dt / 1e9
+    sample = (f"{'full WaveHoltz iteration' if m == n_t else f'{m} of {n_t} leapfrog steps'} per step of "
+              f"the {'x'.join(map(str, g.shape))} grid through oracle/whb_oracle.c (bitwise restatement of the "
+              f"reference, -O2 -ffp-contract=off, OpenMP {threads} threads)")
+    line = {
+        "metric": METRIC, "value": value, "unit": "Gpts/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE forcing recipe)",
+        "config": {"workload": args.workload, "grid": list(g.shape), "omega": cfg.omega, "N_t": n_t,
+                   "iterations": args.steps, "cfl": 0.9},
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "Gpts/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "Gpts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.steps is None:
+        args.steps = WORKLOADS[args.workload][4]
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    dist = init_dist(ws)
+    try:
+        run_ours(args, dist, ws, rank, local)
+    finally:
+        if dist is not None:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

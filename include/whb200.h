@@ -171,6 +171,9 @@ int whb_launch_count(whb_ctx *ctx, int64_t *count);
 int whb_set_timing(whb_ctx *ctx, int enable);
 int whb_last_timing(whb_ctx *ctx, double *step_kernel_ms_total, int64_t *step_kernel_launches,
                     double *solve_ms_total);
+/* Benchmark hygiene: when bytes > 0, whb_fpi writes a scratch buffer of that
+ * size (larger than the 126 MB L2) before every pass, outside the timed span. */
+int whb_set_l2_flush(whb_ctx *ctx, int64_t bytes);
 /* Pinned host buffers for H2D/D2H at full PCIe rate. */
 int whb_host_alloc(void **ptr, int64_t bytes);
 int whb_host_free(void *ptr);

@@ -17,6 +17,7 @@ Extensions beyond the reference: 3D grids, batched frequencies
 from .device import DeviceProblem, release_device_cache
 from .driver import (
     HelmholtzProblem,
+    HostFPIStep,
     NearSingularError,
     WaveHoltzRun,
     apply_A,

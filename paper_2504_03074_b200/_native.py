@@ -28,7 +28,7 @@ EXPORTS = (
     "whb_vec_lincomb", "whb_vec_sub_into", "whb_vec_copy", "whb_matvec", "whb_solve_begin",
     "whb_step", "whb_solve_end", "whb_level_plane_ptr", "whb_stream_ptr", "whb_synchronize",
     "whb_copy_plane", "whb_launch_count", "whb_set_timing", "whb_last_timing", "whb_host_alloc",
-    "whb_host_free", "whb_geometry",
+    "whb_host_free", "whb_geometry", "whb_set_l2_flush",
 )
 
 _lib = None
@@ -88,6 +88,7 @@ def load():
         "whb_host_alloc": ([ctypes.POINTER(vp), c_i64], c_int),
         "whb_host_free": ([vp], c_int),
         "whb_geometry": ([vp, ip64, ip64, ip64], c_int),
+        "whb_set_l2_flush": ([vp, c_i64], c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -320,6 +321,9 @@ class Context:
         check(load().whb_last_timing(self._h, ctypes.byref(a), ctypes.byref(n), ctypes.byref(b)),
               "whb_last_timing")
         return a.value, n.value, b.value
+
+    def set_l2_flush(self, nbytes: int):
+        check(load().whb_set_l2_flush(self._h, int(nbytes)), "whb_set_l2_flush")
 
     def geometry(self):
         s = np.zeros(3, dtype=np.int64)

@@ -28,7 +28,7 @@ from .timestep import correct_explicit, time_schedule
 __all__ = [
     "HelmholtzProblem", "WaveHoltzRun", "NearSingularError", "gaussian_source", "multi_gaussian_source",
     "fpi_solve", "krylov_solve", "waveholtz_operator", "apply_A", "measure_rate",
-    "resolve_time_discretization", "resonance_gap",
+    "resolve_time_discretization", "resonance_gap", "HostFPIStep",
 ]
 
 
@@ -294,3 +294,27 @@ def krylov_solve(problem, config, tol=1e-10, restart=50, maxit=500, deflation=No
     run = WaveHoltzRun(method="gmres", periods=cfg.periods, residuals=[r / scale for r in rep.residual_history],
                        iterations=rep.iterations, converged=rep.converged, wall_time=wall, inner_iterations=0)
     return GridField.from_values(problem.grid, x), run
+
+
+class HostFPIStep:
+    """The body of the reference's fixed-point loop with host buffers
+    (driver.py:222-226): ``diff = step(v_in, v_out)`` copies v_in to the device,
+    runs one W(v, f) pass, copies v_new into v_out and returns
+    ||v_new - v_in||_2 / sqrt(N).  Pass pinned arrays (``_native.PinnedBuffer``)
+    for full-rate transfers; f stays resident after the first call."""
+
+    def __init__(self, problem, config):
+        corr, cfg = resolve_time_discretization(problem, config)
+        self.problem = problem
+        self.config = cfg
+        self.dp = _device_for(problem)
+        self.dp.set_schedule(time_schedule(corr, cfg))
+        self.dp.set_forcing(problem.forcing.values)
+        self._root_n = math.sqrt(problem.grid.size)
+
+    def __call__(self, v_in: np.ndarray, v_out: np.ndarray) -> float:
+        if v_in.shape != tuple(self.problem.grid.shape) or v_out.shape != v_in.shape:
+            raise ValueError("v_in/v_out must have the grid shape")
+        if not (v_in.flags.c_contiguous and v_out.flags.c_contiguous and v_out.flags.writeable):
+            raise ValueError("v_in/v_out must be C-contiguous (v_out writeable)")
+        return math.sqrt(self.dp.ctx.iterate_host(v_in, v_out)) / self._root_n
