@@ -21,6 +21,8 @@
 // cache-line boundary.  2D grids (n0, n1) are stored as (n0, 1, n1) and 1D
 // grids (n) as (1, 1, n), so the same kernel marches along storage axis 0
 // with the contiguous axis across the warp.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -87,9 +89,9 @@ struct Member {
 
 enum { K_FIRST = 0, K_MID = 1, K_LAST = 2 };
 
-__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
-__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
-__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double whb_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double whb_sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double whb_mul(double a, double b) { return __dmul_rn(a, b); }
 
 // Fused leapfrog + filter march over planes [i0, i1) of one (j, k) column.
 template <int KIND, bool ZF, bool A0, bool A1>
@@ -131,46 +133,46 @@ __device__ __forceinline__ void march(const Geom &g, const Member &m, int s, int
         // c^2 * Laplacian in reference order: out = 0; per axis: +lo, +mid, +hi (grid.py:357-366)
         double lap = 0.0;
         if (A0) {
-            lap = dadd(lap, dmul(g.clo0, wm));
-            lap = dadd(lap, dmul(g.cmid0, wc));
-            lap = dadd(lap, dmul(g.clo0, wp));
+            lap = whb_add(lap, whb_mul(g.clo0, wm));
+            lap = whb_add(lap, whb_mul(g.cmid0, wc));
+            lap = whb_add(lap, whb_mul(g.clo0, wp));
         }
         if (A1) {
-            lap = dadd(lap, dmul(g.clo1, yl));
-            lap = dadd(lap, dmul(g.cmid1, wc));
-            lap = dadd(lap, dmul(g.clo1, yh));
+            lap = whb_add(lap, whb_mul(g.clo1, yl));
+            lap = whb_add(lap, whb_mul(g.cmid1, wc));
+            lap = whb_add(lap, whb_mul(g.clo1, yh));
         }
-        lap = dadd(lap, dmul(g.clo2, xl));
-        lap = dadd(lap, dmul(g.cmid2, wc));
-        lap = dadd(lap, dmul(g.clo2, xh));
-        if (g.use_c2) lap = dmul(lap, g.c2);
+        lap = whb_add(lap, whb_mul(g.clo2, xl));
+        lap = whb_add(lap, whb_mul(g.cmid2, wc));
+        lap = whb_add(lap, whb_mul(g.clo2, xh));
+        if (g.use_c2) lap = whb_mul(lap, g.c2);
 
         double wn;
         if (KIND == K_FIRST) {
             // w1 = w + (dt^2/2)*(lap - f)                        timestep.py:137
-            const double d = ZF ? lap : dsub(lap, fv);
-            wn = dadd(wc, dmul(h, d));
+            const double d = ZF ? lap : whb_sub(lap, fv);
+            wn = whb_add(wc, whb_mul(h, d));
         } else {
             // w^{n+1} = (2w - w_prev) + dt^2*(lap - f*cos)       timestep.py:139-140
-            const double d = ZF ? lap : dsub(lap, dmul(fv, cosn));
-            wn = dadd(dsub(dmul(2.0, wc), wpv), dmul(h, d));
+            const double d = ZF ? lap : whb_sub(lap, whb_mul(fv, cosn));
+            wn = whb_add(whb_sub(whb_mul(2.0, wc), wpv), whb_mul(h, d));
         }
         if (KIND == K_FIRST) {
             // acc = c0*w0 ; acc += c1*w1                          timestep.py:284, 298
             wnxt[p] = wn;
-            acc[p] = dadd(dmul(acc0, wc), dmul(accn, wn));
+            acc[p] = whb_add(whb_mul(acc0, wc), whb_mul(accn, wn));
         } else if (KIND == K_MID) {
             wnxt[p] = wn;
-            acc[p] = dadd(av, dmul(accn, wn));
+            acc[p] = whb_add(av, whb_mul(accn, wn));
         } else {
-            const double out = dmul(sc, dadd(av, dmul(accn, wn)));  // timestep.py:298-300
+            const double out = whb_mul(sc, whb_add(av, whb_mul(accn, wn)));  // timestep.py:298-300
             if (m.out_mode == WHB_OUT_FPI) {
                 const double vold = m.v[p];
                 const double dd = out - vold;
                 rsum += dd * dd;
                 m.v[p] = out;
             } else if (m.out_mode == WHB_OUT_AV) {
-                m.dst[p] = dsub(m.v[p], out);  // driver.py:259
+                m.dst[p] = whb_sub(m.v[p], out);  // driver.py:259
             } else {
                 m.dst[p] = out;
             }
@@ -277,6 +279,10 @@ __global__ void zero_boundary_kernel(double *x, long long S0, int P, int n1, int
         if (z) x[(long long)plane * S0 + r] = 0.0;
     }
 }
+
+}  // namespace
+#include "step_bulk.cuh"
+namespace {
 
 // Write a scratch buffer larger than L2 so the next timed pass starts cold.
 __global__ void l2_flush_kernel(double *buf, long long n, double val) {
@@ -390,12 +396,15 @@ struct whb_ctx {
     double *d_red = nullptr;        // vector reduction scratch (kRedBlocks + 1)
     double *h_red = nullptr;        // pinned scalar
     // launch geometry
+    int kern = 1;                   // 1: TMA bulk-copy pipelined kernel (2D/3D), 0: simple LDG kernel
+    size_t smem = 0;                // dynamic smem of the bulk kernel
+    int64_t slack_front = 0, slack_back = 0;  // allocation slack around every field (bulk halo reads)
     int BX = 128, BY = 1, gx = 1, JT = 1, chunk_len = 1, nchunks = 1;
     int upd_lo = 1, upd_hi = 2;     // local update planes [lo, hi)
     int nparts = 1;
     int64_t launches = 0;
     // graphs keyed by (out_mode, zf)
-    std::map<std::pair<int, int>, cudaGraphExec_t> graphs;
+    std::map<std::tuple<int, int, const void *>, cudaGraphExec_t> graphs;
     bool use_graphs = true;
     // timing
     bool timing = false;
@@ -408,6 +417,8 @@ struct whb_ctx {
     // optional L2 flush before every FPI pass (benchmark hygiene; not part of the timed span)
     double *flush_buf = nullptr;
     long long flush_elems = 0;
+    // TMA tensor maps keyed by (buffer, box kind)
+    std::map<std::pair<const double *, int>, CUtensorMap> tmaps;
 };
 
 namespace {
@@ -430,10 +441,20 @@ double *field_ptr(whb_ctx *c, int field, int member) {
     }
 }
 
+// Every field is allocated with slack before and after it: the bulk kernel's
+// row-segment loads may touch up to two rows before plane 0 and a few rows
+// after the last plane (values there only feed points that are never updated).
 int alloc_field(whb_ctx *c, double **p) {
-    WHB_CUDA(cudaMalloc(p, (size_t)c->field_elems * sizeof(double)));
-    WHB_CUDA(cudaMemsetAsync(*p, 0, (size_t)c->field_elems * sizeof(double), c->stream));
+    const size_t total = (size_t)(c->slack_front + c->field_elems + c->slack_back);
+    double *raw = nullptr;
+    WHB_CUDA(cudaMalloc(&raw, total * sizeof(double)));
+    WHB_CUDA(cudaMemsetAsync(raw, 0, total * sizeof(double), c->stream));
+    *p = raw + c->slack_front;
     return 0;
+}
+
+void free_field(whb_ctx *c, double *p) {
+    if (p) cudaFree(p - c->slack_front);
 }
 
 int ensure_out(whb_ctx *c, int member) {
@@ -452,22 +473,79 @@ double *vec_ptr(whb_ctx *c, int id) {
 inline double *owned(double *base, whb_ctx *c) { return base + c->S0; }
 inline long long owned_elems(whb_ctx *c) { return (long long)c->nloc * c->S0; }
 
+// Bulk-kernel tile configurations: 3D 8 x 64 tiles, 6 stages (17.7 KB each,
+// 2 CTAs/SM); 2D 1 x 256 row segments, 8 stages (8.2 KB each, 3 CTAs/SM).
+constexpr int B3_TX = 64, B3_BY = 8, B3_ST = 6;
+constexpr int B2_TX = 256, B2_BY = 1, B2_ST = 8;
+
+template <bool A1, int KIND, bool ZF, bool TENSOR>
+auto bulk_fn() {
+    if constexpr (A1) return bulk::step_bulk_kernel<B3_TX, B3_BY, B3_ST, true, KIND, ZF, TENSOR>;
+    else return bulk::step_bulk_kernel<B2_TX, B2_BY, B2_ST, false, KIND, ZF, false>;
+}
+
+template <bool A1, bool TENSOR>
+cudaError_t bulk_set_attrs(size_t smem) {
+    cudaError_t e = cudaSuccess;
+    auto set = [&](auto fn) {
+        cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (r != cudaSuccess) e = r;
+    };
+    set(bulk_fn<A1, K_FIRST, false, TENSOR>()); set(bulk_fn<A1, K_FIRST, true, TENSOR>());
+    set(bulk_fn<A1, K_MID, false, TENSOR>());   set(bulk_fn<A1, K_MID, true, TENSOR>());
+    set(bulk_fn<A1, K_LAST, false, TENSOR>());  set(bulk_fn<A1, K_LAST, true, TENSOR>());
+    return e;
+}
+
+// ---- TMA tensor maps (3D path) --------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+int get_encoder() {
+    if (g_encode) return 0;
+    cudaDriverEntryPointQueryResult q;
+    void *fn = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+        return fail(WHB_E_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    return 0;
+}
+
 int occupancy_blocks(whb_ctx *c) {
     int nb = 0;
     cudaError_t e;
     const int threads = c->BX * c->BY;
-    if (c->act1) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, step_kernel<true, true>, threads, 0);
+    if (c->kern == 1) {
+        if (c->act1) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, bulk_fn<true, K_MID, false, true>(), B3_TX * B3_BY / 2, c->smem);
+        else e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, bulk_fn<false, K_MID, false, false>(), B2_TX * B2_BY / 2, c->smem);
+    } else if (c->act1) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, step_kernel<true, true>, threads, 0);
     else if (c->act0) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, step_kernel<true, false>, threads, 0);
     else e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, step_kernel<false, false>, threads, 0);
-    if (e != cudaSuccess || nb < 1) nb = 4;
+    if (e != cudaSuccess || nb < 1) nb = 1;
     return nb;
 }
 
 int plan_launch(whb_ctx *c) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-    c->BX = c->act1 ? 32 : 128;
-    c->BY = c->act1 ? 8 : 1;
+    const char *kenv = getenv("WHB_KERNEL");
+    const std::string kname = kenv ? kenv : "";
+    // 3D single problem: TMA tensor boxes (kern 2); 2D / batched: per-row bulk copies (kern 1)
+    c->kern = !c->act0 ? 0 : (kname == "simple" ? 0 : ((c->act1 && c->nbatch == 1 && kname != "bulk") ? 2 : 1));
+    if (c->kern == 2) WHB_TRY(get_encoder());
+    if (c->kern >= 1) {
+        c->BX = c->act1 ? B3_TX : B2_TX;
+        c->BY = c->act1 ? B3_BY : B2_BY;
+        c->smem = c->act1 ? bulk::bulk_smem_bytes<B3_TX, B3_BY, B3_ST, true>()
+                          : bulk::bulk_smem_bytes<B2_TX, B2_BY, B2_ST, false>();
+        cudaError_t e = c->act1 ? (c->kern == 2 ? bulk_set_attrs<true, true>(c->smem) : bulk_set_attrs<true, false>(c->smem))
+                                : bulk_set_attrs<false, false>(c->smem);
+        if (e != cudaSuccess) return fail(WHB_E_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    } else {
+        c->BX = c->act1 ? 32 : 128;
+        c->BY = c->act1 ? 8 : 1;
+        c->smem = 0;
+    }
     const int64_t n1 = c->gshape[1], n2 = c->gshape[2];
     c->gx = (int)((n2 - 1 + c->BX - 1) / c->BX);               // covers k in [0, n2-1)
     c->JT = c->act1 ? (int)((n1 - 1 + c->BY - 1) / c->BY) : 1;  // covers j in [0, n1-1)
@@ -483,20 +561,33 @@ int plan_launch(whb_ctx *c) {
     }
     const int nplanes = std::max(1, c->upd_hi - c->upd_lo);
     const int per_sm = occupancy_blocks(c);
-    const long long target = (long long)sms * per_sm * 2;  // ~2 waves
+    const long long resident = (long long)sms * per_sm;
     const long long tiles = (long long)c->gx * c->JT;
-    int nch = (int)std::max<long long>(1, target / std::max<long long>(1, tiles));
+    int cl;
+    if (c->kern >= 1) {
+        // marching kernel: 2D -> one wave of long-lived CTAs; 3D -> ~4 waves (measured: 257^3
+        // 1 wave 101.6, 2 waves 109.0, 3.5 waves 111.4 Gpts/s); chunk only when tiles are scarce
+        const long long waves = c->act1 ? 4 : 1;
+        const long long nch = std::max<long long>(1, waves * resident / std::max<long long>(1, tiles));
+        cl = (int)((nplanes + nch - 1) / nch);
+    } else {
+        const long long target = resident * 2;
+        int nch = (int)std::max<long long>(1, target / std::max<long long>(1, tiles));
+        cl = (nplanes + nch - 1) / nch;
+        const int min_chunk = c->act1 ? 4 : 8;
+        if (cl < min_chunk) cl = std::min(nplanes, min_chunk);
+    }
     const char *env = getenv("WHB_CHUNK");
-    int cl = (nplanes + nch - 1) / nch;
-    const int min_chunk = c->act1 ? 4 : 8;
-    if (cl < min_chunk) cl = std::min(nplanes, min_chunk);
     if (env && atoi(env) > 0) cl = atoi(env);
     if (!c->act0) cl = 1;
-    c->chunk_len = cl;
-    c->nchunks = (nplanes + cl - 1) / cl;
+    c->chunk_len = std::max(1, cl);
+    c->nchunks = (nplanes + c->chunk_len - 1) / c->chunk_len;
     if ((long long)c->JT * c->nchunks > 65535)
         return fail(WHB_E_ARG, "grid too large for launch plan (axis-1 tiles x chunks > 65535)");
     c->nparts = c->gx * c->JT * (c->nchunks + 2);
+    // slack: bulk row segments start 2 columns / 1 row early and may run BY+1 rows past the last plane
+    c->slack_front = 2 * (int64_t)c->P + 32;
+    c->slack_back = (int64_t)(c->BY + 3) * c->P + c->BX + 64;
     return 0;
 }
 
@@ -558,9 +649,78 @@ int upload_members(whb_ctx *c, int out_mode, int zf, const double *vx = nullptr,
     return 0;
 }
 
+struct StepMaps {
+    CUtensorMap w, p, f, a;
+};
+
+template <bool A1, int KIND, bool ZF, bool TENSOR>
+void launch_bulk(whb_ctx *c, dim3 grid, int member_off, int s, int i_begin, int i_end, int chunk_len, int part_off,
+                 const StepMaps &mp) {
+    constexpr int threads = A1 ? B3_TX * B3_BY / 2 : B2_TX * B2_BY / 2;
+    bulk_fn<A1, KIND, ZF, TENSOR>()<<<grid, threads, c->smem, c->stream>>>(
+        c->geom, c->d_members, member_off, s, i_begin, i_end, chunk_len, c->JT, part_off, mp.w, mp.p, mp.f, mp.a);
+}
+
+template <bool A1, bool TENSOR>
+void launch_bulk_kind(whb_ctx *c, int kind, bool zf, dim3 grid, int off, int s, int ib, int ie, int cl, int po,
+                      const StepMaps &mp) {
+    if (kind == K_FIRST) {
+        if (zf) launch_bulk<A1, K_FIRST, true, TENSOR>(c, grid, off, s, ib, ie, cl, po, mp);
+        else launch_bulk<A1, K_FIRST, false, TENSOR>(c, grid, off, s, ib, ie, cl, po, mp);
+    } else if (kind == K_MID) {
+        if (zf) launch_bulk<A1, K_MID, true, TENSOR>(c, grid, off, s, ib, ie, cl, po, mp);
+        else launch_bulk<A1, K_MID, false, TENSOR>(c, grid, off, s, ib, ie, cl, po, mp);
+    } else {
+        if (zf) launch_bulk<A1, K_LAST, true, TENSOR>(c, grid, off, s, ib, ie, cl, po, mp);
+        else launch_bulk<A1, K_LAST, false, TENSOR>(c, grid, off, s, ib, ie, cl, po, mp);
+    }
+}
+
+// Tensor map of one field buffer viewed as (planes, n1, pitch) float64 with a (BY+2)x(TX+4)
+// box (w, with halo) or a BY x TX box (prev / f / acc).  Cached per (pointer, box).
+int tensor_map(whb_ctx *c, const double *base, bool wbox, CUtensorMap *out);
+
+// Launch step s for the first `nact` members of the table (sorted by n_total,
+// descending).  The bulk kernel is specialised on the step kind, so members
+// finishing at this step (LAST) get their own launch.
 int launch_step(whb_ctx *c, int s, int nact, int i_begin, int i_end, int chunk_len, int part_off) {
     if (nact <= 0 || i_begin >= i_end) return 0;
     const int nch = (i_end - i_begin + chunk_len - 1) / chunk_len;
+    if (c->kern >= 1) {
+        const bool zf = c->cur_zf != 0;
+        StepMaps mp;
+        std::memset(&mp, 0, sizeof(mp));
+        if (c->kern == 2) {
+            // member 0 of the current table (nbatch == 1): buffers of this step
+            const Member &m0 = c->h_members[0];
+            const double *wcur = (s == 0) ? m0.v : ((s & 1) ? m0.wa : m0.wb);
+            const double *wprv = (s == 1) ? m0.v : ((s & 1) ? m0.wb : m0.wa);
+            WHB_TRY(tensor_map(c, wcur, true, &mp.w));
+            WHB_TRY(tensor_map(c, wprv, false, &mp.p));
+            WHB_TRY(tensor_map(c, m0.acc, false, &mp.a));
+            if (m0.f) WHB_TRY(tensor_map(c, m0.f, false, &mp.f));
+        }
+        int nlast = 0;
+        for (int pos = 0; pos < nact; ++pos) nlast += (c->mem[c->order[pos]].n_total - 1 == s);
+        const int nmid = nact - nlast;
+        auto go = [&](int kind, int off, int cnt) {
+            if (cnt <= 0) return;
+            dim3 grid(c->gx, c->JT * nch, cnt);
+            if (c->act1) {
+                if (c->kern == 2) launch_bulk_kind<true, true>(c, kind, zf, grid, off, s, i_begin, i_end, chunk_len, part_off, mp);
+                else launch_bulk_kind<true, false>(c, kind, zf, grid, off, s, i_begin, i_end, chunk_len, part_off, mp);
+            } else
+                launch_bulk_kind<false, false>(c, kind, zf, grid, off, s, i_begin, i_end, chunk_len, part_off, mp);
+            c->launches++;
+        };
+        if (s == 0) go(K_FIRST, 0, nact);
+        else {
+            go(K_MID, 0, nmid);
+            go(K_LAST, nmid, nlast);
+        }
+        WHB_CUDA(cudaGetLastError());
+        return 0;
+    }
     dim3 grid(c->gx, c->JT * nch, nact);
     dim3 block(c->BX, c->BY, 1);
     if (c->act1)
@@ -574,6 +734,28 @@ int launch_step(whb_ctx *c, int s, int nact, int i_begin, int i_end, int chunk_l
                                                                chunk_len, c->JT, part_off);
     c->launches++;
     WHB_CUDA(cudaGetLastError());
+    return 0;
+}
+
+int tensor_map(whb_ctx *c, const double *base, bool wbox, CUtensorMap *out) {
+    auto key = std::make_pair(base, wbox ? 1 : 0);
+    auto it = c->tmaps.find(key);
+    if (it != c->tmaps.end()) {
+        *out = it->second;
+        return 0;
+    }
+    WHB_TRY(get_encoder());
+    CUtensorMap m;
+    cuuint64_t dims[3] = {(cuuint64_t)c->P, (cuuint64_t)c->gshape[1], (cuuint64_t)c->nplanes};
+    cuuint64_t strides[2] = {(cuuint64_t)c->P * sizeof(double), (cuuint64_t)c->S0 * sizeof(double)};
+    cuuint32_t box[3] = {(cuuint32_t)(wbox ? B3_TX + 4 : B3_TX), (cuuint32_t)(wbox ? B3_BY + 2 : B3_BY), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = g_encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(base), dims, strides, box,
+                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(WHB_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    c->tmaps.emplace(key, m);
+    *out = m;
     return 0;
 }
 
@@ -605,8 +787,11 @@ int enqueue_solve(whb_ctx *c, int out_mode) {
 }
 
 int run_solve(whb_ctx *c, int out_mode, int zf) {
+    c->cur_zf = zf;  // the bulk kernel is specialised on zero forcing
     if (!c->use_graphs) return enqueue_solve(c, out_mode);
-    auto key = std::make_pair(out_mode, zf);
+    // the 3D TMA path bakes member 0's tensor maps (its v buffer) into the graph
+    const void *vkey = (c->kern == 2 && !c->h_members.empty()) ? (const void *)c->h_members[0].v : nullptr;
+    auto key = std::make_tuple(out_mode, zf, vkey);
     auto it = c->graphs.find(key);
     if (it == c->graphs.end()) {
         cudaGraph_t g;
@@ -845,11 +1030,12 @@ int whb_destroy(whb_ctx *c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (auto &kv : c->graphs) cudaGraphExecDestroy(kv.second);
     for (auto &m : c->mem) {
-        cudaFree(m.v); cudaFree(m.f); cudaFree(m.wa); cudaFree(m.wb); cudaFree(m.acc); cudaFree(m.out);
+        free_field(c, m.v); free_field(c, m.f); free_field(c, m.wa); free_field(c, m.wb); free_field(c, m.acc);
+        free_field(c, m.out);
         cudaFree(m.cos_f); cudaFree(m.acc_c); cudaFree(m.partials);
     }
-    cudaFree(c->shared_f_ptr);
-    for (double *v : c->vecs) cudaFree(v);
+    free_field(c, c->shared_f_ptr);
+    for (double *v : c->vecs) free_field(c, v);
     cudaFree(c->d_members);
     cudaFree(c->d_hist);
     cudaFree(c->d_counter);
