@@ -182,6 +182,8 @@ def build_workload(name):
 
 
 def forcing_desc(name):
+    if name == "cfg5":
+        return "sum of 4 Gaussians, amp U(-100,100), centre U(0.1,0.9)^2, width U(100,1000), seed 0 (shared)"
     dim, n, omega, forcing, iters = WORKLOADS[name]
     if forcing[0] == "single":
         return f"{forcing[1]}*exp(-{forcing[2]}|x-{forcing[3]}|^2)"
@@ -197,6 +199,8 @@ def cpu_baseline_numpy(g, f, corr, target_s=12.0):
 
     sc = O.step_scalars(corr.steps_per_period, corr.dt, corr.omega_tilde)
     fv = np.array(f.values)
+    if fv.size > (1 << 25):  # 1025^3: time a slab of axis-0 planes (same per-point work, bounded RAM)
+        fv = np.ascontiguousarray(fv[: max(3, (1 << 25) // fv[0].size)])
     v = np.zeros_like(fv)
 
     def run(nsteps):
@@ -209,9 +213,9 @@ def cpu_baseline_numpy(g, f, corr, target_s=12.0):
     t3 = run(3)
     nsteps = int(max(3, min(corr.steps_per_period, target_s / max(t3 / 3, 1e-6))))
     dt = run(nsteps)
-    gpts = g.size * nsteps / dt / 1e9
+    gpts = fv.size * nsteps / dt / 1e9
     return {"value": gpts, "unit": "Gpts/s", "cores": 1, "kind": "port",
-            "sample": f"{nsteps} fused leapfrog+filter steps of the {'x'.join(map(str, g.shape))} grid through "
+            "sample": f"{nsteps} fused leapfrog+filter steps of a {'x'.join(map(str, fv.shape))} grid through "
                       f"oracle/waveholtz_oracle.py (the reference's numpy ufunc sequence, bitwise identical to it; "
                       f"numpy elementwise ufuncs run on 1 core); {dt:.2f} s"}
 
@@ -228,33 +232,137 @@ def load_traffic(workload):
     return None if d is None else d.get("bytes_per_launch")
 
 
+class SingleRun:
+    """One problem (configs 1-4) on this rank's GPU."""
+
+    def __init__(self, args, local):
+        import paper_2504_03074_b200 as wh
+        from paper_2504_03074_b200.device import DeviceProblem
+
+        g, f, corr, cfg, _ = build_workload(args.workload)
+        self.g, self.f, self.corr, self.cfg = g, f, corr, cfg
+        self.prob = wh.HelmholtzProblem(g, 2, 1.0, cfg.omega, f)
+        sched = wh.time_schedule(corr, cfg)
+        self.dp = DeviceProblem(g, c=1.0, device=local)
+        self.dp.set_schedule(sched)
+        self.dp.set_forcing(f.values)
+        self.ctx = self.dp.ctx
+        self.n_t = sched["n_total"]
+        self.npts = g.size
+        self.units_per_step = self.npts * self.n_t
+        self.members = 1
+        self.f_sha = hashlib.sha256(np.ascontiguousarray(f.values).tobytes()).hexdigest()
+        self.desc = {"grid": list(g.shape), "omega": cfg.omega, "N_t": self.n_t}
+
+    def reset(self):
+        from paper_2504_03074_b200 import _native
+
+        self.ctx.zero(_native.V)
+
+    def e2e(self, K, W, dist):
+        import torch
+
+        import paper_2504_03074_b200 as wh
+        from paper_2504_03074_b200 import _native
+
+        stepper = wh.HostFPIStep(self.prob, self.cfg)
+        bufs = [_native.PinnedBuffer(self.g.shape), _native.PinnedBuffer(self.g.shape)]
+        bufs[0].array[...] = 0.0
+        for i in range(W):
+            stepper(bufs[i % 2].array, bufs[(i + 1) % 2].array)
+        bufs[0].array[...] = 0.0
+        barrier(dist)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i in range(K):
+            stepper(bufs[i % 2].array, bufs[(i + 1) % 2].array)
+        torch.cuda.synchronize()
+        te = time.perf_counter() - t0
+        for b in bufs:
+            b.free()
+        return te, {"h2d_bytes_per_step": self.npts * 8, "d2h_bytes_per_step": self.npts * 8 + 8,
+                    "api": "paper_2504_03074_b200.HostFPIStep (C ABI whb_iterate_host), pinned host buffers"}
+
+
+class BatchRun:
+    """Config 5: the rank's LPT share of the 64 frequencies, batched on its GPU."""
+
+    def __init__(self, args, local, ws, rank):
+        import paper_2504_03074_b200 as wh
+        from paper_2504_03074_b200 import timestep as ts
+        from paper_2504_03074_b200.batch import BatchedFPI, lpt_shard
+
+        ts._COURANT[2] = 0.9
+        g = wh.build_grid(2, [(0.0, 1.0)] * 2, [1024, 1024], "dirichlet")
+        f = wh.multi_gaussian_source(g, 150.3, 4, seed=0)
+        omegas = np.linspace(10.3, 200.3, 64)
+        nts = [wh.correct_explicit(w, g, 2, 1.0).steps_per_period for w in omegas]
+        mine = lpt_shard(nts, ws)[rank]
+        self.g = g
+        self.solver = BatchedFPI(g, f, omegas[mine], device=local)
+        self.ctx = self.solver.ctx
+        self.npts = g.size
+        self.members = len(mine)
+        self.units_per_step = self.solver.updates_per_iteration
+        self.n_t = sum(self.solver.steps)
+        self.f_sha = hashlib.sha256(np.ascontiguousarray(f.values).tobytes()).hexdigest()
+        self.desc = {"grid": list(g.shape), "omegas": "np.linspace(10.3, 200.3, 64)", "N_t_sum_rank0": self.n_t,
+                     "members_rank0": self.members, "sharding": "LPT over N_t (batch.lpt_shard)"}
+
+    def reset(self):
+        self.solver.reset()
+
+    def e2e(self, K, W, dist):
+        import torch
+
+        from paper_2504_03074_b200 import _native
+
+        B = self.members
+        host = [_native.PinnedBuffer(self.g.shape) for _ in range(B)]
+        for h in host:
+            h.array[...] = 0.0
+
+        def step():
+            for b in range(B):
+                self.ctx.upload(_native.V, host[b].array, b)
+            self.ctx.fpi(1)
+            for b in range(B):
+                self.ctx.download(_native.V, b, out=host[b].array)
+
+        for _ in range(W):
+            step()
+        for h in host:
+            h.array[...] = 0.0
+        barrier(dist)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(K):
+            step()
+        torch.cuda.synchronize()
+        te = time.perf_counter() - t0
+        for h in host:
+            h.free()
+        return te, {"h2d_bytes_per_step": B * self.npts * 8, "d2h_bytes_per_step": B * self.npts * 8 + 8 * B,
+                    "api": "C ABI whb_upload / whb_fpi / whb_download per member, pinned host buffers"}
+
+
 def run_ours(args, dist, ws, rank, local):
     import torch
 
-    import paper_2504_03074_b200 as wh
     from paper_2504_03074_b200 import _native
-    from paper_2504_03074_b200.device import DeviceProblem
 
     torch.cuda.set_device(local)
-    g, f, corr, cfg, _ = build_workload(args.workload)
-    f_sha = hashlib.sha256(np.ascontiguousarray(f.values).tobytes()).hexdigest()
-    prob = wh.HelmholtzProblem(g, 2, 1.0, cfg.omega, f)
-    sched = wh.time_schedule(corr, cfg)
-    dp = DeviceProblem(g, c=1.0, device=local)
-    dp.set_schedule(sched)
-    dp.set_forcing(f.values)
-    ctx = dp.ctx
+    wl = BatchRun(args, local, ws, rank) if args.workload == "cfg5" else SingleRun(args, local)
+    ctx = wl.ctx
     ctx.set_l2_flush(256 << 20)
     ctx.set_timing(True)
     K, W = args.steps, args.warmup
-    n_t = sched["n_total"]
-    npts = g.size
 
     # warm-up (same code path), then reset to v = 0 so the timed K iterations are the solve itself
-    ctx.zero(_native.V)
+    wl.reset()
     if W > 0:
         ctx.fpi(W)
-    ctx.zero(_native.V)
+    wl.reset()
     torch.cuda.synchronize()
     barrier(dist)
     sampler = ClockSampler(local).start()
@@ -269,67 +377,65 @@ def run_ours(args, dist, ws, rank, local):
     step_ms_total, step_launches, solve_ms = ctx.last_timing()
     barrier(dist)
     dev_s = max_over_ranks(dist, solve_ms / 1e3)
-    residuals = [math.sqrt(x) / math.sqrt(npts) for x in rs[:, 0]]
+    residuals = np.sqrt(rs[:, 0]) / math.sqrt(wl.npts)
 
-    units = npts * n_t * K * ws
+    units_rank = wl.units_per_step * K
+    units = units_rank
+    if dist is not None:
+        import torch as _t
+
+        t = _t.tensor([float(units_rank)], dtype=_t.float64, device="cuda")
+        dist.all_reduce(t)
+        units = float(t.item())
+    elif ws > 1:
+        units = units_rank * ws
     value = units / dev_s / 1e9
     ms_per_step = dev_s * 1e3 / K
-    avg_launch_s = (step_ms_total / 1e3) / max(1, step_launches)
     peak, peak_src = peaks()
-    achieved = BYTES_PER_UPDATE * npts / avg_launch_s / 1e9
+    # algorithmic bytes of this rank's step kernels over the timed passes / their device time
+    achieved = BYTES_PER_UPDATE * units_rank / (step_ms_total / 1e3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": load_traffic(args.workload),
-            "kernel": "step_kernel (fused Laplacian + leapfrog + filter accumulate)",
-            "bytes_per_launch": BYTES_PER_UPDATE * npts, "avg_launch_us": avg_launch_s * 1e6,
+            "kernel": "fused step kernel (Laplacian + leapfrog + filter accumulate), TMA-staged",
+            "bytes_per_update": BYTES_PER_UPDATE,
+            "avg_launch_us": step_ms_total * 1e3 / max(1, step_launches),
             "peak_source": peak_src,
-            "note": "average over all N_t step launches of each pass incl. the first/last-step variants and "
-                    "the per-pass residual reduction (events bracket whole passes)"}
+            "note": "48 algorithmic B per point update (SURVEY 8(d)) x updates / device time of the step "
+                    "launches (CUDA events on the context stream bracketing each pass; includes the "
+                    "per-pass residual reduction and inter-launch gaps)"}
 
-    # e2e: host pinned buffers in and out every step, through the public HostFPIStep call
     e2e = None
     if not args.no_e2e:
-        stepper = wh.HostFPIStep(prob, cfg)
-        bufs = [_native.PinnedBuffer(g.shape), _native.PinnedBuffer(g.shape)]
-        bufs[0].array[...] = 0.0
-        for i in range(W):
-            stepper(bufs[i % 2].array, bufs[(i + 1) % 2].array)
-        bufs[0].array[...] = 0.0
-        barrier(dist)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for i in range(K):
-            stepper(bufs[i % 2].array, bufs[(i + 1) % 2].array)
-        torch.cuda.synchronize()
-        te = max_over_ranks(dist, time.perf_counter() - t0)
-        final = bufs[K % 2].array
-        if rank == 0 and K <= 500:
-            # the e2e path computes the same iterates as the device-resident one
-            vdev = ctx.download(_native.V)
-            if not np.array_equal(final, vdev):
-                print("WARNING: e2e iterate differs from device-resident iterate", file=sys.stderr)
-        e2e = {"value": units / te / 1e9, "unit": "Gpts/s", "h2d_bytes_per_step": npts * 8,
-               "d2h_bytes_per_step": npts * 8 + 8, "iters_per_s": K * ws / te,
-               "api": "paper_2504_03074_b200.HostFPIStep (C ABI whb_iterate_host), pinned host buffers"}
-        for b in bufs:
-            b.free()
+        te, info = wl.e2e(K, W, dist)
+        te = max_over_ranks(dist, te)
+        e2e = {"value": units / te / 1e9, "unit": "Gpts/s", **info, "iters_per_s": K / te}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_numpy(g, f, corr)
+        if args.workload == "cfg5":
+            from paper_2504_03074_b200 import timestep as ts
+            import paper_2504_03074_b200 as wh
+
+            corr = wh.correct_explicit(100.0, wl.g, 2, 1.0)
+            f = wh.multi_gaussian_source(wl.g, 150.3, 4, seed=0)
+            cpu = cpu_baseline_numpy(wl.g, f, corr)
+        else:
+            cpu = cpu_baseline_numpy(wl.g, wl.f, wl.corr)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "Gpts/s", "n_gpus": ws, "steps": K, "warmup": W,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic (BASELINE forcing recipe, SURVEY §8(d)); f sha256 " + f_sha[:16],
-            "config": {"workload": args.workload, "grid": list(g.shape), "omega": cfg.omega,
-                       "N_t": n_t, "iterations": K, "cfl": 0.9, "forcing": forcing_desc(args.workload),
-                       "parallelism": f"independent replicas x{ws}" if ws > 1 else "single GPU",
-                       "l2": f"flushed before every timed iteration (256 MiB write, outside the timed span); "
-                             f"resident set {5 * npts * 8 / 2**20:.0f} MiB"},
-            "iters_per_s": K * ws / dev_s,
+            "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if args.workload == "cfg5" else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (BASELINE forcing recipe, SURVEY 8(d)); f sha256 " + wl.f_sha[:16],
+            "config": {"workload": args.workload, **wl.desc, "iterations": K, "cfl": 0.9,
+                       "forcing": forcing_desc(args.workload),
+                       "parallelism": (f"frequencies LPT-sharded over {ws} GPUs" if args.workload == "cfg5" else
+                                       f"independent replicas x{ws}") if ws > 1 else "single GPU",
+                       "l2": "flushed before every timed iteration (256 MiB write, outside the timed span)"},
+            "iters_per_s": K / dev_s,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": launches,
-            "residuals": {"first": residuals[0], "last": residuals[-1]},
+            "residuals": {"first": float(residuals[0]), "last": float(residuals[-1])},
             "wall_s_timed_region": t_wall, "impl": "ours",
         }
         print(json.dumps(line))
@@ -345,6 +451,8 @@ def run_reference(args, ws, rank):
     from oracle import native as ON
     from oracle import waveholtz_oracle as O
 
+    if args.workload == "cfg5":
+        return run_reference_cfg5(args, ws)
     g, f, corr, cfg, _ = build_workload(args.workload)
     sc = O.step_scalars(corr.steps_per_period, corr.dt, corr.omega_tilde)
     fv = np.array(f.values)
@@ -386,18 +494,58 @@ def run_reference(args, ws, rank):
     print(json.dumps(line))
 
 
+def run_reference_cfg5(args, ws):
+    """Config 5 on the host: every step is one full W pass of each of the 64 omegas
+    (the reference's per-omega loop), C restatement on all host cores."""
+    import paper_2504_03074_b200 as wh
+    from paper_2504_03074_b200 import timestep as ts
+    from oracle import native as ON
+    from oracle import waveholtz_oracle as O
+
+    ts._COURANT[2] = 0.9
+    g = wh.build_grid(2, [(0.0, 1.0)] * 2, [1024, 1024], "dirichlet")
+    fv = np.array(wh.multi_gaussian_source(g, 150.3, 4, seed=0).values)
+    omegas = np.linspace(10.3, 200.3, 64)
+    scs = [O.step_scalars(*O.correct_explicit(w, g.spacing, 2, 1.0, 0.9)) for w in omegas]
+    threads = ON.max_threads()
+    vs = [np.zeros_like(fv) for _ in omegas]
+    steps = min(args.steps, 3)  # bounded sample: ~1.1e10 updates per step
+    for _ in range(min(args.warmup, 1)):
+        ON.wave_solve(vs[0], fv, g.spacing, scs[0], nthreads=threads)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        for b, sc in enumerate(scs):
+            vs[b] = ON.wave_solve(vs[b], fv, g.spacing, sc, nthreads=threads)
+    dt = time.perf_counter() - t0
+    units = g.size * sum(sc["n_total"] for sc in scs) * steps
+    value = units / dt / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "Gpts/s", "n_gpus": ws, "steps": steps, "warmup": args.warmup,
+        "ms_per_step": dt * 1e3 / steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (BASELINE forcing recipe)",
+        "config": {"workload": "cfg5", "grid": list(g.shape), "omegas": "np.linspace(10.3, 200.3, 64)",
+                   "iterations": steps, "cfl": 0.9},
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "Gpts/s", "cores": threads, "kind": "port",
+                         "sample": f"{steps} WaveHoltz iteration(s) of all 64 omegas through oracle/whb_oracle.c "
+                                   f"(OpenMP {threads} threads)"},
+        "e2e": {"value": value, "unit": "Gpts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS) + ["cfg5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.steps is None:
-        args.steps = WORKLOADS[args.workload][4]
+        args.steps = 20 if args.workload == "cfg5" else WORKLOADS[args.workload][4]
     ws, rank, local = dist_env()
     if args.impl == "reference":
         run_reference(args, ws, rank)

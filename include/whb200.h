@@ -139,6 +139,9 @@ int whb_vec_div_into(whb_ctx *ctx, int x, double d, int y);                   /*
 int whb_vec_lincomb(whb_ctx *ctx, int y, int first, int count, const double *coef); /* y += Q[:,first:first+count]@coef, linalg.py:174 */
 int whb_vec_sub_into(whb_ctx *ctx, int x, int y, int z);                      /* z = x - y */
 int whb_vec_copy(whb_ctx *ctx, int x, int y);                                 /* y = x */
+/* y = c^2 * L_h x at interior points, boundary 0 (DiscreteOperator.apply_values,
+ * grid.py:346-368; p = 2, Dirichlet). */
+int whb_apply_operator(whb_ctx *ctx, int x, int y);
 /* y = x - W(x, 0)  (waveholtz_operator.matvec, driver.py:256-262) */
 int whb_matvec(whb_ctx *ctx, int x, int y);
 

@@ -28,7 +28,7 @@ EXPORTS = (
     "whb_vec_lincomb", "whb_vec_sub_into", "whb_vec_copy", "whb_matvec", "whb_solve_begin",
     "whb_step", "whb_solve_end", "whb_level_plane_ptr", "whb_stream_ptr", "whb_synchronize",
     "whb_copy_plane", "whb_launch_count", "whb_set_timing", "whb_last_timing", "whb_host_alloc",
-    "whb_host_free", "whb_geometry", "whb_set_l2_flush",
+    "whb_host_free", "whb_geometry", "whb_set_l2_flush", "whb_apply_operator",
 )
 
 _lib = None
@@ -89,6 +89,7 @@ def load():
         "whb_host_free": ([vp], c_int),
         "whb_geometry": ([vp, ip64, ip64, ip64], c_int),
         "whb_set_l2_flush": ([vp, c_i64], c_int),
+        "whb_apply_operator": ([vp, c_int, c_int], c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -270,6 +271,9 @@ class Context:
     def lincomb(self, y, first, coef):
         coef = np.ascontiguousarray(coef, dtype=np.float64)
         check(load().whb_vec_lincomb(self._h, int(y), int(first), len(coef), _dp(coef)), "whb_vec_lincomb")
+
+    def apply_operator(self, x, y):
+        check(load().whb_apply_operator(self._h, int(x), int(y)), "whb_apply_operator")
 
     def matvec(self, x, y):
         check(load().whb_matvec(self._h, int(x), int(y)), "whb_matvec")

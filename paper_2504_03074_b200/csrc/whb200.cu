@@ -284,6 +284,39 @@ __global__ void zero_boundary_kernel(double *x, long long S0, int P, int n1, int
 #include "step_bulk.cuh"
 namespace {
 
+// y = c^2 * L_h x at owned interior points (DiscreteOperator.apply_values, grid.py:346-368);
+// boundary and padding of y are left untouched (zero by invariant).
+__global__ void apply_operator_kernel(Geom g, const double *__restrict__ x, double *__restrict__ y, int act0,
+                                      int act1, int lp0, int lp1) {
+    const long long total = (long long)(lp1 - lp0) * g.S0;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long pl = t / g.S0;
+        const long long r = t - pl * g.S0;
+        const int j = (int)(r / g.P);
+        const int k = (int)(r - (long long)j * g.P);
+        if (k < 1 || k >= g.n2 - 1) continue;
+        if (act1 && (j < g.j_lo || j >= g.j_hi)) continue;
+        const long long p = (long long)(lp0 + pl) * g.S0 + r;
+        const double wc = x[p];
+        double lap = 0.0;
+        if (act0) {
+            lap = whb_add(lap, whb_mul(g.clo0, x[p - g.S0]));
+            lap = whb_add(lap, whb_mul(g.cmid0, wc));
+            lap = whb_add(lap, whb_mul(g.clo0, x[p + g.S0]));
+        }
+        if (act1) {
+            lap = whb_add(lap, whb_mul(g.clo1, x[p - g.P]));
+            lap = whb_add(lap, whb_mul(g.cmid1, wc));
+            lap = whb_add(lap, whb_mul(g.clo1, x[p + g.P]));
+        }
+        lap = whb_add(lap, whb_mul(g.clo2, x[p - 1]));
+        lap = whb_add(lap, whb_mul(g.cmid2, wc));
+        lap = whb_add(lap, whb_mul(g.clo2, x[p + 1]));
+        y[p] = whb_mul(lap, g.c2);  // out *= c**2 (grid.py:366)
+    }
+}
+
 // Write a scratch buffer larger than L2 so the next timed pass starts cold.
 __global__ void l2_flush_kernel(double *buf, long long n, double val) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -1330,6 +1363,21 @@ int whb_matvec(whb_ctx *c, int xi, int yi) {
         return fail(WHB_E_ARG, "whb_matvec operands may not alias the leapfrog workspace");
     WHB_TRY(upload_members(c, WHB_OUT_AV, 1, x, y));
     WHB_TRY(run_solve(c, WHB_OUT_AV, 1));
+    return 0;
+}
+
+int whb_apply_operator(whb_ctx *c, int xi, int yi) {
+    if (!c) return fail(WHB_E_ARG, "NULL argument");
+    if (xi == yi) return fail(WHB_E_ARG, "whb_apply_operator needs distinct x and y");
+    WHB_TRY(set_dev(c));
+    if (!c->op_set) return fail(WHB_E_STATE, "operator not set (whb_set_operator)");
+    VEC_OR_FAIL(x, xi);
+    VEC_OR_FAIL(y, yi);
+    // update planes exclude global Dirichlet planes; ghost planes of x must hold neighbour data
+    apply_operator_kernel<<<kRedBlocks, kRedThreads, 0, c->stream>>>(c->geom, x, y, c->act0, c->act1, c->upd_lo,
+                                                                     c->upd_hi);
+    c->launches++;
+    WHB_CUDA(cudaGetLastError());
     return 0;
 }
 

@@ -246,6 +246,23 @@ class DiscreteOperator:
     def stencil(self, axis: int) -> np.ndarray:
         return stencil_coefficients(self.order, self.grid.spacing[axis])
 
+    def apply_values(self, values: np.ndarray, ghost_scratch=None) -> np.ndarray:
+        """c^2 * L_h on a stored-point array, Dirichlet rows zero (grid.py:346-352), on the GPU."""
+        from . import _native
+        from .device import device_problem
+
+        dp = device_problem(self.grid, c=self.c, order=self.order)
+        dp.ctx.vec_upload(_native.WA, np.asarray(values, dtype=float))
+        dp.ctx.zero(_native.OUT)
+        dp.ctx.apply_operator(_native.WA, _native.OUT)
+        return dp.ctx.download(_native.OUT)
+
+    def apply(self, u) -> "GridField":
+        """grid.py:333-344."""
+        if u.grid is not self.grid and u.grid != self.grid:
+            raise ValueError("field grid does not match operator grid")
+        return GridField(self.grid, u.ghost, self.apply_values(u.values))
+
 
 def operator_coefficients(grid, order: int, c: float):
     """(clo[d], cmid[d], c2) exactly as the reference forms them: the taps
