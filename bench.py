@@ -346,12 +346,82 @@ class BatchRun:
                     "api": "C ABI whb_upload / whb_fpi / whb_download per member, pinned host buffers"}
 
 
+def run_slab(args, dist, ws, rank, local):
+    """Configs 3/4 at N > 1: one z-slab per GPU (slab.SlabFPI, NCCL halo exchange
+    overlapped with the interior planes).  Strong scaling: the grid is fixed."""
+    import torch
+
+    from paper_2504_03074_b200 import _native
+    from paper_2504_03074_b200.slab import DeviceShard, SlabFPI, TorchHalo, slab_ranges
+
+    g, f, corr, cfg, _ = build_workload(args.workload)
+    rng = slab_ranges(g.shape[0], ws)[rank]
+    shard = DeviceShard(g, rng, device=local)
+    solver = SlabFPI(shard, TorchHalo(dist, rank, ws), corr, cfg, f)
+    n_t = solver.shard.n_total
+    K, W = args.steps, args.warmup
+    for _ in range(W):
+        solver.iterate()
+    solver.reset()
+    shard.synchronize()
+    barrier(dist)
+    sampler = ClockSampler(local).start()
+    l0 = shard.ctx.launch_count()
+    stream = torch.cuda.ExternalStream(shard.ctx.stream_ptr(), device=f"cuda:{local}")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    res = [solver.iterate() for _ in range(K)]
+    e1.record(stream)
+    e1.synchronize()
+    clocks = sampler.stop()
+    launches = shard.ctx.launch_count() - l0
+    dev_s = max_over_ranks(dist, e0.elapsed_time(e1) / 1e3)
+    units = g.size * n_t * K
+    value = units / dev_s / 1e9
+    peak, peak_src = peaks()
+    e2e = None
+    if not args.no_e2e:
+        host = _native.PinnedBuffer(shard.ctx.local_shape)
+        host.array[...] = 0.0
+        barrier(dist)
+        t0 = time.perf_counter()
+        for _ in range(K):
+            shard.upload(_native.V, host.array)
+            solver.iterate()
+            shard.ctx.download(_native.V, out=host.array)
+        te = max_over_ranks(dist, time.perf_counter() - t0)
+        e2e = {"value": units / te / 1e9, "unit": "Gpts/s", "h2d_bytes_per_step": g.size * 8,
+               "d2h_bytes_per_step": g.size * 8 + 8,
+               "api": "slab.SlabFPI with per-rank whb_upload/whb_download of the owned planes (pinned)"}
+        host.free()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "Gpts/s", "n_gpus": ws, "steps": K, "warmup": W,
+            "ms_per_step": dev_s * 1e3 / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (BASELINE forcing recipe, SURVEY 8(d))",
+            "config": {"workload": args.workload, "grid": list(g.shape), "omega": cfg.omega, "N_t": n_t,
+                       "iterations": K, "cfl": 0.9, "forcing": forcing_desc(args.workload),
+                       "parallelism": f"z-slab decomposition over {ws} GPUs, NCCL halo exchange",
+                       "l2": "working set far above L2"},
+            "iters_per_s": K / dev_s,
+            "roofline": {"bound": "hbm", "achieved": BYTES_PER_UPDATE * units / ws / dev_s / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": BYTES_PER_UPDATE * units / ws / dev_s / 1e9 / peak,
+                         "traffic": None, "peak_source": peak_src,
+                         "note": "per GPU: 48 B/update x this rank's share of the updates / wall device time"},
+            "cpu_baseline": None, "e2e": e2e, "clocks": clocks, "gpu_launches": launches,
+            "residuals": {"first": res[0], "last": res[-1]}, "impl": "ours",
+        }
+        print(json.dumps(line))
+
+
 def run_ours(args, dist, ws, rank, local):
     import torch
 
     from paper_2504_03074_b200 import _native
 
     torch.cuda.set_device(local)
+    if ws > 1 and args.workload in ("cfg3", "cfg4") and args.decomp == "slab":
+        return run_slab(args, dist, ws, rank, local)
     wl = BatchRun(args, local, ws, rank) if args.workload == "cfg5" else SingleRun(args, local)
     ctx = wl.ctx
     ctx.set_l2_flush(256 << 20)
@@ -541,6 +611,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS) + ["cfg5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--decomp", default="slab", choices=["slab", "replicas"],
+                    help="N > 1 on configs 3/4: z-slab decomposition (default) or independent replicas")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
