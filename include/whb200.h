@@ -49,10 +49,12 @@ enum whb_status {
 enum whb_field {
     WHB_V = 0,    /* iterate v (W^0 of a solve; FPI updates it in place)      */
     WHB_F = 1,    /* forcing f(x) (shared by all members if shared_forcing)   */
-    WHB_WA = 2,   /* leapfrog buffer A (odd time levels)                      */
-    WHB_WB = 3,   /* leapfrog buffer B (even time levels >= 2)                */
+    WHB_WA = 2,   /* time levels 1, 5, 9, ...  (level L >= 1 in slot L mod 4)  */
+    WHB_WB = 3,   /* time levels 2, 6, 10, ...                                 */
     WHB_ACC = 4,  /* running filter sum                                        */
-    WHB_OUT = 5   /* output of a plain/matvec solve                            */
+    WHB_OUT = 5,  /* output of a plain/matvec solve                            */
+    WHB_WC = 6,   /* time levels 3, 7, 11, ...                                 */
+    WHB_WD = 7    /* time levels 4, 8, 12, ...                                 */
 };
 
 /* What the last step of a filtered solve writes (timestep.py:300-301, driver.py:222-225, 256-262). */
@@ -126,7 +128,7 @@ int whb_iterate_host(whb_ctx *ctx, const double *v_host, double *v_out_host, dou
 
 /* ---- Krylov vectors (gmres_solve, linalg.py:102-183; member 0 only) ------
  * Vector ids >= 0 name full-grid device vectors with the field layout.
- * Slots: id WHB_V..WHB_OUT alias the member-0 fields; ids >= 8 are extra
+ * Slots: ids WHB_V..WHB_WD alias the member-0 fields; ids >= 8 are extra
  * vectors reserved with whb_vec_reserve.  Reductions are deterministic
  * (fixed-order tree), over owned points. */
 int whb_vec_reserve(whb_ctx *ctx, int count, int *first_id);

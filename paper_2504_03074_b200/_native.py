@@ -15,7 +15,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "lib", "libwhb200.so")
 
 # enum whb_field / whb_out_mode (include/whb200.h)
-V, F, WA, WB, ACC, OUT = range(6)
+V, F, WA, WB, ACC, OUT, WC, WD = range(8)
 OUT_PLAIN, OUT_FPI, OUT_AV = 0, 1, 2
 E_ARG, E_CUDA, E_NOMEM, E_STATE, E_NODEV = -1, -2, -3, -4, -5
 

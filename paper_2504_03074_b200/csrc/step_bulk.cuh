@@ -132,9 +132,9 @@ __global__ void __launch_bounds__(Layout<TX, BY, A1>::THREADS)
         return;
     }
 
-    const double *wcur = (s == 0) ? m.v : ((s & 1) ? m.wa : m.wb);
-    const double *wprv = (s == 1) ? m.v : ((s & 1) ? m.wb : m.wa);
-    double *wnxt = ((s + 1) & 1) ? m.wa : m.wb;
+    const double *wcur = level_ptr(m, s);
+    const double *wprv = level_ptr(m, s - 1);
+    double *wnxt = level_ptr(m, s + 1);
     const double cosn = (KIND == K_FIRST) ? 1.0 : m.cos_f[s];
     const double h = (KIND == K_FIRST) ? m.half_dt2 : m.dt2;
     const double acc0 = m.acc_c[0];

@@ -68,6 +68,7 @@ struct Geom {
     int P;            // row pitch (elements)
     int n1, n2;       // extents of storage axes 1 and 2 (incl. boundary)
     int j_lo, j_hi;   // update range on axis 1 ([0,1) when axis 1 is degenerate)
+    int i_lo, i_hi;   // local update planes on axis 0 (global interior, owned)
     int use_c2;
     double clo0, cmid0, clo1, cmid1, clo2, cmid2, c2;
 };
@@ -75,7 +76,8 @@ struct Geom {
 struct Member {
     double *v;              // W^0 / iterate
     const double *f;        // forcing or nullptr (zero forcing)
-    double *wa, *wb, *acc;  // leapfrog pair + filter accumulator
+    double *ring[4];        // time level L >= 1 lives in ring[L & 3] (level 0 = v)
+    double *acc;            // filter accumulator
     double *dst;            // output of the last step (== v for FPI)
     const double *cos_f;    // [n_total]
     const double *acc_c;    // [n_total + 1]
@@ -89,6 +91,12 @@ struct Member {
 
 enum { K_FIRST = 0, K_MID = 1, K_LAST = 2 };
 
+// Buffer holding time level L of a member: W^0 is v, W^L (L >= 1) is ring[L mod 4].  Four
+// slots let a fused two-step pass read levels s, s-1 and write s+1, s+2 with no aliasing.
+__host__ __device__ __forceinline__ double *level_ptr(const Member &m, int L) {
+    return L <= 0 ? m.v : m.ring[L & 3];
+}
+
 __device__ __forceinline__ double whb_add(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double whb_sub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double whb_mul(double a, double b) { return __dmul_rn(a, b); }
@@ -97,9 +105,9 @@ __device__ __forceinline__ double whb_mul(double a, double b) { return __dmul_rn
 template <int KIND, bool ZF, bool A0, bool A1>
 __device__ __forceinline__ void march(const Geom &g, const Member &m, int s, int i0, int i1, int j,
                                       int k, double &rsum) {
-    const double *__restrict__ wcur = (s == 0) ? m.v : ((s & 1) ? m.wa : m.wb);
-    const double *wprv = (s == 1) ? m.v : ((s & 1) ? m.wb : m.wa);
-    double *wnxt = ((s + 1) & 1) ? m.wa : m.wb;  // in place over W^{s-1} for s >= 2
+    const double *__restrict__ wcur = level_ptr(m, s);
+    const double *wprv = level_ptr(m, s - 1);
+    double *wnxt = level_ptr(m, s + 1);  // never aliases levels s, s-1 (4-slot ring)
     const double *__restrict__ f = m.f;
     double *acc = m.acc;
     const double cosn = (KIND == K_FIRST) ? 1.0 : m.cos_f[s];
@@ -282,6 +290,7 @@ __global__ void zero_boundary_kernel(double *x, long long S0, int P, int n1, int
 
 }  // namespace
 #include "step_bulk.cuh"
+#include "step_tb2.cuh"
 namespace {
 
 // y = c^2 * L_h x at owned interior points (DiscreteOperator.apply_values, grid.py:346-368);
@@ -395,7 +404,8 @@ __global__ void lincomb_kernel(CombArgs a, int count, double *y, long long n) {
 // host context
 
 struct MemberHost {
-    double *v = nullptr, *f = nullptr, *wa = nullptr, *wb = nullptr, *acc = nullptr, *out = nullptr;
+    double *v = nullptr, *f = nullptr, *acc = nullptr, *out = nullptr;
+    double *ring[4] = {nullptr, nullptr, nullptr, nullptr};
     double *cos_f = nullptr, *acc_c = nullptr, *partials = nullptr;
     double half_dt2 = 0, dt2 = 0, out_scale = 0;
     int n_total = 0;
@@ -434,10 +444,15 @@ struct whb_ctx {
     int64_t slack_front = 0, slack_back = 0;  // allocation slack around every field (bulk halo reads)
     int BX = 128, BY = 1, gx = 1, JT = 1, chunk_len = 1, nchunks = 1;
     int upd_lo = 1, upd_hi = 2;     // local update planes [lo, hi)
+    // two-step (temporal blocking) plan: whole-grid 2D/3D contexts
+    bool tb2 = false;
+    size_t smem2 = 0;
+    int gx2 = 1, JT2 = 1, chunk2 = 1, nch2 = 1;
     int nparts = 1;
     int64_t launches = 0;
     // graphs keyed by (out_mode, zf)
     std::map<std::tuple<int, int, const void *>, cudaGraphExec_t> graphs;
+    std::map<std::tuple<int, int, const void *>, int64_t> graph_kernels;
     bool use_graphs = true;
     // timing
     bool timing = false;
@@ -451,7 +466,7 @@ struct whb_ctx {
     double *flush_buf = nullptr;
     long long flush_elems = 0;
     // TMA tensor maps keyed by (buffer, box kind)
-    std::map<std::pair<const double *, int>, CUtensorMap> tmaps;
+    std::map<std::tuple<const double *, int, int>, CUtensorMap> tmaps;
 };
 
 namespace {
@@ -466,8 +481,10 @@ double *field_ptr(whb_ctx *c, int field, int member) {
     switch (field) {
         case WHB_V: return m.v;
         case WHB_F: return c->shared_f ? c->shared_f_ptr : m.f;
-        case WHB_WA: return m.wa;
-        case WHB_WB: return m.wb;
+        case WHB_WA: return m.ring[1];
+        case WHB_WB: return m.ring[2];
+        case WHB_WC: return m.ring[3];
+        case WHB_WD: return m.ring[0];
         case WHB_ACC: return m.acc;
         case WHB_OUT: return m.out;
         default: return nullptr;
@@ -496,7 +513,7 @@ int ensure_out(whb_ctx *c, int member) {
 }
 
 double *vec_ptr(whb_ctx *c, int id) {
-    if (id >= 0 && id <= WHB_OUT) return field_ptr(c, id, 0);
+    if (id >= 0 && id <= WHB_WD) return field_ptr(c, id, 0);
     const int e = id - 8;
     if (e >= 0 && e < (int)c->vecs.size()) return c->vecs[e];
     return nullptr;
@@ -510,6 +527,31 @@ inline long long owned_elems(whb_ctx *c) { return (long long)c->nloc * c->S0; }
 // 2 CTAs/SM); 2D 1 x 256 row segments, 8 stages (8.2 KB each, 3 CTAs/SM).
 constexpr int B3_TX = 64, B3_BY = 8, B3_ST = 6;
 constexpr int B2_TX = 256, B2_BY = 1, B2_ST = 8;
+
+// Two-step kernel configurations: 3D 16 x 64 tiles, 5 stages (1 CTA/SM, 512 threads);
+// 2D 256-column row strips, 8 stages (3 CTAs/SM).
+constexpr int T3_TX = 64, T3_BY = 16, T3_ST = 5;
+constexpr int T2_TX = 256, T2_BY = 1, T2_ST = 8;
+
+template <bool A1, int K1, int K2, bool ZF>
+auto tb2_fn() {
+    if constexpr (A1) return tb2::tb2_kernel<T3_TX, T3_BY, T3_ST, true, K1, K2, ZF, true>;
+    else return tb2::tb2_kernel<T2_TX, T2_BY, T2_ST, false, K1, K2, ZF, false>;
+}
+
+template <bool A1>
+cudaError_t tb2_set_attrs(size_t smem) {
+    cudaError_t e = cudaSuccess;
+    auto set = [&](auto fn) {
+        cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (r != cudaSuccess) e = r;
+    };
+    set(tb2_fn<A1, K_FIRST, K_MID, false>()); set(tb2_fn<A1, K_FIRST, K_MID, true>());
+    set(tb2_fn<A1, K_MID, K_MID, false>());   set(tb2_fn<A1, K_MID, K_MID, true>());
+    set(tb2_fn<A1, K_MID, K_LAST, false>());  set(tb2_fn<A1, K_MID, K_LAST, true>());
+    set(tb2_fn<A1, K_FIRST, K_LAST, false>()); set(tb2_fn<A1, K_FIRST, K_LAST, true>());
+    return e;
+}
 
 template <bool A1, int KIND, bool ZF, bool TENSOR>
 auto bulk_fn() {
@@ -618,6 +660,34 @@ int plan_launch(whb_ctx *c) {
     if ((long long)c->JT * c->nchunks > 65535)
         return fail(WHB_E_ARG, "grid too large for launch plan (axis-1 tiles x chunks > 65535)");
     c->nparts = c->gx * c->JT * (c->nchunks + 2);
+    // two-step plan: single-domain 2D/3D contexts (a slab needs 2 ghost planes per exchange)
+    const char *tenv = getenv("WHB_TB2");
+    c->tb2 = c->kern >= 1 && c->plane_begin == 0 && c->plane_end == c->gshape[0] &&
+             !(tenv && std::string(tenv) == "0") && (!c->act1 || c->kern == 2);
+    if (c->tb2) {
+        const int TX = c->act1 ? T3_TX : T2_TX, BYt = c->act1 ? T3_BY : T2_BY;
+        c->smem2 = c->act1 ? tb2::tb2_smem_bytes<T3_TX, T3_BY, T3_ST, true>()
+                           : tb2::tb2_smem_bytes<T2_TX, T2_BY, T2_ST, false>();
+        cudaError_t e = c->act1 ? tb2_set_attrs<true>(c->smem2) : tb2_set_attrs<false>(c->smem2);
+        if (e != cudaSuccess) return fail(WHB_E_CUDA, std::string("cudaFuncSetAttribute(tb2): ") + cudaGetErrorString(e));
+        int nb = 0;
+        if (c->act1) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, tb2_fn<true, K_MID, K_MID, false>(), TX * BYt / 2, c->smem2);
+        else e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, tb2_fn<false, K_MID, K_MID, false>(), TX * BYt / 2, c->smem2);
+        if (e != cudaSuccess || nb < 1) return fail(WHB_E_CUDA, "tb2 kernel does not fit on an SM");
+        c->gx2 = (int)((n2 - 1 + TX - 1) / TX);
+        c->JT2 = c->act1 ? (int)((n1 - 1 + BYt - 1) / BYt) : 1;
+        const long long res2 = (long long)sms * nb;
+        const long long tiles2 = (long long)c->gx2 * c->JT2;
+        const long long waves = c->act1 ? 4 : 1;
+        const long long nch = std::max<long long>(1, waves * res2 / std::max<long long>(1, tiles2));
+        int cl2 = (int)((nplanes + nch - 1) / nch);
+        const char *env2 = getenv("WHB_CHUNK2");
+        if (env2 && atoi(env2) > 0) cl2 = atoi(env2);
+        c->chunk2 = std::max(1, cl2);
+        c->nch2 = (nplanes + c->chunk2 - 1) / c->chunk2;
+        if ((long long)c->JT2 * c->nch2 > 65535) c->tb2 = false;
+        c->nparts = std::max(c->nparts, c->gx2 * c->JT2 * (c->nch2 + 2));
+    }
     // slack: bulk row segments start 2 columns / 1 row early and may run BY+1 rows past the last plane
     c->slack_front = 2 * (int64_t)c->P + 32;
     c->slack_back = (int64_t)(c->BY + 3) * c->P + c->BX + 64;
@@ -648,8 +718,7 @@ int upload_members(whb_ctx *c, int out_mode, int zf, const double *vx = nullptr,
         Member m{};
         m.v = vx ? const_cast<double *>(vx) : h.v;
         m.f = zf ? nullptr : (c->shared_f ? c->shared_f_ptr : h.f);
-        m.wa = h.wa;
-        m.wb = h.wb;
+        for (int q = 0; q < 4; ++q) m.ring[q] = h.ring[q];
         m.acc = h.acc;
         if (out_mode == WHB_OUT_FPI) m.dst = m.v;
         else {
@@ -711,12 +780,12 @@ void launch_bulk_kind(whb_ctx *c, int kind, bool zf, dim3 grid, int off, int s, 
 
 // Tensor map of one field buffer viewed as (planes, n1, pitch) float64 with a (BY+2)x(TX+4)
 // box (w, with halo) or a BY x TX box (prev / f / acc).  Cached per (pointer, box).
-int tensor_map(whb_ctx *c, const double *base, bool wbox, CUtensorMap *out);
+int tensor_map(whb_ctx *c, const double *base, int box_w, int box_h, CUtensorMap *out);
 
 // Launch step s for the first `nact` members of the table (sorted by n_total,
 // descending).  The bulk kernel is specialised on the step kind, so members
 // finishing at this step (LAST) get their own launch.
-int launch_step(whb_ctx *c, int s, int nact, int i_begin, int i_end, int chunk_len, int part_off) {
+int launch_step_members(whb_ctx *c, int s, int moff, int nact, int i_begin, int i_end, int chunk_len, int part_off) {
     if (nact <= 0 || i_begin >= i_end) return 0;
     const int nch = (i_end - i_begin + chunk_len - 1) / chunk_len;
     if (c->kern >= 1) {
@@ -726,18 +795,19 @@ int launch_step(whb_ctx *c, int s, int nact, int i_begin, int i_end, int chunk_l
         if (c->kern == 2) {
             // member 0 of the current table (nbatch == 1): buffers of this step
             const Member &m0 = c->h_members[0];
-            const double *wcur = (s == 0) ? m0.v : ((s & 1) ? m0.wa : m0.wb);
-            const double *wprv = (s == 1) ? m0.v : ((s & 1) ? m0.wb : m0.wa);
-            WHB_TRY(tensor_map(c, wcur, true, &mp.w));
-            WHB_TRY(tensor_map(c, wprv, false, &mp.p));
-            WHB_TRY(tensor_map(c, m0.acc, false, &mp.a));
-            if (m0.f) WHB_TRY(tensor_map(c, m0.f, false, &mp.f));
+            const double *wcur = level_ptr(m0, s);
+            const double *wprv = level_ptr(m0, s - 1);
+            WHB_TRY(tensor_map(c, wcur, B3_TX + 4, B3_BY + 2, &mp.w));
+            WHB_TRY(tensor_map(c, wprv, B3_TX, B3_BY, &mp.p));
+            WHB_TRY(tensor_map(c, m0.acc, B3_TX, B3_BY, &mp.a));
+            if (m0.f) WHB_TRY(tensor_map(c, m0.f, B3_TX, B3_BY, &mp.f));
         }
         int nlast = 0;
-        for (int pos = 0; pos < nact; ++pos) nlast += (c->mem[c->order[pos]].n_total - 1 == s);
+        for (int pos = moff; pos < moff + nact; ++pos) nlast += (c->mem[c->order[pos]].n_total - 1 == s);
         const int nmid = nact - nlast;
-        auto go = [&](int kind, int off, int cnt) {
+        auto go = [&](int kind, int off_rel, int cnt) {
             if (cnt <= 0) return;
+            const int off = moff + off_rel;
             dim3 grid(c->gx, c->JT * nch, cnt);
             if (c->act1) {
                 if (c->kern == 2) launch_bulk_kind<true, true>(c, kind, zf, grid, off, s, i_begin, i_end, chunk_len, part_off, mp);
@@ -754,6 +824,7 @@ int launch_step(whb_ctx *c, int s, int nact, int i_begin, int i_end, int chunk_l
         WHB_CUDA(cudaGetLastError());
         return 0;
     }
+    if (moff != 0) return fail(WHB_E_STATE, "simple kernel launches start at member 0");
     dim3 grid(c->gx, c->JT * nch, nact);
     dim3 block(c->BX, c->BY, 1);
     if (c->act1)
@@ -770,8 +841,8 @@ int launch_step(whb_ctx *c, int s, int nact, int i_begin, int i_end, int chunk_l
     return 0;
 }
 
-int tensor_map(whb_ctx *c, const double *base, bool wbox, CUtensorMap *out) {
-    auto key = std::make_pair(base, wbox ? 1 : 0);
+int tensor_map(whb_ctx *c, const double *base, int box_w, int box_h, CUtensorMap *out) {
+    auto key = std::make_tuple(base, box_w, box_h);
     auto it = c->tmaps.find(key);
     if (it != c->tmaps.end()) {
         *out = it->second;
@@ -781,7 +852,7 @@ int tensor_map(whb_ctx *c, const double *base, bool wbox, CUtensorMap *out) {
     CUtensorMap m;
     cuuint64_t dims[3] = {(cuuint64_t)c->P, (cuuint64_t)c->gshape[1], (cuuint64_t)c->nplanes};
     cuuint64_t strides[2] = {(cuuint64_t)c->P * sizeof(double), (cuuint64_t)c->S0 * sizeof(double)};
-    cuuint32_t box[3] = {(cuuint32_t)(wbox ? B3_TX + 4 : B3_TX), (cuuint32_t)(wbox ? B3_BY + 2 : B3_BY), 1};
+    cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = g_encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(base), dims, strides, box,
                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -789,6 +860,72 @@ int tensor_map(whb_ctx *c, const double *base, bool wbox, CUtensorMap *out) {
     if (r != CUDA_SUCCESS) return fail(WHB_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
     c->tmaps.emplace(key, m);
     *out = m;
+    return 0;
+}
+
+int launch_step(whb_ctx *c, int s, int nact, int i_begin, int i_end, int chunk_len, int part_off) {
+    return launch_step_members(c, s, 0, nact, i_begin, i_end, chunk_len, part_off);
+}
+
+// one-step kernel for table members [moff, moff+cnt) over all update planes
+int launch_step_range(whb_ctx *c, int s, int moff, int cnt) {
+    return launch_step_members(c, s, moff, cnt, c->upd_lo, c->upd_hi, c->chunk_len, 0);
+}
+
+template <bool A1, int K1, int K2, bool ZF>
+void launch_tb2(whb_ctx *c, dim3 grid, int off, int s, int ib, int ie, const StepMaps &mp) {
+    constexpr int threads = A1 ? T3_TX * T3_BY / 2 : T2_TX * T2_BY / 2;
+    tb2_fn<A1, K1, K2, ZF>()<<<grid, threads, c->smem2, c->stream>>>(c->geom, c->d_members, off, s, ib, ie,
+                                                                    c->chunk2, c->JT2, 0, mp.w, mp.p, mp.f, mp.a);
+}
+
+template <bool A1>
+void launch_tb2_kinds(whb_ctx *c, int k1, int k2, bool zf, dim3 grid, int off, int s, int ib, int ie,
+                      const StepMaps &mp) {
+#define WHB_TB2_CASE(K1, K2)                                                         \
+    if (k1 == K1 && k2 == K2) {                                                      \
+        if (zf) launch_tb2<A1, K1, K2, true>(c, grid, off, s, ib, ie, mp);          \
+        else launch_tb2<A1, K1, K2, false>(c, grid, off, s, ib, ie, mp);            \
+        return;                                                                      \
+    }
+    WHB_TB2_CASE(K_FIRST, K_MID)
+    WHB_TB2_CASE(K_MID, K_MID)
+    WHB_TB2_CASE(K_MID, K_LAST)
+    WHB_TB2_CASE(K_FIRST, K_LAST)
+#undef WHB_TB2_CASE
+}
+
+// Fused steps (s, s+1), s even, for the table members [0, nact): those still running
+// after s+1 get (K1, MID), those finishing at s+1 get (K1, LAST).
+int launch_pair(whb_ctx *c, int s) {
+    int n_cont = 0, n_last = 0;
+    for (int pos = 0; pos < c->nbatch; ++pos) {
+        const int N = c->mem[c->order[pos]].n_total;
+        n_cont += (N > s + 2);
+        n_last += (N == s + 2);
+    }
+    if (n_cont + n_last == 0) return 0;
+    const bool zf = c->cur_zf != 0;
+    StepMaps mp;
+    std::memset(&mp, 0, sizeof(mp));
+    if (c->act1) {  // 3D: TMA tensor boxes of member 0 (nbatch == 1)
+        const Member &m0 = c->h_members[0];
+        WHB_TRY(tensor_map(c, level_ptr(m0, s), T3_TX + 4, T3_BY + 4, &mp.w));
+        WHB_TRY(tensor_map(c, level_ptr(m0, s - 1), T3_TX + 4, T3_BY + 2, &mp.p));
+        WHB_TRY(tensor_map(c, m0.acc, T3_TX, T3_BY, &mp.a));
+        if (m0.f) WHB_TRY(tensor_map(c, m0.f, T3_TX + 4, T3_BY + 2, &mp.f));
+    }
+    const int k1 = (s == 0) ? K_FIRST : K_MID;
+    auto go = [&](int k2, int off, int cnt) {
+        if (cnt <= 0) return;
+        dim3 grid(c->gx2, c->JT2 * c->nch2, cnt);
+        if (c->act1) launch_tb2_kinds<true>(c, k1, k2, zf, grid, off, s, c->upd_lo, c->upd_hi, mp);
+        else launch_tb2_kinds<false>(c, k1, k2, zf, grid, off, s, c->upd_lo, c->upd_hi, mp);
+        c->launches++;
+    };
+    go(K_MID, 0, n_cont);
+    go(K_LAST, n_cont, n_last);
+    WHB_CUDA(cudaGetLastError());
     return 0;
 }
 
@@ -807,12 +944,26 @@ int active_members(whb_ctx *c, int s) {
 // Enqueue one full filtered solve (all steps + residual reduction).
 int enqueue_solve(whb_ctx *c, int out_mode) {
     const int ns = max_steps(c);
-    for (int s = 0; s < ns; ++s)
-        WHB_TRY(launch_step(c, s, active_members(c, s), c->upd_lo, c->upd_hi, c->chunk_len, 0));
+    if (c->tb2) {
+        // pairs (0,1), (2,3), ...; a member with odd n_total takes its last step alone
+        for (int s = 0; s < ns; s += 2) {
+            WHB_TRY(launch_pair(c, s));
+            int n_single = 0, off = 0;
+            for (int pos = 0; pos < c->nbatch; ++pos) {
+                const int N = c->mem[c->order[pos]].n_total;
+                if (N > s + 1) ++off;
+                n_single += (N == s + 1);
+            }
+            if (n_single > 0) WHB_TRY(launch_step_range(c, s, off, n_single));
+        }
+    } else {
+        for (int s = 0; s < ns; ++s)
+            WHB_TRY(launch_step(c, s, active_members(c, s), c->upd_lo, c->upd_hi, c->chunk_len, 0));
+    }
     if (out_mode == WHB_OUT_FPI) {
-        reduce_partials_kernel<<<1, 1024, 0, c->stream>>>(c->d_members, c->nbatch,
-                                                          c->gx * c->JT * c->nchunks, c->d_hist,
-                                                          c->d_counter);
+        const int np = c->tb2 ? std::max(c->gx * c->JT * c->nchunks, c->gx2 * c->JT2 * c->nch2)
+                              : c->gx * c->JT * c->nchunks;
+        reduce_partials_kernel<<<1, 1024, 0, c->stream>>>(c->d_members, c->nbatch, np, c->d_hist, c->d_counter);
         c->launches++;
         WHB_CUDA(cudaGetLastError());
     }
@@ -838,13 +989,12 @@ int run_solve(whb_ctx *c, int out_mode, int zf) {
         e = cudaGraphInstantiate(&ge, g, 0);
         cudaGraphDestroy(g);
         if (e != cudaSuccess) return fail(WHB_E_CUDA, std::string("instantiate: ") + cudaGetErrorString(e));
+        c->graph_kernels[key] = c->launches - l0;
         c->launches = l0;
         it = c->graphs.emplace(key, ge).first;
     }
     WHB_CUDA(cudaGraphLaunch(it->second, c->stream));
-    // account the kernels the graph launches
-    const int ns = max_steps(c);
-    c->launches += ns + (out_mode == WHB_OUT_FPI ? 1 : 0);
+    c->launches += c->graph_kernels[key];  // kernels the graph launches
     return 0;
 }
 
@@ -1036,7 +1186,8 @@ int whb_create(whb_ctx **out, int device, int ndim, const int64_t *shape, int64_
     if (rc) return cleanup(rc);
     for (int b = 0; b < nbatch; ++b) {
         MemberHost &m = c->mem[b];
-        if ((rc = alloc_field(c, &m.v)) || (rc = alloc_field(c, &m.wa)) || (rc = alloc_field(c, &m.wb)) ||
+        if ((rc = alloc_field(c, &m.v)) || (rc = alloc_field(c, &m.ring[0])) || (rc = alloc_field(c, &m.ring[1])) ||
+            (rc = alloc_field(c, &m.ring[2])) || (rc = alloc_field(c, &m.ring[3])) ||
             (rc = alloc_field(c, &m.acc)))
             return cleanup(rc);
         if (!c->shared_f && (rc = alloc_field(c, &m.f))) return cleanup(rc);
@@ -1063,7 +1214,8 @@ int whb_destroy(whb_ctx *c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (auto &kv : c->graphs) cudaGraphExecDestroy(kv.second);
     for (auto &m : c->mem) {
-        free_field(c, m.v); free_field(c, m.f); free_field(c, m.wa); free_field(c, m.wb); free_field(c, m.acc);
+        free_field(c, m.v); free_field(c, m.f); free_field(c, m.acc);
+        for (int q = 0; q < 4; ++q) free_field(c, m.ring[q]);
         free_field(c, m.out);
         cudaFree(m.cos_f); cudaFree(m.acc_c); cudaFree(m.partials);
     }
@@ -1090,6 +1242,8 @@ int whb_set_operator(whb_ctx *c, const double *clo, const double *cmid, double c
     g.n2 = (int)c->gshape[2];
     g.j_lo = c->act1 ? 1 : 0;
     g.j_hi = c->act1 ? (int)c->gshape[1] - 1 : 1;
+    g.i_lo = c->upd_lo;
+    g.i_hi = c->upd_hi;
     g.c2 = c2;
     g.use_c2 = (c2 != 1.0);  // x*1.0 == x exactly: skipping keeps bitwise parity
     // map reference axes onto storage axes: 3D (0,1,2); 2D (0,-,2); 1D (-,-,2)
@@ -1140,7 +1294,7 @@ int whb_set_schedule(whb_ctx *c, int member, int n_total, double half_dt2, doubl
 
 int whb_upload(whb_ctx *c, int field, int member, const double *host) {
     if (!c || !host) return fail(WHB_E_ARG, "NULL argument");
-    if (member < 0 || member >= c->nbatch || field < 0 || field > WHB_OUT) return fail(WHB_E_ARG, "bad field/member");
+    if (member < 0 || member >= c->nbatch || field < 0 || field > WHB_WD) return fail(WHB_E_ARG, "bad field/member");
     WHB_TRY(set_dev(c));
     if (field == WHB_OUT) WHB_TRY(ensure_out(c, member));
     double *d = field_ptr(c, field, member);
@@ -1152,7 +1306,7 @@ int whb_upload(whb_ctx *c, int field, int member, const double *host) {
 
 int whb_download(whb_ctx *c, int field, int member, double *host) {
     if (!c || !host) return fail(WHB_E_ARG, "NULL argument");
-    if (member < 0 || member >= c->nbatch || field < 0 || field > WHB_OUT) return fail(WHB_E_ARG, "bad field/member");
+    if (member < 0 || member >= c->nbatch || field < 0 || field > WHB_WD) return fail(WHB_E_ARG, "bad field/member");
     WHB_TRY(set_dev(c));
     if (field == WHB_OUT) WHB_TRY(ensure_out(c, member));
     WHB_TRY(copy_field_d2h(c, field_ptr(c, field, member), host));
@@ -1162,7 +1316,7 @@ int whb_download(whb_ctx *c, int field, int member, double *host) {
 
 int whb_zero(whb_ctx *c, int field, int member) {
     if (!c) return fail(WHB_E_ARG, "NULL argument");
-    if (member < 0 || member >= c->nbatch || field < 0 || field > WHB_OUT) return fail(WHB_E_ARG, "bad field/member");
+    if (member < 0 || member >= c->nbatch || field < 0 || field > WHB_WD) return fail(WHB_E_ARG, "bad field/member");
     WHB_TRY(set_dev(c));
     if (field == WHB_OUT) WHB_TRY(ensure_out(c, member));
     WHB_CUDA(cudaMemsetAsync(field_ptr(c, field, member), 0, (size_t)c->field_elems * sizeof(double), c->stream));
@@ -1358,8 +1512,10 @@ int whb_matvec(whb_ctx *c, int xi, int yi) {
     WHB_TRY(check_ready(c));
     VEC_OR_FAIL(x, xi);
     VEC_OR_FAIL(y, yi);
-    if (x == c->mem[0].wa || x == c->mem[0].wb || x == c->mem[0].acc || y == c->mem[0].wa ||
-        y == c->mem[0].wb || y == c->mem[0].acc)
+    const MemberHost &h0 = c->mem[0];
+    bool alias = (x == h0.acc || y == h0.acc);
+    for (int q = 0; q < 4; ++q) alias = alias || x == h0.ring[q] || y == h0.ring[q];
+    if (alias)
         return fail(WHB_E_ARG, "whb_matvec operands may not alias the leapfrog workspace");
     WHB_TRY(upload_members(c, WHB_OUT_AV, 1, x, y));
     WHB_TRY(run_solve(c, WHB_OUT_AV, 1));
@@ -1444,7 +1600,7 @@ int whb_level_plane_ptr(whb_ctx *c, int level, int64_t plane, uint64_t *dev_ptr,
     if (level < 0) return fail(WHB_E_ARG, "level must be >= 0");
     const MemberHost &m = c->mem[0];
     const double *base = (level == 0) ? (c->cur_mode >= 0 && !c->h_members.empty() ? c->h_members[0].v : m.v)
-                                      : ((level & 1) ? m.wa : m.wb);
+                                      : m.ring[level & 3];
     *dev_ptr = (uint64_t)(uintptr_t)(base + plane * c->S0);
     if (plane_elems) *plane_elems = c->S0;
     return 0;

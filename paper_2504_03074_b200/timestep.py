@@ -162,7 +162,8 @@ def step_explicit(state: WaveState, op, f: np.ndarray, corr) -> WaveState:
     """One leapfrog step of host arrays on the GPU (timestep.py:132-145).
 
     Uses the step-level device API: W^n goes in the level buffer the kernel
-    reads at step s (s = 0 for the start step, s = 2 otherwise) with a
+    reads at step s (s = 0 for the start step, s = 2 otherwise; level L >= 1
+    lives in slot L mod 4: WA, WB, WC, WD) with a
     one-off schedule whose cos factor is cos(wt*t^n)."""
     dt = corr.dt
     dp = device_problem(op.grid, c=op.c, order=op.order)
@@ -176,9 +177,9 @@ def step_explicit(state: WaveState, op, f: np.ndarray, corr) -> WaveState:
         ctx.upload(_native.V, state.w)
         s, out_field = 0, _native.WA
     else:
-        ctx.upload(_native.WB, state.w)       # level 2 (even)
-        ctx.upload(_native.WA, state.w_prev)  # level 1 (odd), overwritten in place by level 3
-        s, out_field = 2, _native.WA
+        ctx.upload(_native.WB, state.w)       # level 2
+        ctx.upload(_native.WA, state.w_prev)  # level 1
+        s, out_field = 2, _native.WC          # level 3
     ctx.solve_begin(_native.OUT_PLAIN, zero_forcing=zero_f)
     ctx.step(s, 0)
     ctx.solve_end()
