@@ -182,6 +182,9 @@ int whb_set_l2_flush(whb_ctx *ctx, int64_t bytes);
 /* Pinned host buffers for H2D/D2H at full PCIe rate. */
 int whb_host_alloc(void **ptr, int64_t bytes);
 int whb_host_free(void *ptr);
+/* Launch plan: kernel 0 = simple LDG, 1 = bulk-copy rows (2D/batched), 2 = TMA tensor
+ * boxes (3D); steps_per_pass = 2 when the two-step (temporal blocking) kernel is used. */
+int whb_plan(whb_ctx *ctx, int *kernel, int *steps_per_pass);
 /* Global and local geometry: shape3[3], pitch, nloc (owned planes). */
 int whb_geometry(whb_ctx *ctx, int64_t *shape3, int64_t *pitch, int64_t *nloc);
 

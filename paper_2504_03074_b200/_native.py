@@ -28,7 +28,7 @@ EXPORTS = (
     "whb_vec_lincomb", "whb_vec_sub_into", "whb_vec_copy", "whb_matvec", "whb_solve_begin",
     "whb_step", "whb_solve_end", "whb_level_plane_ptr", "whb_stream_ptr", "whb_synchronize",
     "whb_copy_plane", "whb_launch_count", "whb_set_timing", "whb_last_timing", "whb_host_alloc",
-    "whb_host_free", "whb_geometry", "whb_set_l2_flush", "whb_apply_operator",
+    "whb_host_free", "whb_geometry", "whb_set_l2_flush", "whb_apply_operator", "whb_plan",
 )
 
 _lib = None
@@ -90,6 +90,7 @@ def load():
         "whb_geometry": ([vp, ip64, ip64, ip64], c_int),
         "whb_set_l2_flush": ([vp, c_i64], c_int),
         "whb_apply_operator": ([vp, c_int, c_int], c_int),
+        "whb_plan": ([vp, ctypes.POINTER(c_int), ctypes.POINTER(c_int)], c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -328,6 +329,13 @@ class Context:
 
     def set_l2_flush(self, nbytes: int):
         check(load().whb_set_l2_flush(self._h, int(nbytes)), "whb_set_l2_flush")
+
+    def plan(self):
+        """(kernel, steps_per_pass): kernel 0 simple, 1 bulk rows, 2 TMA tensor boxes."""
+        k = ctypes.c_int(0)
+        sp = ctypes.c_int(0)
+        check(load().whb_plan(self._h, ctypes.byref(k), ctypes.byref(sp)), "whb_plan")
+        return k.value, sp.value
 
     def geometry(self):
         s = np.zeros(3, dtype=np.int64)

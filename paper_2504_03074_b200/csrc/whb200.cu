@@ -76,7 +76,7 @@ struct Geom {
 struct Member {
     double *v;              // W^0 / iterate
     const double *f;        // forcing or nullptr (zero forcing)
-    double *ring[4];        // time level L >= 1 lives in ring[L & 3] (level 0 = v)
+    double *ring[6];        // time level L >= 1 lives in ring[L mod nring] (level 0 = v)
     double *acc;            // filter accumulator
     double *dst;            // output of the last step (== v for FPI)
     const double *cos_f;    // [n_total]
@@ -86,15 +86,17 @@ struct Member {
     int out_mode;
     double *partials;       // residual partial sums (FPI)
     int idx;                // member index (table order is by n_total, descending)
-    int pad_;
+    int nring;              // 4 (passes of <= 2 steps) or 6 (passes of up to 4 steps)
 };
 
 enum { K_FIRST = 0, K_MID = 1, K_LAST = 2 };
 
-// Buffer holding time level L of a member: W^0 is v, W^L (L >= 1) is ring[L mod 4].  Four
-// slots let a fused two-step pass read levels s, s-1 and write s+1, s+2 with no aliasing.
+// Buffer holding time level L of a member: W^0 is v, W^L (L >= 1) is ring[L mod nring].  A pass
+// of T steps reads levels s, s-1 and writes s+T-1, s+T; the differences 1..T+1 never vanish
+// mod nring when nring >= T+2 (4 slots for T <= 2, 6 slots for T <= 4), so no CTA of a pass
+// ever overwrites a level another CTA of the same pass still reads.
 __host__ __device__ __forceinline__ double *level_ptr(const Member &m, int L) {
-    return L <= 0 ? m.v : m.ring[L & 3];
+    return L <= 0 ? m.v : m.ring[L % m.nring];
 }
 
 __device__ __forceinline__ double whb_add(double a, double b) { return __dadd_rn(a, b); }
@@ -291,6 +293,7 @@ __global__ void zero_boundary_kernel(double *x, long long S0, int P, int n1, int
 }  // namespace
 #include "step_bulk.cuh"
 #include "step_tb2.cuh"
+#include "step_wf2d.cuh"
 namespace {
 
 // y = c^2 * L_h x at owned interior points (DiscreteOperator.apply_values, grid.py:346-368);
@@ -405,7 +408,7 @@ __global__ void lincomb_kernel(CombArgs a, int count, double *y, long long n) {
 
 struct MemberHost {
     double *v = nullptr, *f = nullptr, *acc = nullptr, *out = nullptr;
-    double *ring[4] = {nullptr, nullptr, nullptr, nullptr};
+    double *ring[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     double *cos_f = nullptr, *acc_c = nullptr, *partials = nullptr;
     double half_dt2 = 0, dt2 = 0, out_scale = 0;
     int n_total = 0;
@@ -448,6 +451,11 @@ struct whb_ctx {
     bool tb2 = false;
     size_t smem2 = 0;
     int gx2 = 1, JT2 = 1, chunk2 = 1, nch2 = 1;
+    // 2D wavefront plan (T steps per pass): whole-grid 2D contexts
+    int wfT = 0;                     // 0 = off, else 2 or 4
+    int nring = 4;                   // time-level buffers per member (6 when wfT == 4)
+    int gxw[5] = {1, 1, 1, 1, 1}, chw[5] = {1, 1, 1, 1, 1}, nchw[5] = {1, 1, 1, 1, 1};
+    size_t smemw[5] = {0, 0, 0, 0, 0};
     int nparts = 1;
     int64_t launches = 0;
     // graphs keyed by (out_mode, zf)
@@ -550,6 +558,28 @@ cudaError_t tb2_set_attrs(size_t smem) {
     set(tb2_fn<A1, K_MID, K_MID, false>());   set(tb2_fn<A1, K_MID, K_MID, true>());
     set(tb2_fn<A1, K_MID, K_LAST, false>());  set(tb2_fn<A1, K_MID, K_LAST, true>());
     set(tb2_fn<A1, K_FIRST, K_LAST, false>()); set(tb2_fn<A1, K_FIRST, K_LAST, true>());
+    return e;
+}
+
+// 2D wavefront kernels: 4 consumer warps + 1 producer warp, T + 4 row stages.
+constexpr int WF_NW = 4;
+
+template <int T, int K1, int K2, bool ZF>
+auto wf_fn() {
+    return wf2d::wf2d_kernel<T, WF_NW, T + 4, K1, K2, ZF>;
+}
+
+template <int T>
+cudaError_t wf_set_attrs(size_t smem) {
+    cudaError_t e = cudaSuccess;
+    auto set = [&](auto fn) {
+        cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (r != cudaSuccess) e = r;
+    };
+    set(wf_fn<T, K_FIRST, K_MID, false>()); set(wf_fn<T, K_FIRST, K_MID, true>());
+    set(wf_fn<T, K_MID, K_MID, false>());   set(wf_fn<T, K_MID, K_MID, true>());
+    set(wf_fn<T, K_MID, K_LAST, false>());  set(wf_fn<T, K_MID, K_LAST, true>());
+    set(wf_fn<T, K_FIRST, K_LAST, false>()); set(wf_fn<T, K_FIRST, K_LAST, true>());
     return e;
 }
 
@@ -688,6 +718,33 @@ int plan_launch(whb_ctx *c) {
         if ((long long)c->JT2 * c->nch2 > 65535) c->tb2 = false;
         c->nparts = std::max(c->nparts, c->gx2 * c->JT2 * (c->nch2 + 2));
     }
+    // 2D wavefront plan (default for whole-grid 2D contexts; WHB_WF=0 disables, WHB_WF=2 picks T = 2)
+    const char *wenv = getenv("WHB_WF");
+    c->wfT = (c->tb2 && !c->act1 && !(wenv && std::string(wenv) == "0")) ? ((wenv && std::string(wenv) == "2") ? 2 : 4) : 0;
+    if (c->wfT) {
+        for (int T : {2, 4}) {
+            if (T > c->wfT) continue;
+            const int CW = WF_NW * (64 - 2 * T);
+            c->smemw[T] = T == 2 ? wf2d::wf_smem_bytes<2, WF_NW, 6>() : wf2d::wf_smem_bytes<4, WF_NW, 8>();
+            cudaError_t e = T == 2 ? wf_set_attrs<2>(c->smemw[T]) : wf_set_attrs<4>(c->smemw[T]);
+            if (e != cudaSuccess) return fail(WHB_E_CUDA, std::string("cudaFuncSetAttribute(wf): ") + cudaGetErrorString(e));
+            int nb = 0;
+            e = T == 2 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, wf_fn<2, K_MID, K_MID, false>(), 32 * (WF_NW + 1), c->smemw[T])
+                       : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, wf_fn<4, K_MID, K_MID, false>(), 32 * (WF_NW + 1), c->smemw[T]);
+            if (e != cudaSuccess || nb < 1) return fail(WHB_E_CUDA, "wavefront kernel does not fit on an SM");
+            c->gxw[T] = (int)((n2 - 1 + CW - 1) / CW);
+            const long long res = (long long)sms * nb;
+            const long long nch = std::max<long long>(1, res / std::max<long long>(1, c->gxw[T]));
+            int cl = (int)((nplanes + nch - 1) / nch);
+            const char *ce = getenv("WHB_CHUNKW");
+            if (ce && atoi(ce) > 0) cl = atoi(ce);
+            c->chw[T] = std::max(1, cl);
+            c->nchw[T] = (nplanes + c->chw[T] - 1) / c->chw[T];
+            if (c->nchw[T] > 65535) c->wfT = 0;
+            c->nparts = std::max(c->nparts, c->gxw[T] * (c->nchw[T] + 2));
+        }
+    }
+    c->nring = (c->wfT == 4) ? 6 : 4;
     // slack: bulk row segments start 2 columns / 1 row early and may run BY+1 rows past the last plane
     c->slack_front = 2 * (int64_t)c->P + 32;
     c->slack_back = (int64_t)(c->BY + 3) * c->P + c->BX + 64;
@@ -718,7 +775,8 @@ int upload_members(whb_ctx *c, int out_mode, int zf, const double *vx = nullptr,
         Member m{};
         m.v = vx ? const_cast<double *>(vx) : h.v;
         m.f = zf ? nullptr : (c->shared_f ? c->shared_f_ptr : h.f);
-        for (int q = 0; q < 4; ++q) m.ring[q] = h.ring[q];
+        for (int q = 0; q < 6; ++q) m.ring[q] = h.ring[q];
+        m.nring = c->nring;
         m.acc = h.acc;
         if (out_mode == WHB_OUT_FPI) m.dst = m.v;
         else {
@@ -929,6 +987,75 @@ int launch_pair(whb_ctx *c, int s) {
     return 0;
 }
 
+int max_steps(whb_ctx *c);
+
+template <int T, int K1, int K2, bool ZF>
+void launch_wf(whb_ctx *c, int off, int cnt, int s) {
+    dim3 grid(c->gxw[T], c->nchw[T], cnt);
+    wf_fn<T, K1, K2, ZF>()<<<grid, 32 * (WF_NW + 1), c->smemw[T], c->stream>>>(
+        c->geom, c->d_members, off, s, c->upd_lo, c->upd_hi, c->chw[T], 0);
+}
+
+template <int T>
+void launch_wf_kinds(whb_ctx *c, int k1, int k2, bool zf, int off, int cnt, int s) {
+#define WHB_WF_CASE(K1, K2)                                            \
+    if (k1 == K1 && k2 == K2) {                                        \
+        if (zf) launch_wf<T, K1, K2, true>(c, off, cnt, s);            \
+        else launch_wf<T, K1, K2, false>(c, off, cnt, s);              \
+        return;                                                        \
+    }
+    WHB_WF_CASE(K_FIRST, K_MID)
+    WHB_WF_CASE(K_MID, K_MID)
+    WHB_WF_CASE(K_MID, K_LAST)
+    WHB_WF_CASE(K_FIRST, K_LAST)
+#undef WHB_WF_CASE
+}
+
+// One wavefront pass group: table members [off, off+cnt) advance T steps from step s.
+int launch_wf_group(whb_ctx *c, int T, int off, int cnt, int s, bool last) {
+    if (cnt <= 0) return 0;
+    const int k1 = s == 0 ? K_FIRST : K_MID;
+    const int k2 = last ? K_LAST : K_MID;
+    const bool zf = c->cur_zf != 0;
+    if (T == 4) launch_wf_kinds<4>(c, k1, k2, zf, off, cnt, s);
+    else launch_wf_kinds<2>(c, k1, k2, zf, off, cnt, s);
+    c->launches++;
+    WHB_CUDA(cudaGetLastError());
+    return 0;
+}
+
+// Passes of wfT steps; a member with r < wfT steps left finishes with a 2-step pass and/or a
+// single step.  Members are sorted by n_total (descending), so every group is contiguous.
+int enqueue_wf(whb_ctx *c) {
+    const int T = c->wfT;
+    const int ns = max_steps(c);
+    for (int s = 0; s < ns; s += T) {
+        // remaining steps per table position
+        int cnt_full_mid = 0, cnt_full_last = 0, cnt_r[4] = {0, 0, 0, 0};
+        int pos = 0;
+        for (; pos < c->nbatch; ++pos) {
+            const int rem = c->mem[c->order[pos]].n_total - s;
+            if (rem > T) ++cnt_full_mid;
+            else if (rem == T) ++cnt_full_last;
+            else if (rem > 0) ++cnt_r[rem];
+        }
+        int off = 0;
+        WHB_TRY(launch_wf_group(c, T, off, cnt_full_mid, s, false));
+        off += cnt_full_mid;
+        WHB_TRY(launch_wf_group(c, T, off, cnt_full_last, s, true));
+        off += cnt_full_last;
+        if (T == 4) {
+            // rem 3: 2-step pass (then a single last step); rem 2: 2-step last pass; rem 1: single
+            WHB_TRY(launch_wf_group(c, 2, off, cnt_r[3], s, false));
+            WHB_TRY(launch_wf_group(c, 2, off + cnt_r[3], cnt_r[2], s, true));
+            if (cnt_r[3] > 0) WHB_TRY(launch_step_range(c, s + 2, off, cnt_r[3]));
+            off += cnt_r[3] + cnt_r[2];
+        }
+        if (cnt_r[1] > 0) WHB_TRY(launch_step_range(c, s, off, cnt_r[1]));
+    }
+    return 0;
+}
+
 int max_steps(whb_ctx *c) {
     int mx = 0;
     for (auto &m : c->mem) mx = std::max(mx, m.n_total);
@@ -944,7 +1071,9 @@ int active_members(whb_ctx *c, int s) {
 // Enqueue one full filtered solve (all steps + residual reduction).
 int enqueue_solve(whb_ctx *c, int out_mode) {
     const int ns = max_steps(c);
-    if (c->tb2) {
+    if (c->wfT) {
+        WHB_TRY(enqueue_wf(c));
+    } else if (c->tb2) {
         // pairs (0,1), (2,3), ...; a member with odd n_total takes its last step alone
         for (int s = 0; s < ns; s += 2) {
             WHB_TRY(launch_pair(c, s));
@@ -961,8 +1090,9 @@ int enqueue_solve(whb_ctx *c, int out_mode) {
             WHB_TRY(launch_step(c, s, active_members(c, s), c->upd_lo, c->upd_hi, c->chunk_len, 0));
     }
     if (out_mode == WHB_OUT_FPI) {
-        const int np = c->tb2 ? std::max(c->gx * c->JT * c->nchunks, c->gx2 * c->JT2 * c->nch2)
-                              : c->gx * c->JT * c->nchunks;
+        int np = c->gx * c->JT * c->nchunks;
+        if (c->tb2) np = std::max(np, c->gx2 * c->JT2 * c->nch2);
+        if (c->wfT) np = std::max(np, std::max(c->gxw[2] * c->nchw[2], c->wfT == 4 ? c->gxw[4] * c->nchw[4] : 0));
         reduce_partials_kernel<<<1, 1024, 0, c->stream>>>(c->d_members, c->nbatch, np, c->d_hist, c->d_counter);
         c->launches++;
         WHB_CUDA(cudaGetLastError());
@@ -1022,6 +1152,7 @@ int fpi_impl(whb_ctx *c, int iters, double tol_sq, double *resid_out, int *done)
     if (c->timing) WHB_TRY(ensure_events(c, 2 * iters + 2));
     int k = 0;
     std::vector<double> h(c->nbatch);
+    int64_t step_kernels = 0;
     for (k = 0; k < iters; ++k) {
         if (c->flush_buf) {
             l2_flush_kernel<<<1184, 256, 0, c->stream>>>(c->flush_buf, c->flush_elems, (double)k);
@@ -1029,7 +1160,9 @@ int fpi_impl(whb_ctx *c, int iters, double tol_sq, double *resid_out, int *done)
             WHB_CUDA(cudaGetLastError());
         }
         if (c->timing) WHB_CUDA(cudaEventRecord(c->ev[2 * k], c->stream));
+        const int64_t l0 = c->launches;
         WHB_TRY(run_solve(c, WHB_OUT_FPI, 0));
+        step_kernels += c->launches - l0 - 1;  // minus the residual reduction
         if (c->timing) WHB_CUDA(cudaEventRecord(c->ev[2 * k + 1], c->stream));
         if (tol_sq >= 0.0) {
             WHB_CUDA(cudaMemcpyAsync(h.data(), c->d_hist + (size_t)k * c->nbatch, c->nbatch * sizeof(double),
@@ -1056,7 +1189,7 @@ int fpi_impl(whb_ctx *c, int iters, double tol_sq, double *resid_out, int *done)
         }
         c->t_solve_ms = tot;
         c->t_step_ms = tot;
-        c->t_step_launches = (int64_t)k * max_steps(c);
+        c->t_step_launches = step_kernels;
     }
     if (done) *done = k;
     return 0;
@@ -1186,8 +1319,9 @@ int whb_create(whb_ctx **out, int device, int ndim, const int64_t *shape, int64_
     if (rc) return cleanup(rc);
     for (int b = 0; b < nbatch; ++b) {
         MemberHost &m = c->mem[b];
-        if ((rc = alloc_field(c, &m.v)) || (rc = alloc_field(c, &m.ring[0])) || (rc = alloc_field(c, &m.ring[1])) ||
-            (rc = alloc_field(c, &m.ring[2])) || (rc = alloc_field(c, &m.ring[3])) ||
+        for (int q = 0; q < c->nring && !rc; ++q) rc = alloc_field(c, &m.ring[q]);
+        if (rc) return cleanup(rc);
+        if ((rc = alloc_field(c, &m.v)) ||
             (rc = alloc_field(c, &m.acc)))
             return cleanup(rc);
         if (!c->shared_f && (rc = alloc_field(c, &m.f))) return cleanup(rc);
@@ -1215,7 +1349,7 @@ int whb_destroy(whb_ctx *c) {
     for (auto &kv : c->graphs) cudaGraphExecDestroy(kv.second);
     for (auto &m : c->mem) {
         free_field(c, m.v); free_field(c, m.f); free_field(c, m.acc);
-        for (int q = 0; q < 4; ++q) free_field(c, m.ring[q]);
+        for (int q = 0; q < 6; ++q) free_field(c, m.ring[q]);
         free_field(c, m.out);
         cudaFree(m.cos_f); cudaFree(m.acc_c); cudaFree(m.partials);
     }
@@ -1514,7 +1648,7 @@ int whb_matvec(whb_ctx *c, int xi, int yi) {
     VEC_OR_FAIL(y, yi);
     const MemberHost &h0 = c->mem[0];
     bool alias = (x == h0.acc || y == h0.acc);
-    for (int q = 0; q < 4; ++q) alias = alias || x == h0.ring[q] || y == h0.ring[q];
+    for (int q = 0; q < 6; ++q) alias = alias || x == h0.ring[q] || y == h0.ring[q];
     if (alias)
         return fail(WHB_E_ARG, "whb_matvec operands may not alias the leapfrog workspace");
     WHB_TRY(upload_members(c, WHB_OUT_AV, 1, x, y));
@@ -1600,7 +1734,7 @@ int whb_level_plane_ptr(whb_ctx *c, int level, int64_t plane, uint64_t *dev_ptr,
     if (level < 0) return fail(WHB_E_ARG, "level must be >= 0");
     const MemberHost &m = c->mem[0];
     const double *base = (level == 0) ? (c->cur_mode >= 0 && !c->h_members.empty() ? c->h_members[0].v : m.v)
-                                      : m.ring[level & 3];
+                                      : m.ring[level % c->nring];
     *dev_ptr = (uint64_t)(uintptr_t)(base + plane * c->S0);
     if (plane_elems) *plane_elems = c->S0;
     return 0;
@@ -1684,6 +1818,13 @@ int whb_host_alloc(void **ptr, int64_t bytes) {
 
 int whb_host_free(void *ptr) {
     if (ptr) WHB_CUDA(cudaFreeHost(ptr));
+    return 0;
+}
+
+int whb_plan(whb_ctx *c, int *kernel, int *steps_per_pass) {
+    if (!c) return fail(WHB_E_ARG, "NULL argument");
+    if (kernel) *kernel = c->kern;
+    if (steps_per_pass) *steps_per_pass = c->wfT ? c->wfT : (c->tb2 ? 2 : 1);
     return 0;
 }
 
