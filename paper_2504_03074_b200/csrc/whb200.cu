@@ -564,9 +564,13 @@ cudaError_t tb2_set_attrs(size_t smem) {
 // 2D wavefront kernels: 4 consumer warps + 1 producer warp, T + 4 row stages.
 constexpr int WF_NW = 4;
 
+// T = 4 runs the skewed wavefront (level t at row r - 2t + 1: independent level updates per
+// row, 2T + 4 stages); T = 2 the plain one.
+constexpr int WF_SKEW4 = 1;
 template <int T, int K1, int K2, bool ZF>
 auto wf_fn() {
-    return wf2d::wf2d_kernel<T, WF_NW, T + 4, K1, K2, ZF>;
+    if constexpr (T == 4) return wf2d::wf2d_kernel<4, WF_NW, 4 + wf2d::wf_lag<WF_SKEW4>(4) - 3 + 4, K1, K2, ZF, WF_SKEW4>;
+    else return wf2d::wf2d_kernel<T, WF_NW, T + 4, K1, K2, ZF, 1>;
 }
 
 template <int T>
@@ -725,7 +729,8 @@ int plan_launch(whb_ctx *c) {
         for (int T : {2, 4}) {
             if (T > c->wfT) continue;
             const int CW = WF_NW * (64 - 2 * T);
-            c->smemw[T] = T == 2 ? wf2d::wf_smem_bytes<2, WF_NW, 6>() : wf2d::wf_smem_bytes<4, WF_NW, 8>();
+            c->smemw[T] = T == 2 ? wf2d::wf_smem_bytes<2, WF_NW, 6>()
+                                 : wf2d::wf_smem_bytes<4, WF_NW, 4 + wf2d::wf_lag<WF_SKEW4>(4) - 3 + 4>();
             cudaError_t e = T == 2 ? wf_set_attrs<2>(c->smemw[T]) : wf_set_attrs<4>(c->smemw[T]);
             if (e != cudaSuccess) return fail(WHB_E_CUDA, std::string("cudaFuncSetAttribute(wf): ") + cudaGetErrorString(e));
             int nb = 0;
