@@ -294,6 +294,7 @@ __global__ void zero_boundary_kernel(double *x, long long S0, int P, int n1, int
 #include "step_bulk.cuh"
 #include "step_tb2.cuh"
 #include "step_wf2d.cuh"
+#include "step_tb2r.cuh"
 namespace {
 
 // y = c^2 * L_h x at owned interior points (DiscreteOperator.apply_values, grid.py:346-368);
@@ -451,6 +452,7 @@ struct whb_ctx {
     bool tb2 = false;
     size_t smem2 = 0;
     int gx2 = 1, JT2 = 1, chunk2 = 1, nch2 = 1;
+    bool tb2r = false;               // 3D: balanced 62-column variant of the two-step kernel
     // 2D wavefront plan (T steps per pass): whole-grid 2D contexts
     int wfT = 0;                     // 0 = off, else 2 or 4
     int nring = 4;                   // time-level buffers per member (6 when wfT == 4)
@@ -547,6 +549,26 @@ auto tb2_fn() {
     else return tb2::tb2_kernel<T2_TX, T2_BY, T2_ST, false, K1, K2, ZF, false>;
 }
 
+constexpr int R3_BY = 16, R3_ST = 5;
+
+template <int K1, int K2, bool ZF>
+auto tb2r_fn() {
+    return tb2r::tb2r_kernel<R3_BY, R3_ST, K1, K2, ZF>;
+}
+
+cudaError_t tb2r_set_attrs(size_t smem) {
+    cudaError_t e = cudaSuccess;
+    auto set = [&](auto fn) {
+        cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (r != cudaSuccess) e = r;
+    };
+    set(tb2r_fn<K_FIRST, K_MID, false>()); set(tb2r_fn<K_FIRST, K_MID, true>());
+    set(tb2r_fn<K_MID, K_MID, false>());   set(tb2r_fn<K_MID, K_MID, true>());
+    set(tb2r_fn<K_MID, K_LAST, false>());  set(tb2r_fn<K_MID, K_LAST, true>());
+    set(tb2r_fn<K_FIRST, K_LAST, false>()); set(tb2r_fn<K_FIRST, K_LAST, true>());
+    return e;
+}
+
 template <bool A1>
 cudaError_t tb2_set_attrs(size_t smem) {
     cudaError_t e = cudaSuccess;
@@ -567,9 +589,10 @@ constexpr int WF_NW = 4;
 // T = 4 runs the skewed wavefront (level t at row r - 2t + 1: independent level updates per
 // row, 2T + 4 stages); T = 2 the plain one.
 constexpr int WF_SKEW4 = 1;
+constexpr int WF_ST4 = wf2d::wf_lag<WF_SKEW4>(4) + 5;  // 9 stages, 3 CTAs/SM (measured: 7 stages at 4 CTAs/SM is 1.4 % slower)
 template <int T, int K1, int K2, bool ZF>
 auto wf_fn() {
-    if constexpr (T == 4) return wf2d::wf2d_kernel<4, WF_NW, 4 + wf2d::wf_lag<WF_SKEW4>(4) - 3 + 4, K1, K2, ZF, WF_SKEW4>;
+    if constexpr (T == 4) return wf2d::wf2d_kernel<4, WF_NW, WF_ST4, K1, K2, ZF, WF_SKEW4>;
     else return wf2d::wf2d_kernel<T, WF_NW, T + 4, K1, K2, ZF, 1>;
 }
 
@@ -698,7 +721,29 @@ int plan_launch(whb_ctx *c) {
     const char *tenv = getenv("WHB_TB2");
     c->tb2 = c->kern >= 1 && c->plane_begin == 0 && c->plane_end == c->gshape[0] &&
              !(tenv && std::string(tenv) == "0") && (!c->act1 || c->kern == 2);
-    if (c->tb2) {
+    const char *renv = getenv("WHB_TB2R");
+    // measured on 257^3 / 1025^3: 126.5 / 131.0 Gpts/s vs 143.7 / 149.3 for tb2 -> opt-in (WHB_TB2R=1)
+    c->tb2r = c->tb2 && c->act1 && (renv && std::string(renv) == "1");
+    if (c->tb2r) {
+        c->smem2 = tb2r::smem_bytes<R3_BY, R3_ST>();
+        cudaError_t e = tb2r_set_attrs(c->smem2);
+        if (e != cudaSuccess) return fail(WHB_E_CUDA, std::string("cudaFuncSetAttribute(tb2r): ") + cudaGetErrorString(e));
+        int nb = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, tb2r_fn<K_MID, K_MID, false>(), 32 * (R3_BY + 2), c->smem2);
+        if (e != cudaSuccess || nb < 1) return fail(WHB_E_CUDA, "tb2r kernel does not fit on an SM");
+        c->gx2 = (int)((n2 - 2 + 61) / 62);
+        c->JT2 = (int)((n1 - 1 + R3_BY - 1) / R3_BY);
+        const long long res2 = (long long)sms * nb;
+        const long long tiles2 = (long long)c->gx2 * c->JT2;
+        const long long nch = std::max<long long>(1, 4 * res2 / std::max<long long>(1, tiles2));
+        int cl2 = (int)((nplanes + nch - 1) / nch);
+        const char *env2 = getenv("WHB_CHUNK2");
+        if (env2 && atoi(env2) > 0) cl2 = atoi(env2);
+        c->chunk2 = std::max(1, cl2);
+        c->nch2 = (nplanes + c->chunk2 - 1) / c->chunk2;
+        if ((long long)c->JT2 * c->nch2 > 65535) c->tb2 = c->tb2r = false;
+        c->nparts = std::max(c->nparts, c->gx2 * c->JT2 * (c->nch2 + 2));
+    } else if (c->tb2) {
         const int TX = c->act1 ? T3_TX : T2_TX, BYt = c->act1 ? T3_BY : T2_BY;
         c->smem2 = c->act1 ? tb2::tb2_smem_bytes<T3_TX, T3_BY, T3_ST, true>()
                            : tb2::tb2_smem_bytes<T2_TX, T2_BY, T2_ST, false>();
@@ -730,7 +775,7 @@ int plan_launch(whb_ctx *c) {
             if (T > c->wfT) continue;
             const int CW = WF_NW * (64 - 2 * T);
             c->smemw[T] = T == 2 ? wf2d::wf_smem_bytes<2, WF_NW, 6>()
-                                 : wf2d::wf_smem_bytes<4, WF_NW, 4 + wf2d::wf_lag<WF_SKEW4>(4) - 3 + 4>();
+                                 : wf2d::wf_smem_bytes<4, WF_NW, WF_ST4>();
             cudaError_t e = T == 2 ? wf_set_attrs<2>(c->smemw[T]) : wf_set_attrs<4>(c->smemw[T]);
             if (e != cudaSuccess) return fail(WHB_E_CUDA, std::string("cudaFuncSetAttribute(wf): ") + cudaGetErrorString(e));
             int nb = 0;
@@ -958,6 +1003,27 @@ void launch_tb2_kinds(whb_ctx *c, int k1, int k2, bool zf, dim3 grid, int off, i
 #undef WHB_TB2_CASE
 }
 
+template <int K1, int K2, bool ZF>
+void launch_tb2r(whb_ctx *c, dim3 grid, int off, int s, int ib, int ie, const StepMaps &mp) {
+    tb2r_fn<K1, K2, ZF>()<<<grid, 32 * (R3_BY + 2), c->smem2, c->stream>>>(
+        c->geom, c->d_members, off, s, ib, ie, c->chunk2, c->JT2, 0, mp.w, mp.p, mp.f, mp.a);
+}
+
+void launch_tb2r_kinds(whb_ctx *c, int k1, int k2, bool zf, dim3 grid, int off, int s, int ib, int ie,
+                       const StepMaps &mp) {
+#define WHB_TB2R_CASE(K1, K2)                                                      \
+    if (k1 == K1 && k2 == K2) {                                                    \
+        if (zf) launch_tb2r<K1, K2, true>(c, grid, off, s, ib, ie, mp);           \
+        else launch_tb2r<K1, K2, false>(c, grid, off, s, ib, ie, mp);             \
+        return;                                                                    \
+    }
+    WHB_TB2R_CASE(K_FIRST, K_MID)
+    WHB_TB2R_CASE(K_MID, K_MID)
+    WHB_TB2R_CASE(K_MID, K_LAST)
+    WHB_TB2R_CASE(K_FIRST, K_LAST)
+#undef WHB_TB2R_CASE
+}
+
 // Fused steps (s, s+1), s even, for the table members [0, nact): those still running
 // after s+1 get (K1, MID), those finishing at s+1 get (K1, LAST).
 int launch_pair(whb_ctx *c, int s) {
@@ -978,10 +1044,22 @@ int launch_pair(whb_ctx *c, int s) {
         WHB_TRY(tensor_map(c, m0.acc, T3_TX, T3_BY, &mp.a));
         if (m0.f) WHB_TRY(tensor_map(c, m0.f, T3_TX + 4, T3_BY + 2, &mp.f));
     }
+    if (c->tb2r) {  // balanced 3D variant: boxes W (68, BY+4), P/F (64, BY+2), acc (64, BY)
+        const Member &m0 = c->h_members[0];
+        WHB_TRY(tensor_map(c, level_ptr(m0, s), 68, R3_BY + 4, &mp.w));
+        WHB_TRY(tensor_map(c, level_ptr(m0, s - 1), 64, R3_BY + 2, &mp.p));
+        WHB_TRY(tensor_map(c, m0.acc, 64, R3_BY, &mp.a));
+        if (m0.f) WHB_TRY(tensor_map(c, m0.f, 64, R3_BY + 2, &mp.f));
+    }
     const int k1 = (s == 0) ? K_FIRST : K_MID;
     auto go = [&](int k2, int off, int cnt) {
         if (cnt <= 0) return;
         dim3 grid(c->gx2, c->JT2 * c->nch2, cnt);
+        if (c->tb2r) {
+            launch_tb2r_kinds(c, k1, k2, zf, grid, off, s, c->upd_lo, c->upd_hi, mp);
+            c->launches++;
+            return;
+        }
         if (c->act1) launch_tb2_kinds<true>(c, k1, k2, zf, grid, off, s, c->upd_lo, c->upd_hi, mp);
         else launch_tb2_kinds<false>(c, k1, k2, zf, grid, off, s, c->upd_lo, c->upd_hi, mp);
         c->launches++;
