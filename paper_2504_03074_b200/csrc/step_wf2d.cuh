@@ -60,7 +60,7 @@ constexpr size_t wf_smem_bytes() {
 
 // K1: kind of the first step of the pass (FIRST when s == 0); K2: kind of the last (LAST ends the solve).
 template <int T, int NW, int ST, int K1, int K2, bool ZF, int SKEW = 1>
-__global__ void __launch_bounds__(Lay<T, NW>::THREADS)
+__global__ void __launch_bounds__(Lay<T, NW>::THREADS, 3)
     wf2d_kernel(Geom g, const Member *__restrict__ members, int member_off, int s, int i_begin, int i_end,
                 int chunk_len, int part_off) {
     using L = Lay<T, NW>;
@@ -156,6 +156,7 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS)
     #pragma unroll
             for (int t = 0; t < T; ++t) A[t] = make_double2(0.0, 0.0);
     
+#pragma unroll 3
             for (int idx = 0; idx < nrows; ++idx) {
                 const int r = r0 + idx;
                 const int slot = idx % ST;
