@@ -89,6 +89,13 @@ int whb_destroy(whb_ctx *ctx);
  * Replaces DiscreteOperator (grid.py:309-368), order p = 2, all-Dirichlet. */
 int whb_set_operator(whb_ctx *ctx, const double *clo, const double *cmid, double c2);
 
+/* General operator: order p in {2, 4} and per-axis boundary
+ * conditions — periodic[a] != 0: wrap-around, else homogeneous Dirichlet closed by
+ * odd reflection (grid.py:371-392).  taps[a*(p+1) + q] = stencil_coefficients(p, dx_a)[q]
+ * (grid.py:296-306), c2 = c**2.  Whole-grid contexts only.  Runs a one-step-per-pass
+ * kernel (the temporal-blocked kernels implement p = 2, all-Dirichlet). */
+int whb_set_operator_general(whb_ctx *ctx, int order, const int *periodic, const double *taps, double c2);
+
 /* Per-member time schedule of one filtered solve (n_total = N_p*N_t steps):
  *   cos_f[n_total]   cos(wt*(n*dt)) forcing factor of step n (entry 0 unused)
  *   acc_c[n_total+1] (cos(wt*(n*dt)) - alpha/2)*sigma_n filter weights

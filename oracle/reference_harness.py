@@ -64,11 +64,11 @@ def grid(dim, bounds, cells, bcs="dirichlet"):
     if dim in (1, 2):
         return G.build_grid(dim, bounds, cells, bcs)
     g = object.__new__(G.CartesianGrid)
-    bc = G._as_bc(bcs)
+    per_axis = [bcs] * dim if isinstance(bcs, str) else list(bcs)
     object.__setattr__(g, "dim", dim)
     object.__setattr__(g, "bounds", tuple((float(lo), float(hi)) for lo, hi in bounds))
     object.__setattr__(g, "cells", tuple(int(n) for n in cells))
-    object.__setattr__(g, "bcs", (bc,) * dim)
+    object.__setattr__(g, "bcs", tuple(G._as_bc(b) for b in per_axis))
     return g
 
 

@@ -152,18 +152,72 @@ def laplacian(w: np.ndarray, spacing, c: float = 1.0) -> np.ndarray:
             sl[axis] = slice(g + off, g + off + w.shape[axis])
             out += ck * buf[tuple(sl)]
     out *= c**2
-    zero_boundary(out)
     return zero_boundary(out)
 
 
-def wave_solve_filtered(v: np.ndarray, f: np.ndarray, spacing, sc: dict, c: float = 1.0) -> np.ndarray:
+TAPS = {2: np.array([1.0, -2.0, 1.0]),
+        4: np.array([-1.0 / 12.0, 4.0 / 3.0, -5.0 / 2.0, 4.0 / 3.0, -1.0 / 12.0])}
+
+
+def zero_dirichlet(a: np.ndarray, bcs) -> np.ndarray:
+    """grid.py:395-402 for per-axis boundary conditions."""
+    for axis, bc in enumerate(bcs):
+        if bc == "dirichlet":
+            idx = [slice(None)] * a.ndim
+            for e in (0, -1):
+                idx[axis] = e
+                a[tuple(idx)] = 0.0
+    return a
+
+
+def laplacian_general(w: np.ndarray, spacing, bcs, order: int = 2, c: float = 1.0) -> np.ndarray:
+    """grid.py:346-392 for order p in {2, 4} and per-axis Dirichlet / periodic boundaries:
+    ghosts of width p/2 by odd reflection (Dirichlet) or wrap (periodic), filled axis by
+    axis over the core of the other axes; out = 0; per axis, per tap: out += c_k*buf[shift];
+    out *= c^2; Dirichlet faces zeroed."""
+    g = order // 2
+    shape = w.shape
+    buf = np.empty(tuple(n + 2 * g for n in shape))
+    core = tuple(slice(g, g + n) for n in shape)
+    buf[core] = w
+    for axis, bc in enumerate(bcs):
+        n = shape[axis]
+
+        def ax(idx):
+            sl = [slice(g, g + m) for m in shape]
+            sl[axis] = idx
+            return tuple(sl)
+
+        for k in range(1, g + 1):
+            if bc == "dirichlet":
+                buf[ax(g - k)] = -buf[ax(g + k)]
+                buf[ax(g + n - 1 + k)] = -buf[ax(g + n - 1 - k)]
+            else:
+                buf[ax(g - k)] = buf[ax(g + n - k)]
+                buf[ax(g + n - 1 + k)] = buf[ax(g + k - 1)]
+    out = np.zeros(shape)
+    for axis, dx in enumerate(spacing):
+        taps = TAPS[order] / dx**2
+        for k, ck in enumerate(taps):
+            off = k - g
+            sl = list(core)
+            sl[axis] = slice(g + off, g + off + shape[axis])
+            out += ck * buf[tuple(sl)]
+    out *= c**2
+    return zero_dirichlet(out, bcs)
+
+
+def wave_solve_filtered(v: np.ndarray, f: np.ndarray, spacing, sc: dict, c: float = 1.0, bcs=None,
+                        order: int = 2) -> np.ndarray:
     """timestep.py:250-301, explicit branch, with step_explicit (timestep.py:132-145)."""
     n_total = sc["n_total"]
     w = np.array(v, dtype=float)
     w_prev = np.zeros_like(w)
     acc = sc["acc_c"][0] * w
+    general = bcs is not None or order != 2
+    bcs = bcs or ["dirichlet"] * w.ndim
     for n in range(n_total):
-        lap = laplacian(w, spacing, c)
+        lap = laplacian_general(w, spacing, bcs, order, c) if general else laplacian(w, spacing, c)
         if n == 0:
             w_next = w + sc["half_dt2"] * (lap - f)
         else:
@@ -171,7 +225,7 @@ def wave_solve_filtered(v: np.ndarray, f: np.ndarray, spacing, sc: dict, c: floa
             w_next = 2.0 * w - w_prev + sc["dt2"] * (lap - force)
         w_prev, w = w, w_next
         acc += sc["acc_c"][n + 1] * w
-    return zero_boundary(sc["out_scale"] * acc)
+    return zero_dirichlet(sc["out_scale"] * acc, bcs)
 
 
 def fpi(f: np.ndarray, spacing, sc: dict, iters: int, c: float = 1.0, tol: float = -1.0):
@@ -188,9 +242,9 @@ def fpi(f: np.ndarray, spacing, sc: dict, iters: int, c: float = 1.0, tol: float
     return v, res
 
 
-def apply_A(x: np.ndarray, spacing, sc: dict, c: float = 1.0) -> np.ndarray:
+def apply_A(x: np.ndarray, spacing, sc: dict, c: float = 1.0, bcs=None, order: int = 2) -> np.ndarray:
     """driver.py:256-262: A x = x - W(x, 0)."""
-    return x - wave_solve_filtered(x, np.zeros_like(x), spacing, sc, c)
+    return x - wave_solve_filtered(x, np.zeros_like(x), spacing, sc, c, bcs, order)
 
 
 # ---------------------------------------------------------------------------------

@@ -28,7 +28,7 @@ EXPORTS = (
     "whb_vec_lincomb", "whb_vec_sub_into", "whb_vec_copy", "whb_matvec", "whb_solve_begin",
     "whb_step", "whb_solve_end", "whb_level_plane_ptr", "whb_stream_ptr", "whb_synchronize",
     "whb_copy_plane", "whb_launch_count", "whb_set_timing", "whb_last_timing", "whb_host_alloc",
-    "whb_host_free", "whb_geometry", "whb_set_l2_flush", "whb_apply_operator", "whb_plan",
+    "whb_host_free", "whb_geometry", "whb_set_l2_flush", "whb_apply_operator", "whb_plan", "whb_set_operator_general",
 )
 
 _lib = None
@@ -91,6 +91,7 @@ def load():
         "whb_set_l2_flush": ([vp, c_i64], c_int),
         "whb_apply_operator": ([vp, c_int, c_int], c_int),
         "whb_plan": ([vp, ctypes.POINTER(c_int), ctypes.POINTER(c_int)], c_int),
+        "whb_set_operator_general": ([vp, c_int, ctypes.POINTER(c_int), dp, c_double], c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -189,6 +190,12 @@ class Context:
         clo = np.ascontiguousarray(clo, dtype=np.float64)
         cmid = np.ascontiguousarray(cmid, dtype=np.float64)
         check(load().whb_set_operator(self._h, _dp(clo), _dp(cmid), float(c2)), "whb_set_operator")
+
+    def set_operator_general(self, order, periodic, taps, c2):
+        per = np.ascontiguousarray(periodic, dtype=np.int32)
+        tp = np.ascontiguousarray(taps, dtype=np.float64)
+        check(load().whb_set_operator_general(self._h, int(order), per.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                                              _dp(tp), float(c2)), "whb_set_operator_general")
 
     def set_schedule(self, member, sched):
         cos_f = np.ascontiguousarray(sched["cos_f"], dtype=np.float64)

@@ -273,7 +273,7 @@ __global__ void reduce_partials_kernel(const Member *__restrict__ members, int n
 
 // Zero the Dirichlet boundary (and keep padding zero) of owned planes [lp0, lp1).
 __global__ void zero_boundary_kernel(double *x, long long S0, int P, int n1, int n2, int act1,
-                                     int lp0, int lp1, int zero_plane_lo, int zero_plane_hi) {
+                                     int lp0, int lp1, int zero_plane_lo, int zero_plane_hi, int per1, int per2) {
     const long long total = (long long)(lp1 - lp0) * S0;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
          t += (long long)gridDim.x * blockDim.x) {
@@ -282,8 +282,8 @@ __global__ void zero_boundary_kernel(double *x, long long S0, int P, int n1, int
         const int j = (int)(r / P);
         const int k = (int)(r - (long long)j * P);
         const int plane = lp0 + (int)pl;
-        bool z = (k == 0) || (k >= n2 - 1);
-        if (act1) z = z || (j == 0) || (j == n1 - 1);
+        bool z = per2 ? (k >= n2) : ((k == 0) || (k >= n2 - 1));  // periodic axes have no boundary points
+        if (act1 && !per1) z = z || (j == 0) || (j == n1 - 1);
         if (zero_plane_lo && plane == lp0) z = true;
         if (zero_plane_hi && plane == lp1 - 1) z = true;
         if (z) x[(long long)plane * S0 + r] = 0.0;
@@ -329,6 +329,144 @@ __global__ void apply_operator_kernel(Geom g, const double *__restrict__ x, doub
         y[p] = whb_mul(lap, g.c2);  // out *= c**2 (grid.py:366)
     }
 }
+
+// ---- general operator: order p in {2, 4}, per-axis Dirichlet (odd reflection) or periodic
+// (grid.py:296-306, 371-392).  One thread per point, LDG; every value
+// is formed in the reference order (axis by axis, tap by tap from 0; reflected ghosts are
+// the negated core value, multiplied like any other tap).
+struct GeomG {
+    long long S0;
+    int P;
+    int n[3];          // global extent of each storage axis
+    int act[3];        // axis carries a stencil
+    int per[3];        // periodic axis
+    int order;         // 2 or 4
+    int use_c2;
+    int plane_begin;   // global index of local plane 1
+    double taps[3][5];
+    double c2;
+};
+
+// value of w at (global plane gi + o0, j + o1, k + o2) with boundary images; only one offset is nonzero
+__device__ __forceinline__ double gfetch(const GeomG &g, const double *w, long long p, int gi, int j, int k, int axis,
+                                         int o) {
+    int idx = (axis == 0 ? gi : (axis == 1 ? j : k)) + o;
+    const int n = g.n[axis];
+    double sign = 1.0;
+    if (g.per[axis]) {
+        idx = (idx % n + n) % n;
+    } else if (idx < 0) {
+        idx = -idx;
+        sign = -1.0;
+    } else if (idx > n - 1) {
+        idx = 2 * (n - 1) - idx;
+        sign = -1.0;
+    }
+    long long q = p;
+    if (axis == 0) q += (long long)(idx - gi) * g.S0;
+    else if (axis == 1) q += (long long)(idx - j) * g.P;
+    else q += (idx - k);
+    const double v = w[q];
+    return sign < 0.0 ? -v : v;
+}
+
+__device__ __forceinline__ double general_lap(const GeomG &g, const double *w, long long p, int gi, int j, int k) {
+    const int h = g.order / 2;
+    double lap = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        if (!g.act[a]) continue;
+        for (int q = 0; q <= g.order; ++q) lap = whb_add(lap, whb_mul(g.taps[a][q], gfetch(g, w, p, gi, j, k, a, q - h)));
+    }
+    return g.use_c2 ? whb_mul(lap, g.c2) : lap;
+}
+
+__device__ __forceinline__ bool general_updates(const GeomG &g, int gi, int j, int k) {
+    if (g.act[0] && !g.per[0] && (gi < 1 || gi > g.n[0] - 2)) return false;
+    if (g.act[1] && !g.per[1] && (j < 1 || j > g.n[1] - 2)) return false;
+    if (!g.per[2] && (k < 1 || k > g.n[2] - 2)) return false;
+    return true;
+}
+
+// one leapfrog step for every active member (blockIdx.y), grid-stride over owned points
+__global__ void step_general_kernel(GeomG g, const Member *__restrict__ members, int s, int nloc, int part_off) {
+    const Member m = members[blockIdx.y];
+    const int kind = (s == 0) ? K_FIRST : ((s == m.n_total - 1) ? K_LAST : K_MID);
+    const double *wcur = level_ptr(m, s);
+    const double *wprv = level_ptr(m, s - 1);
+    double *wnxt = level_ptr(m, s + 1);
+    const double cosn = (kind == K_FIRST) ? 1.0 : m.cos_f[s];
+    const double h = (kind == K_FIRST) ? m.half_dt2 : m.dt2;
+    const double acc0 = m.acc_c[0], accn = m.acc_c[s + 1];
+    const int n1 = g.act[1] ? g.n[1] : 1, n2 = g.n[2];
+    const long long total = (long long)nloc * n1 * n2;
+    double rsum = 0.0;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long pl = t / ((long long)n1 * n2);
+        const long long r = t - pl * n1 * n2;
+        const int j = (int)(r / n2);
+        const int k = (int)(r - (long long)j * n2);
+        const int gi = g.plane_begin + (int)pl;
+        if (!general_updates(g, gi, j, k)) continue;
+        const long long p = (pl + 1) * g.S0 + (long long)j * g.P + k;
+        const double wc = wcur[p];
+        const double lap = general_lap(g, wcur, p, gi, j, k);
+        double wn;
+        if (kind == K_FIRST) {
+            const double d = m.f ? whb_sub(lap, m.f[p]) : lap;
+            wn = whb_add(wc, whb_mul(h, d));
+            wnxt[p] = wn;
+            m.acc[p] = whb_add(whb_mul(acc0, wc), whb_mul(accn, wn));
+        } else {
+            const double d = m.f ? whb_sub(lap, whb_mul(m.f[p], cosn)) : lap;
+            wn = whb_add(whb_sub(whb_mul(2.0, wc), wprv[p]), whb_mul(h, d));
+            if (kind == K_MID) {
+                wnxt[p] = wn;
+                m.acc[p] = whb_add(m.acc[p], whb_mul(accn, wn));
+            } else {
+                const double out = whb_mul(m.out_scale, whb_add(m.acc[p], whb_mul(accn, wn)));
+                if (m.out_mode == WHB_OUT_FPI) {
+                    const double dd = out - m.v[p];
+                    rsum += dd * dd;
+                    m.v[p] = out;
+                } else if (m.out_mode == WHB_OUT_AV) {
+                    m.dst[p] = whb_sub(m.v[p], out);
+                } else {
+                    m.dst[p] = out;
+                }
+            }
+        }
+    }
+    if (kind == K_LAST && m.out_mode == WHB_OUT_FPI) {
+        const double b = block_sum(rsum);
+        if (threadIdx.x == 0) m.partials[part_off + blockIdx.x] = b;
+    }
+}
+
+__global__ void apply_general_kernel(GeomG g, const double *__restrict__ x, double *__restrict__ y, int nloc) {
+    const int n1 = g.act[1] ? g.n[1] : 1, n2 = g.n[2];
+    const long long total = (long long)nloc * n1 * n2;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long pl = t / ((long long)n1 * n2);
+        const long long r = t - pl * n1 * n2;
+        const int j = (int)(r / n2);
+        const int k = (int)(r - (long long)j * n2);
+        const int gi = g.plane_begin + (int)pl;
+        if (!general_updates(g, gi, j, k)) continue;
+        const long long p = (pl + 1) * g.S0 + (long long)j * g.P + k;
+        const int h = g.order / 2;
+        double lap = 0.0;
+        for (int a = 0; a < 3; ++a) {
+            if (!g.act[a]) continue;
+            for (int q = 0; q <= g.order; ++q) lap = whb_add(lap, whb_mul(g.taps[a][q], gfetch(g, x, p, gi, j, k, a, q - h)));
+        }
+        y[p] = whb_mul(lap, g.c2);  // out *= c**2 (grid.py:366)
+    }
+}
+
+constexpr int kGenBlocks = 1184;
 
 // Contiguous (rows, n) <-> pitched (rows, P): dir 1 scatters stage -> field, 0 gathers.
 __global__ void repitch_kernel(double *stage, int n, double *field, int P, long long rows, int dir) {
@@ -488,6 +626,7 @@ struct whb_ctx {
     double *flush_buf = nullptr;
     long long flush_elems = 0;
     double *stage = nullptr;         // contiguous staging buffer for host transfers
+    GeomG geomg{};                   // general operator (kern == 3)
     // TMA tensor maps keyed by (buffer, box kind)
     std::map<std::tuple<const double *, int, int>, CUtensorMap> tmaps;
 };
@@ -908,6 +1047,14 @@ int tensor_map(whb_ctx *c, const double *base, int box_w, int box_h, CUtensorMap
 // finishing at this step (LAST) get their own launch.
 int launch_step_members(whb_ctx *c, int s, int moff, int nact, int i_begin, int i_end, int chunk_len, int part_off) {
     if (nact <= 0 || i_begin >= i_end) return 0;
+    if (c->kern == 3) {
+        if (moff != 0) return fail(WHB_E_STATE, "general kernel launches start at member 0");
+        step_general_kernel<<<dim3(kGenBlocks, nact, 1), 256, 0, c->stream>>>(c->geomg, c->d_members, s, (int)c->nloc,
+                                                                          part_off);
+        c->launches++;
+        WHB_CUDA(cudaGetLastError());
+        return 0;
+    }
     const int nch = (i_end - i_begin + chunk_len - 1) / chunk_len;
     if (c->kern >= 1) {
         const bool zf = c->cur_zf != 0;
@@ -1186,7 +1333,7 @@ int enqueue_solve(whb_ctx *c, int out_mode) {
             WHB_TRY(launch_step(c, s, active_members(c, s), c->upd_lo, c->upd_hi, c->chunk_len, 0));
     }
     if (out_mode == WHB_OUT_FPI) {
-        int np = c->gx * c->JT * c->nchunks;
+        int np = c->kern == 3 ? kGenBlocks : c->gx * c->JT * c->nchunks;
         if (c->tb2) np = std::max(np, c->gx2 * c->JT2 * c->nch2);
         if (c->wfT) np = std::max(np, std::max(c->gxw[2] * c->nchw[2], c->wfT == 4 ? c->gxw[4] * c->nchw[4] : 0));
         reduce_partials_kernel<<<1, 1024, 0, c->stream>>>(c->d_members, c->nbatch, np, c->d_hist, c->d_counter);
@@ -1346,10 +1493,13 @@ int copy_field_d2h(whb_ctx *c, const double *dev, double *host) {
 }
 
 int zero_bnd(whb_ctx *c, double *x) {
-    const int zlo = (c->act0 && c->plane_begin == 0) ? 1 : 0;
-    const int zhi = (c->act0 && c->plane_end == c->gshape[0]) ? 1 : 0;
+    const bool gen = c->kern == 3;
+    const int per0 = gen ? c->geomg.per[0] : 0;
+    const int zlo = (c->act0 && !per0 && c->plane_begin == 0) ? 1 : 0;
+    const int zhi = (c->act0 && !per0 && c->plane_end == c->gshape[0]) ? 1 : 0;
     zero_boundary_kernel<<<592, 256, 0, c->stream>>>(x, c->S0, c->P, (int)c->gshape[1], (int)c->gshape[2],
-                                                     c->act1, 1, (int)c->nloc + 1, zlo, zhi);
+                                                     c->act1, 1, (int)c->nloc + 1, zlo, zhi,
+                                                     gen ? c->geomg.per[1] : 0, gen ? c->geomg.per[2] : 0);
     c->launches++;
     WHB_CUDA(cudaGetLastError());
     return 0;
@@ -1525,6 +1675,53 @@ int whb_set_operator(whb_ctx *c, const double *clo, const double *cmid, double c
         g.clo2 = clo[1]; g.cmid2 = cmid[1];
     } else {
         g.clo2 = clo[0]; g.cmid2 = cmid[0];
+    }
+    c->op_set = true;
+    return 0;
+}
+
+int whb_set_operator_general(whb_ctx *c, int order, const int *periodic, const double *taps, double c2) {
+    if (!c || !periodic || !taps) return fail(WHB_E_ARG, "NULL argument");
+    if (order != 2 && order != 4) return fail(WHB_E_ARG, "order must be 2 or 4");
+    if (c->plane_begin != 0 || c->plane_end != (c->ndim == 1 ? 1 : c->gshape[0]))
+        return fail(WHB_E_ARG, "the general operator needs a whole-grid context (no slabs)");
+    WHB_TRY(set_dev(c));
+    GeomG &g = c->geomg;
+    std::memset(&g, 0, sizeof(g));
+    g.S0 = c->S0;
+    g.P = c->P;
+    g.order = order;
+    g.c2 = c2;
+    g.use_c2 = (c2 != 1.0);
+    g.plane_begin = (int)c->plane_begin;
+    const int off = 3 - c->ndim;  // reference axis a -> storage axis: 3D a, 2D (0, 2), 1D 2
+    for (int a = 0; a < c->ndim; ++a) {
+        const int sa = (c->ndim == 2 && a == 1) ? 2 : (c->ndim == 2 ? 0 : off + a);
+        g.act[sa] = 1;
+        g.per[sa] = periodic[a] ? 1 : 0;
+        for (int q = 0; q <= order; ++q) g.taps[sa][q] = taps[a * (order + 1) + q];
+    }
+    g.n[0] = (int)c->gshape[0];
+    g.n[1] = (int)c->gshape[1];
+    g.n[2] = (int)c->gshape[2];
+    for (int a = 0; a < 3; ++a)
+        if (g.act[a] && g.n[a] < order + 1) return fail(WHB_E_ARG, "axis too short for the stencil");
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
+    c->kern = 3;
+    c->tb2 = false;
+    c->tb2r = false;
+    c->wfT = 0;
+    for (auto &kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    c->graphs.clear();
+    c->graph_kernels.clear();
+    if (c->nparts < kGenBlocks) {
+        c->nparts = kGenBlocks;
+        for (auto &m : c->mem) {
+            cudaFree(m.partials);
+            WHB_CUDA(cudaMalloc(&m.partials, (size_t)c->nparts * sizeof(double)));
+            WHB_CUDA(cudaMemset(m.partials, 0, (size_t)c->nparts * sizeof(double)));
+        }
+        c->h_members.clear();
     }
     c->op_set = true;
     return 0;
@@ -1797,6 +1994,12 @@ int whb_apply_operator(whb_ctx *c, int xi, int yi) {
     if (!c->op_set) return fail(WHB_E_STATE, "operator not set (whb_set_operator)");
     VEC_OR_FAIL(x, xi);
     VEC_OR_FAIL(y, yi);
+    if (c->kern == 3) {
+        apply_general_kernel<<<kGenBlocks, 256, 0, c->stream>>>(c->geomg, x, y, (int)c->nloc);
+        c->launches++;
+        WHB_CUDA(cudaGetLastError());
+        return 0;
+    }
     // update planes exclude global Dirichlet planes; ghost planes of x must hold neighbour data
     apply_operator_kernel<<<kRedBlocks, kRedThreads, 0, c->stream>>>(c->geom, x, y, c->act0, c->act1, c->upd_lo,
                                                                      c->upd_hi);

@@ -13,7 +13,7 @@ import collections
 import numpy as np
 
 from . import _native
-from .grid import operator_coefficients
+from .grid import general_operator, is_fast_operator, operator_coefficients
 
 __all__ = ["DeviceProblem", "device_problem", "release_device_cache"]
 
@@ -21,22 +21,30 @@ _MAX_CACHED = 2
 _cache: "collections.OrderedDict[tuple, DeviceProblem]" = collections.OrderedDict()
 
 
-def _grid_key(grid, c, device, nbatch=1, shared=False):
+def set_device_operator(ctx, grid, order, c):
+    """p = 2 all-Dirichlet -> the temporal-blocked kernels; anything else (p = 4, periodic or
+    mixed boundaries) -> the general one-step kernel."""
+    if is_fast_operator(grid, order):
+        ctx.set_operator(*operator_coefficients(grid, order, c))
+    else:
+        ctx.set_operator_general(*general_operator(grid, order, c))
+
+
+def _grid_key(grid, c, device, nbatch=1, shared=False, order=2):
     return (tuple(int(n) for n in grid.shape), tuple(float(d) for d in grid.spacing), float(c), int(device),
-            int(nbatch), bool(shared))
+            int(nbatch), bool(shared), int(order))
 
 
 class DeviceProblem:
     """A grid on one GPU (optionally a batch of problems sharing the grid)."""
 
     def __init__(self, grid, c=1.0, order=2, device=0, nbatch=1, shared_forcing=False, plane_range=None):
-        clo, cmid, c2 = operator_coefficients(grid, order, c)
         self.grid = grid
         self.c = float(c)
         self.nbatch = nbatch
         self.ctx = _native.Context(grid.shape, device=device, plane_range=plane_range, nbatch=nbatch,
                                    shared_forcing=shared_forcing)
-        self.ctx.set_operator(clo, cmid, c2)
+        set_device_operator(self.ctx, grid, order, c)
         self._sched = [None] * nbatch
         self._forcing = [None] * (1 if shared_forcing else nbatch)
         self.shared_forcing = shared_forcing
@@ -69,7 +77,7 @@ class DeviceProblem:
 
 def device_problem(grid, c=1.0, order=2, device=0) -> DeviceProblem:
     """Cached single-problem device state for a grid (LRU of a few entries)."""
-    key = _grid_key(grid, c, device)
+    key = _grid_key(grid, c, device, order=order) + tuple(str(getattr(b, "value", b)) for b in grid.bcs)
     dp = _cache.get(key)
     if dp is not None:
         _cache.move_to_end(key)

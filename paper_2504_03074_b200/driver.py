@@ -36,17 +36,24 @@ class NearSingularError(ValueError):
     """driver.py:58-59."""
 
 
+def _axis_lambda2(n: int, dx: float, bc: str, order: int, c: float) -> np.ndarray:
+    """lambda^2 of the 1D modes of one axis (grid.py:417-446): Dirichlet sines
+    theta = m pi/n (m = 1..n-1), periodic Fourier theta = 2 pi m/n (m = 0..n/2);
+    symbol 4 sin^2(theta/2) (+ its square / 12 at p = 4)."""
+    m = np.arange(1, n) if bc == "dirichlet" else np.arange(0, n // 2 + 1)
+    theta = m * np.pi / n if bc == "dirichlet" else 2.0 * np.pi * m / n
+    s2 = 4.0 * np.sin(theta / 2.0) ** 2
+    sym = s2 if order == 2 else s2 + s2**2 / 12.0
+    return (c / dx) ** 2 * sym
+
+
 def resonance_gap(grid, order: int, c: float, omega: float) -> float:
-    """min |omega - lambda_h| / omega over the discrete Dirichlet spectrum
-    (driver.py:72-81 with grid.py:417-472), without enumerating modes in Python:
-    per-axis lambda^2 lists, the trailing axes combined into one sorted array,
-    then a bisection per leading-axis value."""
-    if order != 2:
-        raise NotImplementedError("resonance check implemented for p = 2")
-    per_axis = []
-    for n, dx in zip(grid.cells, grid.spacing):
-        m = np.arange(1, n)
-        per_axis.append((c / dx) ** 2 * (4.0 * np.sin(m * np.pi / n / 2.0) ** 2))
+    """min |omega - lambda_h| / omega over the discrete spectrum (driver.py:72-81 with
+    grid.py:417-472), without enumerating modes in Python: per-axis lambda^2 lists, the
+    trailing axes combined into one sorted array, then a bisection per leading-axis value."""
+    if order not in (2, 4):
+        raise ValueError(f"unsupported order p={order}")
+    per_axis = [_axis_lambda2(n, dx, bc_name(b), order, c) for n, dx, b in zip(grid.cells, grid.spacing, grid.bcs)]
     w2 = omega * omega
     if len(per_axis) == 1:
         lam = np.sqrt(per_axis[0])
@@ -77,7 +84,8 @@ class HelmholtzProblem:
     def __post_init__(self):
         if not self.omega > 0:
             raise ValueError("omega must be positive")
-        if all(bc_name(b) == "dirichlet" for b in self.grid.bcs) and self.order == 2:
+        names = [bc_name(b) for b in self.grid.bcs]
+        if all(b == "dirichlet" for b in names) or all(b == "periodic" for b in names):
             gap = resonance_gap(self.grid, self.order, self.c, self.omega)
             if gap < 1e-10:
                 raise ResonanceError(f"omega = {self.omega:.12g} is within {gap:.1e} of a discrete eigenvalue")

@@ -22,7 +22,7 @@ import numpy as np
 
 __all__ = [
     "BC", "CartesianGrid", "GridField", "DiscreteOperator", "build_grid", "stencil_coefficients",
-    "bc_name", "operator_coefficients",
+    "bc_name", "operator_coefficients", "general_operator", "is_fast_operator",
 ]
 
 
@@ -264,14 +264,28 @@ class DiscreteOperator:
         return GridField(self.grid, u.ghost, self.apply_values(u.values))
 
 
+def is_fast_operator(grid, order: int) -> bool:
+    """p = 2 with homogeneous Dirichlet on every axis: the temporal-blocked kernels apply."""
+    return order == 2 and all(bc_name(b) == "dirichlet" for b in grid.bcs)
+
+
+def general_operator(grid, order: int, c: float):
+    """(order, periodic[d], taps[d][p+1], c2) exactly as the reference forms them:
+    ``stencil_coefficients(p, dx)`` per axis (grid.py:296-306) and ``c**2`` (grid.py:366).
+    Any order in {2, 4} and per-axis Dirichlet / periodic boundaries."""
+    if order not in (2, 4):
+        raise ValueError(f"unsupported order p={order}; expected 2 or 4")
+    periodic = [1 if bc_name(b) == "periodic" else 0 for b in grid.bcs]
+    taps = np.array([stencil_coefficients(order, dx) for dx in grid.spacing])
+    return order, periodic, taps, float(c**2)
+
+
 def operator_coefficients(grid, order: int, c: float):
     """(clo[d], cmid[d], c2) exactly as the reference forms them: the taps
     ``np.array([1,-2,1]) / dx**2`` of each axis (grid.py:302-306) and ``c**2``
     (grid.py:366).  Only p = 2 with all-Dirichlet boundaries runs on the GPU."""
-    if order != 2:
-        raise NotImplementedError("the GPU path implements the order-2 stencil (p=4 is a SURVEY §8(f) 'next' row)")
-    if not all(bc_name(b) == "dirichlet" for b in grid.bcs):
-        raise NotImplementedError("the GPU path implements homogeneous Dirichlet boundaries only")
+    if not is_fast_operator(grid, order):
+        raise NotImplementedError("operator_coefficients covers p = 2 / all-Dirichlet; use general_operator")
     taps = [stencil_coefficients(2, dx) for dx in grid.spacing]
     clo = np.array([t[0] for t in taps])
     cmid = np.array([t[1] for t in taps])

@@ -284,6 +284,68 @@ def run_small():
     dump("small", {"cases": cases}, arrays)
 
 
+def run_ext():
+    """order-4 stencils and periodic / mixed boundaries."""
+    wh = RH.import_reference()
+    rng = np.random.default_rng(20261019)
+    cases, arrays = {}, {}
+    GF = wh.grid.GridField
+
+    def case(key, dim, bounds, cells, bcs, p, omega, c=1.0, periods=1):
+        g = RH.grid(dim, bounds, cells, bcs)
+        corr, cfg, op = RH.explicit_setup(g, omega, p, c, periods)
+        v = GF.from_values(g, rng.standard_normal(g.shape), ghost=2)
+        f = GF.from_values(g, rng.standard_normal(g.shape) * 30.0, ghost=2)
+        out = wh.timestep.wave_solve_filtered(v, f, cfg, corr, op)
+        lap = op.apply_values(v.values)
+        av = np.array(v.values) - wh.timestep.wave_solve_filtered(v, GF.zeros(g), cfg, corr, op).values
+        cases[key] = {"dim": dim, "bounds": [list(b) for b in bounds], "cells": list(cells),
+                      "bcs": [bcs] * dim if isinstance(bcs, str) else list(bcs), "order": p, "omega": omega,
+                      "c": c, "periods": periods, "corr": corr_dict(corr, cfg), "out_sha256": sha(out.values),
+                      "av_sha256": sha(av), "lap_sha256": sha(lap)}
+        arrays[f"{key}__v"] = np.array(v.values)
+        arrays[f"{key}__f"] = np.array(f.values)
+        arrays[f"{key}__out"] = np.array(out.values)
+
+    case("p4_d1", 1, [(0.0, 1.0)], [20], "dirichlet", 4, 5.5)
+    case("p4_d2", 2, [(0.0, 1.0), (0.0, 1.3)], [16, 22], "dirichlet", 4, 7.0, c=1.1)
+    case("p4_d2_np2", 2, [(0.0, 1.0), (0.0, 1.3)], [16, 22], "dirichlet", 4, 7.0, periods=2)
+    case("p4_d3", 3, [(0.0, 1.0), (0.0, 1.2), (-0.3, 0.6)], [10, 12, 9], "dirichlet", 4, 6.0)
+    case("p4_min", 2, [(0.0, 1.0)] * 2, [4, 4], "dirichlet", 4, 3.0)
+    case("per_p2_d1", 1, [(0.0, 2.0)], [24], "periodic", 2, 4.1)
+    case("per_p2_d2", 2, [(0.0, 1.0), (0.0, 0.8)], [20, 16], "periodic", 2, 9.3)
+    case("per_p2_d3", 3, [(0.0, 1.0)] * 3, [8, 10, 12], "periodic", 2, 7.7)
+    case("per_p4_d1", 1, [(0.0, 2.0)], [24], "periodic", 4, 4.1)
+    case("per_p4_d2", 2, [(0.0, 1.0), (0.0, 0.8)], [18, 20], "periodic", 4, 9.3)
+    case("per_p4_d3", 3, [(0.0, 1.0)] * 3, [8, 6, 10], "periodic", 4, 6.3)
+    case("mix_p2_d2", 2, [(0.0, 1.0), (0.0, 1.0)], [18, 15], ["periodic", "dirichlet"], 2, 8.8)
+    case("mix_p4_d2", 2, [(0.0, 1.0), (0.0, 1.0)], [18, 15], ["dirichlet", "periodic"], 4, 8.8)
+    case("mix_p2_d3", 3, [(0.0, 1.0)] * 3, [9, 8, 12], ["dirichlet", "periodic", "dirichlet"], 2, 7.0)
+    case("mix_p4_d3", 3, [(0.0, 1.0)] * 3, [9, 8, 12], ["periodic", "dirichlet", "periodic"], 4, 7.0)
+
+    # FPI (5 iterations) and GMRES through the public drivers on order-4 problems
+    g = RH.grid(2, [(0.0, 1.0)] * 2, [24, 24], "periodic")
+    f = wh.driver.gaussian_source(g, 6.1, -80.0, 25.0, (0.45, 0.55))
+    fpi = {"iter_sha256": [], "residuals": []}
+    for k, vk, r in RH.fpi_iterates(g, f, 6.1, 5, p=4):
+        fpi["iter_sha256"].append(sha(vk))
+        fpi["residuals"].append(float(r))
+    cases["fpi_per_p4"] = fpi
+    arrays["fpi_per_p4__f"] = np.array(f.values)
+    g1 = RH.grid(1, [(0.0, 1.0)], [32], "dirichlet")
+    f1 = wh.driver.gaussian_source(g1, 5.5, -100.0, 30.0, 0.37)
+    prob = wh.driver.HelmholtzProblem(g1, 4, 1.0, 5.5, f1)
+    cfg0 = wh.filters.FilterConfig(omega=5.5, periods=1, steps_per_period=10, mode="explicit")
+    x, run = wh.driver.krylov_solve(prob, cfg0, tol=1e-10)
+    vf, runf = wh.driver.fpi_solve(prob, cfg0, tol=1e-10, maxit=800)
+    cases["gmres_p4_1d"] = {"iterations": run.iterations, "residuals": [float(r) for r in run.residuals],
+                            "fpi_iterations": runf.iterations}
+    arrays["gmres_p4_1d__x"] = np.array(x.values)
+    arrays["gmres_p4_1d__fpi"] = np.array(vf.values)
+    arrays["gmres_p4_1d__f"] = np.array(f1.values)
+    dump("ext", {"cases": cases}, arrays)
+
+
 class _null:
     def __enter__(self):
         return self
@@ -294,11 +356,13 @@ class _null:
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", choices=["small", "cfg1", "cfg2", "cfg3", "cfg5"])
+    ap.add_argument("which", choices=["small", "ext", "cfg1", "cfg2", "cfg3", "cfg5"])
     ap.add_argument("--procs", type=int, default=4)
     a = ap.parse_args()
     if a.which == "small":
         run_small()
+    elif a.which == "ext":
+        run_ext()
     elif a.which == "cfg5":
         run_cfg5(a.procs)
     else:

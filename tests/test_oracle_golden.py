@@ -139,3 +139,24 @@ def test_eigen_action_kat_on_oracle(cells, ks):
         out = O.wave_solve_filtered(phi, np.zeros_like(phi), sp, sc)
         beta = O.eigen_action_factor(cells, sp, ks, omega, n_t, dt, we, periods)
         assert np.max(np.abs(out - beta * phi)) <= 1e-10
+
+
+EXT = ["p4_d1", "p4_d2", "p4_d2_np2", "p4_d3", "p4_min", "per_p2_d1", "per_p2_d2", "per_p2_d3", "per_p4_d1",
+       "per_p4_d2", "per_p4_d3", "mix_p2_d2", "mix_p4_d2", "mix_p2_d3", "mix_p4_d3"]
+
+
+@pytest.mark.parametrize("key", EXT)
+def test_numpy_oracle_order4_periodic_bitwise(key):
+    """order-4 stencils, periodic and mixed boundaries."""
+    meta, A = load_golden("ext")
+    case = meta["cases"][key]
+    bcs = case["bcs"]
+    sp = tuple((hi - lo) / n for (lo, hi), n in zip(case["bounds"], case["cells"]))
+    p = case["order"]
+    n_t, dt, we = O.correct_explicit(case["omega"], sp, p, case["c"])
+    assert (n_t, dt, we) == (case["corr"]["steps_per_period"], case["corr"]["dt"], case["corr"]["omega_tilde"])
+    sc = O.step_scalars(n_t, dt, we, case["periods"])
+    v, f = A[key + "__v"], A[key + "__f"]
+    assert sha(O.wave_solve_filtered(v, f, sp, sc, case["c"], bcs, p)) == case["out_sha256"]
+    assert sha(O.apply_A(v, sp, sc, case["c"], bcs, p)) == case["av_sha256"]
+    assert sha(O.laplacian_general(v, sp, bcs, p, case["c"])) == case["lap_sha256"]
