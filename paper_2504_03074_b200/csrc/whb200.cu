@@ -295,6 +295,7 @@ __global__ void zero_boundary_kernel(double *x, long long S0, int P, int n1, int
 #include "step_tb2.cuh"
 #include "step_wf2d.cuh"
 #include "step_tb2r.cuh"
+#include "step_tb2w.cuh"
 namespace {
 
 // y = c^2 * L_h x at owned interior points (DiscreteOperator.apply_values, grid.py:346-368);
@@ -603,6 +604,7 @@ struct whb_ctx {
     size_t smem2 = 0;
     int gx2 = 1, JT2 = 1, chunk2 = 1, nch2 = 1;
     bool tb2r = false;               // 3D: balanced 62-column variant of the two-step kernel
+    bool tb2w = false;               // 3D: warp-specialised two-step kernel
     // 2D wavefront plan (T steps per pass): whole-grid 2D contexts
     int wfT = 0;                     // 0 = off, else 2 or 4
     int nring = 4;                   // time-level buffers per member (6 when wfT == 4)
@@ -702,6 +704,25 @@ auto tb2_fn() {
 }
 
 constexpr int R3_BY = 16, R3_ST = 5;
+constexpr int W3_BY = 14, W3_ST = 5;
+
+template <int K1, int K2, bool ZF>
+auto tb2w_fn() {
+    return tb2w::tb2w_kernel<W3_BY, W3_ST, K1, K2, ZF>;
+}
+
+cudaError_t tb2w_set_attrs(size_t smem) {
+    cudaError_t e = cudaSuccess;
+    auto set = [&](auto fn) {
+        cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (r != cudaSuccess) e = r;
+    };
+    set(tb2w_fn<K_FIRST, K_MID, false>()); set(tb2w_fn<K_FIRST, K_MID, true>());
+    set(tb2w_fn<K_MID, K_MID, false>());   set(tb2w_fn<K_MID, K_MID, true>());
+    set(tb2w_fn<K_MID, K_LAST, false>());  set(tb2w_fn<K_MID, K_LAST, true>());
+    set(tb2w_fn<K_FIRST, K_LAST, false>()); set(tb2w_fn<K_FIRST, K_LAST, true>());
+    return e;
+}
 
 template <int K1, int K2, bool ZF>
 auto tb2r_fn() {
@@ -873,10 +894,32 @@ int plan_launch(whb_ctx *c) {
     const char *tenv = getenv("WHB_TB2");
     c->tb2 = c->kern >= 1 && c->plane_begin == 0 && c->plane_end == c->gshape[0] &&
              !(tenv && std::string(tenv) == "0") && (!c->act1 || c->kern == 2);
+    const char *wenv3 = getenv("WHB_TB2W");
+    c->tb2w = c->tb2 && c->act1 && (wenv3 && std::string(wenv3) == "1");
     const char *renv = getenv("WHB_TB2R");
     // measured on 257^3 / 1025^3: 126.5 / 131.0 Gpts/s vs 143.7 / 149.3 for tb2 -> opt-in (WHB_TB2R=1)
-    c->tb2r = c->tb2 && c->act1 && (renv && std::string(renv) == "1");
-    if (c->tb2r) {
+    c->tb2r = c->tb2 && c->act1 && !c->tb2w && (renv && std::string(renv) == "1");
+    if (c->tb2w) {
+        c->smem2 = tb2w::smem_bytes<W3_BY, W3_ST>();
+        cudaError_t e = tb2w_set_attrs(c->smem2);
+        if (e != cudaSuccess) return fail(WHB_E_CUDA, std::string("cudaFuncSetAttribute(tb2w): ") + cudaGetErrorString(e));
+        int nb = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, tb2w_fn<K_MID, K_MID, false>(), tb2w::Lay<W3_BY>::THREADS,
+                                                          c->smem2);
+        if (e != cudaSuccess || nb < 1) return fail(WHB_E_CUDA, "tb2w kernel does not fit on an SM");
+        c->gx2 = (int)((n2 - 2 + 61) / 62);
+        c->JT2 = (int)((n1 - 1 + W3_BY - 1) / W3_BY);
+        const long long res2 = (long long)sms * nb;
+        const long long tiles2 = (long long)c->gx2 * c->JT2;
+        const long long nch = std::max<long long>(1, 4 * res2 / std::max<long long>(1, tiles2));
+        int cl2 = (int)((nplanes + nch - 1) / nch);
+        const char *env2 = getenv("WHB_CHUNK2");
+        if (env2 && atoi(env2) > 0) cl2 = atoi(env2);
+        c->chunk2 = std::max(1, cl2);
+        c->nch2 = (nplanes + c->chunk2 - 1) / c->chunk2;
+        if ((long long)c->JT2 * c->nch2 > 65535) c->tb2 = c->tb2w = false;
+        c->nparts = std::max(c->nparts, c->gx2 * c->JT2 * (c->nch2 + 2));
+    } else if (c->tb2r) {
         c->smem2 = tb2r::smem_bytes<R3_BY, R3_ST>();
         cudaError_t e = tb2r_set_attrs(c->smem2);
         if (e != cudaSuccess) return fail(WHB_E_CUDA, std::string("cudaFuncSetAttribute(tb2r): ") + cudaGetErrorString(e));
@@ -1184,6 +1227,27 @@ void launch_tb2r_kinds(whb_ctx *c, int k1, int k2, bool zf, dim3 grid, int off, 
 #undef WHB_TB2R_CASE
 }
 
+template <int K1, int K2, bool ZF>
+void launch_tb2w(whb_ctx *c, dim3 grid, int off, int s, int ib, int ie, const StepMaps &mp) {
+    tb2w_fn<K1, K2, ZF>()<<<grid, tb2w::Lay<W3_BY>::THREADS, c->smem2, c->stream>>>(
+        c->geom, c->d_members, off, s, ib, ie, c->chunk2, c->JT2, 0, mp.w, mp.p, mp.f, mp.a);
+}
+
+void launch_tb2w_kinds(whb_ctx *c, int k1, int k2, bool zf, dim3 grid, int off, int s, int ib, int ie,
+                       const StepMaps &mp) {
+#define WHB_TB2W_CASE(K1, K2)                                                      \
+    if (k1 == K1 && k2 == K2) {                                                    \
+        if (zf) launch_tb2w<K1, K2, true>(c, grid, off, s, ib, ie, mp);           \
+        else launch_tb2w<K1, K2, false>(c, grid, off, s, ib, ie, mp);             \
+        return;                                                                    \
+    }
+    WHB_TB2W_CASE(K_FIRST, K_MID)
+    WHB_TB2W_CASE(K_MID, K_MID)
+    WHB_TB2W_CASE(K_MID, K_LAST)
+    WHB_TB2W_CASE(K_FIRST, K_LAST)
+#undef WHB_TB2W_CASE
+}
+
 // Fused steps (s, s+1), s even, for the table members [0, nact): those still running
 // after s+1 get (K1, MID), those finishing at s+1 get (K1, LAST).
 int launch_pair(whb_ctx *c, int s) {
@@ -1204,17 +1268,23 @@ int launch_pair(whb_ctx *c, int s) {
         WHB_TRY(tensor_map(c, m0.acc, T3_TX, T3_BY, &mp.a));
         if (m0.f) WHB_TRY(tensor_map(c, m0.f, T3_TX + 4, T3_BY + 2, &mp.f));
     }
-    if (c->tb2r) {  // balanced 3D variant: boxes W (68, BY+4), P/F (64, BY+2), acc (64, BY)
+    if (c->tb2r || c->tb2w) {  // 62-column variants: boxes W (68, BY+4), P/F (64, BY+2), acc (64, BY)
+        const int by = c->tb2w ? W3_BY : R3_BY;
         const Member &m0 = c->h_members[0];
-        WHB_TRY(tensor_map(c, level_ptr(m0, s), 68, R3_BY + 4, &mp.w));
-        WHB_TRY(tensor_map(c, level_ptr(m0, s - 1), 64, R3_BY + 2, &mp.p));
-        WHB_TRY(tensor_map(c, m0.acc, 64, R3_BY, &mp.a));
-        if (m0.f) WHB_TRY(tensor_map(c, m0.f, 64, R3_BY + 2, &mp.f));
+        WHB_TRY(tensor_map(c, level_ptr(m0, s), 68, by + 4, &mp.w));
+        WHB_TRY(tensor_map(c, level_ptr(m0, s - 1), 64, by + 2, &mp.p));
+        WHB_TRY(tensor_map(c, m0.acc, 64, by, &mp.a));
+        if (m0.f) WHB_TRY(tensor_map(c, m0.f, 64, by + 2, &mp.f));
     }
     const int k1 = (s == 0) ? K_FIRST : K_MID;
     auto go = [&](int k2, int off, int cnt) {
         if (cnt <= 0) return;
         dim3 grid(c->gx2, c->JT2 * c->nch2, cnt);
+        if (c->tb2w) {
+            launch_tb2w_kinds(c, k1, k2, zf, grid, off, s, c->upd_lo, c->upd_hi, mp);
+            c->launches++;
+            return;
+        }
         if (c->tb2r) {
             launch_tb2r_kinds(c, k1, k2, zf, grid, off, s, c->upd_lo, c->upd_hi, mp);
             c->launches++;
