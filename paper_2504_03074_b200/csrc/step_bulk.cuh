@@ -204,9 +204,16 @@ __global__ void __launch_bounds__(Layout<TX, BY, A1>::THREADS)
     const int wr = A1 ? ty + 1 : 0;  // center row inside the w segment
     const int wc = kl + 2;           // center column inside the w segment
     double rsum = 0.0;
+    // last step: v of the next plane is loaded one plane ahead (hides its HBM latency)
+    const bool want_v = (KIND == K_LAST) && m.out_mode != WHB_OUT_PLAIN && row_ok && (ok0 || ok1);
+    const long long pbase = (long long)j * P + k;
+    double2 vcur = want_v ? *reinterpret_cast<const double2 *>(m.v + (long long)i0 * S0 + pbase) : make_double2(0.0, 0.0);
 
     for (int i = i0; i < i1; ++i) {
         const int t = i - i0 + 1;  // stage of plane i
+        const double2 vnext = (want_v && i + 1 < i1)
+                                  ? *reinterpret_cast<const double2 *>(m.v + (long long)(i + 1) * S0 + pbase)
+                                  : make_double2(0.0, 0.0);
         if (i > i0) {
             __syncthreads();  // everyone is done with plane i-1: stage of plane i-2 is free
             if (tid == 0) {
@@ -269,23 +276,24 @@ __global__ void __launch_bounds__(Layout<TX, BY, A1>::THREADS)
             const double o1 = whb_mul(m.out_scale, whb_add(a2.y, whb_mul(accn, n1)));
             if (m.out_mode == WHB_OUT_FPI) {
                 if (ok0) {
-                    const double d0 = o0 - m.v[p];
+                    const double d0 = o0 - vcur.x;
                     rsum += d0 * d0;
                     m.v[p] = o0;
                 }
                 if (ok1) {
-                    const double d1 = o1 - m.v[p + 1];
+                    const double d1 = o1 - vcur.y;
                     rsum += d1 * d1;
                     m.v[p + 1] = o1;
                 }
             } else if (m.out_mode == WHB_OUT_AV) {
-                if (ok0) m.dst[p] = whb_sub(m.v[p], o0);
-                if (ok1) m.dst[p + 1] = whb_sub(m.v[p + 1], o1);
+                if (ok0) m.dst[p] = whb_sub(vcur.x, o0);
+                if (ok1) m.dst[p + 1] = whb_sub(vcur.y, o1);
             } else {
                 if (ok0) m.dst[p] = o0;
                 if (ok1) m.dst[p + 1] = o1;
             }
         }
+        vcur = vnext;
     }
     if (KIND == K_LAST && m.out_mode == WHB_OUT_FPI) {
         const double t = block_sum(rsum);

@@ -180,8 +180,16 @@ __global__ void __launch_bounds__(Lay<TX, BY, A1>::THREADS)
         return inside ? w : 0.0;  // Dirichlet (and out-of-domain) points of W^{s+1} are 0
     };
 
+    // last pass: v of the next output plane is loaded one iteration ahead (hides its HBM latency)
+    const bool want_v = (K2 == K_LAST) && m.out_mode != WHB_OUT_PLAIN && row_ok && (ok0 || ok1);
+    const long long pbase = (long long)j * P + k;
+    double2 vcur = make_double2(0.0, 0.0);
     for (int i = i0 - 1; i <= i1; ++i) {
         const int t = i - i0 + 2;  // stage of plane i
+        // output plane of this iteration is i-1; prefetch v for plane i (next iteration's output)
+        const double2 vnext = (want_v && i >= i0 && i < i1)
+                                  ? *reinterpret_cast<const double2 *>(m.v + (long long)i * S0 + pbase)
+                                  : make_double2(0.0, 0.0);
         if (i > i0 - 1) {
             __syncthreads();  // plane i-1 done: stage of plane i-2 and E slot of plane i-3 are free
             if (tid == 0) {
@@ -266,24 +274,25 @@ __global__ void __launch_bounds__(Lay<TX, BY, A1>::THREADS)
                 const double o1 = whb_mul(m.out_scale, a1);
                 if (m.out_mode == WHB_OUT_FPI) {
                     if (ok0) {
-                        const double d0 = o0 - m.v[p];
+                        const double d0 = o0 - vcur.x;
                         rsum += d0 * d0;
                         m.v[p] = o0;
                     }
                     if (ok1) {
-                        const double d1 = o1 - m.v[p + 1];
+                        const double d1 = o1 - vcur.y;
                         rsum += d1 * d1;
                         m.v[p + 1] = o1;
                     }
                 } else if (m.out_mode == WHB_OUT_AV) {
-                    if (ok0) m.dst[p] = whb_sub(m.v[p], o0);
-                    if (ok1) m.dst[p + 1] = whb_sub(m.v[p + 1], o1);
+                    if (ok0) m.dst[p] = whb_sub(vcur.x, o0);
+                    if (ok1) m.dst[p + 1] = whb_sub(vcur.y, o1);
                 } else {
                     if (ok0) m.dst[p] = o0;
                     if (ok1) m.dst[p + 1] = o1;
                 }
             }
         }
+        vcur = vnext;
     }
     if (K2 == K_LAST && m.out_mode == WHB_OUT_FPI) {
         const double t = block_sum(rsum);

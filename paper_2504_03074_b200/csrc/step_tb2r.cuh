@@ -131,9 +131,15 @@ __global__ void __launch_bounds__(Lay<BY>::THREADS)
     const bool ok0 = orow_ok && xin0 && lane > 0;
     const bool ok1 = orow_ok && xin1 && lane < 31 && kx + 1 < k0 + L::TX;
     double rsum = 0.0;
+    const bool want_v = (K2 == K_LAST) && m.out_mode != WHB_OUT_PLAIN && p2 && (ok0 || ok1);
+    const long long pbase = (long long)jo * P + kx;
+    double2 vcur = make_double2(0.0, 0.0);
 
     for (int i = i0 - 1; i <= i1; ++i) {
         const int t = i - i0 + 2;
+        const double2 vnext = (want_v && i >= i0 && i < i1)
+                                  ? *reinterpret_cast<const double2 *>(m.v + (long long)i * S0 + pbase)
+                                  : make_double2(0.0, 0.0);
         if (i > i0 - 1) {
             __syncthreads();
             if (tid == 0) {
@@ -224,17 +230,18 @@ __global__ void __launch_bounds__(Lay<BY>::THREADS)
                 const double o0 = whb_mul(m.out_scale, a0);
                 const double o1 = whb_mul(m.out_scale, a1);
                 if (m.out_mode == WHB_OUT_FPI) {
-                    if (ok0) { const double d = o0 - m.v[p]; rsum += d * d; m.v[p] = o0; }
-                    if (ok1) { const double d = o1 - m.v[p + 1]; rsum += d * d; m.v[p + 1] = o1; }
+                    if (ok0) { const double d = o0 - vcur.x; rsum += d * d; m.v[p] = o0; }
+                    if (ok1) { const double d = o1 - vcur.y; rsum += d * d; m.v[p + 1] = o1; }
                 } else if (m.out_mode == WHB_OUT_AV) {
-                    if (ok0) m.dst[p] = whb_sub(m.v[p], o0);
-                    if (ok1) m.dst[p + 1] = whb_sub(m.v[p + 1], o1);
+                    if (ok0) m.dst[p] = whb_sub(vcur.x, o0);
+                    if (ok1) m.dst[p + 1] = whb_sub(vcur.y, o1);
                 } else {
                     if (ok0) m.dst[p] = o0;
                     if (ok1) m.dst[p + 1] = o1;
                 }
             }
         }
+        vcur = vnext;
     }
     if (K2 == K_LAST && m.out_mode == WHB_OUT_FPI) {
         const double tsum = block_sum(rsum);

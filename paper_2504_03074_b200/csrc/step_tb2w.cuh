@@ -194,7 +194,14 @@ __global__ void __launch_bounds__(Lay<BY>::THREADS)
             mbar_arrive(empty + 0);
             mbar_arrive(empty + 1);
         }
+        const bool want_v = (K2 == K_LAST) && m.out_mode != WHB_OUT_PLAIN && (ok0 || ok1);
+        const long long pbase = (long long)jo * P + kx;
+        double2 vcur = want_v ? *reinterpret_cast<const double2 *>(m.v + (long long)i0 * S0 + pbase)
+                              : make_double2(0.0, 0.0);
         for (int j = i0; j < i1; ++j) {
+            const double2 vnext = (want_v && j + 1 < i1)
+                                      ? *reinterpret_cast<const double2 *>(m.v + (long long)(j + 1) * S0 + pbase)
+                                      : make_double2(0.0, 0.0);
             const int e = j - (i0 - 1);  // E index of plane j
             const int t = j - i0 + 2;    // stage of plane j
             if (j == i0) {
@@ -250,16 +257,17 @@ __global__ void __launch_bounds__(Lay<BY>::THREADS)
                 const double o0 = whb_mul(m.out_scale, a0);
                 const double o1 = whb_mul(m.out_scale, a1);
                 if (m.out_mode == WHB_OUT_FPI) {
-                    if (ok0) { const double d = o0 - m.v[p]; rsum += d * d; m.v[p] = o0; }
-                    if (ok1) { const double d = o1 - m.v[p + 1]; rsum += d * d; m.v[p + 1] = o1; }
+                    if (ok0) { const double d = o0 - vcur.x; rsum += d * d; m.v[p] = o0; }
+                    if (ok1) { const double d = o1 - vcur.y; rsum += d * d; m.v[p + 1] = o1; }
                 } else if (m.out_mode == WHB_OUT_AV) {
-                    if (ok0) m.dst[p] = whb_sub(m.v[p], o0);
-                    if (ok1) m.dst[p + 1] = whb_sub(m.v[p + 1], o1);
+                    if (ok0) m.dst[p] = whb_sub(vcur.x, o0);
+                    if (ok1) m.dst[p + 1] = whb_sub(vcur.y, o1);
                 } else {
                     if (ok0) m.dst[p] = o0;
                     if (ok1) m.dst[p + 1] = o1;
                 }
             }
+            vcur = vnext;
         }
         if (lane == 0) {  // nor those of planes i1 and i1+1 (the producer has issued everything by now)
             mbar_arrive(empty + ((n_st - 2) % ST));

@@ -134,6 +134,8 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, 3)
         const bool okc1 = own && col + 1 >= 1 && col + 1 < g.n2 - 1;
         const bool in0 = col >= 1 && col < g.n2 - 1;          // interior column (any level)
         const bool in1 = col + 1 >= 1 && col + 1 < g.n2 - 1;
+        // every lane of this warp interior in x: then only the (warp-uniform) row test remains
+        const bool warp_in = __all_sync(0xffffffffu, in0 && in1);
         // per-level scalars: level t (1..T) is produced by step s+t-1
         double hcoef[T + 1], cosl[T + 1], cacc[T + 1];
 #pragma unroll
@@ -156,10 +158,20 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, 3)
     #pragma unroll
             for (int t = 0; t < T; ++t) A[t] = make_double2(0.0, 0.0);
     
+            // last pass: v (W^0, needed for the residual / x - W(x,0)) of the row finishing in the
+            // NEXT iteration is loaded one iteration ahead so its HBM latency hides behind a row
+            constexpr bool NEED_V = (K2 == K_LAST);
+            const bool want_v = NEED_V && m.out_mode != WHB_OUT_PLAIN && own;
+            auto vload = [&](int orow) -> double2 {
+                if (!want_v || orow < i0 || orow >= i1) return make_double2(0.0, 0.0);
+                return *reinterpret_cast<const double2 *>(m.v + (long long)orow * S0 + col);
+            };
+            double2 vcur = vload(r0 - T);
 #pragma unroll 3
             for (int idx = 0; idx < nrows; ++idx) {
                 const int r = r0 + idx;
                 const int slot = idx % ST;
+                const double2 vnext = vload(r + 1 - T);
                 mbar_wait(full + slot, (idx / ST) & 1);
                 const double *st = smem + (size_t)slot * L::STAGE;
                 // W^s row r into the level-0 queue
@@ -199,7 +211,8 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, 3)
                                                            hcoef[t], cosl[t]);
                     }
                     const bool rin = (row >= g.i_lo) && (row < g.i_hi);
-                    nw[t] = make_double2((rin && in0) ? a : 0.0, (rin && in1) ? b : 0.0);
+                    if (rin && warp_in) nw[t] = make_double2(a, b);  // uniform: no per-lane selects
+                    else nw[t] = make_double2((rin && in0) ? a : 0.0, (rin && in1) ? b : 0.0);
                     Q[t][0] = Q[t][1];
                     Q[t][1] = Q[t][2];
                     Q[t][2] = nw[t];
@@ -243,17 +256,18 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, 3)
                         const double o0 = whb_mul(oscale, ac.x);
                         const double o1 = whb_mul(oscale, ac.y);
                         if (m.out_mode == WHB_OUT_FPI) {
-                            if (okc0) { const double d = o0 - m.v[p]; rsum += d * d; m.v[p] = o0; }
-                            if (okc1) { const double d = o1 - m.v[p + 1]; rsum += d * d; m.v[p + 1] = o1; }
+                            if (okc0) { const double d = o0 - vcur.x; rsum += d * d; m.v[p] = o0; }
+                            if (okc1) { const double d = o1 - vcur.y; rsum += d * d; m.v[p + 1] = o1; }
                         } else if (m.out_mode == WHB_OUT_AV) {
-                            if (okc0) m.dst[p] = whb_sub(m.v[p], o0);
-                            if (okc1) m.dst[p + 1] = whb_sub(m.v[p + 1], o1);
+                            if (okc0) m.dst[p] = whb_sub(vcur.x, o0);
+                            if (okc1) m.dst[p + 1] = whb_sub(vcur.y, o1);
                         } else {
                             if (okc0) m.dst[p] = o0;
                             if (okc1) m.dst[p + 1] = o1;
                         }
                     }
                 }
+                vcur = vnext;
                 // the stage of row r-T is no longer needed by this warp
                 __syncwarp();
                 if (idx >= T && lane == 0) mbar_arrive(empty + ((idx - T) % ST));
