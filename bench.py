@@ -18,9 +18,11 @@ cpu_baseline = numpy restatement of the reference (1 core), bounded sample
 --impl reference: the C OpenMP restatement of the reference on all host cores
              (the reference is pure numpy; oracle/ holds its bitwise restatement)
 
-N > 1 (torchrun): every rank solves its own copy of the workload on its GPU
-(independent problems, no data-path collective; "scaling": "weak"); time is the
-max over ranks.
+N > 1 (torchrun): configs 1/2 — every rank solves its own copy (independent
+problems, no data-path collective, "scaling": "weak"); config 5 — the 64
+frequencies are LPT-sharded across ranks ("strong"); configs 3/4 — z-slab
+decomposition with NCCL halo exchange ("strong", --decomp replicas for
+independent copies).  Time is the max over ranks.
 """
 
 from __future__ import annotations
