@@ -34,7 +34,10 @@
 extern "C" {
 #endif
 
-#define WHB_ABI_VERSION 1
+#define WHB_ABI_VERSION 2
+
+/* Ghost planes allocated on each side of a context's owned axis-0 planes. */
+#define WHB_GHOST_PLANES 2
 
 enum whb_status {
     WHB_OK = 0,
@@ -157,22 +160,39 @@ int whb_matvec(whb_ctx *ctx, int x, int y);
 /* ---- slab decomposition (multi-GPU) -------------------------------------
  * Step-level control for halo exchange between contexts on different
  * devices.  Step s of a solve advances W^s -> W^{s+1}.  A solve is
- *   whb_solve_begin; for s: whb_step(s, region); ...; whb_solve_end.
- * region 0 = all owned planes, 1 = the first and last owned planes only
- * (the planes neighbours need), 2 = the remaining interior planes.
- * whb_level_plane_ptr returns the device address of local plane `plane`
- * (0 = low ghost, 1..nloc = owned, nloc+1 = high ghost) of the buffer that
- * holds time level `level` of member 0 (level 0 = V). */
+ *   whb_solve_begin; for s: whb_step(s, region); ...; whb_solve_end
+ * or, with two leapfrog steps per HBM pass (whb_plan steps_per_pass == 2),
+ *   whb_solve_begin; for s = 0, 2, ...: whb_pair(s, region); [whb_step(N-1, 0)]; whb_solve_end.
+ * whb_step: region 0 = all owned planes, 1 = the first and last owned update
+ * planes only (the planes neighbours need), 2 = the remaining interior planes;
+ * W^s needs 1 exchanged ghost plane per side.
+ * whb_pair (steps s and s+1): region 0 = all, 1 = the two first and two last
+ * update planes, 2 = the rest; W^s needs 2 exchanged ghost planes per side,
+ * W^{s-1} and F one (F is static: exchange it once after upload); the last
+ * pass of a solve (s + 2 == n_total) must be region 0.
+ * Local plane indices: [0, G) low ghosts, [G, G + nloc) owned,
+ * [G + nloc, 2G + nloc) high ghosts, G = WHB_GHOST_PLANES (whb_ghost_planes).
+ * whb_level_plane_ptr returns the device address of local plane `plane` of
+ * the buffer that holds time level `level` of member 0 (level 0 = V);
+ * consecutive planes are contiguous (plane_elems apart). */
 int whb_solve_begin(whb_ctx *ctx, int out_mode, int zero_forcing);
 int whb_step(whb_ctx *ctx, int s, int region);
+int whb_pair(whb_ctx *ctx, int s, int region);
 int whb_solve_end(whb_ctx *ctx, double *resid_sq);
+int whb_ghost_planes(whb_ctx *ctx, int *ghost);
 int whb_level_plane_ptr(whb_ctx *ctx, int level, int64_t plane, uint64_t *dev_ptr, int64_t *plane_elems);
+/* the same for a field slot (enum whb_field) of a member, e.g. WHB_F for its ghost exchange */
+int whb_field_plane_ptr(whb_ctx *ctx, int field, int member, int64_t plane, uint64_t *dev_ptr,
+                        int64_t *plane_elems);
 int whb_stream_ptr(whb_ctx *ctx, uint64_t *stream);
 int whb_synchronize(whb_ctx *ctx);
 /* copy a plane between two contexts (same or peer device), ordered on src's
  * stream then dst's (the single-process multi-shard path). */
 int whb_copy_plane(whb_ctx *src, int src_level, int64_t src_plane, whb_ctx *dst, int dst_level,
                    int64_t dst_plane);
+/* copy `bytes` between device addresses of two contexts (e.g. several planes from
+ * whb_level_plane_ptr / whb_field_plane_ptr), ordered the same way. */
+int whb_copy_device(whb_ctx *src, uint64_t src_ptr, whb_ctx *dst, uint64_t dst_ptr, int64_t bytes);
 
 /* ---- introspection -------------------------------------------------------- */
 /* Number of kernel launches issued by this context since creation. */

@@ -29,6 +29,7 @@ EXPORTS = (
     "whb_step", "whb_solve_end", "whb_level_plane_ptr", "whb_stream_ptr", "whb_synchronize",
     "whb_copy_plane", "whb_launch_count", "whb_set_timing", "whb_last_timing", "whb_host_alloc",
     "whb_host_free", "whb_geometry", "whb_set_l2_flush", "whb_apply_operator", "whb_plan", "whb_set_operator_general",
+    "whb_pair", "whb_ghost_planes", "whb_field_plane_ptr", "whb_copy_device",
 )
 
 _lib = None
@@ -92,6 +93,10 @@ def load():
         "whb_apply_operator": ([vp, c_int, c_int], c_int),
         "whb_plan": ([vp, ctypes.POINTER(c_int), ctypes.POINTER(c_int)], c_int),
         "whb_set_operator_general": ([vp, c_int, ctypes.POINTER(c_int), dp, c_double], c_int),
+        "whb_pair": ([vp, c_int, c_int], c_int),
+        "whb_ghost_planes": ([vp, ctypes.POINTER(c_int)], c_int),
+        "whb_field_plane_ptr": ([vp, c_int, c_int, c_i64, ctypes.POINTER(c_u64), ip64], c_int),
+        "whb_copy_device": ([vp, c_u64, vp, c_u64, c_i64], c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -292,6 +297,24 @@ class Context:
 
     def step(self, s, region=0):
         check(load().whb_step(self._h, int(s), int(region)), "whb_step")
+
+    def pair(self, s, region=0):
+        check(load().whb_pair(self._h, int(s), int(region)), "whb_pair")
+
+    def ghost_planes(self) -> int:
+        g = ctypes.c_int(0)
+        check(load().whb_ghost_planes(self._h, ctypes.byref(g)), "whb_ghost_planes")
+        return g.value
+
+    def field_plane_ptr(self, field, plane, member=0):
+        p = ctypes.c_uint64(0)
+        n = ctypes.c_int64(0)
+        check(load().whb_field_plane_ptr(self._h, int(field), int(member), int(plane), ctypes.byref(p),
+                                         ctypes.byref(n)), "whb_field_plane_ptr")
+        return p.value, n.value
+
+    def copy_device_to(self, src_ptr: int, dst: "Context", dst_ptr: int, nbytes: int):
+        check(load().whb_copy_device(self._h, int(src_ptr), dst._h, int(dst_ptr), int(nbytes)), "whb_copy_device")
 
     def solve_end(self):
         r = ctypes.c_double(0.0)

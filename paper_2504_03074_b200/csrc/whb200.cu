@@ -16,7 +16,7 @@
 // iterate is bitwise identical to waveholtz.timestep.wave_solve_filtered.
 //
 // Data layout in HBM: a field is stored as 3D
-// (planes, n1, pitch) float64, planes = owned axis-0 planes + 2 ghost planes,
+// (planes, n1, pitch) float64, planes = owned axis-0 planes + 2 x GH ghost planes,
 // row pitch = n2 rounded up to 16 elements (128 B) so every row starts on a
 // cache-line boundary.  2D grids (n0, n1) are stored as (n0, 1, n1) and 1D
 // grids (n) as (1, 1, n), so the same kernel marches along storage axis 0
@@ -40,6 +40,10 @@
 namespace {
 
 thread_local std::string g_last_error;
+
+// ghost planes on each side of the owned planes: the two-step (temporal blocking) pass of a
+// slab reads W^s two planes beyond its owned range
+constexpr int GH = WHB_GHOST_PLANES;
 
 int fail(int code, const std::string &msg) {
     g_last_error = msg;
@@ -68,7 +72,7 @@ struct Geom {
     int P;            // row pitch (elements)
     int n1, n2;       // extents of storage axes 1 and 2 (incl. boundary)
     int j_lo, j_hi;   // update range on axis 1 ([0,1) when axis 1 is degenerate)
-    int i_lo, i_hi;   // local update planes on axis 0 (global interior, owned)
+    int i_lo, i_hi;   // local planes that are global-interior on axis 0 (owned or ghost)
     int use_c2;
     double clo0, cmid0, clo1, cmid1, clo2, cmid2, c2;
 };
@@ -343,7 +347,7 @@ struct GeomG {
     int per[3];        // periodic axis
     int order;         // 2 or 4
     int use_c2;
-    int plane_begin;   // global index of local plane 1
+    int plane_begin;   // global index of local plane GH
     double taps[3][5];
     double c2;
 };
@@ -410,7 +414,7 @@ __global__ void step_general_kernel(GeomG g, const Member *__restrict__ members,
         const int k = (int)(r - (long long)j * n2);
         const int gi = g.plane_begin + (int)pl;
         if (!general_updates(g, gi, j, k)) continue;
-        const long long p = (pl + 1) * g.S0 + (long long)j * g.P + k;
+        const long long p = (pl + GH) * g.S0 + (long long)j * g.P + k;
         const double wc = wcur[p];
         const double lap = general_lap(g, wcur, p, gi, j, k);
         double wn;
@@ -456,7 +460,7 @@ __global__ void apply_general_kernel(GeomG g, const double *__restrict__ x, doub
         const int k = (int)(r - (long long)j * n2);
         const int gi = g.plane_begin + (int)pl;
         if (!general_updates(g, gi, j, k)) continue;
-        const long long p = (pl + 1) * g.S0 + (long long)j * g.P + k;
+        const long long p = (pl + GH) * g.S0 + (long long)j * g.P + k;
         const int h = g.order / 2;
         double lap = 0.0;
         for (int a = 0; a < 3; ++a) {
@@ -572,7 +576,7 @@ struct whb_ctx {
     int64_t gshape[3] = {1, 1, 1};  // global storage shape (axis-0, axis-1, axis-2)
     int64_t plane_begin = 0, plane_end = 1;
     int64_t nloc = 1;               // owned planes
-    int64_t nplanes = 3;            // allocated planes (owned + 2 ghosts)
+    int64_t nplanes = 1 + 2 * GH;   // allocated planes (owned + 2 x GH ghosts)
     int P = 16;
     int64_t S0 = 16;
     int64_t field_elems = 0;        // nplanes * S0
@@ -598,7 +602,7 @@ struct whb_ctx {
     size_t smem = 0;                // dynamic smem of the bulk kernel
     int64_t slack_front = 0, slack_back = 0;  // allocation slack around every field (bulk halo reads)
     int BX = 128, BY = 1, gx = 1, JT = 1, chunk_len = 1, nchunks = 1;
-    int upd_lo = 1, upd_hi = 2;     // local update planes [lo, hi)
+    int upd_lo = GH, upd_hi = GH + 1;  // local update planes [lo, hi)
     // two-step (temporal blocking) plan: whole-grid 2D/3D contexts
     bool tb2 = false;
     size_t smem2 = 0;
@@ -683,8 +687,9 @@ double *vec_ptr(whb_ctx *c, int id) {
     return nullptr;
 }
 
-// owned region [plane 1, plane nloc+1) of a field, as a flat element range
-inline double *owned(double *base, whb_ctx *c) { return base + c->S0; }
+// owned region [plane GH, plane nloc+GH) of a field, as a flat element range
+inline double *owned(double *base, whb_ctx *c) { return base + GH * c->S0; }
+inline const double *owned(const double *base, whb_ctx *c) { return base + GH * c->S0; }
 inline long long owned_elems(whb_ctx *c) { return (long long)c->nloc * c->S0; }
 
 // Bulk-kernel tile configurations: 3D 8 x 64 tiles, 6 stages (17.7 KB each,
@@ -858,11 +863,11 @@ int plan_launch(whb_ctx *c) {
     if (c->act0) {
         const int64_t g_lo = std::max<int64_t>(c->plane_begin, 1);
         const int64_t g_hi = std::min<int64_t>(c->plane_end, c->gshape[0] - 1);
-        c->upd_lo = (int)(g_lo - c->plane_begin + 1);
-        c->upd_hi = (int)std::max<int64_t>(g_hi - c->plane_begin + 1, c->upd_lo);
+        c->upd_lo = (int)(g_lo - c->plane_begin + GH);
+        c->upd_hi = (int)std::max<int64_t>(g_hi - c->plane_begin + GH, c->upd_lo);
     } else {
-        c->upd_lo = 1;
-        c->upd_hi = 2;
+        c->upd_lo = GH;
+        c->upd_hi = GH + 1;
     }
     const int nplanes = std::max(1, c->upd_hi - c->upd_lo);
     const int per_sm = occupancy_blocks(c);
@@ -892,13 +897,15 @@ int plan_launch(whb_ctx *c) {
     c->nparts = c->gx * c->JT * (c->nchunks + 2);
     // two-step plan: single-domain 2D/3D contexts (a slab needs 2 ghost planes per exchange)
     const char *tenv = getenv("WHB_TB2");
-    c->tb2 = c->kern >= 1 && c->plane_begin == 0 && c->plane_end == c->gshape[0] &&
-             !(tenv && std::string(tenv) == "0") && (!c->act1 || c->kern == 2);
+    // (slabs too: GH = 2 ghost planes per side feed the pass)
+    const bool whole = c->plane_begin == 0 && c->plane_end == c->gshape[0];
+    c->tb2 = c->kern >= 1 && c->act0 && !(tenv && std::string(tenv) == "0") && (!c->act1 || c->kern == 2) &&
+             c->upd_hi - c->upd_lo >= 1;
     const char *wenv3 = getenv("WHB_TB2W");
-    c->tb2w = c->tb2 && c->act1 && (wenv3 && std::string(wenv3) == "1");
+    c->tb2w = c->tb2 && whole && c->act1 && (wenv3 && std::string(wenv3) == "1");
     const char *renv = getenv("WHB_TB2R");
     // measured on 257^3 / 1025^3: 126.5 / 131.0 Gpts/s vs 143.7 / 149.3 for tb2 -> opt-in (WHB_TB2R=1)
-    c->tb2r = c->tb2 && c->act1 && !c->tb2w && (renv && std::string(renv) == "1");
+    c->tb2r = c->tb2 && whole && c->act1 && !c->tb2w && (renv && std::string(renv) == "1");
     if (c->tb2w) {
         c->smem2 = tb2w::smem_bytes<W3_BY, W3_ST>();
         cudaError_t e = tb2w_set_attrs(c->smem2);
@@ -964,7 +971,7 @@ int plan_launch(whb_ctx *c) {
     }
     // 2D wavefront plan (default for whole-grid 2D contexts; WHB_WF=0 disables, WHB_WF=2 picks T = 2)
     const char *wenv = getenv("WHB_WF");
-    c->wfT = (c->tb2 && !c->act1 && !(wenv && std::string(wenv) == "0")) ? ((wenv && std::string(wenv) == "2") ? 2 : 4) : 0;
+    c->wfT = (c->tb2 && whole && !c->act1 && !(wenv && std::string(wenv) == "0")) ? ((wenv && std::string(wenv) == "2") ? 2 : 4) : 0;
     if (c->wfT) {
         for (int T : {2, 4}) {
             if (T > c->wfT) continue;
@@ -1184,19 +1191,19 @@ int launch_step_range(whb_ctx *c, int s, int moff, int cnt) {
 }
 
 template <bool A1, int K1, int K2, bool ZF>
-void launch_tb2(whb_ctx *c, dim3 grid, int off, int s, int ib, int ie, const StepMaps &mp) {
+void launch_tb2(whb_ctx *c, dim3 grid, int off, int s, int ib, int ie, int cl, int po, const StepMaps &mp) {
     constexpr int threads = A1 ? T3_TX * T3_BY / 2 : T2_TX * T2_BY / 2;
     tb2_fn<A1, K1, K2, ZF>()<<<grid, threads, c->smem2, c->stream>>>(c->geom, c->d_members, off, s, ib, ie,
-                                                                    c->chunk2, c->JT2, 0, mp.w, mp.p, mp.f, mp.a);
+                                                                    cl, c->JT2, po, mp.w, mp.p, mp.f, mp.a);
 }
 
 template <bool A1>
-void launch_tb2_kinds(whb_ctx *c, int k1, int k2, bool zf, dim3 grid, int off, int s, int ib, int ie,
-                      const StepMaps &mp) {
+void launch_tb2_kinds(whb_ctx *c, int k1, int k2, bool zf, dim3 grid, int off, int s, int ib, int ie, int cl,
+                      int po, const StepMaps &mp) {
 #define WHB_TB2_CASE(K1, K2)                                                         \
     if (k1 == K1 && k2 == K2) {                                                      \
-        if (zf) launch_tb2<A1, K1, K2, true>(c, grid, off, s, ib, ie, mp);          \
-        else launch_tb2<A1, K1, K2, false>(c, grid, off, s, ib, ie, mp);            \
+        if (zf) launch_tb2<A1, K1, K2, true>(c, grid, off, s, ib, ie, cl, po, mp);  \
+        else launch_tb2<A1, K1, K2, false>(c, grid, off, s, ib, ie, cl, po, mp);    \
         return;                                                                      \
     }
     WHB_TB2_CASE(K_FIRST, K_MID)
@@ -1248,9 +1255,12 @@ void launch_tb2w_kinds(whb_ctx *c, int k1, int k2, bool zf, dim3 grid, int off, 
 #undef WHB_TB2W_CASE
 }
 
-// Fused steps (s, s+1), s even, for the table members [0, nact): those still running
-// after s+1 get (K1, MID), those finishing at s+1 get (K1, LAST).
-int launch_pair(whb_ctx *c, int s) {
+// Fused steps (s, s+1) over update planes [ib, ie) in chunks of cl planes (partial slots from
+// po), for the table members [0, nact): those still running after s+1 get (K1, MID), those
+// finishing at s+1 get (K1, LAST).
+int launch_pair_range(whb_ctx *c, int s, int ib, int ie, int cl, int po) {
+    if (ib >= ie) return 0;
+    const int nch = (ie - ib + cl - 1) / cl;
     int n_cont = 0, n_last = 0;
     for (int pos = 0; pos < c->nbatch; ++pos) {
         const int N = c->mem[c->order[pos]].n_total;
@@ -1279,19 +1289,19 @@ int launch_pair(whb_ctx *c, int s) {
     const int k1 = (s == 0) ? K_FIRST : K_MID;
     auto go = [&](int k2, int off, int cnt) {
         if (cnt <= 0) return;
-        dim3 grid(c->gx2, c->JT2 * c->nch2, cnt);
-        if (c->tb2w) {
-            launch_tb2w_kinds(c, k1, k2, zf, grid, off, s, c->upd_lo, c->upd_hi, mp);
+        dim3 grid(c->gx2, c->JT2 * nch, cnt);
+        if (c->tb2w) {  // whole-grid variants (fixed plan chunking)
+            launch_tb2w_kinds(c, k1, k2, zf, grid, off, s, ib, ie, mp);
             c->launches++;
             return;
         }
         if (c->tb2r) {
-            launch_tb2r_kinds(c, k1, k2, zf, grid, off, s, c->upd_lo, c->upd_hi, mp);
+            launch_tb2r_kinds(c, k1, k2, zf, grid, off, s, ib, ie, mp);
             c->launches++;
             return;
         }
-        if (c->act1) launch_tb2_kinds<true>(c, k1, k2, zf, grid, off, s, c->upd_lo, c->upd_hi, mp);
-        else launch_tb2_kinds<false>(c, k1, k2, zf, grid, off, s, c->upd_lo, c->upd_hi, mp);
+        if (c->act1) launch_tb2_kinds<true>(c, k1, k2, zf, grid, off, s, ib, ie, cl, po, mp);
+        else launch_tb2_kinds<false>(c, k1, k2, zf, grid, off, s, ib, ie, cl, po, mp);
         c->launches++;
     };
     go(K_MID, 0, n_cont);
@@ -1299,6 +1309,8 @@ int launch_pair(whb_ctx *c, int s) {
     WHB_CUDA(cudaGetLastError());
     return 0;
 }
+
+int launch_pair(whb_ctx *c, int s) { return launch_pair_range(c, s, c->upd_lo, c->upd_hi, c->chunk2, 0); }
 
 int max_steps(whb_ctx *c);
 
@@ -1532,13 +1544,13 @@ int copy_field_h2d(whb_ctx *c, double *dev, const double *host) {
         WHB_TRY(ensure_stage(c));
         WHB_CUDA(cudaMemcpyAsync(c->stage, host, rows * c->gshape[2] * sizeof(double), cudaMemcpyHostToDevice,
                                  c->stream));
-        repitch_kernel<<<1184, 256, 0, c->stream>>>(c->stage, (int)c->gshape[2], dev + c->S0, c->P,
+        repitch_kernel<<<1184, 256, 0, c->stream>>>(c->stage, (int)c->gshape[2], owned(dev, c), c->P,
                                                     (long long)rows, 1);
         c->launches++;
         WHB_CUDA(cudaGetLastError());
         return 0;
     }
-    WHB_CUDA(cudaMemcpy2DAsync(dev + c->S0, (size_t)c->P * sizeof(double), host,
+    WHB_CUDA(cudaMemcpy2DAsync(owned(dev, c), (size_t)c->P * sizeof(double), host,
                                (size_t)c->gshape[2] * sizeof(double), (size_t)c->gshape[2] * sizeof(double),
                                rows, cudaMemcpyHostToDevice, c->stream));
     return 0;
@@ -1548,7 +1560,7 @@ int copy_field_d2h(whb_ctx *c, const double *dev, double *host) {
     const size_t rows = (size_t)c->nloc * c->gshape[1];
     if (staged(c)) {
         WHB_TRY(ensure_stage(c));
-        repitch_kernel<<<1184, 256, 0, c->stream>>>(c->stage, (int)c->gshape[2], const_cast<double *>(dev) + c->S0,
+        repitch_kernel<<<1184, 256, 0, c->stream>>>(c->stage, (int)c->gshape[2], owned(const_cast<double *>(dev), c),
                                                     c->P, (long long)rows, 0);
         c->launches++;
         WHB_CUDA(cudaGetLastError());
@@ -1556,7 +1568,7 @@ int copy_field_d2h(whb_ctx *c, const double *dev, double *host) {
                                  c->stream));
         return 0;
     }
-    WHB_CUDA(cudaMemcpy2DAsync(host, (size_t)c->gshape[2] * sizeof(double), dev + c->S0,
+    WHB_CUDA(cudaMemcpy2DAsync(host, (size_t)c->gshape[2] * sizeof(double), owned(dev, c),
                                (size_t)c->P * sizeof(double), (size_t)c->gshape[2] * sizeof(double), rows,
                                cudaMemcpyDeviceToHost, c->stream));
     return 0;
@@ -1568,7 +1580,7 @@ int zero_bnd(whb_ctx *c, double *x) {
     const int zlo = (c->act0 && !per0 && c->plane_begin == 0) ? 1 : 0;
     const int zhi = (c->act0 && !per0 && c->plane_end == c->gshape[0]) ? 1 : 0;
     zero_boundary_kernel<<<592, 256, 0, c->stream>>>(x, c->S0, c->P, (int)c->gshape[1], (int)c->gshape[2],
-                                                     c->act1, 1, (int)c->nloc + 1, zlo, zhi,
+                                                     c->act1, GH, (int)c->nloc + GH, zlo, zhi,
                                                      gen ? c->geomg.per[1] : 0, gen ? c->geomg.per[2] : 0);
     c->launches++;
     WHB_CUDA(cudaGetLastError());
@@ -1576,7 +1588,7 @@ int zero_bnd(whb_ctx *c, double *x) {
 }
 
 int vec_reduce_dot(whb_ctx *c, const double *x, const double *y, double *out) {
-    dot_partials_kernel<<<kRedBlocks, kRedThreads, 0, c->stream>>>(x + c->S0, y + c->S0, owned_elems(c), c->d_red);
+    dot_partials_kernel<<<kRedBlocks, kRedThreads, 0, c->stream>>>(owned(x, c), owned(y, c), owned_elems(c), c->d_red);
     final_sum_kernel<<<1, 1024, 0, c->stream>>>(c->d_red, kRedBlocks, c->d_red + kRedBlocks);
     c->launches += 2;
     WHB_CUDA(cudaGetLastError());
@@ -1648,7 +1660,7 @@ int whb_create(whb_ctx **out, int device, int ndim, const int64_t *shape, int64_
     c->plane_begin = plane_begin;
     c->plane_end = plane_end;
     c->nloc = plane_end - plane_begin;
-    c->nplanes = c->nloc + 2;
+    c->nplanes = c->nloc + 2 * GH;
     c->P = (int)((c->gshape[2] + 15) / 16 * 16);
     c->S0 = (int64_t)c->P * c->gshape[1];
     c->field_elems = c->nplanes * c->S0;
@@ -1730,8 +1742,15 @@ int whb_set_operator(whb_ctx *c, const double *clo, const double *cmid, double c
     g.n2 = (int)c->gshape[2];
     g.j_lo = c->act1 ? 1 : 0;
     g.j_hi = c->act1 ? (int)c->gshape[1] - 1 : 1;
-    g.i_lo = c->upd_lo;
-    g.i_hi = c->upd_hi;
+    // global-interior planes [1, n0-1) in local indices, clipped to the allocation: the two-step
+    // pass of a slab computes W^{s+1} on one ghost plane per side (zero where it is global boundary)
+    if (c->act0) {
+        g.i_lo = (int)std::max<int64_t>(0, 1 - c->plane_begin + GH);
+        g.i_hi = (int)std::min<int64_t>(c->nplanes, c->gshape[0] - 1 - c->plane_begin + GH);
+    } else {
+        g.i_lo = c->upd_lo;
+        g.i_hi = c->upd_hi;
+    }
     g.c2 = c2;
     g.use_c2 = (c2 != 1.0);  // x*1.0 == x exactly: skipping keeps bitwise parity
     // map reference axes onto storage axes: 3D (0,1,2); 2D (0,-,2); 1D (-,-,2)
@@ -1780,6 +1799,7 @@ int whb_set_operator_general(whb_ctx *c, int order, const int *periodic, const d
     c->kern = 3;
     c->tb2 = false;
     c->tb2r = false;
+    c->tb2w = false;
     c->wfT = 0;
     for (auto &kv : c->graphs) cudaGraphExecDestroy(kv.second);
     c->graphs.clear();
@@ -2120,6 +2140,59 @@ int whb_step(whb_ctx *c, int s, int region) {
     return 0;
 }
 
+int whb_pair(whb_ctx *c, int s, int region) {
+    if (!c || c->cur_mode < 0) return fail(WHB_E_STATE, "whb_pair outside whb_solve_begin/end");
+    if (!c->tb2 || c->wfT || c->tb2r || c->tb2w) return fail(WHB_E_STATE, "context has no two-step plan (whb_plan)");
+    if (s < 0 || s + 1 >= c->mem[0].n_total) return fail(WHB_E_ARG, "steps (s, s+1) out of range");
+    WHB_TRY(set_dev(c));
+    const int lo = c->upd_lo, hi = c->upd_hi;
+    const bool last = s + 2 == c->mem[0].n_total;
+    if (region == 0) {
+        WHB_TRY(launch_pair_range(c, s, lo, hi, c->chunk2, 0));
+        if (last) c->cur_parts = c->gx2 * c->JT2 * c->nch2;
+    } else if (region == 1) {
+        if (last) return fail(WHB_E_ARG, "the last pass runs as region 0 (nothing needs its halo)");
+        // the two first and two last update planes: W^{s+2} there feeds the neighbours' 2 ghost planes
+        if (hi - lo <= 4) {
+            WHB_TRY(launch_pair_range(c, s, lo, hi, hi - lo, 0));
+        } else {
+            WHB_TRY(launch_pair_range(c, s, lo, lo + 2, 2, 0));
+            WHB_TRY(launch_pair_range(c, s, hi - 2, hi, 2, 0));
+        }
+    } else if (region == 2) {
+        if (last) return fail(WHB_E_ARG, "the last pass runs as region 0 (nothing needs its halo)");
+        if (hi - lo > 4) {
+            const int n = hi - lo - 4;
+            const int cl = std::min(n, c->chunk2);
+            WHB_TRY(launch_pair_range(c, s, lo + 2, hi - 2, cl, 0));
+        }
+    } else
+        return fail(WHB_E_ARG, "region must be 0, 1 or 2");
+    return 0;
+}
+
+int whb_ghost_planes(whb_ctx *c, int *ghost) {
+    if (!c || !ghost) return fail(WHB_E_ARG, "NULL argument");
+    *ghost = GH;
+    return 0;
+}
+
+int whb_field_plane_ptr(whb_ctx *c, int field, int member, int64_t plane, uint64_t *dev_ptr, int64_t *plane_elems) {
+    if (!c || !dev_ptr) return fail(WHB_E_ARG, "NULL argument");
+    if (member < 0 || member >= c->nbatch) return fail(WHB_E_ARG, "member out of range");
+    if (plane < 0 || plane >= c->nplanes) return fail(WHB_E_ARG, "plane out of range");
+    double *base = field_ptr(c, field, member);
+    if (field == WHB_OUT) {
+        WHB_TRY(set_dev(c));
+        WHB_TRY(ensure_out(c, member));
+        base = c->mem[member].out;
+    }
+    if (!base) return fail(WHB_E_ARG, "unknown field");
+    *dev_ptr = (uint64_t)(uintptr_t)(base + plane * c->S0);
+    if (plane_elems) *plane_elems = c->S0;
+    return 0;
+}
+
 int whb_solve_end(whb_ctx *c, double *resid_sq) {
     if (!c || c->cur_mode < 0) return fail(WHB_E_STATE, "whb_solve_end without whb_solve_begin");
     WHB_TRY(set_dev(c));
@@ -2160,12 +2233,9 @@ int whb_synchronize(whb_ctx *c) {
     return 0;
 }
 
-int whb_copy_plane(whb_ctx *src, int src_level, int64_t src_plane, whb_ctx *dst, int dst_level, int64_t dst_plane) {
-    if (!src || !dst) return fail(WHB_E_ARG, "NULL argument");
-    if (src->S0 != dst->S0) return fail(WHB_E_ARG, "plane geometry mismatch");
-    uint64_t sp = 0, dp = 0;
-    WHB_TRY(whb_level_plane_ptr(src, src_level, src_plane, &sp, nullptr));
-    WHB_TRY(whb_level_plane_ptr(dst, dst_level, dst_plane, &dp, nullptr));
+int whb_copy_device(whb_ctx *src, uint64_t src_ptr, whb_ctx *dst, uint64_t dst_ptr, int64_t bytes) {
+    if (!src || !dst || !src_ptr || !dst_ptr) return fail(WHB_E_ARG, "NULL argument");
+    if (bytes <= 0) return 0;
     cudaEvent_t e1, e2;
     WHB_TRY(set_dev(src));
     WHB_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
@@ -2173,14 +2243,23 @@ int whb_copy_plane(whb_ctx *src, int src_level, int64_t src_plane, whb_ctx *dst,
     WHB_TRY(set_dev(dst));
     WHB_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
     WHB_CUDA(cudaStreamWaitEvent(dst->stream, e1, 0));
-    WHB_CUDA(cudaMemcpyPeerAsync((void *)(uintptr_t)dp, dst->device, (const void *)(uintptr_t)sp, src->device,
-                                 (size_t)src->S0 * sizeof(double), dst->stream));
+    WHB_CUDA(cudaMemcpyPeerAsync((void *)(uintptr_t)dst_ptr, dst->device, (const void *)(uintptr_t)src_ptr,
+                                 src->device, (size_t)bytes, dst->stream));
     WHB_CUDA(cudaEventRecord(e2, dst->stream));
     WHB_TRY(set_dev(src));
     WHB_CUDA(cudaStreamWaitEvent(src->stream, e2, 0));
     cudaEventDestroy(e1);
     cudaEventDestroy(e2);
     return 0;
+}
+
+int whb_copy_plane(whb_ctx *src, int src_level, int64_t src_plane, whb_ctx *dst, int dst_level, int64_t dst_plane) {
+    if (!src || !dst) return fail(WHB_E_ARG, "NULL argument");
+    if (src->S0 != dst->S0) return fail(WHB_E_ARG, "plane geometry mismatch");
+    uint64_t sp = 0, dp = 0;
+    WHB_TRY(whb_level_plane_ptr(src, src_level, src_plane, &sp, nullptr));
+    WHB_TRY(whb_level_plane_ptr(dst, dst_level, dst_plane, &dp, nullptr));
+    return whb_copy_device(src, sp, dst, dp, src->S0 * (int64_t)sizeof(double));
 }
 
 int whb_launch_count(whb_ctx *c, int64_t *count) {

@@ -1,26 +1,30 @@
 """Slab (axis-0) domain decomposition of the explicit WaveHoltz iteration across
 GPUs — SURVEY §8(e).
 
-The stencil radius is 1, so every leapfrog step needs exactly one ghost plane
-of W^n from each neighbour; W^{n-1}, f and the accumulator are purely local.
 Each rank owns a contiguous range of axis-0 planes (``slab_ranges``) in one
 whb context (include/whb200.h: plane_begin/plane_end) whose allocation carries
-one ghost plane on each side.  Per leapfrog step s:
+G = 2 ghost planes on each side.  The stencil radius is 1, so a single
+leapfrog step needs one ghost plane of W^s; the two-step pass the 2D/3D
+kernels run (temporal blocking, steps s and s+1 per HBM sweep) needs two
+planes of W^s and one of W^{s-1} and f.  Per pass (s, s+1):
 
-    1. compute the first and last owned planes of W^{s+1}      (whb_step region 1)
-    2. post the halo exchange of those planes                    (NCCL send/recv)
-    3. compute the remaining interior planes                     (whb_step region 2)
-    4. join the exchange before step s+1                         (stream wait)
+    1. compute the two first and two last owned update planes   (whb_pair region 1)
+    2. post the exchange of W^{s+2} (2 planes) and W^{s+1} (1 plane) per side
+    3. compute the remaining interior planes                     (whb_pair region 2)
+    4. join the exchange before the next pass                    (stream wait)
 
-so the transfer of 2 x (n1 x n2 x 8 B) per step overlaps the interior update.
-Per pass the residual sum of squares is all-reduced (one fp64).
+so the halo traffic, 3 x (n1 x n2 x 8 B) per side per TWO steps, overlaps the
+interior update; the one-step schedule (``whb_step`` regions, one plane of
+W^{s+1} per side per step) is used when the context plans one step per pass
+(general operator, 1D).  f is exchanged once (it is static).  Per FPI pass the
+residual sum of squares is all-reduced (one fp64).
 
 The exchange goes through ``torch.distributed`` (NCCL on GPUs, gloo on CPUs)
 on the context's own CUDA stream (``torch.cuda.ExternalStream``); device
-buffers are wrapped zero-copy through ``__cuda_array_interface__``.  The
-in-process ``LocalHalo`` runs several slabs in one process (one GPU or
-several) with device-to-device plane copies, which is how the multi-slab
-kernels are checked on a single GPU.
+buffers are wrapped zero-copy through ``__cuda_array_interface__`` (a halo of
+several planes is one contiguous message).  The in-process ``LocalHalo`` runs
+several slabs in one process (one GPU or several) with device-to-device
+copies, which is how the multi-slab kernels are checked on a single GPU.
 """
 
 from __future__ import annotations
@@ -35,7 +39,8 @@ from .filters import mode_name
 from .grid import operator_coefficients
 from .timestep import time_schedule
 
-__all__ = ["slab_ranges", "DeviceShard", "TorchHalo", "LocalHalo", "SlabFPI", "run_filtered_solve"]
+__all__ = ["slab_ranges", "DeviceShard", "TorchHalo", "LocalHalo", "SlabFPI", "run_filtered_solve",
+           "run_local_solve", "halo_items"]
 
 
 def slab_ranges(n0: int, nranks: int):
@@ -59,6 +64,31 @@ class _CudaArray:
                                          "strides": None, "version": 3}
 
 
+def level(L: int):
+    """Halo item naming time level L (level 0 = V)."""
+    return ("level", int(L))
+
+
+def field(fid: int):
+    """Halo item naming a field slot (e.g. _native.F)."""
+    return ("field", int(fid))
+
+
+def halo_planes(shard, side: str, depth: int):
+    """(send_first, recv_first) local plane indices of a depth-plane halo on one side."""
+    g, n = shard.gh, shard.nloc
+    if side == "lo":
+        return g, g - depth
+    return g + n - depth, g + n
+
+
+def halo_items(s: int, two_step: bool):
+    """What the next step/pass needs from the neighbours after step s (one-step) or pass (s, s+1)."""
+    if two_step:
+        return [(level(s + 2), 2), (level(s + 1), 1)]
+    return [(level(s + 1), 1)]
+
+
 class DeviceShard:
     """One rank's slab on its GPU: a whb context owning planes [p0, p1)."""
 
@@ -69,6 +99,8 @@ class DeviceShard:
         self.ctx = _native.Context(grid.shape, device=device, plane_range=plane_range)
         self.ctx.set_operator(clo, cmid, c2)
         self.nloc = self.plane_range[1] - self.plane_range[0]
+        self.gh = self.ctx.ghost_planes()
+        self.steps_per_pass = self.ctx.plan()[1]
         self.device = device
 
     # schedule / fields
@@ -92,15 +124,25 @@ class DeviceShard:
     def step(self, s, region):
         self.ctx.step(s, region)
 
+    def pair(self, s, region):
+        self.ctx.pair(s, region)
+
     def solve_end(self) -> float:
         return self.ctx.solve_end()
 
     # halo plumbing
-    def plane_tensor(self, level, plane):
+    def plane_ptr(self, item, plane):
+        kind, ident = item
+        if kind == "level":
+            return self.ctx.level_plane_ptr(ident, plane)
+        return self.ctx.field_plane_ptr(ident, plane)
+
+    def planes(self, item, first, count):
+        """Zero-copy torch view of `count` consecutive local planes of a level/field."""
         import torch
 
-        ptr, n = self.ctx.level_plane_ptr(level, plane)
-        return torch.as_tensor(_CudaArray(ptr, n), device=f"cuda:{self.device}")
+        ptr, n = self.plane_ptr(item, first)
+        return torch.as_tensor(_CudaArray(ptr, n * count), device=f"cuda:{self.device}")
 
     def stream(self):
         import torch
@@ -123,16 +165,20 @@ class TorchHalo:
     def nranks(self):
         return self.world
 
-    def start(self, shard, level):
+    def start(self, shard, items):
+        """Post the exchange of [(item, depth), ...]; every rank passes the same list."""
         d = self.dist
         ops = []
         with shard.stream():
-            if self.rank > 0:
-                ops.append(d.P2POp(d.isend, shard.plane_tensor(level, 1), self.rank - 1))
-                ops.append(d.P2POp(d.irecv, shard.plane_tensor(level, 0), self.rank - 1))
-            if self.rank < self.world - 1:
-                ops.append(d.P2POp(d.isend, shard.plane_tensor(level, shard.nloc), self.rank + 1))
-                ops.append(d.P2POp(d.irecv, shard.plane_tensor(level, shard.nloc + 1), self.rank + 1))
+            for item, depth in items:
+                if self.rank > 0:
+                    snd, rcv = halo_planes(shard, "lo", depth)
+                    ops.append(d.P2POp(d.isend, shard.planes(item, snd, depth), self.rank - 1))
+                    ops.append(d.P2POp(d.irecv, shard.planes(item, rcv, depth), self.rank - 1))
+                if self.rank < self.world - 1:
+                    snd, rcv = halo_planes(shard, "hi", depth)
+                    ops.append(d.P2POp(d.isend, shard.planes(item, snd, depth), self.rank + 1))
+                    ops.append(d.P2POp(d.irecv, shard.planes(item, rcv, depth), self.rank + 1))
             works = d.batch_isend_irecv(ops) if ops else []
         return shard, works
 
@@ -161,39 +207,82 @@ class LocalHalo:
     def nranks(self):
         return len(self.shards)
 
-    def exchange(self, level):
+    def exchange(self, items):
         sh = self.shards
-        for r in range(len(sh) - 1):
-            lo, hi = sh[r], sh[r + 1]
-            lo.ctx.copy_plane_to(level, lo.nloc, hi.ctx, level, 0)
-            hi.ctx.copy_plane_to(level, 1, lo.ctx, level, lo.nloc + 1)
+        for item, depth in items:
+            for r in range(len(sh) - 1):
+                lo, hi = sh[r], sh[r + 1]
+                nbytes = depth * lo.plane_ptr(item, 0)[1] * 8
+                lo_send, lo_recv = halo_planes(lo, "hi", depth)
+                hi_send, hi_recv = halo_planes(hi, "lo", depth)
+                lo.ctx.copy_device_to(lo.plane_ptr(item, lo_send)[0], hi.ctx, hi.plane_ptr(item, hi_recv)[0], nbytes)
+                hi.ctx.copy_device_to(hi.plane_ptr(item, hi_send)[0], lo.ctx, lo.plane_ptr(item, lo_recv)[0], nbytes)
+
+
+def _exchange_now(halo, shard, items):
+    if halo.nranks > 1:
+        halo.finish(halo.start(shard, items))
 
 
 def run_filtered_solve(shard, halo, out_mode=_native.OUT_FPI, zero_forcing=False) -> float:
-    """One W(v, f) pass of a slab with halo exchange (the step schedule above).
+    """One W(v, f) pass of a slab with halo exchange (the schedules above).
     Returns this rank's residual sum of squares (FPI mode)."""
     shard.solve_begin(out_mode, zero_forcing)
-    if halo.nranks > 1:
-        halo.finish(halo.start(shard, 0))  # ghost planes of W^0 = v
+    multi = halo.nranks > 1
     n_total = shard.n_total
+    if shard.steps_per_pass == 2:
+        _exchange_now(halo, shard, [(level(0), 2)])  # two ghost planes of W^0 = v
+        s = 0
+        while s + 1 < n_total:
+            if not multi or s + 2 == n_total:
+                shard.pair(s, 0)  # the last pass writes the output; no later step needs its halo
+            else:
+                shard.pair(s, 1)
+                h = halo.start(shard, halo_items(s, True))
+                shard.pair(s, 2)
+                halo.finish(h)
+            s += 2
+        if s < n_total:  # odd step count: the last step alone (its W^s ghosts came with the last pass)
+            shard.step(s, 0)
+        return shard.solve_end()
+    _exchange_now(halo, shard, [(level(0), 1)])  # ghost plane of W^0 = v
     for s in range(n_total):
-        if halo.nranks == 1 or s == n_total - 1:
-            shard.step(s, 0)  # the last step writes the output; no later step needs its halo
+        if not multi or s == n_total - 1:
+            shard.step(s, 0)
             continue
         shard.step(s, 1)
-        h = halo.start(shard, s + 1)
+        h = halo.start(shard, halo_items(s, False))
         shard.step(s, 2)
         halo.finish(h)
     return shard.solve_end()
 
 
 def run_local_solve(shards, halo: LocalHalo, out_mode=_native.OUT_FPI, zero_forcing=False):
-    """The same schedule for in-process slabs (each step: boundary planes of every slab,
-    plane copies, interior planes)."""
+    """The same schedules for in-process slabs (each step/pass: boundary planes of every
+    slab, plane copies, interior planes)."""
     for sh in shards:
         sh.solve_begin(out_mode, zero_forcing)
-    halo.exchange(0)
     n_total = shards[0].n_total
+    two = all(sh.steps_per_pass == 2 for sh in shards)
+    if two:
+        halo.exchange([(level(0), 2)])
+        s = 0
+        while s + 1 < n_total:
+            if s + 2 == n_total:
+                for sh in shards:
+                    sh.pair(s, 0)
+            else:
+                for sh in shards:
+                    sh.pair(s, 1)
+                halo.exchange(halo_items(s, True))
+                for sh in shards:
+                    sh.pair(s, 2)
+            s += 2
+        if s < n_total:
+            for sh in shards:
+                sh.step(s, 0)
+        return [sh.solve_end() for sh in shards]
+    halo.exchange([(level(0), 1)])
     for s in range(n_total):
         if s == n_total - 1:
             for sh in shards:
@@ -201,10 +290,18 @@ def run_local_solve(shards, halo: LocalHalo, out_mode=_native.OUT_FPI, zero_forc
             continue
         for sh in shards:
             sh.step(s, 1)
-        halo.exchange(s + 1)
+        halo.exchange(halo_items(s, False))
         for sh in shards:
             sh.step(s, 2)
     return [sh.solve_end() for sh in shards]
+
+
+def exchange_forcing(shards_or_shard, halo):
+    """f is read one plane beyond the owned range by the two-step pass: exchange it once."""
+    if isinstance(halo, LocalHalo):
+        halo.exchange([(field(_native.F), 1)])
+    else:
+        _exchange_now(halo, shards_or_shard, [(field(_native.F), 1)])
 
 
 class SlabFPI:
@@ -225,7 +322,10 @@ class SlabFPI:
         fv = np.asarray(forcing.values if hasattr(forcing, "values") else forcing, dtype=float)
         if fv.shape[0] == self.grid.shape[0] and fv.shape[0] != p1 - p0:
             fv = fv[p0:p1]
+        if min(b - a for a, b in slab_ranges(self.grid.shape[0], halo.nranks)) < 2:
+            raise ValueError("every slab needs at least 2 owned planes")
         shard.upload(_native.F, np.ascontiguousarray(fv))
+        exchange_forcing(shard, halo)
         self.reset()
 
     def reset(self):

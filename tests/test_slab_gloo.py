@@ -23,27 +23,35 @@ from oracle import waveholtz_oracle as O
 
 
 class NumpyShard:
-    """Test double with DeviceShard's interface; arithmetic in reference order
-    (the same restatement as oracle/waveholtz_oracle.py, per plane)."""
+    """Test double with DeviceShard's interface: the same plane layout (G = 2
+    ghost planes per side, time level L >= 1 in ring slot L mod 4) and the
+    same one-step / two-step region semantics as the device contexts
+    (include/whb200.h whb_step / whb_pair); arithmetic in reference order
+    (the restatement of oracle/waveholtz_oracle.py, per plane)."""
 
-    def __init__(self, grid, plane_range, c=1.0):
+    gh = 2
+
+    def __init__(self, grid, plane_range, c=1.0, steps_per_pass=2):
         self.grid = grid
         self.plane_range = tuple(plane_range)
         self.nloc = plane_range[1] - plane_range[0]
+        self.steps_per_pass = steps_per_pass
         self.clo, self.cmid, self.c2 = operator_coefficients(grid, 2, c)
-        shp = (self.nloc + 2,) + tuple(grid.shape[1:])
-        self.buf = {k: np.zeros(shp) for k in ("v", "f", "wa", "wb", "acc")}
+        shp = (self.nloc + 2 * self.gh,) + tuple(grid.shape[1:])
+        self.buf = {k: np.zeros(shp) for k in ("v", "f", "acc", 0, 1, 2, 3)}
         self.device = 0
-        n0 = grid.shape[0]
+        n0, g, p0 = grid.shape[0], self.gh, plane_range[0]
         g_lo, g_hi = max(plane_range[0], 1), min(plane_range[1], n0 - 1)
-        self.lo, self.hi = g_lo - plane_range[0] + 1, max(g_hi - plane_range[0] + 1, g_lo - plane_range[0] + 1)
+        self.lo, self.hi = g_lo - p0 + g, max(g_hi - p0 + g, g_lo - p0 + g)
+        # global-interior planes in local indices (W^{s+1} of ghost planes is computed there)
+        self.i_lo, self.i_hi = max(0, 1 - p0 + g), min(shp[0], n0 - 1 - p0 + g)
 
     def set_schedule(self, sched):
         self.sc = sched
         self.n_total = sched["n_total"]
 
     def _field(self, field):
-        return {_native.V: "v", _native.F: "f", _native.WA: "wa", _native.WB: "wb", _native.ACC: "acc"}[field]
+        return {_native.V: "v", _native.F: "f", _native.ACC: "acc"}[field]
 
     def upload(self, field, vals):
         a = np.array(vals, dtype=float)
@@ -56,16 +64,16 @@ class NumpyShard:
             a[0] = 0.0
         if self.plane_range[1] == self.grid.shape[0]:
             a[-1] = 0.0
-        self.buf[self._field(field)][1:self.nloc + 1] = a
+        self.buf[self._field(field)][self.gh:self.gh + self.nloc] = a
 
     def download(self, field):
-        return np.array(self.buf[self._field(field)][1:self.nloc + 1])
+        return np.array(self.buf[self._field(field)][self.gh:self.gh + self.nloc])
 
     def zero(self, field):
         self.buf[self._field(field)][...] = 0.0
 
     def level(self, L):
-        return self.buf["v"] if L == 0 else (self.buf["wa"] if L % 2 else self.buf["wb"])
+        return self.buf["v"] if L == 0 else self.buf[L % 4]
 
     def solve_begin(self, out_mode, zero_forcing=False):
         self.mode = out_mode
@@ -91,39 +99,83 @@ class NumpyShard:
             lap = lap * self.c2
         return lap
 
+    def _inner(self):
+        return (slice(1, -1),) * (self.buf["v"].ndim - 1)
+
+    def _advance(self, s, w, wp, i):
+        """interior of W^{s+1} at plane i from W^s (w) and W^{s-1} (wp)"""
+        sc, inner = self.sc, self._inner()
+        lap = self._lap(w, i)
+        f = self.buf["f"][i][inner]
+        wc = w[i][inner]
+        if s == 0:
+            return wc + sc["half_dt2"] * (lap - f)
+        return 2.0 * wc - wp[i][inner] + sc["dt2"] * (lap - f * sc["cos_f"][s])
+
+    def _finish(self, s, i, w, new):
+        """filter update of step s at plane i (W^s = w, W^{s+1} interior = new); returns
+        True when the value must also be stored as W^{s+1}"""
+        sc, inner = self.sc, self._inner()
+        acc = self.buf["acc"][i]
+        if s == 0:
+            acc[inner] = sc["acc_c"][0] * w[i][inner]
+        acc[inner] = acc[inner] + sc["acc_c"][s + 1] * new
+        if s == self.n_total - 1:
+            out = sc["out_scale"] * acc[inner]
+            d = out - self.buf["v"][i][inner]
+            self.rs += float(np.sum(d * d))
+            self.buf["v"][i][inner] = out
+            return False
+        return True
+
     def step(self, s, region):
         lo, hi = self.lo, self.hi
         planes = {0: range(lo, hi), 1: sorted({lo, hi - 1}) if hi > lo else [], 2: range(lo + 1, hi - 1)}[region]
-        sc = self.sc
-        w, wp, wn = self.level(s), self.level(s - 1) if s > 0 else None, self.level(s + 1)
-        inner = (slice(1, -1),) * (w.ndim - 1)
+        w, wp, wn = self.level(s), self.level(s - 1), self.level(s + 1)
+        inner = self._inner()
         for i in planes:
-            lap = self._lap(w, i)
-            f = self.buf["f"][i][inner]
-            wc = w[i][inner]
-            if s == 0:
-                new = wc + sc["half_dt2"] * (lap - f)
-            else:
-                new = 2.0 * wc - wp[i][inner] + sc["dt2"] * (lap - f * sc["cos_f"][s])
-            acc = self.buf["acc"][i]
-            if s == 0:
-                acc[inner] = sc["acc_c"][0] * wc
-            acc[inner] = acc[inner] + sc["acc_c"][s + 1] * new
-            if s == self.n_total - 1:
-                out = sc["out_scale"] * acc[inner]
-                d = out - self.buf["v"][i][inner]
-                self.rs += float(np.sum(d * d))
-                self.buf["v"][i][inner] = out
-            else:
+            new = self._advance(s, w, wp, i)
+            if self._finish(s, i, w, new):
                 wn[i][inner] = new
+
+    def _pair_range(self, s, a, b):
+        """steps s, s+1 on update planes [a, b): W^{s+1} on [a-1, b] (zero outside the global
+        interior, kept aside), then W^{s+2} on [a, b) — what one chunk of the device pass does"""
+        w, wp = self.level(s), self.level(s - 1)
+        inner = self._inner()
+        w1 = np.zeros_like(w)
+        for i in range(a - 1, b + 1):
+            if self.i_lo <= i < self.i_hi:
+                w1[i][inner] = self._advance(s, w, wp, i)
+        for i in range(a, b):
+            self._finish(s, i, w, w1[i][inner])
+            self.level(s + 1)[i][inner] = w1[i][inner]
+            new = self._advance(s + 1, w1, w, i)
+            if self._finish(s + 1, i, w1, new):
+                self.level(s + 2)[i][inner] = new
+
+    def pair(self, s, region):
+        lo, hi = self.lo, self.hi
+        if region == 0:
+            self._pair_range(s, lo, hi)
+        elif region == 1:
+            if hi - lo <= 4:
+                self._pair_range(s, lo, hi)
+            else:
+                self._pair_range(s, lo, lo + 2)
+                self._pair_range(s, hi - 2, hi)
+        elif hi - lo > 4:
+            self._pair_range(s, lo + 2, hi - 2)
 
     def solve_end(self):
         return self.rs
 
-    def plane_tensor(self, level, plane):
+    def planes(self, item, first, count):
         import torch
 
-        return torch.from_numpy(self.level(level)[plane].reshape(-1))
+        kind, ident = item
+        arr = self.level(ident) if kind == "level" else self.buf[self._field(ident)]
+        return torch.from_numpy(arr[first:first + count].reshape(-1))
 
     def stream(self):
         return contextlib.nullcontext()
@@ -135,7 +187,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, dim, cells, omega, iters, q):
+def _worker(rank, world, port, dim, cells, omega, iters, q, spp):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -146,7 +198,7 @@ def _worker(rank, world, port, dim, cells, omega, iters, q):
         corr = correct_explicit(omega, g, 2, 1.0)
         cfg = FilterConfig(omega=omega, periods=1, steps_per_period=corr.steps_per_period, mode="explicit")
         rng = slab_ranges(g.shape[0], world)[rank]
-        shard = NumpyShard(g, rng)
+        shard = NumpyShard(g, rng, steps_per_pass=spp)
         solver = SlabFPI(shard, TorchHalo(dist, rank, world), corr, cfg, f)
         res = [solver.iterate() for _ in range(iters)]
         q.put((rank, rng, solver.local_iterate(), res))
@@ -154,13 +206,17 @@ def _worker(rank, world, port, dim, cells, omega, iters, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("dim,cells,omega", [(2, (40, 24), 12.0), (3, (14, 10, 12), 6.5)])
-def test_slab_fpi_world2_gloo_matches_single_domain(dim, cells, omega):
-    world, iters = 2, 3
+@pytest.mark.parametrize("dim,cells,omega,spp,world", [(2, (40, 24), 12.0, 1, 2), (3, (14, 10, 12), 6.5, 1, 2),
+                                                       (2, (40, 24), 12.0, 2, 2), (3, (14, 10, 12), 6.5, 2, 2),
+                                                       (3, (14, 10, 12), 6.5, 2, 3), (2, (9, 30), 8.0, 2, 3)])
+def test_slab_fpi_gloo_matches_single_domain(dim, cells, omega, spp, world):
+    """world 2 and 3 (a middle slab exchanges both sides; (9, 30) over 3 ranks leaves
+    slabs of 3 and 4 planes, so the two-step boundary regions cover whole slabs)"""
+    iters = 3
     ctx = mp.get_context("fork")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, dim, cells, omega, iters, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, dim, cells, omega, iters, q, spp)) for r in range(world)]
     for p in procs:
         p.start()
     got = [q.get(timeout=120) for _ in range(world)]
@@ -177,7 +233,7 @@ def test_slab_fpi_world2_gloo_matches_single_domain(dim, cells, omega):
     vref, rref = O.fpi(f, g.spacing, sc, iters)
     assert np.array_equal(v, vref)
     np.testing.assert_allclose(got[0][3], rref, rtol=1e-12)
-    assert got[0][3] == got[1][3]
+    assert all(t[3] == got[0][3] for t in got)
 
 
 def test_slab_ranges():
