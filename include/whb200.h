@@ -194,6 +194,35 @@ int whb_copy_plane(whb_ctx *src, int src_level, int64_t src_plane, whb_ctx *dst,
  * whb_level_plane_ptr / whb_field_plane_ptr), ordered the same way. */
 int whb_copy_device(whb_ctx *src, uint64_t src_ptr, whb_ctx *dst, uint64_t dst_ptr, int64_t bytes);
 
+/* ---- implicit trapezoidal stepping ---------------------
+ * Vector ids as for whb_vec_*.  The CG iteration (linalg.py:62-99) runs on the
+ * host over these calls (paper_2504_03074_b200/implicit.py).
+ * whb_imp_apply: y = x - s * c^2 L_h x  (_ImplicitSolver.apply, timestep.py:225-226;
+ *   s = 0.5*dt**2; tmp: scratch vector, used by the general operator only).
+ * whb_imp_rhs: right-hand side and initial guess of one implicit step
+ *   (step_implicit, timestep.py:155-164): first != 0: rhs = w - q0*f, guess = w;
+ *   else rhs = ((2w - wp) + qh*lap) - qd*(f*fs), guess = 2w - wp, lap = c^2 L_h wp.
+ * whb_vec_xpay: y = x + a*y  (p = z + beta*p, linalg.py:97).
+ * whb_mg_setup / whb_mg_vcycle: 2D all-Dirichlet geometric multigrid for
+ *   I - (dt^2/2) c^2 L_h (MultigridHierarchy, linalg.py:189-346): nlev levels,
+ *   cells[2*l + a] cells of level l on axis a (level 0 = the context grid, each
+ *   level halves both), gamma[2*l + a] = coef/dx_a^2, diag[l] = 1 + 2*sum(gamma),
+ *   coarse_inv = inverse of the coarsest interior matrix (row-major, interior
+ *   points row-major), nu1/nu2 pre/post red-black sweeps; whb_mg_vcycle:
+ *   u = one V-cycle applied to b from u = 0 (the CG preconditioner).
+ * whb_tri_setup / whb_tri_solve: 1D Dirichlet tridiagonal elimination
+ *   (TridiagFactorization, linalg.py:380-421): n = points - 2 interior unknowns,
+ *   sub[n-1], dp[n], cp[n-1] the host factorisation; x = scatter(solve(b interior)). */
+int whb_imp_apply(whb_ctx *ctx, int x, int y, double s, int tmp);
+int whb_imp_rhs(whb_ctx *ctx, int w, int wp, int lap, int f, int rhs, int guess, int first, double q0,
+                double qh, double qd, double fs);
+int whb_vec_xpay(whb_ctx *ctx, int x, double a, int y);
+int whb_mg_setup(whb_ctx *ctx, int nlev, const int64_t *cells, const double *gamma, const double *diag,
+                 const double *coarse_inv, int nu1, int nu2);
+int whb_mg_vcycle(whb_ctx *ctx, int b, int u);
+int whb_tri_setup(whb_ctx *ctx, int n, const double *sub, const double *dp, const double *cp);
+int whb_tri_solve(whb_ctx *ctx, int b, int x);
+
 /* ---- introspection -------------------------------------------------------- */
 /* Number of kernel launches issued by this context since creation. */
 int whb_launch_count(whb_ctx *ctx, int64_t *count);

@@ -9,6 +9,9 @@ operation executed by hand-written sm_100a CUDA kernels in libwhb200.so
 so ``waveholtz.driver.wave_solve_filtered = paper_2504_03074_b200.wave_solve_filtered``
 reroutes the reference's own drivers onto the GPU.
 
+Implicit (trapezoidal) mode runs on the device too: CG with a multigrid or
+tridiagonal preconditioner (``implicit.py``).
+
 Extensions beyond the reference: 3D grids, batched frequencies
 (``batch.fpi_solve_batched``) and slab decomposition across GPUs
 (``slab.SlabSolver``).
@@ -37,6 +40,7 @@ from .timestep import (
     WaveState,
     cfl_constant,
     correct_explicit,
+    correct_implicit,
     step_explicit,
     time_schedule,
     wave_solve_filtered,

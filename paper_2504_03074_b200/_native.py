@@ -30,6 +30,7 @@ EXPORTS = (
     "whb_copy_plane", "whb_launch_count", "whb_set_timing", "whb_last_timing", "whb_host_alloc",
     "whb_host_free", "whb_geometry", "whb_set_l2_flush", "whb_apply_operator", "whb_plan", "whb_set_operator_general",
     "whb_pair", "whb_ghost_planes", "whb_field_plane_ptr", "whb_copy_device",
+    "whb_imp_apply", "whb_imp_rhs", "whb_vec_xpay", "whb_mg_setup", "whb_mg_vcycle", "whb_tri_setup", "whb_tri_solve",
 )
 
 _lib = None
@@ -97,6 +98,14 @@ def load():
         "whb_ghost_planes": ([vp, ctypes.POINTER(c_int)], c_int),
         "whb_field_plane_ptr": ([vp, c_int, c_int, c_i64, ctypes.POINTER(c_u64), ip64], c_int),
         "whb_copy_device": ([vp, c_u64, vp, c_u64, c_i64], c_int),
+        "whb_imp_apply": ([vp, c_int, c_int, c_double, c_int], c_int),
+        "whb_imp_rhs": ([vp, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_double, c_double, c_double,
+                         c_double], c_int),
+        "whb_vec_xpay": ([vp, c_int, c_double, c_int], c_int),
+        "whb_mg_setup": ([vp, c_int, ip64, dp, dp, dp, c_int, c_int], c_int),
+        "whb_mg_vcycle": ([vp, c_int, c_int], c_int),
+        "whb_tri_setup": ([vp, c_int, dp, dp, dp], c_int),
+        "whb_tri_solve": ([vp, c_int, c_int], c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -292,6 +301,37 @@ class Context:
         check(load().whb_matvec(self._h, int(x), int(y)), "whb_matvec")
 
     # -- step-level control (slab decomposition) ------------------------------------
+    # -- implicit stepping -------------------------------------
+    def imp_apply(self, x, y, s, tmp=-1):
+        check(load().whb_imp_apply(self._h, int(x), int(y), float(s), int(tmp)), "whb_imp_apply")
+
+    def imp_rhs(self, w, wp, lap, f, rhs, guess, first, q0, qh, qd, fs):
+        check(load().whb_imp_rhs(self._h, int(w), int(wp), int(lap), int(f), int(rhs), int(guess), int(bool(first)),
+                                 float(q0), float(qh), float(qd), float(fs)), "whb_imp_rhs")
+
+    def xpay(self, x, a, y):
+        check(load().whb_vec_xpay(self._h, int(x), float(a), int(y)), "whb_vec_xpay")
+
+    def mg_setup(self, cells, gamma, diag, coarse_inv, nu1=2, nu2=2):
+        cells = np.ascontiguousarray(np.asarray(cells, dtype=np.int64).reshape(-1))
+        gamma = np.ascontiguousarray(np.asarray(gamma, dtype=np.float64).reshape(-1))
+        diag = np.ascontiguousarray(diag, dtype=np.float64)
+        ainv = np.ascontiguousarray(coarse_inv, dtype=np.float64)
+        check(load().whb_mg_setup(self._h, len(diag), cells.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), _dp(gamma),
+                                  _dp(diag), _dp(ainv), int(nu1), int(nu2)), "whb_mg_setup")
+
+    def mg_vcycle(self, b, u):
+        check(load().whb_mg_vcycle(self._h, int(b), int(u)), "whb_mg_vcycle")
+
+    def tri_setup(self, sub, dp_, cp):
+        sub = np.ascontiguousarray(sub, dtype=np.float64)
+        dp_ = np.ascontiguousarray(dp_, dtype=np.float64)
+        cp = np.ascontiguousarray(cp, dtype=np.float64)
+        check(load().whb_tri_setup(self._h, len(dp_), _dp(sub), _dp(dp_), _dp(cp)), "whb_tri_setup")
+
+    def tri_solve(self, b, x):
+        check(load().whb_tri_solve(self._h, int(b), int(x)), "whb_tri_solve")
+
     def solve_begin(self, out_mode, zero_forcing=False):
         check(load().whb_solve_begin(self._h, int(out_mode), int(bool(zero_forcing))), "whb_solve_begin")
 

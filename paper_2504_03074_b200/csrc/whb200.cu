@@ -300,6 +300,7 @@ __global__ void zero_boundary_kernel(double *x, long long S0, int P, int n1, int
 #include "step_wf2d.cuh"
 #include "step_tb2r.cuh"
 #include "step_tb2w.cuh"
+#include "implicit.cuh"
 namespace {
 
 // y = c^2 * L_h x at owned interior points (DiscreteOperator.apply_values, grid.py:346-368);
@@ -570,6 +571,11 @@ struct MemberHost {
     int n_total = 0;
 };
 
+namespace {
+struct MGData;   // 2D multigrid hierarchy of the implicit solve (implicit.cuh)
+struct TriData;  // 1D tridiagonal factorisation of the implicit solve
+}  // namespace
+
 struct whb_ctx {
     int device = 0;
     int ndim = 0;
@@ -635,9 +641,33 @@ struct whb_ctx {
     GeomG geomg{};                   // general operator (kern == 3)
     // TMA tensor maps keyed by (buffer, box kind)
     std::map<std::tuple<const double *, int, int>, CUtensorMap> tmaps;
+    // implicit-mode solvers (whb_mg_setup / whb_tri_setup)
+    MGData *mg = nullptr;
+    TriData *tri = nullptr;
 };
 
 namespace {
+
+struct MGLevelBuf {
+    imp::Lev lev;
+    double *u = nullptr, *b = nullptr, *r = nullptr;  // level 0: u/b are the caller's vectors
+    double *raw[3] = {nullptr, nullptr, nullptr};      // owned allocations (coarse levels; r of level 0)
+};
+
+struct MGData {
+    std::vector<MGLevelBuf> lv;
+    int nu1 = 2, nu2 = 2;
+    double *ainv = nullptr;  // coarsest-level inverse, n x n
+    std::map<std::pair<const double *, const double *>, cudaGraphExec_t> graphs;
+};
+
+struct TriData {
+    int n = 0;
+    double *sub = nullptr, *dp = nullptr, *cp = nullptr, *y = nullptr;
+};
+
+void free_mg(whb_ctx *c);
+void free_tri(whb_ctx *c);
 
 int set_dev(whb_ctx *c) {
     WHB_CUDA(cudaSetDevice(c->device));
@@ -1587,6 +1617,64 @@ int zero_bnd(whb_ctx *c, double *x) {
     return 0;
 }
 
+// ---- implicit-mode helpers (implicit.cuh) ---------------------------------------------------
+
+void free_mg(whb_ctx *c) {
+    if (!c->mg) return;
+    for (auto &kv : c->mg->graphs) cudaGraphExecDestroy(kv.second);
+    for (auto &L : c->mg->lv)
+        for (double *p : L.raw)
+            if (p) cudaFree(p);
+    cudaFree(c->mg->ainv);
+    delete c->mg;
+    c->mg = nullptr;
+}
+
+void free_tri(whb_ctx *c) {
+    if (!c->tri) return;
+    cudaFree(c->tri->sub); cudaFree(c->tri->dp); cudaFree(c->tri->cp); cudaFree(c->tri->y);
+    delete c->tri;
+    c->tri = nullptr;
+}
+
+int grid_blocks(long long n) {
+    return (int)std::max<long long>(1, std::min<long long>(4 * 148, (n + 255) / 256));
+}
+
+// one V-cycle from u = 0 on level `l` (linalg.py:322-339); u of the coarsest level is the
+// coarse solve of b
+int mg_enqueue(whb_ctx *c, int l) {
+    MGData &M = *c->mg;
+    MGLevelBuf &B = M.lv[l];
+    const imp::Lev &L = B.lev;
+    const long long pts = (long long)(L.nx + 1) * (L.ny + 1);
+    if (l == (int)M.lv.size() - 1) {
+        const int n = (L.nx - 1) * (L.ny - 1);
+        imp::coarse_solve_kernel<<<std::max(1, std::min(592, (n + 7) / 8)), 256, 0, c->stream>>>(L, M.ainv, B.b, B.u);
+        c->launches++;
+        WHB_CUDA(cudaGetLastError());
+        return 0;
+    }
+    const long long gs_pts = (long long)(L.nx - 1) * (L.ny / 2 + 1);
+    auto gs = [&](int color) {
+        imp::gs_color_kernel<<<grid_blocks(gs_pts), 256, 0, c->stream>>>(L, B.u, B.b, color);
+        c->launches++;
+    };
+    for (int k = 0; k < M.nu1; ++k) { gs(0); gs(1); }
+    imp::residual_kernel<<<grid_blocks(pts), 256, 0, c->stream>>>(L, B.u, B.b, B.r);
+    MGLevelBuf &N = M.lv[l + 1];
+    const long long cpts = (long long)(N.lev.nx + 1) * (N.lev.ny + 1);
+    imp::restrict_kernel<<<grid_blocks(cpts), 256, 0, c->stream>>>(L, B.r, N.lev, N.b);
+    WHB_CUDA(cudaMemsetAsync(N.u, 0, (size_t)(N.lev.nx + 1) * N.lev.rs * sizeof(double), c->stream));
+    c->launches += 2;
+    WHB_TRY(mg_enqueue(c, l + 1));
+    imp::prolong_add_kernel<<<grid_blocks(pts), 256, 0, c->stream>>>(L, B.u, N.lev, N.u);
+    c->launches++;
+    for (int k = 0; k < M.nu2; ++k) { gs(1); gs(0); }
+    WHB_CUDA(cudaGetLastError());
+    return 0;
+}
+
 int vec_reduce_dot(whb_ctx *c, const double *x, const double *y, double *out) {
     dot_partials_kernel<<<kRedBlocks, kRedThreads, 0, c->stream>>>(owned(x, c), owned(y, c), owned_elems(c), c->d_red);
     final_sum_kernel<<<1, 1024, 0, c->stream>>>(c->d_red, kRedBlocks, c->d_red + kRedBlocks);
@@ -1711,6 +1799,8 @@ int whb_destroy(whb_ctx *c) {
     if (!c) return 0;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    free_mg(c);
+    free_tri(c);
     for (auto &kv : c->graphs) cudaGraphExecDestroy(kv.second);
     for (auto &m : c->mem) {
         free_field(c, m.v); free_field(c, m.f); free_field(c, m.acc);
@@ -2320,6 +2410,182 @@ int whb_geometry(whb_ctx *c, int64_t *shape3, int64_t *pitch, int64_t *nloc) {
         for (int a = 0; a < 3; ++a) shape3[a] = c->gshape[a];
     if (pitch) *pitch = c->P;
     if (nloc) *nloc = c->nloc;
+    return 0;
+}
+
+// ---- implicit trapezoidal stepping ----------------------------------
+
+int whb_imp_apply(whb_ctx *c, int xi, int yi, double s, int tmpi) {
+    if (!c) return fail(WHB_E_ARG, "NULL argument");
+    if (xi == yi) return fail(WHB_E_ARG, "whb_imp_apply needs distinct x and y");
+    WHB_TRY(set_dev(c));
+    if (!c->op_set) return fail(WHB_E_STATE, "operator not set");
+    VEC_OR_FAIL(x, xi);
+    VEC_OR_FAIL(y, yi);
+    if (c->kern == 3) {  // general operator: t = c^2 L x (0 at boundaries), then y = x - s*t
+        VEC_OR_FAIL(t, tmpi);
+        if (t == x || t == y) return fail(WHB_E_ARG, "whb_imp_apply scratch must differ from x and y");
+        apply_general_kernel<<<kGenBlocks, 256, 0, c->stream>>>(c->geomg, x, t, (int)c->nloc);
+        ELEMWISE_LAUNCH(imp::sub_scaled_kernel, owned(x, c), s, owned(t, c), owned(y, c), owned_elems(c));
+        c->launches++;
+        return 0;
+    }
+    const int lp0 = GH, lp1 = GH + (int)c->nloc;
+    auto kfn = c->act1 ? imp::apply_kernel<true, true>
+                       : (c->act0 ? imp::apply_kernel<true, false> : imp::apply_kernel<false, false>);
+    ELEMWISE_LAUNCH(kfn, c->geom, x, y, s, lp0, lp1, c->upd_lo, c->upd_hi);
+    return 0;
+}
+
+int whb_imp_rhs(whb_ctx *c, int wi, int wpi, int lapi, int fi, int rhsi, int guessi, int first, double q0,
+                double qh, double qd, double fs) {
+    if (!c) return fail(WHB_E_ARG, "NULL argument");
+    WHB_TRY(set_dev(c));
+    VEC_OR_FAIL(w, wi);
+    VEC_OR_FAIL(wp, wpi);
+    VEC_OR_FAIL(lap, lapi);
+    VEC_OR_FAIL(f, fi);
+    VEC_OR_FAIL(rhs, rhsi);
+    VEC_OR_FAIL(guess, guessi);
+    ELEMWISE_LAUNCH(imp::rhs_kernel, owned(w, c), owned(wp, c), owned(lap, c), owned(f, c), owned(rhs, c),
+                    owned(guess, c), first, q0, qh, qd, fs, owned_elems(c));
+    return 0;
+}
+
+int whb_vec_xpay(whb_ctx *c, int xi, double a, int yi) {
+    if (!c) return fail(WHB_E_ARG, "NULL argument");
+    WHB_TRY(set_dev(c));
+    VEC_OR_FAIL(x, xi);
+    VEC_OR_FAIL(y, yi);
+    ELEMWISE_LAUNCH(imp::xpay_kernel, owned(x, c), a, owned(y, c), owned_elems(c));
+    return 0;
+}
+
+int whb_mg_setup(whb_ctx *c, int nlev, const int64_t *cells, const double *gamma, const double *diag,
+                 const double *coarse_inv, int nu1, int nu2) {
+    if (!c || !cells || !gamma || !diag || !coarse_inv) return fail(WHB_E_ARG, "NULL argument");
+    if (c->ndim != 2 || c->plane_begin != 0 || c->plane_end != c->gshape[0])
+        return fail(WHB_E_ARG, "multigrid needs a whole-grid 2D context");
+    if (nlev < 1 || nu1 < 0 || nu2 < 0) return fail(WHB_E_ARG, "bad multigrid shape");
+    if (cells[0] != c->gshape[0] - 1 || cells[1] != c->gshape[2] - 1)
+        return fail(WHB_E_ARG, "level 0 must be the context grid");
+    for (int l = 1; l < nlev; ++l)
+        if (2 * cells[2 * l] != cells[2 * l - 2] || 2 * cells[2 * l + 1] != cells[2 * l - 1])
+            return fail(WHB_E_ARG, "levels must halve the cell counts");
+    WHB_TRY(set_dev(c));
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
+    free_mg(c);
+    c->mg = new MGData();
+    MGData &M = *c->mg;
+    M.nu1 = nu1;
+    M.nu2 = nu2;
+    M.lv.resize(nlev);
+    auto fail_free = [&](int rc) { free_mg(c); return rc; };
+    for (int l = 0; l < nlev; ++l) {
+        MGLevelBuf &B = M.lv[l];
+        B.lev.nx = (int)cells[2 * l];
+        B.lev.ny = (int)cells[2 * l + 1];
+        B.lev.gx = gamma[2 * l];
+        B.lev.gy = gamma[2 * l + 1];
+        B.lev.diag = diag[l];
+        if (l == 0) {
+            B.lev.rs = c->S0;  // 2D storage: one row per plane
+            double *r = nullptr;
+            int rc = alloc_field(c, &r);
+            if (rc) return fail_free(rc);
+            B.raw[2] = r - c->slack_front;  // freed as a raw allocation
+            B.r = owned(r, c);
+        } else {
+            B.lev.rs = (B.lev.ny + 1 + 15) / 16 * 16;
+            const size_t n = (size_t)(B.lev.nx + 1) * B.lev.rs;
+            for (int q = 0; q < 3; ++q) {
+                if (cudaMalloc(&B.raw[q], n * sizeof(double)) != cudaSuccess) return fail_free(fail(WHB_E_NOMEM, "mg level"));
+                if (cudaMemsetAsync(B.raw[q], 0, n * sizeof(double), c->stream) != cudaSuccess)
+                    return fail_free(fail(WHB_E_CUDA, "mg memset"));
+            }
+            B.u = B.raw[0];
+            B.b = B.raw[1];
+            B.r = B.raw[2];
+        }
+    }
+    const imp::Lev &C = M.lv[nlev - 1].lev;
+    const size_t nc = (size_t)(C.nx - 1) * (C.ny - 1);
+    if (cudaMalloc(&M.ainv, nc * nc * sizeof(double)) != cudaSuccess) return fail_free(fail(WHB_E_NOMEM, "mg coarse"));
+    if (cudaMemcpy(M.ainv, coarse_inv, nc * nc * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+        return fail_free(fail(WHB_E_CUDA, "mg coarse upload"));
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int whb_mg_vcycle(whb_ctx *c, int bi, int ui) {
+    if (!c) return fail(WHB_E_ARG, "NULL argument");
+    if (!c->mg) return fail(WHB_E_STATE, "multigrid not set up (whb_mg_setup)");
+    if (bi == ui) return fail(WHB_E_ARG, "whb_mg_vcycle needs distinct b and u");
+    WHB_TRY(set_dev(c));
+    VEC_OR_FAIL(b, bi);
+    VEC_OR_FAIL(u, ui);
+    MGData &M = *c->mg;
+    M.lv[0].b = owned(b, c);
+    M.lv[0].u = owned(u, c);
+    WHB_CUDA(cudaMemsetAsync(u - c->slack_front, 0,
+                             (size_t)(c->slack_front + c->field_elems + c->slack_back) * sizeof(double), c->stream));
+    if (!c->use_graphs) return mg_enqueue(c, 0);
+    auto key = std::make_pair((const double *)b, (const double *)u);
+    auto it = M.graphs.find(key);
+    if (it == M.graphs.end()) {
+        cudaGraph_t g;
+        const int64_t l0 = c->launches;
+        WHB_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        int rc = mg_enqueue(c, 0);
+        cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+        if (rc) return rc;
+        if (e != cudaSuccess) return fail(WHB_E_CUDA, std::string("capture: ") + cudaGetErrorString(e));
+        cudaGraphExec_t ge;
+        e = cudaGraphInstantiate(&ge, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return fail(WHB_E_CUDA, std::string("instantiate: ") + cudaGetErrorString(e));
+        c->graph_kernels[std::make_tuple(-1, 0, (const void *)ge)] = c->launches - l0;
+        c->launches = l0;
+        it = M.graphs.emplace(key, ge).first;
+    }
+    WHB_CUDA(cudaGraphLaunch(it->second, c->stream));
+    c->launches += c->graph_kernels[std::make_tuple(-1, 0, (const void *)it->second)];
+    return 0;
+}
+
+int whb_tri_setup(whb_ctx *c, int n, const double *sub, const double *dp, const double *cp) {
+    if (!c || !sub || !dp || !cp) return fail(WHB_E_ARG, "NULL argument");
+    if (c->ndim != 1 || n != (int)c->gshape[2] - 2) return fail(WHB_E_ARG, "tridiagonal solve needs a 1D context with n = points - 2");
+    WHB_TRY(set_dev(c));
+    free_tri(c);
+    c->tri = new TriData();
+    TriData &T = *c->tri;
+    T.n = n;
+    const size_t b = (size_t)std::max(1, n) * sizeof(double);
+    if (cudaMalloc(&T.sub, b) != cudaSuccess || cudaMalloc(&T.dp, b) != cudaSuccess ||
+        cudaMalloc(&T.cp, b) != cudaSuccess || cudaMalloc(&T.y, b) != cudaSuccess) {
+        free_tri(c);
+        return fail(WHB_E_NOMEM, "tridiagonal factors");
+    }
+    if (n > 1) WHB_CUDA(cudaMemcpy(T.sub, sub, (n - 1) * sizeof(double), cudaMemcpyHostToDevice));
+    WHB_CUDA(cudaMemcpy(T.dp, dp, n * sizeof(double), cudaMemcpyHostToDevice));
+    if (n > 1) WHB_CUDA(cudaMemcpy(T.cp, cp, (n - 1) * sizeof(double), cudaMemcpyHostToDevice));
+    return 0;
+}
+
+int whb_tri_solve(whb_ctx *c, int bi, int xi) {
+    if (!c) return fail(WHB_E_ARG, "NULL argument");
+    if (!c->tri) return fail(WHB_E_STATE, "tridiagonal factors not set (whb_tri_setup)");
+    if (bi == xi) return fail(WHB_E_ARG, "whb_tri_solve needs distinct b and x");
+    WHB_TRY(set_dev(c));
+    VEC_OR_FAIL(b, bi);
+    VEC_OR_FAIL(x, xi);
+    TriData &T = *c->tri;
+    // x = scatter_interior(solve(interior_values(b))): boundary points of x are 0 (grid.py:548-556)
+    WHB_CUDA(cudaMemsetAsync(owned(x, c), 0, (size_t)owned_elems(c) * sizeof(double), c->stream));
+    imp::tri_solve_kernel<<<1, 32, 0, c->stream>>>(owned(b, c) + 1, owned(x, c) + 1, T.n, T.sub, T.dp, T.cp, T.y);
+    c->launches++;
+    WHB_CUDA(cudaGetLastError());
     return 0;
 }
 

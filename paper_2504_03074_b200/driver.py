@@ -22,6 +22,7 @@ from . import _native
 from .device import DeviceProblem, device_problem
 from .filters import FilterConfig, ResonanceError, TimeMode, mode_name
 from .grid import DiscreteOperator, GridField, bc_name
+from .implicit import correct_implicit, implicit_solver_for, implicit_wave_solve
 from .linalg import device_gmres
 from .timestep import correct_explicit, time_schedule
 
@@ -207,7 +208,7 @@ def resolve_time_discretization(problem, config):
             cfg = replace(config, steps_per_period=corr.steps_per_period)
         return corr, cfg
     if mode_name(config.mode) == "implicit":
-        raise NotImplementedError("implicit time stepping is out of scope for the GPU path (SURVEY §2)")
+        return correct_implicit(problem.omega, config.steps_per_period), config
     raise ValueError("the continuous filter cannot be time-stepped; pick explicit or implicit")
 
 
@@ -224,6 +225,8 @@ def fpi_solve(problem, config, tol=1e-10, maxit=500, inner_tol=1e-12, device_sta
     pass exactly like driver.py:225-230."""
     corr, cfg = resolve_time_discretization(problem, config)
     dp = device_state or _device_for(problem)
+    if mode_name(cfg.mode) == "implicit":
+        return _fpi_implicit(problem, cfg, corr, dp, tol, maxit, inner_tol)
     dp.set_schedule(time_schedule(corr, cfg))
     dp.set_forcing(problem.forcing.values)
     dp.ctx.zero(_native.V)
@@ -251,6 +254,44 @@ def fpi_solve(problem, config, tol=1e-10, maxit=500, inner_tol=1e-12, device_sta
     return v, run
 
 
+def _implicit_state(problem, dp, corr, inner_tol):
+    solver = implicit_solver_for(dp, problem.grid, problem.order, problem.c, corr.dt, tol=inner_tol)
+    ids = dp.__dict__.get("_implicit_fpi_ids")
+    if ids is None:
+        ids = dp._implicit_fpi_ids = dp.ctx.vec_reserve(2)
+    return solver, ids
+
+
+def _fpi_implicit(problem, cfg, corr, dp, tol, maxit, inner_tol):
+    """_iterate (driver.py:211-244) with implicit wave solves, device resident: v, v_new and
+    every solver vector stay on the GPU; the residual is a device reduction."""
+    ctx = dp.ctx
+    solver, (vnew, diff_id) = _implicit_state(problem, dp, corr, inner_tol)
+    sched = time_schedule(corr, cfg)
+    dp.set_forcing(problem.forcing.values)
+    ctx.zero(_native.V)
+    root_n = math.sqrt(problem.grid.size)
+    residuals = []
+    converged = False
+    inner0 = solver.inner
+    k = 0
+    t0 = time.perf_counter()
+    for k in range(1, maxit + 1):
+        implicit_wave_solve(dp, solver, corr, sched, _native.V, _native.F, vnew)
+        ctx.sub_into(vnew, _native.V, diff_id)
+        diff = math.sqrt(ctx.dot(diff_id, diff_id)) / root_n   # np.linalg.norm(v_new - v)/sqrt(N)
+        residuals.append(diff)
+        ctx.copy(vnew, _native.V)
+        if diff <= tol:
+            converged = True
+            break
+    wall = time.perf_counter() - t0
+    v = GridField.from_values(problem.grid, ctx.download(_native.V), ghost=2)
+    run = WaveHoltzRun(method="fpi", periods=cfg.periods, residuals=residuals, iterations=k,
+                       converged=converged, wall_time=wall, inner_iterations=solver.inner - inner0)
+    return v, run
+
+
 def waveholtz_operator(problem, config, corr=None, linear_solver=None, deflation=None):
     """Matrix-free A v = v - W(v, 0) on host arrays (driver.py:247-264); each call
     uploads v, runs one zero-forcing wave solve on the device and downloads A v."""
@@ -260,6 +301,17 @@ def waveholtz_operator(problem, config, corr=None, linear_solver=None, deflation
         corr, config = resolve_time_discretization(problem, config)
     dp = _device_for(problem)
     sched = time_schedule(corr, config)
+    if mode_name(config.mode) == "implicit":
+        solver, (xv, _) = _implicit_state(problem, dp, corr, 1e-12)
+
+        def matvec_implicit(values: np.ndarray) -> np.ndarray:
+            dp.ctx.vec_upload(xv, np.asarray(values, dtype=float))
+            its = implicit_wave_solve(dp, solver, corr, sched, xv, None, _native.OUT, out_mode=_native.OUT_AV)
+            if linear_solver is not None and hasattr(linear_solver, "inner"):
+                linear_solver.inner += its
+            return dp.ctx.download(_native.OUT)
+
+        return matvec_implicit
 
     def matvec(values: np.ndarray) -> np.ndarray:
         dp.set_schedule(sched)
@@ -285,22 +337,34 @@ def krylov_solve(problem, config, tol=1e-10, restart=50, maxit=500, deflation=No
     dp = _device_for(problem)
     ctx = dp.ctx
     t0 = time.perf_counter()
-    dp.set_schedule(time_schedule(corr, cfg))
+    implicit = mode_name(cfg.mode) == "implicit"
     dp.set_forcing(problem.forcing.values)
     ctx.zero(_native.V)
-    ctx.filtered_solve(_native.OUT_PLAIN)  # OUT = b = W(0, f)   (driver.py:279-281)
+    if implicit:
+        solver, _ = _implicit_state(problem, dp, corr, inner_tol)
+        inner0 = solver.inner
+        sched = time_schedule(corr, cfg)
+        implicit_wave_solve(dp, solver, corr, sched, _native.V, _native.F, _native.OUT)
+
+        def mv(src, dst):
+            implicit_wave_solve(dp, solver, corr, sched, src, None, dst, out_mode=_native.OUT_AV)
+    else:
+        dp.set_schedule(time_schedule(corr, cfg))
+        ctx.filtered_solve(_native.OUT_PLAIN)  # OUT = b = W(0, f)   (driver.py:279-281)
+        mv = ctx.matvec
     m = max(1, min(restart, maxit))
     ids = ctx.vec_reserve(m + 4) if not hasattr(dp, "_krylov_ids") or len(dp._krylov_ids) < m + 4 else dp._krylov_ids
     dp._krylov_ids = ids
     b_id, x_id, work = ids[0], ids[1], ids[2:]
     ctx.copy(_native.OUT, b_id)
     scale = math.sqrt(problem.grid.size)
-    rep = device_gmres(ctx, ctx.matvec, b_id, x_id, tol=0.0, atol=tol * scale, restart=restart, maxit=maxit,
+    rep = device_gmres(ctx, mv, b_id, x_id, tol=0.0, atol=tol * scale, restart=restart, maxit=maxit,
                        work_ids=work)
     x = ctx.vec_download(x_id)
     wall = time.perf_counter() - t0
     run = WaveHoltzRun(method="gmres", periods=cfg.periods, residuals=[r / scale for r in rep.residual_history],
-                       iterations=rep.iterations, converged=rep.converged, wall_time=wall, inner_iterations=0)
+                       iterations=rep.iterations, converged=rep.converged, wall_time=wall,
+                       inner_iterations=(solver.inner - inner0) if implicit else 0)
     return GridField.from_values(problem.grid, x), run
 
 

@@ -6,9 +6,9 @@ per-step scalar schedule, formed with the reference's own Python expressions
  so the device never evaluates a transcendental.
 Device side (libwhb200.so): the fused leapfrog + filter kernel.
 
-The implicit trapezoidal scheme (timestep.py:100-108, 148-247) is out of
-scope; asking for it raises NotImplementedError — there is no
-CPU fallback.
+The implicit trapezoidal scheme (timestep.py:100-108, 148-247) runs on the
+device too (``implicit.py``: CG with a multigrid / tridiagonal
+preconditioner).  There is no CPU fallback.
 """
 
 from __future__ import annotations
@@ -22,9 +22,10 @@ from . import _native
 from .device import device_problem
 from .filters import ExplicitStabilityError, TimeMode, alpha_d, mode_name
 from .grid import GridField
+from .implicit import correct_implicit, implicit_solver_for, implicit_wave_solve
 
 __all__ = [
-    "TimeCorrection", "WaveState", "correct_explicit", "cfl_constant", "step_explicit",
+    "TimeCorrection", "WaveState", "correct_explicit", "correct_implicit", "cfl_constant", "step_explicit",
     "wave_solve_filtered", "time_schedule",
 ]
 
@@ -56,6 +57,11 @@ class TimeCorrection:
             lhs = math.sin(self.omega_tilde * dt / 2.0) / (dt / 2.0)
             if abs(lhs - self.omega) > 1e-13 * self.omega:
                 raise AssertionError("sin(w_e dt/2)/(dt/2) must equal omega")
+        elif mode_name(self.mode) == "implicit":
+            if nt < 5:
+                raise AssertionError("implicit stepping needs N_t >= 5")
+            if abs(math.cos(self.omega_tilde * dt) * (1.0 + (self.omega * dt) ** 2 / 2.0) - 1.0) > 1e-13:
+                raise AssertionError("cos(w_i dt)(1 + (w dt)^2/2) must equal 1")
 
     @property
     def period_tilde(self) -> float:
@@ -114,11 +120,20 @@ def time_schedule(corr, config) -> dict:
     }
 
 
-def _check_explicit(config, corr):
+def _check_modes(config, corr):
+    """timestep.py:266-269."""
     if mode_name(corr.mode) != mode_name(config.mode):
         raise ValueError(f"correction mode {corr.mode} does not match config mode {config.mode}")
+    if mode_name(config.mode) == "implicit" and corr.steps_per_period != config.steps_per_period:
+        raise ValueError("correction and config disagree on steps per period")
+    if mode_name(config.mode) not in ("explicit", "implicit"):
+        raise ValueError("the continuous filter cannot be time-stepped; pick explicit or implicit")
+
+
+def _check_explicit(config, corr):
+    _check_modes(config, corr)
     if mode_name(config.mode) != "explicit":
-        raise NotImplementedError("only the explicit (leapfrog) WaveHoltz path runs on the GPU")
+        raise NotImplementedError("this entry point runs the explicit (leapfrog) path")
 
 
 def _field_type(v):
@@ -129,10 +144,24 @@ def wave_solve_filtered(v, f, config, corr, op, linear_solver=None, implicit_fir
     """One application of W(v, f) on the GPU (timestep.py:250-301, explicit branch).
 
     Inputs are never mutated; a freshly allocated field of the input's type is
-    returned with its Dirichlet boundary zeroed (timestep.py:301)."""
-    _check_explicit(config, corr)
+    returned with its Dirichlet boundary zeroed (timestep.py:301).  Implicit mode
+    marches the trapezoidal scheme with the device CG solver (implicit.py); a
+    ``linear_solver`` passed in (e.g. the reference's _ImplicitSolver, which its
+    drivers hand over) is not used for arithmetic, but its ``inner`` counter is
+    advanced by the device solver's iterations so run records stay meaningful."""
+    _check_modes(config, corr)
     grid = op.grid
     dp = device_problem(grid, c=op.c, order=op.order)
+    if mode_name(config.mode) == "implicit":
+        solver = implicit_solver_for(dp, grid, op.order, op.c, corr.dt)
+        dp.set_forcing(f.values)
+        dp.ctx.upload(_native.V, v.values)
+        its = implicit_wave_solve(dp, solver, corr, time_schedule(corr, config), _native.V, _native.F,
+                                  _native.OUT, implicit_first_step=implicit_first_step)
+        if linear_solver is not None and hasattr(linear_solver, "inner"):
+            linear_solver.inner += its
+        out = dp.ctx.download(_native.OUT)
+        return _field_type(v).from_values(grid, out, ghost=max(2, op.ghost_width))
     dp.set_schedule(time_schedule(corr, config))
     zero_f = dp.set_forcing(f.values)
     dp.ctx.upload(_native.V, v.values)

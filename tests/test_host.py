@@ -159,8 +159,12 @@ def test_mode_errors_raise_before_any_device_work():
     with pytest.raises(ValueError, match="mode"):
         wh.wave_solve_filtered(wh.GridField.zeros(g), wh.GridField.zeros(g), cfg_i, corr, op)
     prob = wh.HelmholtzProblem(g, 2, 1.0, 5.0, wh.GridField.zeros(g))
-    with pytest.raises(NotImplementedError):
-        wh.fpi_solve(prob, cfg_i)
+    corr_i, cfg2 = wh.resolve_time_discretization(prob, cfg_i)  # implicit: N_t from the config
+    assert cfg2 is cfg_i and corr_i.steps_per_period == 10 and corr_i == wh.correct_implicit(5.0, 10)
+    with pytest.raises(ValueError, match="steps per period"):
+        wh.wave_solve_filtered(wh.GridField.zeros(g), wh.GridField.zeros(g), cfg_i, wh.correct_implicit(5.0, 12), op)
+    with pytest.raises(ValueError):
+        wh.correct_implicit(5.0, 4)
     with pytest.raises(ValueError):
         wh.resolve_time_discretization(prob, wh.FilterConfig(omega=5.0, mode="continuous"))
 
