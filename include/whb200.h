@@ -222,6 +222,17 @@ int whb_mg_setup(whb_ctx *ctx, int nlev, const int64_t *cells, const double *gam
 int whb_mg_vcycle(whb_ctx *ctx, int b, int u);
 int whb_tri_setup(whb_ctx *ctx, int n, const double *sub, const double *dp, const double *cp);
 int whb_tri_solve(whb_ctx *ctx, int b, int x);
+/* Device-resident CG (cg_solve, linalg.py:62-99) with scalars kept on the device.
+ * precond: 0 none (z must be r), 1 multigrid V-cycle, 2 tridiagonal.
+ * whb_cg_begin: z = M r, p = z, rz = r.z (device); *rr = r.r.
+ * whb_cg_iterate: one iteration — Ap = A p (A = I - s c^2 L_h, tmp as in
+ *   whb_imp_apply), alpha = rz/pAp, x += alpha p, r -= alpha Ap, z = M r,
+ *   beta = r.z/rz, p = z + beta p — as one CUDA graph; returns *pap = p.Ap and
+ *   *rr = r.r.  When pap <= 0 or is not finite nothing is updated (the
+ *   reference's breakdown exit). */
+int whb_cg_begin(whb_ctx *ctx, int r, int z, int p, int precond, double *rr);
+int whb_cg_iterate(whb_ctx *ctx, int x, int r, int z, int p, int ap, int tmp, double s, int precond, double *pap,
+                   double *rr);
 
 /* ---- introspection -------------------------------------------------------- */
 /* Number of kernel launches issued by this context since creation. */

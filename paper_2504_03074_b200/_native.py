@@ -31,6 +31,7 @@ EXPORTS = (
     "whb_host_free", "whb_geometry", "whb_set_l2_flush", "whb_apply_operator", "whb_plan", "whb_set_operator_general",
     "whb_pair", "whb_ghost_planes", "whb_field_plane_ptr", "whb_copy_device",
     "whb_imp_apply", "whb_imp_rhs", "whb_vec_xpay", "whb_mg_setup", "whb_mg_vcycle", "whb_tri_setup", "whb_tri_solve",
+    "whb_cg_begin", "whb_cg_iterate",
 )
 
 _lib = None
@@ -106,6 +107,8 @@ def load():
         "whb_mg_vcycle": ([vp, c_int, c_int], c_int),
         "whb_tri_setup": ([vp, c_int, dp, dp, dp], c_int),
         "whb_tri_solve": ([vp, c_int, c_int], c_int),
+        "whb_cg_begin": ([vp, c_int, c_int, c_int, c_int, dp], c_int),
+        "whb_cg_iterate": ([vp, c_int, c_int, c_int, c_int, c_int, c_int, c_double, c_int, dp, dp], c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -331,6 +334,18 @@ class Context:
 
     def tri_solve(self, b, x):
         check(load().whb_tri_solve(self._h, int(b), int(x)), "whb_tri_solve")
+
+    def cg_begin(self, r, z, p, precond) -> float:
+        rr = ctypes.c_double(0.0)
+        check(load().whb_cg_begin(self._h, int(r), int(z), int(p), int(precond), ctypes.byref(rr)), "whb_cg_begin")
+        return rr.value
+
+    def cg_iterate(self, x, r, z, p, ap, tmp, s, precond):
+        pap = ctypes.c_double(0.0)
+        rr = ctypes.c_double(0.0)
+        check(load().whb_cg_iterate(self._h, int(x), int(r), int(z), int(p), int(ap), int(tmp), float(s), int(precond),
+                                    ctypes.byref(pap), ctypes.byref(rr)), "whb_cg_iterate")
+        return pap.value, rr.value
 
     def solve_begin(self, out_mode, zero_forcing=False):
         check(load().whb_solve_begin(self._h, int(out_mode), int(bool(zero_forcing))), "whb_solve_begin")

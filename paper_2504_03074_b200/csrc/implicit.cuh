@@ -92,6 +92,57 @@ __global__ void xpay_kernel(const double *__restrict__ x, double a, double *y, l
         y[i] = whb_add(x[i], whb_mul(a, y[i]));
 }
 
+// ---- device-resident CG scalars (cg_solve, linalg.py:62-99) -----------------------------------
+// One CG iteration is enqueued as a fixed kernel sequence (capturable in a graph) whose
+// scalars stay on the device: the host reads back p.Ap and r.r once per iteration, for the
+// breakdown test and the convergence test the reference performs.
+enum { CG_RZ = 0, CG_PAP = 1, CG_ALPHA = 2, CG_RR = 3, CG_RZN = 4, CG_BETA = 5, CG_NSC = 8 };
+
+// finish a dot product (fixed-order tree) and derive the CG scalar that depends on it
+__global__ void cg_final_kernel(const double *__restrict__ partials, int n, double *sc, int mode) {
+    double t = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) t += partials[i];
+    const double b = block_sum(t);
+    if (threadIdx.x != 0) return;
+    if (mode == 0) {         // p.Ap -> alpha = rz / pAp
+        sc[CG_PAP] = b;
+        sc[CG_ALPHA] = __ddiv_rn(sc[CG_RZ], b);
+    } else if (mode == 1) {  // r.r
+        sc[CG_RR] = b;
+    } else if (mode == 2) {  // r.z (new) -> beta = rz_new / rz; rz = rz_new
+        sc[CG_RZN] = b;
+        sc[CG_BETA] = __ddiv_rn(b, sc[CG_RZ]);
+        sc[CG_RZ] = b;
+    } else {                 // initial r.z
+        sc[CG_RZ] = b;
+    }
+}
+
+__device__ __forceinline__ bool cg_ok(const double *sc) {
+    const double pap = sc[CG_PAP];
+    return pap > 0.0 && isfinite(pap);  // the reference stops on breakdown before updating x
+}
+
+// x = x + alpha*p; r = r - alpha*Ap
+__global__ void cg_update_kernel(double *__restrict__ x, double *__restrict__ r, const double *__restrict__ p,
+                                 const double *__restrict__ ap, const double *__restrict__ sc, long long n) {
+    if (!cg_ok(sc)) return;
+    const double a = sc[CG_ALPHA];
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        x[i] = whb_add(x[i], whb_mul(a, p[i]));
+        r[i] = whb_sub(r[i], whb_mul(a, ap[i]));
+    }
+}
+
+// p = z + beta*p
+__global__ void cg_dir_kernel(const double *__restrict__ z, double *__restrict__ p, const double *__restrict__ sc,
+                              long long n) {
+    if (!cg_ok(sc)) return;
+    const double beta = sc[CG_BETA];
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        p[i] = whb_add(z[i], whb_mul(beta, p[i]));
+}
+
 // ---- 2D multigrid levels (linalg.py:189-283) -------------------------------------------------
 
 struct Lev {
@@ -155,6 +206,42 @@ __global__ void restrict_kernel(Lev F, const double *__restrict__ r, Lev C, doub
     }
 }
 
+// Fused r = b - A u on the fine level + full-weighting restriction + zeroing of the coarse
+// iterate: each coarse interior point forms the 9 fine residuals it weights (same values as
+// residual_kernel; fine r is never stored) — one launch instead of three per level.
+__device__ __forceinline__ double fine_resid(const Lev &F, const double *__restrict__ u, const double *__restrict__ b,
+                                             long long p) {
+    const double au = whb_sub(whb_sub(whb_mul(F.diag, u[p]), whb_mul(F.gx, whb_add(u[p - F.rs], u[p + F.rs]))),
+                              whb_mul(F.gy, whb_add(u[p - 1], u[p + 1])));
+    return whb_sub(b[p], au);
+}
+
+__global__ void resid_restrict_kernel(Lev F, const double *__restrict__ u, const double *__restrict__ b, Lev C,
+                                      double *__restrict__ bc, double *__restrict__ uc) {
+    const long long total = (long long)(C.nx + 1) * (C.ny + 1);
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int I = (int)(t / (C.ny + 1));
+        const int J = (int)(t - (long long)I * (C.ny + 1));
+        double v = 0.0;
+        if (I >= 1 && I < C.nx && J >= 1 && J < C.ny) {
+            const long long p = (long long)(2 * I) * F.rs + 2 * J;
+            const long long rs = F.rs;
+            const double edges = whb_add(whb_add(whb_add(fine_resid(F, u, b, p - rs), fine_resid(F, u, b, p + rs)),
+                                                 fine_resid(F, u, b, p - 1)),
+                                         fine_resid(F, u, b, p + 1));
+            const double corners =
+                whb_add(whb_add(whb_add(fine_resid(F, u, b, p - rs - 1), fine_resid(F, u, b, p - rs + 1)),
+                                fine_resid(F, u, b, p + rs - 1)),
+                        fine_resid(F, u, b, p + rs + 1));
+            v = __ddiv_rn(whb_add(whb_add(whb_mul(4.0, fine_resid(F, u, b, p)), whb_mul(2.0, edges)), corners), 16.0);
+        }
+        const long long q = (long long)I * C.rs + J;
+        bc[q] = v;
+        uc[q] = 0.0;
+    }
+}
+
 // u += prolong(ec) (bilinear, linalg.py:259-275, 337)
 __global__ void prolong_add_kernel(Lev F, double *__restrict__ u, Lev C, const double *__restrict__ ec) {
     const long long total = (long long)(F.nx + 1) * (F.ny + 1);
@@ -192,6 +279,137 @@ __global__ void coarse_solve_kernel(Lev C, const double *__restrict__ ainv, cons
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         if (lane == 0) u[(long long)(1 + k / mi) * C.rs + 1 + k % mi] = s;
+    }
+}
+
+// ---- the coarse end of the V-cycle in ONE thread block ---------------------------------------
+// Levels Lc..L-1 of a hierarchy are small (<= 65 x 65 points): their whole sub-cycle
+// (smoothing, residual + restriction, coarse solve, prolongation, smoothing) runs in one CTA
+// out of shared memory with block barriers between phases, instead of ~10 grid-wide launches
+// per level whose cost is launch latency.  Same arithmetic as the per-level kernels above.
+constexpr int kMaxCoarseLevels = 12;
+
+struct CoarseCycle {
+    Lev lev[kMaxCoarseLevels];  // levels Lc..L-1; rs = ny + 1 (compact in shared memory)
+    int nlev, nu1, nu2;
+    long long grs;              // row stride of level Lc's global arrays
+};
+
+__device__ __forceinline__ void cc_colour(const Lev &L, double *u, const double *b, int color) {
+    const int half = L.ny / 2 + 1;
+    const int total = (L.nx - 1) * half;
+    for (int t = threadIdx.x; t < total; t += blockDim.x) {
+        const int i = 1 + t / half;
+        const int j = 2 * (t - (i - 1) * half) + ((i + color) & 1);
+        if (j < 1 || j >= L.ny) continue;
+        const long long p = (long long)i * L.rs + j;
+        const double v = whb_add(whb_add(b[p], whb_mul(L.gx, whb_add(u[p - L.rs], u[p + L.rs]))),
+                                 whb_mul(L.gy, whb_add(u[p - 1], u[p + 1])));
+        u[p] = __ddiv_rn(v, L.diag);
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(1024) coarse_cycle_kernel(CoarseCycle cc, const double *__restrict__ gb,
+                                                            double *__restrict__ gu, const double *__restrict__ ainv) {
+    extern __shared__ __align__(16) double sm[];
+    double *U[kMaxCoarseLevels], *B[kMaxCoarseLevels];
+    {
+        size_t off = 0;
+        for (int l = 0; l < cc.nlev; ++l) {
+            const size_t pts = (size_t)(cc.lev[l].nx + 1) * (cc.lev[l].ny + 1);
+            U[l] = sm + off;
+            off += pts;
+            B[l] = sm + off;
+            off += pts;
+        }
+    }
+    {
+        const Lev &L = cc.lev[0];
+        const int total = (L.nx + 1) * (L.ny + 1);
+        for (int t = threadIdx.x; t < total; t += blockDim.x) {
+            const int i = t / (L.ny + 1), j = t - i * (L.ny + 1);
+            B[0][t] = gb[(long long)i * cc.grs + j];
+            U[0][t] = 0.0;
+        }
+        __syncthreads();
+    }
+    // down: pre-smooth, then r = b - A u restricted to the next level (its u = 0)
+    for (int l = 0; l + 1 < cc.nlev; ++l) {
+        const Lev &F = cc.lev[l];
+        const Lev &C = cc.lev[l + 1];
+        for (int k = 0; k < cc.nu1; ++k) {
+            cc_colour(F, U[l], B[l], 0);
+            cc_colour(F, U[l], B[l], 1);
+        }
+        const int total = (C.nx + 1) * (C.ny + 1);
+        for (int t = threadIdx.x; t < total; t += blockDim.x) {
+            const int I = t / (C.ny + 1), J = t - I * (C.ny + 1);
+            double v = 0.0;
+            if (I >= 1 && I < C.nx && J >= 1 && J < C.ny) {
+                const long long p = (long long)(2 * I) * F.rs + 2 * J;
+                const long long rs = F.rs;
+                const double *u = U[l], *b = B[l];
+                const double edges = whb_add(whb_add(whb_add(fine_resid(F, u, b, p - rs), fine_resid(F, u, b, p + rs)),
+                                                     fine_resid(F, u, b, p - 1)),
+                                             fine_resid(F, u, b, p + 1));
+                const double corners =
+                    whb_add(whb_add(whb_add(fine_resid(F, u, b, p - rs - 1), fine_resid(F, u, b, p - rs + 1)),
+                                    fine_resid(F, u, b, p + rs - 1)),
+                            fine_resid(F, u, b, p + rs + 1));
+                v = __ddiv_rn(whb_add(whb_add(whb_mul(4.0, fine_resid(F, u, b, p)), whb_mul(2.0, edges)), corners),
+                              16.0);
+            }
+            B[l + 1][t] = v;
+            U[l + 1][t] = 0.0;
+        }
+        __syncthreads();
+    }
+    // coarsest: u = Ainv @ interior(b), one warp per unknown
+    {
+        const int c = cc.nlev - 1;
+        const Lev &C = cc.lev[c];
+        const int mi = C.ny - 1;
+        const int n = (C.nx - 1) * mi;
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+        for (int k = warp; k < n; k += nw) {
+            double s = 0.0;
+            for (int l2 = lane; l2 < n; l2 += 32) s += ainv[(long long)k * n + l2] * B[c][(1 + l2 / mi) * C.rs + 1 + l2 % mi];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == 0) U[c][(1 + k / mi) * C.rs + 1 + k % mi] = s;
+        }
+        __syncthreads();
+    }
+    // up: u += prolong(e), post-smooth in reverse colour order
+    for (int l = cc.nlev - 2; l >= 0; --l) {
+        const Lev &F = cc.lev[l];
+        const Lev &C = cc.lev[l + 1];
+        const int total = (F.nx + 1) * (F.ny + 1);
+        const double *ec = U[l + 1];
+        for (int t = threadIdx.x; t < total; t += blockDim.x) {
+            const int i = t / (F.ny + 1), j = t - i * (F.ny + 1);
+            const long long q = (long long)(i >> 1) * C.rs + (j >> 1);
+            double e;
+            if (!(i & 1) && !(j & 1)) e = ec[q];
+            else if ((i & 1) && !(j & 1)) e = whb_mul(0.5, whb_add(ec[q], ec[q + C.rs]));
+            else if (!(i & 1) && (j & 1)) e = whb_mul(0.5, whb_add(ec[q], ec[q + 1]));
+            else e = whb_mul(0.25, whb_add(whb_add(whb_add(ec[q], ec[q + C.rs]), ec[q + 1]), ec[q + C.rs + 1]));
+            U[l][t] = whb_add(U[l][t], e);
+        }
+        __syncthreads();
+        for (int k = 0; k < cc.nu2; ++k) {
+            cc_colour(F, U[l], B[l], 1);
+            cc_colour(F, U[l], B[l], 0);
+        }
+    }
+    {
+        const Lev &L = cc.lev[0];
+        const int total = (L.nx + 1) * (L.ny + 1);
+        for (int t = threadIdx.x; t < total; t += blockDim.x) {
+            const int i = t / (L.ny + 1), j = t - i * (L.ny + 1);
+            gu[(long long)i * cc.grs + j] = U[0][t];
+        }
     }
 }
 

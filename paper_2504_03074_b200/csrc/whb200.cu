@@ -644,6 +644,8 @@ struct whb_ctx {
     // implicit-mode solvers (whb_mg_setup / whb_tri_setup)
     MGData *mg = nullptr;
     TriData *tri = nullptr;
+    double *d_cg = nullptr;          // device CG scalars (imp::CG_*)
+    std::map<std::tuple<int, int, int, int, int, int, int, double>, cudaGraphExec_t> cg_graphs;
 };
 
 namespace {
@@ -657,6 +659,9 @@ struct MGLevelBuf {
 struct MGData {
     std::vector<MGLevelBuf> lv;
     int nu1 = 2, nu2 = 2;
+    int lc = -1;               // first level of the single-CTA coarse sub-cycle (-1: none)
+    size_t cc_smem = 0;
+    imp::CoarseCycle cc{};
     double *ainv = nullptr;  // coarsest-level inverse, n x n
     std::map<std::pair<const double *, const double *>, cudaGraphExec_t> graphs;
 };
@@ -1648,6 +1653,12 @@ int mg_enqueue(whb_ctx *c, int l) {
     MGLevelBuf &B = M.lv[l];
     const imp::Lev &L = B.lev;
     const long long pts = (long long)(L.nx + 1) * (L.ny + 1);
+    if (l == M.lc) {  // the rest of the cycle in one thread block (implicit.cuh)
+        imp::coarse_cycle_kernel<<<1, 1024, M.cc_smem, c->stream>>>(M.cc, B.b, B.u, M.ainv);
+        c->launches++;
+        WHB_CUDA(cudaGetLastError());
+        return 0;
+    }
     if (l == (int)M.lv.size() - 1) {
         const int n = (L.nx - 1) * (L.ny - 1);
         imp::coarse_solve_kernel<<<std::max(1, std::min(592, (n + 7) / 8)), 256, 0, c->stream>>>(L, M.ainv, B.b, B.u);
@@ -1661,17 +1672,61 @@ int mg_enqueue(whb_ctx *c, int l) {
         c->launches++;
     };
     for (int k = 0; k < M.nu1; ++k) { gs(0); gs(1); }
-    imp::residual_kernel<<<grid_blocks(pts), 256, 0, c->stream>>>(L, B.u, B.b, B.r);
+    // r = b - A u, restricted onto the next level, whose iterate starts at 0 (linalg.py:333-335)
     MGLevelBuf &N = M.lv[l + 1];
     const long long cpts = (long long)(N.lev.nx + 1) * (N.lev.ny + 1);
-    imp::restrict_kernel<<<grid_blocks(cpts), 256, 0, c->stream>>>(L, B.r, N.lev, N.b);
-    WHB_CUDA(cudaMemsetAsync(N.u, 0, (size_t)(N.lev.nx + 1) * N.lev.rs * sizeof(double), c->stream));
-    c->launches += 2;
+    imp::resid_restrict_kernel<<<grid_blocks(cpts), 256, 0, c->stream>>>(L, B.u, B.b, N.lev, N.b, N.u);
+    c->launches++;
     WHB_TRY(mg_enqueue(c, l + 1));
     imp::prolong_add_kernel<<<grid_blocks(pts), 256, 0, c->stream>>>(L, B.u, N.lev, N.u);
     c->launches++;
     for (int k = 0; k < M.nu2; ++k) { gs(1); gs(0); }
     WHB_CUDA(cudaGetLastError());
+    return 0;
+}
+
+// dot(x, y) over owned points into the device CG scalars (imp::cg_final_kernel mode)
+int cg_dot(whb_ctx *c, const double *x, const double *y, int mode) {
+    dot_partials_kernel<<<kRedBlocks, kRedThreads, 0, c->stream>>>(owned(x, c), owned(y, c), owned_elems(c), c->d_red);
+    imp::cg_final_kernel<<<1, 1024, 0, c->stream>>>(c->d_red, kRedBlocks, c->d_cg, mode);
+    c->launches += 2;
+    WHB_CUDA(cudaGetLastError());
+    return 0;
+}
+
+int imp_apply_enqueue(whb_ctx *c, const double *x, double *y, double s, double *t) {
+    if (c->kern == 3) {
+        apply_general_kernel<<<kGenBlocks, 256, 0, c->stream>>>(c->geomg, x, t, (int)c->nloc);
+        imp::sub_scaled_kernel<<<kRedBlocks, kRedThreads, 0, c->stream>>>(owned(x, c), s, owned(t, c), owned(y, c),
+                                                                           owned_elems(c));
+        c->launches += 2;
+    } else {
+        auto kfn = c->act1 ? imp::apply_kernel<true, true>
+                           : (c->act0 ? imp::apply_kernel<true, false> : imp::apply_kernel<false, false>);
+        kfn<<<kRedBlocks, kRedThreads, 0, c->stream>>>(c->geom, x, y, s, GH, GH + (int)c->nloc, c->upd_lo, c->upd_hi);
+        c->launches++;
+    }
+    WHB_CUDA(cudaGetLastError());
+    return 0;
+}
+
+// z = M r: 0 none (z is r), 1 multigrid V-cycle, 2 tridiagonal elimination
+int precond_enqueue(whb_ctx *c, const double *r, double *z, int precond) {
+    if (precond == 1) {
+        MGData &M = *c->mg;
+        M.lv[0].b = const_cast<double *>(owned(r, c));
+        M.lv[0].u = owned(z, c);
+        WHB_CUDA(cudaMemsetAsync(z - c->slack_front, 0,
+                                 (size_t)(c->slack_front + c->field_elems + c->slack_back) * sizeof(double), c->stream));
+        return mg_enqueue(c, 0);
+    }
+    if (precond == 2) {
+        TriData &T = *c->tri;
+        WHB_CUDA(cudaMemsetAsync(owned(z, c), 0, (size_t)owned_elems(c) * sizeof(double), c->stream));
+        imp::tri_solve_kernel<<<1, 32, 0, c->stream>>>(owned(r, c) + 1, owned(z, c) + 1, T.n, T.sub, T.dp, T.cp, T.y);
+        c->launches++;
+        WHB_CUDA(cudaGetLastError());
+    }
     return 0;
 }
 
@@ -1801,6 +1856,8 @@ int whb_destroy(whb_ctx *c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     free_mg(c);
     free_tri(c);
+    for (auto &kv : c->cg_graphs) cudaGraphExecDestroy(kv.second);
+    cudaFree(c->d_cg);
     for (auto &kv : c->graphs) cudaGraphExecDestroy(kv.second);
     for (auto &m : c->mem) {
         free_field(c, m.v); free_field(c, m.f); free_field(c, m.acc);
@@ -2422,19 +2479,13 @@ int whb_imp_apply(whb_ctx *c, int xi, int yi, double s, int tmpi) {
     if (!c->op_set) return fail(WHB_E_STATE, "operator not set");
     VEC_OR_FAIL(x, xi);
     VEC_OR_FAIL(y, yi);
+    double *t = nullptr;
     if (c->kern == 3) {  // general operator: t = c^2 L x (0 at boundaries), then y = x - s*t
-        VEC_OR_FAIL(t, tmpi);
-        if (t == x || t == y) return fail(WHB_E_ARG, "whb_imp_apply scratch must differ from x and y");
-        apply_general_kernel<<<kGenBlocks, 256, 0, c->stream>>>(c->geomg, x, t, (int)c->nloc);
-        ELEMWISE_LAUNCH(imp::sub_scaled_kernel, owned(x, c), s, owned(t, c), owned(y, c), owned_elems(c));
-        c->launches++;
-        return 0;
+        VEC_OR_FAIL(tv, tmpi);
+        if (tv == x || tv == y) return fail(WHB_E_ARG, "whb_imp_apply scratch must differ from x and y");
+        t = tv;
     }
-    const int lp0 = GH, lp1 = GH + (int)c->nloc;
-    auto kfn = c->act1 ? imp::apply_kernel<true, true>
-                       : (c->act0 ? imp::apply_kernel<true, false> : imp::apply_kernel<false, false>);
-    ELEMWISE_LAUNCH(kfn, c->geom, x, y, s, lp0, lp1, c->upd_lo, c->upd_hi);
-    return 0;
+    return imp_apply_enqueue(c, x, y, s, t);
 }
 
 int whb_imp_rhs(whb_ctx *c, int wi, int wpi, int lapi, int fi, int rhsi, int guessi, int first, double q0,
@@ -2513,6 +2564,36 @@ int whb_mg_setup(whb_ctx *c, int nlev, const int64_t *cells, const double *gamma
     if (cudaMalloc(&M.ainv, nc * nc * sizeof(double)) != cudaSuccess) return fail_free(fail(WHB_E_NOMEM, "mg coarse"));
     if (cudaMemcpy(M.ainv, coarse_inv, nc * nc * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
         return fail_free(fail(WHB_E_CUDA, "mg coarse upload"));
+    // single-CTA coarse sub-cycle: the deepest levels (>= 1, at least two of them) whose arrays
+    // fit in 160 KB of shared memory together, with a small coarse system
+    const char *cenv = getenv("WHB_MG_COARSE_CTA");
+    if (!(cenv && std::string(cenv) == "0") && nc <= 1024) {
+        size_t bytes = 0;
+        int lc = -1;
+        for (int l = nlev - 1; l >= 1; --l) {
+            const imp::Lev &Lv = M.lv[l].lev;
+            bytes += 2 * (size_t)(Lv.nx + 1) * (Lv.ny + 1) * sizeof(double);
+            if (bytes > 160 * 1024 || nlev - l > imp::kMaxCoarseLevels) break;
+            lc = l;
+        }
+        if (lc >= 1 && lc < nlev - 1) {
+            M.lc = lc;
+            M.cc.nlev = nlev - lc;
+            M.cc.nu1 = nu1;
+            M.cc.nu2 = nu2;
+            M.cc.grs = M.lv[lc].lev.rs;
+            M.cc_smem = 0;
+            for (int l = lc; l < nlev; ++l) {
+                imp::Lev Lv = M.lv[l].lev;
+                Lv.rs = Lv.ny + 1;
+                M.cc.lev[l - lc] = Lv;
+                M.cc_smem += 2 * (size_t)(Lv.nx + 1) * (Lv.ny + 1) * sizeof(double);
+            }
+            if (cudaFuncSetAttribute(imp::coarse_cycle_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)M.cc_smem) != cudaSuccess)
+                M.lc = -1;
+        }
+    }
     WHB_CUDA(cudaStreamSynchronize(c->stream));
     return 0;
 }
@@ -2586,6 +2667,89 @@ int whb_tri_solve(whb_ctx *c, int bi, int xi) {
     imp::tri_solve_kernel<<<1, 32, 0, c->stream>>>(owned(b, c) + 1, owned(x, c) + 1, T.n, T.sub, T.dp, T.cp, T.y);
     c->launches++;
     WHB_CUDA(cudaGetLastError());
+    return 0;
+}
+
+int whb_cg_begin(whb_ctx *c, int ri, int zi, int pi, int precond, double *rr) {
+    if (!c || !rr) return fail(WHB_E_ARG, "NULL argument");
+    if (precond < 0 || precond > 2) return fail(WHB_E_ARG, "precond must be 0, 1 or 2");
+    if ((precond == 0) != (ri == zi)) return fail(WHB_E_ARG, "z is r exactly when there is no preconditioner");
+    if (precond == 1 && !c->mg) return fail(WHB_E_STATE, "multigrid not set up");
+    if (precond == 2 && !c->tri) return fail(WHB_E_STATE, "tridiagonal factors not set");
+    WHB_TRY(set_dev(c));
+    VEC_OR_FAIL(r, ri);
+    VEC_OR_FAIL(z, zi);
+    VEC_OR_FAIL(p, pi);
+    if (!c->d_cg) WHB_CUDA(cudaMalloc(&c->d_cg, imp::CG_NSC * sizeof(double)));
+    WHB_TRY(precond_enqueue(c, r, z, precond));
+    WHB_CUDA(cudaMemcpyAsync(p, z, (size_t)c->field_elems * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    WHB_TRY(cg_dot(c, r, z, 3));
+    WHB_TRY(cg_dot(c, r, r, 1));
+    WHB_CUDA(cudaMemcpyAsync(c->h_red, c->d_cg + imp::CG_RR, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
+    *rr = c->h_red[0];
+    return 0;
+}
+
+int whb_cg_iterate(whb_ctx *c, int xi, int ri, int zi, int pi, int api, int tmpi, double s, int precond, double *pap,
+                   double *rr) {
+    if (!c || !pap || !rr) return fail(WHB_E_ARG, "NULL argument");
+    if (!c->d_cg) return fail(WHB_E_STATE, "whb_cg_iterate before whb_cg_begin");
+    if ((precond == 0) != (ri == zi)) return fail(WHB_E_ARG, "z is r exactly when there is no preconditioner");
+    WHB_TRY(set_dev(c));
+    VEC_OR_FAIL(x, xi);
+    VEC_OR_FAIL(r, ri);
+    VEC_OR_FAIL(z, zi);
+    VEC_OR_FAIL(p, pi);
+    VEC_OR_FAIL(ap, api);
+    double *t = nullptr;
+    if (c->kern == 3) {
+        VEC_OR_FAIL(tv, tmpi);
+        t = tv;
+    }
+    auto enqueue = [&]() -> int {
+        WHB_TRY(imp_apply_enqueue(c, p, ap, s, t));                     // Ap = A p
+        WHB_TRY(cg_dot(c, p, ap, 0));                                   // pAp, alpha = rz / pAp
+        imp::cg_update_kernel<<<kRedBlocks, kRedThreads, 0, c->stream>>>(owned(x, c), owned(r, c), owned(p, c),
+                                                                         owned(ap, c), c->d_cg, owned_elems(c));
+        c->launches++;
+        WHB_TRY(cg_dot(c, r, r, 1));                                    // rnorm^2
+        WHB_TRY(precond_enqueue(c, r, z, precond));                     // z = M r
+        WHB_TRY(cg_dot(c, r, z, 2));                                    // rz_new, beta, rz = rz_new
+        imp::cg_dir_kernel<<<kRedBlocks, kRedThreads, 0, c->stream>>>(owned(z, c), owned(p, c), c->d_cg,
+                                                                      owned_elems(c));
+        c->launches++;
+        WHB_CUDA(cudaMemcpyAsync(c->h_red, c->d_cg, 4 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        WHB_CUDA(cudaGetLastError());
+        return 0;
+    };
+    if (!c->use_graphs) {
+        WHB_TRY(enqueue());
+    } else {
+        auto key = std::make_tuple(xi, ri, zi, pi, api, tmpi, precond, s);
+        auto it = c->cg_graphs.find(key);
+        if (it == c->cg_graphs.end()) {
+            cudaGraph_t g;
+            const int64_t l0 = c->launches;
+            WHB_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+            int rc = enqueue();
+            cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+            if (rc) return rc;
+            if (e != cudaSuccess) return fail(WHB_E_CUDA, std::string("capture: ") + cudaGetErrorString(e));
+            cudaGraphExec_t ge;
+            e = cudaGraphInstantiate(&ge, g, 0);
+            cudaGraphDestroy(g);
+            if (e != cudaSuccess) return fail(WHB_E_CUDA, std::string("instantiate: ") + cudaGetErrorString(e));
+            c->graph_kernels[std::make_tuple(-2, 0, (const void *)ge)] = c->launches - l0;
+            c->launches = l0;
+            it = c->cg_graphs.emplace(key, ge).first;
+        }
+        WHB_CUDA(cudaGraphLaunch(it->second, c->stream));
+        c->launches += c->graph_kernels[std::make_tuple(-2, 0, (const void *)it->second)];
+    }
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
+    *pap = c->h_red[imp::CG_PAP];
+    *rr = c->h_red[imp::CG_RR];
     return 0;
 }
 

@@ -15,8 +15,10 @@ the grid's whb context.  The solver is chosen exactly as the reference's
   one CUDA graph;
 * anything else (3D, periodic, uncoarsenable): plain CG.
 
-The CG loop mirrors ``cg_solve`` line by line on the host; vectors, the
-operator, the V-cycle and the reductions are on the device.  Elementwise
+The CG loop mirrors ``cg_solve``'s control flow on the host (convergence and
+breakdown tests); each iteration's arithmetic — operator, V-cycle, dots and
+the alpha/beta scalars — is one device graph (``whb_cg_iterate``) with one
+readback of p.Ap and r.r.  Elementwise
 values follow the reference's operation order; dots use the device's
 fixed-order tree instead of BLAS, so iterates agree with the reference to the
 inner tolerance (1e-12 relative per solve), not bitwise — the contract is
@@ -145,12 +147,6 @@ class DeviceImplicitSolver:
         """y = x - (0.5*dt**2) * c^2 L_h x  (timestep.py:225-226)."""
         self.ctx.imp_apply(x, y, self.s, self.tmp)
 
-    def _precondition(self, r, z):
-        if self.precond == "mg":
-            self.ctx.mg_vcycle(r, z)   # MultigridHierarchy.preconditioner (linalg.py:342-344)
-        else:
-            self.ctx.tri_solve(r, z)   # tri_precond (timestep.py:202-209)
-
     def solve(self, rhs, guess, x) -> int:
         """x = A^{-1} rhs from the initial guess (cg_solve, linalg.py:62-99, or the direct
         tridiagonal solve); returns the iteration count and raises like the reference."""
@@ -166,31 +162,21 @@ class DeviceImplicitSolver:
         ctx.copy(guess, x)
         self.apply(x, self.ap)
         ctx.sub_into(rhs, self.ap, self.r)  # r = b - A(x)
-        z = self.r if self.precond is None else self.z
-        if self.precond is not None:
-            self._precondition(self.r, z)
-        ctx.copy(z, self.p)
-        rz = ctx.dot(self.r, z)
-        rnorm = math.sqrt(ctx.dot(self.r, self.r))
+        pre = {None: 0, "mg": 1, "tri": 2}[self.precond]
+        z = self.r if pre == 0 else self.z
+        # z = M r, p = z, rz = r.z on the device; rnorm = ||r||
+        rnorm = math.sqrt(ctx.cg_begin(self.r, z, self.p, pre))
         k = 0
         converged = False
         for k in range(self.maxit):
             if rnorm <= self.tol * bnorm:
                 converged = True
                 break
-            self.apply(self.p, self.ap)
-            pap = ctx.dot(self.p, self.ap)
+            # Ap, alpha = rz/pAp, x += alpha p, r -= alpha Ap, z = M r, beta, p = z + beta p: one graph
+            pap, rr = ctx.cg_iterate(x, self.r, z, self.p, self.ap, self.tmp, self.s, pre)
             if pap <= 0.0 or not math.isfinite(pap):
                 break
-            alpha = rz / pap
-            ctx.axpy(alpha, self.p, x)
-            ctx.axpy(-alpha, self.ap, self.r)
-            rnorm = math.sqrt(ctx.dot(self.r, self.r))
-            if self.precond is not None:
-                self._precondition(self.r, z)
-            rz_new = ctx.dot(self.r, z)
-            ctx.xpay(z, rz_new / rz, self.p)
-            rz = rz_new
+            rnorm = math.sqrt(rr)
         else:
             k = self.maxit
             converged = rnorm <= self.tol * bnorm

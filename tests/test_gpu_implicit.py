@@ -132,3 +132,26 @@ def test_implicit_against_oracle_larger(gpu_available, dim, cells, bcs, order, o
     ref, solver = IO.wave_solve_implicit(v0, np.array(wh.GridField.from_values(g, f).values), g.spacing,
                                          [bcs] * dim, order, omega, n_t)
     assert relerr(out, ref) <= TOL, relerr(out, ref)
+
+
+@pytest.mark.parametrize("cells", [(256, 256), (512, 128), (128, 64)])
+def test_vcycle_single_cta_coarse_path_bitwise(gpu_available, monkeypatch, cells):
+    """The single-CTA coarse sub-cycle (shared memory) computes exactly what the per-level
+    kernels compute: one V-cycle both ways, bitwise."""
+    from paper_2504_03074_b200.device import DeviceProblem
+    from paper_2504_03074_b200.implicit import DeviceImplicitSolver
+
+    g = wh.build_grid(2, [(0.0, 1.0)] * 2, cells, "dirichlet")
+    dt = wh.correct_implicit(20.0, 10).dt
+    r = np.random.default_rng(5).standard_normal(g.shape)
+    outs = []
+    for env in ("1", "0"):
+        monkeypatch.setenv("WHB_MG_COARSE_CTA", env)
+        dp = DeviceProblem(g)
+        s = DeviceImplicitSolver(dp.ctx, g, 2, 1.0, dt)
+        dp.ctx.vec_upload(s.r, r)
+        dp.ctx.mg_vcycle(s.r, s.z)
+        outs.append(dp.ctx.vec_download(s.z))
+        dp.close()
+    assert np.array_equal(outs[0], outs[1])
+    assert np.any(outs[0] != 0.0)
