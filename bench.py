@@ -18,6 +18,10 @@ cpu_baseline = numpy restatement of the reference (1 core), bounded sample
 --impl reference: the C OpenMP restatement of the reference on all host cores
              (the reference is pure numpy; oracle/ holds its bitwise restatement)
 
+--workload imp2: the implicit (trapezoidal) path of SURVEY 8(f) rank 4 — 2D 2049^2,
+omega = 50.5, N_t = 20, 8 seeded Gaussians; each step is one implicit WaveHoltz
+iteration (20 implicit steps, each a multigrid-preconditioned CG solve).
+
 N > 1 (torchrun): configs 1/2 — every rank solves its own copy (independent
 problems, no data-path collective, "scaling": "weak"); config 5 — the 64
 frequencies are LPT-sharded across ranks ("strong"); configs 3/4 — z-slab
@@ -416,6 +420,159 @@ def run_slab(args, dist, ws, rank, local):
         print(json.dumps(line))
 
 
+# ------------------------------------------------------------------------------------------
+# implicit path
+
+IMP2 = {"cells": 2048, "omega": 50.5, "n_t": 20, "gauss": 8, "iterations": 5}
+
+
+def mg_vcycle_bytes(cells):
+    """Algorithmic HBM bytes of one V-cycle (nu1 = nu2 = 2) summed over the levels above the
+    single-CTA coarse sub-cycle: per point of a level, 8 red-black colour sweeps x 12 B (read b and
+    the other colour's u, write u; each over half the points), residual + restriction 20 B (read u,
+    b; write coarse b, u), prolongation 18 B (read coarse e, read/write u)."""
+    n, total = cells, 0.0
+    while n > 64:
+        total += (n + 1) ** 2 * (8 * 12 + 20 + 18)
+        n //= 2
+    return total
+
+
+def build_imp2():
+    import paper_2504_03074_b200 as wh
+
+    g = wh.build_grid(2, [(0.0, 1.0)] * 2, [IMP2["cells"]] * 2, "dirichlet")
+    f = wh.multi_gaussian_source(g, IMP2["omega"], IMP2["gauss"], seed=0)
+    cfg = wh.FilterConfig(omega=IMP2["omega"], periods=1, steps_per_period=IMP2["n_t"], mode="implicit")
+    corr = wh.correct_implicit(IMP2["omega"], IMP2["n_t"])
+    return g, f, cfg, corr
+
+
+def cpu_baseline_implicit(g, f, target_s=12.0):
+    from oracle import implicit_oracle as IO
+
+    fv = np.array(f.values)
+    v = np.zeros_like(fv)
+    bcs = ["dirichlet"] * 2
+    t0 = time.perf_counter()
+    _, solver = IO.wave_solve_implicit(v, fv, g.spacing, bcs, 2, IMP2["omega"], IMP2["n_t"], max_steps=1)
+    t1 = time.perf_counter() - t0
+    m = int(max(1, min(IMP2["n_t"], target_s / max(t1, 1e-6))))
+    t0 = time.perf_counter()
+    _, solver = IO.wave_solve_implicit(v, fv, g.spacing, bcs, 2, IMP2["omega"], IMP2["n_t"], max_steps=m)
+    dt = time.perf_counter() - t0
+    return {"value": g.size * m / dt / 1e9, "unit": "Gpts/s", "cores": 1, "kind": "port",
+            "sample": f"the first {m} of {IMP2['n_t']} implicit steps of one WaveHoltz iteration on the "
+                      f"{'x'.join(map(str, g.shape))} grid through oracle/implicit_oracle.py (bitwise restatement of "
+                      f"the reference's MG-preconditioned CG, numpy, 1 core); {solver.inner} CG iterations, {dt:.2f} s"}
+
+
+def run_implicit(args, dist, ws, rank, local):
+    import torch
+
+    import paper_2504_03074_b200 as wh
+    from paper_2504_03074_b200 import _native
+    from paper_2504_03074_b200.device import device_problem
+    from paper_2504_03074_b200.implicit import implicit_solver_for
+
+    torch.cuda.set_device(local)
+    g, f, cfg, corr = build_imp2()
+    prob = wh.HelmholtzProblem(g, 2, 1.0, IMP2["omega"], f)
+    dp = device_problem(g, device=local)
+    ctx = dp.ctx
+    K, W = args.steps, args.warmup
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=f"cuda:{local}")
+    for _ in range(max(1, W)):
+        wh.fpi_solve(prob, cfg, tol=-1.0, maxit=1)
+    torch.cuda.synchronize()
+    barrier(dist)
+    sampler = ClockSampler(local).start()
+    l0 = ctx.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    v, run = wh.fpi_solve(prob, cfg, tol=-1.0, maxit=K)  # K implicit iterations from v = 0
+    e1.record(stream)
+    e1.synchronize()
+    clocks = sampler.stop()
+    launches = ctx.launch_count() - l0
+    dev_s = max_over_ranks(dist, e0.elapsed_time(e1) / 1e3)
+    units = g.size * IMP2["n_t"] * K * max(1, ws)
+    value = units / dev_s / 1e9
+    # dominant unit: the multigrid V-cycle graph (timed alone with events on the context stream)
+    solver = implicit_solver_for(dp, g, 2, 1.0, corr.dt)
+    ctx.vec_upload(solver.r, np.random.default_rng(0).standard_normal(g.shape))
+    for _ in range(3):
+        ctx.mg_vcycle(solver.r, solver.z)
+    reps = 30
+    v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    v0.record(stream)
+    for _ in range(reps):
+        ctx.mg_vcycle(solver.r, solver.z)
+    v1.record(stream)
+    v1.synchronize()
+    vc_s = v0.elapsed_time(v1) / 1e3 / reps
+    vbytes = mg_vcycle_bytes(IMP2["cells"])
+    peak, peak_src = peaks()
+    achieved = vbytes / vc_s / 1e9
+    cg_per_step = run.inner_iterations / (K * IMP2["n_t"])
+    e2e = None
+    if not args.no_e2e:
+        # through the public surface with host fields: wave_solve_filtered(v, f) per iteration
+        op = wh.DiscreteOperator(g, 2, 1.0)
+        vf = wh.GridField.zeros(g)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(K):
+            vf = wh.wave_solve_filtered(vf, f, cfg, corr, op)
+        torch.cuda.synchronize()
+        te = max_over_ranks(dist, time.perf_counter() - t0)
+        e2e = {"value": units / te / 1e9, "unit": "Gpts/s", "h2d_bytes_per_step": g.size * 8,
+               "d2h_bytes_per_step": g.size * 8, "iters_per_s": K / te,
+               "api": "paper_2504_03074_b200.wave_solve_filtered (implicit mode) with host GridFields"}
+    cpu = None if (rank != 0 or ws != 1 or args.no_cpu_baseline) else cpu_baseline_implicit(g, f)
+    if rank == 0:
+        line = {
+            "metric": "implicit WaveHoltz Gpts/s (grid-point updates per s) and iters/s", "value": value,
+            "unit": "Gpts/s", "n_gpus": ws, "steps": K, "warmup": W, "ms_per_step": dev_s * 1e3 / K,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (BASELINE forcing recipe, 8 Gaussians, seed 0)",
+            "config": {"workload": "imp2", "grid": list(g.shape), "omega": IMP2["omega"], "N_t": IMP2["n_t"],
+                       "mode": "implicit (trapezoidal), MG-preconditioned CG to 1e-12 per step",
+                       "iterations": K, "cg_iterations_per_step": cg_per_step,
+                       "l2": "working set (~15 fields of 33.6 MB) far above L2",
+                       "parallelism": f"independent replicas x{ws}" if ws > 1 else "single GPU"},
+            "iters_per_s": K / dev_s,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                         "kernel": "multigrid V-cycle (CUDA graph: red-black GS sweeps, fused residual+restriction, "
+                                   "prolongation per level; levels <= 64 cells in one shared-memory CTA)",
+                         "bytes_per_vcycle": vbytes, "vcycle_us": vc_s * 1e6,
+                         "note": "algorithmic bytes of one V-cycle (see bench.mg_vcycle_bytes) / its device time "
+                                 "(CUDA events around graph replays); the V-cycle is the preconditioner of every "
+                                 "CG iteration"},
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": launches,
+            "residuals": {"first": run.residuals[0], "last": run.residuals[-1]}, "impl": "ours",
+        }
+        print(json.dumps(line))
+
+
+def run_reference_implicit(args, ws, rank):
+    if rank != 0:
+        return
+    g, f, cfg, corr = build_imp2()
+    cpu = cpu_baseline_implicit(g, f, target_s=20.0)
+    line = {
+        "metric": "implicit WaveHoltz Gpts/s (grid-point updates per s) and iters/s", "value": cpu["value"],
+        "unit": "Gpts/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE forcing recipe, 8 Gaussians, seed 0)",
+        "config": {"workload": "imp2", "grid": list(g.shape), "omega": IMP2["omega"], "N_t": IMP2["n_t"]},
+        "impl": "reference", "cpu_baseline": cpu,
+        "e2e": {"value": cpu["value"], "unit": "Gpts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
 def run_ours(args, dist, ws, rank, local):
     import torch
 
@@ -624,7 +781,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS) + ["cfg5"])
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS) + ["cfg5", "imp2"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--decomp", default="slab", choices=["slab", "replicas"],
                     help="N > 1 on configs 3/4: z-slab decomposition (default) or independent replicas")
@@ -632,14 +789,20 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.steps is None:
-        args.steps = 20 if args.workload == "cfg5" else WORKLOADS[args.workload][4]
+        args.steps = {"cfg5": 20, "imp2": IMP2["iterations"]}.get(args.workload) or WORKLOADS[args.workload][4]
     ws, rank, local = dist_env()
     if args.impl == "reference":
-        run_reference(args, ws, rank)
+        if args.workload == "imp2":
+            run_reference_implicit(args, ws, rank)
+        else:
+            run_reference(args, ws, rank)
         return
     dist = init_dist(ws)
     try:
-        run_ours(args, dist, ws, rank, local)
+        if args.workload == "imp2":
+            run_implicit(args, dist, ws, rank, local)
+        else:
+            run_ours(args, dist, ws, rank, local)
     finally:
         if dist is not None:
             dist.destroy_process_group()

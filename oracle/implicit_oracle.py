@@ -244,8 +244,10 @@ class ImplicitSolver:
         return x
 
 
-def wave_solve_implicit(v, f, spacing, bcs, order, omega, n_t, c=1.0, solver=None, implicit_first_step=True):
-    """The implicit branch of wave_solve_filtered (timestep.py:270-301), N_p = 1."""
+def wave_solve_implicit(v, f, spacing, bcs, order, omega, n_t, c=1.0, solver=None, implicit_first_step=True,
+                        max_steps=None):
+    """The implicit branch of wave_solve_filtered (timestep.py:270-301), N_p = 1.
+    ``max_steps`` stops after that many steps (a bounded timing sample; output then partial)."""
     n_t, dt, wt = correct_implicit(omega, n_t)
     alpha = alpha_d(wt * dt)
     solver = solver or ImplicitSolver(v.shape, spacing, bcs, order, c, dt)
@@ -254,7 +256,7 @@ def wave_solve_implicit(v, f, spacing, bcs, order, omega, n_t, c=1.0, solver=Non
     acc = (math.cos(0.0) - 0.5 * alpha) * 0.5 * w
     cos_fac = math.cos(wt * dt)
     t = 0.0
-    for n in range(n_t):
+    for n in range(n_t if max_steps is None else min(n_t, max_steps)):
         if n == 0 and not implicit_first_step:
             w_next = w + 0.5 * dt**2 * (lap(w) - f * math.cos(wt * dt))
         elif n == 0:

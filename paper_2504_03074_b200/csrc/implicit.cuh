@@ -24,37 +24,35 @@ namespace imp {
 template <bool A0, bool A1>
 __global__ void apply_kernel(Geom g, const double *__restrict__ x, double *__restrict__ y, double s, int lp0,
                              int lp1, int up0, int up1) {
-    const long long total = (long long)(lp1 - lp0) * g.S0;
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-         t += (long long)gridDim.x * blockDim.x) {
-        const long long pl = t / g.S0;
-        const long long r = t - pl * g.S0;
-        const int j = (int)(r / g.P);
-        const int k = (int)(r - (long long)j * g.P);
-        if (k >= g.n2) continue;  // row padding stays 0
-        const int plane = lp0 + (int)pl;
-        const long long p = (long long)plane * g.S0 + r;
-        const double xc = x[p];
-        double lap = 0.0;
-        const bool in = (k >= 1 && k < g.n2 - 1) && (!A1 || (j >= g.j_lo && j < g.j_hi)) &&
-                        (!A0 || (plane >= up0 && plane < up1));
-        if (in) {
-            if (A0) {
-                lap = whb_add(lap, whb_mul(g.clo0, x[p - g.S0]));
-                lap = whb_add(lap, whb_mul(g.cmid0, xc));
-                lap = whb_add(lap, whb_mul(g.clo0, x[p + g.S0]));
+    // one block per row (plane, j); threads along the contiguous axis: no index divisions
+    const long long nrows = (long long)(lp1 - lp0) * g.n1;
+    for (long long row = blockIdx.x; row < nrows; row += gridDim.x) {
+        const int plane = lp0 + (int)(row / g.n1);
+        const int j = (int)(row - (long long)(plane - lp0) * g.n1);
+        const bool row_in = (!A1 || (j >= g.j_lo && j < g.j_hi)) && (!A0 || (plane >= up0 && plane < up1));
+        const long long base = (long long)plane * g.S0 + (long long)j * g.P;
+        for (int k = threadIdx.x; k < g.n2; k += blockDim.x) {
+            const long long p = base + k;
+            const double xc = x[p];
+            double lap = 0.0;
+            if (row_in && k >= 1 && k < g.n2 - 1) {
+                if (A0) {
+                    lap = whb_add(lap, whb_mul(g.clo0, x[p - g.S0]));
+                    lap = whb_add(lap, whb_mul(g.cmid0, xc));
+                    lap = whb_add(lap, whb_mul(g.clo0, x[p + g.S0]));
+                }
+                if (A1) {
+                    lap = whb_add(lap, whb_mul(g.clo1, x[p - g.P]));
+                    lap = whb_add(lap, whb_mul(g.cmid1, xc));
+                    lap = whb_add(lap, whb_mul(g.clo1, x[p + g.P]));
+                }
+                lap = whb_add(lap, whb_mul(g.clo2, x[p - 1]));
+                lap = whb_add(lap, whb_mul(g.cmid2, xc));
+                lap = whb_add(lap, whb_mul(g.clo2, x[p + 1]));
+                lap = whb_mul(lap, g.c2);  // out *= c**2 (grid.py:366)
             }
-            if (A1) {
-                lap = whb_add(lap, whb_mul(g.clo1, x[p - g.P]));
-                lap = whb_add(lap, whb_mul(g.cmid1, xc));
-                lap = whb_add(lap, whb_mul(g.clo1, x[p + g.P]));
-            }
-            lap = whb_add(lap, whb_mul(g.clo2, x[p - 1]));
-            lap = whb_add(lap, whb_mul(g.cmid2, xc));
-            lap = whb_add(lap, whb_mul(g.clo2, x[p + 1]));
-            lap = whb_mul(lap, g.c2);  // out *= c**2 (grid.py:366)
+            y[p] = whb_sub(xc, whb_mul(s, lap));
         }
-        y[p] = whb_sub(xc, whb_mul(s, lap));
     }
 }
 
@@ -151,58 +149,20 @@ struct Lev {
     double gx, gy, diag;
 };
 
-// r = b - A u (A u = 0 at boundary points) over the whole level (linalg.py:206-217, 333)
-__global__ void residual_kernel(Lev L, const double *__restrict__ u, const double *__restrict__ b,
-                                double *__restrict__ r) {
-    const long long total = (long long)(L.nx + 1) * (L.ny + 1);
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-         t += (long long)gridDim.x * blockDim.x) {
-        const int i = (int)(t / (L.ny + 1));
-        const int j = (int)(t - (long long)i * (L.ny + 1));
-        const long long p = (long long)i * L.rs + j;
-        double au = 0.0;
-        if (i >= 1 && i < L.nx && j >= 1 && j < L.ny) {
-            au = whb_sub(whb_sub(whb_mul(L.diag, u[p]), whb_mul(L.gx, whb_add(u[p - L.rs], u[p + L.rs]))),
-                         whb_mul(L.gy, whb_add(u[p - 1], u[p + 1])));
-        }
-        r[p] = whb_sub(b[p], au);
-    }
-}
-
-// one red-black colour: points with (i + j) % 2 == colour (linalg.py:230-238)
+// one red-black colour: points with (i + j) % 2 == colour (linalg.py:230-238); one block per row
 __global__ void gs_color_kernel(Lev L, double *__restrict__ u, const double *__restrict__ b, int color) {
     const int half = L.ny / 2 + 1;
-    const long long total = (long long)(L.nx - 1) * half;
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-         t += (long long)gridDim.x * blockDim.x) {
-        const int i = 1 + (int)(t / half);
-        const int m = (int)(t - (long long)(i - 1) * half);
-        const int j = 2 * m + ((i + color) & 1);
-        if (j < 1 || j >= L.ny) continue;
-        const long long p = (long long)i * L.rs + j;
-        const double v = whb_add(whb_add(b[p], whb_mul(L.gx, whb_add(u[p - L.rs], u[p + L.rs]))),
-                                 whb_mul(L.gy, whb_add(u[p - 1], u[p + 1])));
-        u[p] = __ddiv_rn(v, L.diag);
-    }
-}
-
-// full-weighting restriction of the fine residual r onto the coarse level (boundary 0)
-// (linalg.py:247-257)
-__global__ void restrict_kernel(Lev F, const double *__restrict__ r, Lev C, double *__restrict__ rc) {
-    const long long total = (long long)(C.nx + 1) * (C.ny + 1);
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-         t += (long long)gridDim.x * blockDim.x) {
-        const int I = (int)(t / (C.ny + 1));
-        const int J = (int)(t - (long long)I * (C.ny + 1));
-        double v = 0.0;
-        if (I >= 1 && I < C.nx && J >= 1 && J < C.ny) {
-            const long long p = (long long)(2 * I) * F.rs + 2 * J;
-            const long long rs = F.rs;
-            const double edges = whb_add(whb_add(whb_add(r[p - rs], r[p + rs]), r[p - 1]), r[p + 1]);
-            const double corners = whb_add(whb_add(whb_add(r[p - rs - 1], r[p - rs + 1]), r[p + rs - 1]), r[p + rs + 1]);
-            v = __ddiv_rn(whb_add(whb_add(whb_mul(4.0, r[p]), whb_mul(2.0, edges)), corners), 16.0);
+    for (int i = 1 + blockIdx.x; i < L.nx; i += gridDim.x) {
+        const int j0 = (i + color) & 1;
+        const long long base = (long long)i * L.rs;
+        for (int m = threadIdx.x; m < half; m += blockDim.x) {
+            const int j = 2 * m + j0;
+            if (j < 1 || j >= L.ny) continue;
+            const long long p = base + j;
+            const double v = whb_add(whb_add(b[p], whb_mul(L.gx, whb_add(u[p - L.rs], u[p + L.rs]))),
+                                     whb_mul(L.gy, whb_add(u[p - 1], u[p + 1])));
+            u[p] = __ddiv_rn(v, L.diag);
         }
-        rc[(long long)I * C.rs + J] = v;
     }
 }
 
@@ -218,46 +178,43 @@ __device__ __forceinline__ double fine_resid(const Lev &F, const double *__restr
 
 __global__ void resid_restrict_kernel(Lev F, const double *__restrict__ u, const double *__restrict__ b, Lev C,
                                       double *__restrict__ bc, double *__restrict__ uc) {
-    const long long total = (long long)(C.nx + 1) * (C.ny + 1);
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-         t += (long long)gridDim.x * blockDim.x) {
-        const int I = (int)(t / (C.ny + 1));
-        const int J = (int)(t - (long long)I * (C.ny + 1));
-        double v = 0.0;
-        if (I >= 1 && I < C.nx && J >= 1 && J < C.ny) {
-            const long long p = (long long)(2 * I) * F.rs + 2 * J;
-            const long long rs = F.rs;
-            const double edges = whb_add(whb_add(whb_add(fine_resid(F, u, b, p - rs), fine_resid(F, u, b, p + rs)),
-                                                 fine_resid(F, u, b, p - 1)),
-                                         fine_resid(F, u, b, p + 1));
-            const double corners =
-                whb_add(whb_add(whb_add(fine_resid(F, u, b, p - rs - 1), fine_resid(F, u, b, p - rs + 1)),
-                                fine_resid(F, u, b, p + rs - 1)),
-                        fine_resid(F, u, b, p + rs + 1));
-            v = __ddiv_rn(whb_add(whb_add(whb_mul(4.0, fine_resid(F, u, b, p)), whb_mul(2.0, edges)), corners), 16.0);
+    for (int I = blockIdx.x; I <= C.nx; I += gridDim.x) {
+        for (int J = threadIdx.x; J <= C.ny; J += blockDim.x) {
+            double v = 0.0;
+            if (I >= 1 && I < C.nx && J >= 1 && J < C.ny) {
+                const long long p = (long long)(2 * I) * F.rs + 2 * J;
+                const long long rs = F.rs;
+                const double edges = whb_add(whb_add(whb_add(fine_resid(F, u, b, p - rs), fine_resid(F, u, b, p + rs)),
+                                                     fine_resid(F, u, b, p - 1)),
+                                             fine_resid(F, u, b, p + 1));
+                const double corners =
+                    whb_add(whb_add(whb_add(fine_resid(F, u, b, p - rs - 1), fine_resid(F, u, b, p - rs + 1)),
+                                    fine_resid(F, u, b, p + rs - 1)),
+                            fine_resid(F, u, b, p + rs + 1));
+                v = __ddiv_rn(whb_add(whb_add(whb_mul(4.0, fine_resid(F, u, b, p)), whb_mul(2.0, edges)), corners),
+                              16.0);
+            }
+            const long long q = (long long)I * C.rs + J;
+            bc[q] = v;
+            uc[q] = 0.0;
         }
-        const long long q = (long long)I * C.rs + J;
-        bc[q] = v;
-        uc[q] = 0.0;
     }
 }
 
-// u += prolong(ec) (bilinear, linalg.py:259-275, 337)
+// u += prolong(ec) (bilinear, linalg.py:259-275, 337); one block per fine row
 __global__ void prolong_add_kernel(Lev F, double *__restrict__ u, Lev C, const double *__restrict__ ec) {
-    const long long total = (long long)(F.nx + 1) * (F.ny + 1);
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-         t += (long long)gridDim.x * blockDim.x) {
-        const int i = (int)(t / (F.ny + 1));
-        const int j = (int)(t - (long long)i * (F.ny + 1));
-        const int a = i >> 1, bq = j >> 1;
-        const long long q = (long long)a * C.rs + bq;
-        double e;
-        if (!(i & 1) && !(j & 1)) e = ec[q];
-        else if ((i & 1) && !(j & 1)) e = whb_mul(0.5, whb_add(ec[q], ec[q + C.rs]));
-        else if (!(i & 1) && (j & 1)) e = whb_mul(0.5, whb_add(ec[q], ec[q + 1]));
-        else e = whb_mul(0.25, whb_add(whb_add(whb_add(ec[q], ec[q + C.rs]), ec[q + 1]), ec[q + C.rs + 1]));
-        const long long p = (long long)i * F.rs + j;
-        u[p] = whb_add(u[p], e);
+    for (int i = blockIdx.x; i <= F.nx; i += gridDim.x) {
+        const long long qrow = (long long)(i >> 1) * C.rs;
+        const long long prow = (long long)i * F.rs;
+        for (int j = threadIdx.x; j <= F.ny; j += blockDim.x) {
+            const long long q = qrow + (j >> 1);
+            double e;
+            if (!(i & 1) && !(j & 1)) e = ec[q];
+            else if ((i & 1) && !(j & 1)) e = whb_mul(0.5, whb_add(ec[q], ec[q + C.rs]));
+            else if (!(i & 1) && (j & 1)) e = whb_mul(0.5, whb_add(ec[q], ec[q + 1]));
+            else e = whb_mul(0.25, whb_add(whb_add(whb_add(ec[q], ec[q + C.rs]), ec[q + 1]), ec[q + C.rs + 1]));
+            u[prow + j] = whb_add(u[prow + j], e);
+        }
     }
 }
 

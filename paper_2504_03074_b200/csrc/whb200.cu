@@ -1642,17 +1642,12 @@ void free_tri(whb_ctx *c) {
     c->tri = nullptr;
 }
 
-int grid_blocks(long long n) {
-    return (int)std::max<long long>(1, std::min<long long>(4 * 148, (n + 255) / 256));
-}
-
 // one V-cycle from u = 0 on level `l` (linalg.py:322-339); u of the coarsest level is the
 // coarse solve of b
 int mg_enqueue(whb_ctx *c, int l) {
     MGData &M = *c->mg;
     MGLevelBuf &B = M.lv[l];
     const imp::Lev &L = B.lev;
-    const long long pts = (long long)(L.nx + 1) * (L.ny + 1);
     if (l == M.lc) {  // the rest of the cycle in one thread block (implicit.cuh)
         imp::coarse_cycle_kernel<<<1, 1024, M.cc_smem, c->stream>>>(M.cc, B.b, B.u, M.ainv);
         c->launches++;
@@ -1666,19 +1661,17 @@ int mg_enqueue(whb_ctx *c, int l) {
         WHB_CUDA(cudaGetLastError());
         return 0;
     }
-    const long long gs_pts = (long long)(L.nx - 1) * (L.ny / 2 + 1);
     auto gs = [&](int color) {
-        imp::gs_color_kernel<<<grid_blocks(gs_pts), 256, 0, c->stream>>>(L, B.u, B.b, color);
+        imp::gs_color_kernel<<<std::max(1, L.nx - 1), 256, 0, c->stream>>>(L, B.u, B.b, color);
         c->launches++;
     };
     for (int k = 0; k < M.nu1; ++k) { gs(0); gs(1); }
     // r = b - A u, restricted onto the next level, whose iterate starts at 0 (linalg.py:333-335)
     MGLevelBuf &N = M.lv[l + 1];
-    const long long cpts = (long long)(N.lev.nx + 1) * (N.lev.ny + 1);
-    imp::resid_restrict_kernel<<<grid_blocks(cpts), 256, 0, c->stream>>>(L, B.u, B.b, N.lev, N.b, N.u);
+    imp::resid_restrict_kernel<<<N.lev.nx + 1, 128, 0, c->stream>>>(L, B.u, B.b, N.lev, N.b, N.u);
     c->launches++;
     WHB_TRY(mg_enqueue(c, l + 1));
-    imp::prolong_add_kernel<<<grid_blocks(pts), 256, 0, c->stream>>>(L, B.u, N.lev, N.u);
+    imp::prolong_add_kernel<<<L.nx + 1, 256, 0, c->stream>>>(L, B.u, N.lev, N.u);
     c->launches++;
     for (int k = 0; k < M.nu2; ++k) { gs(1); gs(0); }
     WHB_CUDA(cudaGetLastError());
@@ -1703,7 +1696,9 @@ int imp_apply_enqueue(whb_ctx *c, const double *x, double *y, double s, double *
     } else {
         auto kfn = c->act1 ? imp::apply_kernel<true, true>
                            : (c->act0 ? imp::apply_kernel<true, false> : imp::apply_kernel<false, false>);
-        kfn<<<kRedBlocks, kRedThreads, 0, c->stream>>>(c->geom, x, y, s, GH, GH + (int)c->nloc, c->upd_lo, c->upd_hi);
+        const long long rows = (long long)c->nloc * c->gshape[1];
+        kfn<<<(int)std::min<long long>(rows, 1 << 20), 256, 0, c->stream>>>(c->geom, x, y, s, GH, GH + (int)c->nloc,
+                                                                          c->upd_lo, c->upd_hi);
         c->launches++;
     }
     WHB_CUDA(cudaGetLastError());
