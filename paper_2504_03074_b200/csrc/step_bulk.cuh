@@ -79,22 +79,40 @@ constexpr size_t bulk_smem_bytes() {
 }
 
 // One point of the fused update, reference order (grid.py:357-366, timestep.py:137-140, 284-300).
-template <int KIND, bool ZF, bool A1>
+// SQ: every axis carries the same taps (square / cubic cells, clo_a and cmid_a bitwise equal):
+// the centre product cmid*wc is formed once and added per axis — the same values, in the same
+// order, as the reference's per-axis products.
+template <int KIND, bool ZF, bool A1, bool SQ = false>
 __device__ __forceinline__ double update_point(const Geom &g, double wm, double wc, double wp, double yl,
                                                double yh, double xl, double xh, double fv, double wpv,
                                                double h, double cosn) {
     double lap = 0.0;
-    lap = whb_add(lap, whb_mul(g.clo0, wm));
-    lap = whb_add(lap, whb_mul(g.cmid0, wc));
-    lap = whb_add(lap, whb_mul(g.clo0, wp));
-    if (A1) {
-        lap = whb_add(lap, whb_mul(g.clo1, yl));
-        lap = whb_add(lap, whb_mul(g.cmid1, wc));
-        lap = whb_add(lap, whb_mul(g.clo1, yh));
+    if constexpr (SQ) {
+        const double mc = whb_mul(g.cmid0, wc);
+        lap = whb_add(lap, whb_mul(g.clo0, wm));
+        lap = whb_add(lap, mc);
+        lap = whb_add(lap, whb_mul(g.clo0, wp));
+        if (A1) {
+            lap = whb_add(lap, whb_mul(g.clo0, yl));
+            lap = whb_add(lap, mc);
+            lap = whb_add(lap, whb_mul(g.clo0, yh));
+        }
+        lap = whb_add(lap, whb_mul(g.clo0, xl));
+        lap = whb_add(lap, mc);
+        lap = whb_add(lap, whb_mul(g.clo0, xh));
+    } else {
+        lap = whb_add(lap, whb_mul(g.clo0, wm));
+        lap = whb_add(lap, whb_mul(g.cmid0, wc));
+        lap = whb_add(lap, whb_mul(g.clo0, wp));
+        if (A1) {
+            lap = whb_add(lap, whb_mul(g.clo1, yl));
+            lap = whb_add(lap, whb_mul(g.cmid1, wc));
+            lap = whb_add(lap, whb_mul(g.clo1, yh));
+        }
+        lap = whb_add(lap, whb_mul(g.clo2, xl));
+        lap = whb_add(lap, whb_mul(g.cmid2, wc));
+        lap = whb_add(lap, whb_mul(g.clo2, xh));
     }
-    lap = whb_add(lap, whb_mul(g.clo2, xl));
-    lap = whb_add(lap, whb_mul(g.cmid2, wc));
-    lap = whb_add(lap, whb_mul(g.clo2, xh));
     if (g.use_c2) lap = whb_mul(lap, g.c2);
     if (KIND == K_FIRST) {
         const double d = ZF ? lap : whb_sub(lap, fv);

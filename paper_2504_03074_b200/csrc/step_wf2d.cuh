@@ -58,11 +58,20 @@ constexpr size_t wf_smem_bytes() {
     return (size_t)ST * Lay<T, NW>::STAGE * sizeof(double) + 2 * ST * sizeof(uint64_t);
 }
 
+// Per-pass scalars of a single-member launch, passed as kernel parameters: the update chain
+// reads them straight from the constant bank instead of holding ~28 registers per thread.
+struct WfScal {
+    double h[5], cs[5], ca[5];  // level t = 1..T: dt^2 factor, forcing cos factor, filter weight
+    double acc0, osc;
+};
+
 // K1: kind of the first step of the pass (FIRST when s == 0); K2: kind of the last (LAST ends the solve).
-template <int T, int NW, int ST, int K1, int K2, bool ZF, int SKEW = 1>
+// PS: scalars from `ps` (one member per launch) instead of the member table.
+// SQ: square cells (both axes carry bitwise-equal taps): one centre product per point.
+template <int T, int NW, int ST, int K1, int K2, bool ZF, int SKEW = 1, bool PS = false, bool SQ = false>
 __global__ void __launch_bounds__(Lay<T, NW>::THREADS, 3)
     wf2d_kernel(Geom g, const Member *__restrict__ members, int member_off, int s, int i_begin, int i_end,
-                int chunk_len, int part_off) {
+                int chunk_len, int part_off, WfScal ps) {
     using L = Lay<T, NW>;
     constexpr int DL = wf_lag<SKEW>(T);  // output row lag
     static_assert(T % 2 == 0 && T >= 2 && T <= 12, "T even (pair-aligned output columns)");
@@ -141,12 +150,18 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, 3)
 #pragma unroll
         for (int t = 1; t <= T; ++t) {
             const bool first = (K1 == K_FIRST) && (t == 1);
-            hcoef[t] = first ? m.half_dt2 : m.dt2;
-            cosl[t] = first ? 1.0 : m.cos_f[s + t - 1];
-            cacc[t] = m.acc_c[s + t];
+            if constexpr (PS) {
+                hcoef[t] = ps.h[t];
+                cosl[t] = ps.cs[t];
+                cacc[t] = ps.ca[t];
+            } else {
+                hcoef[t] = first ? m.half_dt2 : m.dt2;
+                cosl[t] = first ? 1.0 : m.cos_f[s + t - 1];
+                cacc[t] = m.acc_c[s + t];
+            }
         }
-        const double acc0 = m.acc_c[0];
-        const double oscale = m.out_scale;
+        const double acc0 = PS ? ps.acc0 : m.acc_c[0];
+        const double oscale = PS ? ps.osc : m.out_scale;
         if constexpr (SKEW == 1) {
         // level queues: Q[t][0..2] = level t at rows (r-t-2, r-t-1, r-t); Q[0] = W^s
             double2 Q[T + 1][3];
@@ -200,14 +215,14 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, 3)
                     const bool firstk = (K1 == K_FIRST) && (t == 1);
                     double a, b;
                     if (firstk) {
-                        a = update_point<K_FIRST, ZF, false>(g, cm.x, cc.x, cp.x, 0.0, 0.0, xl, cc.y, fv.x, 0.0,
+                        a = update_point<K_FIRST, ZF, false, SQ>(g, cm.x, cc.x, cp.x, 0.0, 0.0, xl, cc.y, fv.x, 0.0,
                                                              hcoef[t], cosl[t]);
-                        b = update_point<K_FIRST, ZF, false>(g, cm.y, cc.y, cp.y, 0.0, 0.0, cc.x, xh, fv.y, 0.0,
+                        b = update_point<K_FIRST, ZF, false, SQ>(g, cm.y, cc.y, cp.y, 0.0, 0.0, cc.x, xh, fv.y, 0.0,
                                                              hcoef[t], cosl[t]);
                     } else {
-                        a = update_point<K_MID, ZF, false>(g, cm.x, cc.x, cp.x, 0.0, 0.0, xl, cc.y, fv.x, pv.x,
+                        a = update_point<K_MID, ZF, false, SQ>(g, cm.x, cc.x, cp.x, 0.0, 0.0, xl, cc.y, fv.x, pv.x,
                                                            hcoef[t], cosl[t]);
-                        b = update_point<K_MID, ZF, false>(g, cm.y, cc.y, cp.y, 0.0, 0.0, cc.x, xh, fv.y, pv.y,
+                        b = update_point<K_MID, ZF, false, SQ>(g, cm.y, cc.y, cp.y, 0.0, 0.0, cc.x, xh, fv.y, pv.y,
                                                            hcoef[t], cosl[t]);
                     }
                     const bool rin = (row >= g.i_lo) && (row < g.i_hi);
@@ -321,14 +336,14 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, 3)
                     if (!ZF) fv = *reinterpret_cast<const double2 *>(sr + 2 * L::SEGP + xs + 2 * lane);
                     double a, b;
                     if ((K1 == K_FIRST) && (t == 1)) {
-                        a = update_point<K_FIRST, ZF, false>(g, cm.x, cc.x, cp.x, 0.0, 0.0, xl, cc.y, fv.x, 0.0,
+                        a = update_point<K_FIRST, ZF, false, SQ>(g, cm.x, cc.x, cp.x, 0.0, 0.0, xl, cc.y, fv.x, 0.0,
                                                              hcoef[t], cosl[t]);
-                        b = update_point<K_FIRST, ZF, false>(g, cm.y, cc.y, cp.y, 0.0, 0.0, cc.x, xh, fv.y, 0.0,
+                        b = update_point<K_FIRST, ZF, false, SQ>(g, cm.y, cc.y, cp.y, 0.0, 0.0, cc.x, xh, fv.y, 0.0,
                                                              hcoef[t], cosl[t]);
                     } else {
-                        a = update_point<K_MID, ZF, false>(g, cm.x, cc.x, cp.x, 0.0, 0.0, xl, cc.y, fv.x, pv.x,
+                        a = update_point<K_MID, ZF, false, SQ>(g, cm.x, cc.x, cp.x, 0.0, 0.0, xl, cc.y, fv.x, pv.x,
                                                            hcoef[t], cosl[t]);
-                        b = update_point<K_MID, ZF, false>(g, cm.y, cc.y, cp.y, 0.0, 0.0, cc.x, xh, fv.y, pv.y,
+                        b = update_point<K_MID, ZF, false, SQ>(g, cm.y, cc.y, cp.y, 0.0, 0.0, cc.x, xh, fv.y, pv.y,
                                                            hcoef[t], cosl[t]);
                     }
                     const bool rin = (row >= g.i_lo) && (row < g.i_hi);

@@ -567,6 +567,7 @@ struct MemberHost {
     double *v = nullptr, *f = nullptr, *acc = nullptr, *out = nullptr;
     double *ring[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     double *cos_f = nullptr, *acc_c = nullptr, *partials = nullptr;
+    std::vector<double> h_cos, h_acc;  // host copies (per-pass kernel parameters)
     double half_dt2 = 0, dt2 = 0, out_scale = 0;
     int n_total = 0;
 };
@@ -803,10 +804,10 @@ constexpr int WF_NW = 4;
 // row, 2T + 4 stages); T = 2 the plain one.
 constexpr int WF_SKEW4 = 1;
 constexpr int WF_ST4 = wf2d::wf_lag<WF_SKEW4>(4) + 5;  // 9 stages, 3 CTAs/SM (measured: 7 stages at 4 CTAs/SM is 1.4 % slower)
-template <int T, int K1, int K2, bool ZF>
+template <int T, int K1, int K2, bool ZF, bool PS = false, bool SQ = false>
 auto wf_fn() {
-    if constexpr (T == 4) return wf2d::wf2d_kernel<4, WF_NW, WF_ST4, K1, K2, ZF, WF_SKEW4>;
-    else return wf2d::wf2d_kernel<T, WF_NW, T + 4, K1, K2, ZF, 1>;
+    if constexpr (T == 4) return wf2d::wf2d_kernel<4, WF_NW, WF_ST4, K1, K2, ZF, WF_SKEW4, PS, SQ>;
+    else return wf2d::wf2d_kernel<T, WF_NW, T + 4, K1, K2, ZF, 1, PS, SQ>;
 }
 
 template <int T>
@@ -820,6 +821,14 @@ cudaError_t wf_set_attrs(size_t smem) {
     set(wf_fn<T, K_MID, K_MID, false>());   set(wf_fn<T, K_MID, K_MID, true>());
     set(wf_fn<T, K_MID, K_LAST, false>());  set(wf_fn<T, K_MID, K_LAST, true>());
     set(wf_fn<T, K_FIRST, K_LAST, false>()); set(wf_fn<T, K_FIRST, K_LAST, true>());
+    set(wf_fn<T, K_FIRST, K_MID, false, true>()); set(wf_fn<T, K_FIRST, K_MID, true, true>());
+    set(wf_fn<T, K_MID, K_MID, false, true>());   set(wf_fn<T, K_MID, K_MID, true, true>());
+    set(wf_fn<T, K_MID, K_LAST, false, true>());  set(wf_fn<T, K_MID, K_LAST, true, true>());
+    set(wf_fn<T, K_FIRST, K_LAST, false, true>()); set(wf_fn<T, K_FIRST, K_LAST, true, true>());
+    set(wf_fn<T, K_FIRST, K_MID, false, true, true>()); set(wf_fn<T, K_FIRST, K_MID, true, true, true>());
+    set(wf_fn<T, K_MID, K_MID, false, true, true>());   set(wf_fn<T, K_MID, K_MID, true, true, true>());
+    set(wf_fn<T, K_MID, K_LAST, false, true, true>());  set(wf_fn<T, K_MID, K_LAST, true, true, true>());
+    set(wf_fn<T, K_FIRST, K_LAST, false, true, true>()); set(wf_fn<T, K_FIRST, K_LAST, true, true, true>());
     return e;
 }
 
@@ -1352,8 +1361,28 @@ int max_steps(whb_ctx *c);
 template <int T, int K1, int K2, bool ZF>
 void launch_wf(whb_ctx *c, int off, int cnt, int s) {
     dim3 grid(c->gxw[T], c->nchw[T], cnt);
+    wf2d::WfScal ps{};
+    if (cnt == 1) {  // one member: its pass scalars go in as kernel parameters
+        const MemberHost &m = c->mem[c->order[off]];
+        for (int t = 1; t <= T; ++t) {
+            const bool first = (K1 == K_FIRST) && (t == 1);
+            ps.h[t] = first ? m.half_dt2 : m.dt2;
+            ps.cs[t] = first ? 1.0 : m.h_cos[s + t - 1];
+            ps.ca[t] = m.h_acc[s + t];
+        }
+        ps.acc0 = m.h_acc[0];
+        ps.osc = m.out_scale;
+        const Geom &g = c->geom;
+        if (g.clo0 == g.clo2 && g.cmid0 == g.cmid2)
+            wf_fn<T, K1, K2, ZF, true, true>()<<<grid, 32 * (WF_NW + 1), c->smemw[T], c->stream>>>(
+                g, c->d_members, off, s, c->upd_lo, c->upd_hi, c->chw[T], 0, ps);
+        else
+            wf_fn<T, K1, K2, ZF, true>()<<<grid, 32 * (WF_NW + 1), c->smemw[T], c->stream>>>(
+                g, c->d_members, off, s, c->upd_lo, c->upd_hi, c->chw[T], 0, ps);
+        return;
+    }
     wf_fn<T, K1, K2, ZF>()<<<grid, 32 * (WF_NW + 1), c->smemw[T], c->stream>>>(
-        c->geom, c->d_members, off, s, c->upd_lo, c->upd_hi, c->chw[T], 0);
+        c->geom, c->d_members, off, s, c->upd_lo, c->upd_hi, c->chw[T], 0, ps);
 }
 
 template <int T>
@@ -1976,6 +2005,8 @@ int whb_set_schedule(whb_ctx *c, int member, int n_total, double half_dt2, doubl
     }
     WHB_CUDA(cudaMemcpy(m.cos_f, cos_f, n_total * sizeof(double), cudaMemcpyHostToDevice));
     WHB_CUDA(cudaMemcpy(m.acc_c, acc_c, (n_total + 1) * sizeof(double), cudaMemcpyHostToDevice));
+    m.h_cos.assign(cos_f, cos_f + n_total);
+    m.h_acc.assign(acc_c, acc_c + n_total + 1);
     m.n_total = n_total;
     m.half_dt2 = half_dt2;
     m.dt2 = dt2;

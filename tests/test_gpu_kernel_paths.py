@@ -19,7 +19,7 @@ from conftest import ROOT
 pytestmark = pytest.mark.gpu
 
 CASES = [((512, 512), 40.0), ((512, 512), 61.0), ((1024, 1024), 90.0), ((600, 600), 50.0), ((300, 300), 33.0),
-         ((256, 256), 40.0), ((90, 47, 61), 20.0), ((64, 64, 64), 11.0)]
+         ((256, 256), 40.0), ((400, 250), 30.0), ((90, 47, 61), 20.0), ((64, 64, 64), 11.0)]
 
 SCRIPT = r"""
 import json, sys, numpy as np
