@@ -254,14 +254,19 @@ __global__ void __launch_bounds__(256) step_kernel(Geom g, const Member *__restr
 }
 
 // Deterministic residual reduction: hist[(*counter)*nb + b] = sum(partials_b[0:nparts]).
+// The slots are zeroed as they are read: the last launch of the next pass (whose kernel, and so
+// its number of partial sums, can differ after a schedule change) then only has to write its own.
 __global__ void reduce_partials_kernel(const Member *__restrict__ members, int nb, int nparts,
                                        double *hist, int *counter) {
     __shared__ double red[32];
     const int slot = *counter;
     for (int b = 0; b < nb; ++b) {
-        const double *pp = members[b].partials;
+        double *pp = members[b].partials;
         double t = 0.0;
-        for (int i = threadIdx.x; i < nparts; i += blockDim.x) t += pp[i];
+        for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
+            t += pp[i];
+            pp[i] = 0.0;
+        }
         for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
         __syncthreads();
