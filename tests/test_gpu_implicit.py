@@ -155,3 +155,45 @@ def test_vcycle_single_cta_coarse_path_bitwise(gpu_available, monkeypatch, cells
         dp.close()
     assert np.array_equal(outs[0], outs[1])
     assert np.any(outs[0] != 0.0)
+
+
+def test_mixed_explicit_implicit_calls_share_one_device_problem(gpu_available):
+    """Explicit and implicit solves, FPI, GMRES and single wave solves interleaved on one cached
+    device problem (shared fields, vectors and graphs): every result matches its checker."""
+    from oracle import implicit_oracle as IO
+    from oracle import native as ON
+    from oracle import waveholtz_oracle as O
+
+    g = wh.build_grid(2, [(0.0, 1.0)] * 2, (64, 64), "dirichlet")
+    f = wh.multi_gaussian_source(g, 9.0, 3, seed=8)
+    fv = np.array(f.values)
+    op = wh.DiscreteOperator(g, 2, 1.0)
+    for rnd in range(2):
+        for omega in (7.5, 10.0):
+            prob = wh.HelmholtzProblem(g, 2, 1.0, omega, f)
+            # explicit FPI (bitwise)
+            cfg_e = wh.FilterConfig(omega=omega, mode="explicit")
+            v, run = wh.fpi_solve(prob, cfg_e, tol=-1.0, maxit=2)
+            corr_e = wh.correct_explicit(omega, g, 2, 1.0)
+            sc = O.step_scalars(corr_e.steps_per_period, corr_e.dt, corr_e.omega_tilde)
+            vref, rref = ON.fpi(fv, g.spacing, sc, 2)
+            assert np.array_equal(v.values, vref)
+            np.testing.assert_allclose(run.residuals, rref, rtol=1e-12)
+            # implicit single solve from that iterate (<= 1e-10)
+            cfg_i = wh.FilterConfig(omega=omega, periods=1, steps_per_period=8, mode="implicit")
+            corr_i = wh.correct_implicit(omega, 8)
+            out = wh.wave_solve_filtered(v, f, cfg_i, corr_i, op).values
+            ref, _ = IO.wave_solve_implicit(np.array(v.values), fv, g.spacing, ["dirichlet"] * 2, 2, omega, 8)
+            assert relerr(out, ref) <= TOL
+            # explicit single solve again (bitwise)
+            out_e = wh.wave_solve_filtered(v, f, cfg_e.__class__(omega=omega, periods=1,
+                                                                  steps_per_period=corr_e.steps_per_period,
+                                                                  mode="explicit"), corr_e, op).values
+            assert np.array_equal(out_e, ON.wave_solve(np.array(v.values), fv, g.spacing, sc))
+            # implicit FPI
+            vi, runi = wh.fpi_solve(prob, cfg_i, tol=-1.0, maxit=2)
+            w = np.zeros_like(fv)
+            solver = None
+            for _ in range(2):
+                w, solver = IO.wave_solve_implicit(w, fv, g.spacing, ["dirichlet"] * 2, 2, omega, 8, solver=solver)
+            assert relerr(vi.values, w) <= TOL
