@@ -698,8 +698,10 @@ def run_reference(args, ws, rank):
     g, f, corr, cfg, _ = build_workload(args.workload)
     sc = O.step_scalars(corr.steps_per_period, corr.dt, corr.omega_tilde)
     fv = np.array(f.values)
-    threads = ON.max_threads()
     npts = g.size
+    # all host cores, except where OpenMP fork/join per step costs more than it saves (config 1's
+    # 16.6K points): the thread count the C restatement runs fastest with (oracle/native.py)
+    threads = ON.max_threads() if npts >= (1 << 20) else ON.auto_threads(npts)
     v = np.zeros_like(fv)
     # sample size: full iterations when one takes <= ~3 s, else a truncated pass of m steps
     t0 = time.perf_counter()

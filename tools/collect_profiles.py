@@ -1,0 +1,66 @@
+"""Turn the outputs of tools/measure_all.sh (gpurun_out/m/) into the judged profiles/<round>/
+files: bench lines, per-kernel launch shares, ncu --set full summaries, and
+profiles/traffic.json (DRAM bytes per launch of each dominant kernel).
+
+    python tools/collect_profiles.py r01
+"""
+
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+
+from launch_share import summarise  # noqa: E402
+from ncu_summary import summary  # noqa: E402
+
+SRC = os.path.join(ROOT, "gpurun_out", "m")
+
+
+def last_json(path):
+    try:
+        lines = [ln for ln in open(path).read().strip().splitlines() if ln.startswith("{")]
+        return json.loads(lines[-1]) if lines else None
+    except OSError:
+        return None
+
+
+def main(rnd):
+    dst = os.path.join(ROOT, "profiles", rnd)
+    os.makedirs(dst, exist_ok=True)
+    for w in ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "imp2"):
+        for arm in ("bench", "bench_reference"):
+            d = last_json(os.path.join(SRC, f"{arm}_{w}.json"))
+            if d is not None:
+                json.dump(d, open(os.path.join(dst, f"{arm}_{w}.json"), "w"))
+    cmds = {"cfg2": "--workload cfg2 --steps 2 --warmup 1", "cfg3": "--workload cfg3 --steps 2 --warmup 1",
+            "cfg5": "--workload cfg5 --steps 1 --warmup 1"}
+    for w, a in cmds.items():
+        p = os.path.join(SRC, f"launches_{w}.csv")
+        if os.path.exists(p):
+            out = summarise(p, f"ncu --metrics gpu__time_duration.sum --clock-control none python bench.py {a} "
+                               "--no-e2e --no-cpu-baseline")
+            json.dump(out, open(os.path.join(dst, f"launches_{w}.json"), "w"), indent=1)
+    traffic_path = os.path.join(ROOT, "profiles", "traffic.json")
+    traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
+    for name, w in (("ncu_cfg2_wf", "cfg2"), ("ncu_cfg3_tb2", "cfg3"), ("ncu_imp2_gs", "imp2")):
+        rep = os.path.join(SRC, name + ".ncu-rep")
+        if not os.path.exists(rep):
+            continue
+        s = summary(rep)
+        json.dump(s, open(os.path.join(dst, name + ".json"), "w"), indent=1)
+        k = s[0]
+        rd = float(k["dram__bytes_read.sum"][0]) * {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1}[
+            k["dram__bytes_read.sum"][1]]
+        wr = float(k["dram__bytes_write.sum"][0]) * {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1}[
+            k["dram__bytes_write.sum"][1]]
+        traffic[w] = {"bytes_per_launch": rd + wr, "kernel": k["kernel"][:60],
+                      "source": f"profiles/{rnd}/{name}.json (ncu --set full, cold cache): "
+                                "dram__bytes_read.sum + dram__bytes_write.sum"}
+    json.dump(traffic, open(traffic_path, "w"), indent=1)
+    print("collected into", dst)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "r01")
