@@ -625,6 +625,7 @@ struct whb_ctx {
     int wfT = 0;                     // 0 = off, else 2 or 4
     int nring = 4;                   // time-level buffers per member (6 when wfT == 4)
     int gxw[5] = {1, 1, 1, 1, 1}, chw[5] = {1, 1, 1, 1, 1}, nchw[5] = {1, 1, 1, 1, 1};
+    long long wf_res[5] = {1, 1, 1, 1, 1};  // resident wavefront CTAs (SMs x CTAs per SM)
     size_t smemw[5] = {0, 0, 0, 0, 0};
     int nparts = 1;
     int64_t launches = 0;
@@ -1035,6 +1036,7 @@ int plan_launch(whb_ctx *c) {
             if (e != cudaSuccess || nb < 1) return fail(WHB_E_CUDA, "wavefront kernel does not fit on an SM");
             c->gxw[T] = (int)((n2 - 1 + CW - 1) / CW);
             const long long res = (long long)sms * nb;
+            c->wf_res[T] = res;
             const long long nch = std::max<long long>(1, res / std::max<long long>(1, c->gxw[T]));
             int cl = (int)((nplanes + nch - 1) / nch);
             const char *ce = getenv("WHB_CHUNKW");
@@ -1365,7 +1367,18 @@ int max_steps(whb_ctx *c);
 
 template <int T, int K1, int K2, bool ZF>
 void launch_wf(whb_ctx *c, int off, int cnt, int s) {
-    dim3 grid(c->gxw[T], c->nchw[T], cnt);
+    // Row chunks per strip: one wave of CTAs for a single member (nchw); with cnt members
+    // per launch, longer chunks — every chunk re-streams T + lag warm-up rows (8 at T = 4),
+    // which at the single-member chunk length of a 1025^2 grid (12 rows) is 67 % extra.
+    int nch = c->nchw[T], cl = c->chw[T];
+    if (cnt > 1) {
+        const long long want = c->wf_res[T] / ((long long)c->gxw[T] * cnt);  // one wave of CTAs
+        nch = (int)std::max<long long>(1, std::min<long long>(nch, want));
+        const int nplanes = c->upd_hi - c->upd_lo;
+        cl = (nplanes + nch - 1) / nch;
+        nch = (nplanes + cl - 1) / cl;
+    }
+    dim3 grid(c->gxw[T], nch, cnt);
     wf2d::WfScal ps{};
     if (cnt == 1) {  // one member: its pass scalars go in as kernel parameters
         const MemberHost &m = c->mem[c->order[off]];
@@ -1380,14 +1393,14 @@ void launch_wf(whb_ctx *c, int off, int cnt, int s) {
         const Geom &g = c->geom;
         if (g.clo0 == g.clo2 && g.cmid0 == g.cmid2)
             wf_fn<T, K1, K2, ZF, true, true>()<<<grid, 32 * (WF_NW + 1), c->smemw[T], c->stream>>>(
-                g, c->d_members, off, s, c->upd_lo, c->upd_hi, c->chw[T], 0, ps);
+                g, c->d_members, off, s, c->upd_lo, c->upd_hi, cl, 0, ps);
         else
             wf_fn<T, K1, K2, ZF, true>()<<<grid, 32 * (WF_NW + 1), c->smemw[T], c->stream>>>(
-                g, c->d_members, off, s, c->upd_lo, c->upd_hi, c->chw[T], 0, ps);
+                g, c->d_members, off, s, c->upd_lo, c->upd_hi, cl, 0, ps);
         return;
     }
     wf_fn<T, K1, K2, ZF>()<<<grid, 32 * (WF_NW + 1), c->smemw[T], c->stream>>>(
-        c->geom, c->d_members, off, s, c->upd_lo, c->upd_hi, c->chw[T], 0, ps);
+        c->geom, c->d_members, off, s, c->upd_lo, c->upd_hi, cl, 0, ps);
 }
 
 template <int T>
