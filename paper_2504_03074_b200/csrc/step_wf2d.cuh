@@ -162,7 +162,20 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, 3)
         }
         const double acc0 = PS ? ps.acc0 : m.acc_c[0];
         const double oscale = PS ? ps.osc : m.out_scale;
-        if constexpr (SKEW == 1) {
+        // a strip wholly past the last interior column (the ragged right edge of the grid) has
+        // nothing to write: it only keeps the stage barriers' arrival counts, so the issue slots go
+        // to the SM's other warps
+        const bool idle = __all_sync(0xffffffffu, !(okc0 || okc1));
+        if (SKEW == 1 && idle) {
+            for (int idx = 0; idx < nrows; ++idx) {
+                mbar_wait(full + (idx % ST), (idx / ST) & 1);
+                __syncwarp();
+                if (idx >= T && lane == 0) mbar_arrive(empty + ((idx - T) % ST));
+            }
+            if (lane == 0)
+                for (int idx = max(0, nrows - T); idx < nrows; ++idx) mbar_arrive(empty + (idx % ST));
+            __syncwarp();
+        } else if constexpr (SKEW == 1) {
         // level queues: Q[t][0..2] = level t at rows (r-t-2, r-t-1, r-t); Q[0] = W^s
             double2 Q[T + 1][3];
             double2 A[T];  // A[t-1] = partial filter sum of row r-t
