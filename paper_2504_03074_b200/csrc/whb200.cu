@@ -305,6 +305,7 @@ __global__ void zero_boundary_kernel(double *x, long long S0, int P, int n1, int
 #include "step_wf2d.cuh"
 #include "step_tb2r.cuh"
 #include "step_tb2w.cuh"
+#include "step_wf3.cuh"
 #include "implicit.cuh"
 namespace {
 
@@ -621,6 +622,10 @@ struct whb_ctx {
     int gx2 = 1, JT2 = 1, chunk2 = 1, nch2 = 1;
     bool tb2r = false;               // 3D: balanced 62-column variant of the two-step kernel
     bool tb2w = false;               // 3D: warp-specialised two-step kernel
+    // 3D three-step wavefront plan (whole-grid 3D contexts)
+    bool wf3 = false;
+    size_t smem3 = 0;
+    int gx3 = 1, JT3 = 1, chunk3 = 1, nch3 = 1;
     // 2D wavefront plan (T steps per pass): whole-grid 2D contexts
     int wfT = 0;                     // 0 = off, else 2 or 4
     int nring = 4;                   // time-level buffers per member (6 when wfT == 4)
@@ -800,6 +805,27 @@ cudaError_t tb2_set_attrs(size_t smem) {
     set(tb2_fn<A1, K_MID, K_MID, false>());   set(tb2_fn<A1, K_MID, K_MID, true>());
     set(tb2_fn<A1, K_MID, K_LAST, false>());  set(tb2_fn<A1, K_MID, K_LAST, true>());
     set(tb2_fn<A1, K_FIRST, K_LAST, false>()); set(tb2_fn<A1, K_FIRST, K_LAST, true>());
+    return e;
+}
+
+// 3D three-step wavefront: 12 x 64 tiles, 384 threads, one CTA per SM (220 KB shared memory).
+constexpr int W3D_BY = 12;
+
+template <int K1, int K2, bool ZF>
+auto wf3_fn() {
+    return wf3::wf3_kernel<W3D_BY, K1, K2, ZF>;
+}
+
+cudaError_t wf3_set_attrs(size_t smem) {
+    cudaError_t e = cudaSuccess;
+    auto set = [&](auto fn) {
+        cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (r != cudaSuccess) e = r;
+    };
+    set(wf3_fn<K_FIRST, K_MID, false>()); set(wf3_fn<K_FIRST, K_MID, true>());
+    set(wf3_fn<K_MID, K_MID, false>());   set(wf3_fn<K_MID, K_MID, true>());
+    set(wf3_fn<K_MID, K_LAST, false>());  set(wf3_fn<K_MID, K_LAST, true>());
+    set(wf3_fn<K_FIRST, K_LAST, false>()); set(wf3_fn<K_FIRST, K_LAST, true>());
     return e;
 }
 
@@ -1047,7 +1073,33 @@ int plan_launch(whb_ctx *c) {
             c->nparts = std::max(c->nparts, c->gxw[T] * (c->nchw[T] + 2));
         }
     }
-    c->nring = (c->wfT == 4) ? 6 : 4;
+    // 3D three-step wavefront (WHB_WF3=1 opt-in): whole-grid, single-problem 3D contexts.  Measured
+    // 124 / 146 Gpts/s on configs 3 / 4 against 165 / 176 for tb2: 18.7 instead of 28 B/update, but
+    // three block barriers per plane, 12 warps per SM and 21 % ring recomputation leave it slower.
+    const char *w3env = getenv("WHB_WF3");
+    c->wf3 = c->tb2 && whole && c->act1 && c->kern == 2 && !c->tb2w && !c->tb2r && w3env && std::string(w3env) == "1";
+    if (c->wf3) {
+        c->smem3 = wf3::smem_bytes<W3D_BY>();
+        cudaError_t e = wf3_set_attrs(c->smem3);
+        if (e != cudaSuccess) return fail(WHB_E_CUDA, std::string("cudaFuncSetAttribute(wf3): ") + cudaGetErrorString(e));
+        int nb = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, wf3_fn<K_MID, K_MID, false>(), wf3::Lay<W3D_BY>::THREADS,
+                                                          c->smem3);
+        if (e != cudaSuccess || nb < 1) return fail(WHB_E_CUDA, "wf3 kernel does not fit on an SM");
+        c->gx3 = (int)((n2 - 1 + wf3::TX - 1) / wf3::TX);
+        c->JT3 = (int)((n1 - 1 + W3D_BY - 1) / W3D_BY);
+        const long long res3 = (long long)sms * nb;
+        const long long tiles3 = (long long)c->gx3 * c->JT3;
+        const long long nch = std::max<long long>(1, 4 * res3 / std::max<long long>(1, tiles3));
+        int cl3 = (int)((nplanes + nch - 1) / nch);
+        const char *env3 = getenv("WHB_CHUNK3");
+        if (env3 && atoi(env3) > 0) cl3 = atoi(env3);
+        c->chunk3 = std::max(1, cl3);
+        c->nch3 = (nplanes + c->chunk3 - 1) / c->chunk3;
+        if ((long long)c->JT3 * c->nch3 > 65535) c->wf3 = false;
+        c->nparts = std::max(c->nparts, c->gx3 * c->JT3 * (c->nch3 + 2));
+    }
+    c->nring = (c->wfT == 4 || c->wf3) ? 6 : 4;
     // slack: bulk row segments start 2 columns / 1 row early and may run BY+1 rows past the last plane
     c->slack_front = 2 * (int64_t)c->P + 32;
     c->slack_back = (int64_t)(c->BY + 3) * c->P + c->BX + 64;
@@ -1363,6 +1415,39 @@ int launch_pair_range(whb_ctx *c, int s, int ib, int ie, int cl, int po) {
 
 int launch_pair(whb_ctx *c, int s) { return launch_pair_range(c, s, c->upd_lo, c->upd_hi, c->chunk2, 0); }
 
+template <int K1, int K2, bool ZF>
+void launch_wf3k(whb_ctx *c, dim3 grid, int s, const StepMaps &mp) {
+    wf3_fn<K1, K2, ZF>()<<<grid, wf3::Lay<W3D_BY>::THREADS, c->smem3, c->stream>>>(
+        c->geom, c->d_members, 0, s, c->upd_lo, c->upd_hi, c->chunk3, c->JT3, 0, mp.w, mp.p, mp.f, mp.a);
+}
+
+// Fused steps (s, s+1, s+2) of the (single) member; `last` when they end its solve.
+int launch_wf3(whb_ctx *c, int s, bool last) {
+    const bool zf = c->cur_zf != 0;
+    StepMaps mp;
+    std::memset(&mp, 0, sizeof(mp));
+    const Member &m0 = c->h_members[0];
+    WHB_TRY(tensor_map(c, level_ptr(m0, s), wf3::TX + 8, W3D_BY + 6, &mp.w));
+    WHB_TRY(tensor_map(c, level_ptr(m0, s - 1), wf3::TX + 4, W3D_BY + 4, &mp.p));
+    WHB_TRY(tensor_map(c, m0.acc, wf3::TX, W3D_BY, &mp.a));
+    if (m0.f) WHB_TRY(tensor_map(c, m0.f, wf3::TX + 4, W3D_BY + 4, &mp.f));
+    dim3 grid(c->gx3, c->JT3 * c->nch3, 1);
+    const int k1 = (s == 0) ? K_FIRST : K_MID;
+#define WHB_WF3_CASE(K1, K2)                                           \
+    if (k1 == K1 && (last ? K_LAST : K_MID) == K2) {                   \
+        if (zf) launch_wf3k<K1, K2, true>(c, grid, s, mp);             \
+        else launch_wf3k<K1, K2, false>(c, grid, s, mp);               \
+    }
+    WHB_WF3_CASE(K_FIRST, K_MID)
+    WHB_WF3_CASE(K_MID, K_MID)
+    WHB_WF3_CASE(K_MID, K_LAST)
+    WHB_WF3_CASE(K_FIRST, K_LAST)
+#undef WHB_WF3_CASE
+    c->launches++;
+    WHB_CUDA(cudaGetLastError());
+    return 0;
+}
+
 int max_steps(whb_ctx *c);
 
 template <int T, int K1, int K2, bool ZF>
@@ -1480,6 +1565,15 @@ int enqueue_solve(whb_ctx *c, int out_mode) {
     const int ns = max_steps(c);
     if (c->wfT) {
         WHB_TRY(enqueue_wf(c));
+    } else if (c->wf3) {
+        // passes of 3 steps; a remainder of 2 is one two-step pass, of 1 a single step
+        int s = 0;
+        while (ns - s >= 3) {
+            WHB_TRY(launch_wf3(c, s, ns - s == 3));
+            s += 3;
+        }
+        if (ns - s == 2) WHB_TRY(launch_pair(c, s));
+        else if (ns - s == 1) WHB_TRY(launch_step_range(c, s, 0, 1));
     } else if (c->tb2) {
         // pairs (0,1), (2,3), ...; a member with odd n_total takes its last step alone
         for (int s = 0; s < ns; s += 2) {
@@ -1499,6 +1593,7 @@ int enqueue_solve(whb_ctx *c, int out_mode) {
     if (out_mode == WHB_OUT_FPI) {
         int np = c->kern == 3 ? kGenBlocks : c->gx * c->JT * c->nchunks;
         if (c->tb2) np = std::max(np, c->gx2 * c->JT2 * c->nch2);
+        if (c->wf3) np = std::max(np, c->gx3 * c->JT3 * c->nch3);
         if (c->wfT) np = std::max(np, std::max(c->gxw[2] * c->nchw[2], c->wfT == 4 ? c->gxw[4] * c->nchw[4] : 0));
         reduce_partials_kernel<<<1, 1024, 0, c->stream>>>(c->d_members, c->nbatch, np, c->d_hist, c->d_counter);
         c->launches++;
@@ -1988,6 +2083,7 @@ int whb_set_operator_general(whb_ctx *c, int order, const int *periodic, const d
     c->kern = 3;
     c->tb2 = false;
     c->tb2r = false;
+    c->wf3 = false;
     c->tb2w = false;
     c->wfT = 0;
     for (auto &kv : c->graphs) cudaGraphExecDestroy(kv.second);
@@ -2501,7 +2597,7 @@ int whb_host_free(void *ptr) {
 int whb_plan(whb_ctx *c, int *kernel, int *steps_per_pass) {
     if (!c) return fail(WHB_E_ARG, "NULL argument");
     if (kernel) *kernel = c->kern;
-    if (steps_per_pass) *steps_per_pass = c->wfT ? c->wfT : (c->tb2 ? 2 : 1);
+    if (steps_per_pass) *steps_per_pass = c->wfT ? c->wfT : (c->wf3 ? 3 : (c->tb2 ? 2 : 1));
     return 0;
 }
 
