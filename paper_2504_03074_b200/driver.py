@@ -375,18 +375,32 @@ class HostFPIStep:
     ||v_new - v_in||_2 / sqrt(N).  Pass pinned arrays (``_native.PinnedBuffer``)
     for full-rate transfers; f stays resident after the first call."""
 
-    def __init__(self, problem, config):
+    def __init__(self, problem, config, inner_tol=1e-12):
         corr, cfg = resolve_time_discretization(problem, config)
         self.problem = problem
         self.config = cfg
+        self.corr = corr
         self.dp = _device_for(problem)
         self.dp.set_schedule(time_schedule(corr, cfg))
         self.dp.set_forcing(problem.forcing.values)
         self._root_n = math.sqrt(problem.grid.size)
+        self._implicit = None
+        if mode_name(cfg.mode) == "implicit":
+            self._implicit = _implicit_state(problem, self.dp, corr, inner_tol)
+            self._sched = time_schedule(corr, cfg)
 
     def __call__(self, v_in: np.ndarray, v_out: np.ndarray) -> float:
         if v_in.shape != tuple(self.problem.grid.shape) or v_out.shape != v_in.shape:
             raise ValueError("v_in/v_out must have the grid shape")
         if not (v_in.flags.c_contiguous and v_out.flags.c_contiguous and v_out.flags.writeable):
             raise ValueError("v_in/v_out must be C-contiguous (v_out writeable)")
+        if self._implicit is not None:
+            ctx = self.dp.ctx
+            solver, (vnew, diff_id) = self._implicit
+            ctx.upload(_native.V, v_in)
+            implicit_wave_solve(self.dp, solver, self.corr, self._sched, _native.V, _native.F, vnew)
+            ctx.sub_into(vnew, _native.V, diff_id)
+            d = math.sqrt(ctx.dot(diff_id, diff_id)) / self._root_n
+            ctx.vec_download(vnew, out=v_out)
+            return d
         return math.sqrt(self.dp.ctx.iterate_host(v_in, v_out)) / self._root_n

@@ -130,12 +130,6 @@ def _check_modes(config, corr):
         raise ValueError("the continuous filter cannot be time-stepped; pick explicit or implicit")
 
 
-def _check_explicit(config, corr):
-    _check_modes(config, corr)
-    if mode_name(config.mode) != "explicit":
-        raise NotImplementedError("this entry point runs the explicit (leapfrog) path")
-
-
 def _field_type(v):
     return type(v) if hasattr(type(v), "from_values") else GridField
 

@@ -197,3 +197,21 @@ def test_mixed_explicit_implicit_calls_share_one_device_problem(gpu_available):
             for _ in range(2):
                 w, solver = IO.wave_solve_implicit(w, fv, g.spacing, ["dirichlet"] * 2, 2, omega, 8, solver=solver)
             assert relerr(vi.values, w) <= TOL
+
+
+def test_host_fpi_step_implicit(gpu_available):
+    """HostFPIStep (host buffers in and out each pass) in implicit mode reproduces fpi_solve's
+    device-resident iterates and residuals."""
+    name = "mg2d_64"
+    m, g, corr, cfg, op = setup(name)
+    prob = wh.HelmholtzProblem(g, m["order"], 1.0, m["omega"], wh.GridField.from_values(g, ARR[f"{name}/f"]))
+    step = wh.HostFPIStep(prob, cfg)
+    a, b = np.zeros(g.shape), np.zeros(g.shape)
+    res = []
+    for _ in range(3):
+        res.append(step(a, b))
+        a, b = b, a
+    v, run = wh.fpi_solve(prob, cfg, tol=-1.0, maxit=3)
+    assert np.array_equal(a, v.values)
+    np.testing.assert_allclose(res, run.residuals, rtol=1e-13)
+    assert relerr(a, ARR[f"{name}/fpi3"]) <= TOL
