@@ -39,8 +39,8 @@ from .filters import mode_name
 from .grid import operator_coefficients
 from .timestep import time_schedule
 
-__all__ = ["slab_ranges", "DeviceShard", "TorchHalo", "LocalHalo", "SlabFPI", "run_filtered_solve",
-           "run_local_solve", "halo_items"]
+__all__ = ["slab_ranges", "DeviceShard", "TorchHalo", "LocalHalo", "SlabFPI", "SlabKrylov", "ShardedVectors",
+           "run_filtered_solve", "run_local_solve", "halo_items", "exchange_forcing"]
 
 
 def slab_ranges(n0: int, nranks: int):
@@ -302,6 +302,105 @@ def exchange_forcing(shards_or_shard, halo):
         halo.exchange([(field(_native.F), 1)])
     else:
         _exchange_now(halo, shards_or_shard, [(field(_native.F), 1)])
+
+
+class ShardedVectors:
+    """The vector interface ``linalg.device_gmres`` uses, over the slab contexts this process
+    owns: element-wise operations act on every local slab, dot products are the sum of the
+    slabs' owned-point dots completed by ``reduce`` (the cross-rank all-reduce for TorchHalo;
+    identity when every slab is local).  The Krylov basis is thereby sharded like the grid —
+    (restart + 1) vectors of 8.6 GB at 1025^3 do not fit one GPU."""
+
+    def __init__(self, shards, reduce=None):
+        self.shards = list(shards)
+        self.reduce = reduce or (lambda x: x)
+
+    def _each(self, name, *args):
+        for sh in self.shards:
+            getattr(sh.ctx, name)(*args)
+
+    def vec_reserve(self, count):
+        ids = [sh.ctx.vec_reserve(count) for sh in self.shards]
+        if any(i != ids[0] for i in ids):
+            raise RuntimeError("slab contexts disagree on vector ids")
+        return ids[0]
+
+    def dot(self, x, y) -> float:
+        return self.reduce(sum(sh.ctx.dot(x, y) for sh in self.shards))
+
+    def axpy(self, a, x, y):
+        self._each("axpy", a, x, y)
+
+    def scale_into(self, a, x, y):
+        self._each("scale_into", a, x, y)
+
+    def div_into(self, x, d, y):
+        self._each("div_into", x, d, y)
+
+    def sub_into(self, x, y, z):
+        self._each("sub_into", x, y, z)
+
+    def copy(self, x, y):
+        self._each("copy", x, y)
+
+    def lincomb(self, y, first, coef):
+        self._each("lincomb", y, first, coef)
+
+
+class SlabKrylov:
+    """GMRES on A v = v - W(v, 0), b = W(0, f) (driver.py:247-300) over slab-decomposed
+    grids: ``linalg.device_gmres`` (the reference's GMRES control flow, linalg.py:102-183)
+    on ``ShardedVectors``; each mat-vec is one zero-forcing slab solve with halo exchange.
+
+    ``shards`` / ``forcings``: this process's DeviceShards and their owned planes of f —
+    one of each under TorchHalo (one rank per GPU), all of them under LocalHalo."""
+
+    def __init__(self, shards, halo, corr, config, forcings):
+        if mode_name(config.mode) != "explicit":
+            raise NotImplementedError("the slab path runs the explicit scheme")
+        self.shards = list(shards)
+        self.halo = halo
+        self.grid = self.shards[0].grid
+        sched = time_schedule(corr, config)
+        for sh, f in zip(self.shards, forcings):
+            sh.set_schedule(sched)
+            sh.upload(_native.F, np.ascontiguousarray(np.asarray(f, dtype=float)))
+        self._local = isinstance(halo, LocalHalo)
+        exchange_forcing(self.shards if self._local else self.shards[0], halo)
+        reduce = None
+        if not self._local and halo.nranks > 1:
+            reduce = lambda x: halo.allreduce_sum(x, self.shards[0])  # noqa: E731
+        self.vec = ShardedVectors(self.shards, reduce)
+
+    def _solve(self, out_mode, zero_forcing):
+        if self._local:
+            run_local_solve(self.shards, self.halo, out_mode, zero_forcing)
+        else:
+            run_filtered_solve(self.shards[0], self.halo, out_mode, zero_forcing)
+
+    def matvec(self, src, dst):
+        """dst = src - W(src, 0)"""
+        self.vec.copy(src, _native.V)
+        self._solve(_native.OUT_AV, True)
+        self.vec.copy(_native.OUT, dst)
+
+    def solve(self, tol=1e-10, restart=50, maxit=500):
+        """Returns (owned planes of x per local shard, report); residuals are scaled by
+        1/sqrt(N) like driver.py:294."""
+        from .linalg import device_gmres
+
+        for sh in self.shards:
+            sh.zero(_native.V)
+        self._solve(_native.OUT_PLAIN, False)  # OUT = b = W(0, f)
+        m = max(1, min(restart, maxit))
+        ids = self.vec.vec_reserve(m + 4)
+        b_id, x_id, work = ids[0], ids[1], ids[2:]
+        self.vec.copy(_native.OUT, b_id)
+        scale = math.sqrt(self.grid.size)
+        rep = device_gmres(self.vec, self.matvec, b_id, x_id, tol=0.0, atol=tol * scale, restart=restart,
+                           maxit=maxit, work_ids=work)
+        rep.residual_history = [r / scale for r in rep.residual_history]
+        return [sh.ctx.vec_download(x_id) for sh in self.shards], rep
 
 
 class SlabFPI:

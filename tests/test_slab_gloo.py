@@ -38,7 +38,9 @@ class NumpyShard:
         self.steps_per_pass = steps_per_pass
         self.clo, self.cmid, self.c2 = operator_coefficients(grid, 2, c)
         shp = (self.nloc + 2 * self.gh,) + tuple(grid.shape[1:])
-        self.buf = {k: np.zeros(shp) for k in ("v", "f", "acc", 0, 1, 2, 3)}
+        self.buf = {k: np.zeros(shp) for k in ("v", "f", "acc", "out", 0, 1, 2, 3)}
+        self.ctx = NumpyVecs(self)
+        self.zf = False
         self.device = 0
         n0, g, p0 = grid.shape[0], self.gh, plane_range[0]
         g_lo, g_hi = max(plane_range[0], 1), min(plane_range[1], n0 - 1)
@@ -51,7 +53,7 @@ class NumpyShard:
         self.n_total = sched["n_total"]
 
     def _field(self, field):
-        return {_native.V: "v", _native.F: "f", _native.ACC: "acc"}[field]
+        return {_native.V: "v", _native.F: "f", _native.ACC: "acc", _native.OUT: "out"}[field]
 
     def upload(self, field, vals):
         a = np.array(vals, dtype=float)
@@ -77,6 +79,7 @@ class NumpyShard:
 
     def solve_begin(self, out_mode, zero_forcing=False):
         self.mode = out_mode
+        self.zf = bool(zero_forcing) or out_mode == _native.OUT_AV
         self.rs = 0.0
 
     def _lap(self, w, i):
@@ -106,7 +109,7 @@ class NumpyShard:
         """interior of W^{s+1} at plane i from W^s (w) and W^{s-1} (wp)"""
         sc, inner = self.sc, self._inner()
         lap = self._lap(w, i)
-        f = self.buf["f"][i][inner]
+        f = self.buf["f"][i][inner] * 0.0 if self.zf else self.buf["f"][i][inner]
         wc = w[i][inner]
         if s == 0:
             return wc + sc["half_dt2"] * (lap - f)
@@ -122,9 +125,14 @@ class NumpyShard:
         acc[inner] = acc[inner] + sc["acc_c"][s + 1] * new
         if s == self.n_total - 1:
             out = sc["out_scale"] * acc[inner]
-            d = out - self.buf["v"][i][inner]
-            self.rs += float(np.sum(d * d))
-            self.buf["v"][i][inner] = out
+            if self.mode == _native.OUT_FPI:
+                d = out - self.buf["v"][i][inner]
+                self.rs += float(np.sum(d * d))
+                self.buf["v"][i][inner] = out
+            elif self.mode == _native.OUT_AV:
+                self.buf["out"][i][inner] = self.buf["v"][i][inner] - out
+            else:
+                self.buf["out"][i][inner] = out
             return False
         return True
 
@@ -179,6 +187,56 @@ class NumpyShard:
 
     def stream(self):
         return contextlib.nullcontext()
+
+
+class NumpyVecs:
+    """The vector half of the whb context interface (ids 0..7 alias the shard's fields,
+    ids >= 8 are extra vectors) over a NumpyShard's owned planes."""
+
+    def __init__(self, shard):
+        self.sh = shard
+        self.extra = []
+
+    def _a(self, vid):
+        if vid >= 8:
+            return self.extra[vid - 8]
+        return self.sh.buf[self.sh._field(vid)]
+
+    def _own(self, vid):
+        g = self.sh.gh
+        return self._a(vid)[g:g + self.sh.nloc]
+
+    def vec_reserve(self, count):
+        first = 8 + len(self.extra)
+        self.extra += [np.zeros_like(self.sh.buf["v"]) for _ in range(count)]
+        return list(range(first, first + count))
+
+    def vec_download(self, vid):
+        return np.array(self._own(vid))
+
+    def dot(self, x, y):
+        return float(np.sum(self._own(x) * self._own(y)))
+
+    def axpy(self, a, x, y):
+        self._own(y)[...] = self._own(y) - (-a) * self._own(x)
+
+    def scale_into(self, a, x, y):
+        self._own(y)[...] = self._own(x) * a
+
+    def div_into(self, x, d, y):
+        self._own(y)[...] = self._own(x) / d
+
+    def sub_into(self, x, y, z):
+        self._own(z)[...] = self._own(x) - self._own(y)
+
+    def copy(self, x, y):
+        self._a(y)[...] = self._a(x)
+
+    def lincomb(self, y, first, coef):
+        acc = self._own(y)
+        for j, c in enumerate(coef):
+            acc = acc + c * self._own(first + j)
+        self._own(y)[...] = acc
 
 
 def _free_port():
@@ -242,3 +300,54 @@ def test_slab_ranges():
     assert slab_ranges(10, 1) == [(0, 10)]
     with pytest.raises(ValueError):
         slab_ranges(3, 4)
+
+
+def _krylov_worker(rank, world, port, cells, omega, q):
+    import torch.distributed as dist
+
+    from paper_2504_03074_b200.slab import SlabKrylov
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        dim = len(cells)
+        g = build_grid(dim, [(0.0, 1.0)] * dim, cells, "dirichlet")
+        f = O.multi_gaussian(g.shape, g.bounds, g.spacing, 3, seed=7)
+        corr = correct_explicit(omega, g, 2, 1.0)
+        cfg = FilterConfig(omega=omega, periods=1, steps_per_period=corr.steps_per_period, mode="explicit")
+        p0, p1 = slab_ranges(g.shape[0], world)[rank]
+        shard = NumpyShard(g, (p0, p1))
+        solver = SlabKrylov([shard], TorchHalo(dist, rank, world), corr, cfg, [f[p0:p1]])
+        xs, rep = solver.solve(tol=1e-9, restart=6, maxit=30)
+        q.put((rank, xs[0], rep.iterations, rep.residual_history))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cells,omega,world", [((30, 22), 9.0, 2), ((12, 10, 11), 6.5, 3)])
+def test_slab_krylov_gloo_matches_single_domain(cells, omega, world):
+    """GMRES with the Krylov basis sharded over z-slabs (dots all-reduced across ranks,
+    mat-vecs as slab solves with halo exchange) against the single-domain oracle GMRES."""
+    ctx = mp.get_context("fork")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_krylov_worker, args=(r, world, port, cells, omega, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = sorted([q.get(timeout=180) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    dim = len(cells)
+    g = build_grid(dim, [(0.0, 1.0)] * dim, cells, "dirichlet")
+    f = O.multi_gaussian(g.shape, g.bounds, g.spacing, 3, seed=7)
+    corr = correct_explicit(omega, g, 2, 1.0)
+    sc = O.step_scalars(corr.steps_per_period, corr.dt, corr.omega_tilde)
+    b = O.wave_solve_filtered(np.zeros(g.shape), f, g.spacing, sc)
+    scale = math.sqrt(g.size)
+    xref, hist, its, conv = O.gmres(lambda x: O.apply_A(x, g.spacing, sc), b, tol=0.0, restart=6, maxit=30,
+                                    atol=1e-9 * scale)
+    x = np.concatenate([t[1] for t in got], axis=0)
+    assert all(t[2] == its for t in got)
+    np.testing.assert_allclose(got[0][3], np.array(hist) / scale, rtol=1e-8)
+    assert np.max(np.abs(x - xref)) <= 1e-9 * np.max(np.abs(xref))
