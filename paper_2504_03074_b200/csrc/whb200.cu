@@ -628,7 +628,7 @@ struct whb_ctx {
     int gx3 = 1, JT3 = 1, chunk3 = 1, nch3 = 1;
     // 2D wavefront plan (T steps per pass): whole-grid 2D contexts
     int wfT = 0;                     // 0 = off, else 2 or 4
-    int nring = 4;                   // time-level buffers per member (6 when wfT == 4)
+    int nring = 4;                   // time-level buffers per member (6 for 3- and 4-step passes)
     int gxw[5] = {1, 1, 1, 1, 1}, chw[5] = {1, 1, 1, 1, 1}, nchw[5] = {1, 1, 1, 1, 1};
     long long wf_res[5] = {1, 1, 1, 1, 1};  // resident wavefront CTAs (SMs x CTAs per SM)
     size_t smemw[5] = {0, 0, 0, 0, 0};
@@ -971,9 +971,9 @@ int plan_launch(whb_ctx *c) {
     if ((long long)c->JT * c->nchunks > 65535)
         return fail(WHB_E_ARG, "grid too large for launch plan (axis-1 tiles x chunks > 65535)");
     c->nparts = c->gx * c->JT * (c->nchunks + 2);
-    // two-step plan: single-domain 2D/3D contexts (a slab needs 2 ghost planes per exchange)
+    // two-step plan: 2D/3D contexts, whole grids and slabs (GH = 2 ghost planes per side feed the
+    // pass); WHB_TB2=0 keeps one step per pass
     const char *tenv = getenv("WHB_TB2");
-    // (slabs too: GH = 2 ghost planes per side feed the pass)
     const bool whole = c->plane_begin == 0 && c->plane_end == c->gshape[0];
     c->tb2 = c->kern >= 1 && c->act0 && !(tenv && std::string(tenv) == "0") && (!c->act1 || c->kern == 2) &&
              c->upd_hi - c->upd_lo >= 1;
