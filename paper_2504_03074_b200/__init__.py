@@ -14,7 +14,7 @@ tridiagonal preconditioner (``implicit.py``).
 
 Extensions beyond the reference: 3D grids, batched frequencies
 (``batch.fpi_solve_batched``) and slab decomposition across GPUs
-(``slab.SlabSolver``).
+(``slab.SlabFPI``, ``slab.SlabKrylov``).
 """
 
 from .device import DeviceProblem, release_device_cache
