@@ -151,6 +151,12 @@ int whb_vec_div_into(whb_ctx *ctx, int x, double d, int y);                   /*
 int whb_vec_lincomb(whb_ctx *ctx, int y, int first, int count, const double *coef); /* y += Q[:,first:first+count]@coef, linalg.py:174 */
 int whb_vec_sub_into(whb_ctx *ctx, int x, int y, int z);                      /* z = x - y */
 int whb_vec_copy(whb_ctx *ctx, int x, int y);                                 /* y = x */
+/* Modified Gram-Schmidt against basis vectors q_first .. q_first+count-1 on the device
+ * (linalg.py:143-150): for j: h[j] = q_j.w; w -= h[j] q_j; then h[count] = w.w and, when
+ * q_next >= 0 and h[count] > 0, q_next = w / sqrt(h[count]).  h_out[count+1] (host) receives
+ * the coefficients after one synchronisation (the per-dot host round trips of the vector
+ * calls above disappear). */
+int whb_vec_mgs(whb_ctx *ctx, int w, int q_first, int count, int q_next, double *h_out);
 /* y = c^2 * L_h x at interior points, boundary 0 (DiscreteOperator.apply_values,
  * grid.py:346-368; p = 2, Dirichlet). */
 int whb_apply_operator(whb_ctx *ctx, int x, int y);

@@ -31,7 +31,7 @@ EXPORTS = (
     "whb_host_free", "whb_geometry", "whb_set_l2_flush", "whb_apply_operator", "whb_plan", "whb_set_operator_general",
     "whb_pair", "whb_ghost_planes", "whb_field_plane_ptr", "whb_copy_device",
     "whb_imp_apply", "whb_imp_rhs", "whb_vec_xpay", "whb_mg_setup", "whb_mg_vcycle", "whb_tri_setup", "whb_tri_solve",
-    "whb_cg_begin", "whb_cg_iterate",
+    "whb_cg_begin", "whb_cg_iterate", "whb_vec_mgs",
 )
 
 _lib = None
@@ -108,6 +108,7 @@ def load():
         "whb_tri_setup": ([vp, c_int, dp, dp, dp], c_int),
         "whb_tri_solve": ([vp, c_int, c_int], c_int),
         "whb_cg_begin": ([vp, c_int, c_int, c_int, c_int, dp], c_int),
+        "whb_vec_mgs": ([vp, c_int, c_int, c_int, c_int, dp], c_int),
         "whb_cg_iterate": ([vp, c_int, c_int, c_int, c_int, c_int, c_int, c_double, c_int, dp, dp], c_int),
     }
     for name, (args, res) in sig.items():
@@ -334,6 +335,12 @@ class Context:
 
     def tri_solve(self, b, x):
         check(load().whb_tri_solve(self._h, int(b), int(x)), "whb_tri_solve")
+
+    def mgs(self, w, q_first, count, q_next=-1):
+        """Device MGS (whb_vec_mgs): returns h[0..count] (h[count] = w.w after projection)."""
+        h = np.zeros(count + 1)
+        check(load().whb_vec_mgs(self._h, int(w), int(q_first), int(count), int(q_next), _dp(h)), "whb_vec_mgs")
+        return h
 
     def cg_begin(self, r, z, p, precond) -> float:
         rr = ctypes.c_double(0.0)

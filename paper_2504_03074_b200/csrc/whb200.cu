@@ -541,6 +541,39 @@ __global__ void div_kernel(const double *__restrict__ x, double d, double *y, lo
         y[i] = __ddiv_rn(x[i], d);
 }
 
+// Modified Gram-Schmidt on the device (gmres_solve, linalg.py:143-150): one pass per basis
+// vector applies the previous projection, w -= h[j-1] q[j-1] (h read from device memory), and
+// forms the partial sums of the next coefficient q[j].w with the updated w — the same values,
+// in the same order, as a separate axpy and dot (dot_partials_kernel's grid and order).
+__global__ void mgs_step_kernel(double *__restrict__ w, const double *__restrict__ qprev,
+                                const double *__restrict__ hprev, const double *__restrict__ q, long long n,
+                                double *partials) {
+    const double h = qprev ? *hprev : 0.0;
+    double t = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        double wi = w[i];
+        if (qprev) {
+            wi = __dsub_rn(wi, __dmul_rn(h, qprev[i]));
+            w[i] = wi;
+        }
+        t += (q ? q[i] : wi) * wi;  // q == nullptr: w.w
+    }
+    const double b = block_sum(t);
+    if (threadIdx.x == 0) partials[blockIdx.x] = b;
+}
+
+// q = w / sqrt(ww) when ww > 0 (Q[:, k+1] = w / ||w||, linalg.py:149-150)
+__global__ void mgs_normalise_kernel(const double *__restrict__ w, const double *__restrict__ ww, double *q,
+                                     long long n) {
+    const double d2 = *ww;
+    if (!(d2 > 0.0)) return;
+    const double d = __dsqrt_rn(d2);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        q[i] = __ddiv_rn(w[i], d);
+}
+
 __global__ void sub_kernel(const double *__restrict__ x, const double *__restrict__ y, double *z,
                            long long n) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -610,6 +643,8 @@ struct whb_ctx {
     int *d_counter = nullptr;
     double *d_red = nullptr;        // vector reduction scratch (kRedBlocks + 1)
     double *h_red = nullptr;        // pinned scalar
+    double *d_mgs = nullptr, *h_mgs = nullptr;  // device / pinned MGS coefficients (whb_vec_mgs)
+    int mgs_cap = 0;
     // launch geometry
     int kern = 1;                   // 1: TMA bulk-copy pipelined kernel (2D/3D), 0: simple LDG kernel
     size_t smem = 0;                // dynamic smem of the bulk kernel
@@ -2011,6 +2046,8 @@ int whb_destroy(whb_ctx *c) {
     cudaFree(c->flush_buf);
     cudaFree(c->stage);
     if (c->h_red) cudaFreeHost(c->h_red);
+    cudaFree(c->d_mgs);
+    if (c->h_mgs) cudaFreeHost(c->h_mgs);
     for (auto e : c->ev) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -2890,6 +2927,51 @@ int whb_cg_iterate(whb_ctx *c, int xi, int ri, int zi, int pi, int api, int tmpi
     WHB_CUDA(cudaStreamSynchronize(c->stream));
     *pap = c->h_red[imp::CG_PAP];
     *rr = c->h_red[imp::CG_RR];
+    return 0;
+}
+
+int whb_vec_mgs(whb_ctx *c, int wi, int q_first, int count, int q_next, double *h_out) {
+    if (!c || !h_out) return fail(WHB_E_ARG, "NULL argument");
+    if (count < 1) return fail(WHB_E_ARG, "count must be >= 1");
+    WHB_TRY(set_dev(c));
+    VEC_OR_FAIL(w, wi);
+    std::vector<double *> q(count);
+    for (int j = 0; j < count; ++j) {
+        q[j] = vec_ptr(c, q_first + j);
+        if (!q[j]) return fail(WHB_E_ARG, "unknown basis vector id");
+    }
+    double *qn = nullptr;
+    if (q_next >= 0) {
+        qn = vec_ptr(c, q_next);
+        if (!qn) return fail(WHB_E_ARG, "unknown vector id for the next basis vector");
+    }
+    if (count + 1 > c->mgs_cap) {
+        cudaFree(c->d_mgs);
+        if (c->h_mgs) cudaFreeHost(c->h_mgs);
+        c->d_mgs = c->h_mgs = nullptr;
+        c->mgs_cap = std::max(64, 2 * (count + 1));
+        WHB_CUDA(cudaMalloc(&c->d_mgs, c->mgs_cap * sizeof(double)));
+        WHB_CUDA(cudaMallocHost(&c->h_mgs, c->mgs_cap * sizeof(double)));
+    }
+    const long long n = owned_elems(c);
+    for (int j = 0; j <= count; ++j) {
+        // j < count: w -= h[j-1] q[j-1]; h[j] = q[j].w   j == count: w -= h[count-1] q[count-1]; h[count] = w.w
+        const double *qp = j > 0 ? owned(q[j - 1], c) : nullptr;
+        const double *qj = j < count ? owned(q[j], c) : nullptr;
+        double *wo = owned(w, c);
+        mgs_step_kernel<<<kRedBlocks, kRedThreads, 0, c->stream>>>(wo, qp, j > 0 ? c->d_mgs + (j - 1) : nullptr, qj,
+                                                                   n, c->d_red);
+        final_sum_kernel<<<1, 1024, 0, c->stream>>>(c->d_red, kRedBlocks, c->d_mgs + j);
+        c->launches += 2;
+    }
+    if (qn) {
+        mgs_normalise_kernel<<<kRedBlocks, kRedThreads, 0, c->stream>>>(owned(w, c), c->d_mgs + count, owned(qn, c), n);
+        c->launches++;
+    }
+    WHB_CUDA(cudaGetLastError());
+    WHB_CUDA(cudaMemcpyAsync(c->h_mgs, c->d_mgs, (count + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
+    std::memcpy(h_out, c->h_mgs, (count + 1) * sizeof(double));
     return 0;
 }
 

@@ -49,6 +49,7 @@ def device_gmres(ctx, matvec, b_id: int, x_id: int, tol=1e-10, restart=30, maxit
     if work_ids is None:
         work_ids = ctx.vec_reserve(m_max + 2)
     r_id, q_ids = work_ids[0], work_ids[1:]
+    contiguous_basis = all(q_ids[i] == q_ids[0] + i for i in range(len(q_ids)))
     ctx.scale_into(0.0, b_id, x_id)  # x = 0 (b has no NaN/inf)
     if bnorm == 0.0:
         return report
@@ -81,13 +82,19 @@ def device_gmres(ctx, matvec, b_id: int, x_id: int, tol=1e-10, restart=30, maxit
         for k in range(m):
             w = r_id  # workspace reused for w = A Q_k
             mv(q_ids[k], w)
-            for j in range(k + 1):
-                H[j, k] = ctx.dot(q_ids[j], w)
-                ctx.axpy(-H[j, k], q_ids[j], w)  # w -= H[j,k]*Q[:,j]
-            h_next = math.sqrt(ctx.dot(w, w))
+            if contiguous_basis and hasattr(ctx, "mgs"):
+                # the whole MGS column on the device, one host round trip (same values as below)
+                h = ctx.mgs(w, q_ids[0], k + 1, q_ids[k + 1])
+                H[:k + 1, k] = h[:k + 1]
+                h_next = math.sqrt(h[k + 1])
+            else:
+                for j in range(k + 1):
+                    H[j, k] = ctx.dot(q_ids[j], w)
+                    ctx.axpy(-H[j, k], q_ids[j], w)  # w -= H[j,k]*Q[:,j]
+                h_next = math.sqrt(ctx.dot(w, w))
+                if h_next > 0:
+                    ctx.div_into(w, h_next, q_ids[k + 1])
             H[k + 1, k] = h_next
-            if h_next > 0:
-                ctx.div_into(w, h_next, q_ids[k + 1])
             for j in range(k):
                 t = cs[j] * H[j, k] + sn[j] * H[j + 1, k]
                 H[j + 1, k] = -sn[j] * H[j, k] + cs[j] * H[j + 1, k]
