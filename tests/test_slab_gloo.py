@@ -271,7 +271,7 @@ def test_slab_fpi_gloo_matches_single_domain(dim, cells, omega, spp, world):
     """world 2 and 3 (a middle slab exchanges both sides; (9, 30) over 3 ranks leaves
     slabs of 3 and 4 planes, so the two-step boundary regions cover whole slabs)"""
     iters = 3
-    ctx = mp.get_context("fork")
+    ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, dim, cells, omega, iters, q, spp)) for r in range(world)]
@@ -328,7 +328,7 @@ def _krylov_worker(rank, world, port, cells, omega, q):
 def test_slab_krylov_gloo_matches_single_domain(cells, omega, world):
     """GMRES with the Krylov basis sharded over z-slabs (dots all-reduced across ranks,
     mat-vecs as slab solves with halo exchange) against the single-domain oracle GMRES."""
-    ctx = mp.get_context("fork")
+    ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_krylov_worker, args=(r, world, port, cells, omega, q)) for r in range(world)]
