@@ -166,6 +166,55 @@ __global__ void gs_color_kernel(Lev L, double *__restrict__ u, const double *__r
     }
 }
 
+// H consecutive red-black half-sweeps (colours c0, 1-c0, c0, ...) in one pass: a CTA loads a
+// (TY+2H) x (TX+2H) window of u and b into shared memory, applies half-sweep h on the window
+// shrunk by h+1 cells (every value there depends only on window data), and writes back its
+// TY x TX tile — the same arithmetic as H gs_color_kernel launches (temporal blocking of the
+// smoother: one HBM pass and one launch instead of H).  Input and output are different arrays:
+// neighbouring CTAs read their halos from `uin` while this one writes `uout`.
+template <int TY, int TXW, int H>
+__global__ void __launch_bounds__(256) gs_block_kernel(Lev L, const double *__restrict__ uin, double *__restrict__ uout,
+                                                       const double *__restrict__ b, int c0) {
+    constexpr int WR = TY + 2 * H, WC = TXW + 2 * H;
+    __shared__ double su[WR * WC];
+    __shared__ double sb[WR * WC];
+    const int i0 = blockIdx.y * TY, j0 = blockIdx.x * TXW;  // tile origin (grid rows / columns)
+    for (int t = threadIdx.x; t < WR * WC; t += blockDim.x) {
+        const int wr = t / WC, wc = t - (t / WC) * WC;
+        const int i = i0 - H + wr, j = j0 - H + wc;
+        const bool in = i >= 0 && i <= L.nx && j >= 0 && j <= L.ny;
+        const long long p = (long long)i * L.rs + j;
+        su[t] = in ? uin[p] : 0.0;
+        sb[t] = in ? b[p] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+        const int col = (c0 + h) & 1;
+        const int m = h + 1;                    // margin: window cells not valid after this half-sweep
+        const int nr = WR - 2 * m;              // rows updated
+        const int nq = (WC - 2 * m + 1) / 2;    // colour points per row (upper bound)
+        for (int t = threadIdx.x; t < nr * nq; t += blockDim.x) {
+            const int wr = m + t / nq;
+            const int i = i0 - H + wr;
+            // first window column >= m whose grid column has the colour in this row
+            const int wc = m + ((col - i - (j0 - H + m)) & 1) + 2 * (t - (t / nq) * nq);
+            const int j = j0 - H + wc;
+            if (wc >= WC - m || i < 1 || i >= L.nx || j < 1 || j >= L.ny) continue;
+            const int w = wr * WC + wc;
+            const double v = whb_add(whb_add(sb[w], whb_mul(L.gx, whb_add(su[w - WC], su[w + WC]))),
+                                     whb_mul(L.gy, whb_add(su[w - 1], su[w + 1])));
+            su[w] = __ddiv_rn(v, L.diag);
+        }
+        __syncthreads();
+    }
+    for (int t = threadIdx.x; t < TY * TXW; t += blockDim.x) {
+        const int r = t / TXW, c = t - (t / TXW) * TXW;
+        const int i = i0 + r, j = j0 + c;
+        if (i >= 1 && i < L.nx && j >= 1 && j < L.ny) uout[(long long)i * L.rs + j] = su[(r + H) * WC + c + H];
+    }
+}
+
 // Fused r = b - A u on the fine level + full-weighting restriction + zeroing of the coarse
 // iterate: each coarse interior point forms the 9 fine residuals it weights (same values as
 // residual_kernel; fine r is never stored) — one launch instead of three per level.

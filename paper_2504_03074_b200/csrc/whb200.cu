@@ -1838,19 +1838,50 @@ int mg_enqueue(whb_ctx *c, int l) {
         WHB_CUDA(cudaGetLastError());
         return 0;
     }
+    // The level's current iterate: the blocked smoother cannot update in place (neighbouring CTAs
+    // read their halos while it writes), so it ping-pongs between u and r (r is otherwise free:
+    // the residual is formed inside the restriction); the cycle ends with the iterate in u.
+    double *cur = B.u;
     auto gs = [&](int color) {
-        imp::gs_color_kernel<<<std::max(1, L.nx - 1), 256, 0, c->stream>>>(L, B.u, B.b, color);
+        imp::gs_color_kernel<<<std::max(1, L.nx - 1), 256, 0, c->stream>>>(L, cur, B.b, color);
         c->launches++;
     };
-    for (int k = 0; k < M.nu1; ++k) { gs(0); gs(1); }
+    // nu sweeps = 2 nu half-sweeps; with nu = 2 they run as one temporally blocked launch
+    const char *gsenv = getenv("WHB_GS_BLOCK");
+    const bool block4 = !(gsenv && std::string(gsenv) == "0");
+    // 32 x 64 tiles while they fill the GPU, 16 x 32 on smaller levels (latency-bound there)
+    const bool big = (long long)((L.ny + 63) / 64) * ((L.nx + 31) / 32) >= 4 * 148;
+    auto gsb = [&](const double *uin, double *uout, int c0) {
+        if (big)
+            imp::gs_block_kernel<32, 64, 4><<<dim3((L.ny + 63) / 64, (L.nx + 31) / 32), 256, 0, c->stream>>>(
+                L, uin, uout, B.b, c0);
+        else
+            imp::gs_block_kernel<16, 32, 4><<<dim3((L.ny + 31) / 32, (L.nx + 15) / 16), 256, 0, c->stream>>>(
+                L, uin, uout, B.b, c0);
+        c->launches++;
+    };
+    if (block4 && M.nu1 == 2) {
+        gsb(B.u, B.r, 0);
+        cur = B.r;
+    } else
+        for (int k = 0; k < M.nu1; ++k) { gs(0); gs(1); }
     // r = b - A u, restricted onto the next level, whose iterate starts at 0 (linalg.py:333-335)
     MGLevelBuf &N = M.lv[l + 1];
-    imp::resid_restrict_kernel<<<N.lev.nx + 1, 128, 0, c->stream>>>(L, B.u, B.b, N.lev, N.b, N.u);
+    imp::resid_restrict_kernel<<<N.lev.nx + 1, 128, 0, c->stream>>>(L, cur, B.b, N.lev, N.b, N.u);
     c->launches++;
     WHB_TRY(mg_enqueue(c, l + 1));
-    imp::prolong_add_kernel<<<L.nx + 1, 256, 0, c->stream>>>(L, B.u, N.lev, N.u);
+    imp::prolong_add_kernel<<<L.nx + 1, 256, 0, c->stream>>>(L, cur, N.lev, N.u);
     c->launches++;
-    for (int k = 0; k < M.nu2; ++k) { gs(1); gs(0); }
+    if (block4 && M.nu2 == 2 && cur != B.u) {
+        gsb(cur, B.u, 1);
+    } else {
+        if (cur != B.u) {
+            WHB_CUDA(cudaMemcpyAsync(B.u, cur, (size_t)(L.nx + 1) * L.rs * sizeof(double), cudaMemcpyDeviceToDevice,
+                                     c->stream));
+            cur = B.u;
+        }
+        for (int k = 0; k < M.nu2; ++k) { gs(1); gs(0); }
+    }
     WHB_CUDA(cudaGetLastError());
     return 0;
 }

@@ -134,10 +134,11 @@ def test_implicit_against_oracle_larger(gpu_available, dim, cells, bcs, order, o
     assert relerr(out, ref) <= TOL, relerr(out, ref)
 
 
-@pytest.mark.parametrize("cells", [(256, 256), (512, 128), (128, 64)])
+@pytest.mark.parametrize("cells", [(256, 256), (512, 128), (128, 64), (1024, 1024), (192, 320)])
 def test_vcycle_single_cta_coarse_path_bitwise(gpu_available, monkeypatch, cells):
-    """The single-CTA coarse sub-cycle (shared memory) computes exactly what the per-level
-    kernels compute: one V-cycle both ways, bitwise."""
+    """The single-CTA coarse sub-cycle (shared memory) and the temporally blocked smoother (four
+    half-sweeps per launch) compute exactly what the per-level / per-colour kernels compute:
+    one V-cycle both ways, bitwise."""
     from paper_2504_03074_b200.device import DeviceProblem
     from paper_2504_03074_b200.implicit import DeviceImplicitSolver
 
@@ -147,6 +148,7 @@ def test_vcycle_single_cta_coarse_path_bitwise(gpu_available, monkeypatch, cells
     outs = []
     for env in ("1", "0"):
         monkeypatch.setenv("WHB_MG_COARSE_CTA", env)
+        monkeypatch.setenv("WHB_GS_BLOCK", env)
         dp = DeviceProblem(g)
         s = DeviceImplicitSolver(dp.ctx, g, 2, 1.0, dt)
         dp.ctx.vec_upload(s.r, r)
