@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, 3)
                 return *reinterpret_cast<const double2 *>(m.v + (long long)orow * S0 + col);
             };
             double2 vcur = vload(r0 - T);
-#pragma unroll 3
+#pragma unroll 2
             for (int idx = 0; idx < nrows; ++idx) {
                 const int r = r0 + idx;
                 const int slot = idx % ST;
