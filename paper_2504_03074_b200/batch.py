@@ -26,7 +26,7 @@ from .filters import FilterConfig
 from .grid import GridField, operator_coefficients
 from .timestep import correct_explicit, time_schedule
 
-__all__ = ["BatchedFPI", "fpi_solve_batched", "lpt_shard"]
+__all__ = ["BatchedFPI", "fpi_solve_batched", "fpi_solve_batched_distributed", "lpt_shard"]
 
 
 def lpt_shard(weights, nranks: int):
@@ -125,3 +125,41 @@ def fpi_solve_batched(grid, forcing, omegas, tol=1e-10, maxit=500, c=1.0, order=
         out.append((v, run))
     solver.close()
     return out
+
+
+def fpi_solve_batched_distributed(grid, forcing, omegas, dist, tol=1e-10, maxit=500, c=1.0, order=2, periods=1,
+                                  device=None, gather_iterates=False):
+    """``fpi_solve_batched`` across the ranks of a ``torch.distributed`` group (one GPU per
+    rank): the omegas are LPT-sharded over their N_t (``lpt_shard``), every rank solves its
+    share as one batch on its own GPU (no data-path collective), and the only collective is
+    the final gather of the runs (residual histories) — SURVEY §8(e), config 5.
+
+    Returns, on every rank, a list over ALL omegas (input order) of
+    (GridField or None, WaveHoltzRun): the iterate is present for this rank's own omegas, and
+    for every omega when ``gather_iterates`` (rank 0 receives them; other ranks get None)."""
+    import os
+
+    rank, world = dist.get_rank(), dist.get_world_size()
+    if device is None:
+        device = int(os.environ.get("LOCAL_RANK", "0"))
+    omegas = [float(w) for w in omegas]
+    nts = [correct_explicit(w, grid, order, c).steps_per_period * periods for w in omegas]
+    mine = lpt_shard(nts, world)[rank]
+    local = fpi_solve_batched(grid, forcing, [omegas[i] for i in mine], tol=tol, maxit=maxit, c=c, order=order,
+                              periods=periods, device=device) if mine else []
+    runs = {i: run for i, (_, run) in zip(mine, local)}
+    parts = [None] * world
+    dist.all_gather_object(parts, runs)
+    all_runs = {}
+    for p in parts:
+        all_runs.update(p)
+    fields = {i: v for i, (v, _) in zip(mine, local)}
+    if gather_iterates:
+        payload = {i: np.asarray(v.values) for i, v in fields.items()}
+        got = [None] * world if rank == 0 else None
+        dist.gather_object(payload, got, dst=0)
+        if rank == 0:
+            fields = {}
+            for part in got:
+                fields.update({i: GridField.from_values(grid, a) for i, a in part.items()})
+    return [(fields.get(i), all_runs[i]) for i in range(len(omegas))]

@@ -351,3 +351,62 @@ def test_slab_krylov_gloo_matches_single_domain(cells, omega, world):
     assert all(t[2] == its for t in got)
     np.testing.assert_allclose(got[0][3], np.array(hist) / scale, rtol=1e-8)
     assert np.max(np.abs(x - xref)) <= 1e-9 * np.max(np.abs(xref))
+
+
+def _batch_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    import paper_2504_03074_b200.batch as B
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # the device solve replaced by the oracle (host logic under test: sharding + gathers)
+        def fake(grid, forcing, omegas, tol=1e-10, maxit=500, c=1.0, order=2, periods=1, device=0):
+            from paper_2504_03074_b200.driver import WaveHoltzRun
+            from paper_2504_03074_b200.grid import GridField
+
+            out = []
+            f = np.asarray(forcing.values)
+            for w in omegas:
+                corr = correct_explicit(w, grid, order, c)
+                sc = O.step_scalars(corr.steps_per_period, corr.dt, corr.omega_tilde)
+                v, res = O.fpi(f, grid.spacing, sc, maxit)
+                out.append((GridField.from_values(grid, v), WaveHoltzRun("fpi", periods, list(res), maxit, False)))
+            return out
+
+        B.fpi_solve_batched = fake
+        g = build_grid(2, [(0.0, 1.0)] * 2, (16, 12), "dirichlet")
+        f = O.multi_gaussian(g.shape, g.bounds, g.spacing, 2, seed=3)
+        from paper_2504_03074_b200.grid import GridField
+
+        omegas = [4.0, 6.5, 9.0, 11.5, 14.0]
+        out = B.fpi_solve_batched_distributed(g, GridField.from_values(g, f), omegas, dist, tol=-1.0, maxit=2,
+                                             device=0, gather_iterates=True)
+        q.put((rank, [run.residuals for _, run in out], [None if v is None else np.asarray(v.values) for v, _ in out]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_batched_distributed_gathers_runs_world2():
+    """config 5 across ranks: LPT sharding of the omegas, runs gathered on every rank, iterates on
+    rank 0, each equal to its single-omega solve."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batch_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = sorted([q.get(timeout=180) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = build_grid(2, [(0.0, 1.0)] * 2, (16, 12), "dirichlet")
+    f = O.multi_gaussian(g.shape, g.bounds, g.spacing, 2, seed=3)
+    for k, w in enumerate([4.0, 6.5, 9.0, 11.5, 14.0]):
+        corr = correct_explicit(w, g, 2, 1.0)
+        sc = O.step_scalars(corr.steps_per_period, corr.dt, corr.omega_tilde)
+        v, res = O.fpi(f, g.spacing, sc, 2)
+        assert got[0][1][k] == list(res) and got[1][1][k] == list(res)
+        assert np.array_equal(got[0][2][k], v)
