@@ -43,7 +43,7 @@ struct Lay {
     static constexpr int STAGE = W_EL + 2 * P_EL + A_EL;  // W^s | W^{s-1} | f | acc
     static constexpr int E_EL = pad16(ER * RW);
     static constexpr int THREADS = TX * BY / 2;
-    static constexpr int RING = A1 ? TX + 2 * (BY + 2) : 2;  // ext-ring work items (pairs + singles)
+    static constexpr int RING = A1 ? 2 * (TX + 2) + 2 * BY : 2;  // ext-ring points, one per thread
 };
 
 template <int TX, int BY, int ST, bool A1>
@@ -143,16 +143,17 @@ __global__ void __launch_bounds__(Lay<TX, BY, A1>::THREADS)
     int r_ey = 0, r_ex = 0;
     bool r_pair = false, r_any = false;
     if (A1) {
-        if (tid < TX) {
+        // one ring point per thread for the first RING threads (the barrier after the W^{s+1}
+        // phase waits for the slowest thread: 3 points, not 4 as with pairs on the top/bottom rows)
+        if (tid < 2 * (TX + 2)) {
             r_any = true;
-            r_pair = true;
-            r_ey = (tid < TX / 2) ? -1 : BY;
-            r_ex = 2 * (tid % (TX / 2));
-        } else if (tid < TX + 2 * (BY + 2)) {
+            r_ey = (tid < TX + 2) ? -1 : BY;
+            r_ex = (tid % (TX + 2)) - 1;
+        } else if (tid < L::RING) {
             r_any = true;
-            const int q = tid - TX;
-            r_ex = (q < BY + 2) ? -1 : TX;
-            r_ey = (q % (BY + 2)) - 1;
+            const int q = tid - 2 * (TX + 2);
+            r_ex = (q < BY) ? -1 : TX;
+            r_ey = q % BY;
         }
     } else if (tid < 2) {
         r_any = true;
