@@ -185,6 +185,11 @@ __global__ void __launch_bounds__(Lay<TX, BY, A1>::THREADS)
     const bool want_v = (K2 == K_LAST) && m.out_mode != WHB_OUT_PLAIN && row_ok && (ok0 || ok1);
     const long long pbase = (long long)j * P + k;
     double2 vcur = make_double2(0.0, 0.0);
+    // register queues along axis 0 for the main pair: W^s at planes i-1, i and W^{s+1} at
+    // planes i-2, i-1 (each value was read from / written to shared memory by this thread)
+    double2 wsm = make_double2(0.0, 0.0), wsc = wsm, em2 = wsm, em1 = wsm;
+    const int rmain = (A1 ? ty + 2 : 0) * L::RW + kl + 2;  // main pair in a W^s stage
+    const int emain = (A1 ? ty + 1 : 0) * L::RW + kl + 2;  // main pair in an E slot / prev / f row
     for (int i = i0 - 1; i <= i1; ++i) {
         const int t = i - i0 + 2;  // stage of plane i
         // output plane of this iteration is i-1; prefetch v for plane i (next iteration's output)
@@ -211,10 +216,30 @@ __global__ void __launch_bounds__(Lay<TX, BY, A1>::THREADS)
         double *E = ering + (size_t)(i % 3) * L::E_EL;
 
         // ---- step s: W^{s+1}(plane i) on the ext tile -> E ring
+        double2 enew, wsp;
         {
-            const double a = step1(sm_m, sm_c, sm_p, i, ty, kl);
-            const double b = step1(sm_m, sm_c, sm_p, i, ty, kl + 1);
-            *reinterpret_cast<double2 *>(E + (A1 ? ty + 1 : 0) * L::RW + kl + 2) = make_double2(a, b);
+            if (i == i0 - 1) {
+                wsm = *reinterpret_cast<const double2 *>(sm_m + rmain);
+                wsc = *reinterpret_cast<const double2 *>(sm_c + rmain);
+            }
+            wsp = *reinterpret_cast<const double2 *>(sm_p + rmain);
+            const double *P_ = sm_c + L::W_EL;
+            const double *F_ = P_ + L::P_EL;
+            double2 yl2 = make_double2(0.0, 0.0), yh2 = yl2;
+            if (A1) {
+                yl2 = *reinterpret_cast<const double2 *>(sm_c + rmain - L::RW);
+                yh2 = *reinterpret_cast<const double2 *>(sm_c + rmain + L::RW);
+            }
+            const double xl = sm_c[rmain - 1], xh = sm_c[rmain + 2];
+            const double2 fv2 = ZF ? make_double2(0.0, 0.0) : *reinterpret_cast<const double2 *>(F_ + emain);
+            const double2 pv2 = LOAD_P ? *reinterpret_cast<const double2 *>(P_ + emain) : make_double2(0.0, 0.0);
+            const double a = update_point<K1, ZF, A1>(g, wsm.x, wsc.x, wsp.x, yl2.x, yh2.x, xl, wsc.y, fv2.x, pv2.x,
+                                                     h1, cos1);
+            const double b = update_point<K1, ZF, A1>(g, wsm.y, wsc.y, wsp.y, yl2.y, yh2.y, wsc.x, xh, fv2.y, pv2.y,
+                                                     h1, cos1);
+            const bool pin = (i >= g.i_lo) && (i < g.i_hi);
+            enew = make_double2((pin && ok0) ? a : 0.0, (pin && ok1) ? b : 0.0);
+            *reinterpret_cast<double2 *>(E + emain) = enew;
         }
         if (r_any) {
             const double a = step1(sm_m, sm_c, sm_p, i, r_ey, r_ex);
@@ -226,18 +251,15 @@ __global__ void __launch_bounds__(Lay<TX, BY, A1>::THREADS)
         // ---- step s+1: W^{s+2}(plane i-1) on the tile
         const int ip = i - 1;
         if (ip >= i0) {
-            const double *Em = ering + (size_t)((ip + 2) % 3) * L::E_EL;  // plane ip-1
             const double *Ec = ering + (size_t)(ip % 3) * L::E_EL;
-            const double *Ep = E;                                          // plane ip+1 = i
             const double *st_c = sm_m;                                     // stage of plane ip
             const double *F_ = st_c + L::W_EL + L::P_EL;
             const double *A_ = F_ + L::P_EL;
             const int re = A1 ? ty + 1 : 0;
-            const int rw = A1 ? ty + 2 : 0;
             const int c = kl + 2;
-            const double2 e_c = *reinterpret_cast<const double2 *>(Ec + re * L::RW + c);
-            const double2 e_m = *reinterpret_cast<const double2 *>(Em + re * L::RW + c);
-            const double2 e_p = *reinterpret_cast<const double2 *>(Ep + re * L::RW + c);
+            const double2 e_c = em1;  // W^{s+1} at planes ip, ip-1, ip+1 (register queue)
+            const double2 e_m = em2;
+            const double2 e_p = enew;
             double2 e_yl = make_double2(0.0, 0.0), e_yh = make_double2(0.0, 0.0);
             if (A1) {
                 e_yl = *reinterpret_cast<const double2 *>(Ec + (re - 1) * L::RW + c);
@@ -245,7 +267,7 @@ __global__ void __launch_bounds__(Lay<TX, BY, A1>::THREADS)
             }
             const double e_xl = Ec[re * L::RW + c - 1];
             const double e_xh = Ec[re * L::RW + c + 2];
-            const double2 w0 = *reinterpret_cast<const double2 *>(st_c + rw * L::RW + c);  // W^s (prev of step s+1)
+            const double2 w0 = wsm;  // W^s at plane ip (prev of step s+1)
             const double2 f2 = ZF ? make_double2(0.0, 0.0) : *reinterpret_cast<const double2 *>(F_ + re * L::RW + c);
             const double n0 = update_point<K_MID, ZF, A1>(g, e_m.x, e_c.x, e_p.x, e_yl.x, e_yh.x, e_xl, e_c.y, f2.x,
                                                          w0.x, h2, cos2);
@@ -294,6 +316,10 @@ __global__ void __launch_bounds__(Lay<TX, BY, A1>::THREADS)
             }
         }
         vcur = vnext;
+        wsm = wsc;
+        wsc = wsp;
+        em2 = em1;
+        em1 = enew;
     }
     if (K2 == K_LAST && m.out_mode == WHB_OUT_FPI) {
         const double t = block_sum(rsum);
