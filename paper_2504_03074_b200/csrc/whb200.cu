@@ -781,7 +781,7 @@ constexpr int B2_TX = 256, B2_BY = 1, B2_ST = 8;
 
 // Two-step kernel configurations: 3D 16 x 64 tiles, 5 stages (1 CTA/SM, 512 threads);
 // 2D 256-column row strips, 8 stages (3 CTAs/SM).
-constexpr int T3_TX = 64, T3_BY = 16, T3_ST = 5;  // measured: BY = 8 / 4 stages / 2 CTAs per SM is 6 % slower on 1025^3
+constexpr int T3_TX = 64, T3_BY = 16, T3_ST = 5;  // measured on 257^3: BY = 8 / 4 stages / 2 CTAs per SM -0.6 %, BY = 12 / 6 stages -6 %
 constexpr int T2_TX = 256, T2_BY = 1, T2_ST = 8;
 
 template <bool A1, int K1, int K2, bool ZF>
