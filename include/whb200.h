@@ -130,6 +130,14 @@ int whb_filtered_solve(whb_ctx *ctx, int out_mode, int zero_forcing, double *res
  * iters_done (may be NULL) receives the number of passes run. */
 int whb_fpi(whb_ctx *ctx, int iters, double tol_sq, double *resid_sq_out, int *iters_done);
 
+/* whb_fpi with the reference's own stopping test (driver.py:225-230): stop after
+ * the first iteration with sqrt(resid_sq) / root_n <= tol for every member
+ * (IEEE sqrt and division, so the decision is the host loop's bit for bit;
+ * root_n = sqrt(N) as the caller computes it, > 0; tol < 0: never stop early).
+ * Cluster-resident grids (whb_plan kernel 4, one member) take the test inside
+ * the kernel: the whole tol-driven fpi_solve is one launch. */
+int whb_fpi_scaled(whb_ctx *ctx, int iters, double tol, double root_n, double *resid_sq_out, int *iters_done);
+
 /* End-to-end single-member pass with host buffers (member 0): copy v_host
  * H2D, v <- W(v, f), copy v D2H into v_out_host, resid_sq as in whb_fpi.
  * The drop-in for one call of wave_solve_filtered inside _iterate
@@ -256,7 +264,11 @@ int whb_set_l2_flush(whb_ctx *ctx, int64_t bytes);
 int whb_host_alloc(void **ptr, int64_t bytes);
 int whb_host_free(void *ptr);
 /* Launch plan: kernel 0 = simple LDG, 1 = bulk-copy rows (2D/batched), 2 = TMA tensor
- * boxes (3D); steps_per_pass = 2 when the two-step (temporal blocking) kernel is used. */
+ * boxes (3D), 3 = general operator, 4 = cluster-resident small 2D grid (the whole solve,
+ * and a whole fixed-point loop, in one launch from shared memory); steps_per_pass = leapfrog
+ * steps per HBM pass of the whole-solve kernels (2 two-step, 3/4 wavefront; 0 for kernel 4,
+ * which makes no per-step HBM pass).  Step-level (slab) control always uses the multi-pass
+ * kernels. */
 int whb_plan(whb_ctx *ctx, int *kernel, int *steps_per_pass);
 /* Global and local geometry: shape3[3], pitch, nloc (owned planes). */
 int whb_geometry(whb_ctx *ctx, int64_t *shape3, int64_t *pitch, int64_t *nloc);

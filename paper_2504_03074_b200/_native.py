@@ -23,7 +23,7 @@ E_ARG, E_CUDA, E_NOMEM, E_STATE, E_NODEV = -1, -2, -3, -4, -5
 EXPORTS = (
     "whb_abi_version", "whb_last_error", "whb_device_count", "whb_create", "whb_destroy",
     "whb_set_operator", "whb_set_schedule", "whb_upload", "whb_download", "whb_zero",
-    "whb_filtered_solve", "whb_fpi", "whb_iterate_host", "whb_vec_reserve", "whb_vec_upload",
+    "whb_filtered_solve", "whb_fpi", "whb_fpi_scaled", "whb_iterate_host", "whb_vec_reserve", "whb_vec_upload",
     "whb_vec_download", "whb_vec_dot", "whb_vec_axpy", "whb_vec_scale_into", "whb_vec_div_into",
     "whb_vec_lincomb", "whb_vec_sub_into", "whb_vec_copy", "whb_matvec", "whb_solve_begin",
     "whb_step", "whb_solve_end", "whb_level_plane_ptr", "whb_stream_ptr", "whb_synchronize",
@@ -66,6 +66,7 @@ def load():
         "whb_zero": ([vp, c_int, c_int], c_int),
         "whb_filtered_solve": ([vp, c_int, c_int, dp], c_int),
         "whb_fpi": ([vp, c_int, c_double, dp, ctypes.POINTER(c_int)], c_int),
+        "whb_fpi_scaled": ([vp, c_int, c_double, c_double, dp, ctypes.POINTER(c_int)], c_int),
         "whb_iterate_host": ([vp, dp, dp, dp], c_int),
         "whb_vec_reserve": ([vp, c_int, ctypes.POINTER(c_int)], c_int),
         "whb_vec_upload": ([vp, c_int, dp], c_int),
@@ -252,6 +253,14 @@ class Context:
         res = np.zeros(max(1, iters) * self.nbatch)
         done = ctypes.c_int(0)
         check(load().whb_fpi(self._h, int(iters), float(tol_sq), _dp(res), ctypes.byref(done)), "whb_fpi")
+        return res[: done.value * self.nbatch].reshape(done.value, self.nbatch)
+
+    def fpi_scaled(self, iters, tol, root_n):
+        """Up to `iters` passes, stopping on sqrt(r)/root_n <= tol (driver.py:225-230)."""
+        res = np.zeros(max(1, iters) * self.nbatch)
+        done = ctypes.c_int(0)
+        check(load().whb_fpi_scaled(self._h, int(iters), float(tol), float(root_n), _dp(res), ctypes.byref(done)),
+              "whb_fpi_scaled")
         return res[: done.value * self.nbatch].reshape(done.value, self.nbatch)
 
     def iterate_host(self, v_in, v_out):

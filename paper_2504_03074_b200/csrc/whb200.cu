@@ -306,6 +306,7 @@ __global__ void zero_boundary_kernel(double *x, long long S0, int P, int n1, int
 #include "step_tb2r.cuh"
 #include "step_tb2w.cuh"
 #include "step_wf3.cuh"
+#include "step_cres2d.cuh"
 #include "implicit.cuh"
 namespace {
 
@@ -657,6 +658,9 @@ struct whb_ctx {
     int gx2 = 1, JT2 = 1, chunk2 = 1, nch2 = 1;
     bool tb2r = false;               // 3D: balanced 62-column variant of the two-step kernel
     bool tb2w = false;               // 3D: warp-specialised two-step kernel
+    // cluster-resident small-grid 2D plan (whole grid in one cluster's shared memory)
+    bool cres = false;
+    int cres_cl = 0, cres_r = 0;
     // 3D three-step wavefront plan (whole-grid 3D contexts)
     bool wf3 = false;
     size_t smem3 = 0;
@@ -932,6 +936,45 @@ int get_encoder() {
     return 0;
 }
 
+// ---- cluster-resident small-grid 2D kernel (step_cres2d.cuh) --------------------------------
+constexpr size_t kCresSmemMax = 227 * 1024;
+
+template <bool ZF, bool SQ>
+auto cres_fn() {
+    return cres::cres2d_kernel<ZF, SQ>;
+}
+
+cudaError_t cres_set_attrs() {
+    cudaError_t e = cudaSuccess;
+    auto set = [&](auto fn) {
+        cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCresSmemMax);
+        if (r != cudaSuccess) e = r;
+        r = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (r != cudaSuccess) e = r;
+    };
+    set(cres_fn<false, false>()); set(cres_fn<true, false>());
+    set(cres_fn<false, true>());  set(cres_fn<true, true>());
+    return e;
+}
+
+int cres_max_clusters(whb_ctx *c, int cl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cl, 1, 1);
+    cfg.blockDim = dim3(cres::NT, 1, 1);
+    const int R = ((int)c->gshape[0] - 2 + cl - 1) / cl;
+    cfg.dynamicSmemBytes = cres::smem_doubles(R, (int)c->gshape[2], false, 64, cl) * sizeof(double);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, cres_fn<false, false>(), &cfg) != cudaSuccess) n = 0;
+    return n;
+}
+
 int occupancy_blocks(whb_ctx *c) {
     int nb = 0;
     cudaError_t e;
@@ -1135,6 +1178,33 @@ int plan_launch(whb_ctx *c) {
         c->nparts = std::max(c->nparts, c->gx3 * c->JT3 * (c->nch3 + 2));
     }
     c->nring = (c->wfT == 4 || c->wf3) ? 6 : 4;
+    // cluster-resident plan (whole-grid 2D with the fields in one cluster's shared memory; the
+    // per-launch fit against the step count is cres_fits); WHB_CRES=0 disables, WHB_CRES_CL=n
+    // caps the cluster size
+    const char *cenv = getenv("WHB_CRES");
+    c->cres = false;
+    if (whole && c->act0 && !c->act1 && c->kern >= 1 && !(cenv && std::string(cenv) == "0")) {
+        const int NR = (int)c->gshape[0] - 2;
+        const char *clenv = getenv("WHB_CRES_CL");
+        int cl = clenv && atoi(clenv) > 0 ? atoi(clenv) : cres::MAX_CL;
+        cl = std::min(cl, cres::MAX_CL);
+        while (cl > 1 && cl > NR) cl >>= 1;
+        const int W = (int)c->gshape[2];
+        if (NR >= 1 && cres_set_attrs() == cudaSuccess) {
+            // the cluster must be schedulable (cl SMs of one GPC): fall back to smaller clusters
+            for (; cl >= 1; cl >>= 1) {
+                const int R = (NR + cl - 1) / cl;
+                if (cres::smem_doubles(R, W, false, 64, cl) * sizeof(double) > kCresSmemMax) break;
+                if (cres_max_clusters(c, cl) > 0) {
+                    c->cres = true;
+                    c->cres_cl = cl;
+                    c->cres_r = R;
+                    break;
+                }
+            }
+        }
+        cudaGetLastError();
+    }
     // slack: bulk row segments start 2 columns / 1 row early and may run BY+1 rows past the last plane
     c->slack_front = 2 * (int64_t)c->P + 32;
     c->slack_back = (int64_t)(c->BY + 3) * c->P + c->BX + 64;
@@ -1595,9 +1665,68 @@ int active_members(whb_ctx *c, int s) {
     return n;
 }
 
+// Shared memory of a cluster-resident launch over the current members (0: does not fit).
+size_t cres_smem(whb_ctx *c) {
+    if (!c->cres || c->kern == 3) return 0;
+    const size_t b = cres::smem_doubles(c->cres_r, (int)c->gshape[2], c->cur_zf != 0, max_steps(c), c->cres_cl) *
+                     sizeof(double);
+    return b <= kCresSmemMax ? b : 0;
+}
+
+// One cluster per member (table positions [0, nbatch)); iters > 1 (FPI) runs that many fixed-point
+// iterations inside the launch, hist == nullptr leaves the residual in partials[0] for the reduction.
+int launch_cres(whb_ctx *c, size_t smem, int iters, double tol_sq, double *hist, int k0, int *done,
+                double tol = -1.0, double root_n = 0.0) {
+    cres::Args a{};
+    a.tol = tol;
+    a.root_n = root_n;
+    a.CL = c->cres_cl;
+    a.R = c->cres_r;
+    a.W = (int)c->gshape[2];
+    a.nmax = max_steps(c);
+    a.iters = iters;
+    a.tol_sq = tol_sq;
+    a.hist = hist;
+    a.k0 = k0;
+    a.nb = c->nbatch;
+    a.done = done;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c->cres_cl, c->nbatch, 1);
+    cfg.blockDim = dim3(cres::NT, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = c->cres_cl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const Geom &g = c->geom;
+    const bool sq = g.clo0 == g.clo2 && g.cmid0 == g.cmid2;
+    const bool zf = c->cur_zf != 0;
+    cudaError_t e;
+    if (zf) e = sq ? cudaLaunchKernelEx(&cfg, cres_fn<true, true>(), g, (const Member *)c->d_members, 0, a)
+                   : cudaLaunchKernelEx(&cfg, cres_fn<true, false>(), g, (const Member *)c->d_members, 0, a);
+    else e = sq ? cudaLaunchKernelEx(&cfg, cres_fn<false, true>(), g, (const Member *)c->d_members, 0, a)
+                : cudaLaunchKernelEx(&cfg, cres_fn<false, false>(), g, (const Member *)c->d_members, 0, a);
+    WHB_CUDA(e);
+    c->launches++;
+    return 0;
+}
+
 // Enqueue one full filtered solve (all steps + residual reduction).
 int enqueue_solve(whb_ctx *c, int out_mode) {
     const int ns = max_steps(c);
+    if (const size_t cs = cres_smem(c)) {
+        WHB_TRY(launch_cres(c, cs, 1, -1.0, nullptr, 0, nullptr));
+        if (out_mode == WHB_OUT_FPI) {
+            reduce_partials_kernel<<<1, 1024, 0, c->stream>>>(c->d_members, c->nbatch, 1, c->d_hist, c->d_counter);
+            c->launches++;
+            WHB_CUDA(cudaGetLastError());
+        }
+        return 0;
+    }
     if (c->wfT) {
         WHB_TRY(enqueue_wf(c));
     } else if (c->wf3) {
@@ -1681,7 +1810,16 @@ int check_ready(whb_ctx *c) {
     return 0;
 }
 
-int fpi_impl(whb_ctx *c, int iters, double tol_sq, double *resid_out, int *done) {
+// Stopping test of the fixed-point loop for one member's resid^2: root_n > 0 follows
+// driver.py:225-230 exactly (sqrt(r) / sqrt(N) <= tol, IEEE sqrt and division), else r <= tol_sq.
+bool fpi_stop(double r, double tol_sq, double tol, double root_n) {
+    if (root_n > 0.0) return tol >= 0.0 && std::sqrt(r) / root_n <= tol;
+    return tol_sq >= 0.0 && r <= tol_sq;
+}
+
+int fpi_impl(whb_ctx *c, int iters, double tol_sq, double *resid_out, int *done, double tol = -1.0,
+             double root_n = 0.0) {
+    const bool checks = root_n > 0.0 ? tol >= 0.0 : tol_sq >= 0.0;
     WHB_TRY(check_ready(c));
     WHB_TRY(ensure_hist(c, iters));
     WHB_TRY(upload_members(c, WHB_OUT_FPI, 0));
@@ -1690,6 +1828,38 @@ int fpi_impl(whb_ctx *c, int iters, double tol_sq, double *resid_out, int *done)
     int k = 0;
     std::vector<double> h(c->nbatch);
     int64_t step_kernels = 0;
+    // cluster-resident grids: the whole fixed-point loop is one launch (the convergence test runs
+    // in the kernel; with several members only a fixed iteration count, as the host loop stops on
+    // all members together)
+    c->cur_zf = 0;
+    const size_t cs = cres_smem(c);
+    if (cs && iters > 0 && (c->nbatch == 1 || !checks)) {
+        if (c->flush_buf) {
+            l2_flush_kernel<<<1184, 256, 0, c->stream>>>(c->flush_buf, c->flush_elems, 0.0);
+            c->launches++;
+            WHB_CUDA(cudaGetLastError());
+        }
+        if (c->timing) WHB_CUDA(cudaEventRecord(c->ev[0], c->stream));
+        WHB_TRY(launch_cres(c, cs, iters, tol_sq, c->d_hist, 0, c->d_counter, tol, root_n));
+        if (c->timing) WHB_CUDA(cudaEventRecord(c->ev[1], c->stream));
+        int kd = 0;
+        WHB_CUDA(cudaMemcpyAsync(&kd, c->d_counter, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        WHB_CUDA(cudaStreamSynchronize(c->stream));
+        k = kd;
+        if (resid_out && k > 0)
+            WHB_CUDA(cudaMemcpyAsync(resid_out, c->d_hist, (size_t)k * c->nbatch * sizeof(double),
+                                     cudaMemcpyDeviceToHost, c->stream));
+        WHB_CUDA(cudaStreamSynchronize(c->stream));
+        if (c->timing) {
+            float ms = 0.f;
+            WHB_CUDA(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+            c->t_solve_ms = ms;
+            c->t_step_ms = ms;
+            c->t_step_launches = 1;
+        }
+        if (done) *done = k;
+        return 0;
+    }
     for (k = 0; k < iters; ++k) {
         if (c->flush_buf) {
             l2_flush_kernel<<<1184, 256, 0, c->stream>>>(c->flush_buf, c->flush_elems, (double)k);
@@ -1701,12 +1871,12 @@ int fpi_impl(whb_ctx *c, int iters, double tol_sq, double *resid_out, int *done)
         WHB_TRY(run_solve(c, WHB_OUT_FPI, 0));
         step_kernels += c->launches - l0 - 1;  // minus the residual reduction
         if (c->timing) WHB_CUDA(cudaEventRecord(c->ev[2 * k + 1], c->stream));
-        if (tol_sq >= 0.0) {
+        if (checks) {
             WHB_CUDA(cudaMemcpyAsync(h.data(), c->d_hist + (size_t)k * c->nbatch, c->nbatch * sizeof(double),
                                      cudaMemcpyDeviceToHost, c->stream));
             WHB_CUDA(cudaStreamSynchronize(c->stream));
             bool conv = true;
-            for (double r : h) conv = conv && (r <= tol_sq);
+            for (double r : h) conv = conv && fpi_stop(r, tol_sq, tol, root_n);
             if (conv) {
                 ++k;
                 break;
@@ -2149,6 +2319,7 @@ int whb_set_operator_general(whb_ctx *c, int order, const int *periodic, const d
         if (g.act[a] && g.n[a] < order + 1) return fail(WHB_E_ARG, "axis too short for the stencil");
     WHB_CUDA(cudaStreamSynchronize(c->stream));
     c->kern = 3;
+    c->cres = false;
     c->tb2 = false;
     c->tb2r = false;
     c->wf3 = false;
@@ -2269,6 +2440,16 @@ int whb_fpi(whb_ctx *c, int iters, double tol_sq, double *resid_sq_out, int *ite
         return 0;
     }
     return fpi_impl(c, iters, tol_sq, resid_sq_out, iters_done);
+}
+
+int whb_fpi_scaled(whb_ctx *c, int iters, double tol, double root_n, double *resid_sq_out, int *iters_done) {
+    if (!c || iters < 0 || !(root_n > 0.0)) return fail(WHB_E_ARG, "bad argument");
+    WHB_TRY(set_dev(c));
+    if (iters == 0) {
+        if (iters_done) *iters_done = 0;
+        return 0;
+    }
+    return fpi_impl(c, iters, -1.0, resid_sq_out, iters_done, tol, root_n);
 }
 
 int whb_iterate_host(whb_ctx *c, const double *v_host, double *v_out_host, double *resid_sq) {
@@ -2664,8 +2845,8 @@ int whb_host_free(void *ptr) {
 
 int whb_plan(whb_ctx *c, int *kernel, int *steps_per_pass) {
     if (!c) return fail(WHB_E_ARG, "NULL argument");
-    if (kernel) *kernel = c->kern;
-    if (steps_per_pass) *steps_per_pass = c->wfT ? c->wfT : (c->wf3 ? 3 : (c->tb2 ? 2 : 1));
+    if (kernel) *kernel = c->cres ? 4 : c->kern;
+    if (steps_per_pass) *steps_per_pass = c->cres ? 0 : (c->wfT ? c->wfT : (c->wf3 ? 3 : (c->tb2 ? 2 : 1)));
     return 0;
 }
 

@@ -221,8 +221,9 @@ def fpi_solve(problem, config, tol=1e-10, maxit=500, inner_tol=1e-12, device_sta
     (driver.py:201-203, 211-244), device resident.
 
     tol < 0 runs exactly ``maxit`` passes with no host synchronisation between
-    them; otherwise the scaled residual is checked on the host after every
-    pass exactly like driver.py:225-230."""
+    them; otherwise every pass is followed by the stopping test of
+    driver.py:225-230 (sqrt(r)/sqrt(N) <= tol, the same IEEE operations) — on
+    the host, or inside the kernel for cluster-resident grids."""
     corr, cfg = resolve_time_discretization(problem, config)
     dp = device_state or _device_for(problem)
     if mode_name(cfg.mode) == "implicit":
@@ -240,13 +241,10 @@ def fpi_solve(problem, config, tol=1e-10, maxit=500, inner_tol=1e-12, device_sta
         residuals = [math.sqrt(x) / root_n for x in rs[:, 0]]
         k = len(residuals)
     else:
-        for k in range(1, maxit + 1):
-            rs = dp.ctx.fpi(1)
-            diff = math.sqrt(rs[0, 0]) / root_n
-            residuals.append(diff)
-            if diff <= tol:
-                converged = True
-                break
+        rs = dp.ctx.fpi_scaled(maxit, tol, root_n)
+        residuals = [math.sqrt(x) / root_n for x in rs[:, 0]]
+        k = len(residuals)
+        converged = k > 0 and residuals[-1] <= tol
     wall = time.perf_counter() - t0
     v = GridField.from_values(problem.grid, dp.ctx.download(_native.V), ghost=2)
     run = WaveHoltzRun(method="fpi", periods=cfg.periods, residuals=residuals, iterations=k,

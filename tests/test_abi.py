@@ -54,3 +54,4 @@ def test_null_arguments_are_rejected():
     assert lib.whb_create(None, 0, 2, None, 0, 1, 1, 0) == _native.E_ARG
     assert lib.whb_destroy(None) == 0
     assert lib.whb_fpi(None, 1, -1.0, None, None) == _native.E_ARG
+    assert lib.whb_fpi_scaled(None, 1, -1.0, 1.0, None, None) == _native.E_ARG

@@ -19,7 +19,8 @@ from conftest import ROOT
 pytestmark = pytest.mark.gpu
 
 CASES = [((512, 512), 40.0), ((512, 512), 61.0), ((1024, 1024), 90.0), ((600, 600), 50.0), ((300, 300), 33.0),
-         ((256, 256), 40.0), ((400, 250), 30.0), ((90, 47, 61), 20.0), ((64, 64, 64), 11.0)]
+         ((256, 256), 40.0), ((400, 250), 30.0), ((90, 47, 61), 20.0), ((64, 64, 64), 11.0),
+         ((128, 128), 20.3), ((100, 37), 25.0), ((5, 300), 9.0), ((37, 4), 3.0)]
 
 SCRIPT = r"""
 import json, sys, numpy as np
@@ -46,7 +47,7 @@ print(json.dumps(out))
 """
 
 
-@pytest.mark.parametrize("env", [{}, {"WHB_WF": "2"}, {"WHB_WF": "0"}, {"WHB_TB2": "0"}, {"WHB_TB2R": "1"}, {"WHB_TB2W": "1"}, {"WHB_WF3": "1"}, {"WHB_KERNEL": "bulk"},
+@pytest.mark.parametrize("env", [{}, {"WHB_CRES": "0"}, {"WHB_CRES_CL": "8"}, {"WHB_CRES_CL": "3"}, {"WHB_WF": "2"}, {"WHB_WF": "0"}, {"WHB_TB2": "0"}, {"WHB_TB2R": "1"}, {"WHB_TB2W": "1"}, {"WHB_WF3": "1"}, {"WHB_KERNEL": "bulk"},
                                  {"WHB_KERNEL": "simple"}, {"WHB_NO_GRAPHS": "1"}])
 def test_every_kernel_path_bitwise(gpu_available, env):
     e = dict(os.environ, **env)
@@ -60,3 +61,5 @@ def test_every_kernel_path_bitwise(gpu_available, env):
     if not env:
         plans = {tuple(c): tuple(p) for c, _, _, p in res}
         assert plans[(512, 512)][1] == 4 and plans[(64, 64, 64)] == (2, 2)
+        # small 2D grids run cluster-resident (kernel 4)
+        assert plans[(128, 128)][0] == 4 and plans[(256, 256)][0] == 4 and plans[(300, 300)][0] == 1
