@@ -71,6 +71,7 @@ struct Args {
     double *hist;     // FPI: hist[(k0 + it) * nb + member idx] (nullptr: partials[0] for the reduction kernel)
     int k0, nb;
     int *done;        // FPI: iterations performed (written by member 0's cluster), may be nullptr
+    int dbg;
 };
 
 template <int KIND, bool ZF, bool SQ>
@@ -142,11 +143,11 @@ __global__ void __launch_bounds__(NT, 1)
     const int tx = threadIdx.x % TXc, ty = threadIdx.x / TXc;
     const bool active = ty < TY;
 
-    const double acc0 = accc[0], osc = m.out_scale;
     const bool fpi = m.out_mode == WHB_OUT_FPI;
     int p = 0;  // buffer holding W^0 of the current iteration
     int it = 0;
     cluster_sync();  // shared memory initialised cluster-wide before any remote store
+    const double acc0 = accc[0], osc = m.out_scale;  // (the table is filled before the barrier)
     for (; it < a.iters; ++it) {
         double rsum = 0.0;
         for (int s = 0; s < N; ++s) {
@@ -191,8 +192,10 @@ __global__ void __launch_bounds__(NT, 1)
                         }
                         if (store) {
                             nxt[c] = wn;
-                            if (lr == 0 && has_up) st_remote(upb + 8u * k, wn);
-                            if (lr == nr - 1 && has_dn) st_remote(dnb + 8u * k, wn);
+                            if (!(a.dbg & 8)) {
+                                if (lr == 0 && has_up) st_remote(upb + 8u * k, wn);
+                                if (lr == nr - 1 && has_dn) st_remote(dnb + 8u * k, wn);
+                            }
                         }
                     }
                 }
@@ -203,7 +206,10 @@ __global__ void __launch_bounds__(NT, 1)
                 if (threadIdx.x == 0)
                     for (int q = 0; q < CL; ++q) st_remote(map_rank(part_local, q), b);
             }
+            if (a.dbg & 2) __syncthreads();
             cluster_sync();
+            if (a.dbg & 1) __syncthreads();
+            if (a.dbg & 4) cluster_sync();
         }
         p ^= (N & 1);  // the last step wrote W^0 of the next iteration into buffer (N + p) & 1
         if (!fpi) {

@@ -937,7 +937,7 @@ int get_encoder() {
 }
 
 // ---- cluster-resident small-grid 2D kernel (step_cres2d.cuh) --------------------------------
-constexpr size_t kCresSmemMax = 227 * 1024;
+constexpr size_t kCresSmemMax = 227 * 1024 - 1024;  // opt-in maximum less the static block_sum scratch
 
 template <bool ZF, bool SQ>
 auto cres_fn() {
@@ -971,7 +971,12 @@ int cres_max_clusters(whb_ctx *c, int cl) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, cres_fn<false, false>(), &cfg) != cudaSuccess) n = 0;
+    const cudaError_t e = cudaOccupancyMaxActiveClusters(&n, cres_fn<false, false>(), &cfg);
+    if (e != cudaSuccess) {
+        if (getenv("WHB_DEBUG")) fprintf(stderr, "[whb] cudaOccupancyMaxActiveClusters: %s\n", cudaGetErrorString(e));
+        cudaGetLastError();
+        n = 0;
+    }
     return n;
 }
 
@@ -1190,12 +1195,16 @@ int plan_launch(whb_ctx *c) {
         cl = std::min(cl, cres::MAX_CL);
         while (cl > 1 && cl > NR) cl >>= 1;
         const int W = (int)c->gshape[2];
-        if (NR >= 1 && cres_set_attrs() == cudaSuccess) {
+        const cudaError_t ae = NR >= 1 ? cres_set_attrs() : cudaErrorInvalidValue;
+        if (getenv("WHB_DEBUG")) fprintf(stderr, "[whb] cres attrs: %s\n", cudaGetErrorString(ae));
+        if (ae == cudaSuccess) {
             // the cluster must be schedulable (cl SMs of one GPC): fall back to smaller clusters
             for (; cl >= 1; cl >>= 1) {
                 const int R = (NR + cl - 1) / cl;
                 if (cres::smem_doubles(R, W, false, 64, cl) * sizeof(double) > kCresSmemMax) break;
-                if (cres_max_clusters(c, cl) > 0) {
+                const int mc = cres_max_clusters(c, cl);
+                if (getenv("WHB_DEBUG")) fprintf(stderr, "[whb] cres cluster %d: %d active clusters\n", cl, mc);
+                if (mc > 0) {
                     c->cres = true;
                     c->cres_cl = cl;
                     c->cres_r = R;
@@ -1690,6 +1699,7 @@ int launch_cres(whb_ctx *c, size_t smem, int iters, double tol_sq, double *hist,
     a.k0 = k0;
     a.nb = c->nbatch;
     a.done = done;
+    a.dbg = getenv("WHB_CRES_DBG") ? atoi(getenv("WHB_CRES_DBG")) : 0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(c->cres_cl, c->nbatch, 1);
     cfg.blockDim = dim3(cres::NT, 1, 1);
