@@ -5,12 +5,13 @@
 // a pass is ~1 us of traffic but ~5-7 us of launch + pipeline fill, so config 1 ran at 8 Gpts/s.
 // Here one cluster of CL CTAs (CL <= 16, one per SM) owns one problem for a whole launch:
 //
-//   * CTA r of the cluster owns the band of interior rows [rb, re) (CL near-equal bands).  Its
-//     shared memory holds two time-level buffers (W^n and W^{n+1}/W^{n-1}, each with one halo
-//     row above and below the band), f, acc, v and the per-step scalars (cos(w t^n),
-//     (cos - alpha/2) sigma_n): every step of every iteration is computed from shared memory.
-//   * Step n reads W^n from buffer n&1 and writes W^{n+1} over W^{n-1} in the other buffer (the
-//     point's own W^{n-1} is read by the same thread just before).  A band's first and last rows
+//   * CTA r of the cluster owns the band of interior rows [rb, re) (CL near-equal bands); each
+//     thread owns up to PPT of its points and keeps their f, acc, v, W^n and W^{n-1} in
+//     registers.  Shared memory holds two time-level buffers (each with one halo row above and
+//     below the band) through which neighbours read W^n, and the per-step scalars (cos(w t^n),
+//     (cos - alpha/2) sigma_n): every step of every iteration runs from registers + shared memory.
+//   * Step n reads the 4 neighbours' W^n from buffer n&1 and publishes the point's W^{n+1} in the
+//     other buffer (over W^{n-1}, which nobody reads any more).  A band's first and last rows
 //     are also stored into the neighbouring CTAs' halo rows with st.shared::cluster (DSMEM);
 //     one cluster barrier (arrive.release / wait.acquire) per step orders those stores before
 //     the neighbours' next reads and every read of a buffer before its next overwrite.
@@ -27,7 +28,8 @@
 
 namespace cres {
 
-constexpr int NT = 1024;  // threads per CTA (one CTA per SM)
+constexpr int NT = 512;  // threads per CTA (one CTA per SM)
+constexpr int MAX_PPT = 8;  // band points per thread (registers)
 constexpr int MAX_CL = 16;
 
 __device__ __forceinline__ uint32_t cta_rank() {
@@ -54,10 +56,10 @@ __device__ __forceinline__ void st_remote(uint32_t addr, double v) {
 // Band of interior rows owned by CTA r: [1 + r*NR/CL, 1 + (r+1)*NR/CL), NR = n0 - 2.
 __host__ __device__ __forceinline__ int band_begin(int r, int NR, int CL) { return 1 + (int)(((long long)r * NR) / CL); }
 
-// Shared-memory layout (doubles): buf[0] | buf[1] ((R+2) x W each) | f (R x W, absent when
-// ZF) | acc | v (R x W) | cos_f[Nmax] | acc_c[Nmax + 1] | partials[CL]
-__host__ __device__ __forceinline__ size_t smem_doubles(int R, int W, bool zf, int nmax, int CL) {
-    return (size_t)2 * (R + 2) * W + (size_t)(zf ? 2 : 3) * R * W + (size_t)(2 * nmax + 1) + CL;
+// Shared-memory layout (doubles): buf[0] | buf[1] ((R+2) x W each) | cos_f[Nmax] |
+// acc_c[Nmax + 1] | partials[CL].  f, acc, v and the point's own W^n, W^{n-1} live in registers.
+__host__ __device__ __forceinline__ size_t smem_doubles(int R, int W, int nmax, int CL) {
+    return (size_t)2 * (R + 2) * W + (size_t)(2 * nmax + 1) + CL;
 }
 
 struct Args {
@@ -74,14 +76,7 @@ struct Args {
     int dbg;
 };
 
-template <int KIND, bool ZF, bool SQ>
-__device__ __forceinline__ double cres_point(const Geom &g, const double *cur, int c, int W, double fv, double wpv,
-                                             double h, double cosn) {
-    return bulk::update_point<KIND, ZF, false, SQ>(g, cur[c - W], cur[c], cur[c + W], 0.0, 0.0, cur[c - 1],
-                                                   cur[c + 1], fv, wpv, h, cosn);
-}
-
-template <bool ZF, bool SQ>
+template <bool ZF, bool SQ, int PPT>
 __global__ void __launch_bounds__(NT, 1)
     cres2d_kernel(Geom g, const Member *__restrict__ members, int member_off, Args a) {
     extern __shared__ __align__(16) double sm[];
@@ -95,32 +90,22 @@ __global__ void __launch_bounds__(NT, 1)
     const bool has_up = rank > 0, has_dn = rank < CL - 1;
     const size_t BUF = (size_t)(a.R + 2) * W;
     double *buf0 = sm, *buf1 = sm + BUF;
-    double *fs = buf1 + BUF;
-    double *accs = fs + (ZF ? 0 : (size_t)a.R * W);
-    double *vs = accs + (size_t)a.R * W;
-    double *cosf = vs + (size_t)a.R * W;
+    double *cosf = buf1 + BUF;
     double *accc = cosf + a.nmax;
     double *part = accc + a.nmax + 1;
     const int N = m.n_total;
     const long long S0 = g.S0;
     const int GH0 = g.i_lo - 1;  // local plane of global row 0 (= ghost planes)
 
-    // zero everything (boundary columns, halo rows at the global boundary), then load v (band +
-    // the rows above/below it: W^0 halos), f and the scalar tables
-    const size_t total = smem_doubles(a.R, W, ZF, a.nmax, CL);
+    // zero the two level buffers (boundary columns, halo rows at the global boundary), then
+    // W^0 = v on the band and the rows above/below it, and the scalar tables
+    const size_t total = smem_doubles(a.R, W, a.nmax, CL);
     for (size_t i = threadIdx.x; i < total; i += NT) sm[i] = 0.0;
     __syncthreads();
     for (int t = threadIdx.x; t < (nr + 2) * n2; t += NT) {
         const int lr = t / n2, k = t - lr * n2;  // buffer row lr <-> global row rb - 1 + lr
-        const double x = m.v[(long long)(GH0 + rb - 1 + lr) * S0 + k];
-        buf0[lr * W + k] = x;
-        if (lr >= 1 && lr <= nr) vs[(lr - 1) * W + k] = x;
+        buf0[lr * W + k] = m.v[(long long)(GH0 + rb - 1 + lr) * S0 + k];
     }
-    if (!ZF)
-        for (int t = threadIdx.x; t < nr * n2; t += NT) {
-            const int lr = t / n2, k = t - lr * n2;
-            fs[lr * W + k] = m.f[(long long)(GH0 + rb + lr) * S0 + k];
-        }
     for (int t = threadIdx.x; t < N; t += NT) cosf[t] = m.cos_f[t];
     for (int t = threadIdx.x; t <= N; t += NT) accc[t] = m.acc_c[t];
     // remote halo rows: my first row lands in the upper neighbour's bottom halo row (nr_up + 1),
@@ -136,17 +121,36 @@ __global__ void __launch_bounds__(NT, 1)
     }
     const uint32_t part_local = bulk::smem_u32(part + rank);
 
-    // thread -> (row group, column) map: TXc columns (warp multiple) x TY row groups
+    // the thread's points (band-interior point q = threadIdx.x + i * NT, row-major over nr x (n2-2)):
+    // shared index, global offset, halo duties, and the point's own state in registers
     const int ncol = n2 - 2;
-    const int TXc = min(NT, (ncol + 31) / 32 * 32);
-    const int TY = NT / TXc;
-    const int tx = threadIdx.x % TXc, ty = threadIdx.x / TXc;
-    const bool active = ty < TY;
+    const int npts = nr * ncol;
+    int cidx[PPT], kidx[PPT];
+    int goff[PPT];  // < 2^31: the grid fits in one cluster's shared memory
+    bool ok[PPT], pu[PPT], pd[PPT];
+    double wc[PPT], wp[PPT], fv[PPT], ac[PPT], vv[PPT];
+#pragma unroll
+    for (int i = 0; i < PPT; ++i) {
+        const int q = threadIdx.x + i * NT;
+        ok[i] = q < npts;
+        const int lr = ok[i] ? q / ncol : 0;
+        const int k = ok[i] ? 1 + (q - lr * ncol) : 1;
+        cidx[i] = (lr + 1) * W + k;
+        kidx[i] = k;
+        goff[i] = (int)((long long)(GH0 + rb + lr) * S0 + k);
+        pu[i] = ok[i] && lr == 0 && has_up;
+        pd[i] = ok[i] && lr == nr - 1 && has_dn;
+        vv[i] = ok[i] ? m.v[goff[i]] : 0.0;
+        fv[i] = (ok[i] && !ZF) ? m.f[goff[i]] : 0.0;
+        wc[i] = vv[i];
+        wp[i] = 0.0;
+        ac[i] = 0.0;
+    }
 
     const bool fpi = m.out_mode == WHB_OUT_FPI;
     int p = 0;  // buffer holding W^0 of the current iteration
     int it = 0;
-    cluster_sync();  // shared memory initialised cluster-wide before any remote store
+    cluster_sync();  // shared memory initialised cluster-wide before any read or remote store
     const double acc0 = accc[0], osc = m.out_scale;  // (the table is filled before the barrier)
     for (; it < a.iters; ++it) {
         double rsum = 0.0;
@@ -155,60 +159,47 @@ __global__ void __launch_bounds__(NT, 1)
             const double *cur = bc ? buf1 : buf0;
             double *nxt = bc ? buf0 : buf1;
             const uint32_t upb = bc ? up0 : up1, dnb = bc ? dn0 : dn1;  // remote halos of nxt
-            const double h = s == 0 ? m.half_dt2 : m.dt2;
-            const double cosn = s == 0 ? 1.0 : cosf[s];
             const double accn = accc[s + 1];
-            if (active) {
-                for (int lr = ty; lr < nr; lr += TY) {
-                    for (int k = 1 + tx; k < n2 - 1; k += TXc) {
-                        const int c = (lr + 1) * W + k;  // buffer index (row lr of the band)
-                        const int o = lr * W + k;        // band index (f, acc, v)
-                        const double fv = ZF ? 0.0 : fs[o];
-                        double wn, out = 0.0;
-                        bool store = true;
-                        if (s == 0) {
-                            wn = cres_point<K_FIRST, ZF, SQ>(g, cur, c, W, fv, 0.0, h, cosn);
-                            const double ac = whb_add(whb_mul(acc0, cur[c]), whb_mul(accn, wn));
-                            if (s == N - 1) out = whb_mul(osc, ac);
-                            else accs[o] = ac;
-                        } else {
-                            wn = cres_point<K_MID, ZF, SQ>(g, cur, c, W, fv, nxt[c], h, cosn);
-                            const double ac = whb_add(accs[o], whb_mul(accn, wn));
-                            if (s == N - 1) out = whb_mul(osc, ac);
-                            else accs[o] = ac;
-                        }
-                        if (s == N - 1) {
-                            const double vo = vs[o];
-                            if (fpi) {
-                                const double d = out - vo;
-                                rsum += d * d;
-                                vs[o] = out;
-                                wn = out;  // W^0 of the next iteration
-                            } else {
-                                double *dst = m.dst + (long long)(GH0 + rb + lr) * S0 + k;
-                                *dst = (m.out_mode == WHB_OUT_AV) ? whb_sub(vo, out) : out;
-                                store = false;
-                            }
-                        }
-                        if (store) {
-                            nxt[c] = wn;
-                            if (!(a.dbg & 8)) {
-                                if (lr == 0 && has_up) st_remote(upb + 8u * k, wn);
-                                if (lr == nr - 1 && has_dn) st_remote(dnb + 8u * k, wn);
-                            }
-                        }
+            const bool last = s == N - 1;
+#pragma unroll
+            for (int i = 0; i < PPT; ++i) {
+                if (!ok[i]) continue;
+                const int c = cidx[i];
+                double wn;
+                if (s == 0) {
+                    wn = bulk::update_point<K_FIRST, ZF, false, SQ>(g, cur[c - W], wc[i], cur[c + W], 0.0, 0.0,
+                                                                  cur[c - 1], cur[c + 1], fv[i], 0.0, m.half_dt2, 1.0);
+                    ac[i] = whb_add(whb_mul(acc0, wc[i]), whb_mul(accn, wn));
+                } else {
+                    wn = bulk::update_point<K_MID, ZF, false, SQ>(g, cur[c - W], wc[i], cur[c + W], 0.0, 0.0,
+                                                                cur[c - 1], cur[c + 1], fv[i], wp[i], m.dt2, cosf[s]);
+                    ac[i] = whb_add(ac[i], whb_mul(accn, wn));
+                }
+                wp[i] = wc[i];
+                wc[i] = wn;
+                if (last) {
+                    const double out = whb_mul(osc, ac[i]);
+                    if (fpi) {
+                        const double d = out - vv[i];
+                        rsum += d * d;
+                        vv[i] = out;
+                        wc[i] = out;  // W^0 of the next iteration
+                    } else {
+                        m.dst[goff[i]] = (m.out_mode == WHB_OUT_AV) ? whb_sub(vv[i], out) : out;
+                        continue;
                     }
                 }
+                nxt[c] = wc[i];
+                if (pu[i]) st_remote(upb + 8u * kidx[i], wc[i]);
+                if (pd[i]) st_remote(dnb + 8u * kidx[i], wc[i]);
             }
-            if (s == N - 1 && fpi) {
+            if (last && fpi) {
                 // CTA partial -> slot `rank` of every CTA's partial table (ordered by the barrier below)
                 const double b = block_sum(rsum);
                 if (threadIdx.x == 0)
                     for (int q = 0; q < CL; ++q) st_remote(map_rank(part_local, q), b);
             }
-            if (a.dbg & 2) __syncthreads();
             cluster_sync();
-            if (a.dbg & 1) __syncthreads();
             if (a.dbg & 4) cluster_sync();
         }
         p ^= (N & 1);  // the last step wrote W^0 of the next iteration into buffer (N + p) & 1
@@ -229,12 +220,11 @@ __global__ void __launch_bounds__(NT, 1)
             break;
         }
     }
-    // the iterate (FPI) back to HBM
-    if (fpi)
-        for (int t = threadIdx.x; t < nr * n2; t += NT) {
-            const int lr = t / n2, k = t - lr * n2;
-            m.v[(long long)(GH0 + rb + lr) * S0 + k] = vs[lr * W + k];
-        }
+    if (fpi) {  // the iterate back to HBM
+#pragma unroll
+        for (int i = 0; i < PPT; ++i)
+            if (ok[i]) m.v[goff[i]] = vv[i];
+    }
     if (a.done && blockIdx.y == 0 && rank == 0 && threadIdx.x == 0) *a.done = it;
     cluster_sync();  // no CTA exits while a neighbour may still address its shared memory
 }

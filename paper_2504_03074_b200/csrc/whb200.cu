@@ -660,7 +660,7 @@ struct whb_ctx {
     bool tb2w = false;               // 3D: warp-specialised two-step kernel
     // cluster-resident small-grid 2D plan (whole grid in one cluster's shared memory)
     bool cres = false;
-    int cres_cl = 0, cres_r = 0;
+    int cres_cl = 0, cres_r = 0, cres_ppt = 1;
     // 3D three-step wavefront plan (whole-grid 3D contexts)
     bool wf3 = false;
     size_t smem3 = 0;
@@ -939,9 +939,9 @@ int get_encoder() {
 // ---- cluster-resident small-grid 2D kernel (step_cres2d.cuh) --------------------------------
 constexpr size_t kCresSmemMax = 227 * 1024 - 1024;  // opt-in maximum less the static block_sum scratch
 
-template <bool ZF, bool SQ>
+template <bool ZF, bool SQ, int PPT>
 auto cres_fn() {
-    return cres::cres2d_kernel<ZF, SQ>;
+    return cres::cres2d_kernel<ZF, SQ, PPT>;
 }
 
 cudaError_t cres_set_attrs() {
@@ -952,9 +952,21 @@ cudaError_t cres_set_attrs() {
         r = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (r != cudaSuccess) e = r;
     };
-    set(cres_fn<false, false>()); set(cres_fn<true, false>());
-    set(cres_fn<false, true>());  set(cres_fn<true, true>());
+#define WHB_CRES_SET(PPT)                                                  \
+    set(cres_fn<false, false, PPT>()); set(cres_fn<true, false, PPT>());   \
+    set(cres_fn<false, true, PPT>());  set(cres_fn<true, true, PPT>());
+    WHB_CRES_SET(1) WHB_CRES_SET(2) WHB_CRES_SET(4) WHB_CRES_SET(8)
+#undef WHB_CRES_SET
     return e;
+}
+
+// points per thread of a cluster of cl CTAs on this grid (0: more than cres::MAX_PPT)
+int cres_ppt(whb_ctx *c, int cl) {
+    const int NR = (int)c->gshape[0] - 2;
+    const long long pts = (long long)((NR + cl - 1) / cl) * (c->gshape[2] - 2);
+    for (int p = 1; p <= cres::MAX_PPT; p *= 2)
+        if (pts <= (long long)p * cres::NT) return p;
+    return 0;
 }
 
 int cres_max_clusters(whb_ctx *c, int cl) {
@@ -962,7 +974,7 @@ int cres_max_clusters(whb_ctx *c, int cl) {
     cfg.gridDim = dim3(cl, 1, 1);
     cfg.blockDim = dim3(cres::NT, 1, 1);
     const int R = ((int)c->gshape[0] - 2 + cl - 1) / cl;
-    cfg.dynamicSmemBytes = cres::smem_doubles(R, (int)c->gshape[2], false, 64, cl) * sizeof(double);
+    cfg.dynamicSmemBytes = cres::smem_doubles(R, (int)c->gshape[2], 64, cl) * sizeof(double);
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = cl;
@@ -971,7 +983,7 @@ int cres_max_clusters(whb_ctx *c, int cl) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int n = 0;
-    const cudaError_t e = cudaOccupancyMaxActiveClusters(&n, cres_fn<false, false>(), &cfg);
+    const cudaError_t e = cudaOccupancyMaxActiveClusters(&n, cres_fn<false, false, 8>(), &cfg);
     if (e != cudaSuccess) {
         if (getenv("WHB_DEBUG")) fprintf(stderr, "[whb] cudaOccupancyMaxActiveClusters: %s\n", cudaGetErrorString(e));
         cudaGetLastError();
@@ -1201,13 +1213,14 @@ int plan_launch(whb_ctx *c) {
             // the cluster must be schedulable (cl SMs of one GPC): fall back to smaller clusters
             for (; cl >= 1; cl >>= 1) {
                 const int R = (NR + cl - 1) / cl;
-                if (cres::smem_doubles(R, W, false, 64, cl) * sizeof(double) > kCresSmemMax) break;
+                if (cres::smem_doubles(R, W, 64, cl) * sizeof(double) > kCresSmemMax || !cres_ppt(c, cl)) break;
                 const int mc = cres_max_clusters(c, cl);
                 if (getenv("WHB_DEBUG")) fprintf(stderr, "[whb] cres cluster %d: %d active clusters\n", cl, mc);
                 if (mc > 0) {
                     c->cres = true;
                     c->cres_cl = cl;
                     c->cres_r = R;
+                    c->cres_ppt = cres_ppt(c, cl);
                     break;
                 }
             }
@@ -1677,8 +1690,7 @@ int active_members(whb_ctx *c, int s) {
 // Shared memory of a cluster-resident launch over the current members (0: does not fit).
 size_t cres_smem(whb_ctx *c) {
     if (!c->cres || c->kern == 3) return 0;
-    const size_t b = cres::smem_doubles(c->cres_r, (int)c->gshape[2], c->cur_zf != 0, max_steps(c), c->cres_cl) *
-                     sizeof(double);
+    const size_t b = cres::smem_doubles(c->cres_r, (int)c->gshape[2], max_steps(c), c->cres_cl) * sizeof(double);
     return b <= kCresSmemMax ? b : 0;
 }
 
@@ -1715,11 +1727,17 @@ int launch_cres(whb_ctx *c, size_t smem, int iters, double tol_sq, double *hist,
     const Geom &g = c->geom;
     const bool sq = g.clo0 == g.clo2 && g.cmid0 == g.cmid2;
     const bool zf = c->cur_zf != 0;
-    cudaError_t e;
-    if (zf) e = sq ? cudaLaunchKernelEx(&cfg, cres_fn<true, true>(), g, (const Member *)c->d_members, 0, a)
-                   : cudaLaunchKernelEx(&cfg, cres_fn<true, false>(), g, (const Member *)c->d_members, 0, a);
-    else e = sq ? cudaLaunchKernelEx(&cfg, cres_fn<false, true>(), g, (const Member *)c->d_members, 0, a)
-                : cudaLaunchKernelEx(&cfg, cres_fn<false, false>(), g, (const Member *)c->d_members, 0, a);
+    cudaError_t e = cudaErrorInvalidValue;
+    const Member *mt = c->d_members;
+#define WHB_CRES_GO(PPT)                                                                               \
+    if (c->cres_ppt == PPT) {                                                                          \
+        if (zf) e = sq ? cudaLaunchKernelEx(&cfg, cres_fn<true, true, PPT>(), g, mt, 0, a)             \
+                       : cudaLaunchKernelEx(&cfg, cres_fn<true, false, PPT>(), g, mt, 0, a);           \
+        else e = sq ? cudaLaunchKernelEx(&cfg, cres_fn<false, true, PPT>(), g, mt, 0, a)               \
+                    : cudaLaunchKernelEx(&cfg, cres_fn<false, false, PPT>(), g, mt, 0, a);             \
+    }
+    WHB_CRES_GO(1) WHB_CRES_GO(2) WHB_CRES_GO(4) WHB_CRES_GO(8)
+#undef WHB_CRES_GO
     WHB_CUDA(e);
     c->launches++;
     return 0;
