@@ -34,7 +34,8 @@ def main(rnd):
             d = last_json(os.path.join(SRC, f"{arm}_{w}.json"))
             if d is not None:
                 json.dump(d, open(os.path.join(dst, f"{arm}_{w}.json"), "w"))
-    cmds = {"cfg2": "--workload cfg2 --steps 2 --warmup 1", "cfg3": "--workload cfg3 --steps 2 --warmup 1",
+    cmds = {"cfg1": "--workload cfg1 --steps 2 --warmup 1", "cfg2": "--workload cfg2 --steps 2 --warmup 1",
+            "cfg3": "--workload cfg3 --steps 2 --warmup 1", "cfg4": "--workload cfg4 --steps 1 --warmup 1",
             "cfg5": "--workload cfg5 --steps 1 --warmup 1"}
     for w, a in cmds.items():
         p = os.path.join(SRC, f"launches_{w}.csv")
@@ -44,7 +45,8 @@ def main(rnd):
             json.dump(out, open(os.path.join(dst, f"launches_{w}.json"), "w"), indent=1)
     traffic_path = os.path.join(ROOT, "profiles", "traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
-    for name, w in (("ncu_cfg2_wf", "cfg2"), ("ncu_cfg3_tb2", "cfg3"), ("ncu_imp2_gs", "imp2")):
+    for name, w in (("ncu_cfg1_cres", "cfg1"), ("ncu_cfg2_wf", "cfg2"), ("ncu_cfg3_tb2", "cfg3"),
+                    ("ncu_cfg4_tb2", "cfg4"), ("ncu_imp2_gs", "imp2")):
         rep = os.path.join(SRC, name + ".ncu-rep")
         if not os.path.exists(rep):
             continue
