@@ -13,6 +13,9 @@ import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "lib", "libwhb200.so")
+# tuning sweeps only: WHB_LIB names a variant build under lib/variants/ (tools/variants.py)
+if os.environ.get("WHB_LIB"):
+    LIB_PATH = os.path.join(_PKG, "lib", "variants", os.path.basename(os.environ["WHB_LIB"]))
 
 # enum whb_field / whb_out_mode (include/whb200.h)
 V, F, WA, WB, ACC, OUT, WC, WD = range(8)

@@ -69,7 +69,10 @@ struct WfScal {
 // PS: scalars from `ps` (one member per launch) instead of the member table.
 // SQ: square cells (both axes carry bitwise-equal taps): one centre product per point.
 template <int T, int NW, int ST, int K1, int K2, bool ZF, int SKEW = 1, bool PS = false, bool SQ = false>
-__global__ void __launch_bounds__(Lay<T, NW>::THREADS, 3)
+#ifndef WHB_WF_MINB
+#define WHB_WF_MINB 3
+#endif
+__global__ void __launch_bounds__(Lay<T, NW>::THREADS, WHB_WF_MINB)
     wf2d_kernel(Geom g, const Member *__restrict__ members, int member_off, int s, int i_begin, int i_end,
                 int chunk_len, int part_off, WfScal ps) {
     using L = Lay<T, NW>;

@@ -869,12 +869,22 @@ cudaError_t wf3_set_attrs(size_t smem) {
 }
 
 // 2D wavefront kernels: 4 consumer warps + 1 producer warp, T + 4 row stages.
-constexpr int WF_NW = 4;
+// (the WHB_WF_* macros exist for variant builds in tuning sweeps: tools/variants.py)
+#ifndef WHB_WF_NW
+#define WHB_WF_NW 4
+#endif
+#ifndef WHB_WF_SKEW
+#define WHB_WF_SKEW 1
+#endif
+#ifndef WHB_WF_ST_EXTRA
+#define WHB_WF_ST_EXTRA 5
+#endif
+constexpr int WF_NW = WHB_WF_NW;
 
 // T = 4 runs the skewed wavefront (level t at row r - 2t + 1: independent level updates per
 // row, 2T + 4 stages); T = 2 the plain one.
-constexpr int WF_SKEW4 = 1;
-constexpr int WF_ST4 = wf2d::wf_lag<WF_SKEW4>(4) + 5;  // 9 stages, 3 CTAs/SM (measured: 7 stages at 4 CTAs/SM is 1.4 % slower)
+constexpr int WF_SKEW4 = WHB_WF_SKEW;
+constexpr int WF_ST4 = wf2d::wf_lag<WF_SKEW4>(4) + WHB_WF_ST_EXTRA;  // 9 stages, 3 CTAs/SM (measured: 7 stages at 4 CTAs/SM is 1.4 % slower)
 template <int T, int K1, int K2, bool ZF, bool PS = false, bool SQ = false>
 auto wf_fn() {
     if constexpr (T == 4) return wf2d::wf2d_kernel<4, WF_NW, WF_ST4, K1, K2, ZF, WF_SKEW4, PS, SQ>;
