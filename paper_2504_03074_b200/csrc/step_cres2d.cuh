@@ -28,7 +28,10 @@
 
 namespace cres {
 
-constexpr int NT = 512;  // threads per CTA (one CTA per SM)
+#ifndef WHB_CRES_NT
+#define WHB_CRES_NT 512
+#endif
+constexpr int NT = WHB_CRES_NT;  // threads per CTA (one CTA per SM)
 constexpr int MAX_PPT = 8;  // band points per thread (registers)
 constexpr int MAX_CL = 16;
 
@@ -42,6 +45,20 @@ __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// Per-step barrier: shared-memory writes of this CTA are ordered by bar.sync; only the threads
+// that stored into a neighbour's shared memory (DSMEM) fence at cluster scope before a relaxed
+// cluster arrival (WHB_CRES_RELAXED variant; the default is the release/acquire cluster barrier).
+__device__ __forceinline__ void step_sync(bool remote) {
+#ifdef WHB_CRES_RELAXED
+    if (remote) asm volatile("fence.acq_rel.cluster;" ::: "memory");
+    __syncthreads();
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+#else
+    (void)remote;
+    cluster_sync();
+#endif
+}
+
 // shared::cta address -> the same offset in CTA `rank` of the cluster (shared::cluster window)
 __device__ __forceinline__ uint32_t map_rank(uint32_t addr, uint32_t rank) {
     uint32_t r;
@@ -53,13 +70,30 @@ __device__ __forceinline__ void st_remote(uint32_t addr, double v) {
     asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
 }
 
+// Neighbour-only step synchronisation (WHB_CRES_NBSYNC variant): an mbarrier per level buffer
+// counts the neighbours' "my edge rows of this buffer are stored, and I finished reading the
+// other buffer" arrivals (remote arrive with release at cluster scope after the CTA barrier).
+__device__ __forceinline__ void mbar_remote_arrive(uint32_t remote_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_addr) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t addr, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WHB_CW%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WHB_CW%=;\n}" ::"r"(addr),
+        "r"(parity)
+        : "memory");
+}
+
 // Band of interior rows owned by CTA r: [1 + r*NR/CL, 1 + (r+1)*NR/CL), NR = n0 - 2.
 __host__ __device__ __forceinline__ int band_begin(int r, int NR, int CL) { return 1 + (int)(((long long)r * NR) / CL); }
 
 // Shared-memory layout (doubles): buf[0] | buf[1] ((R+2) x W each) | cos_f[Nmax] |
 // acc_c[Nmax + 1] | partials[CL].  f, acc, v and the point's own W^n, W^{n-1} live in registers.
 __host__ __device__ __forceinline__ size_t smem_doubles(int R, int W, int nmax, int CL) {
-    return (size_t)2 * (R + 2) * W + (size_t)(2 * nmax + 1) + CL;
+    return (size_t)2 * (R + 2) * W + (size_t)(2 * nmax + 1) + CL + 2;  // + 2 mbarriers
 }
 
 struct Args {
@@ -93,6 +127,7 @@ __global__ void __launch_bounds__(NT, 1)
     double *cosf = buf1 + BUF;
     double *accc = cosf + a.nmax;
     double *part = accc + a.nmax + 1;
+    uint64_t *nbar = reinterpret_cast<uint64_t *>(part + CL);  // per level buffer (NBSYNC variant)
     const int N = m.n_total;
     const long long S0 = g.S0;
     const int GH0 = g.i_lo - 1;  // local plane of global row 0 (= ghost planes)
@@ -102,6 +137,18 @@ __global__ void __launch_bounds__(NT, 1)
     const size_t total = smem_doubles(a.R, W, a.nmax, CL);
     for (size_t i = threadIdx.x; i < total; i += NT) sm[i] = 0.0;
     __syncthreads();
+#ifdef WHB_CRES_NBSYNC
+    if (threadIdx.x == 0) {
+        const uint32_t nn = (rank > 0 ? 1u : 0u) + (rank < CL - 1 ? 1u : 0u);
+        bulk::mbar_init(nbar, nn > 0 ? nn : 1u);
+        bulk::mbar_init(nbar + 1, nn > 0 ? nn : 1u);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    uint32_t nphase[2] = {0u, 0u};
+    const uint32_t nbar_local = bulk::smem_u32(nbar);
+    const uint32_t nbar_up = rank > 0 ? map_rank(nbar_local, rank - 1) : 0u;
+    const uint32_t nbar_dn = rank < CL - 1 ? map_rank(nbar_local, rank + 1) : 0u;
+#endif
     for (int t = threadIdx.x; t < (nr + 2) * n2; t += NT) {
         const int lr = t / n2, k = t - lr * n2;  // buffer row lr <-> global row rb - 1 + lr
         buf0[lr * W + k] = m.v[(long long)(GH0 + rb - 1 + lr) * S0 + k];
@@ -147,6 +194,9 @@ __global__ void __launch_bounds__(NT, 1)
         ac[i] = 0.0;
     }
 
+    bool has_remote = false;
+#pragma unroll
+    for (int i = 0; i < PPT; ++i) has_remote = has_remote || pu[i] || pd[i];
     const bool fpi = m.out_mode == WHB_OUT_FPI;
     int p = 0;  // buffer holding W^0 of the current iteration
     int it = 0;
@@ -199,8 +249,25 @@ __global__ void __launch_bounds__(NT, 1)
                 if (threadIdx.x == 0)
                     for (int q = 0; q < CL; ++q) st_remote(map_rank(part_local, q), b);
             }
-            cluster_sync();
+#ifdef WHB_CRES_NBSYNC
+            if (last) {
+                cluster_sync();  // the residual partials: once per fixed-point iteration, whole cluster
+            } else {
+                __syncthreads();
+                const int bn = bc ^ 1;  // buffer this step filled
+                if (threadIdx.x == 0) {
+                    if (has_up) mbar_remote_arrive(nbar_up + 8u * bn);
+                    if (has_dn) mbar_remote_arrive(nbar_dn + 8u * bn);
+                }
+                if (has_up || has_dn) {
+                    mbar_wait_cluster(nbar_local + 8u * bn, nphase[bn] & 1u);
+                    nphase[bn]++;
+                }
+            }
+#else
+            step_sync(has_remote || (last && fpi && threadIdx.x == 0));
             if (a.dbg & 4) cluster_sync();
+#endif
         }
         p ^= (N & 1);  // the last step wrote W^0 of the next iteration into buffer (N + p) & 1
         if (!fpi) {
