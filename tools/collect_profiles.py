@@ -2,7 +2,12 @@
 files: bench lines, per-kernel launch shares, ncu --set full summaries, and
 profiles/traffic.json (DRAM bytes per launch of each dominant kernel).
 
-    python tools/collect_profiles.py r01
+    python tools/collect_profiles.py r01 [SRC [DST_ROOT]]
+
+On the GPU box measure_all.sh runs it with DST_ROOT=gpurun_out/m/collected (the .ncu-rep
+files are summarised there and then deleted: gpurun copies back at most 64 MiB); here,
+`python tools/collect_profiles.py r01 gpurun_out/m/collected/profiles/r01 .` is not needed —
+copy gpurun_out/m/collected/profiles/ over profiles/.
 """
 
 import json
@@ -26,8 +31,12 @@ def last_json(path):
         return None
 
 
-def main(rnd):
-    dst = os.path.join(ROOT, "profiles", rnd)
+def main(rnd, src=None, dst_root=None):
+    global SRC
+    if src:
+        SRC = os.path.abspath(src)
+    dst_root = os.path.abspath(dst_root) if dst_root else ROOT
+    dst = os.path.join(dst_root, "profiles", rnd)
     os.makedirs(dst, exist_ok=True)
     for w in ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "imp2"):
         for arm in ("bench", "bench_reference"):
@@ -43,7 +52,11 @@ def main(rnd):
             out = summarise(p, f"ncu --metrics gpu__time_duration.sum --clock-control none python bench.py {a} "
                                "--no-e2e --no-cpu-baseline")
             json.dump(out, open(os.path.join(dst, f"launches_{w}.json"), "w"), indent=1)
-    traffic_path = os.path.join(ROOT, "profiles", "traffic.json")
+    traffic_path = os.path.join(dst_root, "profiles", "traffic.json")
+    if not os.path.exists(traffic_path) and os.path.exists(os.path.join(ROOT, "profiles", "traffic.json")):
+        traffic_path_src = os.path.join(ROOT, "profiles", "traffic.json")
+        os.makedirs(os.path.dirname(traffic_path), exist_ok=True)
+        open(traffic_path, "w").write(open(traffic_path_src).read())
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
     for name, w in (("ncu_cfg1_cres", "cfg1"), ("ncu_cfg2_wf", "cfg2"), ("ncu_cfg3_tb2", "cfg3"),
                     ("ncu_cfg4_tb2", "cfg4"), ("ncu_imp2_gs", "imp2")):
@@ -65,4 +78,4 @@ def main(rnd):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "r01")
+    main(sys.argv[1] if len(sys.argv) > 1 else "r01", *sys.argv[2:4])

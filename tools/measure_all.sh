@@ -8,10 +8,14 @@ OUT=gpurun_out/m
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/gpu.txt 2>&1
 
-for w in cfg1 cfg2 cfg3 cfg4 cfg5 imp2; do
+PART=${MEASURE_PART:-all}
+if [ "$PART" != ncu ]; then
+for w in ${MEASURE_WORKLOADS:-cfg1 cfg2 cfg3 cfg4 cfg5 imp2}; do
   python bench.py --workload $w > $OUT/bench_$w.json 2> $OUT/bench_$w.err
   python bench.py --workload $w --impl reference > $OUT/bench_reference_$w.json 2> $OUT/bench_reference_$w.err
 done
+fi
+if [ "$PART" != bench ]; then
 
 # launch lists (cold-cache, serialised: shares only); each command first runs plainly
 L="--metrics gpu__time_duration.sum --clock-control none --csv"
@@ -34,4 +38,12 @@ $C1 > $OUT/plain_cfg1b.json && ncu $F -k regex:cres2d_kernel -s 1 -o $OUT/ncu_cf
 $C4 > $OUT/plain_cfg4b.json && ncu $F -k regex:tb2_kernel -s 10 -o $OUT/ncu_cfg4_tb2 $C4 > $OUT/ncu_f_cfg4.log 2>&1
 CI="python bench.py --workload imp2 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
 $CI > $OUT/plain_imp2.json && ncu $F -k regex:gs_block_kernel -s 200 -o $OUT/ncu_imp2_gs $CI > $OUT/ncu_f_imp2.log 2>&1
+fi
+# summarise on the box (ncu -i) and drop the reports: gpurun copies back at most 64 MiB
+python tools/collect_profiles.py r01 $OUT $OUT/collected > $OUT/collect.log 2>&1
+for r in $OUT/*.ncu-rep; do
+  [ -e "$r" ] || continue
+  ncu -i "$r" --page raw --csv > "${r%.ncu-rep}_raw.csv" 2>/dev/null
+  rm -f "$r"
+done
 echo done > $OUT/DONE
