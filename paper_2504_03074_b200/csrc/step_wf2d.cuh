@@ -69,6 +69,11 @@ struct WfScal {
 // PS: scalars from `ps` (one member per launch) instead of the member table.
 // SQ: square cells (both axes carry bitwise-equal taps): one centre product per point.
 template <int T, int NW, int ST, int K1, int K2, bool ZF, int SKEW = 1, bool PS = false, bool SQ = false>
+// WHB_WF_PAIRWAIT=1: both stage waits of a row pair first (measured: no gain, 324.1 vs 325.1 Gpts/s
+// on config 2, 303.8 vs 302.5 on config 5)
+#ifndef WHB_WF_PAIRWAIT
+#define WHB_WF_PAIRWAIT 0
+#endif
 #ifndef WHB_WF_MINB
 #define WHB_WF_MINB 3
 #endif
@@ -198,12 +203,11 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, WHB_WF_MINB)
                 return *reinterpret_cast<const double2 *>(m.v + (long long)orow * S0 + col);
             };
             double2 vcur = vload(r0 - T);
-#pragma unroll 2
-            for (int idx = 0; idx < nrows; ++idx) {
+            // one input row of the wavefront (its stage already waited for)
+            auto row_step = [&](const int idx) {
                 const int r = r0 + idx;
                 const int slot = idx % ST;
                 const double2 vnext = vload(r + 1 - T);
-                mbar_wait(full + slot, (idx / ST) & 1);
                 const double *st = smem + (size_t)slot * L::STAGE;
                 // W^s row r into the level-0 queue
                 Q[0][0] = Q[0][1];
@@ -302,7 +306,29 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, WHB_WF_MINB)
                 // the stage of row r-T is no longer needed by this warp
                 __syncwarp();
                 if (idx >= T && lane == 0) mbar_arrive(empty + ((idx - T) % ST));
+            };
+#if WHB_WF_PAIRWAIT
+            // Two rows per iteration with both stage waits first: the waits are spin loops (basic
+            // block boundaries), so this puts both rows' level chains into one block and the
+            // scheduler can overlap row idx+1's lower levels with row idx's upper ones.
+            int idx = 0;
+            for (; idx + 1 < nrows; idx += 2) {
+                mbar_wait(full + (idx % ST), (idx / ST) & 1);
+                mbar_wait(full + ((idx + 1) % ST), ((idx + 1) / ST) & 1);
+                row_step(idx);
+                row_step(idx + 1);
             }
+            if (idx < nrows) {
+                mbar_wait(full + (idx % ST), (idx / ST) & 1);
+                row_step(idx);
+            }
+#else
+#pragma unroll 2
+            for (int idx = 0; idx < nrows; ++idx) {
+                mbar_wait(full + (idx % ST), (idx / ST) & 1);
+                row_step(idx);
+            }
+#endif
             // release the stages still held (rows nrows-T .. nrows-1) so the producer never blocks
             if (lane == 0)
                 for (int idx = max(0, nrows - T); idx < nrows; ++idx) mbar_arrive(empty + (idx % ST));
