@@ -263,6 +263,25 @@ int whb_set_l2_flush(whb_ctx *ctx, int64_t bytes);
 /* Pinned host buffers for H2D/D2H at full PCIe rate. */
 int whb_host_alloc(void **ptr, int64_t bytes);
 int whb_host_free(void *ptr);
+/* Peer-memory halo exchange between slab ranks (slab.PeerHalo; SURVEY §8(e) "P2P over
+ * NVLink" alternative to NCCL send/recv; no reference counterpart — the reference is
+ * single-process).  whb_ipc_handle: CUDA IPC handle (64 bytes) of the allocation holding
+ * dev_ptr and dev_ptr's byte offset in it; whb_ipc_open / whb_ipc_close map / unmap a peer's
+ * allocation in this process.  whb_flags_alloc: `count` zeroed uint32 flags in device memory.
+ * whb_copy_async: stream-ordered copy on the context stream (any two device addresses, e.g.
+ * local boundary planes -> a neighbour's ghost planes over NVLink).  whb_stream_write_u32 /
+ * whb_stream_wait_u32: stream memory operations (write after the stream's earlier work, with
+ * a fence; wait until (int32)(*flag - value) >= 0) — the ranks' flags order the exchange
+ * without host round trips and without any kernel spinning on the device. */
+int whb_ipc_handle(whb_ctx *ctx, uint64_t dev_ptr, void *handle_out, int64_t *offset_out);
+int whb_ipc_open(whb_ctx *ctx, const void *handle, uint64_t *base_out);
+int whb_ipc_close(whb_ctx *ctx, uint64_t base);
+int whb_flags_alloc(whb_ctx *ctx, int count, uint64_t *dev_ptr);
+int whb_flags_free(whb_ctx *ctx, uint64_t dev_ptr);
+int whb_copy_async(whb_ctx *ctx, uint64_t src_ptr, uint64_t dst_ptr, int64_t bytes);
+int whb_stream_write_u32(whb_ctx *ctx, uint64_t dev_ptr, uint32_t value);
+int whb_stream_wait_u32(whb_ctx *ctx, uint64_t dev_ptr, uint32_t value);
+
 /* Launch plan: kernel 0 = simple LDG, 1 = bulk-copy rows (2D/batched), 2 = TMA tensor
  * boxes (3D), 3 = general operator, 4 = cluster-resident small 2D grid (the whole solve,
  * and a whole fixed-point loop, in one launch from shared memory); steps_per_pass = leapfrog

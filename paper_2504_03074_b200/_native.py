@@ -26,7 +26,8 @@ E_ARG, E_CUDA, E_NOMEM, E_STATE, E_NODEV = -1, -2, -3, -4, -5
 EXPORTS = (
     "whb_abi_version", "whb_last_error", "whb_device_count", "whb_create", "whb_destroy",
     "whb_set_operator", "whb_set_schedule", "whb_upload", "whb_download", "whb_zero",
-    "whb_filtered_solve", "whb_fpi", "whb_fpi_scaled", "whb_iterate_host", "whb_vec_reserve", "whb_vec_upload",
+    "whb_filtered_solve", "whb_fpi", "whb_fpi_scaled", "whb_ipc_handle", "whb_ipc_open", "whb_ipc_close",
+    "whb_flags_alloc", "whb_flags_free", "whb_copy_async", "whb_stream_write_u32", "whb_stream_wait_u32", "whb_iterate_host", "whb_vec_reserve", "whb_vec_upload",
     "whb_vec_download", "whb_vec_dot", "whb_vec_axpy", "whb_vec_scale_into", "whb_vec_div_into",
     "whb_vec_lincomb", "whb_vec_sub_into", "whb_vec_copy", "whb_matvec", "whb_solve_begin",
     "whb_step", "whb_solve_end", "whb_level_plane_ptr", "whb_stream_ptr", "whb_synchronize",
@@ -70,6 +71,14 @@ def load():
         "whb_filtered_solve": ([vp, c_int, c_int, dp], c_int),
         "whb_fpi": ([vp, c_int, c_double, dp, ctypes.POINTER(c_int)], c_int),
         "whb_fpi_scaled": ([vp, c_int, c_double, c_double, dp, ctypes.POINTER(c_int)], c_int),
+        "whb_ipc_handle": ([vp, c_u64, ctypes.c_char_p, ip64], c_int),
+        "whb_ipc_open": ([vp, ctypes.c_char_p, ctypes.POINTER(c_u64)], c_int),
+        "whb_ipc_close": ([vp, c_u64], c_int),
+        "whb_flags_alloc": ([vp, c_int, ctypes.POINTER(c_u64)], c_int),
+        "whb_flags_free": ([vp, c_u64], c_int),
+        "whb_copy_async": ([vp, c_u64, c_u64, c_i64], c_int),
+        "whb_stream_write_u32": ([vp, c_u64, ctypes.c_uint32], c_int),
+        "whb_stream_wait_u32": ([vp, c_u64, ctypes.c_uint32], c_int),
         "whb_iterate_host": ([vp, dp, dp, dp], c_int),
         "whb_vec_reserve": ([vp, c_int, ctypes.POINTER(c_int)], c_int),
         "whb_vec_upload": ([vp, c_int, dp], c_int),
@@ -401,6 +410,40 @@ class Context:
         check(load().whb_level_plane_ptr(self._h, int(level), int(plane), ctypes.byref(p), ctypes.byref(n)),
               "whb_level_plane_ptr")
         return p.value, n.value
+
+    # -- peer-memory halo exchange (slab.PeerHalo) ------------------------------------------
+    def ipc_handle(self, dev_ptr: int):
+        """(64-byte IPC handle of the allocation holding dev_ptr, byte offset of dev_ptr in it)"""
+        buf = ctypes.create_string_buffer(64)
+        off = ctypes.c_int64(0)
+        check(load().whb_ipc_handle(self._h, int(dev_ptr), buf, ctypes.byref(off)), "whb_ipc_handle")
+        return buf.raw, off.value
+
+    def ipc_open(self, handle: bytes) -> int:
+        p = ctypes.c_uint64(0)
+        check(load().whb_ipc_open(self._h, ctypes.create_string_buffer(bytes(handle), 64), ctypes.byref(p)),
+              "whb_ipc_open")
+        return p.value
+
+    def ipc_close(self, base: int):
+        check(load().whb_ipc_close(self._h, int(base)), "whb_ipc_close")
+
+    def flags_alloc(self, count: int) -> int:
+        p = ctypes.c_uint64(0)
+        check(load().whb_flags_alloc(self._h, int(count), ctypes.byref(p)), "whb_flags_alloc")
+        return p.value
+
+    def flags_free(self, ptr: int):
+        check(load().whb_flags_free(self._h, int(ptr)), "whb_flags_free")
+
+    def copy_async(self, src_ptr: int, dst_ptr: int, nbytes: int):
+        check(load().whb_copy_async(self._h, int(src_ptr), int(dst_ptr), int(nbytes)), "whb_copy_async")
+
+    def stream_write_u32(self, ptr: int, value: int):
+        check(load().whb_stream_write_u32(self._h, int(ptr), int(value) & 0xFFFFFFFF), "whb_stream_write_u32")
+
+    def stream_wait_u32(self, ptr: int, value: int):
+        check(load().whb_stream_wait_u32(self._h, int(ptr), int(value) & 0xFFFFFFFF), "whb_stream_wait_u32")
 
     def stream_ptr(self) -> int:
         p = ctypes.c_uint64(0)

@@ -2827,6 +2827,111 @@ int whb_copy_device(whb_ctx *src, uint64_t src_ptr, whb_ctx *dst, uint64_t dst_p
     return 0;
 }
 
+// ---- peer-memory halo exchange (slab.PeerHalo): CUDA IPC mappings, copies and stream flags ----
+
+namespace {
+PFN_cuStreamWriteValue32_v11070 g_write32 = nullptr;
+PFN_cuStreamWaitValue32_v11070 g_wait32 = nullptr;
+PFN_cuMemGetAddressRange_v3020 g_addr_range = nullptr;
+
+int get_memops() {
+    if (g_write32 && g_wait32 && g_addr_range) return 0;
+    cudaDriverEntryPointQueryResult q;
+    void *fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+        return fail(WHB_E_CUDA, "cuStreamWriteValue32 entry point unavailable");
+    g_write32 = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(fn);
+    fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+        return fail(WHB_E_CUDA, "cuStreamWaitValue32 entry point unavailable");
+    g_wait32 = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(fn);
+    fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+        return fail(WHB_E_CUDA, "cuMemGetAddressRange entry point unavailable");
+    g_addr_range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
+    return 0;
+}
+}  // namespace
+
+int whb_ipc_handle(whb_ctx *c, uint64_t dev_ptr, void *handle_out, int64_t *offset_out) {
+    if (!c || !dev_ptr || !handle_out || !offset_out) return fail(WHB_E_ARG, "NULL argument");
+    WHB_TRY(set_dev(c));
+    WHB_TRY(get_memops());
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (g_addr_range(&base, &size, (CUdeviceptr)dev_ptr) != CUDA_SUCCESS)
+        return fail(WHB_E_ARG, "pointer is not inside a device allocation");
+    cudaIpcMemHandle_t h;
+    WHB_CUDA(cudaIpcGetMemHandle(&h, (void *)(uintptr_t)base));
+    memcpy(handle_out, &h, sizeof(h));
+    *offset_out = (int64_t)(dev_ptr - (uint64_t)base);
+    return 0;
+}
+
+int whb_ipc_open(whb_ctx *c, const void *handle, uint64_t *base_out) {
+    if (!c || !handle || !base_out) return fail(WHB_E_ARG, "NULL argument");
+    WHB_TRY(set_dev(c));
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    void *p = nullptr;
+    WHB_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    *base_out = (uint64_t)(uintptr_t)p;
+    return 0;
+}
+
+int whb_ipc_close(whb_ctx *c, uint64_t base) {
+    if (!c || !base) return fail(WHB_E_ARG, "NULL argument");
+    WHB_TRY(set_dev(c));
+    WHB_CUDA(cudaIpcCloseMemHandle((void *)(uintptr_t)base));
+    return 0;
+}
+
+int whb_flags_alloc(whb_ctx *c, int count, uint64_t *dev_ptr) {
+    if (!c || count <= 0 || !dev_ptr) return fail(WHB_E_ARG, "bad argument");
+    WHB_TRY(set_dev(c));
+    void *p = nullptr;
+    WHB_CUDA(cudaMalloc(&p, (size_t)count * sizeof(uint32_t)));
+    WHB_CUDA(cudaMemset(p, 0, (size_t)count * sizeof(uint32_t)));
+    *dev_ptr = (uint64_t)(uintptr_t)p;
+    return 0;
+}
+
+int whb_flags_free(whb_ctx *c, uint64_t dev_ptr) {
+    if (!c) return fail(WHB_E_ARG, "NULL argument");
+    WHB_TRY(set_dev(c));
+    if (dev_ptr) WHB_CUDA(cudaFree((void *)(uintptr_t)dev_ptr));
+    return 0;
+}
+
+int whb_copy_async(whb_ctx *c, uint64_t src_ptr, uint64_t dst_ptr, int64_t bytes) {
+    if (!c || !src_ptr || !dst_ptr) return fail(WHB_E_ARG, "NULL argument");
+    if (bytes <= 0) return 0;
+    WHB_TRY(set_dev(c));
+    WHB_CUDA(cudaMemcpyAsync((void *)(uintptr_t)dst_ptr, (const void *)(uintptr_t)src_ptr, (size_t)bytes,
+                             cudaMemcpyDefault, c->stream));
+    return 0;
+}
+
+int whb_stream_write_u32(whb_ctx *c, uint64_t dev_ptr, uint32_t value) {
+    if (!c || !dev_ptr) return fail(WHB_E_ARG, "NULL argument");
+    WHB_TRY(set_dev(c));
+    WHB_TRY(get_memops());
+    // default flags: the write is preceded by a memory fence (earlier copies on the stream are visible first)
+    if (g_write32((CUstream)c->stream, (CUdeviceptr)dev_ptr, value, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+        return fail(WHB_E_CUDA, "cuStreamWriteValue32 failed");
+    return 0;
+}
+
+int whb_stream_wait_u32(whb_ctx *c, uint64_t dev_ptr, uint32_t value) {
+    if (!c || !dev_ptr) return fail(WHB_E_ARG, "NULL argument");
+    WHB_TRY(set_dev(c));
+    WHB_TRY(get_memops());
+    // (int32_t)(*addr - value) >= 0: wrap-safe monotone counters
+    if (g_wait32((CUstream)c->stream, (CUdeviceptr)dev_ptr, value, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+        return fail(WHB_E_CUDA, "cuStreamWaitValue32 failed");
+    return 0;
+}
+
 int whb_copy_plane(whb_ctx *src, int src_level, int64_t src_plane, whb_ctx *dst, int dst_level, int64_t dst_plane) {
     if (!src || !dst) return fail(WHB_E_ARG, "NULL argument");
     if (src->S0 != dst->S0) return fail(WHB_E_ARG, "plane geometry mismatch");

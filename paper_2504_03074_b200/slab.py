@@ -39,7 +39,7 @@ from .filters import mode_name
 from .grid import operator_coefficients
 from .timestep import time_schedule
 
-__all__ = ["slab_ranges", "DeviceShard", "TorchHalo", "LocalHalo", "SlabFPI", "SlabKrylov", "ShardedVectors",
+__all__ = ["slab_ranges", "DeviceShard", "TorchHalo", "LocalHalo", "PeerHalo", "run_peer_local_solve", "SlabFPI", "SlabKrylov", "ShardedVectors",
            "run_filtered_solve", "run_local_solve", "halo_items", "exchange_forcing"]
 
 
@@ -219,6 +219,193 @@ class LocalHalo:
                 hi.ctx.copy_device_to(hi.plane_ptr(item, hi_send)[0], lo.ctx, lo.plane_ptr(item, lo_recv)[0], nbytes)
 
 
+_PEER_LEVELS = 9  # levels 0..8 cover V and every ring slot (nring <= 6)
+
+
+def _buffer_table(shard):
+    """Plane-0 device address of every buffer a halo item can name: level L (0..8) and field F."""
+    tab = {level(L): shard.plane_ptr(level(L), 0)[0] for L in range(_PEER_LEVELS)}
+    tab[field(_native.F)] = shard.plane_ptr(field(_native.F), 0)[0]
+    return tab
+
+
+def _ring_size(tab):
+    """Time-level ring length of a shard from its buffer table (level L >= 1 lives in slot L mod n)."""
+    for n in range(1, _PEER_LEVELS - 1):
+        if tab[level(1 + n)] == tab[level(1)]:
+            return n
+    raise RuntimeError("time-level ring longer than the buffer table")
+
+
+def _canon(item, nring):
+    kind, ident = item
+    if kind != "level" or ident == 0:
+        return item
+    return level((ident - 1) % nring + 1)
+
+
+class PeerHalo:
+    """Halo exchange through peer memory: after the boundary planes are computed, this rank copies
+    them straight into its neighbours' ghost planes (NVLink copy engines on the context stream;
+    the neighbours' buffers are mapped with CUDA IPC across processes, or used directly when the
+    slabs share a process), then bumps a flag in each neighbour's memory with a stream write; a
+    rank waits for its own flags with a stream wait before the pass that reads the ghosts.  No
+    NCCL on the data path, no host round trip per pass, no kernel spinning on the device.
+
+    Ordering: ``start`` after region 1 of pass s (copy levels s+2, s+1; flag := seq), ``finish``
+    after region 2 (wait until my flags >= seq).  A rank enters ``start`` of exchange e only after
+    its ``finish`` of exchange e-1, i.e. after each neighbour completed region 1 of the pass that
+    produced e-1, hence the whole pass before it — the last pass that read the ghost planes being
+    overwritten (region 2 never reads ghosts).  Every rank runs the same exchange sequence, so
+    the sequence numbers agree.
+
+    Flags: flags[0] is written by the lower neighbour (rank - 1), flags[1] by the upper one."""
+
+    def __init__(self, shard, rank: int, world: int, nlocs, peers, dist=None, opened=None):
+        self.shard, self.rank, self.world = shard, rank, world
+        self.nlocs = list(nlocs)
+        self.peers = peers          # {neighbour rank: {"buf": {item: base}, "flags": ptr, "plane_bytes": b}}
+        self.dist = dist
+        self.opened = opened or []  # IPC mappings to close
+        self.seq = 0
+        self.nring = _ring_size(_buffer_table(shard))
+
+    @property
+    def nranks(self):
+        return self.world
+
+    # -- construction ----------------------------------------------------------------------
+    @staticmethod
+    def local_group(shards):
+        """PeerHalos for slabs that all live in this process (direct device addresses)."""
+        flags = [sh.ctx.flags_alloc(2) for sh in shards]
+        tabs = [_buffer_table(sh) for sh in shards]
+        pb = [sh.plane_ptr(level(0), 0)[1] * 8 for sh in shards]
+        nlocs = [sh.nloc for sh in shards]
+        out = []
+        for r, sh in enumerate(shards):
+            peers = {q: {"buf": tabs[q], "flags": flags[q], "plane_bytes": pb[q]}
+                     for q in (r - 1, r + 1) if 0 <= q < len(shards)}
+            h = PeerHalo(sh, r, len(shards), nlocs, peers)
+            h.flags = flags[r]
+            out.append(h)
+        return out
+
+    @staticmethod
+    def from_dist(shard, dist, rank: int, world: int):
+        """One PeerHalo per rank: IPC handles of the halo buffers and flags are all-gathered and
+        the neighbours' allocations mapped into this process."""
+        flags = shard.ctx.flags_alloc(2)
+        mine = {"buf": {k: shard.ctx.ipc_handle(p) for k, p in _buffer_table(shard).items()},
+                "flags": shard.ctx.ipc_handle(flags), "plane_bytes": shard.plane_ptr(level(0), 0)[1] * 8,
+                "nloc": shard.nloc}
+        allv = [None] * world
+        dist.all_gather_object(allv, mine)
+        bases, peers, opened = {}, {}, []
+
+        def mapped(h_off):
+            h, off = h_off
+            if h not in bases:
+                bases[h] = shard.ctx.ipc_open(h)
+                opened.append(bases[h])
+            return bases[h] + off
+
+        for q in (rank - 1, rank + 1):
+            if 0 <= q < world:
+                peers[q] = {"buf": {k: mapped(v) for k, v in allv[q]["buf"].items()},
+                            "flags": mapped(allv[q]["flags"]), "plane_bytes": allv[q]["plane_bytes"]}
+        h = PeerHalo(shard, rank, world, [a["nloc"] for a in allv], peers, dist=dist, opened=opened)
+        h.flags = flags
+        return h
+
+    def close(self):
+        for b in self.opened:
+            self.shard.ctx.ipc_close(b)
+        self.opened = []
+        if getattr(self, "flags", 0):
+            self.shard.ctx.flags_free(self.flags)
+            self.flags = 0
+
+    # -- exchange --------------------------------------------------------------------------
+    def _recv_plane(self, q, side_of_q, depth):
+        """First ghost plane of neighbour q on its side `side_of_q` (its geometry: gh, nloc_q)."""
+        g, n = self.shard.gh, self.nlocs[q]
+        return g - depth if side_of_q == "lo" else g + n
+
+    def start(self, shard, items):
+        ctx = shard.ctx
+        for item, depth in items:
+            for q, my_side, q_side in ((self.rank - 1, "lo", "hi"), (self.rank + 1, "hi", "lo")):
+                if q not in self.peers:
+                    continue
+                snd, _ = halo_planes(shard, my_side, depth)
+                pq = self.peers[q]
+                dst = pq["buf"][_canon(item, self.nring)] + self._recv_plane(q, q_side, depth) * pq["plane_bytes"]
+                ctx.copy_async(shard.plane_ptr(item, snd)[0], dst, depth * pq["plane_bytes"])
+        self.seq += 1
+        for q, slot in ((self.rank - 1, 1), (self.rank + 1, 0)):  # I am q's upper / lower neighbour
+            if q in self.peers:
+                ctx.stream_write_u32(self.peers[q]["flags"] + 4 * slot, self.seq)
+        return self.seq
+
+    def finish(self, seq):
+        for q, slot in ((self.rank - 1, 0), (self.rank + 1, 1)):
+            if q in self.peers:
+                self.shard.ctx.stream_wait_u32(self.flags + 4 * slot, seq)
+
+    def allreduce_sum(self, x: float, shard) -> float:
+        import torch
+
+        dev = "cpu" if self.dist.get_backend() == "gloo" else f"cuda:{shard.device}"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        self.dist.all_reduce(t)
+        return float(t.item())
+
+
+def run_peer_local_solve(shards, halos, out_mode=_native.OUT_FPI, zero_forcing=False):
+    """``run_filtered_solve``'s schedule for slabs of this process that exchange through
+    ``PeerHalo.local_group`` (each op issued for every slab in turn, so the stream waits of one
+    slab always follow the neighbour's enqueued flag writes).  Returns the residual sums."""
+    for sh in shards:
+        sh.solve_begin(out_mode, zero_forcing)
+    n_total = shards[0].n_total
+    two = all(sh.steps_per_pass == 2 for sh in shards)
+
+    def exchange_both(items, between=None):
+        hs = [h.start(sh, items) for sh, h in zip(shards, halos)]
+        if between:
+            between()
+        for h, q in zip(halos, hs):
+            h.finish(q)
+
+    if two:
+        exchange_both([(level(0), 2)])
+        s = 0
+        while s + 1 < n_total:
+            if s + 2 == n_total:
+                for sh in shards:
+                    sh.pair(s, 0)
+            else:
+                for sh in shards:
+                    sh.pair(s, 1)
+                exchange_both(halo_items(s, True), lambda: [sh.pair(s, 2) for sh in shards])
+            s += 2
+        if s < n_total:
+            for sh in shards:
+                sh.step(s, 0)
+        return [sh.solve_end() for sh in shards]
+    exchange_both([(level(0), 1)])
+    for s in range(n_total):
+        if s == n_total - 1:
+            for sh in shards:
+                sh.step(s, 0)
+            continue
+        for sh in shards:
+            sh.step(s, 1)
+        exchange_both(halo_items(s, False), lambda: [sh.step(s, 2) for sh in shards])
+    return [sh.solve_end() for sh in shards]
+
+
 def _exchange_now(halo, shard, items):
     if halo.nranks > 1:
         halo.finish(halo.start(shard, items))
@@ -300,6 +487,10 @@ def exchange_forcing(shards_or_shard, halo):
     """f is read one plane beyond the owned range by the two-step pass: exchange it once."""
     if isinstance(halo, LocalHalo):
         halo.exchange([(field(_native.F), 1)])
+    elif isinstance(halo, (list, tuple)):  # PeerHalo.local_group
+        hs = [h.start(sh, [(field(_native.F), 1)]) for sh, h in zip(shards_or_shard, halo)]
+        for h, q in zip(halo, hs):
+            h.finish(q)
     else:
         _exchange_now(halo, shards_or_shard, [(field(_native.F), 1)])
 

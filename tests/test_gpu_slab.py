@@ -99,3 +99,99 @@ def test_slab_krylov_local_matches_single_domain(gpu_available, cells, nslabs, o
     assert np.max(np.abs(x - xw.values)) <= 1e-9 * np.max(np.abs(xw.values))
     for sh in shards:
         sh.ctx.close()
+
+
+@pytest.mark.parametrize("two_step", [True, False])
+@pytest.mark.parametrize("cells,nslabs,omega", [((69, 49), 4, 15.0), ((32, 19, 23), 3, 9.0), ((8, 12, 10), 4, 5.0),
+                                                ((64, 64, 64), 2, 20.0)])
+def test_peer_halo_slabs_match_single_domain_bitwise(gpu_available, monkeypatch, cells, nslabs, omega, two_step):
+    """The peer-memory exchange (slab.PeerHalo): boundary planes copied straight into the
+    neighbours' ghost planes on each slab's own stream, ordered by stream flag writes / waits
+    between the slabs' streams (no host synchronisation inside a solve)."""
+    from paper_2504_03074_b200.slab import PeerHalo, run_peer_local_solve
+
+    if not two_step:
+        monkeypatch.setenv("WHB_TB2", "0")
+    d = len(cells)
+    g = wh.build_grid(d, [(0.0, 1.0)] * d, cells, "dirichlet")
+    f = O.multi_gaussian(g.shape, g.bounds, g.spacing, 3, seed=2)
+    corr = wh.correct_explicit(omega, g, 2, 1.0)
+    cfg = wh.FilterConfig(omega=omega, periods=1, steps_per_period=corr.steps_per_period, mode="explicit")
+    ranges = slab_ranges(g.shape[0], nslabs)
+    shards = [DeviceShard(g, r) for r in ranges]
+    for sh, (p0, p1) in zip(shards, ranges):
+        sh.set_schedule(wh.time_schedule(corr, cfg))
+        sh.upload(_native.F, np.ascontiguousarray(f[p0:p1]))
+        sh.zero(_native.V)
+    halos = PeerHalo.local_group(shards)
+    exchange_forcing(shards, halos)
+    iters = 3
+    sums = [sum(run_peer_local_solve(shards, halos)) for _ in range(iters)]
+    v = np.concatenate([sh.download(_native.V) for sh in shards], axis=0)
+    sc = O.step_scalars(corr.steps_per_period, corr.dt, corr.omega_tilde)
+    vref, rref = ON.fpi(f, g.spacing, sc, iters)
+    assert np.array_equal(v, vref), (corr.steps_per_period, two_step)
+    np.testing.assert_allclose(np.sqrt(sums) / np.sqrt(g.size), rref, rtol=1e-12)
+    for h in halos:
+        h.close()
+
+
+def _ipc_worker(rank, port, q):
+    """Two processes on one GPU: each maps the other's level buffer and flags through CUDA IPC
+    (PeerHalo.from_dist), copies its boundary plane into the other's ghost plane and bumps the
+    other's flag with a stream write; the host (gloo barrier), not the device, waits."""
+    import os
+
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        from paper_2504_03074_b200.slab import PeerHalo, level
+
+        g = wh.build_grid(2, [(0.0, 1.0)] * 2, [20, 16], "dirichlet")
+        sh = DeviceShard(g, slab_ranges(g.shape[0], 2)[rank])
+        vals = np.full((sh.nloc, g.shape[1]), float(rank + 1))
+        sh.upload(_native.V, vals)
+        h = PeerHalo.from_dist(sh, dist, rank, 2)
+        seq = h.start(sh, [(level(0), 1)])
+        sh.synchronize()
+        dist.barrier()
+        import torch
+
+        from paper_2504_03074_b200.slab import _CudaArray
+
+        ghost_ptr, n = sh.plane_ptr(level(0), sh.gh - 1 if rank == 1 else sh.gh + sh.nloc)
+        got = torch.as_tensor(_CudaArray(ghost_ptr, n), device="cuda").cpu().numpy()
+        # the two uint32 flags, read through a one-element float64 view
+        raw = torch.as_tensor(_CudaArray(h.flags, 1), device="cuda").cpu().numpy().view(np.uint32)
+        dist.barrier()
+        h.close()
+        q.put((rank, seq, got.tolist(), raw.tolist(), None))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_halo_ipc_two_processes(gpu_available):
+    import multiprocessing as mp
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = sorted([q.get(timeout=300) for _ in range(2)])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, seq, ghost, flags, _ in got:
+        other = 2 - rank  # the neighbour's value (rank 0 holds 1.0, rank 1 holds 2.0)
+        g = np.array(ghost)
+        # interior columns of the received plane carry the neighbour's value (boundary columns 0)
+        assert np.all(g[1:16] == float(other)), (rank, g[:20])
+        slot = 1 if rank == 0 else 0  # rank 0 hears from its upper neighbour, rank 1 from its lower one
+        assert flags[slot] == seq == 1 and flags[1 - slot] == 0
