@@ -358,12 +358,13 @@ def run_slab(args, dist, ws, rank, local):
     import torch
 
     from paper_2504_03074_b200 import _native
-    from paper_2504_03074_b200.slab import DeviceShard, SlabFPI, TorchHalo, slab_ranges
+    from paper_2504_03074_b200.slab import DeviceShard, PeerHalo, SlabFPI, TorchHalo, slab_ranges
 
     g, f, corr, cfg, _ = build_workload(args.workload)
     rng = slab_ranges(g.shape[0], ws)[rank]
     shard = DeviceShard(g, rng, device=local)
-    solver = SlabFPI(shard, TorchHalo(dist, rank, ws), corr, cfg, f)
+    halo = PeerHalo.from_dist(shard, dist, rank, ws) if args.halo == "peer" else TorchHalo(dist, rank, ws)
+    solver = SlabFPI(shard, halo, corr, cfg, f)
     n_t = solver.shard.n_total
     K, W = args.steps, args.warmup
     for _ in range(W):
@@ -407,7 +408,9 @@ def run_slab(args, dist, ws, rank, local):
             "dtype": "f64", "data": "synthetic (BASELINE forcing recipe, SURVEY 8(d))",
             "config": {"workload": args.workload, "grid": list(g.shape), "omega": cfg.omega, "N_t": n_t,
                        "iterations": K, "cfl": 0.9, "forcing": forcing_desc(args.workload),
-                       "parallelism": f"z-slab decomposition over {ws} GPUs, NCCL halo exchange",
+                       "parallelism": f"z-slab decomposition over {ws} GPUs, " + (
+                           "peer-memory halo exchange (CUDA IPC copies + stream flags)" if args.halo == "peer"
+                           else "NCCL halo exchange"),
                        "l2": "working set far above L2"},
             "iters_per_s": K / dev_s,
             "roofline": {"bound": "hbm", "achieved": BYTES_PER_UPDATE * units / ws / dev_s / 1e9, "peak": peak,
@@ -799,6 +802,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--decomp", default="slab", choices=["slab", "replicas"],
                     help="N > 1 on configs 3/4: z-slab decomposition (default) or independent replicas")
+    ap.add_argument("--halo", choices=["nccl", "peer"], default="nccl",
+                    help="z-slab halo exchange at N > 1: NCCL send/recv (default) or peer memory "
+                         "(CUDA IPC mappings of the neighbours' ghost planes, stream flags)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

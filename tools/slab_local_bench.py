@@ -27,6 +27,9 @@ def main():
     ap.add_argument("--slabs", type=int, nargs="+", default=[1, 2])
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--no-whole", action="store_true")
+    ap.add_argument("--halo", choices=["local", "peer"], default="local",
+                    help="local: LocalHalo (event-ordered device copies); peer: PeerHalo.local_group "
+                         "(copies into the neighbours' ghost planes on each slab's stream, stream flags)")
     a = ap.parse_args()
 
     import torch
@@ -67,19 +70,26 @@ def main():
             sh.set_schedule(sched)
             sh.upload(_native.F, np.ascontiguousarray(fv[p0:p1]))
             sh.zero(_native.V)
-        halo = LocalHalo(shards)
+        if a.halo == "peer":
+            from paper_2504_03074_b200.slab import PeerHalo, run_peer_local_solve
+
+            halo = PeerHalo.local_group(shards)
+            solve = lambda: run_peer_local_solve(shards, halo)  # noqa: E731
+        else:
+            halo = LocalHalo(shards)
+            solve = lambda: run_local_solve(shards, halo)  # noqa: E731
         exchange_forcing(shards, halo)
-        run_local_solve(shards, halo)  # warm-up pass (also the first FPI iterate)
+        solve()  # warm-up pass (also the first FPI iterate)
         for sh in shards:
             sh.synchronize()
         l0 = sum(sh.ctx.launch_count() for sh in shards)
         t0 = time.perf_counter()
-        sums = [sum(run_local_solve(shards, halo)) for _ in range(a.iters)]
+        sums = [sum(solve()) for _ in range(a.iters)]
         for sh in shards:
             sh.synchronize()
         dt = time.perf_counter() - t0
         launches = sum(sh.ctx.launch_count() for sh in shards) - l0
-        row = {"slabs": k, "two_step": shards[0].steps_per_pass == 2, "gpts": g.size * n_t * a.iters / dt / 1e9,
+        row = {"slabs": k, "halo": a.halo, "two_step": shards[0].steps_per_pass == 2, "gpts": g.size * n_t * a.iters / dt / 1e9,
                "launches_per_iter": launches / a.iters, "resid_sq_last": sums[-1]}
         if not a.no_whole:
             v = np.concatenate([sh.download(_native.V) for sh in shards], axis=0)
