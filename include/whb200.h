@@ -282,6 +282,16 @@ int whb_copy_async(whb_ctx *ctx, uint64_t src_ptr, uint64_t dst_ptr, int64_t byt
 int whb_stream_write_u32(whb_ctx *ctx, uint64_t dev_ptr, uint32_t value);
 int whb_stream_wait_u32(whb_ctx *ctx, uint64_t dev_ptr, uint32_t value);
 
+/* Caller-captured graphs: whb_capture_begin starts stream capture on the context stream
+ * (relaxed mode, so several contexts can capture at once), every later call enqueues into the
+ * capture (whb_solve_end then leaves the residual on the device), whb_capture_end instantiates
+ * it; whb_graph_launch replays it; whb_resid_read copies the last residual sum to the host.
+ * Used for one slab iteration with its peer-memory exchange (slab.PeerSlabGraphs). */
+int whb_capture_begin(whb_ctx *ctx);
+int whb_capture_end(whb_ctx *ctx, int *graph_id);
+int whb_graph_launch(whb_ctx *ctx, int graph_id);
+int whb_resid_read(whb_ctx *ctx, double *resid_sq);
+
 /* Launch plan: kernel 0 = simple LDG, 1 = bulk-copy rows (2D/batched), 2 = TMA tensor
  * boxes (3D), 3 = general operator, 4 = cluster-resident small 2D grid (the whole solve,
  * and a whole fixed-point loop, in one launch from shared memory); steps_per_pass = leapfrog

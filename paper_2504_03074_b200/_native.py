@@ -27,7 +27,8 @@ EXPORTS = (
     "whb_abi_version", "whb_last_error", "whb_device_count", "whb_create", "whb_destroy",
     "whb_set_operator", "whb_set_schedule", "whb_upload", "whb_download", "whb_zero",
     "whb_filtered_solve", "whb_fpi", "whb_fpi_scaled", "whb_ipc_handle", "whb_ipc_open", "whb_ipc_close",
-    "whb_flags_alloc", "whb_flags_free", "whb_copy_async", "whb_stream_write_u32", "whb_stream_wait_u32", "whb_iterate_host", "whb_vec_reserve", "whb_vec_upload",
+    "whb_flags_alloc", "whb_flags_free", "whb_copy_async", "whb_stream_write_u32", "whb_stream_wait_u32",
+    "whb_capture_begin", "whb_capture_end", "whb_graph_launch", "whb_resid_read", "whb_iterate_host", "whb_vec_reserve", "whb_vec_upload",
     "whb_vec_download", "whb_vec_dot", "whb_vec_axpy", "whb_vec_scale_into", "whb_vec_div_into",
     "whb_vec_lincomb", "whb_vec_sub_into", "whb_vec_copy", "whb_matvec", "whb_solve_begin",
     "whb_step", "whb_solve_end", "whb_level_plane_ptr", "whb_stream_ptr", "whb_synchronize",
@@ -77,6 +78,10 @@ def load():
         "whb_flags_alloc": ([vp, c_int, ctypes.POINTER(c_u64)], c_int),
         "whb_flags_free": ([vp, c_u64], c_int),
         "whb_copy_async": ([vp, c_u64, c_u64, c_i64], c_int),
+        "whb_capture_begin": ([vp], c_int),
+        "whb_capture_end": ([vp, ctypes.POINTER(c_int)], c_int),
+        "whb_graph_launch": ([vp, c_int], c_int),
+        "whb_resid_read": ([vp, dp], c_int),
         "whb_stream_write_u32": ([vp, c_u64, ctypes.c_uint32], c_int),
         "whb_stream_wait_u32": ([vp, c_u64, ctypes.c_uint32], c_int),
         "whb_iterate_host": ([vp, dp, dp, dp], c_int),
@@ -435,6 +440,22 @@ class Context:
 
     def flags_free(self, ptr: int):
         check(load().whb_flags_free(self._h, int(ptr)), "whb_flags_free")
+
+    def capture_begin(self):
+        check(load().whb_capture_begin(self._h), "whb_capture_begin")
+
+    def capture_end(self) -> int:
+        g = ctypes.c_int(-1)
+        check(load().whb_capture_end(self._h, ctypes.byref(g)), "whb_capture_end")
+        return g.value
+
+    def graph_launch(self, graph_id: int):
+        check(load().whb_graph_launch(self._h, int(graph_id)), "whb_graph_launch")
+
+    def resid_read(self) -> float:
+        r = ctypes.c_double(0.0)
+        check(load().whb_resid_read(self._h, ctypes.byref(r)), "whb_resid_read")
+        return r.value
 
     def copy_async(self, src_ptr: int, dst_ptr: int, nbytes: int):
         check(load().whb_copy_async(self._h, int(src_ptr), int(dst_ptr), int(nbytes)), "whb_copy_async")

@@ -697,6 +697,9 @@ struct whb_ctx {
     TriData *tri = nullptr;
     double *d_cg = nullptr;          // device CG scalars (imp::CG_*)
     std::map<std::tuple<int, int, int, int, int, int, int, double>, cudaGraphExec_t> cg_graphs;
+    // caller-captured graphs (whb_capture_begin/end): e.g. one slab iteration with its peer exchange
+    bool capturing = false;
+    std::vector<cudaGraphExec_t> user_graphs;
 };
 
 namespace {
@@ -1254,6 +1257,7 @@ int ensure_hist(whb_ctx *c, int iters) {
     c->hist_cap = cap;
     // graphs bake the hist pointer
     for (auto &kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    for (auto &ge : c->user_graphs) cudaGraphExecDestroy(ge);
     c->graphs.clear();
     return 0;
 }
@@ -2775,10 +2779,57 @@ int whb_solve_end(whb_ctx *c, double *resid_sq) {
         reduce_partials_kernel<<<1, 1024, 0, c->stream>>>(c->d_members, 1, c->cur_parts, c->d_hist, c->d_counter);
         c->launches++;
         WHB_CUDA(cudaGetLastError());
+        if (c->capturing) {  // the residual stays on the device (whb_resid_read after the replay)
+            c->cur_mode = -1;
+            if (resid_sq) *resid_sq = 0.0;
+            return 0;
+        }
         if (resid_sq) WHB_CUDA(cudaMemcpyAsync(resid_sq, c->d_hist, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    }
+    if (c->capturing) {
+        c->cur_mode = -1;
+        return 0;
     }
     WHB_CUDA(cudaStreamSynchronize(c->stream));
     c->cur_mode = -1;
+    return 0;
+}
+
+int whb_capture_begin(whb_ctx *c) {
+    if (!c || c->capturing) return fail(WHB_E_STATE, "capture already active");
+    WHB_TRY(set_dev(c));
+    WHB_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
+    c->capturing = true;
+    return 0;
+}
+
+int whb_capture_end(whb_ctx *c, int *graph_id) {
+    if (!c || !c->capturing || !graph_id) return fail(WHB_E_STATE, "no capture active");
+    WHB_TRY(set_dev(c));
+    c->capturing = false;
+    cudaGraph_t g;
+    WHB_CUDA(cudaStreamEndCapture(c->stream, &g));
+    cudaGraphExec_t ge;
+    cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(WHB_E_CUDA, std::string("instantiate: ") + cudaGetErrorString(e));
+    c->user_graphs.push_back(ge);
+    *graph_id = (int)c->user_graphs.size() - 1;
+    return 0;
+}
+
+int whb_graph_launch(whb_ctx *c, int graph_id) {
+    if (!c || graph_id < 0 || graph_id >= (int)c->user_graphs.size()) return fail(WHB_E_ARG, "bad graph id");
+    WHB_TRY(set_dev(c));
+    WHB_CUDA(cudaGraphLaunch(c->user_graphs[graph_id], c->stream));
+    return 0;
+}
+
+int whb_resid_read(whb_ctx *c, double *resid_sq) {
+    if (!c || !resid_sq) return fail(WHB_E_ARG, "NULL argument");
+    WHB_TRY(set_dev(c));
+    WHB_CUDA(cudaMemcpyAsync(resid_sq, c->d_hist, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
     return 0;
 }
 

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--slabs", type=int, nargs="+", default=[1, 2])
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--no-whole", action="store_true")
+    ap.add_argument("--graph", action="store_true", help="with --halo peer: one CUDA graph per slab iteration")
     ap.add_argument("--halo", choices=["local", "peer"], default="local",
                     help="local: LocalHalo (event-ordered device copies); peer: PeerHalo.local_group "
                          "(copies into the neighbours' ghost planes on each slab's stream, stream flags)")
@@ -75,11 +76,20 @@ def main():
 
             halo = PeerHalo.local_group(shards)
             solve = lambda: run_peer_local_solve(shards, halo)  # noqa: E731
+            if a.graph:
+                from paper_2504_03074_b200.slab import PeerSlabGraphs
+
+                exchange_forcing(shards, halo)
+                for h, sh in zip(halo, shards):
+                    h.epoch_end(sh)
+                pg = PeerSlabGraphs(shards, halo)  # warm-up + capture (the warm-up is the first iterate)
+                solve = pg.iterate
         else:
             halo = LocalHalo(shards)
             solve = lambda: run_local_solve(shards, halo)  # noqa: E731
-        exchange_forcing(shards, halo)
-        solve()  # warm-up pass (also the first FPI iterate)
+        if not (a.halo == "peer" and a.graph):
+            exchange_forcing(shards, halo)
+            solve()  # warm-up pass (also the first FPI iterate)
         for sh in shards:
             sh.synchronize()
         l0 = sum(sh.ctx.launch_count() for sh in shards)
@@ -89,7 +99,7 @@ def main():
             sh.synchronize()
         dt = time.perf_counter() - t0
         launches = sum(sh.ctx.launch_count() for sh in shards) - l0
-        row = {"slabs": k, "halo": a.halo, "two_step": shards[0].steps_per_pass == 2, "gpts": g.size * n_t * a.iters / dt / 1e9,
+        row = {"slabs": k, "halo": a.halo + ("+graph" if a.graph else ""), "two_step": shards[0].steps_per_pass == 2, "gpts": g.size * n_t * a.iters / dt / 1e9,
                "launches_per_iter": launches / a.iters, "resid_sq_last": sums[-1]}
         if not a.no_whole:
             v = np.concatenate([sh.download(_native.V) for sh in shards], axis=0)
