@@ -364,7 +364,7 @@ def run_slab(args, dist, ws, rank, local):
     rng = slab_ranges(g.shape[0], ws)[rank]
     shard = DeviceShard(g, rng, device=local)
     halo = PeerHalo.from_dist(shard, dist, rank, ws) if args.halo == "peer" else TorchHalo(dist, rank, ws)
-    solver = SlabFPI(shard, halo, corr, cfg, f)
+    solver = SlabFPI(shard, halo, corr, cfg, f, graph=args.halo == "peer")
     n_t = solver.shard.n_total
     K, W = args.steps, args.warmup
     for _ in range(W):
@@ -409,7 +409,8 @@ def run_slab(args, dist, ws, rank, local):
             "config": {"workload": args.workload, "grid": list(g.shape), "omega": cfg.omega, "N_t": n_t,
                        "iterations": K, "cfl": 0.9, "forcing": forcing_desc(args.workload),
                        "parallelism": f"z-slab decomposition over {ws} GPUs, " + (
-                           "peer-memory halo exchange (CUDA IPC copies + stream flags)" if args.halo == "peer"
+                           "peer-memory halo exchange (CUDA IPC copies + stream flags), one CUDA graph per "
+                           "iteration" if args.halo == "peer"
                            else "NCCL halo exchange"),
                        "l2": "working set far above L2"},
             "iters_per_s": K / dev_s,

@@ -647,7 +647,7 @@ class SlabFPI:
     is either the full field (sliced here) or this rank's owned planes.
     """
 
-    def __init__(self, shard, halo, corr, config, forcing):
+    def __init__(self, shard, halo, corr, config, forcing, graph=False):
         if mode_name(config.mode) != "explicit":
             raise NotImplementedError("only the explicit path runs on the GPU")
         self.shard = shard
@@ -662,6 +662,13 @@ class SlabFPI:
             raise ValueError("every slab needs at least 2 owned planes")
         shard.upload(_native.F, np.ascontiguousarray(fv))
         exchange_forcing(shard, halo)
+        # graph=True (PeerHalo only): after one host-driven iteration, each iteration is one CUDA
+        # graph replay (kernels, peer copies, flag writes / waits) + the residual all-reduce
+        self.graph = bool(graph) and isinstance(halo, PeerHalo)
+        self._gid = None
+        if self.graph:
+            halo.epoch_end(shard)
+            shard.synchronize()
         self.reset()
 
     def reset(self):
@@ -669,8 +676,23 @@ class SlabFPI:
 
     def iterate(self) -> float:
         """One pass; returns the global scaled residual ||v_new - v||_2 / sqrt(N)."""
-        rs = run_filtered_solve(self.shard, self.halo)
+        if self.graph and self._gid is not None:
+            self.shard.ctx.graph_launch(self._gid)
+            rs = self.shard.ctx.resid_read()  # synchronises: the epoch's flag reset has executed
+        else:
+            rs = run_filtered_solve(self.shard, self.halo)
+            if self.graph:
+                self.halo.epoch_end(self.shard)
+                self.shard.synchronize()
         total = self.halo.allreduce_sum(rs, self.shard) if self.halo.nranks > 1 else rs
+        if self.graph and self._gid is None:
+            # capture the next iterations (nothing executes during capture)
+            self.shard.ctx.capture_begin()
+            try:
+                run_filtered_solve(self.shard, self.halo)
+                self.halo.epoch_end(self.shard)
+            finally:
+                self._gid = self.shard.ctx.capture_end()
         return math.sqrt(total) / math.sqrt(self.grid.size)
 
     def local_iterate(self) -> np.ndarray:
