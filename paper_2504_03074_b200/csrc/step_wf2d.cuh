@@ -74,6 +74,10 @@ template <int T, int NW, int ST, int K1, int K2, bool ZF, int SKEW = 1, bool PS 
 #ifndef WHB_WF_PAIRWAIT
 #define WHB_WF_PAIRWAIT 0
 #endif
+// WHB_WF_WARMSKIP=0: compute every level on every input row (the pre-cone rows too)
+#ifndef WHB_WF_WARMSKIP
+#define WHB_WF_WARMSKIP 1
+#endif
 #ifndef WHB_WF_MINB
 #define WHB_WF_MINB 3
 #endif
@@ -204,7 +208,11 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, WHB_WF_MINB)
             };
             double2 vcur = vload(r0 - T);
             // one input row of the wavefront (its stage already waited for)
-            auto row_step = [&](const int idx) {
+            // WARM (input rows idx < 2T): level t at row r - t is only needed (by the outputs
+            // [i0, i1) through the stencil cone) from row i0 - (T - t) on, i.e. for idx >= 2t; the
+            // earlier rows of each level are skipped (left 0) instead of computed.
+            auto row_step = [&](const int idx, auto warm_tag) {
+                constexpr bool WARM = decltype(warm_tag)::value;
                 const int r = r0 + idx;
                 const int slot = idx % ST;
                 const double2 vnext = vload(r + 1 - T);
@@ -217,6 +225,9 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, WHB_WF_MINB)
     #pragma unroll
                 for (int t = 1; t <= T; ++t) {
                     const int row = r - t;  // plane of level t computed now
+                    if (WARM && idx < 2 * t) {  // warp-uniform: row below the cone of the outputs
+                        nw[t] = make_double2(0.0, 0.0);
+                    } else {
                     // stage holding row `row` (rows r-T..r are resident)
                     const double *sr = smem + (size_t)((idx - t + ST) % ST) * L::STAGE;
                     const double2 cm = Q[t - 1][0], cc = Q[t - 1][1], cp = Q[t - 1][2];
@@ -248,6 +259,7 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, WHB_WF_MINB)
                     const bool rin = (row >= g.i_lo) && (row < g.i_hi);
                     if (rin && warp_in) nw[t] = make_double2(a, b);  // uniform: no per-lane selects
                     else nw[t] = make_double2((rin && in0) ? a : 0.0, (rin && in1) ? b : 0.0);
+                    }
                     Q[t][0] = Q[t][1];
                     Q[t][1] = Q[t][2];
                     Q[t][2] = nw[t];
@@ -315,18 +327,24 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, WHB_WF_MINB)
             for (; idx + 1 < nrows; idx += 2) {
                 mbar_wait(full + (idx % ST), (idx / ST) & 1);
                 mbar_wait(full + ((idx + 1) % ST), ((idx + 1) / ST) & 1);
-                row_step(idx);
-                row_step(idx + 1);
+                row_step(idx, std::true_type{});
+                row_step(idx + 1, std::true_type{});
             }
             if (idx < nrows) {
                 mbar_wait(full + (idx % ST), (idx / ST) & 1);
-                row_step(idx);
+                row_step(idx, std::true_type{});
             }
 #else
-#pragma unroll 2
-            for (int idx = 0; idx < nrows; ++idx) {
+            const int nwarm = WHB_WF_WARMSKIP ? min(nrows, 2 * T) : 0;
+            int idx = 0;
+            for (; idx < nwarm; ++idx) {
                 mbar_wait(full + (idx % ST), (idx / ST) & 1);
-                row_step(idx);
+                row_step(idx, std::true_type{});
+            }
+#pragma unroll 2
+            for (; idx < nrows; ++idx) {
+                mbar_wait(full + (idx % ST), (idx / ST) & 1);
+                row_step(idx, std::false_type{});
             }
 #endif
             // release the stages still held (rows nrows-T .. nrows-1) so the producer never blocks

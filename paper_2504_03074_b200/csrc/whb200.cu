@@ -32,6 +32,7 @@
 #include <cstring>
 #include <map>
 #include <string>
+#include <type_traits>
 #include <tuple>
 #include <vector>
 
