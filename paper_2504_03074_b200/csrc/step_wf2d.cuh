@@ -74,6 +74,15 @@ template <int T, int NW, int ST, int K1, int K2, bool ZF, int SKEW = 1, bool PS 
 #ifndef WHB_WF_PAIRWAIT
 #define WHB_WF_PAIRWAIT 0
 #endif
+// steady-state row-loop unroll (measured: 3, the period of the level queues, is within noise
+// of 2 -- 321.4 vs 322.3 Gpts/s on config 2, 302.9 vs 299.9 on config 5; the queue shifts are
+// renames either way)
+#ifndef WHB_WF_UNROLL
+#define WHB_WF_UNROLL 2
+#endif
+#define WF_PRAGMA_(x) _Pragma(#x)
+#define WF_UNROLL_(n) WF_PRAGMA_(unroll n)
+#define WF_UNROLL(n) WF_UNROLL_(n)
 // WHB_WF_WARMSKIP=0: compute every level on every input row (the pre-cone rows too)
 #ifndef WHB_WF_WARMSKIP
 #define WHB_WF_WARMSKIP 1
@@ -341,7 +350,7 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, WHB_WF_MINB)
                 mbar_wait(full + (idx % ST), (idx / ST) & 1);
                 row_step(idx, std::true_type{});
             }
-#pragma unroll 2
+            WF_UNROLL(WHB_WF_UNROLL)
             for (; idx < nrows; ++idx) {
                 mbar_wait(full + (idx % ST), (idx / ST) & 1);
                 row_step(idx, std::false_type{});
