@@ -34,13 +34,18 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// row-segment padding in the stages (elements; bulk copies need 16-B aligned destinations)
+#ifndef WHB_WF_PAD
+#define WHB_WF_PAD 16
+#endif
+
 template <int T, int NW>
 struct Lay {
     static constexpr int OW = 64 - 2 * T;          // output columns per warp
     static constexpr int CW = NW * OW;             // output columns per CTA
     static constexpr int SEG = CW + 2 * T;         // staged columns per row (start at c0 - T)
-    static constexpr int SEGP = (SEG + 15) / 16 * 16;
-    static constexpr int CWP = (CW + 15) / 16 * 16;
+    static constexpr int SEGP = (SEG + WHB_WF_PAD - 1) / WHB_WF_PAD * WHB_WF_PAD;
+    static constexpr int CWP = (CW + WHB_WF_PAD - 1) / WHB_WF_PAD * WHB_WF_PAD;
     static constexpr int STAGE = 3 * SEGP + CWP;   // W^s | W^{s-1} | f | acc
     static constexpr int THREADS = 32 * (NW + 1);
 };
