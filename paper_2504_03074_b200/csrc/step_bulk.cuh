@@ -82,7 +82,9 @@ constexpr size_t bulk_smem_bytes() {
 // SQ: every axis carries the same taps (square / cubic cells, clo_a and cmid_a bitwise equal):
 // the centre product cmid*wc is formed once and added per axis — the same values, in the same
 // order, as the reference's per-axis products.
-template <int KIND, bool ZF, bool A1, bool SQ = false>
+// C2: -1 = multiply by c^2 when g.use_c2 (runtime), 0 = never (c^2 == 1: x * 1.0 == x, so skipping
+// the product is bitwise neutral), 1 = always.
+template <int KIND, bool ZF, bool A1, bool SQ = false, int C2 = -1>
 __device__ __forceinline__ double update_point(const Geom &g, double wm, double wc, double wp, double yl,
                                                double yh, double xl, double xh, double fv, double wpv,
                                                double h, double cosn) {
@@ -113,7 +115,7 @@ __device__ __forceinline__ double update_point(const Geom &g, double wm, double 
         lap = whb_add(lap, whb_mul(g.cmid2, wc));
         lap = whb_add(lap, whb_mul(g.clo2, xh));
     }
-    if (g.use_c2) lap = whb_mul(lap, g.c2);
+    if (C2 < 0 ? g.use_c2 != 0 : C2 != 0) lap = whb_mul(lap, g.c2);
     if (KIND == K_FIRST) {
         const double d = ZF ? lap : whb_sub(lap, fv);
         return whb_add(wc, whb_mul(h, d));

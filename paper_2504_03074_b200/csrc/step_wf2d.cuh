@@ -72,8 +72,10 @@ struct WfScal {
 
 // K1: kind of the first step of the pass (FIRST when s == 0); K2: kind of the last (LAST ends the solve).
 // PS: scalars from `ps` (one member per launch) instead of the member table.
-// SQ: square cells (both axes carry bitwise-equal taps): one centre product per point.
-template <int T, int NW, int ST, int K1, int K2, bool ZF, int SKEW = 1, bool PS = false, bool SQ = false>
+// GM: geometry mode -- 0 generic; 1 square cells (both axes carry bitwise-equal taps): one centre
+// product per point; 2 square cells and c^2 == 1 (no c^2 product: a dependent fp64 multiply and two
+// selects less per update).
+template <int T, int NW, int ST, int K1, int K2, bool ZF, int SKEW = 1, bool PS = false, int GM = 0>
 // WHB_WF_PAIRWAIT=1: both stage waits of a row pair first (measured: no gain, 324.1 vs 325.1 Gpts/s
 // on config 2, 303.8 vs 302.5 on config 5)
 #ifndef WHB_WF_PAIRWAIT
@@ -99,6 +101,8 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, WHB_WF_MINB)
     wf2d_kernel(Geom g, const Member *__restrict__ members, int member_off, int s, int i_begin, int i_end,
                 int chunk_len, int part_off, WfScal ps) {
     using L = Lay<T, NW>;
+    constexpr bool SQ = GM >= 1;
+    constexpr int C2M = GM == 2 ? 0 : -1;
     constexpr int DL = wf_lag<SKEW>(T);  // output row lag
     static_assert(T % 2 == 0 && T >= 2 && T <= 12, "T even (pair-aligned output columns)");
     static_assert(ST >= DL + 2, "stages must cover rows r-DL .. r plus one in flight");
@@ -260,14 +264,14 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, WHB_WF_MINB)
                     const bool firstk = (K1 == K_FIRST) && (t == 1);
                     double a, b;
                     if (firstk) {
-                        a = update_point<K_FIRST, ZF, false, SQ>(g, cm.x, cc.x, cp.x, 0.0, 0.0, xl, cc.y, fv.x, 0.0,
+                        a = update_point<K_FIRST, ZF, false, SQ, C2M>(g, cm.x, cc.x, cp.x, 0.0, 0.0, xl, cc.y, fv.x, 0.0,
                                                              hcoef[t], cosl[t]);
-                        b = update_point<K_FIRST, ZF, false, SQ>(g, cm.y, cc.y, cp.y, 0.0, 0.0, cc.x, xh, fv.y, 0.0,
+                        b = update_point<K_FIRST, ZF, false, SQ, C2M>(g, cm.y, cc.y, cp.y, 0.0, 0.0, cc.x, xh, fv.y, 0.0,
                                                              hcoef[t], cosl[t]);
                     } else {
-                        a = update_point<K_MID, ZF, false, SQ>(g, cm.x, cc.x, cp.x, 0.0, 0.0, xl, cc.y, fv.x, pv.x,
+                        a = update_point<K_MID, ZF, false, SQ, C2M>(g, cm.x, cc.x, cp.x, 0.0, 0.0, xl, cc.y, fv.x, pv.x,
                                                            hcoef[t], cosl[t]);
-                        b = update_point<K_MID, ZF, false, SQ>(g, cm.y, cc.y, cp.y, 0.0, 0.0, cc.x, xh, fv.y, pv.y,
+                        b = update_point<K_MID, ZF, false, SQ, C2M>(g, cm.y, cc.y, cp.y, 0.0, 0.0, cc.x, xh, fv.y, pv.y,
                                                            hcoef[t], cosl[t]);
                     }
                     const bool rin = (row >= g.i_lo) && (row < g.i_hi);
@@ -410,14 +414,14 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, WHB_WF_MINB)
                     if (!ZF) fv = *reinterpret_cast<const double2 *>(sr + 2 * L::SEGP + xs + 2 * lane);
                     double a, b;
                     if ((K1 == K_FIRST) && (t == 1)) {
-                        a = update_point<K_FIRST, ZF, false, SQ>(g, cm.x, cc.x, cp.x, 0.0, 0.0, xl, cc.y, fv.x, 0.0,
+                        a = update_point<K_FIRST, ZF, false, SQ, C2M>(g, cm.x, cc.x, cp.x, 0.0, 0.0, xl, cc.y, fv.x, 0.0,
                                                              hcoef[t], cosl[t]);
-                        b = update_point<K_FIRST, ZF, false, SQ>(g, cm.y, cc.y, cp.y, 0.0, 0.0, cc.x, xh, fv.y, 0.0,
+                        b = update_point<K_FIRST, ZF, false, SQ, C2M>(g, cm.y, cc.y, cp.y, 0.0, 0.0, cc.x, xh, fv.y, 0.0,
                                                              hcoef[t], cosl[t]);
                     } else {
-                        a = update_point<K_MID, ZF, false, SQ>(g, cm.x, cc.x, cp.x, 0.0, 0.0, xl, cc.y, fv.x, pv.x,
+                        a = update_point<K_MID, ZF, false, SQ, C2M>(g, cm.x, cc.x, cp.x, 0.0, 0.0, xl, cc.y, fv.x, pv.x,
                                                            hcoef[t], cosl[t]);
-                        b = update_point<K_MID, ZF, false, SQ>(g, cm.y, cc.y, cp.y, 0.0, 0.0, cc.x, xh, fv.y, pv.y,
+                        b = update_point<K_MID, ZF, false, SQ, C2M>(g, cm.y, cc.y, cp.y, 0.0, 0.0, cc.x, xh, fv.y, pv.y,
                                                            hcoef[t], cosl[t]);
                     }
                     const bool rin = (row >= g.i_lo) && (row < g.i_hi);

@@ -889,10 +889,10 @@ constexpr int WF_NW = WHB_WF_NW;
 // row, 2T + 4 stages); T = 2 the plain one.
 constexpr int WF_SKEW4 = WHB_WF_SKEW;
 constexpr int WF_ST4 = wf2d::wf_lag<WF_SKEW4>(4) + WHB_WF_ST_EXTRA;  // 9 stages, 3 CTAs/SM (measured: 7 stages at 4 CTAs/SM is 1.4 % slower)
-template <int T, int K1, int K2, bool ZF, bool PS = false, bool SQ = false>
+template <int T, int K1, int K2, bool ZF, bool PS = false, int GM = 0>
 auto wf_fn() {
-    if constexpr (T == 4) return wf2d::wf2d_kernel<4, WF_NW, WF_ST4, K1, K2, ZF, WF_SKEW4, PS, SQ>;
-    else return wf2d::wf2d_kernel<T, WF_NW, T + 4, K1, K2, ZF, 1, PS, SQ>;
+    if constexpr (T == 4) return wf2d::wf2d_kernel<4, WF_NW, WF_ST4, K1, K2, ZF, WF_SKEW4, PS, GM>;
+    else return wf2d::wf2d_kernel<T, WF_NW, T + 4, K1, K2, ZF, 1, PS, GM>;
 }
 
 template <int T>
@@ -902,18 +902,21 @@ cudaError_t wf_set_attrs(size_t smem) {
         cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (r != cudaSuccess) e = r;
     };
-    set(wf_fn<T, K_FIRST, K_MID, false>()); set(wf_fn<T, K_FIRST, K_MID, true>());
-    set(wf_fn<T, K_MID, K_MID, false>());   set(wf_fn<T, K_MID, K_MID, true>());
-    set(wf_fn<T, K_MID, K_LAST, false>());  set(wf_fn<T, K_MID, K_LAST, true>());
-    set(wf_fn<T, K_FIRST, K_LAST, false>()); set(wf_fn<T, K_FIRST, K_LAST, true>());
-    set(wf_fn<T, K_FIRST, K_MID, false, true>()); set(wf_fn<T, K_FIRST, K_MID, true, true>());
-    set(wf_fn<T, K_MID, K_MID, false, true>());   set(wf_fn<T, K_MID, K_MID, true, true>());
-    set(wf_fn<T, K_MID, K_LAST, false, true>());  set(wf_fn<T, K_MID, K_LAST, true, true>());
-    set(wf_fn<T, K_FIRST, K_LAST, false, true>()); set(wf_fn<T, K_FIRST, K_LAST, true, true>());
-    set(wf_fn<T, K_FIRST, K_MID, false, true, true>()); set(wf_fn<T, K_FIRST, K_MID, true, true, true>());
-    set(wf_fn<T, K_MID, K_MID, false, true, true>());   set(wf_fn<T, K_MID, K_MID, true, true, true>());
-    set(wf_fn<T, K_MID, K_LAST, false, true, true>());  set(wf_fn<T, K_MID, K_LAST, true, true, true>());
-    set(wf_fn<T, K_FIRST, K_LAST, false, true, true>()); set(wf_fn<T, K_FIRST, K_LAST, true, true, true>());
+    auto set_gm = [&](auto ps, auto gm) {
+        constexpr bool PS = decltype(ps)::value;
+        constexpr int GM = decltype(gm)::value;
+        set(wf_fn<T, K_FIRST, K_MID, false, PS, GM>()); set(wf_fn<T, K_FIRST, K_MID, true, PS, GM>());
+        set(wf_fn<T, K_MID, K_MID, false, PS, GM>());   set(wf_fn<T, K_MID, K_MID, true, PS, GM>());
+        set(wf_fn<T, K_MID, K_LAST, false, PS, GM>());  set(wf_fn<T, K_MID, K_LAST, true, PS, GM>());
+        set(wf_fn<T, K_FIRST, K_LAST, false, PS, GM>()); set(wf_fn<T, K_FIRST, K_LAST, true, PS, GM>());
+    };
+    using F = std::false_type;
+    using Tr = std::true_type;
+    using G0 = std::integral_constant<int, 0>;
+    using G1 = std::integral_constant<int, 1>;
+    using G2 = std::integral_constant<int, 2>;
+    set_gm(F{}, G0{}); set_gm(F{}, G1{}); set_gm(F{}, G2{});
+    set_gm(Tr{}, G0{}); set_gm(Tr{}, G1{}); set_gm(Tr{}, G2{});
     return e;
 }
 
@@ -1617,17 +1620,28 @@ void launch_wf(whb_ctx *c, int off, int cnt, int s) {
         }
         ps.acc0 = m.h_acc[0];
         ps.osc = m.out_scale;
-        const Geom &g = c->geom;
-        if (g.clo0 == g.clo2 && g.cmid0 == g.cmid2)
-            wf_fn<T, K1, K2, ZF, true, true>()<<<grid, 32 * (WF_NW + 1), c->smemw[T], c->stream>>>(
-                g, c->d_members, off, s, c->upd_lo, c->upd_hi, cl, 0, ps);
-        else
-            wf_fn<T, K1, K2, ZF, true>()<<<grid, 32 * (WF_NW + 1), c->smemw[T], c->stream>>>(
-                g, c->d_members, off, s, c->upd_lo, c->upd_hi, cl, 0, ps);
-        return;
     }
-    wf_fn<T, K1, K2, ZF>()<<<grid, 32 * (WF_NW + 1), c->smemw[T], c->stream>>>(
-        c->geom, c->d_members, off, s, c->upd_lo, c->upd_hi, cl, 0, ps);
+    // geometry mode: square cells share one centre product; c^2 == 1 drops the c^2 product
+    const Geom &g = c->geom;
+    const bool sq = g.clo0 == g.clo2 && g.cmid0 == g.cmid2;
+    const int gm = sq ? (g.use_c2 ? 1 : 2) : 0;
+    auto go = [&](auto ps_tag, auto gm_tag) {
+        wf_fn<T, K1, K2, ZF, decltype(ps_tag)::value, decltype(gm_tag)::value>()
+            <<<grid, 32 * (WF_NW + 1), c->smemw[T], c->stream>>>(g, c->d_members, off, s, c->upd_lo, c->upd_hi, cl,
+                                                                0, ps);
+    };
+    using G0 = std::integral_constant<int, 0>;
+    using G1 = std::integral_constant<int, 1>;
+    using G2 = std::integral_constant<int, 2>;
+    if (cnt == 1) {  // one member: pass scalars as kernel parameters
+        if (gm == 2) go(std::true_type{}, G2{});
+        else if (gm == 1) go(std::true_type{}, G1{});
+        else go(std::true_type{}, G0{});
+    } else {
+        if (gm == 2) go(std::false_type{}, G2{});
+        else if (gm == 1) go(std::false_type{}, G1{});
+        else go(std::false_type{}, G0{});
+    }
 }
 
 template <int T>
