@@ -52,13 +52,17 @@ constexpr size_t tb2_smem_bytes() {
     return (size_t)(ST * L::STAGE + 3 * L::E_EL) * sizeof(double) + ST * sizeof(uint64_t);
 }
 
-template <int TX, int BY, int ST, bool A1, int K1, int K2, bool ZF, bool TENSOR>
+// GM: geometry mode as in wf2d (0 generic; 1 equal taps on every axis: one centre product per
+// point; 2 equal taps and c^2 == 1: no c^2 product).
+template <int TX, int BY, int ST, bool A1, int K1, int K2, bool ZF, bool TENSOR, int GM = 0>
 __global__ void __launch_bounds__(Lay<TX, BY, A1>::THREADS)
     tb2_kernel(Geom g, const Member *__restrict__ members, int member_off, int s, int i_begin, int i_end,
                int chunk_len, int JT, int part_off, const __grid_constant__ CUtensorMap tm_w,
                const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_f,
                const __grid_constant__ CUtensorMap tm_a) {
     using L = Lay<TX, BY, A1>;
+    constexpr bool SQ = GM >= 1;
+    constexpr int C2M = GM == 2 ? 0 : -1;
     static_assert(ST >= 4, "3 live planes + 1 in flight");
     static_assert(L::THREADS >= L::RING, "ext ring needs one thread per item");
     extern __shared__ __align__(128) double smem[];
@@ -173,7 +177,7 @@ __global__ void __launch_bounds__(Lay<TX, BY, A1>::THREADS)
         const double yh = A1 ? sm_c[(r + 1) * L::RW + c] : 0.0;
         const double fv = ZF ? 0.0 : F_[re * L::RW + c];
         const double pv = LOAD_P ? P_[re * L::RW + c] : 0.0;
-        const double w = update_point<K1, ZF, A1>(g, sm_m[r * L::RW + c], wc, sm_p[r * L::RW + c], yl, yh,
+        const double w = update_point<K1, ZF, A1, SQ, C2M>(g, sm_m[r * L::RW + c], wc, sm_p[r * L::RW + c], yl, yh,
                                                  sm_c[r * L::RW + c - 1], sm_c[r * L::RW + c + 1], fv, pv, h1, cos1);
         const int jj = j0 + ey, kk = k0 + ex;
         const bool inside = (i >= g.i_lo) && (i < g.i_hi) && (kk >= 1) && (kk < g.n2 - 1) &&
@@ -233,9 +237,9 @@ __global__ void __launch_bounds__(Lay<TX, BY, A1>::THREADS)
             const double xl = sm_c[rmain - 1], xh = sm_c[rmain + 2];
             const double2 fv2 = ZF ? make_double2(0.0, 0.0) : *reinterpret_cast<const double2 *>(F_ + emain);
             const double2 pv2 = LOAD_P ? *reinterpret_cast<const double2 *>(P_ + emain) : make_double2(0.0, 0.0);
-            const double a = update_point<K1, ZF, A1>(g, wsm.x, wsc.x, wsp.x, yl2.x, yh2.x, xl, wsc.y, fv2.x, pv2.x,
+            const double a = update_point<K1, ZF, A1, SQ, C2M>(g, wsm.x, wsc.x, wsp.x, yl2.x, yh2.x, xl, wsc.y, fv2.x, pv2.x,
                                                      h1, cos1);
-            const double b = update_point<K1, ZF, A1>(g, wsm.y, wsc.y, wsp.y, yl2.y, yh2.y, wsc.x, xh, fv2.y, pv2.y,
+            const double b = update_point<K1, ZF, A1, SQ, C2M>(g, wsm.y, wsc.y, wsp.y, yl2.y, yh2.y, wsc.x, xh, fv2.y, pv2.y,
                                                      h1, cos1);
             const bool pin = (i >= g.i_lo) && (i < g.i_hi);
             enew = make_double2((pin && ok0) ? a : 0.0, (pin && ok1) ? b : 0.0);
@@ -269,9 +273,9 @@ __global__ void __launch_bounds__(Lay<TX, BY, A1>::THREADS)
             const double e_xh = Ec[re * L::RW + c + 2];
             const double2 w0 = wsm;  // W^s at plane ip (prev of step s+1)
             const double2 f2 = ZF ? make_double2(0.0, 0.0) : *reinterpret_cast<const double2 *>(F_ + re * L::RW + c);
-            const double n0 = update_point<K_MID, ZF, A1>(g, e_m.x, e_c.x, e_p.x, e_yl.x, e_yh.x, e_xl, e_c.y, f2.x,
+            const double n0 = update_point<K_MID, ZF, A1, SQ, C2M>(g, e_m.x, e_c.x, e_p.x, e_yl.x, e_yh.x, e_xl, e_c.y, f2.x,
                                                          w0.x, h2, cos2);
-            const double n1 = update_point<K_MID, ZF, A1>(g, e_m.y, e_c.y, e_p.y, e_yl.y, e_yh.y, e_c.x, e_xh, f2.y,
+            const double n1 = update_point<K_MID, ZF, A1, SQ, C2M>(g, e_m.y, e_c.y, e_p.y, e_yl.y, e_yh.y, e_c.x, e_xh, f2.y,
                                                          w0.y, h2, cos2);
             double a0, a1;
             if (K1 == K_FIRST) {  // acc = c0*W^0 + c1*W^1, then += c2*W^2   (timestep.py:284, 298)

@@ -792,10 +792,18 @@ constexpr int B2_TX = 256, B2_BY = 1, B2_ST = 8;
 constexpr int T3_TX = 64, T3_BY = 16, T3_ST = 5;  // measured on 257^3: BY = 8 / 4 stages / 2 CTAs per SM -0.6 %, BY = 12 / 6 stages -6 %
 constexpr int T2_TX = 256, T2_BY = 1, T2_ST = 8;
 
-template <bool A1, int K1, int K2, bool ZF>
+template <bool A1, int K1, int K2, bool ZF, int GM = 0>
 auto tb2_fn() {
-    if constexpr (A1) return tb2::tb2_kernel<T3_TX, T3_BY, T3_ST, true, K1, K2, ZF, true>;
-    else return tb2::tb2_kernel<T2_TX, T2_BY, T2_ST, false, K1, K2, ZF, false>;
+    if constexpr (A1) return tb2::tb2_kernel<T3_TX, T3_BY, T3_ST, true, K1, K2, ZF, true, GM>;
+    else return tb2::tb2_kernel<T2_TX, T2_BY, T2_ST, false, K1, K2, ZF, false, GM>;
+}
+
+// geometry mode of a context (wf2d / tb2 GM): equal taps on every active axis -> 1, and c^2 == 1 -> 2
+int geom_mode(const whb_ctx *c) {
+    const Geom &g = c->geom;
+    const bool sq = c->act0 && g.clo0 == g.clo2 && g.cmid0 == g.cmid2 &&
+                    (!c->act1 || (g.clo1 == g.clo0 && g.cmid1 == g.cmid0));
+    return sq ? (g.use_c2 ? 1 : 2) : 0;
 }
 
 constexpr int R3_BY = 16, R3_ST = 5;
@@ -844,10 +852,16 @@ cudaError_t tb2_set_attrs(size_t smem) {
         cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (r != cudaSuccess) e = r;
     };
-    set(tb2_fn<A1, K_FIRST, K_MID, false>()); set(tb2_fn<A1, K_FIRST, K_MID, true>());
-    set(tb2_fn<A1, K_MID, K_MID, false>());   set(tb2_fn<A1, K_MID, K_MID, true>());
-    set(tb2_fn<A1, K_MID, K_LAST, false>());  set(tb2_fn<A1, K_MID, K_LAST, true>());
-    set(tb2_fn<A1, K_FIRST, K_LAST, false>()); set(tb2_fn<A1, K_FIRST, K_LAST, true>());
+    auto set_gm = [&](auto gm) {
+        constexpr int GM = decltype(gm)::value;
+        set(tb2_fn<A1, K_FIRST, K_MID, false, GM>()); set(tb2_fn<A1, K_FIRST, K_MID, true, GM>());
+        set(tb2_fn<A1, K_MID, K_MID, false, GM>());   set(tb2_fn<A1, K_MID, K_MID, true, GM>());
+        set(tb2_fn<A1, K_MID, K_LAST, false, GM>());  set(tb2_fn<A1, K_MID, K_LAST, true, GM>());
+        set(tb2_fn<A1, K_FIRST, K_LAST, false, GM>()); set(tb2_fn<A1, K_FIRST, K_LAST, true, GM>());
+    };
+    set_gm(std::integral_constant<int, 0>{});
+    set_gm(std::integral_constant<int, 1>{});
+    set_gm(std::integral_constant<int, 2>{});
     return e;
 }
 
@@ -1441,8 +1455,14 @@ int launch_step_range(whb_ctx *c, int s, int moff, int cnt) {
 template <bool A1, int K1, int K2, bool ZF>
 void launch_tb2(whb_ctx *c, dim3 grid, int off, int s, int ib, int ie, int cl, int po, const StepMaps &mp) {
     constexpr int threads = A1 ? T3_TX * T3_BY / 2 : T2_TX * T2_BY / 2;
-    tb2_fn<A1, K1, K2, ZF>()<<<grid, threads, c->smem2, c->stream>>>(c->geom, c->d_members, off, s, ib, ie,
-                                                                    cl, c->JT2, po, mp.w, mp.p, mp.f, mp.a);
+    auto go = [&](auto gm) {
+        tb2_fn<A1, K1, K2, ZF, decltype(gm)::value>()<<<grid, threads, c->smem2, c->stream>>>(
+            c->geom, c->d_members, off, s, ib, ie, cl, c->JT2, po, mp.w, mp.p, mp.f, mp.a);
+    };
+    const int gm = geom_mode(c);
+    if (gm == 2) go(std::integral_constant<int, 2>{});
+    else if (gm == 1) go(std::integral_constant<int, 1>{});
+    else go(std::integral_constant<int, 0>{});
 }
 
 template <bool A1>
@@ -1621,10 +1641,8 @@ void launch_wf(whb_ctx *c, int off, int cnt, int s) {
         ps.acc0 = m.h_acc[0];
         ps.osc = m.out_scale;
     }
-    // geometry mode: square cells share one centre product; c^2 == 1 drops the c^2 product
     const Geom &g = c->geom;
-    const bool sq = g.clo0 == g.clo2 && g.cmid0 == g.cmid2;
-    const int gm = sq ? (g.use_c2 ? 1 : 2) : 0;
+    const int gm = geom_mode(c);
     auto go = [&](auto ps_tag, auto gm_tag) {
         wf_fn<T, K1, K2, ZF, decltype(ps_tag)::value, decltype(gm_tag)::value>()
             <<<grid, 32 * (WF_NW + 1), c->smemw[T], c->stream>>>(g, c->d_members, off, s, c->upd_lo, c->upd_hi, cl,
