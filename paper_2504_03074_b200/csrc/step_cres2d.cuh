@@ -110,9 +110,12 @@ struct Args {
     int dbg;
 };
 
-template <bool ZF, bool SQ, int PPT>
+// GM: geometry mode (wf2d.cuh): 1 = square cells, 2 = square cells and c^2 == 1
+template <bool ZF, int GM, int PPT>
 __global__ void __launch_bounds__(NT, 1)
     cres2d_kernel(Geom g, const Member *__restrict__ members, int member_off, Args a) {
+    constexpr bool SQ = GM >= 1;
+    constexpr int C2M = GM == 2 ? 0 : -1;
     extern __shared__ __align__(16) double sm[];
     const Member m = members[member_off + blockIdx.y];
     const int CL = a.CL, W = a.W, n2 = g.n2;
@@ -217,11 +220,11 @@ __global__ void __launch_bounds__(NT, 1)
                 const int c = cidx[i];
                 double wn;
                 if (s == 0) {
-                    wn = bulk::update_point<K_FIRST, ZF, false, SQ>(g, cur[c - W], wc[i], cur[c + W], 0.0, 0.0,
+                    wn = bulk::update_point<K_FIRST, ZF, false, SQ, C2M>(g, cur[c - W], wc[i], cur[c + W], 0.0, 0.0,
                                                                   cur[c - 1], cur[c + 1], fv[i], 0.0, m.half_dt2, 1.0);
                     ac[i] = whb_add(whb_mul(acc0, wc[i]), whb_mul(accn, wn));
                 } else {
-                    wn = bulk::update_point<K_MID, ZF, false, SQ>(g, cur[c - W], wc[i], cur[c + W], 0.0, 0.0,
+                    wn = bulk::update_point<K_MID, ZF, false, SQ, C2M>(g, cur[c - W], wc[i], cur[c + W], 0.0, 0.0,
                                                                 cur[c - 1], cur[c + 1], fv[i], wp[i], m.dt2, cosf[s]);
                     ac[i] = whb_add(ac[i], whb_mul(accn, wn));
                 }

@@ -970,9 +970,9 @@ int get_encoder() {
 // ---- cluster-resident small-grid 2D kernel (step_cres2d.cuh) --------------------------------
 constexpr size_t kCresSmemMax = 227 * 1024 - 1024;  // opt-in maximum less the static block_sum scratch
 
-template <bool ZF, bool SQ, int PPT>
+template <bool ZF, int GM, int PPT>
 auto cres_fn() {
-    return cres::cres2d_kernel<ZF, SQ, PPT>;
+    return cres::cres2d_kernel<ZF, GM, PPT>;
 }
 
 cudaError_t cres_set_attrs() {
@@ -984,8 +984,9 @@ cudaError_t cres_set_attrs() {
         if (r != cudaSuccess) e = r;
     };
 #define WHB_CRES_SET(PPT)                                                  \
-    set(cres_fn<false, false, PPT>()); set(cres_fn<true, false, PPT>());   \
-    set(cres_fn<false, true, PPT>());  set(cres_fn<true, true, PPT>());
+    set(cres_fn<false, 0, PPT>()); set(cres_fn<true, 0, PPT>());           \
+    set(cres_fn<false, 1, PPT>()); set(cres_fn<true, 1, PPT>());           \
+    set(cres_fn<false, 2, PPT>()); set(cres_fn<true, 2, PPT>());
     WHB_CRES_SET(1) WHB_CRES_SET(2) WHB_CRES_SET(4) WHB_CRES_SET(8)
 #undef WHB_CRES_SET
     return e;
@@ -1014,7 +1015,7 @@ int cres_max_clusters(whb_ctx *c, int cl) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int n = 0;
-    const cudaError_t e = cudaOccupancyMaxActiveClusters(&n, cres_fn<false, false, 8>(), &cfg);
+    const cudaError_t e = cudaOccupancyMaxActiveClusters(&n, cres_fn<false, 0, 8>(), &cfg);
     if (e != cudaSuccess) {
         if (getenv("WHB_DEBUG")) fprintf(stderr, "[whb] cudaOccupancyMaxActiveClusters: %s\n", cudaGetErrorString(e));
         cudaGetLastError();
@@ -1772,16 +1773,18 @@ int launch_cres(whb_ctx *c, size_t smem, int iters, double tol_sq, double *hist,
     cfg.attrs = at;
     cfg.numAttrs = 1;
     const Geom &g = c->geom;
-    const bool sq = g.clo0 == g.clo2 && g.cmid0 == g.cmid2;
+    const int gm = geom_mode(c);
     const bool zf = c->cur_zf != 0;
     cudaError_t e = cudaErrorInvalidValue;
     const Member *mt = c->d_members;
 #define WHB_CRES_GO(PPT)                                                                               \
     if (c->cres_ppt == PPT) {                                                                          \
-        if (zf) e = sq ? cudaLaunchKernelEx(&cfg, cres_fn<true, true, PPT>(), g, mt, 0, a)             \
-                       : cudaLaunchKernelEx(&cfg, cres_fn<true, false, PPT>(), g, mt, 0, a);           \
-        else e = sq ? cudaLaunchKernelEx(&cfg, cres_fn<false, true, PPT>(), g, mt, 0, a)               \
-                    : cudaLaunchKernelEx(&cfg, cres_fn<false, false, PPT>(), g, mt, 0, a);             \
+        if (zf) e = gm == 2   ? cudaLaunchKernelEx(&cfg, cres_fn<true, 2, PPT>(), g, mt, 0, a)         \
+                    : gm == 1 ? cudaLaunchKernelEx(&cfg, cres_fn<true, 1, PPT>(), g, mt, 0, a)         \
+                              : cudaLaunchKernelEx(&cfg, cres_fn<true, 0, PPT>(), g, mt, 0, a);        \
+        else e = gm == 2   ? cudaLaunchKernelEx(&cfg, cres_fn<false, 2, PPT>(), g, mt, 0, a)           \
+                 : gm == 1 ? cudaLaunchKernelEx(&cfg, cres_fn<false, 1, PPT>(), g, mt, 0, a)           \
+                           : cudaLaunchKernelEx(&cfg, cres_fn<false, 0, PPT>(), g, mt, 0, a);          \
     }
     WHB_CRES_GO(1) WHB_CRES_GO(2) WHB_CRES_GO(4) WHB_CRES_GO(8)
 #undef WHB_CRES_GO
