@@ -90,6 +90,13 @@ template <int T, int NW, int ST, int K1, int K2, bool ZF, int SKEW = 1, bool PS 
 #define WF_PRAGMA_(x) _Pragma(#x)
 #define WF_UNROLL_(n) WF_PRAGMA_(unroll n)
 #define WF_UNROLL(n) WF_UNROLL_(n)
+// WHB_WF_CLEAN=1: in batched launches (scalars from the member table), rows whose levels are all
+// interior (and strips wholly interior in x) run a row body without the zeroing selects.
+// Measured: batched config 5 296 -> 306 Gpts/s; single-member config 2 343 -> 329, so the
+// single-member (PS) kernels keep one row body.
+#ifndef WHB_WF_CLEAN
+#define WHB_WF_CLEAN 1
+#endif
 // WHB_WF_WARMSKIP=0: compute every level on every input row (the pre-cone rows too)
 #ifndef WHB_WF_WARMSKIP
 #define WHB_WF_WARMSKIP 1
@@ -103,6 +110,7 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, WHB_WF_MINB)
     using L = Lay<T, NW>;
     constexpr bool SQ = GM >= 1;
     constexpr int C2M = GM == 2 ? 0 : -1;
+    constexpr bool USE_CLEAN = WHB_WF_CLEAN && !PS;
     constexpr int DL = wf_lag<SKEW>(T);  // output row lag
     static_assert(T % 2 == 0 && T >= 2 && T <= 12, "T even (pair-aligned output columns)");
     static_assert(ST >= DL + 2, "stages must cover rows r-DL .. r plus one in flight");
@@ -229,8 +237,11 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, WHB_WF_MINB)
             // WARM (input rows idx < 2T): level t at row r - t is only needed (by the outputs
             // [i0, i1) through the stencil cone) from row i0 - (T - t) on, i.e. for idx >= 2t; the
             // earlier rows of each level are skipped (left 0) instead of computed.
-            auto row_step = [&](const int idx, auto warm_tag) {
+            // CLEAN: every lane interior in x (warp_in) and the rows r-T .. r-1 of this input row's
+            // levels all interior: no zeroing selects
+            auto row_step = [&](const int idx, auto warm_tag, auto clean_tag) {
                 constexpr bool WARM = decltype(warm_tag)::value;
+                constexpr bool CLEAN = decltype(clean_tag)::value;
                 const int r = r0 + idx;
                 const int slot = idx % ST;
                 const double2 vnext = vload(r + 1 - T);
@@ -274,9 +285,13 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, WHB_WF_MINB)
                         b = update_point<K_MID, ZF, false, SQ, C2M>(g, cm.y, cc.y, cp.y, 0.0, 0.0, cc.x, xh, fv.y, pv.y,
                                                            hcoef[t], cosl[t]);
                     }
-                    const bool rin = (row >= g.i_lo) && (row < g.i_hi);
-                    if (rin && warp_in) nw[t] = make_double2(a, b);  // uniform: no per-lane selects
-                    else nw[t] = make_double2((rin && in0) ? a : 0.0, (rin && in1) ? b : 0.0);
+                    if (CLEAN) {
+                        nw[t] = make_double2(a, b);
+                    } else {
+                        const bool rin = (row >= g.i_lo) && (row < g.i_hi);
+                        if (rin && warp_in) nw[t] = make_double2(a, b);  // uniform: no per-lane selects
+                        else nw[t] = make_double2((rin && in0) ? a : 0.0, (rin && in1) ? b : 0.0);
+                    }
                     }
                     Q[t][0] = Q[t][1];
                     Q[t][1] = Q[t][2];
@@ -345,24 +360,30 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, WHB_WF_MINB)
             for (; idx + 1 < nrows; idx += 2) {
                 mbar_wait(full + (idx % ST), (idx / ST) & 1);
                 mbar_wait(full + ((idx + 1) % ST), ((idx + 1) / ST) & 1);
-                row_step(idx, std::true_type{});
-                row_step(idx + 1, std::true_type{});
+                row_step(idx, std::true_type{}, std::false_type{});
+                row_step(idx + 1, std::true_type{}, std::false_type{});
             }
             if (idx < nrows) {
                 mbar_wait(full + (idx % ST), (idx / ST) & 1);
-                row_step(idx, std::true_type{});
+                row_step(idx, std::true_type{}, std::false_type{});
             }
 #else
             const int nwarm = WHB_WF_WARMSKIP ? min(nrows, 2 * T) : 0;
             int idx = 0;
             for (; idx < nwarm; ++idx) {
                 mbar_wait(full + (idx % ST), (idx / ST) & 1);
-                row_step(idx, std::true_type{});
+                row_step(idx, std::true_type{}, std::false_type{});
             }
             WF_UNROLL(WHB_WF_UNROLL)
             for (; idx < nrows; ++idx) {
                 mbar_wait(full + (idx % ST), (idx / ST) & 1);
-                row_step(idx, std::false_type{});
+                if constexpr (USE_CLEAN) {
+                    const int r = r0 + idx;
+                    if (warp_in && r - T >= g.i_lo && r - 1 < g.i_hi) row_step(idx, std::false_type{}, std::true_type{});
+                    else row_step(idx, std::false_type{}, std::false_type{});
+                } else {
+                    row_step(idx, std::false_type{}, std::false_type{});
+                }
             }
 #endif
             // release the stages still held (rows nrows-T .. nrows-1) so the producer never blocks
