@@ -69,9 +69,18 @@ struct WfScal {
     double h[5], cs[5], ca[5];  // level t = 1..T: dt^2 factor, forcing cos factor, filter weight
     double acc0, osc;
 };
+// Batched launches: one WfScal per member of the launch (blockIdx.z), also as kernel parameters
+// (8.7 KB; CUDA 12.1+ allows 32 KB): CTA-uniform, so they stay in the constant bank / uniform
+// registers instead of ~30 per-thread registers loaded from the member table.
+constexpr int WF_TAB = 64;
+template <int N>
+struct WfTab {
+    WfScal m[N];
+};
 
 // K1: kind of the first step of the pass (FIRST when s == 0); K2: kind of the last (LAST ends the solve).
-// PS: scalars from `ps` (one member per launch) instead of the member table.
+// PS: one member per launch (scalars in ps.m[0]); otherwise up to WF_TAB members, scalars of member
+// blockIdx.z in ps.m[blockIdx.z].
 // GM: geometry mode -- 0 generic; 1 square cells (both axes carry bitwise-equal taps): one centre
 // product per point; 2 square cells and c^2 == 1 (no c^2 product: a dependent fp64 multiply and two
 // selects less per update).
@@ -106,7 +115,7 @@ template <int T, int NW, int ST, int K1, int K2, bool ZF, int SKEW = 1, bool PS 
 #endif
 __global__ void __launch_bounds__(Lay<T, NW>::THREADS, WHB_WF_MINB)
     wf2d_kernel(Geom g, const Member *__restrict__ members, int member_off, int s, int i_begin, int i_end,
-                int chunk_len, int part_off, WfScal ps) {
+                int chunk_len, int part_off, const WfTab<PS ? 1 : WF_TAB> ps) {
     using L = Lay<T, NW>;
     constexpr bool SQ = GM >= 1;
     constexpr int C2M = GM == 2 ? 0 : -1;
@@ -185,21 +194,15 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, WHB_WF_MINB)
         const bool warp_in = __all_sync(0xffffffffu, in0 && in1);
         // per-level scalars: level t (1..T) is produced by step s+t-1
         double hcoef[T + 1], cosl[T + 1], cacc[T + 1];
+        const WfScal &sc = ps.m[PS ? 0 : blockIdx.z];
 #pragma unroll
         for (int t = 1; t <= T; ++t) {
-            const bool first = (K1 == K_FIRST) && (t == 1);
-            if constexpr (PS) {
-                hcoef[t] = ps.h[t];
-                cosl[t] = ps.cs[t];
-                cacc[t] = ps.ca[t];
-            } else {
-                hcoef[t] = first ? m.half_dt2 : m.dt2;
-                cosl[t] = first ? 1.0 : m.cos_f[s + t - 1];
-                cacc[t] = m.acc_c[s + t];
-            }
+            hcoef[t] = sc.h[t];
+            cosl[t] = sc.cs[t];
+            cacc[t] = sc.ca[t];
         }
-        const double acc0 = PS ? ps.acc0 : m.acc_c[0];
-        const double oscale = PS ? ps.osc : m.out_scale;
+        const double acc0 = sc.acc0;
+        const double oscale = sc.osc;
         // a strip wholly past the last interior column (the ragged right edge of the grid) has
         // nothing to write: it only keeps the stage barriers' arrival counts, so the issue slots go
         // to the SM's other warps

@@ -1630,9 +1630,8 @@ void launch_wf(whb_ctx *c, int off, int cnt, int s) {
         nch = (nplanes + cl - 1) / cl;
     }
     dim3 grid(c->gxw[T], nch, cnt);
-    wf2d::WfScal ps{};
-    if (cnt == 1) {  // one member: its pass scalars go in as kernel parameters
-        const MemberHost &m = c->mem[c->order[off]];
+    // per-member pass scalars (the reference's host expressions, as in the member table)
+    auto fill = [&](wf2d::WfScal &ps, const MemberHost &m) {
         for (int t = 1; t <= T; ++t) {
             const bool first = (K1 == K_FIRST) && (t == 1);
             ps.h[t] = first ? m.half_dt2 : m.dt2;
@@ -1641,13 +1640,25 @@ void launch_wf(whb_ctx *c, int off, int cnt, int s) {
         }
         ps.acc0 = m.h_acc[0];
         ps.osc = m.out_scale;
+    };
+    wf2d::WfTab<1> ps1{};
+    wf2d::WfTab<wf2d::WF_TAB> psn;  // copied into the launch parameters at the launch
+    if (cnt == 1) {
+        fill(ps1.m[0], c->mem[c->order[off]]);
+    } else {
+        for (int z = 0; z < cnt; ++z) fill(psn.m[z], c->mem[c->order[off + z]]);
     }
     const Geom &g = c->geom;
     const int gm = geom_mode(c);
     auto go = [&](auto ps_tag, auto gm_tag) {
-        wf_fn<T, K1, K2, ZF, decltype(ps_tag)::value, decltype(gm_tag)::value>()
-            <<<grid, 32 * (WF_NW + 1), c->smemw[T], c->stream>>>(g, c->d_members, off, s, c->upd_lo, c->upd_hi, cl,
-                                                                0, ps);
+        constexpr bool PS = decltype(ps_tag)::value;
+        auto fn = wf_fn<T, K1, K2, ZF, PS, decltype(gm_tag)::value>();
+        if constexpr (PS)
+            fn<<<grid, 32 * (WF_NW + 1), c->smemw[T], c->stream>>>(g, c->d_members, off, s, c->upd_lo, c->upd_hi, cl,
+                                                                  0, ps1);
+        else
+            fn<<<grid, 32 * (WF_NW + 1), c->smemw[T], c->stream>>>(g, c->d_members, off, s, c->upd_lo, c->upd_hi, cl,
+                                                                  0, psn);
     };
     using G0 = std::integral_constant<int, 0>;
     using G1 = std::integral_constant<int, 1>;
@@ -1681,6 +1692,11 @@ void launch_wf_kinds(whb_ctx *c, int k1, int k2, bool zf, int off, int cnt, int 
 // One wavefront pass group: table members [off, off+cnt) advance T steps from step s.
 int launch_wf_group(whb_ctx *c, int T, int off, int cnt, int s, bool last) {
     if (cnt <= 0) return 0;
+    if (cnt > wf2d::WF_TAB) {  // one launch per WF_TAB members (the launch parameters hold their scalars)
+        for (int o = 0; o < cnt; o += wf2d::WF_TAB)
+            WHB_TRY(launch_wf_group(c, T, off + o, std::min(wf2d::WF_TAB, cnt - o), s, last));
+        return 0;
+    }
     const int k1 = s == 0 ? K_FIRST : K_MID;
     const int k2 = last ? K_LAST : K_MID;
     const bool zf = c->cur_zf != 0;
