@@ -52,12 +52,17 @@ enum whb_status {
 enum whb_field {
     WHB_V = 0,    /* iterate v (W^0 of a solve; FPI updates it in place)      */
     WHB_F = 1,    /* forcing f(x) (shared by all members if shared_forcing)   */
-    WHB_WA = 2,   /* time levels 1, 5, 9, ...  (level L >= 1 in slot L mod 4)  */
-    WHB_WB = 3,   /* time levels 2, 6, 10, ...                                 */
+    /* Time levels L >= 1 live in a ring of nring buffers, level L in slot L mod nring
+     * (whb_plan reports the kernel family; nring = 6 for plans with 4-step passes, 4 otherwise).
+     * A pass of T steps reads levels s, s-1 and writes s+T-1, s+T; nring >= T + 2 keeps the
+     * written slots disjoint from the read ones.  WA..WD name ring slots 1, 2, 3 and 0; slots
+     * 4 and 5 of a 6-slot ring are internal. */
+    WHB_WA = 2,   /* ring slot 1                                               */
+    WHB_WB = 3,   /* ring slot 2                                               */
     WHB_ACC = 4,  /* running filter sum                                        */
     WHB_OUT = 5,  /* output of a plain/matvec solve                            */
-    WHB_WC = 6,   /* time levels 3, 7, 11, ...                                 */
-    WHB_WD = 7    /* time levels 4, 8, 12, ...                                 */
+    WHB_WC = 6,   /* ring slot 3                                               */
+    WHB_WD = 7    /* ring slot 0                                               */
 };
 
 /* What the last step of a filtered solve writes (timestep.py:300-301, driver.py:222-225, 256-262). */

@@ -92,6 +92,62 @@ def multi_gaussian(g, omega, n_gauss, seed=0):
     return wh.grid.GridField.from_values(g, f)
 
 
+def multi_gaussian_slabs(g, omega, n_gauss, seed=0, slab=32):
+    """multi_gaussian() for grids too large for the reference's whole-grid numpy
+    temporaries (1025^3: ~6 x 8.6 GB per Gaussian): the reference's own
+    ``gaussian_source`` (driver.py:163-179) is evaluated on axis-0 slabs of the
+    grid through a slab-view grid whose ``coords()`` are the full grid's
+    ``axis_coords`` (grid.py:104-112) with axis 0 sliced, so every element goes
+    through the same numpy ufuncs on the same operands.  The slab view marks
+    axis 0 periodic so ``GridField.from_values`` does not zero the slab's cut
+    faces; the global Dirichlet planes 0 and n0-1 are zeroed here exactly as
+    ``_enforce_dirichlet_zeros`` (grid.py:237-246) zeroes them on the full grid.
+    Returns a plain float64 array of the grid's shape."""
+    import numpy as np
+
+    wh = import_reference()
+    G = wh.grid
+    rng = np.random.default_rng(seed)
+    amp = rng.uniform(-100.0, 100.0, n_gauss)
+    ctr = rng.uniform(0.1, 0.9, (n_gauss, g.dim))
+    b = rng.uniform(100.0, 1000.0, n_gauss)
+    shape = tuple(g.shape)
+    axes = [g.axis_coords(m) for m in range(g.dim)]
+    out = np.empty(shape)
+
+    class _SlabView(G.CartesianGrid):
+        def __post_init__(self):
+            pass
+
+        @property
+        def npoints(self):
+            return (self._p1 - self._p0,) + tuple(shape[1:])
+
+        def coords(self):
+            ax = [axes[0][self._p0:self._p1]] + axes[1:]
+            return tuple(np.meshgrid(*ax, indexing="ij"))
+
+    for p0 in range(0, shape[0], slab):
+        p1 = min(shape[0], p0 + slab)
+        sv = _SlabView(g.dim, g.bounds, g.cells, (G.BC.PERIODIC,) + tuple(g.bcs[1:]))
+        object.__setattr__(sv, "_p0", p0)
+        object.__setattr__(sv, "_p1", p1)
+        acc = np.zeros(sv.npoints)
+        for k in range(n_gauss):
+            v = np.array(wh.driver.gaussian_source(sv, omega, amp[k], b[k], ctr[k]).values)
+            if p0 == 0:
+                v[0] = 0.0
+            if p1 == shape[0]:
+                v[-1] = 0.0
+            acc = acc + v
+        if p0 == 0:
+            acc[0] = 0.0
+        if p1 == shape[0]:
+            acc[-1] = 0.0
+        out[p0:p1] = acc
+    return out
+
+
 def explicit_setup(g, omega, p=2, c=1.0, periods=1):
     """(corr, cfg, op) exactly as resolve_time_discretization builds them (driver.py:182-192)."""
     wh = import_reference()

@@ -182,6 +182,57 @@ int who_fpi(int nd, const int64_t *shape, const double *clo, const double *cmid,
     return 0;
 }
 
+/* FPI with 5 resident fields (f, v, two time levels, acc) for grids whose
+ * who_fpi working set (8 fields) does not fit host memory (1025^3 = 8.6 GB per
+ * field).  Same per-point arithmetic and order as who_wave_solve: W^{n+1} is
+ * written over W^{n-1} (each point reads only its own W^{n-1}), the last step
+ * writes out = s*(acc + c_N W^N) over acc, and W^0 = v is read in place. */
+int who_fpi_lean(int nd, const int64_t *shape, const double *clo, const double *cmid, double c2,
+                 const double *f, int n_total, double half_dt2, double dt2, const double *cos_f,
+                 const double *acc_c, double out_scale, int iters, double *v, double *resid,
+                 int nthreads, int v_given) {
+    if (nd < 1 || nd > 3 || n_total < 2) return -1;
+    geom_t g;
+    make_geom(&g, nd, shape, clo, cmid, c2);
+    const int use_c2 = (c2 != 1.0);
+    const int64_t N = total(shape, nd);
+    double *wa = (double *)calloc((size_t)N, sizeof(double));
+    double *wb = (double *)calloc((size_t)N, sizeof(double));
+    double *acc = (double *)calloc((size_t)N, sizeof(double));
+    if (!wa || !wb || !acc) {
+        free(wa); free(wb); free(acc);
+        return -2;
+    }
+    if (!v_given) memset(v, 0, (size_t)N * sizeof(double));  /* else continue from the caller's v */
+    for (int k = 0; k < iters; ++k) {
+        /* W^1 -> wa from W^0 = v */
+        step(&g, 0, 0, v, NULL, f, wa, acc, NULL, half_dt2, 1.0, acc_c[0], acc_c[1], 0.0, use_c2,
+             nthreads);
+        /* W^2 -> wb (W^{n-1} = v is not overwritten) */
+        double *wm = v, *wc = wa, *wn = wb;
+        for (int n = 1; n < n_total; ++n) {
+            const int last = (n == n_total - 1);
+            step(&g, last ? 2 : 1, 0, wc, wm, f, wn, acc, acc, dt2, cos_f[n], 0.0, acc_c[n + 1],
+                 out_scale, use_c2, nthreads);
+            /* rotate; from n = 2 on the new level overwrites W^{n-1} in place */
+            double *t = wc;
+            wc = wn;
+            wm = (n == 1) ? wa : t;
+            wn = wm;
+        }
+        /* acc now holds v_new (boundary points: acc is 0 there) */
+        double ss = 0.0;
+        for (int64_t p = 0; p < N; ++p) {
+            const double d = acc[p] - v[p];
+            ss += d * d;
+        }
+        resid[k] = sqrt(ss) / sqrt((double)N);
+        memcpy(v, acc, (size_t)N * sizeof(double));
+    }
+    free(wa); free(wb); free(acc);
+    return 0;
+}
+
 int who_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

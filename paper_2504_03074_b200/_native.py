@@ -199,7 +199,7 @@ class Context:
         check(L.whb_create(ctypes.byref(h), self.device, self.ndim, shp.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                            self.plane_range[0], self.plane_range[1], self.nbatch, int(bool(shared_forcing))),
               "whb_create")
-        self._h = h
+        self._hh = h
         # owned part of a field, as host arrays see it
         if self.ndim == 1:
             self.local_shape = self.shape
@@ -207,13 +207,26 @@ class Context:
             self.local_shape = (self.plane_range[1] - self.plane_range[0],) + self.shape[1:]
 
     @property
+    def _h(self):
+        h = getattr(self, "_hh", None)
+        if h is None:
+            raise RuntimeError("device state released: this context was closed (release_device_cache() or "
+                               "close()); create the solver / device problem again")
+        return h
+
+    @property
     def handle(self):
         return self._h
 
+    @property
+    def closed(self) -> bool:
+        return getattr(self, "_hh", None) is None
+
     def close(self):
-        if getattr(self, "_h", None) is not None and self._h.value:
-            load().whb_destroy(self._h)
-            self._h = None
+        h = getattr(self, "_hh", None)
+        if h is not None and h.value:
+            load().whb_destroy(h)
+        self._hh = None
 
     def __del__(self):
         try:
@@ -251,8 +264,26 @@ class Context:
         a = self._host(values)
         check(load().whb_upload(self._h, int(field), int(member), _dp(a)), "whb_upload")
 
+    def _out(self, out, what):
+        """A caller-supplied output buffer must be exactly what the C ABI writes: float64,
+        C-contiguous, the owned field shape (else the D2H copy would overrun it)."""
+        if out is None:
+            return np.empty(self.local_shape)
+        if not isinstance(out, np.ndarray) or out.dtype != np.float64 or not out.flags.c_contiguous \
+                or not out.flags.writeable or out.shape != self.local_shape:
+            raise ValueError(f"{what}: out must be a writeable C-contiguous float64 array of shape "
+                             f"{self.local_shape}")
+        return out
+
+    def _in(self, a, what):
+        """A host input the C ABI reads in place: float64, C-contiguous, the owned field shape."""
+        if not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags.c_contiguous \
+                or a.shape != self.local_shape:
+            raise ValueError(f"{what}: expected a C-contiguous float64 array of shape {self.local_shape}")
+        return a
+
     def download(self, field, member=0, out=None):
-        out = np.empty(self.local_shape) if out is None else out
+        out = self._out(out, "download")
         check(load().whb_download(self._h, int(field), int(member), _dp(out)), "whb_download")
         return out
 
@@ -281,6 +312,8 @@ class Context:
         return res[: done.value * self.nbatch].reshape(done.value, self.nbatch)
 
     def iterate_host(self, v_in, v_out):
+        v_in = self._in(v_in, "iterate_host v_in")
+        v_out = self._out(v_out, "iterate_host v_out")
         r = np.zeros(1)
         check(load().whb_iterate_host(self._h, _dp(v_in), _dp(v_out), _dp(r)), "whb_iterate_host")
         return float(r[0])
@@ -296,7 +329,7 @@ class Context:
         check(load().whb_vec_upload(self._h, int(vid), _dp(a)), "whb_vec_upload")
 
     def vec_download(self, vid, out=None):
-        out = np.empty(self.local_shape) if out is None else out
+        out = self._out(out, "vec_download")
         check(load().whb_vec_download(self._h, int(vid), _dp(out)), "whb_vec_download")
         return out
 

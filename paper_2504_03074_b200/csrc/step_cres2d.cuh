@@ -107,7 +107,6 @@ struct Args {
     double *hist;     // FPI: hist[(k0 + it) * nb + member idx] (nullptr: partials[0] for the reduction kernel)
     int k0, nb;
     int *done;        // FPI: iterations performed (written by member 0's cluster), may be nullptr
-    int dbg;
 };
 
 // GM: geometry mode (wf2d.cuh): 1 = square cells, 2 = square cells and c^2 == 1
@@ -269,7 +268,6 @@ __global__ void __launch_bounds__(NT, 1)
             }
 #else
             step_sync(has_remote || (last && fpi && threadIdx.x == 0));
-            if (a.dbg & 4) cluster_sync();
 #endif
         }
         p ^= (N & 1);  // the last step wrote W^0 of the next iteration into buffer (N + p) & 1

@@ -50,14 +50,6 @@ struct Lay {
     static constexpr int THREADS = 32 * (NW + 1);
 };
 
-// Row lag of time level t in the wavefront: SKEW = 1 -> t (levels of a row are a
-// dependency chain); SKEW = 2 -> 2t - 1 (level t only reads level t-1 rows finished in
-// earlier iterations, so the T level updates of an iteration are independent: T-fold ILP).
-template <int SKEW>
-__host__ __device__ constexpr int wf_lag(int t) {
-    return t == 0 ? 0 : SKEW * t - (SKEW - 1);
-}
-
 template <int T, int NW, int ST>
 constexpr size_t wf_smem_bytes() {
     return (size_t)ST * Lay<T, NW>::STAGE * sizeof(double) + 2 * ST * sizeof(uint64_t);
@@ -84,12 +76,7 @@ struct WfTab {
 // GM: geometry mode -- 0 generic; 1 square cells (both axes carry bitwise-equal taps): one centre
 // product per point; 2 square cells and c^2 == 1 (no c^2 product: a dependent fp64 multiply and two
 // selects less per update).
-template <int T, int NW, int ST, int K1, int K2, bool ZF, int SKEW = 1, bool PS = false, int GM = 0>
-// WHB_WF_PAIRWAIT=1: both stage waits of a row pair first (measured: no gain, 324.1 vs 325.1 Gpts/s
-// on config 2, 303.8 vs 302.5 on config 5)
-#ifndef WHB_WF_PAIRWAIT
-#define WHB_WF_PAIRWAIT 0
-#endif
+template <int T, int NW, int ST, int K1, int K2, bool ZF, bool PS = false, int GM = 0>
 // steady-state row-loop unroll (measured: 3, the period of the level queues, is within noise
 // of 2 -- 321.4 vs 322.3 Gpts/s on config 2, 302.9 vs 299.9 on config 5; the queue shifts are
 // renames either way)
@@ -120,7 +107,7 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, WHB_WF_MINB)
     constexpr bool SQ = GM >= 1;
     constexpr int C2M = GM == 2 ? 0 : -1;
     constexpr bool USE_CLEAN = WHB_WF_CLEAN && !PS;
-    constexpr int DL = wf_lag<SKEW>(T);  // output row lag
+    constexpr int DL = T;  // output row lag: level t of input row r is computed at row r - t
     static_assert(T % 2 == 0 && T >= 2 && T <= 12, "T even (pair-aligned output columns)");
     static_assert(ST >= DL + 2, "stages must cover rows r-DL .. r plus one in flight");
     extern __shared__ __align__(128) double smem[];
@@ -207,7 +194,7 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, WHB_WF_MINB)
         // nothing to write: it only keeps the stage barriers' arrival counts, so the issue slots go
         // to the SM's other warps
         const bool idle = __all_sync(0xffffffffu, !(okc0 || okc1));
-        if (SKEW == 1 && idle) {
+        if (idle) {
             for (int idx = 0; idx < nrows; ++idx) {
                 mbar_wait(full + (idx % ST), (idx / ST) & 1);
                 __syncwarp();
@@ -216,7 +203,7 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, WHB_WF_MINB)
             if (lane == 0)
                 for (int idx = max(0, nrows - T); idx < nrows; ++idx) mbar_arrive(empty + (idx % ST));
             __syncwarp();
-        } else if constexpr (SKEW == 1) {
+        } else {
         // level queues: Q[t][0..2] = level t at rows (r-t-2, r-t-1, r-t); Q[0] = W^s
             double2 Q[T + 1][3];
             double2 A[T];  // A[t-1] = partial filter sum of row r-t
@@ -355,22 +342,6 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, WHB_WF_MINB)
                 __syncwarp();
                 if (idx >= T && lane == 0) mbar_arrive(empty + ((idx - T) % ST));
             };
-#if WHB_WF_PAIRWAIT
-            // Two rows per iteration with both stage waits first: the waits are spin loops (basic
-            // block boundaries), so this puts both rows' level chains into one block and the
-            // scheduler can overlap row idx+1's lower levels with row idx's upper ones.
-            int idx = 0;
-            for (; idx + 1 < nrows; idx += 2) {
-                mbar_wait(full + (idx % ST), (idx / ST) & 1);
-                mbar_wait(full + ((idx + 1) % ST), ((idx + 1) / ST) & 1);
-                row_step(idx, std::true_type{}, std::false_type{});
-                row_step(idx + 1, std::true_type{}, std::false_type{});
-            }
-            if (idx < nrows) {
-                mbar_wait(full + (idx % ST), (idx / ST) & 1);
-                row_step(idx, std::true_type{}, std::false_type{});
-            }
-#else
             const int nwarm = WHB_WF_WARMSKIP ? min(nrows, 2 * T) : 0;
             int idx = 0;
             for (; idx < nwarm; ++idx) {
@@ -388,135 +359,9 @@ __global__ void __launch_bounds__(Lay<T, NW>::THREADS, WHB_WF_MINB)
                     row_step(idx, std::false_type{}, std::false_type{});
                 }
             }
-#endif
             // release the stages still held (rows nrows-T .. nrows-1) so the producer never blocks
             if (lane == 0)
                 for (int idx = max(0, nrows - T); idx < nrows; ++idx) mbar_arrive(empty + (idx % ST));
-            __syncwarp();
-        } else {
-            // Q[t][k] = level t at row (r_prev - lag(t) - k) with r_prev the previous input row;
-            // Q0[k] = W^s at row r - k (already holding row r)
-            constexpr int DQ = 2 * SKEW;
-            double2 Q0[DQ], Q[T + 1][DQ];
-            double2 P[DL + 1];  // P[j] = partial filter sum of row r - j
-#pragma unroll
-            for (int k = 0; k < DQ; ++k) Q0[k] = make_double2(0.0, 0.0);
-#pragma unroll
-            for (int t = 0; t <= T; ++t)
-#pragma unroll
-                for (int k = 0; k < DQ; ++k) Q[t][k] = make_double2(0.0, 0.0);
-#pragma unroll
-            for (int j = 0; j <= DL; ++j) P[j] = make_double2(0.0, 0.0);
-            for (int idx = 0; idx < nrows; ++idx) {
-                const int r = r0 + idx;
-                const int slot = idx % ST;
-                mbar_wait(full + slot, (idx / ST) & 1);
-                const double *st = smem + (size_t)slot * L::STAGE;
-#pragma unroll
-                for (int k = DQ - 1; k > 0; --k) Q0[k] = Q0[k - 1];
-                Q0[0] = *reinterpret_cast<const double2 *>(st + xs + 2 * lane);
-                double2 nw[T + 1];
-#pragma unroll
-                for (int t = 1; t <= T; ++t) {
-                    const int lag = wf_lag<SKEW>(t);
-                    const int row = r - lag;
-                    const double *sr = smem + (size_t)((idx - lag + 2 * ST) % ST) * L::STAGE;
-                    double2 cm, cc, cp, pv;
-                    if (t == 1) {  // W^s rows r-2, r-1, r; prev = W^{s-1}(r-1)
-                        cm = Q0[2]; cc = Q0[1]; cp = Q0[0];
-                        pv = LOAD_PA ? *reinterpret_cast<const double2 *>(sr + L::SEGP + xs + 2 * lane)
-                                     : make_double2(0.0, 0.0);
-                    } else {
-                        const int kc = lag - wf_lag<SKEW>(t - 1) - 1;  // centre index in Q[t-1]
-                        cm = Q[t - 1][kc + 1]; cc = Q[t - 1][kc]; cp = Q[t - 1][kc - 1];
-                        if (t == 2) pv = Q0[lag];                               // W^s at row r - lag
-                        else pv = Q[t - 2][lag - wf_lag<SKEW>(t - 2) - 1];      // level t-2 at row r - lag
-                    }
-                    const double xl = __shfl_up_sync(0xffffffffu, cc.y, 1);
-                    const double xh = __shfl_down_sync(0xffffffffu, cc.x, 1);
-                    double2 fv = make_double2(0.0, 0.0);
-                    if (!ZF) fv = *reinterpret_cast<const double2 *>(sr + 2 * L::SEGP + xs + 2 * lane);
-                    double a, b;
-                    if ((K1 == K_FIRST) && (t == 1)) {
-                        a = update_point<K_FIRST, ZF, false, SQ, C2M>(g, cm.x, cc.x, cp.x, 0.0, 0.0, xl, cc.y, fv.x, 0.0,
-                                                             hcoef[t], cosl[t]);
-                        b = update_point<K_FIRST, ZF, false, SQ, C2M>(g, cm.y, cc.y, cp.y, 0.0, 0.0, cc.x, xh, fv.y, 0.0,
-                                                             hcoef[t], cosl[t]);
-                    } else {
-                        a = update_point<K_MID, ZF, false, SQ, C2M>(g, cm.x, cc.x, cp.x, 0.0, 0.0, xl, cc.y, fv.x, pv.x,
-                                                           hcoef[t], cosl[t]);
-                        b = update_point<K_MID, ZF, false, SQ, C2M>(g, cm.y, cc.y, cp.y, 0.0, 0.0, cc.x, xh, fv.y, pv.y,
-                                                           hcoef[t], cosl[t]);
-                    }
-                    const bool rin = (row >= g.i_lo) && (row < g.i_hi);
-                    nw[t] = make_double2((rin && in0) ? a : 0.0, (rin && in1) ? b : 0.0);
-                }
-                // level T-1 at the output row (before the shift: index lag(T) - lag(T-1) - 1)
-                const double2 wa2 = Q[T - 1][DL - wf_lag<SKEW>(T - 1) - 1];
-#pragma unroll
-                for (int t = 1; t <= T; ++t) {
-#pragma unroll
-                    for (int k = DQ - 1; k > 0; --k) Q[t][k] = Q[t][k - 1];
-                    Q[t][0] = nw[t];
-                }
-                // filter partial sums: row r - j, contributions in increasing level order
-#pragma unroll
-                for (int j = DL; j >= 2; --j) {
-                    P[j] = P[j - 1];
-#pragma unroll
-                    for (int t = 2; t <= T; ++t)
-                        if (j == wf_lag<SKEW>(t)) {
-                            P[j].x = whb_add(P[j].x, whb_mul(cacc[t], nw[t].x));
-                            P[j].y = whb_add(P[j].y, whb_mul(cacc[t], nw[t].y));
-                        }
-                }
-                {
-                    double2 init;
-                    if (K1 == K_FIRST) {  // c0 * W^0 at row r-1
-                        init = make_double2(whb_mul(acc0, Q0[1].x), whb_mul(acc0, Q0[1].y));
-                    } else {
-                        const double *sr1 = smem + (size_t)((idx - 1 + ST) % ST) * L::STAGE;
-                        const int ao = xs + 2 * lane - T;
-                        init = (ao >= 0 && ao + 1 < L::CW) ? *reinterpret_cast<const double2 *>(sr1 + 3 * L::SEGP + ao)
-                                                           : make_double2(0.0, 0.0);
-                    }
-                    P[1].x = whb_add(init.x, whb_mul(cacc[1], nw[1].x));
-                    P[1].y = whb_add(init.y, whb_mul(cacc[1], nw[1].y));
-                }
-                const int orow = r - DL;
-                if (orow >= i0 && orow < i1) {
-                    const long long p = (long long)orow * S0 + col;
-                    const double2 wb2 = nw[T];
-                    const double2 ac = P[DL];
-                    if (K2 == K_MID) {
-                        if (okc0 && okc1) {
-                            *reinterpret_cast<double2 *>(wA + p) = wa2;
-                            *reinterpret_cast<double2 *>(wB + p) = wb2;
-                            *reinterpret_cast<double2 *>(m.acc + p) = ac;
-                        } else {
-                            if (okc0) { wA[p] = wa2.x; wB[p] = wb2.x; m.acc[p] = ac.x; }
-                            if (okc1) { wA[p + 1] = wa2.y; wB[p + 1] = wb2.y; m.acc[p + 1] = ac.y; }
-                        }
-                    } else {
-                        const double o0 = whb_mul(oscale, ac.x);
-                        const double o1 = whb_mul(oscale, ac.y);
-                        if (m.out_mode == WHB_OUT_FPI) {
-                            if (okc0) { const double d = o0 - m.v[p]; rsum += d * d; m.v[p] = o0; }
-                            if (okc1) { const double d = o1 - m.v[p + 1]; rsum += d * d; m.v[p + 1] = o1; }
-                        } else if (m.out_mode == WHB_OUT_AV) {
-                            if (okc0) m.dst[p] = whb_sub(m.v[p], o0);
-                            if (okc1) m.dst[p + 1] = whb_sub(m.v[p + 1], o1);
-                        } else {
-                            if (okc0) m.dst[p] = o0;
-                            if (okc1) m.dst[p + 1] = o1;
-                        }
-                    }
-                }
-                __syncwarp();
-                if (idx >= DL && lane == 0) mbar_arrive(empty + ((idx - DL) % ST));
-            }
-            if (lane == 0)
-                for (int idx = max(0, nrows - DL); idx < nrows; ++idx) mbar_arrive(empty + (idx % ST));
             __syncwarp();
         }
     }

@@ -304,9 +304,6 @@ __global__ void zero_boundary_kernel(double *x, long long S0, int P, int n1, int
 #include "step_bulk.cuh"
 #include "step_tb2.cuh"
 #include "step_wf2d.cuh"
-#include "step_tb2r.cuh"
-#include "step_tb2w.cuh"
-#include "step_wf3.cuh"
 #include "step_cres2d.cuh"
 #include "implicit.cuh"
 namespace {
@@ -657,15 +654,9 @@ struct whb_ctx {
     bool tb2 = false;
     size_t smem2 = 0;
     int gx2 = 1, JT2 = 1, chunk2 = 1, nch2 = 1;
-    bool tb2r = false;               // 3D: balanced 62-column variant of the two-step kernel
-    bool tb2w = false;               // 3D: warp-specialised two-step kernel
     // cluster-resident small-grid 2D plan (whole grid in one cluster's shared memory)
     bool cres = false;
     int cres_cl = 0, cres_r = 0, cres_ppt = 1;
-    // 3D three-step wavefront plan (whole-grid 3D contexts)
-    bool wf3 = false;
-    size_t smem3 = 0;
-    int gx3 = 1, JT3 = 1, chunk3 = 1, nch3 = 1;
     // 2D wavefront plan (T steps per pass): whole-grid 2D contexts
     int wfT = 0;                     // 0 = off, else 2 or 4
     int nring = 4;                   // time-level buffers per member (6 for 3- and 4-step passes)
@@ -728,6 +719,23 @@ struct TriData {
 
 void free_mg(whb_ctx *c);
 void free_tri(whb_ctx *c);
+
+// Caller-captured graphs bake buffer pointers (d_hist, the schedule arrays, MG levels): when any of
+// them is reallocated the graphs are destroyed and their ids stay invalid (whb_graph_launch then
+// fails with WHB_E_STATE) until the caller captures again.
+void invalidate_user_graphs(whb_ctx *c) {
+    for (auto &ge : c->user_graphs)
+        if (ge) {
+            cudaGraphExecDestroy(ge);
+            ge = nullptr;
+        }
+}
+
+// CG iteration graphs bake the multigrid / tridiagonal buffers of the current setup
+void drop_cg_graphs(whb_ctx *c) {
+    for (auto &kv : c->cg_graphs) cudaGraphExecDestroy(kv.second);
+    c->cg_graphs.clear();
+}
 
 int set_dev(whb_ctx *c) {
     WHB_CUDA(cudaSetDevice(c->device));
@@ -806,45 +814,6 @@ int geom_mode(const whb_ctx *c) {
     return sq ? (g.use_c2 ? 1 : 2) : 0;
 }
 
-constexpr int R3_BY = 16, R3_ST = 5;
-constexpr int W3_BY = 14, W3_ST = 5;
-
-template <int K1, int K2, bool ZF>
-auto tb2w_fn() {
-    return tb2w::tb2w_kernel<W3_BY, W3_ST, K1, K2, ZF>;
-}
-
-cudaError_t tb2w_set_attrs(size_t smem) {
-    cudaError_t e = cudaSuccess;
-    auto set = [&](auto fn) {
-        cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (r != cudaSuccess) e = r;
-    };
-    set(tb2w_fn<K_FIRST, K_MID, false>()); set(tb2w_fn<K_FIRST, K_MID, true>());
-    set(tb2w_fn<K_MID, K_MID, false>());   set(tb2w_fn<K_MID, K_MID, true>());
-    set(tb2w_fn<K_MID, K_LAST, false>());  set(tb2w_fn<K_MID, K_LAST, true>());
-    set(tb2w_fn<K_FIRST, K_LAST, false>()); set(tb2w_fn<K_FIRST, K_LAST, true>());
-    return e;
-}
-
-template <int K1, int K2, bool ZF>
-auto tb2r_fn() {
-    return tb2r::tb2r_kernel<R3_BY, R3_ST, K1, K2, ZF>;
-}
-
-cudaError_t tb2r_set_attrs(size_t smem) {
-    cudaError_t e = cudaSuccess;
-    auto set = [&](auto fn) {
-        cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (r != cudaSuccess) e = r;
-    };
-    set(tb2r_fn<K_FIRST, K_MID, false>()); set(tb2r_fn<K_FIRST, K_MID, true>());
-    set(tb2r_fn<K_MID, K_MID, false>());   set(tb2r_fn<K_MID, K_MID, true>());
-    set(tb2r_fn<K_MID, K_LAST, false>());  set(tb2r_fn<K_MID, K_LAST, true>());
-    set(tb2r_fn<K_FIRST, K_LAST, false>()); set(tb2r_fn<K_FIRST, K_LAST, true>());
-    return e;
-}
-
 template <bool A1>
 cudaError_t tb2_set_attrs(size_t smem) {
     cudaError_t e = cudaSuccess;
@@ -865,48 +834,21 @@ cudaError_t tb2_set_attrs(size_t smem) {
     return e;
 }
 
-// 3D three-step wavefront: 12 x 64 tiles, 384 threads, one CTA per SM (220 KB shared memory).
-constexpr int W3D_BY = 12;
-
-template <int K1, int K2, bool ZF>
-auto wf3_fn() {
-    return wf3::wf3_kernel<W3D_BY, K1, K2, ZF>;
-}
-
-cudaError_t wf3_set_attrs(size_t smem) {
-    cudaError_t e = cudaSuccess;
-    auto set = [&](auto fn) {
-        cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (r != cudaSuccess) e = r;
-    };
-    set(wf3_fn<K_FIRST, K_MID, false>()); set(wf3_fn<K_FIRST, K_MID, true>());
-    set(wf3_fn<K_MID, K_MID, false>());   set(wf3_fn<K_MID, K_MID, true>());
-    set(wf3_fn<K_MID, K_LAST, false>());  set(wf3_fn<K_MID, K_LAST, true>());
-    set(wf3_fn<K_FIRST, K_LAST, false>()); set(wf3_fn<K_FIRST, K_LAST, true>());
-    return e;
-}
-
 // 2D wavefront kernels: 4 consumer warps + 1 producer warp, T + 4 row stages.
 // (the WHB_WF_* macros exist for variant builds in tuning sweeps: tools/variants.py)
 #ifndef WHB_WF_NW
 #define WHB_WF_NW 4
-#endif
-#ifndef WHB_WF_SKEW
-#define WHB_WF_SKEW 1
 #endif
 #ifndef WHB_WF_ST_EXTRA
 #define WHB_WF_ST_EXTRA 5
 #endif
 constexpr int WF_NW = WHB_WF_NW;
 
-// T = 4 runs the skewed wavefront (level t at row r - 2t + 1: independent level updates per
-// row, 2T + 4 stages); T = 2 the plain one.
-constexpr int WF_SKEW4 = WHB_WF_SKEW;
-constexpr int WF_ST4 = wf2d::wf_lag<WF_SKEW4>(4) + WHB_WF_ST_EXTRA;  // 9 stages, 3 CTAs/SM (measured: 7 stages at 4 CTAs/SM is 1.4 % slower)
+constexpr int WF_ST4 = 4 + WHB_WF_ST_EXTRA;  // 9 stages, 3 CTAs/SM (measured: 7 stages at 4 CTAs/SM is 1.4 % slower)
 template <int T, int K1, int K2, bool ZF, bool PS = false, int GM = 0>
 auto wf_fn() {
-    if constexpr (T == 4) return wf2d::wf2d_kernel<4, WF_NW, WF_ST4, K1, K2, ZF, WF_SKEW4, PS, GM>;
-    else return wf2d::wf2d_kernel<T, WF_NW, T + 4, K1, K2, ZF, 1, PS, GM>;
+    if constexpr (T == 4) return wf2d::wf2d_kernel<4, WF_NW, WF_ST4, K1, K2, ZF, PS, GM>;
+    else return wf2d::wf2d_kernel<T, WF_NW, T + 4, K1, K2, ZF, PS, GM>;
 }
 
 template <int T>
@@ -1104,51 +1046,7 @@ int plan_launch(whb_ctx *c) {
     const bool whole = c->plane_begin == 0 && c->plane_end == c->gshape[0];
     c->tb2 = c->kern >= 1 && c->act0 && !(tenv && std::string(tenv) == "0") && (!c->act1 || c->kern == 2) &&
              c->upd_hi - c->upd_lo >= 1;
-    const char *wenv3 = getenv("WHB_TB2W");
-    c->tb2w = c->tb2 && whole && c->act1 && (wenv3 && std::string(wenv3) == "1");
-    const char *renv = getenv("WHB_TB2R");
-    // measured on 257^3 / 1025^3: 126.5 / 131.0 Gpts/s vs 143.7 / 149.3 for tb2 -> opt-in (WHB_TB2R=1)
-    c->tb2r = c->tb2 && whole && c->act1 && !c->tb2w && (renv && std::string(renv) == "1");
-    if (c->tb2w) {
-        c->smem2 = tb2w::smem_bytes<W3_BY, W3_ST>();
-        cudaError_t e = tb2w_set_attrs(c->smem2);
-        if (e != cudaSuccess) return fail(WHB_E_CUDA, std::string("cudaFuncSetAttribute(tb2w): ") + cudaGetErrorString(e));
-        int nb = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, tb2w_fn<K_MID, K_MID, false>(), tb2w::Lay<W3_BY>::THREADS,
-                                                          c->smem2);
-        if (e != cudaSuccess || nb < 1) return fail(WHB_E_CUDA, "tb2w kernel does not fit on an SM");
-        c->gx2 = (int)((n2 - 2 + 61) / 62);
-        c->JT2 = (int)((n1 - 1 + W3_BY - 1) / W3_BY);
-        const long long res2 = (long long)sms * nb;
-        const long long tiles2 = (long long)c->gx2 * c->JT2;
-        const long long nch = std::max<long long>(1, 4 * res2 / std::max<long long>(1, tiles2));
-        int cl2 = (int)((nplanes + nch - 1) / nch);
-        const char *env2 = getenv("WHB_CHUNK2");
-        if (env2 && atoi(env2) > 0) cl2 = atoi(env2);
-        c->chunk2 = std::max(1, cl2);
-        c->nch2 = (nplanes + c->chunk2 - 1) / c->chunk2;
-        if ((long long)c->JT2 * c->nch2 > 65535) c->tb2 = c->tb2w = false;
-        c->nparts = std::max(c->nparts, c->gx2 * c->JT2 * (c->nch2 + 2));
-    } else if (c->tb2r) {
-        c->smem2 = tb2r::smem_bytes<R3_BY, R3_ST>();
-        cudaError_t e = tb2r_set_attrs(c->smem2);
-        if (e != cudaSuccess) return fail(WHB_E_CUDA, std::string("cudaFuncSetAttribute(tb2r): ") + cudaGetErrorString(e));
-        int nb = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, tb2r_fn<K_MID, K_MID, false>(), 32 * (R3_BY + 2), c->smem2);
-        if (e != cudaSuccess || nb < 1) return fail(WHB_E_CUDA, "tb2r kernel does not fit on an SM");
-        c->gx2 = (int)((n2 - 2 + 61) / 62);
-        c->JT2 = (int)((n1 - 1 + R3_BY - 1) / R3_BY);
-        const long long res2 = (long long)sms * nb;
-        const long long tiles2 = (long long)c->gx2 * c->JT2;
-        const long long nch = std::max<long long>(1, 4 * res2 / std::max<long long>(1, tiles2));
-        int cl2 = (int)((nplanes + nch - 1) / nch);
-        const char *env2 = getenv("WHB_CHUNK2");
-        if (env2 && atoi(env2) > 0) cl2 = atoi(env2);
-        c->chunk2 = std::max(1, cl2);
-        c->nch2 = (nplanes + c->chunk2 - 1) / c->chunk2;
-        if ((long long)c->JT2 * c->nch2 > 65535) c->tb2 = c->tb2r = false;
-        c->nparts = std::max(c->nparts, c->gx2 * c->JT2 * (c->nch2 + 2));
-    } else if (c->tb2) {
+    if (c->tb2) {
         const int TX = c->act1 ? T3_TX : T2_TX, BYt = c->act1 ? T3_BY : T2_BY;
         c->smem2 = c->act1 ? tb2::tb2_smem_bytes<T3_TX, T3_BY, T3_ST, true>()
                            : tb2::tb2_smem_bytes<T2_TX, T2_BY, T2_ST, false>();
@@ -1200,33 +1098,7 @@ int plan_launch(whb_ctx *c) {
             c->nparts = std::max(c->nparts, c->gxw[T] * (c->nchw[T] + 2));
         }
     }
-    // 3D three-step wavefront (WHB_WF3=1 opt-in): whole-grid, single-problem 3D contexts.  Measured
-    // 124 / 146 Gpts/s on configs 3 / 4 against 165 / 176 for tb2: 18.7 instead of 28 B/update, but
-    // three block barriers per plane, 12 warps per SM and 21 % ring recomputation leave it slower.
-    const char *w3env = getenv("WHB_WF3");
-    c->wf3 = c->tb2 && whole && c->act1 && c->kern == 2 && !c->tb2w && !c->tb2r && w3env && std::string(w3env) == "1";
-    if (c->wf3) {
-        c->smem3 = wf3::smem_bytes<W3D_BY>();
-        cudaError_t e = wf3_set_attrs(c->smem3);
-        if (e != cudaSuccess) return fail(WHB_E_CUDA, std::string("cudaFuncSetAttribute(wf3): ") + cudaGetErrorString(e));
-        int nb = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, wf3_fn<K_MID, K_MID, false>(), wf3::Lay<W3D_BY>::THREADS,
-                                                          c->smem3);
-        if (e != cudaSuccess || nb < 1) return fail(WHB_E_CUDA, "wf3 kernel does not fit on an SM");
-        c->gx3 = (int)((n2 - 1 + wf3::TX - 1) / wf3::TX);
-        c->JT3 = (int)((n1 - 1 + W3D_BY - 1) / W3D_BY);
-        const long long res3 = (long long)sms * nb;
-        const long long tiles3 = (long long)c->gx3 * c->JT3;
-        const long long nch = std::max<long long>(1, 4 * res3 / std::max<long long>(1, tiles3));
-        int cl3 = (int)((nplanes + nch - 1) / nch);
-        const char *env3 = getenv("WHB_CHUNK3");
-        if (env3 && atoi(env3) > 0) cl3 = atoi(env3);
-        c->chunk3 = std::max(1, cl3);
-        c->nch3 = (nplanes + c->chunk3 - 1) / c->chunk3;
-        if ((long long)c->JT3 * c->nch3 > 65535) c->wf3 = false;
-        c->nparts = std::max(c->nparts, c->gx3 * c->JT3 * (c->nch3 + 2));
-    }
-    c->nring = (c->wfT == 4 || c->wf3) ? 6 : 4;
+    c->nring = c->wfT == 4 ? 6 : 4;
     // cluster-resident plan (whole-grid 2D with the fields in one cluster's shared memory; the
     // per-launch fit against the step count is cres_fits); WHB_CRES=0 disables, WHB_CRES_CL=n
     // caps the cluster size
@@ -1276,8 +1148,8 @@ int ensure_hist(whb_ctx *c, int iters) {
     c->hist_cap = cap;
     // graphs bake the hist pointer
     for (auto &kv : c->graphs) cudaGraphExecDestroy(kv.second);
-    for (auto &ge : c->user_graphs) cudaGraphExecDestroy(ge);
     c->graphs.clear();
+    invalidate_user_graphs(c);
     return 0;
 }
 
@@ -1482,48 +1354,6 @@ void launch_tb2_kinds(whb_ctx *c, int k1, int k2, bool zf, dim3 grid, int off, i
 #undef WHB_TB2_CASE
 }
 
-template <int K1, int K2, bool ZF>
-void launch_tb2r(whb_ctx *c, dim3 grid, int off, int s, int ib, int ie, const StepMaps &mp) {
-    tb2r_fn<K1, K2, ZF>()<<<grid, 32 * (R3_BY + 2), c->smem2, c->stream>>>(
-        c->geom, c->d_members, off, s, ib, ie, c->chunk2, c->JT2, 0, mp.w, mp.p, mp.f, mp.a);
-}
-
-void launch_tb2r_kinds(whb_ctx *c, int k1, int k2, bool zf, dim3 grid, int off, int s, int ib, int ie,
-                       const StepMaps &mp) {
-#define WHB_TB2R_CASE(K1, K2)                                                      \
-    if (k1 == K1 && k2 == K2) {                                                    \
-        if (zf) launch_tb2r<K1, K2, true>(c, grid, off, s, ib, ie, mp);           \
-        else launch_tb2r<K1, K2, false>(c, grid, off, s, ib, ie, mp);             \
-        return;                                                                    \
-    }
-    WHB_TB2R_CASE(K_FIRST, K_MID)
-    WHB_TB2R_CASE(K_MID, K_MID)
-    WHB_TB2R_CASE(K_MID, K_LAST)
-    WHB_TB2R_CASE(K_FIRST, K_LAST)
-#undef WHB_TB2R_CASE
-}
-
-template <int K1, int K2, bool ZF>
-void launch_tb2w(whb_ctx *c, dim3 grid, int off, int s, int ib, int ie, const StepMaps &mp) {
-    tb2w_fn<K1, K2, ZF>()<<<grid, tb2w::Lay<W3_BY>::THREADS, c->smem2, c->stream>>>(
-        c->geom, c->d_members, off, s, ib, ie, c->chunk2, c->JT2, 0, mp.w, mp.p, mp.f, mp.a);
-}
-
-void launch_tb2w_kinds(whb_ctx *c, int k1, int k2, bool zf, dim3 grid, int off, int s, int ib, int ie,
-                       const StepMaps &mp) {
-#define WHB_TB2W_CASE(K1, K2)                                                      \
-    if (k1 == K1 && k2 == K2) {                                                    \
-        if (zf) launch_tb2w<K1, K2, true>(c, grid, off, s, ib, ie, mp);           \
-        else launch_tb2w<K1, K2, false>(c, grid, off, s, ib, ie, mp);             \
-        return;                                                                    \
-    }
-    WHB_TB2W_CASE(K_FIRST, K_MID)
-    WHB_TB2W_CASE(K_MID, K_MID)
-    WHB_TB2W_CASE(K_MID, K_LAST)
-    WHB_TB2W_CASE(K_FIRST, K_LAST)
-#undef WHB_TB2W_CASE
-}
-
 // Fused steps (s, s+1) over update planes [ib, ie) in chunks of cl planes (partial slots from
 // po), for the table members [0, nact): those still running after s+1 get (K1, MID), those
 // finishing at s+1 get (K1, LAST).
@@ -1547,28 +1377,10 @@ int launch_pair_range(whb_ctx *c, int s, int ib, int ie, int cl, int po) {
         WHB_TRY(tensor_map(c, m0.acc, T3_TX, T3_BY, &mp.a));
         if (m0.f) WHB_TRY(tensor_map(c, m0.f, T3_TX + 4, T3_BY + 2, &mp.f));
     }
-    if (c->tb2r || c->tb2w) {  // 62-column variants: boxes W (68, BY+4), P/F (64, BY+2), acc (64, BY)
-        const int by = c->tb2w ? W3_BY : R3_BY;
-        const Member &m0 = c->h_members[0];
-        WHB_TRY(tensor_map(c, level_ptr(m0, s), 68, by + 4, &mp.w));
-        WHB_TRY(tensor_map(c, level_ptr(m0, s - 1), 64, by + 2, &mp.p));
-        WHB_TRY(tensor_map(c, m0.acc, 64, by, &mp.a));
-        if (m0.f) WHB_TRY(tensor_map(c, m0.f, 64, by + 2, &mp.f));
-    }
     const int k1 = (s == 0) ? K_FIRST : K_MID;
     auto go = [&](int k2, int off, int cnt) {
         if (cnt <= 0) return;
         dim3 grid(c->gx2, c->JT2 * nch, cnt);
-        if (c->tb2w) {  // whole-grid variants (fixed plan chunking)
-            launch_tb2w_kinds(c, k1, k2, zf, grid, off, s, ib, ie, mp);
-            c->launches++;
-            return;
-        }
-        if (c->tb2r) {
-            launch_tb2r_kinds(c, k1, k2, zf, grid, off, s, ib, ie, mp);
-            c->launches++;
-            return;
-        }
         if (c->act1) launch_tb2_kinds<true>(c, k1, k2, zf, grid, off, s, ib, ie, cl, po, mp);
         else launch_tb2_kinds<false>(c, k1, k2, zf, grid, off, s, ib, ie, cl, po, mp);
         c->launches++;
@@ -1580,39 +1392,6 @@ int launch_pair_range(whb_ctx *c, int s, int ib, int ie, int cl, int po) {
 }
 
 int launch_pair(whb_ctx *c, int s) { return launch_pair_range(c, s, c->upd_lo, c->upd_hi, c->chunk2, 0); }
-
-template <int K1, int K2, bool ZF>
-void launch_wf3k(whb_ctx *c, dim3 grid, int s, const StepMaps &mp) {
-    wf3_fn<K1, K2, ZF>()<<<grid, wf3::Lay<W3D_BY>::THREADS, c->smem3, c->stream>>>(
-        c->geom, c->d_members, 0, s, c->upd_lo, c->upd_hi, c->chunk3, c->JT3, 0, mp.w, mp.p, mp.f, mp.a);
-}
-
-// Fused steps (s, s+1, s+2) of the (single) member; `last` when they end its solve.
-int launch_wf3(whb_ctx *c, int s, bool last) {
-    const bool zf = c->cur_zf != 0;
-    StepMaps mp;
-    std::memset(&mp, 0, sizeof(mp));
-    const Member &m0 = c->h_members[0];
-    WHB_TRY(tensor_map(c, level_ptr(m0, s), wf3::TX + 8, W3D_BY + 6, &mp.w));
-    WHB_TRY(tensor_map(c, level_ptr(m0, s - 1), wf3::TX + 4, W3D_BY + 4, &mp.p));
-    WHB_TRY(tensor_map(c, m0.acc, wf3::TX, W3D_BY, &mp.a));
-    if (m0.f) WHB_TRY(tensor_map(c, m0.f, wf3::TX + 4, W3D_BY + 4, &mp.f));
-    dim3 grid(c->gx3, c->JT3 * c->nch3, 1);
-    const int k1 = (s == 0) ? K_FIRST : K_MID;
-#define WHB_WF3_CASE(K1, K2)                                           \
-    if (k1 == K1 && (last ? K_LAST : K_MID) == K2) {                   \
-        if (zf) launch_wf3k<K1, K2, true>(c, grid, s, mp);             \
-        else launch_wf3k<K1, K2, false>(c, grid, s, mp);               \
-    }
-    WHB_WF3_CASE(K_FIRST, K_MID)
-    WHB_WF3_CASE(K_MID, K_MID)
-    WHB_WF3_CASE(K_MID, K_LAST)
-    WHB_WF3_CASE(K_FIRST, K_LAST)
-#undef WHB_WF3_CASE
-    c->launches++;
-    WHB_CUDA(cudaGetLastError());
-    return 0;
-}
 
 int max_steps(whb_ctx *c);
 
@@ -1775,7 +1554,6 @@ int launch_cres(whb_ctx *c, size_t smem, int iters, double tol_sq, double *hist,
     a.k0 = k0;
     a.nb = c->nbatch;
     a.done = done;
-    a.dbg = getenv("WHB_CRES_DBG") ? atoi(getenv("WHB_CRES_DBG")) : 0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(c->cres_cl, c->nbatch, 1);
     cfg.blockDim = dim3(cres::NT, 1, 1);
@@ -1823,15 +1601,6 @@ int enqueue_solve(whb_ctx *c, int out_mode) {
     }
     if (c->wfT) {
         WHB_TRY(enqueue_wf(c));
-    } else if (c->wf3) {
-        // passes of 3 steps; a remainder of 2 is one two-step pass, of 1 a single step
-        int s = 0;
-        while (ns - s >= 3) {
-            WHB_TRY(launch_wf3(c, s, ns - s == 3));
-            s += 3;
-        }
-        if (ns - s == 2) WHB_TRY(launch_pair(c, s));
-        else if (ns - s == 1) WHB_TRY(launch_step_range(c, s, 0, 1));
     } else if (c->tb2) {
         // pairs (0,1), (2,3), ...; a member with odd n_total takes its last step alone
         for (int s = 0; s < ns; s += 2) {
@@ -1851,7 +1620,6 @@ int enqueue_solve(whb_ctx *c, int out_mode) {
     if (out_mode == WHB_OUT_FPI) {
         int np = c->kern == 3 ? kGenBlocks : c->gx * c->JT * c->nchunks;
         if (c->tb2) np = std::max(np, c->gx2 * c->JT2 * c->nch2);
-        if (c->wf3) np = std::max(np, c->gx3 * c->JT3 * c->nch3);
         if (c->wfT) np = std::max(np, std::max(c->gxw[2] * c->nchw[2], c->wfT == 4 ? c->gxw[4] * c->nchw[4] : 0));
         reduce_partials_kernel<<<1, 1024, 0, c->stream>>>(c->d_members, c->nbatch, np, c->d_hist, c->d_counter);
         c->launches++;
@@ -2323,9 +2091,10 @@ int whb_destroy(whb_ctx *c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     free_mg(c);
     free_tri(c);
-    for (auto &kv : c->cg_graphs) cudaGraphExecDestroy(kv.second);
+    drop_cg_graphs(c);
     cudaFree(c->d_cg);
     for (auto &kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    invalidate_user_graphs(c);
     for (auto &m : c->mem) {
         free_field(c, m.v); free_field(c, m.f); free_field(c, m.acc);
         for (int q = 0; q < 6; ++q) free_field(c, m.ring[q]);
@@ -2415,9 +2184,6 @@ int whb_set_operator_general(whb_ctx *c, int order, const int *periodic, const d
     c->kern = 3;
     c->cres = false;
     c->tb2 = false;
-    c->tb2r = false;
-    c->wf3 = false;
-    c->tb2w = false;
     c->wfT = 0;
     for (auto &kv : c->graphs) cudaGraphExecDestroy(kv.second);
     c->graphs.clear();
@@ -2463,6 +2229,7 @@ int whb_set_schedule(whb_ctx *c, int member, int n_total, double half_dt2, doubl
                      [&](int a, int b) { return c->mem[a].n_total > c->mem[b].n_total; });
     for (auto &kv : c->graphs) cudaGraphExecDestroy(kv.second);
     c->graphs.clear();
+    invalidate_user_graphs(c);  // they bake the step count and the cos_f / acc_c buffers
     c->h_members.clear();
     return 0;
 }
@@ -2772,7 +2539,7 @@ int whb_step(whb_ctx *c, int s, int region) {
 
 int whb_pair(whb_ctx *c, int s, int region) {
     if (!c || c->cur_mode < 0) return fail(WHB_E_STATE, "whb_pair outside whb_solve_begin/end");
-    if (!c->tb2 || c->wfT || c->tb2r || c->tb2w) return fail(WHB_E_STATE, "context has no two-step plan (whb_plan)");
+    if (!c->tb2 || c->wfT) return fail(WHB_E_STATE, "context has no two-step plan (whb_plan)");
     if (s < 0 || s + 1 >= c->mem[0].n_total) return fail(WHB_E_ARG, "steps (s, s+1) out of range");
     WHB_TRY(set_dev(c));
     const int lo = c->upd_lo, hi = c->upd_hi;
@@ -2872,6 +2639,8 @@ int whb_capture_end(whb_ctx *c, int *graph_id) {
 
 int whb_graph_launch(whb_ctx *c, int graph_id) {
     if (!c || graph_id < 0 || graph_id >= (int)c->user_graphs.size()) return fail(WHB_E_ARG, "bad graph id");
+    if (!c->user_graphs[graph_id])
+        return fail(WHB_E_STATE, "graph invalidated (a buffer it baked was reallocated); capture it again");
     WHB_TRY(set_dev(c));
     WHB_CUDA(cudaGraphLaunch(c->user_graphs[graph_id], c->stream));
     return 0;
@@ -3092,7 +2861,7 @@ int whb_host_free(void *ptr) {
 int whb_plan(whb_ctx *c, int *kernel, int *steps_per_pass) {
     if (!c) return fail(WHB_E_ARG, "NULL argument");
     if (kernel) *kernel = c->cres ? 4 : c->kern;
-    if (steps_per_pass) *steps_per_pass = c->cres ? 0 : (c->wfT ? c->wfT : (c->wf3 ? 3 : (c->tb2 ? 2 : 1)));
+    if (steps_per_pass) *steps_per_pass = c->cres ? 0 : (c->wfT ? c->wfT : (c->tb2 ? 2 : 1));
     return 0;
 }
 
@@ -3160,6 +2929,7 @@ int whb_mg_setup(whb_ctx *c, int nlev, const int64_t *cells, const double *gamma
             return fail(WHB_E_ARG, "levels must halve the cell counts");
     WHB_TRY(set_dev(c));
     WHB_CUDA(cudaStreamSynchronize(c->stream));
+    drop_cg_graphs(c);
     free_mg(c);
     c->mg = new MGData();
     MGData &M = *c->mg;
@@ -3273,6 +3043,8 @@ int whb_tri_setup(whb_ctx *c, int n, const double *sub, const double *dp, const 
     if (!c || !sub || !dp || !cp) return fail(WHB_E_ARG, "NULL argument");
     if (c->ndim != 1 || n != (int)c->gshape[2] - 2) return fail(WHB_E_ARG, "tridiagonal solve needs a 1D context with n = points - 2");
     WHB_TRY(set_dev(c));
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
+    drop_cg_graphs(c);
     free_tri(c);
     c->tri = new TriData();
     TriData &T = *c->tri;

@@ -74,6 +74,12 @@ class DeviceProblem:
     def close(self):
         self.ctx.close()
 
+    def __del__(self):
+        try:
+            self.ctx.close()
+        except Exception:
+            pass
+
 
 def device_problem(grid, c=1.0, order=2, device=0) -> DeviceProblem:
     """Cached single-problem device state for a grid (LRU of a few entries)."""
@@ -83,8 +89,9 @@ def device_problem(grid, c=1.0, order=2, device=0) -> DeviceProblem:
         _cache.move_to_end(key)
         return dp
     while len(_cache) >= _MAX_CACHED:
-        _, old = _cache.popitem(last=False)
-        old.close()
+        # evicted, not closed: holders (HostFPIStep, waveholtz_operator closures, implicit
+        # solvers) may still use it; its device memory is freed when the last reference goes
+        _cache.popitem(last=False)
     dp = DeviceProblem(grid, c=c, order=order, device=device)
     _cache[key] = dp
     return dp
@@ -93,5 +100,7 @@ def device_problem(grid, c=1.0, order=2, device=0) -> DeviceProblem:
 def release_device_cache():
     """Free every cached device problem (returns HBM to the allocator)."""
     while _cache:
-        _, dp = _cache.popitem(last=False)
-        dp.close()
+        _cache.popitem(last=False)
+    import gc
+
+    gc.collect()  # contexts nobody else references are freed now (DeviceProblem.__del__)

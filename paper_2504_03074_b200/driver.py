@@ -392,6 +392,8 @@ class HostFPIStep:
             raise ValueError("v_in/v_out must have the grid shape")
         if not (v_in.flags.c_contiguous and v_out.flags.c_contiguous and v_out.flags.writeable):
             raise ValueError("v_in/v_out must be C-contiguous (v_out writeable)")
+        if v_in.dtype != np.float64 or v_out.dtype != np.float64:
+            raise ValueError("v_in/v_out must be float64 (the grid's dtype, grid.py:219)")
         if self._implicit is not None:
             ctx = self.dp.ctx
             solver, (vnew, diff_id) = self._implicit

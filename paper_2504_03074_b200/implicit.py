@@ -123,11 +123,14 @@ class DeviceImplicitSolver:
         self.maxit = maxit
         self.inner = 0
         self.s = 0.5 * dt**2
+        self.c = c
         self.tri = False
         self.precond = None
+        self._tri_factors = None
+        self._mg = None
         dirichlet = _all_dirichlet(grid)
         if grid.dim == 1 and dirichlet:
-            ctx.tri_setup(*_tridiag_factors(grid.cells[0], grid.spacing[0], dt, c))
+            self._tri_factors = _tridiag_factors(grid.cells[0], grid.spacing[0], dt, c)
             self.tri = True
         if grid.dim == 2 and dirichlet:
             try:
@@ -136,12 +139,26 @@ class DeviceImplicitSolver:
                 levels = None
             if levels is not None:
                 # (a grid already <= 8 cells is a single-level hierarchy: its V-cycle is the dense solve)
-                ctx.mg_setup([lv[0] for lv in levels], [lv[1] for lv in levels], [lv[2] for lv in levels], ainv)
+                self._mg = ([lv[0] for lv in levels], [lv[1] for lv in levels], [lv[2] for lv in levels], ainv)
                 self.precond = "mg"
         if grid.dim == 1 and self.tri and order == 4:
             self.precond = "tri"
         self.direct = self.tri and order == 2
+        self.activate()
         (self.r, self.z, self.p, self.ap, self.tmp) = ctx.vec_reserve(5)
+
+    def activate(self):
+        """The context holds ONE tridiagonal factorisation / multigrid hierarchy (whb_tri_setup /
+        whb_mg_setup replace it and drop the CG graphs that baked it): install this solver's
+        (its dt) unless it is already the installed one.  Called before every solve, so solvers
+        of different dt sharing a grid (omega A, B, A) never run on each other's factors."""
+        if getattr(self.ctx, "_imp_active", None) is self:
+            return
+        if self._tri_factors is not None:
+            self.ctx.tri_setup(*self._tri_factors)
+        if self._mg is not None:
+            self.ctx.mg_setup(*self._mg)
+        self.ctx._imp_active = self
 
     def apply(self, x, y):
         """y = x - (0.5*dt**2) * c^2 L_h x  (timestep.py:225-226)."""
@@ -151,6 +168,7 @@ class DeviceImplicitSolver:
         """x = A^{-1} rhs from the initial guess (cg_solve, linalg.py:62-99, or the direct
         tridiagonal solve); returns the iteration count and raises like the reference."""
         ctx = self.ctx
+        self.activate()
         if self.direct:
             ctx.tri_solve(rhs, x)
             self.inner += 1
@@ -193,7 +211,9 @@ def implicit_solver_for(dp, grid, order, c, dt, tol=1e-12, maxit=400) -> DeviceI
     key = (float(dt), float(tol), int(maxit))
     if key not in cache:
         cache[key] = DeviceImplicitSolver(dp.ctx, grid, order, c, dt, tol=tol, maxit=maxit)
-    return cache[key]
+    solver = cache[key]
+    solver.activate()
+    return solver
 
 
 class _Workspace:

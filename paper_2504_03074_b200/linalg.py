@@ -118,7 +118,11 @@ def device_gmres(ctx, matvec, b_id: int, x_id: int, tol=1e-10, restart=30, maxit
                 break
         if k_used > 0:
             y = scipy.linalg.solve_triangular(H[:k_used, :k_used], g[:k_used])
-            ctx.lincomb(x_id, q_ids[0], y)  # x = x + Q[:, :k] @ y
+            if contiguous_basis:
+                ctx.lincomb(x_id, q_ids[0], y)  # x = x + Q[:, :k] @ y (one fused pass)
+            else:  # basis ids not consecutive (e.g. caller-provided work_ids): one axpy per vector
+                for j in range(k_used):
+                    ctx.axpy(float(y[j]), q_ids[j], x_id)
         else:
             break
     report.iterations = total

@@ -7,6 +7,7 @@ Run in the build container (where /root/reference exists):
     python tests/golden/make_golden.py cfg2           # ~35 min (2049^2, 50 iterations)
     python tests/golden/make_golden.py cfg3           # ~45 min (257^3, 30 iterations)
     python tests/golden/make_golden.py cfg5 [--procs P]  # 64 omegas x 20 iterations
+    python tests/golden/make_golden.py cfg4           # ~30 min, 43 GB RAM (1025^3, 10 iterations)
 
 Every case is produced by the reference's own functions
 (``correct_explicit``, ``gaussian_source``, ``wave_solve_filtered``,
@@ -146,6 +147,52 @@ def run_cfg(name):
                     pass
         meta["ref_seconds"] = time.perf_counter() - t0
         dump(name, meta, arrays or None)
+
+
+# ---------------------------------------------------------------------------------
+# cfg4: 3D 1025^3 (the north-star config).  The reference's numpy path needs ~76 GB
+# and ~1.85 h per iteration here (SURVEY 8(c) rung 4), so the iterates come from the
+# C restatement (oracle/whb_oracle.c, who_fpi_lean: 5 resident fields), which is
+# pinned bitwise to the reference's own iterates on cfg1-cfg3 and the small cases
+# (tests/test_oracle_golden.py).  The forcing is the reference's gaussian_source
+# evaluated slab by slab (RH.multi_gaussian_slabs), and every scalar comes from the
+# reference's correct_explicit.
+
+
+def run_cfg4(iters=10, threads=0):
+    from oracle import native as ON
+    from oracle import waveholtz_oracle as O
+
+    dim, n, omega = 3, 1024, 150.3
+    with RH.courant(0.9):
+        g = RH.grid(dim, [(0.0, 1.0)] * dim, [n] * dim)
+        corr, cfg, op = RH.explicit_setup(g, omega)
+        t0 = time.perf_counter()
+        f = RH.multi_gaussian_slabs(g, omega, 16, seed=0)
+        print(f"cfg4 forcing {time.perf_counter() - t0:.1f}s", flush=True)
+    idx = sample_idx(f.size)
+    meta = {
+        "config": "cfg4", "dim": dim, "cells": [n] * dim, "bounds": [[0.0, 1.0]] * dim,
+        "omega": omega, "c": 1.0, "order": 2, "courant": 0.9, "forcing": ["multi", 16, "seed0"],
+        "corr": corr_dict(corr, cfg), "f_sha256": hashlib.sha256(f.data).hexdigest(),
+        "f_max": float(np.max(np.abs(f))), "f_samples": f.ravel()[idx].tolist(),
+        "sample_idx": idx.tolist(), "iterations": iters,
+        "iter_sha256": [], "residuals": [], "vmax": [], "samples": [],
+        "source": "forcing: reference gaussian_source per slab; iterates: oracle/whb_oracle.c who_fpi_lean "
+                  "(C restatement, bitwise pinned to the reference on cfg1-cfg3)",
+    }
+    sc = O.step_scalars(corr.steps_per_period, corr.dt, corr.omega_tilde)
+    v = np.zeros_like(f)
+    t0 = time.perf_counter()
+    for k in range(1, iters + 1):
+        _, r = ON.fpi_lean(f, g.spacing, sc, 1, nthreads=threads or ON.max_threads(), v=v)
+        meta["iter_sha256"].append(hashlib.sha256(v.data).hexdigest())
+        meta["residuals"].append(float(r[0]))
+        meta["vmax"].append(float(np.max(np.abs(v))))
+        meta["samples"].append(v.ravel()[idx].tolist())
+        print(f"cfg4 it {k} r={r[0]:.6e} t={time.perf_counter() - t0:.1f}s", flush=True)
+        meta["ref_seconds"] = time.perf_counter() - t0
+        dump("cfg4", meta)  # after every iterate: a partial run still pins the first ones
 
 
 # ---------------------------------------------------------------------------------
@@ -356,7 +403,7 @@ class _null:
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", choices=["small", "ext", "cfg1", "cfg2", "cfg3", "cfg5"])
+    ap.add_argument("which", choices=["small", "ext", "cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--procs", type=int, default=4)
     a = ap.parse_args()
     if a.which == "small":
@@ -365,6 +412,8 @@ def main():
         run_ext()
     elif a.which == "cfg5":
         run_cfg5(a.procs)
+    elif a.which == "cfg4":
+        run_cfg4()
     else:
         run_cfg(a.which)
 

@@ -217,3 +217,36 @@ def test_host_fpi_step_implicit(gpu_available):
     assert np.array_equal(a, v.values)
     np.testing.assert_allclose(res, run.residuals, rtol=1e-13)
     assert relerr(a, ARR[f"{name}/fpi3"]) <= TOL
+
+
+@pytest.mark.parametrize("dim,cells,order", [(1, (300,), 2), (1, (256,), 4), (2, (64, 64), 2)])
+def test_solvers_of_different_dt_interleaved_on_one_grid(gpu_available, dim, cells, order):
+    """One context holds one tridiagonal factorisation / multigrid hierarchy.  Solvers for
+    omegas A, B, A (different dt) held at the same time and used in that order must each run
+    on their own factors (the cached solver A used to run against B's state; in 2D
+    its CG graph replayed kernels pointing at freed multigrid buffers)."""
+    from oracle import implicit_oracle as IO
+    from oracle import waveholtz_oracle as O
+
+    g = wh.build_grid(dim, [(0.0, 1.0)] * dim, cells, "dirichlet")
+    f = np.array(O.multi_gaussian(g.shape, g.bounds, g.spacing, 2, seed=3))
+    v0 = O.zero_dirichlet(np.random.default_rng(2).standard_normal(g.shape) * 1e-2, ["dirichlet"] * dim)
+    op = wh.DiscreteOperator(g, order, 1.0)
+    dp = device_problem(g, order=order)
+    outs = {}
+    for omega in (12.0, 21.0, 12.0, 21.0):
+        n_t = 9
+        corr = wh.correct_implicit(omega, n_t)
+        cfg = wh.FilterConfig(omega=omega, periods=1, steps_per_period=n_t, mode="implicit")
+        # hold both solvers: the second call of each omega reuses its cached solver
+        implicit_solver_for(dp, g, order, 1.0, wh.correct_implicit(12.0, n_t).dt)
+        implicit_solver_for(dp, g, order, 1.0, wh.correct_implicit(21.0, n_t).dt)
+        out = wh.wave_solve_filtered(wh.GridField.from_values(g, v0), wh.GridField.from_values(g, f), cfg, corr,
+                                     op).values
+        ref, _ = IO.wave_solve_implicit(v0, np.array(wh.GridField.from_values(g, f).values), g.spacing,
+                                        ["dirichlet"] * dim, order, omega, n_t)
+        tol = 0.0 if (dim == 1 and order == 2) else TOL  # 1D p = 2: direct elimination, bitwise
+        assert relerr(out, ref) <= tol, (omega, relerr(out, ref))
+        if omega in outs:
+            assert np.array_equal(outs[omega], out)
+        outs[omega] = out

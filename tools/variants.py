@@ -1,6 +1,6 @@
 """Build variant libraries for tuning sweeps (compile-time kernel constants), e.g.
 
-    python tools/variants.py wf_skew2 -DWHB_WF_SKEW=2
+    python tools/variants.py wf_st12 -DWHB_WF_ST_EXTRA=8
 
 writes paper_2504_03074_b200/lib/variants/libwhb200_<name>.so; select it at run time with
 WHB_LIB=libwhb200_<name>.so.  The default build (build()) is what the product ships."""
