@@ -1,32 +1,45 @@
 """Benchmark: explicit WaveHoltz fixed-point iterations on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4] [--impl ours|reference]
 
 A "step" is one WaveHoltz fixed-point iteration v <- W(v, f) (N_t fused
 leapfrog+filter steps over the whole grid + the residual reduction).  The
-default workload is BASELINE config 2 (2D 2049^2, omega = 100.5, 8 seeded
-Gaussians, CFL 0.9, N_t = 202) and the default K = 50 is that config's full
-iteration count: the timed region is the complete 50-iteration solve from
-v = 0.  Inputs are resident in HBM when timing starts; an L2 flush (256 MiB
-scratch write) runs before every timed iteration, outside the timed span.
+default workload, at every N, is BASELINE config 4 -- the north-star config:
+3D 1025^3 fp64, omega = 150.3, 16 seeded Gaussians, CFL 0.9, N_t = 83 -- and
+the default K = 10 is that config's iteration count (the timed region is the
+solve from v = 0).  N = 1 runs the whole grid on one GPU; N > 1 splits it into
+z-slabs (axis-0 plane ranges, one per GPU, halo exchange overlapped with the
+interior planes, strong scaling).  Inputs are resident in HBM when timing
+starts; the 1025^3 working set (7 x 8.6 GB) is far above L2 (an L2 flush still
+runs before every timed iteration on one GPU, outside the timed span).
 
 value      = grid-point updates / s (N stored points x N_t x K / device time), Gpts/s
-e2e        = the same through HostFPIStep (host pinned v in, v_new out, every step)
-roofline   = fused step kernel: 48 algorithmic bytes per point update / average
-             launch duration (CUDA events on the launching stream) vs measured HBM peak
+e2e        = the same through the reference-facing C-ABI call with HOST buffers:
+             whb_iterate_host (paper_2504_03074_b200.HostFPIStep), v copied in from pinned
+             host memory and v_new copied out every step (the reference's _iterate loop body,
+             driver.py:222-226); e2e_solve = whb_upload(f) + whb_fpi(K) + whb_download(v)
+             (the fpi_solve call: f in once, residual out every step, v out once)
+roofline   = the dominant (multi-step) kernel: bytes per launch / average launch duration
+             (CUDA events on the launching stream) against the measured HBM peak.  ``frac``
+             uses the kernel's DRAM bytes per launch from the ncu capture of THIS build
+             (profiles/traffic.json, matched by the library's sha256) and falls back to the
+             kernel's compulsory bytes (56/T per update for a T-step pass) when no capture of
+             this build exists; ``frac_48B`` is SURVEY 8(d)'s 48 B/update figure (> 1 for
+             temporally blocked kernels by construction).
 cpu_baseline = numpy restatement of the reference (1 core), bounded sample
 --impl reference: the C OpenMP restatement of the reference on all host cores
              (the reference is pure numpy; oracle/ holds its bitwise restatement)
 
---workload imp2: the implicit (trapezoidal) path of SURVEY 8(f) rank 4 — 2D 2049^2,
+--gpus N without torchrun: bench.py re-launches itself through torch.distributed.run
+(one process per GPU, 127.0.0.1 rendezvous); rank 0 prints the line.
+
+--workload imp2: the implicit (trapezoidal) path of SURVEY 8(f) rank 4 -- 2D 2049^2,
 omega = 50.5, N_t = 20, 8 seeded Gaussians; each step is one implicit WaveHoltz
 iteration (20 implicit steps, each a multigrid-preconditioned CG solve).
 
-N > 1 (torchrun): configs 1/2 — every rank solves its own copy (independent
-problems, no data-path collective, "scaling": "weak"); config 5 — the 64
-frequencies are LPT-sharded across ranks ("strong"); configs 3/4 — z-slab
-decomposition with NCCL halo exchange ("strong", --decomp replicas for
-independent copies).  Time is the max over ranks.
+N > 1: configs 3/4 -- z-slabs ("strong"; --decomp replicas for independent copies);
+config 5 -- the 64 frequencies LPT-sharded across ranks ("strong"); configs 1/2 --
+every rank solves its own copy ("weak").  Time is the max over ranks.
 """
 
 from __future__ import annotations
@@ -181,7 +194,7 @@ def build_workload(name):
     if forcing[0] == "single":
         f = wh.gaussian_source(g, omega, forcing[1], forcing[2], forcing[3])
     else:
-        f = wh.multi_gaussian_source(g, omega, forcing[1], seed=0, slab_planes=64 if dim == 3 else 0)
+        f = wh.multi_gaussian_source(g, omega, forcing[1], seed=0, slab_planes=16 if dim == 3 else 64)
     corr = wh.correct_explicit(omega, g, 2, 1.0)
     cfg = wh.FilterConfig(omega=omega, periods=1, steps_per_period=corr.steps_per_period, mode="explicit")
     return g, f, corr, cfg, iters
@@ -194,6 +207,41 @@ def forcing_desc(name):
     if forcing[0] == "single":
         return f"{forcing[1]}*exp(-{forcing[2]}|x-{forcing[3]}|^2)"
     return f"sum of {forcing[1]} Gaussians, amp U(-100,100), centre U(0.1,0.9)^{dim}, width U(100,1000), seed 0"
+
+
+def config_for(name, iterations, ws, decomp="slab", halo="nccl", g=None, cfg=None, n_t=None):
+    """The workload description both arms print (identical dicts: same_config)."""
+    if name == "cfg5":
+        desc = {"workload": "cfg5", "grid": [1025, 1025], "omegas": "np.linspace(10.3, 200.3, 64)",
+                "N_t_sum": 10522, "iterations": iterations, "cfl": 0.9, "forcing": forcing_desc(name),
+                "parallelism": (f"frequencies LPT-sharded over {ws} GPUs (batch.lpt_shard)" if ws > 1
+                                else "single GPU, 64 frequencies batched"),
+                "l2": "flushed before every timed iteration (256 MiB write, outside the timed span)"}
+        return desc
+    dim, n, omega, forcing, _ = WORKLOADS[name]
+    if ws > 1 and name in ("cfg3", "cfg4") and decomp == "slab":
+        par = (f"z-slab decomposition over {ws} GPUs (slab_ranges: contiguous axis-0 plane ranges), "
+               + ("peer-memory halo exchange (CUDA IPC copies on a comm stream + stream flags)" if halo == "peer"
+                  else "NCCL send/recv halo exchange overlapped with the interior planes"))
+    elif ws > 1:
+        par = f"independent replicas x{ws}"
+    else:
+        par = "single GPU"
+    l2 = ("working set (7 fields x 8.6 GB) far above L2; flushed before every timed iteration anyway"
+          if name == "cfg4" else "flushed before every timed iteration (256 MiB write, outside the timed span)")
+    return {"workload": name, "grid": [n + 1] * dim, "omega": omega, "N_t": n_t, "iterations": iterations,
+            "cfl": 0.9, "forcing": forcing_desc(name), "parallelism": par, "l2": l2}
+
+
+def lib_sha16():
+    """sha256 (16 hex digits) of the CUDA library this process runs (the build being measured)."""
+    from paper_2504_03074_b200 import _build
+
+    try:
+        with open(_build.LIB, "rb") as fh:
+            return hashlib.sha256(fh.read()).hexdigest()[:16]
+    except OSError:
+        return None
 
 
 # ------------------------------------------------------------------------------------------
@@ -231,11 +279,17 @@ def cpu_baseline_numpy(g, f, corr, target_s=12.0):
 
 
 def load_traffic(workload):
+    """ncu DRAM bytes per launch of the workload's dominant kernel, only if captured from the
+    library this process loaded (profiles/traffic.json "lib_sha16"); else None."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(p):
-        return None
+        return None, "no profiles/traffic.json"
     d = json.load(open(p)).get(workload)
-    return None if d is None else d.get("bytes_per_launch")
+    if d is None:
+        return None, f"no ncu capture for {workload}"
+    if d.get("lib_sha16") != lib_sha16():
+        return None, f"ncu capture is of another build ({d.get('lib_sha16')})"
+    return d.get("bytes_per_launch"), d.get("source")
 
 
 class SingleRun:
@@ -257,8 +311,8 @@ class SingleRun:
         self.npts = g.size
         self.units_per_step = self.npts * self.n_t
         self.members = 1
-        self.f_sha = hashlib.sha256(np.ascontiguousarray(f.values).tobytes()).hexdigest()
-        self.desc = {"grid": list(g.shape), "omega": cfg.omega, "N_t": self.n_t}
+        self.n_t_config = self.n_t
+        self.f_sha = hashlib.sha256(np.ascontiguousarray(f.values).data).hexdigest()
 
     def reset(self):
         from paper_2504_03074_b200 import _native
@@ -271,7 +325,7 @@ class SingleRun:
         import paper_2504_03074_b200 as wh
         from paper_2504_03074_b200 import _native
 
-        stepper = wh.HostFPIStep(self.prob, self.cfg)
+        stepper = wh.HostFPIStep(self.prob, self.cfg, device_state=self.dp)
         bufs = [_native.PinnedBuffer(self.g.shape), _native.PinnedBuffer(self.g.shape)]
         bufs[0].array[...] = 0.0
         for i in range(W):
@@ -288,6 +342,30 @@ class SingleRun:
             b.free()
         return te, {"h2d_bytes_per_step": self.npts * 8, "d2h_bytes_per_step": self.npts * 8 + 8,
                     "api": "paper_2504_03074_b200.HostFPIStep (C ABI whb_iterate_host), pinned host buffers"}
+
+    def e2e_solve(self, K, dist):
+        """The fpi_solve call through the C ABI with host buffers: f copied in from pinned memory,
+        K device-resident iterations, the residual history and v copied out."""
+        import torch
+
+        from paper_2504_03074_b200 import _native
+
+        fb, vb = _native.PinnedBuffer(self.g.shape), _native.PinnedBuffer(self.g.shape)
+        fb.array[...] = self.f.values
+        barrier(dist)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        self.ctx.upload(_native.F, fb.array)
+        self.ctx.zero(_native.V)
+        rs = self.ctx.fpi(K)
+        self.ctx.download(_native.V, out=vb.array)
+        te = time.perf_counter() - t0
+        assert rs.shape[0] == K
+        fb.free()
+        vb.free()
+        return te, {"h2d_bytes_per_step": self.npts * 8 / K, "d2h_bytes_per_step": self.npts * 8 / K + 8,
+                    "api": "C ABI whb_upload(F) + whb_fpi(K) + whb_download(V), pinned host buffers (f in "
+                           "once, v out once, the K residuals read at the end)"}
 
 
 class BatchRun:
@@ -311,6 +389,7 @@ class BatchRun:
         self.members = len(mine)
         self.units_per_step = self.solver.updates_per_iteration
         self.n_t = sum(self.solver.steps)
+        self.n_t_config = None
         self.f_sha = hashlib.sha256(np.ascontiguousarray(f.values).tobytes()).hexdigest()
         self.desc = {"grid": list(g.shape), "omegas": "np.linspace(10.3, 200.3, 64)", "N_t_sum_rank0": self.n_t,
                      "members_rank0": self.members, "sharding": "LPT over N_t (batch.lpt_shard)"}
@@ -353,43 +432,65 @@ class BatchRun:
 
 
 def run_slab(args, dist, ws, rank, local):
-    """Configs 3/4 at N > 1: one z-slab per GPU (slab.SlabFPI, NCCL halo exchange
-    overlapped with the interior planes).  Strong scaling: the grid is fixed."""
-    import torch
-
+    """Configs 3/4 at N > 1: one z-slab per GPU (slab.SlabFPI; halo exchange overlapped with the
+    interior planes).  Strong scaling: the grid is fixed.  --emulate-cpu runs the same driver with
+    the numpy stand-in shard over gloo (CPU test of the launcher; the numbers mean nothing)."""
     from paper_2504_03074_b200 import _native
-    from paper_2504_03074_b200.slab import DeviceShard, PeerHalo, SlabFPI, TorchHalo, slab_ranges
+    from paper_2504_03074_b200.slab import PeerHalo, SlabFPI, TorchHalo, slab_ranges
 
     g, f, corr, cfg, _ = build_workload(args.workload)
     rng = slab_ranges(g.shape[0], ws)[rank]
-    shard = DeviceShard(g, rng, device=local)
-    halo = PeerHalo.from_dist(shard, dist, rank, ws) if args.halo == "peer" else TorchHalo(dist, rank, ws)
+    emulate = args.emulate_cpu
+    if emulate:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from slab_numpy import NumpyShard
+
+        shard = NumpyShard(g, rng)
+        halo = TorchHalo(dist, rank, ws)
+    else:
+        import torch
+
+        from paper_2504_03074_b200.slab import DeviceShard
+
+        shard = DeviceShard(g, rng, device=local)
+        halo = PeerHalo.from_dist(shard, dist, rank, ws) if args.halo == "peer" else TorchHalo(dist, rank, ws)
     solver = SlabFPI(shard, halo, corr, cfg, f, graph=args.halo == "peer")
     n_t = solver.shard.n_total
     K, W = args.steps, args.warmup
     for _ in range(W):
         solver.iterate()
     solver.reset()
-    shard.synchronize()
+    if not emulate:
+        shard.synchronize()
     barrier(dist)
-    sampler = ClockSampler(local).start()
-    l0 = shard.ctx.launch_count()
-    stream = torch.cuda.ExternalStream(shard.ctx.stream_ptr(), device=f"cuda:{local}")
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    res = [solver.iterate() for _ in range(K)]
-    e1.record(stream)
-    e1.synchronize()
-    clocks = sampler.stop()
-    launches = shard.ctx.launch_count() - l0
-    dev_s = max_over_ranks(dist, e0.elapsed_time(e1) / 1e3)
+    sampler = ClockSampler(local).start() if not emulate else None
+    if emulate:
+        t0 = time.perf_counter()
+        res = [solver.iterate() for _ in range(K)]
+        dev_s = max_over_ranks(dist, time.perf_counter() - t0)
+        clocks, launches = None, 0
+    else:
+        l0 = shard.ctx.launch_count()
+        stream = torch.cuda.ExternalStream(shard.ctx.stream_ptr(), device=f"cuda:{local}")
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res = [solver.iterate() for _ in range(K)]
+        e1.record(stream)
+        e1.synchronize()
+        clocks = sampler.stop()
+        launches = shard.ctx.launch_count() - l0
+        dev_s = max_over_ranks(dist, e0.elapsed_time(e1) / 1e3)
     units = g.size * n_t * K
     value = units / dev_s / 1e9
     peak, peak_src = peaks()
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not emulate:
+        # the reference-facing call with host buffers, every step: each rank copies its owned
+        # planes of v in from pinned memory, runs one slab iteration, copies v_new out
         host = _native.PinnedBuffer(shard.ctx.local_shape)
         host.array[...] = 0.0
+        solver.reset()
+        shard.synchronize()
         barrier(dist)
         t0 = time.perf_counter()
         for _ in range(K):
@@ -398,30 +499,31 @@ def run_slab(args, dist, ws, rank, local):
             shard.ctx.download(_native.V, out=host.array)
         te = max_over_ranks(dist, time.perf_counter() - t0)
         e2e = {"value": units / te / 1e9, "unit": "Gpts/s", "h2d_bytes_per_step": g.size * 8,
-               "d2h_bytes_per_step": g.size * 8 + 8,
-               "api": "slab.SlabFPI with per-rank whb_upload/whb_download of the owned planes (pinned)"}
+               "d2h_bytes_per_step": g.size * 8 + 8 * ws, "iters_per_s": K / te,
+               "api": "slab.SlabFPI with per-rank whb_upload / whb_download of the owned planes (pinned)"}
         host.free()
     if rank == 0:
+        own_bpu = 56.0 / shard.steps_per_pass if shard.steps_per_pass > 1 else float(BYTES_PER_UPDATE)
+        per_gpu = units / ws / dev_s
         line = {
             "metric": METRIC, "value": value, "unit": "Gpts/s", "n_gpus": ws, "steps": K, "warmup": W,
             "ms_per_step": dev_s * 1e3 / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic (BASELINE forcing recipe, SURVEY 8(d))",
-            "config": {"workload": args.workload, "grid": list(g.shape), "omega": cfg.omega, "N_t": n_t,
-                       "iterations": K, "cfl": 0.9, "forcing": forcing_desc(args.workload),
-                       "parallelism": f"z-slab decomposition over {ws} GPUs, " + (
-                           "peer-memory halo exchange (CUDA IPC copies + stream flags), one CUDA graph per "
-                           "iteration" if args.halo == "peer"
-                           else "NCCL halo exchange"),
-                       "l2": "working set far above L2"},
+            "dtype": "f64", "data": "synthetic (BASELINE forcing recipe, SURVEY 8(d)); f sha256 "
+                    + hashlib.sha256(np.ascontiguousarray(f.values).data).hexdigest()[:16],
+            "config": config_for(args.workload, K, ws, args.decomp, args.halo, n_t=n_t),
             "iters_per_s": K / dev_s,
-            "roofline": {"bound": "hbm", "achieved": BYTES_PER_UPDATE * units / ws / dev_s / 1e9, "peak": peak,
-                         "unit": "GB/s", "frac": BYTES_PER_UPDATE * units / ws / dev_s / 1e9 / peak,
-                         "traffic": None, "peak_source": peak_src,
-                         "note": "per GPU: 48 B/update x this rank's share of the updates / wall device time"},
+            "roofline": {"bound": "hbm", "achieved": own_bpu * per_gpu / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": own_bpu * per_gpu / 1e9 / peak, "traffic": None, "peak_source": peak_src,
+                         "bytes_per_update": own_bpu,
+                         "frac_48B": BYTES_PER_UPDATE * per_gpu / 1e9 / peak,
+                         "frac_source": "compulsory bytes of the slab's multi-step passes per GPU / device wall "
+                                        "time of the timed iterations (exchange and region split included)"},
             "cpu_baseline": None, "e2e": e2e, "clocks": clocks, "gpu_launches": launches,
             "residuals": {"first": res[0], "last": res[-1]}, "impl": "ours",
+            **({"emulated_cpu": "numpy stand-in shard over gloo: a launcher test, not a measurement"}
+               if emulate else {}),
         }
-        print(json.dumps(line))
+        print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------------------------------
@@ -582,6 +684,10 @@ def run_ours(args, dist, ws, rank, local):
 
     from paper_2504_03074_b200 import _native
 
+    if args.emulate_cpu:
+        if not (ws > 1 and args.workload in ("cfg3", "cfg4") and args.decomp == "slab"):
+            raise SystemExit("--emulate-cpu runs the z-slab path only (configs 3/4 at N > 1)")
+        return run_slab(args, dist, ws, rank, local)
     torch.cuda.set_device(local)
     if ws > 1 and args.workload in ("cfg3", "cfg4") and args.decomp == "slab":
         return run_slab(args, dist, ws, rank, local)
@@ -615,28 +721,32 @@ def run_ours(args, dist, ws, rank, local):
     units_rank = wl.units_per_step * K
     units = units_rank
     if dist is not None:
-        import torch as _t
-
-        t = _t.tensor([float(units_rank)], dtype=_t.float64, device="cuda")
+        t = torch.tensor([float(units_rank)], dtype=torch.float64, device="cuda")
         dist.all_reduce(t)
         units = float(t.item())
-    elif ws > 1:
-        units = units_rank * ws
     value = units / dev_s / 1e9
     ms_per_step = dev_s * 1e3 / K
     peak, peak_src = peaks()
-    # algorithmic bytes of this rank's step kernels over the timed passes / their device time
-    achieved = BYTES_PER_UPDATE * units_rank / (step_ms_total / 1e3) / 1e9
     kern, steps_per_pass = ctx.plan()
-    # a pass of T fused steps reads W^s, W^{s-1}, f, acc and writes W^{s+T-1}, W^{s+T}, acc: 56 B per T updates;
-    # the cluster-resident kernel (plan kernel 4) reads v and f and writes v once per fpi call
+    # compulsory bytes of the kernel's algorithm: a pass of T fused steps reads W^s, W^{s-1}, f, acc
+    # and writes W^{s+T-1}, W^{s+T}, acc (56 B per T updates); the cluster-resident kernel (plan
+    # kernel 4) reads v and f and writes v once per fpi call
     if kern == 4:
         own_bpu = 24.0 * wl.npts / units_rank
     else:
         own_bpu = BYTES_PER_UPDATE if steps_per_pass == 1 else 56 / steps_per_pass
-    own = own_bpu * units_rank / (step_ms_total / 1e3) / 1e9
+    step_s = step_ms_total / 1e3
+    avg_launch_s = step_s / max(1, step_launches)
+    bytes_per_launch_comp = own_bpu * units_rank / max(1, step_launches)
+    traffic, traffic_src = load_traffic(args.workload)
+    if traffic:
+        achieved, frac_source = traffic / avg_launch_s / 1e9, (
+            "ncu DRAM bytes per launch of this build (profiles/traffic.json: " + str(traffic_src) + ")")
+    else:
+        achieved, frac_source = bytes_per_launch_comp / avg_launch_s / 1e9, (
+            f"compulsory bytes per launch ({own_bpu:g} B/update; {traffic_src})")
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": load_traffic(args.workload),
+            "traffic": traffic, "frac_source": frac_source,
             "kernel": ("cluster-resident solve kernel (the whole grid in the shared memory of one thread-block "
                        "cluster, DSMEM halo rows, one cluster barrier per leapfrog step; all K fixed-point "
                        "iterations in one launch)" if kern == 4 else
@@ -644,32 +754,30 @@ def run_ours(args, dist, ws, rank, local):
                         f"{steps_per_pass} consecutive steps per HBM pass)" if steps_per_pass > 1
                         else "fused step kernel (Laplacian + leapfrog + filter accumulate)")
                        + (", TMA tensor boxes" if kern == 2 else ", cp.async.bulk rows" if kern == 1 else "")),
-            "bytes_per_update": BYTES_PER_UPDATE,
-            "avg_launch_us": step_ms_total * 1e3 / max(1, step_launches),
-            "launches_timed": step_launches,
-            "kernel_compulsory": {"bytes_per_update": own_bpu, "achieved": own, "frac": own / peak},
-            "peak_source": peak_src,
-            "note": "achieved/frac use SURVEY 8(d)'s 48 algorithmic B per point update x updates / device time "
-                    "of the step launches (CUDA events on the context stream bracketing each pass; includes "
-                    "the per-pass residual reduction and inter-launch gaps). "
-                    + ("The cluster-resident kernel keeps every field in shared memory for the whole launch: "
-                       "its HBM traffic is v and f in and v out once per launch (kernel_compulsory), so it is "
-                       "bound by the per-step cluster barrier and fp64 latency, not HBM. " if kern == 4 else "")
-                    + (f"The {steps_per_pass}-step kernel moves only {56 / steps_per_pass:g} compulsory B per update "
-                       f"(reads W^s, W^(s-1), f, acc; writes the last two levels and acc once per {steps_per_pass} "
-                       "updates), so frac > 1 is expected; kernel_compulsory is its fraction against its own "
-                       "traffic." if steps_per_pass > 1 else "")}
+            "avg_launch_us": avg_launch_s * 1e6, "launches_timed": step_launches,
+            "bytes_per_update": own_bpu,
+            "achieved_compulsory": bytes_per_launch_comp / avg_launch_s / 1e9,
+            "frac_compulsory": bytes_per_launch_comp / avg_launch_s / 1e9 / peak,
+            "frac_48B": BYTES_PER_UPDATE * units_rank / step_s / 1e9 / peak,
+            "peak_source": peak_src, "lib_sha16": lib_sha16(),
+            "note": "avg_launch_us = CUDA events on the context stream bracketing every pass of the timed "
+                    "iterations / passes (includes the per-pass residual reduction and inter-launch gaps). "
+                    "frac_48B uses SURVEY 8(d)'s 48 B per update and exceeds 1 for multi-step kernels by "
+                    "construction (they move 56/T B per update)."}
 
-    e2e = None
+    e2e = e2e_solve = None
     if not args.no_e2e:
         te, info = wl.e2e(K, W, dist)
         te = max_over_ranks(dist, te)
         e2e = {"value": units / te / 1e9, "unit": "Gpts/s", **info, "iters_per_s": K / te}
+        if hasattr(wl, "e2e_solve"):
+            ts_, info_s = wl.e2e_solve(K, dist)
+            ts_ = max_over_ranks(dist, ts_)
+            e2e_solve = {"value": units / ts_ / 1e9, "unit": "Gpts/s", **info_s, "iters_per_s": K / ts_}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         if args.workload == "cfg5":
-            from paper_2504_03074_b200 import timestep as ts
             import paper_2504_03074_b200 as wh
 
             corr = wh.correct_explicit(100.0, wl.g, 2, 1.0)
@@ -684,19 +792,14 @@ def run_ours(args, dist, ws, rank, local):
             "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong" if args.workload == "cfg5" else "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (BASELINE forcing recipe, SURVEY 8(d)); f sha256 " + wl.f_sha[:16],
-            "config": {"workload": args.workload, **wl.desc, "iterations": K, "cfl": 0.9,
-                       "forcing": forcing_desc(args.workload),
-                       "parallelism": (f"frequencies LPT-sharded over {ws} GPUs" if args.workload == "cfg5" else
-                                       f"independent replicas x{ws}") if ws > 1 else "single GPU",
-                       "l2": ("flushed before the timed launch (256 MiB write, outside the timed span); the "
-                              "cluster-resident kernel then holds every field in shared memory" if kern == 4 else
-                              "flushed before every timed iteration (256 MiB write, outside the timed span)")},
+            "config": config_for(args.workload, K, ws, args.decomp, args.halo, n_t=getattr(wl, "n_t_config", None)),
             "iters_per_s": K / dev_s,
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": launches,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_solve": e2e_solve, "clocks": clocks,
+            "gpu_launches": launches,
             "residuals": {"first": float(residuals[0]), "last": float(residuals[-1])},
             "wall_s_timed_region": t_wall, "impl": "ours",
         }
-        print(json.dumps(line))
+        print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------------------------------
@@ -729,13 +832,15 @@ def run_reference(args, ws, rank):
     m = n_t if per_step * n_t <= 3.0 else max(5, int(3.0 / per_step))
     sm = dict(sc)
     sm["n_total"] = m
-    for _ in range(args.warmup):
+    for _ in range(min(args.warmup, 1)):
         v = ON.wave_solve(v, fv, g.spacing, sm, nthreads=threads)
     v[...] = 0.0
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        v = ON.wave_solve(v, fv, g.spacing, sm, nthreads=threads)
-        _ = np.linalg.norm(v)  # the reference's per-iteration residual norm (driver.py:225)
+        vn = ON.wave_solve(v, fv, g.spacing, sm, nthreads=threads)
+        # the reference's per-iteration residual ||v_new - v||_2 / sqrt(N) (driver.py:225)
+        _ = np.linalg.norm(vn - v) / math.sqrt(npts)
+        v = vn
     dt = time.perf_counter() - t0
     value = npts * m * args.steps / dt / 1e9
     sample = (f"{'full WaveHoltz iteration' if m == n_t else f'{m} of {n_t} leapfrog steps'} per step of "
@@ -743,10 +848,12 @@ def run_reference(args, ws, rank):
               f"reference, -O2 -ffp-contract=off, OpenMP {threads} threads)")
     line = {
         "metric": METRIC, "value": value, "unit": "Gpts/s", "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE forcing recipe)",
-        "config": {"workload": args.workload, "grid": list(g.shape), "omega": cfg.omega, "N_t": n_t,
-                   "iterations": args.steps, "cfl": 0.9},
+        "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
+        "scaling": "strong" if (ws > 1 and args.workload in ("cfg3", "cfg4") and args.decomp == "slab") else "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE forcing recipe, SURVEY 8(d)); f sha256 "
+                + hashlib.sha256(np.ascontiguousarray(fv).data).hexdigest()[:16],
+        "config": config_for(args.workload, args.steps, ws, args.decomp, args.halo, n_t=n_t),
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": "Gpts/s", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "Gpts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -783,8 +890,7 @@ def run_reference_cfg5(args, ws):
         "metric": METRIC, "value": value, "unit": "Gpts/s", "n_gpus": ws, "steps": steps, "warmup": args.warmup,
         "ms_per_step": dt * 1e3 / steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (BASELINE forcing recipe)",
-        "config": {"workload": "cfg5", "grid": list(g.shape), "omegas": "np.linspace(10.3, 200.3, 64)",
-                   "iterations": steps, "cfl": 0.9},
+        "config": config_for("cfg5", args.steps, ws),
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": "Gpts/s", "cores": threads, "kind": "port",
                          "sample": f"{steps} WaveHoltz iteration(s) of all 64 omegas through oracle/whb_oracle.c "
@@ -794,12 +900,29 @@ def run_reference_cfg5(args, ws):
     print(json.dumps(line))
 
 
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def relaunch(n: int) -> int:
+    """--gpus N outside torchrun: one process per GPU through torch.distributed.run on this
+    node (127.0.0.1 rendezvous).  Rank 0's stdout carries the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS) + ["cfg5", "imp2"])
+    ap.add_argument("--workload", default="cfg4", choices=sorted(WORKLOADS) + ["cfg5", "imp2"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--decomp", default="slab", choices=["slab", "replicas"],
                     help="N > 1 on configs 3/4: z-slab decomposition (default) or independent replicas")
@@ -808,17 +931,28 @@ def main():
                          "(CUDA IPC mappings of the neighbours' ghost planes, stream flags)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--emulate-cpu", action="store_true",
+                    help="TEST ONLY: the z-slab driver with a numpy stand-in shard over gloo (no GPU)")
+    ap.add_argument("--cells", type=int, default=None,
+                    help="TEST ONLY: override the workload's cells per axis (CPU launcher test)")
     args = ap.parse_args()
+    if args.cells:
+        d, _, om, fo, it = WORKLOADS[args.workload]
+        WORKLOADS[args.workload] = (d, args.cells, om, fo, it)
     if args.steps is None:
         args.steps = {"cfg5": 20, "imp2": IMP2["iterations"]}.get(args.workload) or WORKLOADS[args.workload][4]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args.gpus))
     ws, rank, local = dist_env()
+    if ws != args.gpus and rank == 0:
+        sys.stderr.write(f"bench.py: WORLD_SIZE={ws} but --gpus {args.gpus}; using WORLD_SIZE\n")
     if args.impl == "reference":
         if args.workload == "imp2":
             run_reference_implicit(args, ws, rank)
         else:
             run_reference(args, ws, rank)
         return
-    dist = init_dist(ws)
+    dist = init_dist(ws) if not args.emulate_cpu else _init_gloo(ws)
     try:
         if args.workload == "imp2":
             run_implicit(args, dist, ws, rank, local)
@@ -827,6 +961,15 @@ def main():
     finally:
         if dist is not None:
             dist.destroy_process_group()
+
+
+def _init_gloo(ws):
+    if ws <= 1:
+        return None
+    import torch.distributed as dist
+
+    dist.init_process_group(backend="gloo")
+    return dist
 
 
 if __name__ == "__main__":
