@@ -221,8 +221,11 @@ def config_for(name, iterations, ws, decomp="slab", halo="nccl", g=None, cfg=Non
     dim, n, omega, forcing, _ = WORKLOADS[name]
     if ws > 1 and name in ("cfg3", "cfg4") and decomp == "slab":
         par = (f"z-slab decomposition over {ws} GPUs (slab_ranges: contiguous axis-0 plane ranges), "
-               + ("peer-memory halo exchange (CUDA IPC copies on a comm stream + stream flags)" if halo == "peer"
-                  else "NCCL send/recv halo exchange overlapped with the interior planes"))
+               + {"peer": "peer-memory halo exchange (CUDA IPC copies on the exchange stream + stream flags), "
+                          "one CUDA graph per iteration",
+                  "nccl": "NCCL send/recv halo exchange in the C ABI on the exchange stream, overlapped with "
+                          "the interior planes, one CUDA graph per iteration",
+                  "torch": "torch.distributed NCCL P2P halo exchange overlapped with the interior planes"}[halo])
     elif ws > 1:
         par = f"independent replicas x{ws}"
     else:
@@ -436,7 +439,7 @@ def run_slab(args, dist, ws, rank, local):
     interior planes).  Strong scaling: the grid is fixed.  --emulate-cpu runs the same driver with
     the numpy stand-in shard over gloo (CPU test of the launcher; the numbers mean nothing)."""
     from paper_2504_03074_b200 import _native
-    from paper_2504_03074_b200.slab import PeerHalo, SlabFPI, TorchHalo, slab_ranges
+    from paper_2504_03074_b200.slab import NcclHalo, PeerHalo, SlabFPI, TorchHalo, slab_ranges
 
     g, f, corr, cfg, _ = build_workload(args.workload)
     rng = slab_ranges(g.shape[0], ws)[rank]
@@ -453,8 +456,13 @@ def run_slab(args, dist, ws, rank, local):
         from paper_2504_03074_b200.slab import DeviceShard
 
         shard = DeviceShard(g, rng, device=local)
-        halo = PeerHalo.from_dist(shard, dist, rank, ws) if args.halo == "peer" else TorchHalo(dist, rank, ws)
-    solver = SlabFPI(shard, halo, corr, cfg, f, graph=args.halo == "peer")
+        if args.halo == "peer":
+            halo = PeerHalo.from_dist(shard, dist, rank, ws)
+        elif args.halo == "nccl":
+            halo = NcclHalo(shard, dist, rank, ws)
+        else:
+            halo = TorchHalo(dist, rank, ws)
+    solver = SlabFPI(shard, halo, corr, cfg, f, graph=args.halo in ("peer", "nccl"))
     n_t = solver.shard.n_total
     K, W = args.steps, args.warmup
     for _ in range(W):
@@ -926,9 +934,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--decomp", default="slab", choices=["slab", "replicas"],
                     help="N > 1 on configs 3/4: z-slab decomposition (default) or independent replicas")
-    ap.add_argument("--halo", choices=["nccl", "peer"], default="nccl",
-                    help="z-slab halo exchange at N > 1: NCCL send/recv (default) or peer memory "
-                         "(CUDA IPC mappings of the neighbours' ghost planes, stream flags)")
+    ap.add_argument("--halo", choices=["nccl", "torch", "peer"], default="nccl",
+                    help="z-slab halo exchange at N > 1: NCCL send/recv inside the C ABI on the exchange "
+                         "stream, one CUDA graph per iteration (default); torch.distributed P2P; or peer "
+                         "memory (CUDA IPC mappings of the neighbours' ghost planes, stream flags, graph)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--emulate-cpu", action="store_true",

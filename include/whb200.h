@@ -273,7 +273,8 @@ int whb_host_free(void *ptr);
  * single-process).  whb_ipc_handle: CUDA IPC handle (64 bytes) of the allocation holding
  * dev_ptr and dev_ptr's byte offset in it; whb_ipc_open / whb_ipc_close map / unmap a peer's
  * allocation in this process.  whb_flags_alloc: `count` zeroed uint32 flags in device memory.
- * whb_copy_async: stream-ordered copy on the context stream (any two device addresses, e.g.
+ * whb_copy_async: stream-ordered copy on the context stream, or on the exchange stream inside
+ * whb_comm_begin / whb_comm_end (any two device addresses, e.g.
  * local boundary planes -> a neighbour's ghost planes over NVLink).  whb_stream_write_u32 /
  * whb_stream_wait_u32: stream memory operations (write after the stream's earlier work, with
  * a fence; wait until (int32)(*flag - value) >= 0) — the ranks' flags order the exchange
@@ -286,6 +287,27 @@ int whb_flags_free(whb_ctx *ctx, uint64_t dev_ptr);
 int whb_copy_async(whb_ctx *ctx, uint64_t src_ptr, uint64_t dst_ptr, int64_t bytes);
 int whb_stream_write_u32(whb_ctx *ctx, uint64_t dev_ptr, uint32_t value);
 int whb_stream_wait_u32(whb_ctx *ctx, uint64_t dev_ptr, uint32_t value);
+
+/* Halo exchange stream (slab.py start/finish).  whb_comm_begin: the context's exchange stream
+ * waits for everything enqueued so far (the boundary planes), and whb_copy_async /
+ * whb_stream_write_u32 / whb_nccl_exchange go on it until whb_comm_end; whb_comm_join: the
+ * context stream waits for that exchange.  Kernels enqueued between end and join (the interior
+ * planes) run while the exchange is in flight.  Graph capture follows the fork and join. */
+int whb_comm_begin(whb_ctx *ctx);
+int whb_comm_end(whb_ctx *ctx);
+int whb_comm_join(whb_ctx *ctx);
+
+/* NCCL halo path inside the C ABI (replaces torch.distributed P2P on the data path; libnccl is
+ * dlopen'ed, reusing the copy the process already loaded).  whb_nccl_unique_id writes the
+ * 128-byte ncclUniqueId (rank 0; the caller broadcasts it), whb_nccl_init creates the context's
+ * communicator, whb_nccl_exchange posts n (send, recv) pairs of `counts[i]` doubles with
+ * peers[i] as one NCCL group on the exchange stream (inside whb_comm_begin/end; capturable),
+ * whb_nccl_allreduce_sum sums one double across the ranks (synchronous). */
+int whb_nccl_unique_id(void *id_out);
+int whb_nccl_init(whb_ctx *ctx, int nranks, int rank, const void *id);
+int whb_nccl_exchange(whb_ctx *ctx, int n, const uint64_t *send_ptrs, const uint64_t *recv_ptrs,
+                      const int64_t *counts, const int *peers);
+int whb_nccl_allreduce_sum(whb_ctx *ctx, double *value);
 
 /* Caller-captured graphs: whb_capture_begin starts stream capture on the context stream
  * (relaxed mode, so several contexts can capture at once), every later call enqueues into the

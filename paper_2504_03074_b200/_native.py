@@ -37,6 +37,8 @@ EXPORTS = (
     "whb_pair", "whb_ghost_planes", "whb_field_plane_ptr", "whb_copy_device",
     "whb_imp_apply", "whb_imp_rhs", "whb_vec_xpay", "whb_mg_setup", "whb_mg_vcycle", "whb_tri_setup", "whb_tri_solve",
     "whb_cg_begin", "whb_cg_iterate", "whb_vec_mgs",
+    "whb_comm_begin", "whb_comm_end", "whb_comm_join", "whb_nccl_unique_id", "whb_nccl_init", "whb_nccl_exchange",
+    "whb_nccl_allreduce_sum",
 )
 
 _lib = None
@@ -84,6 +86,14 @@ def load():
         "whb_resid_read": ([vp, dp], c_int),
         "whb_stream_write_u32": ([vp, c_u64, ctypes.c_uint32], c_int),
         "whb_stream_wait_u32": ([vp, c_u64, ctypes.c_uint32], c_int),
+        "whb_comm_begin": ([vp], c_int),
+        "whb_comm_end": ([vp], c_int),
+        "whb_comm_join": ([vp], c_int),
+        "whb_nccl_unique_id": ([ctypes.c_void_p], c_int),
+        "whb_nccl_init": ([vp, c_int, c_int, ctypes.c_void_p], c_int),
+        "whb_nccl_exchange": ([vp, c_int, ctypes.POINTER(c_u64), ctypes.POINTER(c_u64), ctypes.POINTER(c_i64),
+                               ctypes.POINTER(c_int)], c_int),
+        "whb_nccl_allreduce_sum": ([vp, dp], c_int),
         "whb_iterate_host": ([vp, dp, dp, dp], c_int),
         "whb_vec_reserve": ([vp, c_int, ctypes.POINTER(c_int)], c_int),
         "whb_vec_upload": ([vp, c_int, dp], c_int),
@@ -498,6 +508,37 @@ class Context:
 
     def stream_wait_u32(self, ptr: int, value: int):
         check(load().whb_stream_wait_u32(self._h, int(ptr), int(value) & 0xFFFFFFFF), "whb_stream_wait_u32")
+
+    # -- halo exchange stream and the NCCL path ----------------------------------------
+    def comm_begin(self):
+        check(load().whb_comm_begin(self._h), "whb_comm_begin")
+
+    def comm_end(self):
+        check(load().whb_comm_end(self._h), "whb_comm_end")
+
+    def comm_join(self):
+        check(load().whb_comm_join(self._h), "whb_comm_join")
+
+    def nccl_init(self, nranks: int, rank: int, uid: bytes):
+        buf = ctypes.create_string_buffer(bytes(uid), 128)
+        check(load().whb_nccl_init(self._h, int(nranks), int(rank), buf), "whb_nccl_init")
+
+    def nccl_exchange(self, sends, recvs, counts, peers):
+        n = len(sends)
+        arr = lambda t, v: (t * max(1, n))(*[int(x) for x in v])  # noqa: E731
+        check(load().whb_nccl_exchange(self._h, n, arr(ctypes.c_uint64, sends), arr(ctypes.c_uint64, recvs),
+                                       arr(ctypes.c_int64, counts), arr(ctypes.c_int, peers)), "whb_nccl_exchange")
+
+    def nccl_allreduce_sum(self, x: float) -> float:
+        v = np.array([float(x)])
+        check(load().whb_nccl_allreduce_sum(self._h, _dp(v)), "whb_nccl_allreduce_sum")
+        return float(v[0])
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    check(load().whb_nccl_unique_id(buf), "whb_nccl_unique_id")
+    return buf.raw
 
     def stream_ptr(self) -> int:
         p = ctypes.c_uint64(0)

@@ -1,0 +1,298 @@
+// Three leapfrog steps per HBM pass over a 3D grid (temporal blocking T = 3), TMA-pipelined,
+// skewed so that ONE block barrier per plane orders everything (sm_100a).
+//
+// A CTA owns a BY x TX output tile (axis 1 x axis 2) and marches it through a chunk of axis-0
+// planes [i0, i1).  Its 16 warps cover the level-1 region: warp w <-> row j0 - 2 + w, lane l <->
+// the column pair k0 - 2 + 2l, +1 (64 columns).  Levels (time level s+t = "level t"):
+//
+//     level 1 on rows j0-2 .. j0+BY+1, columns k0-2 .. k0+TX+1   (16 x 64, halo 2)
+//     level 2 on rows j0-1 .. j0+BY,   columns k0-1 .. k0+TX     (14 x 62, halo 1)
+//     level 3 on rows j0   .. j0+BY-1, columns k0   .. k0+TX-1   (12 x 60, the tile)
+//
+// Iteration i computes level 1 at plane i, level 2 at plane i-2 and level 3 at plane i-4.  Every
+// input of an iteration was produced by an EARLIER iteration (level 2 at i-2 reads level 1 at
+// planes i-3..i-1; level 3 at i-4 reads level 2 at i-5..i-3), so the three level updates of an
+// iteration are independent (3-way ILP per thread) and one __syncthreads per plane publishes
+// them.  Axis-0 neighbours and the pointwise terms (W^{s-1}, f, the previous level, the filter
+// sum) come from per-thread register queues; the axis-1/axis-2 neighbours of the level being
+// stepped come from shared memory (W^s: the TMA stage; levels 1 and 2: 3-plane rings), axis-2
+// neighbours inside a warp by shuffles.
+//
+// HBM traffic per output point per pass: read W^s, W^{s-1}, f, acc; write W^{s+2}, W^{s+3}, acc:
+// 56 B for 3 updates = 18.7 B/update (28 for two steps per pass, 48 for one).  Halo boxes are
+// re-read by the neighbouring tiles, mostly from L2.  Redundant level-1/2 work on the halo:
+// (16*64 + 14*64) / (2*12*60) - 1 = 33 % of those two levels (the level-3 tile carries none).
+//
+// Arithmetic and its order are exactly three consecutive reference steps (update_point, the
+// filter sum in step order), so the iterates stay bitwise equal to the reference's.
+#pragma once
+
+namespace t3 {
+
+using bulk::fence_proxy_async;
+using bulk::mbar_expect_tx;
+using bulk::mbar_init;
+using bulk::mbar_wait;
+using bulk::tma_load_3d;
+using bulk::update_point;
+
+constexpr int TX = 60;                 // output columns per tile
+constexpr int BY = 12;                 // output rows per tile
+constexpr int NW = BY + 4;             // warps = level-1 rows
+constexpr int THREADS = 32 * NW;       // 512
+constexpr int LW = 64;                 // level-1 row width (columns k0-2 .. k0+61)
+constexpr int RW = 68;                 // staged W^s row: columns k0-4 .. k0+63
+constexpr int WR = BY + 6;             // staged W^s rows: j0-3 .. j0+BY+2
+constexpr int W_EL = (WR * RW + 15) / 16 * 16;   // 1232 (128-B aligned sub-buffers for TMA)
+constexpr int P_EL = NW * LW;                    // 1024: W^{s-1} / f box (the level-1 region)
+constexpr int STAGE = W_EL + 2 * P_EL;           // 3280 doubles = 26.2 KB
+constexpr int L1_EL = NW * LW;                   // level-1 plane
+constexpr int L2_EL = (NW - 2) * LW;             // level-2 plane (rows j0-1 .. j0+BY)
+
+template <int ST>
+constexpr size_t smem_bytes() {
+    return (size_t)(ST * STAGE + 3 * L1_EL + 3 * L2_EL) * sizeof(double) + ST * sizeof(uint64_t);
+}
+
+// Per-pass scalars (the reference's host expressions), passed as a kernel parameter.
+struct Scal {
+    double h1, cos1;            // step s (K_FIRST: dt^2/2 and 1)
+    double cos2, cos3, dt2;     // steps s+1, s+2
+    double c0, c1, c2, c3;      // filter weights acc_c[0], acc_c[s+1..s+3]
+    double osc;                 // (2/T) dt (last pass)
+};
+
+// K1: kind of step s (FIRST when s == 0); K2: MID, or LAST when step s+2 ends the solve.
+// GM: geometry mode as in tb2 / wf2d (0 generic, 1 equal taps, 2 equal taps and c^2 == 1).
+template <int ST, int K1, int K2, bool ZF, int GM>
+__global__ void __launch_bounds__(THREADS, 1)
+    t3_kernel(Geom g, const Member *__restrict__ members, int s, int i_begin, int i_end, int chunk_len, int JT,
+              const Scal sc, const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_p,
+              const __grid_constant__ CUtensorMap tm_f) {
+    constexpr bool SQ = GM >= 1;
+    constexpr int C2M = GM == 2 ? 0 : -1;
+    constexpr bool LOAD_P = (K1 != K_FIRST);
+    static_assert(ST >= 3, "planes i and i+1 resident plus one in flight");
+    extern __shared__ __align__(128) double smem[];
+    double *l1buf = smem + (size_t)ST * STAGE;
+    double *l2buf = l1buf + 3 * L1_EL;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(l2buf + 3 * L2_EL);
+
+    const Member m = members[0];
+    const int w = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // warp-uniform
+    const int lane = threadIdx.x & 31;
+    const int jt = blockIdx.y % JT;
+    const int ch = blockIdx.y / JT;
+    const int k0 = blockIdx.x * TX;
+    const int j0 = jt * BY;
+    const int i0 = i_begin + ch * chunk_len;
+    const int i1 = min(i_end, i0 + chunk_len);
+    if (i0 >= i1) {
+        if (K2 == K_LAST && m.out_mode == WHB_OUT_FPI && threadIdx.x == 0)
+            m.partials[blockIdx.y * gridDim.x + blockIdx.x] = 0.0;
+        return;
+    }
+    double *w2g = level_ptr(m, s + 2);
+    double *w3g = level_ptr(m, s + 3);
+    const long long S0 = g.S0;
+    const int P = g.P;
+
+    constexpr uint32_t stage_bytes = (uint32_t)((RW * WR + (LOAD_P ? P_EL : 0) + (ZF ? 0 : P_EL)) * 8);
+    // staged planes i0-3 .. i1+2; stage slot of plane p: (p - (i0 - 3)) % ST
+    const int pfirst = i0 - 3;
+    const int plast = i1 + 2;
+    auto issue = [&](int plane) {
+        const int slot = (plane - pfirst) % ST;
+        double *st = smem + (size_t)slot * STAGE;
+        uint64_t *bar = bars + slot;
+        mbar_expect_tx(bar, stage_bytes);
+        tma_load_3d(st, &tm_w, k0 - 4, j0 - 3, plane, bar);
+        if (LOAD_P) tma_load_3d(st + W_EL, &tm_p, k0 - 2, j0 - 2, plane, bar);
+        if (!ZF) tma_load_3d(st + W_EL + P_EL, &tm_f, k0 - 2, j0 - 2, plane, bar);
+    };
+    auto wait_plane = [&](int plane) {
+        const int t = plane - pfirst;
+        mbar_wait(bars + (t % ST), (t / ST) & 1);
+    };
+    auto stage_of = [&](int plane) -> const double * { return smem + (size_t)((plane - pfirst) % ST) * STAGE; };
+
+    if (threadIdx.x == 0) {
+        for (int t = 0; t < ST; ++t) mbar_init(bars + t, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int p = pfirst; p <= plast && p < pfirst + ST; ++p) issue(p);
+    }
+    __syncthreads();
+
+    // this thread's rows / columns
+    const int y = j0 - 2 + w;                  // level-1 row
+    const int x = k0 - 2 + 2 * lane;           // first column of the pair
+    const bool yin = (y >= g.j_lo) && (y < g.j_hi);
+    const bool xin0 = (x >= 1) && (x < g.n2 - 1);
+    const bool xin1 = (x + 1 >= 1) && (x + 1 < g.n2 - 1);
+    const bool do2 = (w >= 1) && (w <= NW - 2);        // warp-uniform: rows of level 2
+    const bool do3 = (w >= 2) && (w <= NW - 3);        // rows of level 3 (the output tile)
+    // output points: the tile's rows / columns, interior only
+    const bool own = do3 && lane >= 1 && lane <= 30;
+    const bool ok0 = own && yin && xin0;
+    const bool ok1 = own && yin && xin1;
+    const int wrow = (w + 1) * RW + 2 + 2 * lane;      // this pair in a W^s stage (row y)
+    const int prow = w * LW + 2 * lane;                // this pair in a W^{s-1} / f box, level-1 plane
+    const long long pbase = (long long)y * P + x;
+
+    auto plane_in = [&](int p) { return p >= g.i_lo && p < g.i_hi; };
+    auto shl = [&](double v) { return __shfl_up_sync(0xffffffffu, v, 1); };
+    auto shr = [&](double v) { return __shfl_down_sync(0xffffffffu, v, 1); };
+
+    // register queues (own column pair): W^s at planes i+1 .. i-4, level 1 at i .. i-4,
+    // level 2 at i-2 .. i-5, f at i .. i-4
+    const double2 z2 = make_double2(0.0, 0.0);
+    double2 ws0 = z2, ws1 = z2, ws2 = z2, ws3 = z2, ws4 = z2, ws5 = z2;  // ws0 = W^s(i+1), ws1 = W^s(i), ...
+    double2 q10 = z2, q11 = z2, q12 = z2, q13 = z2, q14 = z2;           // q1k = level 1 at plane i-k
+    double2 q20 = z2, q21 = z2, q22 = z2, q23 = z2;                     // q2k = level 2 at plane i-2-k
+    double2 fq0 = z2, fq1 = z2, fq2 = z2, fq3 = z2, fq4 = z2;           // fqk = f at plane i-k
+    double rsum = 0.0;
+
+    // W^s centres of planes i0-3 and i0-2 (the first iteration, i = i0-2, adds plane i0-1)
+    wait_plane(pfirst);
+    wait_plane(pfirst + 1);
+    ws1 = *reinterpret_cast<const double2 *>(stage_of(pfirst) + wrow);    // becomes W^s(i-1) below
+    ws0 = *reinterpret_cast<const double2 *>(stage_of(pfirst + 1) + wrow);
+    // the filter-sum input and v of the first output plane
+    const bool want_v = (K2 == K_LAST) && m.out_mode != WHB_OUT_PLAIN;
+    auto ld2 = [&](const double *base, int p) -> double2 {
+        return *reinterpret_cast<const double2 *>(base + (long long)p * S0 + pbase);
+    };
+    double2 acc_n = (K1 != K_FIRST && (ok0 || ok1)) ? ld2(m.acc, i0) : z2;
+    double2 v_n = (want_v && (ok0 || ok1)) ? ld2(m.v, i0) : z2;
+    __syncthreads();  // every thread has read plane pfirst: its slot takes plane pfirst + ST
+    if (threadIdx.x == 0 && pfirst + ST <= plast) {
+        fence_proxy_async();
+        issue(pfirst + ST);
+    }
+
+    for (int i = i0 - 2; i <= i1 + 3; ++i) {
+        // shift the queues: plane i+1 of W^s enters
+        ws5 = ws4; ws4 = ws3; ws3 = ws2; ws2 = ws1; ws1 = ws0;
+        const bool has_next = (i + 1 <= plast);
+        if (has_next) {
+            wait_plane(i + 1);
+            ws0 = *reinterpret_cast<const double2 *>(stage_of(i + 1) + wrow);
+        } else {
+            ws0 = z2;
+        }
+        q14 = q13; q13 = q12; q12 = q11; q11 = q10;
+        q23 = q22; q22 = q21; q21 = q20;
+        fq4 = fq3; fq3 = fq2; fq2 = fq1; fq1 = fq0;
+        const int sl1 = (i % 3 + 3) % 3;
+
+        // ---- level 1 at plane i (step s)
+        if (i <= i1 + 1) {
+            const double *st = stage_of(i);
+            const double2 yl = *reinterpret_cast<const double2 *>(st + wrow - RW);
+            const double2 yh = *reinterpret_cast<const double2 *>(st + wrow + RW);
+            double xl = shl(ws1.y), xh = shr(ws1.x);
+            if (lane == 0) xl = st[wrow - 1];
+            if (lane == 31) xh = st[wrow + 2];
+            const double2 pv = LOAD_P ? *reinterpret_cast<const double2 *>(st + W_EL + prow) : z2;
+            fq0 = ZF ? z2 : *reinterpret_cast<const double2 *>(st + W_EL + P_EL + prow);
+            const double a = update_point<K1, ZF, true, SQ, C2M>(g, ws2.x, ws1.x, ws0.x, yl.x, yh.x, xl, ws1.y, fq0.x,
+                                                               pv.x, sc.h1, sc.cos1);
+            const double b = update_point<K1, ZF, true, SQ, C2M>(g, ws2.y, ws1.y, ws0.y, yl.y, yh.y, ws1.x, xh, fq0.y,
+                                                               pv.y, sc.h1, sc.cos1);
+            const bool pin = plane_in(i) && yin;
+            q10 = make_double2((pin && xin0) ? a : 0.0, (pin && xin1) ? b : 0.0);
+            *reinterpret_cast<double2 *>(l1buf + sl1 * L1_EL + prow) = q10;
+        } else {
+            q10 = z2;
+            fq0 = z2;
+        }
+
+        // ---- level 2 at plane i-2 (step s+1): level 1 at i-3, i-2, i-1 (queue), rows y-1, y+1 (ring)
+        const int p2 = i - 2;
+        if (do2 && p2 >= i0 - 1 && p2 <= i1) {
+            const double *l1 = l1buf + ((p2 % 3 + 3) % 3) * L1_EL;
+            const double2 yl = *reinterpret_cast<const double2 *>(l1 + prow - LW);
+            const double2 yh = *reinterpret_cast<const double2 *>(l1 + prow + LW);
+            const double xl = shl(q12.y), xh = shr(q12.x);
+            // prev of step s+1 = W^s at plane i-2 (ws3), f at plane i-2 (fq2)
+            const double a = update_point<K_MID, ZF, true, SQ, C2M>(g, q13.x, q12.x, q11.x, yl.x, yh.x, xl, q12.y,
+                                                                  fq2.x, ws3.x, sc.dt2, sc.cos2);
+            const double b = update_point<K_MID, ZF, true, SQ, C2M>(g, q13.y, q12.y, q11.y, yl.y, yh.y, q12.x, xh,
+                                                                  fq2.y, ws3.y, sc.dt2, sc.cos2);
+            const bool pin = plane_in(p2) && yin;
+            q20 = make_double2((pin && xin0) ? a : 0.0, (pin && xin1) ? b : 0.0);
+            *reinterpret_cast<double2 *>(l2buf + ((p2 % 3 + 3) % 3) * L2_EL + prow - LW) = q20;
+        } else {
+            q20 = z2;
+        }
+
+        // ---- level 3 at plane i-4 (step s+2) on the tile, then the filter sum and the outputs
+        const int p3 = i - 4;
+        if (do3 && p3 >= i0 && p3 < i1) {
+            const double *l2 = l2buf + ((p3 % 3 + 3) % 3) * L2_EL;
+            const double2 yl = *reinterpret_cast<const double2 *>(l2 + prow - 2 * LW);
+            const double2 yh = *reinterpret_cast<const double2 *>(l2 + prow);
+            const double xl = shl(q22.y), xh = shr(q22.x);
+            // level 2 at i-5, i-4, i-3 = q23, q22, q21; prev = level 1 at i-4 (q14); f at i-4 (fq4)
+            const double a3 = update_point<K_MID, ZF, true, SQ, C2M>(g, q23.x, q22.x, q21.x, yl.x, yh.x, xl, q22.y,
+                                                                   fq4.x, q14.x, sc.dt2, sc.cos3);
+            const double b3 = update_point<K_MID, ZF, true, SQ, C2M>(g, q23.y, q22.y, q21.y, yl.y, yh.y, q22.x, xh,
+                                                                   fq4.y, q14.y, sc.dt2, sc.cos3);
+            // next output plane's acc / v (one iteration ahead: hides the HBM latency)
+            const double2 acc_c = acc_n, v_c = v_n;
+            if (p3 + 1 < i1 && (ok0 || ok1)) {
+                if (K1 != K_FIRST) acc_n = ld2(m.acc, p3 + 1);
+                if (want_v) v_n = ld2(m.v, p3 + 1);
+            }
+            if (ok0 || ok1) {
+                // acc (+ c0 W^0 on the first pass) + c1 W^{s+1} + c2 W^{s+2} + c3 W^{s+3}, in step order
+                double s0, s1;
+                if (K1 == K_FIRST) {  // timestep.py:284 then :298 per step
+                    s0 = whb_add(whb_mul(sc.c0, ws5.x), whb_mul(sc.c1, q14.x));
+                    s1 = whb_add(whb_mul(sc.c0, ws5.y), whb_mul(sc.c1, q14.y));
+                } else {
+                    s0 = whb_add(acc_c.x, whb_mul(sc.c1, q14.x));
+                    s1 = whb_add(acc_c.y, whb_mul(sc.c1, q14.y));
+                }
+                s0 = whb_add(whb_add(s0, whb_mul(sc.c2, q22.x)), whb_mul(sc.c3, a3));
+                s1 = whb_add(whb_add(s1, whb_mul(sc.c2, q22.y)), whb_mul(sc.c3, b3));
+                const long long p = (long long)p3 * S0 + pbase;
+                if (K2 == K_MID) {
+                    if (ok0 && ok1) {
+                        *reinterpret_cast<double2 *>(w2g + p) = q22;
+                        *reinterpret_cast<double2 *>(w3g + p) = make_double2(a3, b3);
+                        *reinterpret_cast<double2 *>(m.acc + p) = make_double2(s0, s1);
+                    } else {
+                        if (ok0) { w2g[p] = q22.x; w3g[p] = a3; m.acc[p] = s0; }
+                        if (ok1) { w2g[p + 1] = q22.y; w3g[p + 1] = b3; m.acc[p + 1] = s1; }
+                    }
+                } else {
+                    const double o0 = whb_mul(sc.osc, s0);
+                    const double o1 = whb_mul(sc.osc, s1);
+                    if (m.out_mode == WHB_OUT_FPI) {
+                        if (ok0) { const double d = o0 - v_c.x; rsum += d * d; m.v[p] = o0; }
+                        if (ok1) { const double d = o1 - v_c.y; rsum += d * d; m.v[p + 1] = o1; }
+                    } else if (m.out_mode == WHB_OUT_AV) {
+                        if (ok0) m.dst[p] = whb_sub(v_c.x, o0);
+                        if (ok1) m.dst[p + 1] = whb_sub(v_c.y, o1);
+                    } else {
+                        if (ok0) m.dst[p] = o0;
+                        if (ok1) m.dst[p + 1] = o1;
+                    }
+                }
+            }
+        }
+
+        __syncthreads();  // level 1 (plane i) and level 2 (plane i-2) published; stage of plane i free
+        if (threadIdx.x == 0 && i + ST <= plast) {
+            fence_proxy_async();
+            issue(i + ST);
+        }
+    }
+    if (K2 == K_LAST && m.out_mode == WHB_OUT_FPI) {
+        const double t = block_sum(rsum);
+        if (threadIdx.x == 0) m.partials[blockIdx.y * gridDim.x + blockIdx.x] = t;
+    }
+}
+
+}  // namespace t3

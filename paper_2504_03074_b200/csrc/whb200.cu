@@ -24,6 +24,9 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include "nccl.h"
 
 #include <algorithm>
 #include <cstdint>
@@ -303,6 +306,7 @@ __global__ void zero_boundary_kernel(double *x, long long S0, int P, int n1, int
 }  // namespace
 #include "step_bulk.cuh"
 #include "step_tb2.cuh"
+#include "step_t3.cuh"
 #include "step_wf2d.cuh"
 #include "step_cres2d.cuh"
 #include "implicit.cuh"
@@ -654,6 +658,10 @@ struct whb_ctx {
     bool tb2 = false;
     size_t smem2 = 0;
     int gx2 = 1, JT2 = 1, chunk2 = 1, nch2 = 1;
+    // three-step (T = 3) plan: whole-grid single-problem 3D contexts (step_t3.cuh)
+    bool t3 = false;
+    size_t smem3 = 0;
+    int gx3 = 1, JT3 = 1, chunk3 = 1, nch3 = 1;
     // cluster-resident small-grid 2D plan (whole grid in one cluster's shared memory)
     bool cres = false;
     int cres_cl = 0, cres_r = 0, cres_ppt = 1;
@@ -692,6 +700,15 @@ struct whb_ctx {
     // caller-captured graphs (whb_capture_begin/end): e.g. one slab iteration with its peer exchange
     bool capturing = false;
     std::vector<cudaGraphExec_t> user_graphs;
+    // halo exchange stream: whb_comm_begin forks it from the context stream (event), copies / flag
+    // writes / NCCL transfers issued until whb_comm_end go on it, whb_comm_join makes the context
+    // stream wait for them -- so the interior planes enqueued in between overlap the exchange
+    cudaStream_t comm = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool on_comm = false;
+    // NCCL communicator of the slab ranks (whb_nccl_init), transfers on `comm`
+    ncclComm_t nccl = nullptr;
+    double *d_nccl = nullptr;  // all-reduce scratch
 };
 
 namespace {
@@ -827,6 +844,36 @@ cudaError_t tb2_set_attrs(size_t smem) {
         set(tb2_fn<A1, K_MID, K_MID, false, GM>());   set(tb2_fn<A1, K_MID, K_MID, true, GM>());
         set(tb2_fn<A1, K_MID, K_LAST, false, GM>());  set(tb2_fn<A1, K_MID, K_LAST, true, GM>());
         set(tb2_fn<A1, K_FIRST, K_LAST, false, GM>()); set(tb2_fn<A1, K_FIRST, K_LAST, true, GM>());
+    };
+    set_gm(std::integral_constant<int, 0>{});
+    set_gm(std::integral_constant<int, 1>{});
+    set_gm(std::integral_constant<int, 2>{});
+    return e;
+}
+
+// Three-step 3D kernel (step_t3.cuh): 5 TMA stages of 26 KB + the level-1/2 rings, 1 CTA/SM.
+#ifndef WHB_S3_ST
+#define WHB_S3_ST 5
+#endif
+constexpr int S3_ST = WHB_S3_ST;
+
+template <int K1, int K2, bool ZF, int GM>
+auto t3_fn() {
+    return t3::t3_kernel<S3_ST, K1, K2, ZF, GM>;
+}
+
+cudaError_t t3_set_attrs(size_t smem) {
+    cudaError_t e = cudaSuccess;
+    auto set = [&](auto fn) {
+        cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (r != cudaSuccess) e = r;
+    };
+    auto set_gm = [&](auto gm) {
+        constexpr int GM = decltype(gm)::value;
+        // (K_FIRST, K_LAST) is never launched: a 3-step solve would write v while reading it as W^0
+        set(t3_fn<K_FIRST, K_MID, false, GM>()); set(t3_fn<K_FIRST, K_MID, true, GM>());
+        set(t3_fn<K_MID, K_MID, false, GM>());   set(t3_fn<K_MID, K_MID, true, GM>());
+        set(t3_fn<K_MID, K_LAST, false, GM>());  set(t3_fn<K_MID, K_LAST, true, GM>());
     };
     set_gm(std::integral_constant<int, 0>{});
     set_gm(std::integral_constant<int, 1>{});
@@ -1098,7 +1145,34 @@ int plan_launch(whb_ctx *c) {
             c->nparts = std::max(c->nparts, c->gxw[T] * (c->nchw[T] + 2));
         }
     }
-    c->nring = c->wfT == 4 ? 6 : 4;
+    // three-step plan (default for whole-grid single-problem 3D contexts; WHB_T3=0 disables): output
+    // tiles of 12 x 60 (t3::BY x t3::TX), axis-0 chunks of ~256 planes (a chunk re-streams 5 warm-up
+    // planes); small grids whose tiles cannot fill the GPU with chunks of >= 48 planes keep tb2
+    const char *t3env = getenv("WHB_T3");
+    c->t3 = false;
+    if (c->tb2 && whole && c->act1 && c->kern == 2 && c->nbatch == 1 && !(t3env && std::string(t3env) == "0")) {
+        c->smem3 = t3::smem_bytes<S3_ST>();
+        cudaError_t e = t3_set_attrs(c->smem3);
+        if (e != cudaSuccess) return fail(WHB_E_CUDA, std::string("cudaFuncSetAttribute(t3): ") + cudaGetErrorString(e));
+        int nb = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, t3_fn<K_MID, K_MID, false, 2>(), t3::THREADS, c->smem3);
+        if (e != cudaSuccess || nb < 1) return fail(WHB_E_CUDA, "t3 kernel does not fit on an SM");
+        c->gx3 = (int)((n2 - 1 + t3::TX - 1) / t3::TX);
+        c->JT3 = (int)((n1 - 1 + t3::BY - 1) / t3::BY);
+        const long long tiles3 = (long long)c->gx3 * c->JT3;
+        const long long res3 = (long long)sms * nb;
+        // chunks: ~256 planes, but at least 4 waves of CTAs
+        long long nch = std::max<long long>((nplanes + 255) / 256, (4 * res3 + tiles3 - 1) / tiles3);
+        int cl3 = (int)((nplanes + nch - 1) / nch);
+        const char *env3 = getenv("WHB_CHUNK3");
+        if (env3 && atoi(env3) > 0) cl3 = atoi(env3);
+        c->chunk3 = std::max(1, cl3);
+        c->nch3 = (nplanes + c->chunk3 - 1) / c->chunk3;
+        c->t3 = ((long long)c->JT3 * c->nch3 <= 65535) &&
+                (c->chunk3 >= 48 || (t3env && std::string(t3env) == "1"));
+        if (c->t3) c->nparts = std::max(c->nparts, c->gx3 * c->JT3 * c->nch3);
+    }
+    c->nring = (c->wfT == 4 || c->t3) ? 6 : 4;
     // cluster-resident plan (whole-grid 2D with the fields in one cluster's shared memory; the
     // per-launch fit against the step count is cres_fits); WHB_CRES=0 disables, WHB_CRES_CL=n
     // caps the cluster size
@@ -1393,6 +1467,57 @@ int launch_pair_range(whb_ctx *c, int s, int ib, int ie, int cl, int po) {
 
 int launch_pair(whb_ctx *c, int s) { return launch_pair_range(c, s, c->upd_lo, c->upd_hi, c->chunk2, 0); }
 
+// Steps (s, s+1, s+2) of the single member in one pass (step_t3.cuh); `last` when they end the solve.
+int launch_t3(whb_ctx *c, int s, bool last) {
+    const bool zf = c->cur_zf != 0;
+    const Member &m0 = c->h_members[0];
+    const MemberHost &mh = c->mem[c->order[0]];
+    CUtensorMap tw, tp, tf;
+    std::memset(&tp, 0, sizeof(tp));
+    std::memset(&tf, 0, sizeof(tf));
+    WHB_TRY(tensor_map(c, level_ptr(m0, s), t3::RW, t3::WR, &tw));
+    WHB_TRY(tensor_map(c, level_ptr(m0, s - 1), t3::LW, t3::NW, &tp));
+    if (m0.f) WHB_TRY(tensor_map(c, m0.f, t3::LW, t3::NW, &tf));
+    t3::Scal sc;
+    const bool first = (s == 0);
+    sc.h1 = first ? mh.half_dt2 : mh.dt2;
+    sc.cos1 = first ? 1.0 : mh.h_cos[s];
+    sc.cos2 = mh.h_cos[s + 1];
+    sc.cos3 = mh.h_cos[s + 2];
+    sc.dt2 = mh.dt2;
+    sc.c0 = mh.h_acc[0];
+    sc.c1 = mh.h_acc[s + 1];
+    sc.c2 = mh.h_acc[s + 2];
+    sc.c3 = mh.h_acc[s + 3];
+    sc.osc = mh.out_scale;
+    dim3 grid(c->gx3, c->JT3 * c->nch3, 1);
+    const int gm = geom_mode(c);
+    auto go = [&](auto k1, auto k2, auto zft, auto gmt) {
+        t3_fn<decltype(k1)::value, decltype(k2)::value, decltype(zft)::value, decltype(gmt)::value>()
+            <<<grid, t3::THREADS, c->smem3, c->stream>>>(c->geom, c->d_members, s, c->upd_lo, c->upd_hi, c->chunk3,
+                                                         c->JT3, sc, tw, tp, tf);
+    };
+    using KF = std::integral_constant<int, K_FIRST>;
+    using KM = std::integral_constant<int, K_MID>;
+    using KL = std::integral_constant<int, K_LAST>;
+    auto by_gm = [&](auto k1, auto k2, auto zft) {
+        if (gm == 2) go(k1, k2, zft, std::integral_constant<int, 2>{});
+        else if (gm == 1) go(k1, k2, zft, std::integral_constant<int, 1>{});
+        else go(k1, k2, zft, std::integral_constant<int, 0>{});
+    };
+    auto by_zf = [&](auto k1, auto k2) {
+        if (zf) by_gm(k1, k2, std::true_type{});
+        else by_gm(k1, k2, std::false_type{});
+    };
+    if (first && last) return fail(WHB_E_STATE, "t3: a pass may not be both the first and the last");
+    if (first) by_zf(KF{}, KM{});
+    else if (last) by_zf(KM{}, KL{});
+    else by_zf(KM{}, KM{});
+    c->launches++;
+    WHB_CUDA(cudaGetLastError());
+    return 0;
+}
+
 int max_steps(whb_ctx *c);
 
 template <int T, int K1, int K2, bool ZF>
@@ -1601,6 +1726,15 @@ int enqueue_solve(whb_ctx *c, int out_mode) {
     }
     if (c->wfT) {
         WHB_TRY(enqueue_wf(c));
+    } else if (c->t3 && ns > 3) {
+        // passes of 3 steps; a remainder of 2 is one two-step pass, of 1 a single step
+        int s = 0;
+        while (ns - s >= 3) {
+            WHB_TRY(launch_t3(c, s, ns - s == 3));
+            s += 3;
+        }
+        if (ns - s == 2) WHB_TRY(launch_pair(c, s));
+        else if (ns - s == 1) WHB_TRY(launch_step_range(c, s, 0, 1));
     } else if (c->tb2) {
         // pairs (0,1), (2,3), ...; a member with odd n_total takes its last step alone
         for (int s = 0; s < ns; s += 2) {
@@ -1620,6 +1754,7 @@ int enqueue_solve(whb_ctx *c, int out_mode) {
     if (out_mode == WHB_OUT_FPI) {
         int np = c->kern == 3 ? kGenBlocks : c->gx * c->JT * c->nchunks;
         if (c->tb2) np = std::max(np, c->gx2 * c->JT2 * c->nch2);
+        if (c->t3) np = std::max(np, c->gx3 * c->JT3 * c->nch3);
         if (c->wfT) np = std::max(np, std::max(c->gxw[2] * c->nchw[2], c->wfT == 4 ? c->gxw[4] * c->nchw[4] : 0));
         reduce_partials_kernel<<<1, 1024, 0, c->stream>>>(c->d_members, c->nbatch, np, c->d_hist, c->d_counter);
         c->launches++;
@@ -1981,6 +2116,56 @@ int vec_reduce_dot(whb_ctx *c, const double *x, const double *y, double *out) {
 // ==========================================================================================
 // C ABI
 
+// ---- NCCL (dlopen'ed: the process's already-loaded libnccl, e.g. torch's, is reused) ----------
+namespace {
+struct NcclApi {
+    void *h = nullptr;
+    decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+    decltype(&ncclCommInitRank) init_rank = nullptr;
+    decltype(&ncclCommDestroy) destroy = nullptr;
+    decltype(&ncclSend) send = nullptr;
+    decltype(&ncclRecv) recv = nullptr;
+    decltype(&ncclGroupStart) group_start = nullptr;
+    decltype(&ncclGroupEnd) group_end = nullptr;
+    decltype(&ncclAllReduce) all_reduce = nullptr;
+    decltype(&ncclGetErrorString) err = nullptr;
+} g_nccl;
+
+int nccl_load() {
+    if (g_nccl.h) return 0;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return fail(WHB_E_STATE, std::string("libnccl.so.2 not loadable: ") + dlerror());
+    auto sym = [&](const char *n) { return dlsym(h, n); };
+#define WHB_NCCL_SYM(field, name)                                                         \
+    g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(sym(name));                  \
+    if (!g_nccl.field) return fail(WHB_E_STATE, std::string("libnccl lacks ") + name);
+    WHB_NCCL_SYM(get_unique_id, "ncclGetUniqueId")
+    WHB_NCCL_SYM(init_rank, "ncclCommInitRank")
+    WHB_NCCL_SYM(destroy, "ncclCommDestroy")
+    WHB_NCCL_SYM(send, "ncclSend")
+    WHB_NCCL_SYM(recv, "ncclRecv")
+    WHB_NCCL_SYM(group_start, "ncclGroupStart")
+    WHB_NCCL_SYM(group_end, "ncclGroupEnd")
+    WHB_NCCL_SYM(all_reduce, "ncclAllReduce")
+    WHB_NCCL_SYM(err, "ncclGetErrorString")
+#undef WHB_NCCL_SYM
+    g_nccl.h = h;
+    return 0;
+}
+
+void nccl_comm_destroy(ncclComm_t comm) {
+    if (comm && g_nccl.destroy) g_nccl.destroy(comm);
+}
+
+#define WHB_NCCL(call)                                                                         \
+    do {                                                                                       \
+        ncclResult_t _r = (call);                                                              \
+        if (_r != ncclSuccess) return fail(WHB_E_CUDA, std::string(#call) + ": " + g_nccl.err(_r)); \
+    } while (0)
+}  // namespace
+
 extern "C" {
 
 int whb_abi_version(void) { return WHB_ABI_VERSION; }
@@ -2113,6 +2298,14 @@ int whb_destroy(whb_ctx *c) {
     cudaFree(c->d_mgs);
     if (c->h_mgs) cudaFreeHost(c->h_mgs);
     for (auto e : c->ev) cudaEventDestroy(e);
+    if (c->nccl) nccl_comm_destroy(c->nccl);
+    cudaFree(c->d_nccl);
+    if (c->comm) {
+        cudaStreamSynchronize(c->comm);
+        cudaStreamDestroy(c->comm);
+        cudaEventDestroy(c->ev_fork);
+        cudaEventDestroy(c->ev_join);
+    }
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
     return 0;
@@ -2780,7 +2973,7 @@ int whb_copy_async(whb_ctx *c, uint64_t src_ptr, uint64_t dst_ptr, int64_t bytes
     if (bytes <= 0) return 0;
     WHB_TRY(set_dev(c));
     WHB_CUDA(cudaMemcpyAsync((void *)(uintptr_t)dst_ptr, (const void *)(uintptr_t)src_ptr, (size_t)bytes,
-                             cudaMemcpyDefault, c->stream));
+                             cudaMemcpyDefault, c->on_comm ? c->comm : c->stream));
     return 0;
 }
 
@@ -2789,7 +2982,8 @@ int whb_stream_write_u32(whb_ctx *c, uint64_t dev_ptr, uint32_t value) {
     WHB_TRY(set_dev(c));
     WHB_TRY(get_memops());
     // default flags: the write is preceded by a memory fence (earlier copies on the stream are visible first)
-    if (g_write32((CUstream)c->stream, (CUdeviceptr)dev_ptr, value, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+    if (g_write32((CUstream)(c->on_comm ? c->comm : c->stream), (CUdeviceptr)dev_ptr, value,
+                  CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
         return fail(WHB_E_CUDA, "cuStreamWriteValue32 failed");
     return 0;
 }
@@ -2801,6 +2995,95 @@ int whb_stream_wait_u32(whb_ctx *c, uint64_t dev_ptr, uint32_t value) {
     // (int32_t)(*addr - value) >= 0: wrap-safe monotone counters
     if (g_wait32((CUstream)c->stream, (CUdeviceptr)dev_ptr, value, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
         return fail(WHB_E_CUDA, "cuStreamWaitValue32 failed");
+    return 0;
+}
+
+int whb_comm_begin(whb_ctx *c) {
+    if (!c) return fail(WHB_E_ARG, "NULL argument");
+    if (c->on_comm) return fail(WHB_E_STATE, "whb_comm_begin: exchange already open");
+    WHB_TRY(set_dev(c));
+    if (!c->comm) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);  // the exchange gets the higher priority
+        WHB_CUDA(cudaStreamCreateWithPriority(&c->comm, cudaStreamNonBlocking, hi));
+        WHB_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        WHB_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    }
+    WHB_CUDA(cudaEventRecord(c->ev_fork, c->stream));
+    WHB_CUDA(cudaStreamWaitEvent(c->comm, c->ev_fork, 0));
+    c->on_comm = true;
+    return 0;
+}
+
+int whb_comm_end(whb_ctx *c) {
+    if (!c || !c->on_comm) return fail(WHB_E_STATE, "whb_comm_end: no exchange open");
+    WHB_TRY(set_dev(c));
+    c->on_comm = false;
+    WHB_CUDA(cudaEventRecord(c->ev_join, c->comm));
+    return 0;
+}
+
+int whb_comm_join(whb_ctx *c) {
+    if (!c) return fail(WHB_E_ARG, "NULL argument");
+    if (!c->comm) return 0;
+    WHB_TRY(set_dev(c));
+    WHB_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+    return 0;
+}
+
+
+int whb_nccl_unique_id(void *id_out) {
+    if (!id_out) return fail(WHB_E_ARG, "NULL argument");
+    WHB_TRY(nccl_load());
+    ncclUniqueId id;
+    WHB_NCCL(g_nccl.get_unique_id(&id));
+    std::memcpy(id_out, &id, sizeof(id));
+    return 0;
+}
+
+int whb_nccl_init(whb_ctx *c, int nranks, int rank, const void *id) {
+    if (!c || !id) return fail(WHB_E_ARG, "NULL argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(WHB_E_ARG, "bad rank / nranks");
+    if (c->nccl) return fail(WHB_E_STATE, "NCCL communicator already initialised");
+    WHB_TRY(nccl_load());
+    WHB_TRY(set_dev(c));
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    WHB_NCCL(g_nccl.init_rank(&c->nccl, nranks, uid, rank));
+    WHB_CUDA(cudaMalloc(&c->d_nccl, sizeof(double)));
+    return 0;
+}
+
+int whb_nccl_exchange(whb_ctx *c, int n, const uint64_t *send_ptrs, const uint64_t *recv_ptrs, const int64_t *counts,
+                      const int *peers) {
+    if (!c || (n > 0 && (!send_ptrs || !recv_ptrs || !counts || !peers))) return fail(WHB_E_ARG, "NULL argument");
+    if (!c->nccl) return fail(WHB_E_STATE, "whb_nccl_init first");
+    if (!c->on_comm) return fail(WHB_E_STATE, "NCCL transfers go between whb_comm_begin and whb_comm_end");
+    WHB_TRY(set_dev(c));
+    WHB_NCCL(g_nccl.group_start());
+    for (int i = 0; i < n; ++i) {
+        if (counts[i] <= 0) continue;
+        ncclResult_t r = g_nccl.send((const void *)(uintptr_t)send_ptrs[i], (size_t)counts[i], ncclDouble, peers[i],
+                                     c->nccl, c->comm);
+        if (r == ncclSuccess)
+            r = g_nccl.recv((void *)(uintptr_t)recv_ptrs[i], (size_t)counts[i], ncclDouble, peers[i], c->nccl, c->comm);
+        if (r != ncclSuccess) {
+            g_nccl.group_end();
+            return fail(WHB_E_CUDA, std::string("ncclSend/Recv: ") + g_nccl.err(r));
+        }
+    }
+    WHB_NCCL(g_nccl.group_end());
+    return 0;
+}
+
+int whb_nccl_allreduce_sum(whb_ctx *c, double *value) {
+    if (!c || !value) return fail(WHB_E_ARG, "NULL argument");
+    if (!c->nccl) return fail(WHB_E_STATE, "whb_nccl_init first");
+    WHB_TRY(set_dev(c));
+    WHB_CUDA(cudaMemcpyAsync(c->d_nccl, value, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    WHB_NCCL(g_nccl.all_reduce(c->d_nccl, c->d_nccl, 1, ncclDouble, ncclSum, c->nccl, c->stream));
+    WHB_CUDA(cudaMemcpyAsync(value, c->d_nccl, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
     return 0;
 }
 
@@ -2861,7 +3144,7 @@ int whb_host_free(void *ptr) {
 int whb_plan(whb_ctx *c, int *kernel, int *steps_per_pass) {
     if (!c) return fail(WHB_E_ARG, "NULL argument");
     if (kernel) *kernel = c->cres ? 4 : c->kern;
-    if (steps_per_pass) *steps_per_pass = c->cres ? 0 : (c->wfT ? c->wfT : (c->tb2 ? 2 : 1));
+    if (steps_per_pass) *steps_per_pass = c->cres ? 0 : (c->wfT ? c->wfT : (c->t3 ? 3 : (c->tb2 ? 2 : 1)));
     return 0;
 }
 

@@ -39,7 +39,7 @@ from .filters import mode_name
 from .grid import operator_coefficients
 from .timestep import time_schedule
 
-__all__ = ["slab_ranges", "DeviceShard", "TorchHalo", "LocalHalo", "PeerHalo", "PeerSlabGraphs", "run_peer_local_solve", "SlabFPI", "SlabKrylov", "ShardedVectors",
+__all__ = ["slab_ranges", "DeviceShard", "TorchHalo", "NcclHalo", "LocalHalo", "PeerHalo", "PeerSlabGraphs", "run_peer_local_solve", "SlabFPI", "SlabKrylov", "ShardedVectors",
            "run_filtered_solve", "run_local_solve", "halo_items", "exchange_forcing"]
 
 
@@ -219,6 +219,49 @@ class LocalHalo:
                 hi.ctx.copy_device_to(hi.plane_ptr(item, hi_send)[0], lo.ctx, lo.plane_ptr(item, lo_recv)[0], nbytes)
 
 
+class NcclHalo:
+    """Halo exchange with NCCL inside the C ABI (whb_nccl_*): the boundary planes of every item go
+    to the neighbours as one ncclSend/ncclRecv group on the context's exchange stream, forked
+    after the boundary planes (whb_comm_begin) and joined before the next pass (whb_comm_join),
+    so the interior planes run while the planes are on NVLink -- and, unlike the torch.distributed
+    path, the exchange is capturable: SlabFPI(graph=True) replays one CUDA graph per iteration
+    (kernels + NCCL transfers) and all-reduces the residual once (whb_nccl_allreduce_sum)."""
+
+    def __init__(self, shard, dist, rank: int, world: int):
+        self.shard, self.rank, self.world = shard, rank, world
+        uid = [_native.nccl_unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(uid, src=0)
+        shard.ctx.nccl_init(world, rank, uid[0])
+
+    @property
+    def nranks(self):
+        return self.world
+
+    def start(self, shard, items):
+        sends, recvs, counts, peers = [], [], [], []
+        for item, depth in items:
+            for q, side in ((self.rank - 1, "lo"), (self.rank + 1, "hi")):
+                if 0 <= q < self.world:
+                    snd, rcv = halo_planes(shard, side, depth)
+                    sp, n = shard.plane_ptr(item, snd)
+                    rp, _ = shard.plane_ptr(item, rcv)
+                    sends.append(sp)
+                    recvs.append(rp)
+                    counts.append(n * depth)
+                    peers.append(q)
+        shard.ctx.comm_begin()
+        shard.ctx.nccl_exchange(sends, recvs, counts, peers)
+        shard.ctx.comm_end()
+        return shard
+
+    def finish(self, shard):
+        shard.ctx.comm_join()
+
+    def allreduce_sum(self, x: float, shard) -> float:
+        return shard.ctx.nccl_allreduce_sum(x)
+
+
 _PEER_LEVELS = 9  # levels 0..8 cover V and every ring slot (nring <= 6)
 
 
@@ -345,6 +388,7 @@ class PeerHalo:
 
     def start(self, shard, items):
         ctx = shard.ctx
+        ctx.comm_begin()  # copies + flag writes on the exchange stream, after the boundary planes
         for item, depth in items:
             for q, my_side, q_side in ((self.rank - 1, "lo", "hi"), (self.rank + 1, "hi", "lo")):
                 if q not in self.peers:
@@ -357,9 +401,13 @@ class PeerHalo:
         for q, slot in ((self.rank - 1, 1), (self.rank + 1, 0)):  # I am q's upper / lower neighbour
             if q in self.peers:
                 ctx.stream_write_u32(self.peers[q]["flags"] + 4 * slot, self.seq)
+        ctx.comm_end()
         return self.seq
 
     def finish(self, seq):
+        # my outgoing copies done (their source planes may be overwritten from the next pass on),
+        # then the neighbours' copies into my ghost planes (their flags)
+        self.shard.ctx.comm_join()
         for q, slot in ((self.rank - 1, 0), (self.rank + 1, 1)):
             if q in self.peers:
                 self.shard.ctx.stream_wait_u32(self.flags + 4 * slot, seq)
@@ -664,10 +712,12 @@ class SlabFPI:
         exchange_forcing(shard, halo)
         # graph=True (PeerHalo only): after one host-driven iteration, each iteration is one CUDA
         # graph replay (kernels, peer copies, flag writes / waits) + the residual all-reduce
-        self.graph = bool(graph) and isinstance(halo, PeerHalo)
+        self.graph = bool(graph) and isinstance(halo, (PeerHalo, NcclHalo))
+        self._peer = isinstance(halo, PeerHalo)
         self._gid = None
         if self.graph:
-            halo.epoch_end(shard)
+            if self._peer:
+                halo.epoch_end(shard)
             shard.synchronize()
         self.reset()
 
@@ -682,7 +732,8 @@ class SlabFPI:
         else:
             rs = run_filtered_solve(self.shard, self.halo)
             if self.graph:
-                self.halo.epoch_end(self.shard)
+                if self._peer:
+                    self.halo.epoch_end(self.shard)
                 self.shard.synchronize()
         total = self.halo.allreduce_sum(rs, self.shard) if self.halo.nranks > 1 else rs
         if self.graph and self._gid is None:
@@ -690,7 +741,8 @@ class SlabFPI:
             self.shard.ctx.capture_begin()
             try:
                 run_filtered_solve(self.shard, self.halo)
-                self.halo.epoch_end(self.shard)
+                if self._peer:
+                    self.halo.epoch_end(self.shard)
             finally:
                 self._gid = self.shard.ctx.capture_end()
         return math.sqrt(total) / math.sqrt(self.grid.size)

@@ -227,3 +227,46 @@ def test_peer_slab_graphs_match_single_domain_bitwise(gpu_available, cells, nsla
     np.testing.assert_allclose(np.sqrt(sums) / np.sqrt(g.size), rref[1:], rtol=1e-12)
     for h in halos:
         h.close()
+
+
+def test_nccl_exchange_in_the_c_abi_self_peer_and_graph(gpu_available):
+    """The C-ABI NCCL path on one GPU: a one-rank communicator whose exchange sends two owned
+    planes to itself (peer = own rank) into the ghost planes, on the exchange stream between
+    whb_comm_begin / whb_comm_end, joined by whb_comm_join -- eagerly and replayed from a captured
+    CUDA graph; the ghost planes then hold the owned planes' bits."""
+    import paper_2504_03074_b200 as wh
+    from paper_2504_03074_b200 import _native
+    from paper_2504_03074_b200.slab import DeviceShard, level
+
+    g = wh.build_grid(3, [(0.0, 1.0)] * 3, (20, 18, 22), "dirichlet")
+    sh = DeviceShard(g, (0, g.shape[0]))
+    ctx = sh.ctx
+    ctx.nccl_init(1, 0, _native.nccl_unique_id())
+    rng = np.random.default_rng(4)
+    gh, n = sh.gh, sh.nloc
+
+    def once():
+        sp, cnt = sh.plane_ptr(level(0), gh + 3)
+        rp, _ = sh.plane_ptr(level(0), gh - 2)
+        ctx.comm_begin()
+        ctx.nccl_exchange([sp], [rp], [2 * cnt], [0])
+        ctx.comm_end()
+        ctx.comm_join()
+
+    for mode in ("eager", "graph"):
+        v = rng.standard_normal(g.shape)
+        sh.upload(_native.V, v)
+        ctx.synchronize()
+        if mode == "eager":
+            once()
+        else:
+            ctx.capture_begin()
+            once()
+            gid = ctx.capture_end()
+            ctx.graph_launch(gid)
+        ctx.synchronize()
+        ghost = sh.planes(level(0), gh - 2, 2).cpu().numpy()
+        own = sh.planes(level(0), gh + 3, 2).cpu().numpy()
+        assert np.array_equal(ghost, own) and np.any(own != 0.0), mode
+    assert ctx.nccl_allreduce_sum(2.5) == 2.5
+    ctx.close()

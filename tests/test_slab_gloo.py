@@ -194,3 +194,62 @@ def test_batched_distributed_gathers_runs_world2():
         v, res = O.fpi(f, g.spacing, sc, 2)
         assert got[0][1][k] == list(res) and got[1][1][k] == list(res)
         assert np.array_equal(got[0][2][k], v)
+
+
+def test_nccl_halo_posts_the_torch_halo_pairs():
+    """NcclHalo (the C-ABI NCCL path) posts, per item and neighbour, the same (send planes, recv
+    planes, peer) as the torch.distributed path, as ONE group between whb_comm_begin / end, and
+    joins in finish -- checked with a recording stand-in for the context (world 3, middle rank)."""
+    from paper_2504_03074_b200.slab import NcclHalo, halo_planes, level, field
+
+    calls = []
+
+    class Ctx:
+        def nccl_init(self, *a):
+            calls.append(("init",) + a[:2])
+
+        def comm_begin(self):
+            calls.append(("begin",))
+
+        def comm_end(self):
+            calls.append(("end",))
+
+        def comm_join(self):
+            calls.append(("join",))
+
+        def nccl_exchange(self, *a):
+            calls.append(("exchange",) + tuple(list(x) for x in a))
+
+    class Shard:
+        gh, nloc = 2, 7
+        ctx = Ctx()
+
+        def plane_ptr(self, item, plane):
+            base = {level(3): 10_000, level(2): 20_000, field(_native.F): 30_000}[item]
+            return base + 100 * plane, 50
+
+    import paper_2504_03074_b200.slab as slab_mod
+
+    old = slab_mod._native.nccl_unique_id
+    slab_mod._native.nccl_unique_id = lambda: b"x" * 128
+    try:
+        sh = Shard()
+
+        class Dist:
+            @staticmethod
+            def broadcast_object_list(lst, src):
+                lst[0] = b"x" * 128
+
+        h = NcclHalo(sh, Dist, 1, 3)
+        h.finish(h.start(sh, [(level(3), 2), (level(2), 1)]))
+    finally:
+        slab_mod._native.nccl_unique_id = old
+    assert calls[0] == ("init", 3, 1)
+    assert [c[0] for c in calls[1:]] == ["begin", "exchange", "end", "join"]
+    _, sends, recvs, counts, peers = calls[2]
+    want = []
+    for item, depth, base in ((level(3), 2, 10_000), (level(2), 1, 20_000)):
+        for q, side in ((0, "lo"), (2, "hi")):
+            snd, rcv = halo_planes(sh, side, depth)
+            want.append((base + 100 * snd, base + 100 * rcv, 50 * depth, q))
+    assert list(zip(sends, recvs, counts, peers)) == want
