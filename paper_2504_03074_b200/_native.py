@@ -535,11 +535,6 @@ class Context:
         return float(v[0])
 
 
-def nccl_unique_id() -> bytes:
-    buf = ctypes.create_string_buffer(128)
-    check(load().whb_nccl_unique_id(buf), "whb_nccl_unique_id")
-    return buf.raw
-
     def stream_ptr(self) -> int:
         p = ctypes.c_uint64(0)
         check(load().whb_stream_ptr(self._h, ctypes.byref(p)), "whb_stream_ptr")
@@ -586,3 +581,9 @@ def nccl_unique_id() -> bytes:
         check(load().whb_geometry(self._h, s.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), ctypes.byref(p),
                                   ctypes.byref(n)), "whb_geometry")
         return tuple(int(x) for x in s), p.value, n.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    check(load().whb_nccl_unique_id(buf), "whb_nccl_unique_id")
+    return buf.raw

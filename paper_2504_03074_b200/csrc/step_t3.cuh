@@ -114,7 +114,6 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int t = plane - pfirst;
         mbar_wait(bars + (t % ST), (t / ST) & 1);
     };
-    auto stage_of = [&](int plane) -> const double * { return smem + (size_t)((plane - pfirst) % ST) * STAGE; };
 
     if (threadIdx.x == 0) {
         for (int t = 0; t < ST; ++t) mbar_init(bars + t, 1);
@@ -129,6 +128,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const bool yin = (y >= g.j_lo) && (y < g.j_hi);
     const bool xin0 = (x >= 1) && (x < g.n2 - 1);
     const bool xin1 = (x + 1 >= 1) && (x + 1 < g.n2 - 1);
+    const bool xall = __all_sync(0xffffffffu, xin0 && xin1);  // every column of the warp interior
     const bool do2 = (w >= 1) && (w <= NW - 2);        // warp-uniform: rows of level 2
     const bool do3 = (w >= 2) && (w <= NW - 3);        // rows of level 3 (the output tile)
     // output points: the tile's rows / columns, interior only
@@ -142,9 +142,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     auto plane_in = [&](int p) { return p >= g.i_lo && p < g.i_hi; };
     auto shl = [&](double v) { return __shfl_up_sync(0xffffffffu, v, 1); };
     auto shr = [&](double v) { return __shfl_down_sync(0xffffffffu, v, 1); };
+    // Dirichlet / out-of-domain points of a level are 0; warp-uniform fast path when all are inside
+    auto mask = [&](bool pin, double a, double b) -> double2 {
+        if (pin && xall) return make_double2(a, b);
+        return make_double2((pin && xin0) ? a : 0.0, (pin && xin1) ? b : 0.0);
+    };
 
     // register queues (own column pair): W^s at planes i+1 .. i-4, level 1 at i .. i-4,
-    // level 2 at i-2 .. i-5, f at i .. i-4
+    // level 2 at i-2 .. i-5, f at i .. i-4.  The plane loop is unrolled by ST = 6 (a multiple of
+    // the level-ring period 3), so the queue shifts are register renames and every stage / ring
+    // slot below is a compile-time constant.
     const double2 z2 = make_double2(0.0, 0.0);
     double2 ws0 = z2, ws1 = z2, ws2 = z2, ws3 = z2, ws4 = z2, ws5 = z2;  // ws0 = W^s(i+1), ws1 = W^s(i), ...
     double2 q10 = z2, q11 = z2, q12 = z2, q13 = z2, q14 = z2;           // q1k = level 1 at plane i-k
@@ -155,8 +162,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     // W^s centres of planes i0-3 and i0-2 (the first iteration, i = i0-2, adds plane i0-1)
     wait_plane(pfirst);
     wait_plane(pfirst + 1);
-    ws1 = *reinterpret_cast<const double2 *>(stage_of(pfirst) + wrow);    // becomes W^s(i-1) below
-    ws0 = *reinterpret_cast<const double2 *>(stage_of(pfirst + 1) + wrow);
+    ws1 = *reinterpret_cast<const double2 *>(smem + 0 * STAGE + wrow);    // becomes W^s(i-1) below
+    ws0 = *reinterpret_cast<const double2 *>(smem + 1 * STAGE + wrow);
     // the filter-sum input and v of the first output plane
     const bool want_v = (K2 == K_LAST) && m.out_mode != WHB_OUT_PLAIN;
     auto ld2 = [&](const double *base, int p) -> double2 {
@@ -170,47 +177,48 @@ __global__ void __launch_bounds__(THREADS, 1)
         issue(pfirst + ST);
     }
 
-    for (int i = i0 - 2; i <= i1 + 3; ++i) {
+    const int ibeg = i0 - 2;  // iteration i: level 1 at i, level 2 at i-2, level 3 at i-4
+    const int iend = i1 + 3;
+    // copy K of a round: i = ibeg + ST*round + K; plane p <-> stage slot (p - pfirst) % ST
+    auto iter = [&](auto kc, const int i, const int round) {
+        constexpr int K = decltype(kc)::value;
+        constexpr int SL_I = (K + 1) % ST;      // stage of plane i
+        constexpr int SL_N = (K + 2) % ST;      // stage of plane i+1
+        constexpr int R1W = K % 3;              // level-1 ring slot written (plane i)
+        constexpr int R12 = (K + 1) % 3;        // level-1 slot of plane i-2 / level-2 slot written (i-2)
+        constexpr int R24 = (K + 2) % 3;        // level-2 slot of plane i-4
         // shift the queues: plane i+1 of W^s enters
         ws5 = ws4; ws4 = ws3; ws3 = ws2; ws2 = ws1; ws1 = ws0;
-        const bool has_next = (i + 1 <= plast);
-        if (has_next) {
-            wait_plane(i + 1);
-            ws0 = *reinterpret_cast<const double2 *>(stage_of(i + 1) + wrow);
-        } else {
-            ws0 = z2;
+        if (i + 1 <= plast) {
+            mbar_wait(bars + SL_N, (round + (K + 2) / ST) & 1);
+            ws0 = *reinterpret_cast<const double2 *>(smem + SL_N * STAGE + wrow);
         }
         q14 = q13; q13 = q12; q12 = q11; q11 = q10;
         q23 = q22; q22 = q21; q21 = q20;
         fq4 = fq3; fq3 = fq2; fq2 = fq1; fq1 = fq0;
-        const int sl1 = (i % 3 + 3) % 3;
 
         // ---- level 1 at plane i (step s)
         if (i <= i1 + 1) {
-            const double *st = stage_of(i);
+            const double *st = smem + SL_I * STAGE;
             const double2 yl = *reinterpret_cast<const double2 *>(st + wrow - RW);
             const double2 yh = *reinterpret_cast<const double2 *>(st + wrow + RW);
             double xl = shl(ws1.y), xh = shr(ws1.x);
             if (lane == 0) xl = st[wrow - 1];
             if (lane == 31) xh = st[wrow + 2];
             const double2 pv = LOAD_P ? *reinterpret_cast<const double2 *>(st + W_EL + prow) : z2;
-            fq0 = ZF ? z2 : *reinterpret_cast<const double2 *>(st + W_EL + P_EL + prow);
+            if (!ZF) fq0 = *reinterpret_cast<const double2 *>(st + W_EL + P_EL + prow);
             const double a = update_point<K1, ZF, true, SQ, C2M>(g, ws2.x, ws1.x, ws0.x, yl.x, yh.x, xl, ws1.y, fq0.x,
                                                                pv.x, sc.h1, sc.cos1);
             const double b = update_point<K1, ZF, true, SQ, C2M>(g, ws2.y, ws1.y, ws0.y, yl.y, yh.y, ws1.x, xh, fq0.y,
                                                                pv.y, sc.h1, sc.cos1);
-            const bool pin = plane_in(i) && yin;
-            q10 = make_double2((pin && xin0) ? a : 0.0, (pin && xin1) ? b : 0.0);
-            *reinterpret_cast<double2 *>(l1buf + sl1 * L1_EL + prow) = q10;
-        } else {
-            q10 = z2;
-            fq0 = z2;
+            q10 = mask(plane_in(i) && yin, a, b);
+            *reinterpret_cast<double2 *>(l1buf + R1W * L1_EL + prow) = q10;
         }
 
         // ---- level 2 at plane i-2 (step s+1): level 1 at i-3, i-2, i-1 (queue), rows y-1, y+1 (ring)
         const int p2 = i - 2;
         if (do2 && p2 >= i0 - 1 && p2 <= i1) {
-            const double *l1 = l1buf + ((p2 % 3 + 3) % 3) * L1_EL;
+            const double *l1 = l1buf + R12 * L1_EL;
             const double2 yl = *reinterpret_cast<const double2 *>(l1 + prow - LW);
             const double2 yh = *reinterpret_cast<const double2 *>(l1 + prow + LW);
             const double xl = shl(q12.y), xh = shr(q12.x);
@@ -219,17 +227,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                                                                   fq2.x, ws3.x, sc.dt2, sc.cos2);
             const double b = update_point<K_MID, ZF, true, SQ, C2M>(g, q13.y, q12.y, q11.y, yl.y, yh.y, q12.x, xh,
                                                                   fq2.y, ws3.y, sc.dt2, sc.cos2);
-            const bool pin = plane_in(p2) && yin;
-            q20 = make_double2((pin && xin0) ? a : 0.0, (pin && xin1) ? b : 0.0);
-            *reinterpret_cast<double2 *>(l2buf + ((p2 % 3 + 3) % 3) * L2_EL + prow - LW) = q20;
-        } else {
-            q20 = z2;
+            q20 = mask(plane_in(p2) && yin, a, b);
+            *reinterpret_cast<double2 *>(l2buf + R12 * L2_EL + prow - LW) = q20;
         }
 
         // ---- level 3 at plane i-4 (step s+2) on the tile, then the filter sum and the outputs
         const int p3 = i - 4;
         if (do3 && p3 >= i0 && p3 < i1) {
-            const double *l2 = l2buf + ((p3 % 3 + 3) % 3) * L2_EL;
+            const double *l2 = l2buf + R24 * L2_EL;
             const double2 yl = *reinterpret_cast<const double2 *>(l2 + prow - 2 * LW);
             const double2 yh = *reinterpret_cast<const double2 *>(l2 + prow);
             const double xl = shl(q22.y), xh = shr(q22.x);
@@ -240,11 +245,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                                                                    fq4.y, q14.y, sc.dt2, sc.cos3);
             // next output plane's acc / v (one iteration ahead: hides the HBM latency)
             const double2 acc_c = acc_n, v_c = v_n;
-            if (p3 + 1 < i1 && (ok0 || ok1)) {
-                if (K1 != K_FIRST) acc_n = ld2(m.acc, p3 + 1);
-                if (want_v) v_n = ld2(m.v, p3 + 1);
-            }
             if (ok0 || ok1) {
+                if (p3 + 1 < i1) {
+                    if (K1 != K_FIRST) acc_n = ld2(m.acc, p3 + 1);
+                    if (want_v) v_n = ld2(m.v, p3 + 1);
+                }
                 // acc (+ c0 W^0 on the first pass) + c1 W^{s+1} + c2 W^{s+2} + c3 W^{s+3}, in step order
                 double s0, s1;
                 if (K1 == K_FIRST) {  // timestep.py:284 then :298 per step
@@ -288,6 +293,26 @@ __global__ void __launch_bounds__(THREADS, 1)
             fence_proxy_async();
             issue(i + ST);
         }
+    };
+    using I0 = std::integral_constant<int, 0>;
+    using I1 = std::integral_constant<int, 1>;
+    using I2 = std::integral_constant<int, 2>;
+    using I3 = std::integral_constant<int, 3>;
+    using I4 = std::integral_constant<int, 4>;
+    using I5 = std::integral_constant<int, 5>;
+    static_assert(ST == 6, "the unrolled plane loop assumes 6 stages");
+    for (int round = 0, ib = ibeg; ib <= iend; ++round, ib += ST) {
+        iter(I0{}, ib, round);
+        if (ib + 1 > iend) break;
+        iter(I1{}, ib + 1, round);
+        if (ib + 2 > iend) break;
+        iter(I2{}, ib + 2, round);
+        if (ib + 3 > iend) break;
+        iter(I3{}, ib + 3, round);
+        if (ib + 4 > iend) break;
+        iter(I4{}, ib + 4, round);
+        if (ib + 5 > iend) break;
+        iter(I5{}, ib + 5, round);
     }
     if (K2 == K_LAST && m.out_mode == WHB_OUT_FPI) {
         const double t = block_sum(rsum);

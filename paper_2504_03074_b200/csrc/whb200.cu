@@ -851,9 +851,9 @@ cudaError_t tb2_set_attrs(size_t smem) {
     return e;
 }
 
-// Three-step 3D kernel (step_t3.cuh): 5 TMA stages of 26 KB + the level-1/2 rings, 1 CTA/SM.
+// Three-step 3D kernel (step_t3.cuh): 6 TMA stages of 26 KB + the level-1/2 rings (202 KB), 1 CTA/SM.
 #ifndef WHB_S3_ST
-#define WHB_S3_ST 5
+#define WHB_S3_ST 6
 #endif
 constexpr int S3_ST = WHB_S3_ST;
 

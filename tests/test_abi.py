@@ -55,3 +55,19 @@ def test_null_arguments_are_rejected():
     assert lib.whb_destroy(None) == 0
     assert lib.whb_fpi(None, 1, -1.0, None, None) == _native.E_ARG
     assert lib.whb_fpi_scaled(None, 1, -1.0, 1.0, None, None) == _native.E_ARG
+
+
+def test_context_binding_is_complete():
+    """Every method the product modules call on a context exists on _native.Context (a module-level
+    def placed inside the class once silently truncated it; this catches that on the CPU)."""
+    import inspect
+    import re as _re
+
+    pkg = os.path.join(ROOT, "paper_2504_03074_b200")
+    used = set()
+    for fn in os.listdir(pkg):
+        if fn.endswith(".py") and fn != "_native.py":
+            used |= set(_re.findall(r"\bctx\.([a-z_][a-z0-9_]*)\(", open(os.path.join(pkg, fn)).read()))
+    have = {n for n, _ in inspect.getmembers(_native.Context)}
+    missing = sorted(used - have)
+    assert not missing, missing
