@@ -117,6 +117,13 @@ int whb_set_schedule(whb_ctx *ctx, int member, int n_total, double half_dt2, dou
  * (GridField.set_values, grid.py:218-227).  member is ignored for a shared f. */
 int whb_upload(whb_ctx *ctx, int field, int member, const double *host);
 int whb_download(whb_ctx *ctx, int field, int member, double *host);
+/* The same with a strided host view (e.g. the interior of a ghost-padded GridField buffer,
+ * grid.py:185-216): element strides between storage planes and between rows, the last axis
+ * contiguous; one 3D copy, no host-side packing. */
+int whb_upload_strided(whb_ctx *ctx, int field, int member, const double *host, int64_t plane_stride,
+                       int64_t row_stride);
+int whb_download_strided(whb_ctx *ctx, int field, int member, double *host, int64_t plane_stride,
+                         int64_t row_stride);
 int whb_zero(whb_ctx *ctx, int field, int member);
 
 /* One filtered solve W(v, f) for every member, device resident

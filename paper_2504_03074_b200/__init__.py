@@ -34,7 +34,8 @@ from .driver import (
 )
 from .filters import ExplicitStabilityError, FilterConfig, ResonanceError, TimeMode, alpha_d
 from .grid import BC, CartesianGrid, DiscreteOperator, GridField, build_grid, stencil_coefficients
-from .linalg import SolveReport, device_gmres
+from .implicit import HostImplicitSolver, make_implicit_solver
+from .linalg import SolveReport, device_gmres, gmres_solve
 from .timestep import (
     TimeCorrection,
     WaveState,
@@ -42,6 +43,7 @@ from .timestep import (
     correct_explicit,
     correct_implicit,
     step_explicit,
+    step_implicit,
     time_schedule,
     wave_solve_filtered,
 )

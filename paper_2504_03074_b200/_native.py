@@ -38,7 +38,7 @@ EXPORTS = (
     "whb_imp_apply", "whb_imp_rhs", "whb_vec_xpay", "whb_mg_setup", "whb_mg_vcycle", "whb_tri_setup", "whb_tri_solve",
     "whb_cg_begin", "whb_cg_iterate", "whb_vec_mgs",
     "whb_comm_begin", "whb_comm_end", "whb_comm_join", "whb_nccl_unique_id", "whb_nccl_init", "whb_nccl_exchange",
-    "whb_nccl_allreduce_sum",
+    "whb_nccl_allreduce_sum", "whb_upload_strided", "whb_download_strided",
 )
 
 _lib = None
@@ -86,6 +86,8 @@ def load():
         "whb_resid_read": ([vp, dp], c_int),
         "whb_stream_write_u32": ([vp, c_u64, ctypes.c_uint32], c_int),
         "whb_stream_wait_u32": ([vp, c_u64, ctypes.c_uint32], c_int),
+        "whb_upload_strided": ([vp, c_int, c_int, dp, c_i64, c_i64], c_int),
+        "whb_download_strided": ([vp, c_int, c_int, dp, c_i64, c_i64], c_int),
         "whb_comm_begin": ([vp], c_int),
         "whb_comm_end": ([vp], c_int),
         "whb_comm_join": ([vp], c_int),
@@ -291,6 +293,37 @@ class Context:
                 or a.shape != self.local_shape:
             raise ValueError(f"{what}: expected a C-contiguous float64 array of shape {self.local_shape}")
         return a
+
+    def _strides(self, a):
+        """(plane, row) element strides of a float64 view whose last axis is contiguous, in the
+        context's storage axes (2D (n0, n1) -> planes = rows of axis 0), or None."""
+        if not isinstance(a, np.ndarray) or a.dtype != np.float64 or a.shape != self.local_shape:
+            return None
+        st = [x // 8 for x in a.strides]
+        if a.strides[-1] != 8 or any(x % 8 for x in a.strides):
+            return None
+        if self.ndim == 3:
+            return st[0], st[1]
+        if self.ndim == 2:
+            return st[0], st[0]
+        return None
+
+    def upload_view(self, field, values, member=0):
+        """upload() of a strided view (e.g. GridField.values) without packing it on the host."""
+        st = None if (isinstance(values, np.ndarray) and values.flags.c_contiguous) else self._strides(values)
+        if st is None:
+            return self.upload(field, values, member)
+        check(load().whb_upload_strided(self._h, int(field), int(member), _dp(values), st[0], st[1]),
+              "whb_upload_strided")
+
+    def download_into(self, field, out, member=0):
+        """download() straight into a strided writeable view (e.g. a new GridField's interior)."""
+        st = None if out.flags.c_contiguous else self._strides(out)
+        if st is None or not out.flags.writeable:
+            return self.download(field, member, out=out)
+        check(load().whb_download_strided(self._h, int(field), int(member), _dp(out), st[0], st[1]),
+              "whb_download_strided")
+        return out
 
     def download(self, field, member=0, out=None):
         out = self._out(out, "download")

@@ -2449,6 +2449,50 @@ int whb_download(whb_ctx *c, int field, int member, double *host) {
     return 0;
 }
 
+namespace {
+// One 3D copy between a strided host view of the owned planes (element strides sp between
+// storage planes and sr between rows, last axis contiguous) and the pitched device field.
+int copy_field_strided(whb_ctx *c, double *dev, double *host, int64_t sp, int64_t sr, bool h2d) {
+    const int64_t n1 = c->gshape[1], n2 = c->gshape[2];
+    if (sr < n2 || (n1 > 1 && sp % sr) || sp < n1 * sr)
+        return fail(WHB_E_ARG, "strided host view: row / plane strides do not describe the field");
+    cudaMemcpy3DParms q = {};
+    const size_t hpitch = (size_t)(n1 > 1 ? sr : sp) * sizeof(double);
+    const size_t hrows = (size_t)(n1 > 1 ? sp / sr : 1);
+    cudaPitchedPtr hp = make_cudaPitchedPtr(host, hpitch, (size_t)n2, hrows);
+    cudaPitchedPtr dp = make_cudaPitchedPtr(owned(dev, c), (size_t)c->P * sizeof(double), (size_t)n2, (size_t)n1);
+    q.srcPtr = h2d ? hp : dp;
+    q.dstPtr = h2d ? dp : hp;
+    q.extent = make_cudaExtent((size_t)n2 * sizeof(double), (size_t)n1, (size_t)c->nloc);
+    q.kind = h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+    WHB_CUDA(cudaMemcpy3DAsync(&q, c->stream));
+    return 0;
+}
+}  // namespace
+
+int whb_upload_strided(whb_ctx *c, int field, int member, const double *host, int64_t plane_stride,
+                       int64_t row_stride) {
+    if (!c || !host) return fail(WHB_E_ARG, "NULL argument");
+    if (member < 0 || member >= c->nbatch || field < 0 || field > WHB_WD) return fail(WHB_E_ARG, "bad field/member");
+    WHB_TRY(set_dev(c));
+    if (field == WHB_OUT) WHB_TRY(ensure_out(c, member));
+    double *d = field_ptr(c, field, member);
+    WHB_TRY(copy_field_strided(c, d, const_cast<double *>(host), plane_stride, row_stride, true));
+    WHB_TRY(zero_bnd(c, d));
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int whb_download_strided(whb_ctx *c, int field, int member, double *host, int64_t plane_stride, int64_t row_stride) {
+    if (!c || !host) return fail(WHB_E_ARG, "NULL argument");
+    if (member < 0 || member >= c->nbatch || field < 0 || field > WHB_WD) return fail(WHB_E_ARG, "bad field/member");
+    WHB_TRY(set_dev(c));
+    if (field == WHB_OUT) WHB_TRY(ensure_out(c, member));
+    WHB_TRY(copy_field_strided(c, field_ptr(c, field, member), host, plane_stride, row_stride, false));
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
 int whb_zero(whb_ctx *c, int field, int member) {
     if (!c) return fail(WHB_E_ARG, "NULL argument");
     if (member < 0 || member >= c->nbatch || field < 0 || field > WHB_WD) return fail(WHB_E_ARG, "bad field/member");

@@ -47,6 +47,7 @@ class DeviceProblem:
         set_device_operator(self.ctx, grid, order, c)
         self._sched = [None] * nbatch
         self._forcing = [None] * (1 if shared_forcing else nbatch)
+        self._forcing_key = {}
         self.shared_forcing = shared_forcing
 
     @property
@@ -60,6 +61,27 @@ class DeviceProblem:
             self.ctx.set_schedule(member, sched)
             self._sched[member] = key
 
+    def set_forcing_field(self, field, member: int = 0) -> bool:
+        """set_forcing() for a GridField (ours or the reference's): the device copy is keyed on
+        the field object and its write counter (``generation``, grid.py:185-216: values are a
+        read-only view, every write goes through set_values / _touch), so an unchanged forcing
+        costs no host pass over its values; the cache holds the field, so its id cannot be
+        reused while it is keyed.  Returns True when f is identically zero."""
+        gen = getattr(field, "generation", None)
+        if gen is None:
+            return self.set_forcing(field.values, member)
+        slot = 0 if self.shared_forcing else member
+        key = (id(field), gen)
+        cached = self._forcing_key.get(slot)
+        if cached is not None and cached[0] == key and cached[1] is field:
+            return cached[2]
+        vals = field.values
+        self.ctx.upload_view(_native.F, vals, member)
+        zero = not np.any(vals)  # once per upload (exact: a dot product could underflow to 0)
+        self._forcing[slot] = None  # the array-keyed cache no longer describes the device copy
+        self._forcing_key[slot] = (key, field, zero)
+        return zero
+
     def set_forcing(self, values, member: int = 0) -> bool:
         """Upload f unless the device already holds exactly these values; returns
         True when f is identically zero (the zero-forcing kernel variant applies)."""
@@ -69,6 +91,7 @@ class DeviceProblem:
         if cached is None or cached.shape != vals.shape or not np.array_equal(cached, vals):
             self.ctx.upload(_native.F, vals, member)
             self._forcing[slot] = np.array(vals)
+            self._forcing_key.pop(slot, None)
         return not np.any(self._forcing[slot])
 
     def close(self):

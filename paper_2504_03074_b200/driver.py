@@ -25,7 +25,7 @@ from .filters import FilterConfig, ResonanceError, TimeMode, mode_name
 from .grid import DiscreteOperator, GridField, bc_name
 from .implicit import correct_implicit, implicit_solver_for, implicit_wave_solve
 from .linalg import device_gmres
-from .timestep import correct_explicit, time_schedule
+from .timestep import correct_explicit, field_from_device, time_schedule
 
 __all__ = [
     "HelmholtzProblem", "WaveHoltzRun", "NearSingularError", "gaussian_source", "multi_gaussian_source",
@@ -243,7 +243,7 @@ def fpi_solve(problem, config, tol=1e-10, maxit=500, inner_tol=1e-12, device_sta
     if mode_name(cfg.mode) == "implicit":
         return _fpi_implicit(problem, cfg, corr, dp, tol, maxit, inner_tol)
     dp.set_schedule(time_schedule(corr, cfg))
-    dp.set_forcing(problem.forcing.values)
+    dp.set_forcing_field(problem.forcing)
     dp.ctx.zero(_native.V)
     root_n = math.sqrt(problem.grid.size)
     residuals = []
@@ -260,7 +260,7 @@ def fpi_solve(problem, config, tol=1e-10, maxit=500, inner_tol=1e-12, device_sta
         k = len(residuals)
         converged = k > 0 and residuals[-1] <= tol
     wall = time.perf_counter() - t0
-    v = GridField.from_values(problem.grid, dp.ctx.download(_native.V), ghost=2)
+    v = field_from_device(GridField, problem.grid, 2, dp.ctx, _native.V)
     run = WaveHoltzRun(method="fpi", periods=cfg.periods, residuals=residuals, iterations=k,
                        converged=converged, wall_time=wall, inner_iterations=0)
     return v, run
@@ -280,7 +280,7 @@ def _fpi_implicit(problem, cfg, corr, dp, tol, maxit, inner_tol):
     ctx = dp.ctx
     solver, (vnew, diff_id) = _implicit_state(problem, dp, corr, inner_tol)
     sched = time_schedule(corr, cfg)
-    dp.set_forcing(problem.forcing.values)
+    dp.set_forcing_field(problem.forcing)
     ctx.zero(_native.V)
     root_n = math.sqrt(problem.grid.size)
     residuals = []
@@ -350,7 +350,7 @@ def krylov_solve(problem, config, tol=1e-10, restart=50, maxit=500, deflation=No
     ctx = dp.ctx
     t0 = time.perf_counter()
     implicit = mode_name(cfg.mode) == "implicit"
-    dp.set_forcing(problem.forcing.values)
+    dp.set_forcing_field(problem.forcing)
     ctx.zero(_native.V)
     if implicit:
         solver, _ = _implicit_state(problem, dp, corr, inner_tol)
@@ -394,7 +394,7 @@ class HostFPIStep:
         self.corr = corr
         self.dp = device_state or _device_for(problem)
         self.dp.set_schedule(time_schedule(corr, cfg))
-        self.dp.set_forcing(problem.forcing.values)
+        self.dp.set_forcing_field(problem.forcing)
         self._root_n = math.sqrt(problem.grid.size)
         self._implicit = None
         if mode_name(cfg.mode) == "implicit":

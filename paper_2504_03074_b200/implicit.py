@@ -275,3 +275,44 @@ def implicit_wave_solve(dp, solver: DeviceImplicitSolver, corr, sched: dict, v_i
     else:
         ctx.scale_into(sched["out_scale"], ws.acc, out_id)
     return solver.inner - inner0
+
+
+class HostImplicitSolver:
+    """make_implicit_solver's object (timestep.py:173-247, _ImplicitSolver): ``solver(rhs, guess)``
+    solves (I - (dt^2/2) c^2 L_h) w = rhs for host arrays and returns (w, iterations); ``apply``
+    is the operator; ``inner`` counts inner iterations.  The solve runs on the device (the same
+    DeviceImplicitSolver the drivers use: tridiagonal elimination, MG- or tridiagonal-
+    preconditioned CG), and wave_solve_filtered(linear_solver=this) uses ``device_solver``
+    directly -- so the reference's driver, rebound onto this package, builds no
+    CPU multigrid hierarchy."""
+
+    def __init__(self, op, dt: float, tol: float = 1e-12, maxit: int = 400):
+        from .device import device_problem
+
+        self.op, self.dt, self.tol, self.maxit = op, float(dt), float(tol), int(maxit)
+        self.inner = 0
+        self._dp = device_problem(op.grid, c=op.c, order=op.order)
+        self.device_solver = implicit_solver_for(self._dp, op.grid, op.order, op.c, self.dt, tol=self.tol,
+                                                 maxit=self.maxit)
+        self._ids = self._dp.ctx.vec_reserve(3)
+
+    def apply(self, values: np.ndarray) -> np.ndarray:
+        ctx = self._dp.ctx
+        x, y, _ = self._ids
+        ctx.vec_upload(x, np.asarray(values, dtype=float))
+        self.device_solver.apply(x, y)
+        return ctx.vec_download(y)
+
+    def __call__(self, rhs: np.ndarray, guess: np.ndarray | None = None):
+        ctx = self._dp.ctx
+        r, g, x = self._ids
+        ctx.vec_upload(r, np.asarray(rhs, dtype=float))
+        ctx.vec_upload(g, np.zeros(np.shape(rhs)) if guess is None else np.asarray(guess, dtype=float))
+        its = self.device_solver.solve(r, g, x)
+        self.inner += its
+        return ctx.vec_download(x), its
+
+
+def make_implicit_solver(op, dt: float, tol: float = 1e-12) -> HostImplicitSolver:
+    """timestep.py:246-247."""
+    return HostImplicitSolver(op, dt, tol=tol)

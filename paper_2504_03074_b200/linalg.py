@@ -19,7 +19,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import scipy.linalg
 
-__all__ = ["SolveReport", "device_gmres"]
+__all__ = ["SolveReport", "device_gmres", "gmres_solve"]
 
 
 @dataclass
@@ -131,3 +131,63 @@ def device_gmres(ctx, matvec, b_id: int, x_id: int, tol=1e-10, restart=30, maxit
     if not report.converged:
         report.message = f"stagnated after {total} iterations"
     return report
+
+
+def _host_operator(A):
+    if isinstance(A, np.ndarray):
+        return lambda x: A @ x
+    if hasattr(A, "matvec") and callable(A.matvec):
+        return A.matvec
+    if callable(A):
+        return A
+    raise TypeError(f"cannot interpret {type(A)} as a linear operator")
+
+
+def gmres_solve(A, b, tol=1e-10, restart=30, maxit=500, x0=None, atol=0.0, callback=None):
+    """Restarted GMRES with modified Gram-Schmidt Arnoldi and Givens rotations for HOST
+    operands (linalg.py:102-183): stops when ||b - A x||_2 <= max(tol*||b||_2, atol); the
+    residual history holds the absolute 2-norm after every inner iteration.
+
+    The Krylov basis, the MGS dot/axpy sequence and the solution update run on device vectors
+    (device_gmres; the vector is held in the interior of a 1D device field of n + 2 points,
+    whose two Dirichlet end points stay 0); ``A`` -- a matrix or a callable on arrays of b's
+    shape -- is applied on the host, its operand and result copied per mat-vec.  A nonzero x0
+    solves for the correction e = x - x0 from r0 = b - A x0: the same Krylov spaces, iterations
+    and residual history as restarting from x0."""
+    from . import _native
+
+    op = _host_operator(A)
+    b = np.asarray(b, dtype=float)
+    shape = b.shape
+    n = b.size
+    bnorm = float(np.linalg.norm(b.ravel()))
+    if bnorm == 0.0 and x0 is None:
+        return np.zeros(shape), SolveReport(0, 0.0, True, 0)
+    x0v = None if x0 is None else np.array(x0, dtype=float).reshape(shape)
+    r0 = b if x0v is None else b - np.asarray(op(x0v), dtype=float).reshape(shape)
+    target = max(tol * bnorm, atol)
+    ctx = _native.Context((n + 2,))
+    try:
+        b_id, x_id = ctx.vec_reserve(2)
+        pad = np.zeros(n + 2)
+
+        def up(vid, vec):
+            pad[1:-1] = np.asarray(vec, dtype=float).ravel()
+            ctx.vec_upload(vid, pad)
+
+        def matvec(src, dst):
+            v = ctx.vec_download(src)[1:-1].reshape(shape)
+            up(dst, np.asarray(op(v), dtype=float))
+
+        up(b_id, r0)
+        rep = device_gmres(ctx, matvec, b_id, x_id, tol=0.0, restart=restart, maxit=maxit, atol=target,
+                           callback=callback)
+        x = ctx.vec_download(x_id)[1:-1].reshape(shape)
+    finally:
+        ctx.close()
+    if x0v is not None:
+        x = x0v + x
+        r0n = float(np.linalg.norm(r0.ravel()))
+        rep.work_units += 1
+        rep.relative_residual = rep.relative_residual * r0n / bnorm if bnorm > 0 else rep.relative_residual * r0n
+    return x, rep

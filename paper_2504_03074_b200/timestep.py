@@ -134,6 +134,21 @@ def _field_type(v):
     return type(v) if hasattr(type(v), "from_values") else GridField
 
 
+def field_from_device(ftype, grid, ghost, ctx, field_id):
+    """A freshly allocated field of type ``ftype`` (ours or the reference's GridField) holding
+    device field ``field_id``: copied straight into the new field's (possibly ghost-padded)
+    buffer with one strided D2H copy, no host-side repacking.  The device field's Dirichlet
+    points are 0 by invariant, so the field is in the state set_values would leave it in."""
+    try:
+        fld = ftype(grid, ghost=ghost)
+        buf = fld._writable()
+    except (AttributeError, TypeError):
+        return ftype.from_values(grid, ctx.download(field_id), ghost=ghost)
+    ctx.download_into(field_id, buf)
+    fld._touch()
+    return fld
+
+
 def wave_solve_filtered(v, f, config, corr, op, linear_solver=None, implicit_first_step=True):
     """One application of W(v, f) on the GPU (timestep.py:250-301, explicit branch).
 
@@ -147,21 +162,20 @@ def wave_solve_filtered(v, f, config, corr, op, linear_solver=None, implicit_fir
     grid = op.grid
     dp = device_problem(grid, c=op.c, order=op.order)
     if mode_name(config.mode) == "implicit":
-        solver = implicit_solver_for(dp, grid, op.order, op.c, corr.dt)
-        dp.set_forcing(f.values)
-        dp.ctx.upload(_native.V, v.values)
+        own = getattr(linear_solver, "device_solver", None)
+        solver = own if own is not None else implicit_solver_for(dp, grid, op.order, op.c, corr.dt)
+        dp.set_forcing_field(f)
+        dp.ctx.upload_view(_native.V, v.values)
         its = implicit_wave_solve(dp, solver, corr, time_schedule(corr, config), _native.V, _native.F,
                                   _native.OUT, implicit_first_step=implicit_first_step)
         if linear_solver is not None and hasattr(linear_solver, "inner"):
             linear_solver.inner += its
-        out = dp.ctx.download(_native.OUT)
-        return _field_type(v).from_values(grid, out, ghost=max(2, op.ghost_width))
+        return field_from_device(_field_type(v), grid, max(2, op.ghost_width), dp.ctx, _native.OUT)
     dp.set_schedule(time_schedule(corr, config))
-    zero_f = dp.set_forcing(f.values)
-    dp.ctx.upload(_native.V, v.values)
+    zero_f = dp.set_forcing_field(f)
+    dp.ctx.upload_view(_native.V, v.values)
     dp.ctx.filtered_solve(_native.OUT_PLAIN, zero_forcing=zero_f)
-    out = dp.ctx.download(_native.OUT)
-    return _field_type(v).from_values(grid, out, ghost=max(2, op.ghost_width))
+    return field_from_device(_field_type(v), grid, max(2, op.ghost_width), dp.ctx, _native.OUT)
 
 
 @dataclass
@@ -218,3 +232,27 @@ def explicit_stability_check(lam_max: float, dt: float):
     """lambda*dt <= 2 (filters.py:205-215)."""
     if lam_max * dt / 2.0 > 1.0:
         raise ExplicitStabilityError(f"lambda*dt = {lam_max * dt:.6g} > 2")
+
+
+def step_implicit(state: WaveState, op, f: np.ndarray, corr, linear_solver) -> WaveState:
+    """One trapezoidal step (timestep.py:148-170): (I - (dt^2/2) L) W^{n+1} = rhs, the first
+    step included (W^{-1} eliminated).  The reference's host expressions for rhs / guess, the
+    Laplacian of W^{n-1} on the device (DiscreteOperator.apply_values), and the solve by
+    ``linear_solver`` (make_implicit_solver: on the device)."""
+    dt = corr.dt
+    cos_fac = math.cos(corr.omega_tilde * dt)
+    if state.n == 0:
+        rhs = state.w - 0.5 * dt**2 * cos_fac * f
+        guess = state.w
+    else:
+        lap_prev = op.apply_values(state.w_prev)
+        force = f * (math.cos(corr.omega_tilde * state.t) * cos_fac)
+        rhs = 2.0 * state.w - state.w_prev + 0.5 * dt**2 * lap_prev - dt**2 * force
+        guess = 2.0 * state.w - state.w_prev
+    w_next, iters = linear_solver(rhs, guess)
+    state.inner_iterations = getattr(state, "inner_iterations", 0) + iters
+    state.w_prev = state.w
+    state.w = w_next
+    state.n += 1
+    state.t = state.n * dt
+    return state

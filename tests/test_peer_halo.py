@@ -56,6 +56,21 @@ class PeerCtx:
         a, o = self.space.resolve(ptr)
         a[o // 4] = value
 
+    # the exchange stream protocol: copies and flag writes of an exchange between begin and end,
+    # the join before the next exchange begins (synchronous here, so only the order is checked)
+    def comm_begin(self):
+        assert not getattr(self, "open", False), "whb_comm_begin while an exchange is open"
+        assert getattr(self, "joined", True), "exchange started before the previous one was joined"
+        self.open, self.joined = True, False
+
+    def comm_end(self):
+        assert getattr(self, "open", False), "whb_comm_end without whb_comm_begin"
+        self.open = False
+
+    def comm_join(self):
+        assert not getattr(self, "open", False), "whb_comm_join inside an open exchange"
+        self.joined = True
+
     def stream_wait_u32(self, ptr, value):
         a, o = self.space.resolve(ptr)
         assert np.int32(np.uint32(a[o // 4]) - np.uint32(value)) >= 0, "wait on a flag no neighbour has written"

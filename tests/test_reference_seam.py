@@ -39,6 +39,13 @@ class FakeCtx:
     def download(self, field, member=0, out=None):
         return np.array(self.fields[field])
 
+    def upload_view(self, field, values, member=0):
+        self.upload(field, values, member)
+
+    def download_into(self, field, out, member=0):
+        out[...] = self.fields[field]
+        return out
+
     def filtered_solve(self, out_mode=_native.OUT_PLAIN, zero_forcing=False):
         f = np.zeros_like(self.fields[_native.V]) if zero_forcing else self.fields[_native.F]
         bcs = [getattr(b, "value", b) for b in self.grid.bcs]
@@ -58,6 +65,9 @@ class FakeProblem:
     def set_forcing(self, values, member=0):
         self.ctx.upload(_native.F, values)
         return not np.any(values)
+
+    def set_forcing_field(self, field, member=0):
+        return self.set_forcing(field.values, member)
 
 
 def test_rebinding_reroutes_the_reference_drivers(monkeypatch):
