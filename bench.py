@@ -346,6 +346,28 @@ class SingleRun:
         return te, {"h2d_bytes_per_step": self.npts * 8, "d2h_bytes_per_step": self.npts * 8 + 8,
                     "api": "paper_2504_03074_b200.HostFPIStep (C ABI whb_iterate_host), pinned host buffers"}
 
+    def e2e_seam(self, K, dist):
+        """The reference-facing Python seam: v = wave_solve_filtered(v, f, cfg, corr, op) with host
+        GridFields, the call the reference's _iterate makes (driver.py:222) once the seam is rebound
+        (INTEGRATION.md section 1): v in and W(v, f) out through host memory every call."""
+        import torch
+
+        import paper_2504_03074_b200 as wh
+        from paper_2504_03074_b200 import timestep as ts
+
+        op = wh.DiscreteOperator(self.g, 2, 1.0)
+        v = wh.GridField.zeros(self.g)
+        wh.wave_solve_filtered(v, self.f, self.cfg, self.corr, op)  # warm (forcing cached by generation)
+        barrier(dist)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(K):
+            v = ts.wave_solve_filtered(v, self.f, self.cfg, self.corr, op)
+        te = time.perf_counter() - t0
+        return te, {"h2d_bytes_per_step": self.npts * 8, "d2h_bytes_per_step": self.npts * 8,
+                    "api": "paper_2504_03074_b200.wave_solve_filtered(GridField v, GridField f, ...) -> new "
+                           "GridField (pageable host fields, strided copies straight into the new field)"}
+
     def e2e_solve(self, K, dist):
         """The fpi_solve call through the C ABI with host buffers: f copied in from pinned memory,
         K device-resident iterations, the residual history and v copied out."""
@@ -773,7 +795,7 @@ def run_ours(args, dist, ws, rank, local):
                     "frac_48B uses SURVEY 8(d)'s 48 B per update and exceeds 1 for multi-step kernels by "
                     "construction (they move 56/T B per update)."}
 
-    e2e = e2e_solve = None
+    e2e = e2e_solve = e2e_seam = None
     if not args.no_e2e:
         te, info = wl.e2e(K, W, dist)
         te = max_over_ranks(dist, te)
@@ -782,6 +804,12 @@ def run_ours(args, dist, ws, rank, local):
             ts_, info_s = wl.e2e_solve(K, dist)
             ts_ = max_over_ranks(dist, ts_)
             e2e_solve = {"value": units / ts_ / 1e9, "unit": "Gpts/s", **info_s, "iters_per_s": K / ts_}
+        if hasattr(wl, "e2e_seam"):
+            ks = K if wl.npts < (1 << 28) else min(K, 3)  # 1025^3: 17 GB of pageable copies per call
+            tss, info_m = wl.e2e_seam(ks, dist)
+            tss = max_over_ranks(dist, tss)
+            e2e_seam = {"value": wl.units_per_step * ks / tss / 1e9, "unit": "Gpts/s", "calls": ks, **info_m,
+                        "iters_per_s": ks / tss}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -802,7 +830,8 @@ def run_ours(args, dist, ws, rank, local):
             "dtype": "f64", "data": "synthetic (BASELINE forcing recipe, SURVEY 8(d)); f sha256 " + wl.f_sha[:16],
             "config": config_for(args.workload, K, ws, args.decomp, args.halo, n_t=getattr(wl, "n_t_config", None)),
             "iters_per_s": K / dev_s,
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_solve": e2e_solve, "clocks": clocks,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_solve": e2e_solve, "e2e_seam": e2e_seam,
+            "clocks": clocks,
             "gpu_launches": launches,
             "residuals": {"first": float(residuals[0]), "last": float(residuals[-1])},
             "wall_s_timed_region": t_wall, "impl": "ours",

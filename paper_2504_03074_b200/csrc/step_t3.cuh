@@ -38,16 +38,15 @@ using bulk::update_point;
 
 constexpr int TX = 60;                 // output columns per tile
 constexpr int BY = 12;                 // output rows per tile
-constexpr int NW = BY + 4;             // warps = level-1 rows
-constexpr int THREADS = 32 * NW;       // 512
+constexpr int NR = BY + 4;             // level-1 rows (16): NR / R warps of R rows each
 constexpr int LW = 64;                 // level-1 row width (columns k0-2 .. k0+61)
 constexpr int RW = 68;                 // staged W^s row: columns k0-4 .. k0+63
 constexpr int WR = BY + 6;             // staged W^s rows: j0-3 .. j0+BY+2
 constexpr int W_EL = (WR * RW + 15) / 16 * 16;   // 1232 (128-B aligned sub-buffers for TMA)
-constexpr int P_EL = NW * LW;                    // 1024: W^{s-1} / f box (the level-1 region)
+constexpr int P_EL = NR * LW;                    // 1024: W^{s-1} / f box (the level-1 region)
 constexpr int STAGE = W_EL + 2 * P_EL;           // 3280 doubles = 26.2 KB
-constexpr int L1_EL = NW * LW;                   // level-1 plane
-constexpr int L2_EL = (NW - 2) * LW;             // level-2 plane (rows j0-1 .. j0+BY)
+constexpr int L1_EL = NR * LW;                   // level-1 plane
+constexpr int L2_EL = (NR - 2) * LW;             // level-2 plane (rows j0-1 .. j0+BY)
 
 template <int ST>
 constexpr size_t smem_bytes() {
@@ -64,15 +63,24 @@ struct Scal {
 
 // K1: kind of step s (FIRST when s == 0); K2: MID, or LAST when step s+2 ends the solve.
 // GM: geometry mode as in tb2 / wf2d (0 generic, 1 equal taps, 2 equal taps and c^2 == 1).
-template <int ST, int K1, int K2, bool ZF, int GM>
-__global__ void __launch_bounds__(THREADS, 1)
+template <int R>
+constexpr int threads() {
+    return 32 * NR / R;
+}
+
+// K1: kind of step s (FIRST when s == 0); K2: MID, or LAST when step s+2 ends the solve.
+// GM: geometry mode as in tb2 / wf2d (0 generic, 1 equal taps, 2 equal taps and c^2 == 1).
+// R: level-1 rows per warp (each lane: R rows x 2 columns); the axis-1 neighbours between a
+// thread's own rows come from its registers, only the outer two from shared memory.
+template <int ST, int K1, int K2, bool ZF, int GM, int R>
+__global__ void __launch_bounds__(threads<R>(), 1)
     t3_kernel(Geom g, const Member *__restrict__ members, int s, int i_begin, int i_end, int chunk_len, int JT,
               const Scal sc, const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_p,
               const __grid_constant__ CUtensorMap tm_f) {
     constexpr bool SQ = GM >= 1;
     constexpr int C2M = GM == 2 ? 0 : -1;
     constexpr bool LOAD_P = (K1 != K_FIRST);
-    static_assert(ST >= 3, "planes i and i+1 resident plus one in flight");
+    static_assert(NR % R == 0, "rows per warp must divide the level-1 rows");
     extern __shared__ __align__(128) double smem[];
     double *l1buf = smem + (size_t)ST * STAGE;
     double *l2buf = l1buf + 3 * L1_EL;
@@ -110,10 +118,6 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (LOAD_P) tma_load_3d(st + W_EL, &tm_p, k0 - 2, j0 - 2, plane, bar);
         if (!ZF) tma_load_3d(st + W_EL + P_EL, &tm_f, k0 - 2, j0 - 2, plane, bar);
     };
-    auto wait_plane = [&](int plane) {
-        const int t = plane - pfirst;
-        mbar_wait(bars + (t % ST), (t / ST) & 1);
-    };
 
     if (threadIdx.x == 0) {
         for (int t = 0; t < ST; ++t) mbar_init(bars + t, 1);
@@ -122,22 +126,37 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     __syncthreads();
 
-    // this thread's rows / columns
-    const int y = j0 - 2 + w;                  // level-1 row
-    const int x = k0 - 2 + 2 * lane;           // first column of the pair
-    const bool yin = (y >= g.j_lo) && (y < g.j_hi);
+    // this thread's rows rho = w*R + r (level-1 region rows; y = j0 - 2 + rho) and column pair
+    const int x = k0 - 2 + 2 * lane;
     const bool xin0 = (x >= 1) && (x < g.n2 - 1);
     const bool xin1 = (x + 1 >= 1) && (x + 1 < g.n2 - 1);
     const bool xall = __all_sync(0xffffffffu, xin0 && xin1);  // every column of the warp interior
-    const bool do2 = (w >= 1) && (w <= NW - 2);        // warp-uniform: rows of level 2
-    const bool do3 = (w >= 2) && (w <= NW - 3);        // rows of level 3 (the output tile)
-    // output points: the tile's rows / columns, interior only
-    const bool own = do3 && lane >= 1 && lane <= 30;
-    const bool ok0 = own && yin && xin0;
-    const bool ok1 = own && yin && xin1;
-    const int wrow = (w + 1) * RW + 2 + 2 * lane;      // this pair in a W^s stage (row y)
-    const int prow = w * LW + 2 * lane;                // this pair in a W^{s-1} / f box, level-1 plane
-    const long long pbase = (long long)y * P + x;
+    const int rho0 = w * R;
+    bool yin[R], ok0[R], ok1[R];
+    long long pbase[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int y = j0 - 2 + rho0 + r;
+        yin[r] = (y >= g.j_lo) && (y < g.j_hi);
+        const bool own = (rho0 + r >= 2) && (rho0 + r <= NR - 3) && lane >= 1 && lane <= 30;
+        ok0[r] = own && yin[r] && xin0;
+        ok1[r] = own && yin[r] && xin1;
+        pbase[r] = (long long)y * P + x;
+    }
+    bool any_ok = false;
+#pragma unroll
+    for (int r = 0; r < R; ++r) any_ok = any_ok || ok0[r] || ok1[r];
+    // warp-uniform row ranges: level 2 on rows 1 .. NR-2, level 3 on rows 2 .. NR-3
+    auto row2 = [&](int r) { return rho0 + r >= 1 && rho0 + r <= NR - 2; };
+    auto row3 = [&](int r) { return rho0 + r >= 2 && rho0 + r <= NR - 3; };
+    bool any2 = false, any3 = false;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        any2 = any2 || row2(r);
+        any3 = any3 || row3(r);
+    }
+    const int wrow0 = (rho0 + 1) * RW + 2 + 2 * lane;  // first own row in a W^s stage
+    const int prow0 = rho0 * LW + 2 * lane;            // first own row in a W^{s-1} / f box, level-1 plane
 
     auto plane_in = [&](int p) { return p >= g.i_lo && p < g.i_hi; };
     auto shl = [&](double v) { return __shfl_up_sync(0xffffffffu, v, 1); };
@@ -147,30 +166,39 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (pin && xall) return make_double2(a, b);
         return make_double2((pin && xin0) ? a : 0.0, (pin && xin1) ? b : 0.0);
     };
+    auto lds2 = [&](const double *p) { return *reinterpret_cast<const double2 *>(p); };
 
-    // register queues (own column pair): W^s at planes i+1 .. i-4, level 1 at i .. i-4,
+    // register queues per own row (column pair): W^s at planes i+1 .. i-4, level 1 at i .. i-4,
     // level 2 at i-2 .. i-5, f at i .. i-4.  The plane loop is unrolled by ST = 6 (a multiple of
     // the level-ring period 3), so the queue shifts are register renames and every stage / ring
     // slot below is a compile-time constant.
     const double2 z2 = make_double2(0.0, 0.0);
-    double2 ws0 = z2, ws1 = z2, ws2 = z2, ws3 = z2, ws4 = z2, ws5 = z2;  // ws0 = W^s(i+1), ws1 = W^s(i), ...
-    double2 q10 = z2, q11 = z2, q12 = z2, q13 = z2, q14 = z2;           // q1k = level 1 at plane i-k
-    double2 q20 = z2, q21 = z2, q22 = z2, q23 = z2;                     // q2k = level 2 at plane i-2-k
-    double2 fq0 = z2, fq1 = z2, fq2 = z2, fq3 = z2, fq4 = z2;           // fqk = f at plane i-k
+    double2 ws0[R], ws1[R], ws2[R], ws3[R], ws4[R], ws5[R];  // ws0 = W^s(i+1), ws1 = W^s(i), ...
+    double2 q10[R], q11[R], q12[R], q13[R], q14[R];          // q1k = level 1 at plane i-k
+    double2 q20[R], q21[R], q22[R], q23[R];                  // q2k = level 2 at plane i-2-k
+    double2 fq0[R], fq1[R], fq2[R], fq3[R], fq4[R];          // fqk = f at plane i-k
+    double2 acc_n[R], v_n[R];
     double rsum = 0.0;
 
-    // W^s centres of planes i0-3 and i0-2 (the first iteration, i = i0-2, adds plane i0-1)
-    wait_plane(pfirst);
-    wait_plane(pfirst + 1);
-    ws1 = *reinterpret_cast<const double2 *>(smem + 0 * STAGE + wrow);    // becomes W^s(i-1) below
-    ws0 = *reinterpret_cast<const double2 *>(smem + 1 * STAGE + wrow);
-    // the filter-sum input and v of the first output plane
+    // W^s centres of planes i0-3 and i0-2 (the first iteration, i = i0-2, adds plane i0-1); the
+    // filter-sum input and v of the first output plane
+    mbar_wait(bars + 0, 0);
+    mbar_wait(bars + 1, 0);
     const bool want_v = (K2 == K_LAST) && m.out_mode != WHB_OUT_PLAIN;
-    auto ld2 = [&](const double *base, int p) -> double2 {
-        return *reinterpret_cast<const double2 *>(base + (long long)p * S0 + pbase);
+    auto ld2 = [&](const double *base, int p, int r) -> double2 {
+        return *reinterpret_cast<const double2 *>(base + (long long)p * S0 + pbase[r]);
     };
-    double2 acc_n = (K1 != K_FIRST && (ok0 || ok1)) ? ld2(m.acc, i0) : z2;
-    double2 v_n = (want_v && (ok0 || ok1)) ? ld2(m.v, i0) : z2;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        ws1[r] = lds2(smem + 0 * STAGE + wrow0 + r * RW);  // becomes W^s(i-1) below
+        ws0[r] = lds2(smem + 1 * STAGE + wrow0 + r * RW);
+        ws2[r] = ws3[r] = ws4[r] = ws5[r] = z2;
+        q10[r] = q11[r] = q12[r] = q13[r] = q14[r] = z2;
+        q20[r] = q21[r] = q22[r] = q23[r] = z2;
+        fq0[r] = fq1[r] = fq2[r] = fq3[r] = fq4[r] = z2;
+        acc_n[r] = (K1 != K_FIRST && (ok0[r] || ok1[r])) ? ld2(m.acc, i0, r) : z2;
+        v_n[r] = (want_v && (ok0[r] || ok1[r])) ? ld2(m.v, i0, r) : z2;
+    }
     __syncthreads();  // every thread has read plane pfirst: its slot takes plane pfirst + ST
     if (threadIdx.x == 0 && pfirst + ST <= plast) {
         fence_proxy_async();
@@ -188,101 +216,133 @@ __global__ void __launch_bounds__(THREADS, 1)
         constexpr int R12 = (K + 1) % 3;        // level-1 slot of plane i-2 / level-2 slot written (i-2)
         constexpr int R24 = (K + 2) % 3;        // level-2 slot of plane i-4
         // shift the queues: plane i+1 of W^s enters
-        ws5 = ws4; ws4 = ws3; ws3 = ws2; ws2 = ws1; ws1 = ws0;
-        if (i + 1 <= plast) {
-            mbar_wait(bars + SL_N, (round + (K + 2) / ST) & 1);
-            ws0 = *reinterpret_cast<const double2 *>(smem + SL_N * STAGE + wrow);
+        // Every queue entry is assigned unconditionally in every copy (values outside a level's
+        // plane range are computed from stale data and never stored or consumed), so the
+        // compiler can rename the shifts instead of moving registers.
+        if (i + 1 <= plast) mbar_wait(bars + SL_N, (round + (K + 2) / ST) & 1);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            ws5[r] = ws4[r]; ws4[r] = ws3[r]; ws3[r] = ws2[r]; ws2[r] = ws1[r]; ws1[r] = ws0[r];
+            ws0[r] = lds2(smem + SL_N * STAGE + wrow0 + r * RW);
+            q14[r] = q13[r]; q13[r] = q12[r]; q12[r] = q11[r]; q11[r] = q10[r];
+            q23[r] = q22[r]; q22[r] = q21[r]; q21[r] = q20[r];
+            fq4[r] = fq3[r]; fq3[r] = fq2[r]; fq2[r] = fq1[r]; fq1[r] = fq0[r];
         }
-        q14 = q13; q13 = q12; q12 = q11; q11 = q10;
-        q23 = q22; q22 = q21; q21 = q20;
-        fq4 = fq3; fq3 = fq2; fq2 = fq1; fq1 = fq0;
 
-        // ---- level 1 at plane i (step s)
-        if (i <= i1 + 1) {
+        // ---- level 1 at plane i (step s) on every row (needed for i <= i1 + 1)
+        {
             const double *st = smem + SL_I * STAGE;
-            const double2 yl = *reinterpret_cast<const double2 *>(st + wrow - RW);
-            const double2 yh = *reinterpret_cast<const double2 *>(st + wrow + RW);
-            double xl = shl(ws1.y), xh = shr(ws1.x);
-            if (lane == 0) xl = st[wrow - 1];
-            if (lane == 31) xh = st[wrow + 2];
-            const double2 pv = LOAD_P ? *reinterpret_cast<const double2 *>(st + W_EL + prow) : z2;
-            if (!ZF) fq0 = *reinterpret_cast<const double2 *>(st + W_EL + P_EL + prow);
-            const double a = update_point<K1, ZF, true, SQ, C2M>(g, ws2.x, ws1.x, ws0.x, yl.x, yh.x, xl, ws1.y, fq0.x,
-                                                               pv.x, sc.h1, sc.cos1);
-            const double b = update_point<K1, ZF, true, SQ, C2M>(g, ws2.y, ws1.y, ws0.y, yl.y, yh.y, ws1.x, xh, fq0.y,
-                                                               pv.y, sc.h1, sc.cos1);
-            q10 = mask(plane_in(i) && yin, a, b);
-            *reinterpret_cast<double2 *>(l1buf + R1W * L1_EL + prow) = q10;
+            const double2 ylo = lds2(st + wrow0 - RW);             // row rho0 - 1
+            const double2 yhi = lds2(st + wrow0 + R * RW);         // row rho0 + R
+            const bool pin = plane_in(i);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const double2 yl = r == 0 ? ylo : ws1[r - 1];
+                const double2 yh = r == R - 1 ? yhi : ws1[r + 1];
+                const int wrow = wrow0 + r * RW;
+                double xl = shl(ws1[r].y), xh = shr(ws1[r].x);
+                if (lane == 0) xl = st[wrow - 1];
+                if (lane == 31) xh = st[wrow + 2];
+                const int prow = prow0 + r * LW;
+                const double2 pv = LOAD_P ? lds2(st + W_EL + prow) : z2;
+                if (!ZF) fq0[r] = lds2(st + W_EL + P_EL + prow);
+                const double a = update_point<K1, ZF, true, SQ, C2M>(g, ws2[r].x, ws1[r].x, ws0[r].x, yl.x, yh.x, xl,
+                                                                   ws1[r].y, fq0[r].x, pv.x, sc.h1, sc.cos1);
+                const double b = update_point<K1, ZF, true, SQ, C2M>(g, ws2[r].y, ws1[r].y, ws0[r].y, yl.y, yh.y,
+                                                                   ws1[r].x, xh, fq0[r].y, pv.y, sc.h1, sc.cos1);
+                q10[r] = mask(pin && yin[r], a, b);
+                *reinterpret_cast<double2 *>(l1buf + R1W * L1_EL + prow) = q10[r];
+            }
         }
 
-        // ---- level 2 at plane i-2 (step s+1): level 1 at i-3, i-2, i-1 (queue), rows y-1, y+1 (ring)
-        const int p2 = i - 2;
-        if (do2 && p2 >= i0 - 1 && p2 <= i1) {
+        // ---- level 2 at plane i-2 (step s+1): level 1 at i-3, i-2, i-1 (queues), rows rho-1, rho+1
+        const int p2 = i - 2;  // needed for i0 - 1 <= p2 <= i1
+        if (any2) {
             const double *l1 = l1buf + R12 * L1_EL;
-            const double2 yl = *reinterpret_cast<const double2 *>(l1 + prow - LW);
-            const double2 yh = *reinterpret_cast<const double2 *>(l1 + prow + LW);
-            const double xl = shl(q12.y), xh = shr(q12.x);
-            // prev of step s+1 = W^s at plane i-2 (ws3), f at plane i-2 (fq2)
-            const double a = update_point<K_MID, ZF, true, SQ, C2M>(g, q13.x, q12.x, q11.x, yl.x, yh.x, xl, q12.y,
-                                                                  fq2.x, ws3.x, sc.dt2, sc.cos2);
-            const double b = update_point<K_MID, ZF, true, SQ, C2M>(g, q13.y, q12.y, q11.y, yl.y, yh.y, q12.x, xh,
-                                                                  fq2.y, ws3.y, sc.dt2, sc.cos2);
-            q20 = mask(plane_in(p2) && yin, a, b);
-            *reinterpret_cast<double2 *>(l2buf + R12 * L2_EL + prow - LW) = q20;
+            const double2 ylo = row2(0) ? lds2(l1 + prow0 - LW) : z2;
+            const double2 yhi = row2(R - 1) ? lds2(l1 + prow0 + R * LW) : z2;
+            const bool pin = plane_in(p2);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                if (!row2(r)) {
+                    q20[r] = z2;
+                    continue;
+                }
+                const double2 yl = r == 0 ? ylo : q12[r - 1];
+                const double2 yh = r == R - 1 ? yhi : q12[r + 1];
+                const double xl = shl(q12[r].y), xh = shr(q12[r].x);
+                // prev of step s+1 = W^s at plane i-2 (ws3), f at plane i-2 (fq2)
+                const double a = update_point<K_MID, ZF, true, SQ, C2M>(g, q13[r].x, q12[r].x, q11[r].x, yl.x, yh.x,
+                                                                      xl, q12[r].y, fq2[r].x, ws3[r].x, sc.dt2,
+                                                                      sc.cos2);
+                const double b = update_point<K_MID, ZF, true, SQ, C2M>(g, q13[r].y, q12[r].y, q11[r].y, yl.y, yh.y,
+                                                                      q12[r].x, xh, fq2[r].y, ws3[r].y, sc.dt2,
+                                                                      sc.cos2);
+                q20[r] = mask(pin && yin[r], a, b);
+                *reinterpret_cast<double2 *>(l2buf + R12 * L2_EL + prow0 + r * LW - LW) = q20[r];
+            }
         }
 
         // ---- level 3 at plane i-4 (step s+2) on the tile, then the filter sum and the outputs
         const int p3 = i - 4;
-        if (do3 && p3 >= i0 && p3 < i1) {
+        const bool out3 = p3 >= i0 && p3 < i1;  // outputs (stores, residual, prefetch) only then
+        if (any3) {
             const double *l2 = l2buf + R24 * L2_EL;
-            const double2 yl = *reinterpret_cast<const double2 *>(l2 + prow - 2 * LW);
-            const double2 yh = *reinterpret_cast<const double2 *>(l2 + prow);
-            const double xl = shl(q22.y), xh = shr(q22.x);
-            // level 2 at i-5, i-4, i-3 = q23, q22, q21; prev = level 1 at i-4 (q14); f at i-4 (fq4)
-            const double a3 = update_point<K_MID, ZF, true, SQ, C2M>(g, q23.x, q22.x, q21.x, yl.x, yh.x, xl, q22.y,
-                                                                   fq4.x, q14.x, sc.dt2, sc.cos3);
-            const double b3 = update_point<K_MID, ZF, true, SQ, C2M>(g, q23.y, q22.y, q21.y, yl.y, yh.y, q22.x, xh,
-                                                                   fq4.y, q14.y, sc.dt2, sc.cos3);
-            // next output plane's acc / v (one iteration ahead: hides the HBM latency)
-            const double2 acc_c = acc_n, v_c = v_n;
-            if (ok0 || ok1) {
+            const double2 ylo = row3(0) ? lds2(l2 + prow0 - 2 * LW) : z2;        // level-2 row rho0 - 1
+            const double2 yhi = row3(R - 1) ? lds2(l2 + prow0 + (R - 1) * LW) : z2;  // row rho0 + R
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                if (!row3(r)) continue;
+                const double2 yl = r == 0 ? ylo : q22[r - 1];
+                const double2 yh = r == R - 1 ? yhi : q22[r + 1];
+                const double xl = shl(q22[r].y), xh = shr(q22[r].x);
+                // level 2 at i-5, i-4, i-3 = q23, q22, q21; prev = level 1 at i-4 (q14); f at i-4 (fq4)
+                const double a3 = update_point<K_MID, ZF, true, SQ, C2M>(g, q23[r].x, q22[r].x, q21[r].x, yl.x, yh.x,
+                                                                       xl, q22[r].y, fq4[r].x, q14[r].x, sc.dt2,
+                                                                       sc.cos3);
+                const double b3 = update_point<K_MID, ZF, true, SQ, C2M>(g, q23[r].y, q22[r].y, q21[r].y, yl.y, yh.y,
+                                                                       q22[r].x, xh, fq4[r].y, q14[r].y, sc.dt2,
+                                                                       sc.cos3);
+                // next output plane's acc / v (one iteration ahead: hides the HBM latency)
+                const double2 acc_c = acc_n[r], v_c = v_n[r];
+                if (!out3 || !(ok0[r] || ok1[r])) continue;
                 if (p3 + 1 < i1) {
-                    if (K1 != K_FIRST) acc_n = ld2(m.acc, p3 + 1);
-                    if (want_v) v_n = ld2(m.v, p3 + 1);
+                    if (K1 != K_FIRST) acc_n[r] = ld2(m.acc, p3 + 1, r);
+                    if (want_v) v_n[r] = ld2(m.v, p3 + 1, r);
                 }
                 // acc (+ c0 W^0 on the first pass) + c1 W^{s+1} + c2 W^{s+2} + c3 W^{s+3}, in step order
                 double s0, s1;
                 if (K1 == K_FIRST) {  // timestep.py:284 then :298 per step
-                    s0 = whb_add(whb_mul(sc.c0, ws5.x), whb_mul(sc.c1, q14.x));
-                    s1 = whb_add(whb_mul(sc.c0, ws5.y), whb_mul(sc.c1, q14.y));
+                    s0 = whb_add(whb_mul(sc.c0, ws5[r].x), whb_mul(sc.c1, q14[r].x));
+                    s1 = whb_add(whb_mul(sc.c0, ws5[r].y), whb_mul(sc.c1, q14[r].y));
                 } else {
-                    s0 = whb_add(acc_c.x, whb_mul(sc.c1, q14.x));
-                    s1 = whb_add(acc_c.y, whb_mul(sc.c1, q14.y));
+                    s0 = whb_add(acc_c.x, whb_mul(sc.c1, q14[r].x));
+                    s1 = whb_add(acc_c.y, whb_mul(sc.c1, q14[r].y));
                 }
-                s0 = whb_add(whb_add(s0, whb_mul(sc.c2, q22.x)), whb_mul(sc.c3, a3));
-                s1 = whb_add(whb_add(s1, whb_mul(sc.c2, q22.y)), whb_mul(sc.c3, b3));
-                const long long p = (long long)p3 * S0 + pbase;
+                s0 = whb_add(whb_add(s0, whb_mul(sc.c2, q22[r].x)), whb_mul(sc.c3, a3));
+                s1 = whb_add(whb_add(s1, whb_mul(sc.c2, q22[r].y)), whb_mul(sc.c3, b3));
+                const long long p = (long long)p3 * S0 + pbase[r];
                 if (K2 == K_MID) {
-                    if (ok0 && ok1) {
-                        *reinterpret_cast<double2 *>(w2g + p) = q22;
+                    if (ok0[r] && ok1[r]) {
+                        *reinterpret_cast<double2 *>(w2g + p) = q22[r];
                         *reinterpret_cast<double2 *>(w3g + p) = make_double2(a3, b3);
                         *reinterpret_cast<double2 *>(m.acc + p) = make_double2(s0, s1);
                     } else {
-                        if (ok0) { w2g[p] = q22.x; w3g[p] = a3; m.acc[p] = s0; }
-                        if (ok1) { w2g[p + 1] = q22.y; w3g[p + 1] = b3; m.acc[p + 1] = s1; }
+                        if (ok0[r]) { w2g[p] = q22[r].x; w3g[p] = a3; m.acc[p] = s0; }
+                        if (ok1[r]) { w2g[p + 1] = q22[r].y; w3g[p + 1] = b3; m.acc[p + 1] = s1; }
                     }
                 } else {
                     const double o0 = whb_mul(sc.osc, s0);
                     const double o1 = whb_mul(sc.osc, s1);
                     if (m.out_mode == WHB_OUT_FPI) {
-                        if (ok0) { const double d = o0 - v_c.x; rsum += d * d; m.v[p] = o0; }
-                        if (ok1) { const double d = o1 - v_c.y; rsum += d * d; m.v[p + 1] = o1; }
+                        if (ok0[r]) { const double d = o0 - v_c.x; rsum += d * d; m.v[p] = o0; }
+                        if (ok1[r]) { const double d = o1 - v_c.y; rsum += d * d; m.v[p + 1] = o1; }
                     } else if (m.out_mode == WHB_OUT_AV) {
-                        if (ok0) m.dst[p] = whb_sub(v_c.x, o0);
-                        if (ok1) m.dst[p + 1] = whb_sub(v_c.y, o1);
+                        if (ok0[r]) m.dst[p] = whb_sub(v_c.x, o0);
+                        if (ok1[r]) m.dst[p + 1] = whb_sub(v_c.y, o1);
                     } else {
-                        if (ok0) m.dst[p] = o0;
-                        if (ok1) m.dst[p + 1] = o1;
+                        if (ok0[r]) m.dst[p] = o0;
+                        if (ok1[r]) m.dst[p + 1] = o1;
                     }
                 }
             }
@@ -314,6 +374,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (ib + 5 > iend) break;
         iter(I5{}, ib + 5, round);
     }
+    (void)any_ok;
     if (K2 == K_LAST && m.out_mode == WHB_OUT_FPI) {
         const double t = block_sum(rsum);
         if (threadIdx.x == 0) m.partials[blockIdx.y * gridDim.x + blockIdx.x] = t;
