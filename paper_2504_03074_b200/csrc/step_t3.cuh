@@ -130,7 +130,6 @@ __global__ void __launch_bounds__(threads<R>(), 1)
     const int x = k0 - 2 + 2 * lane;
     const bool xin0 = (x >= 1) && (x < g.n2 - 1);
     const bool xin1 = (x + 1 >= 1) && (x + 1 < g.n2 - 1);
-    const bool xall = __all_sync(0xffffffffu, xin0 && xin1);  // every column of the warp interior
     const int rho0 = w * R;
     bool yin[R], ok0[R], ok1[R];
     long long pbase[R];
@@ -161,9 +160,8 @@ __global__ void __launch_bounds__(threads<R>(), 1)
     auto plane_in = [&](int p) { return p >= g.i_lo && p < g.i_hi; };
     auto shl = [&](double v) { return __shfl_up_sync(0xffffffffu, v, 1); };
     auto shr = [&](double v) { return __shfl_down_sync(0xffffffffu, v, 1); };
-    // Dirichlet / out-of-domain points of a level are 0; warp-uniform fast path when all are inside
+    // Dirichlet / out-of-domain points of a level are 0 (one select per value)
     auto mask = [&](bool pin, double a, double b) -> double2 {
-        if (pin && xall) return make_double2(a, b);
         return make_double2((pin && xin0) ? a : 0.0, (pin && xin1) ? b : 0.0);
     };
     auto lds2 = [&](const double *p) { return *reinterpret_cast<const double2 *>(p); };
@@ -207,19 +205,18 @@ __global__ void __launch_bounds__(threads<R>(), 1)
 
     const int ibeg = i0 - 2;  // iteration i: level 1 at i, level 2 at i-2, level 3 at i-4
     const int iend = i1 + 3;
-    // copy K of a round: i = ibeg + ST*round + K; plane p <-> stage slot (p - pfirst) % ST
-    auto iter = [&](auto kc, const int i, const int round) {
-        constexpr int K = decltype(kc)::value;
-        constexpr int SL_I = (K + 1) % ST;      // stage of plane i
-        constexpr int SL_N = (K + 2) % ST;      // stage of plane i+1
-        constexpr int R1W = K % 3;              // level-1 ring slot written (plane i)
-        constexpr int R12 = (K + 1) % 3;        // level-1 slot of plane i-2 / level-2 slot written (i-2)
-        constexpr int R24 = (K + 2) % 3;        // level-2 slot of plane i-4
+    // Plane loop, one copy of the body (a 6-way unrolled version with compile-time slots was
+    // measured slower: 4-7K instructions of loop body thrash the instruction cache).  Stage and
+    // ring slots advance incrementally: plane p <-> stage slot (p - pfirst) % ST.
+    int sl_i = 1 % ST, sl_n = 2 % ST, ph_n = 0;  // stages of planes i and i+1, phase of the latter
+    int r1w = 0, r12 = 1, r24 = 2;                // level-1 slot of plane i, level-1/-2 slot of i-2, level-2 of i-4
+    for (int i = ibeg; i <= iend; ++i) {
+        const int SL_I = sl_i, SL_N = sl_n, R1W = r1w, R12 = r12, R24 = r24;
         // shift the queues: plane i+1 of W^s enters
         // Every queue entry is assigned unconditionally in every copy (values outside a level's
         // plane range are computed from stale data and never stored or consumed), so the
         // compiler can rename the shifts instead of moving registers.
-        if (i + 1 <= plast) mbar_wait(bars + SL_N, (round + (K + 2) / ST) & 1);
+        if (i + 1 <= plast) mbar_wait(bars + SL_N, ph_n);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             ws5[r] = ws4[r]; ws4[r] = ws3[r]; ws3[r] = ws2[r]; ws2[r] = ws1[r]; ws1[r] = ws0[r];
@@ -240,9 +237,7 @@ __global__ void __launch_bounds__(threads<R>(), 1)
                 const double2 yl = r == 0 ? ylo : ws1[r - 1];
                 const double2 yh = r == R - 1 ? yhi : ws1[r + 1];
                 const int wrow = wrow0 + r * RW;
-                double xl = shl(ws1[r].y), xh = shr(ws1[r].x);
-                if (lane == 0) xl = st[wrow - 1];
-                if (lane == 31) xh = st[wrow + 2];
+                const double xl = st[wrow - 1], xh = st[wrow + 2];  // the stage has the halo columns
                 const int prow = prow0 + r * LW;
                 const double2 pv = LOAD_P ? lds2(st + W_EL + prow) : z2;
                 if (!ZF) fq0[r] = lds2(st + W_EL + P_EL + prow);
@@ -259,8 +254,9 @@ __global__ void __launch_bounds__(threads<R>(), 1)
         const int p2 = i - 2;  // needed for i0 - 1 <= p2 <= i1
         if (any2) {
             const double *l1 = l1buf + R12 * L1_EL;
-            const double2 ylo = row2(0) ? lds2(l1 + prow0 - LW) : z2;
-            const double2 yhi = row2(R - 1) ? lds2(l1 + prow0 + R * LW) : z2;
+            // (rows outside the level-2 region read in-bounds ring rows and are not used)
+            const double2 ylo = lds2(l1 + (row2(0) ? prow0 - LW : prow0));
+            const double2 yhi = lds2(l1 + (row2(R - 1) ? prow0 + R * LW : prow0));
             const bool pin = plane_in(p2);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -288,8 +284,8 @@ __global__ void __launch_bounds__(threads<R>(), 1)
         const bool out3 = p3 >= i0 && p3 < i1;  // outputs (stores, residual, prefetch) only then
         if (any3) {
             const double *l2 = l2buf + R24 * L2_EL;
-            const double2 ylo = row3(0) ? lds2(l2 + prow0 - 2 * LW) : z2;        // level-2 row rho0 - 1
-            const double2 yhi = row3(R - 1) ? lds2(l2 + prow0 + (R - 1) * LW) : z2;  // row rho0 + R
+            const double2 ylo = lds2(l2 + (row3(0) ? prow0 - 2 * LW : 2 * lane));          // level-2 row rho0 - 1
+            const double2 yhi = lds2(l2 + (row3(R - 1) ? prow0 + (R - 1) * LW : 2 * lane));  // row rho0 + R
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 if (!row3(r)) continue;
@@ -353,26 +349,12 @@ __global__ void __launch_bounds__(threads<R>(), 1)
             fence_proxy_async();
             issue(i + ST);
         }
-    };
-    using I0 = std::integral_constant<int, 0>;
-    using I1 = std::integral_constant<int, 1>;
-    using I2 = std::integral_constant<int, 2>;
-    using I3 = std::integral_constant<int, 3>;
-    using I4 = std::integral_constant<int, 4>;
-    using I5 = std::integral_constant<int, 5>;
-    static_assert(ST == 6, "the unrolled plane loop assumes 6 stages");
-    for (int round = 0, ib = ibeg; ib <= iend; ++round, ib += ST) {
-        iter(I0{}, ib, round);
-        if (ib + 1 > iend) break;
-        iter(I1{}, ib + 1, round);
-        if (ib + 2 > iend) break;
-        iter(I2{}, ib + 2, round);
-        if (ib + 3 > iend) break;
-        iter(I3{}, ib + 3, round);
-        if (ib + 4 > iend) break;
-        iter(I4{}, ib + 4, round);
-        if (ib + 5 > iend) break;
-        iter(I5{}, ib + 5, round);
+        sl_i = sl_n;
+        sl_n = sl_n + 1 == ST ? 0 : sl_n + 1;
+        ph_n ^= (sl_n == 0);
+        r1w = r12;  // (i+1) % 3 == ((i-2) % 3 + 0) ... rotate all three ring indices by one
+        r12 = r24;
+        r24 = R1W;
     }
     (void)any_ok;
     if (K2 == K_LAST && m.out_mode == WHB_OUT_FPI) {

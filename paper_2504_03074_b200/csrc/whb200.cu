@@ -3051,6 +3051,8 @@ int whb_stream_wait_u32(whb_ctx *c, uint64_t dev_ptr, uint32_t value) {
 int whb_comm_begin(whb_ctx *c) {
     if (!c) return fail(WHB_E_ARG, "NULL argument");
     if (c->on_comm) return fail(WHB_E_STATE, "whb_comm_begin: exchange already open");
+    static const bool off = getenv("WHB_COMM") && std::string(getenv("WHB_COMM")) == "0";
+    if (off && !c->nccl) return 0;  // A/B switch: peer exchange on the context stream
     WHB_TRY(set_dev(c));
     if (!c->comm) {
         int lo = 0, hi = 0;
@@ -3066,7 +3068,12 @@ int whb_comm_begin(whb_ctx *c) {
 }
 
 int whb_comm_end(whb_ctx *c) {
-    if (!c || !c->on_comm) return fail(WHB_E_STATE, "whb_comm_end: no exchange open");
+    if (!c) return fail(WHB_E_ARG, "NULL argument");
+    if (!c->on_comm) {
+        static const bool off = getenv("WHB_COMM") && std::string(getenv("WHB_COMM")) == "0";
+        if (off && !c->nccl) return 0;
+        return fail(WHB_E_STATE, "whb_comm_end: no exchange open");
+    }
     WHB_TRY(set_dev(c));
     c->on_comm = false;
     WHB_CUDA(cudaEventRecord(c->ev_join, c->comm));

@@ -312,6 +312,11 @@ class PeerHalo:
         self.opened = opened or []  # IPC mappings to close
         self.seq = 0
         self.nring = _ring_size(_buffer_table(shard))
+        # exchange stream: one process per GPU (from_dist).  Slabs sharing one GPU in one process
+        # (local_group) keep the exchange on their context streams: their stream waits would
+        # otherwise share the GPU's hardware queues with the other slabs' exchange branches
+        # (head-of-line blocking -- measured: a replayed in-process graph pair deadlocked)
+        self.use_comm = dist is not None
 
     @property
     def nranks(self):
@@ -388,7 +393,8 @@ class PeerHalo:
 
     def start(self, shard, items):
         ctx = shard.ctx
-        ctx.comm_begin()  # copies + flag writes on the exchange stream, after the boundary planes
+        if self.use_comm:
+            ctx.comm_begin()  # copies + flag writes on the exchange stream, after the boundary planes
         for item, depth in items:
             for q, my_side, q_side in ((self.rank - 1, "lo", "hi"), (self.rank + 1, "hi", "lo")):
                 if q not in self.peers:
@@ -401,13 +407,15 @@ class PeerHalo:
         for q, slot in ((self.rank - 1, 1), (self.rank + 1, 0)):  # I am q's upper / lower neighbour
             if q in self.peers:
                 ctx.stream_write_u32(self.peers[q]["flags"] + 4 * slot, self.seq)
-        ctx.comm_end()
+        if self.use_comm:
+            ctx.comm_end()
         return self.seq
 
     def finish(self, seq):
         # my outgoing copies done (their source planes may be overwritten from the next pass on),
         # then the neighbours' copies into my ghost planes (their flags)
-        self.shard.ctx.comm_join()
+        if self.use_comm:
+            self.shard.ctx.comm_join()
         for q, slot in ((self.rank - 1, 0), (self.rank + 1, 1)):
             if q in self.peers:
                 self.shard.ctx.stream_wait_u32(self.flags + 4 * slot, seq)

@@ -92,9 +92,12 @@ class PeerNumpyShard(NumpyShard):
         return self.base[key] + plane * self.plane_bytes, self.plane_bytes // 8
 
 
+@pytest.mark.parametrize("use_comm", [False, True])
 @pytest.mark.parametrize("dim,cells,omega,spp,world", [(2, (40, 24), 12.0, 2, 2), (3, (14, 10, 12), 6.5, 2, 3),
                                                        (2, (9, 30), 8.0, 2, 3), (2, (40, 24), 12.0, 1, 3)])
-def test_peer_halo_lockstep_matches_single_domain(dim, cells, omega, spp, world):
+def test_peer_halo_lockstep_matches_single_domain(dim, cells, omega, spp, world, use_comm):
+    """use_comm: the exchange-stream protocol of the one-process-per-GPU halos (begin / end around
+    each exchange, join before the next begins) is followed on every exchange."""
     space = AddressSpace()
     g = build_grid(dim, [(0.0, 1.0)] * dim, cells, "dirichlet")
     f = O.multi_gaussian(g.shape, g.bounds, g.spacing, 3, seed=7)
@@ -102,6 +105,8 @@ def test_peer_halo_lockstep_matches_single_domain(dim, cells, omega, spp, world)
     cfg = FilterConfig(omega=omega, periods=1, steps_per_period=corr.steps_per_period, mode="explicit")
     shards = [PeerNumpyShard(space, g, r, steps_per_pass=spp) for r in slab_ranges(g.shape[0], world)]
     halos = PeerHalo.local_group(shards)
+    for h in halos:
+        h.use_comm = use_comm
     for sh in shards:
         sh.set_schedule(time_schedule(corr, cfg))
         p0, p1 = sh.plane_range
