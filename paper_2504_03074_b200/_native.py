@@ -553,6 +553,7 @@ class Context:
         check(load().whb_comm_join(self._h), "whb_comm_join")
 
     def nccl_init(self, nranks: int, rank: int, uid: bytes):
+        _load_torch_nccl()
         buf = ctypes.create_string_buffer(bytes(uid), 128)
         check(load().whb_nccl_init(self._h, int(nranks), int(rank), buf), "whb_nccl_init")
 
@@ -616,7 +617,18 @@ class Context:
         return tuple(int(x) for x in s), p.value, n.value
 
 
+def _load_torch_nccl():
+    """whb_nccl_* dlopen libnccl.so.2 and reuse a copy the process already loaded: load torch's
+    (libtorch_cuda links it) first, so torch and the C ABI share one NCCL -- a system libnccl
+    loaded first would shadow torch's newer one (its symbols then fail to resolve)."""
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
+
+
 def nccl_unique_id() -> bytes:
+    _load_torch_nccl()
     buf = ctypes.create_string_buffer(128)
     check(load().whb_nccl_unique_id(buf), "whb_nccl_unique_id")
     return buf.raw
