@@ -856,9 +856,9 @@ cudaError_t tb2_set_attrs(size_t smem) {
 #define WHB_S3_ST 6
 #endif
 constexpr int S3_ST = WHB_S3_ST;
-// level-1 rows per warp (2: 8 warps, each lane 2 rows x 2 columns; 1: 16 warps)
+// level-1 rows per warp (1: 16 warps, measured fastest; 2: 8 warps, each lane 2 rows x 2 columns)
 #ifndef WHB_S3_R
-#define WHB_S3_R 2
+#define WHB_S3_R 1
 #endif
 constexpr int S3_R = WHB_S3_R;
 constexpr int S3_THREADS = t3::threads<S3_R>();
