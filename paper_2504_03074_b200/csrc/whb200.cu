@@ -851,16 +851,21 @@ cudaError_t tb2_set_attrs(size_t smem) {
     return e;
 }
 
-// Three-step 3D kernel (step_t3.cuh): 7 W^s / W^{s-1} TMA stages of 18 KB + the level rings (196 KB),
-// one 512-thread CTA per SM.
+// Three-step 3D kernel (step_t3.cuh): 6 TMA stages of 26 KB + the level-1/2 rings (202 KB), 1 CTA/SM.
 #ifndef WHB_S3_ST
-#define WHB_S3_ST 7
+#define WHB_S3_ST 6
 #endif
 constexpr int S3_ST = WHB_S3_ST;
+// level-1 rows per warp (1: 16 warps, measured fastest; 2: 8 warps, each lane 2 rows x 2 columns)
+#ifndef WHB_S3_R
+#define WHB_S3_R 1
+#endif
+constexpr int S3_R = WHB_S3_R;
+constexpr int S3_THREADS = t3::threads<S3_R>();
 
 template <int K1, int K2, bool ZF, int GM>
 auto t3_fn() {
-    return t3::t3_kernel<S3_ST, K1, K2, ZF, GM>;
+    return t3::t3_kernel<S3_ST, K1, K2, ZF, GM, S3_R>;
 }
 
 cudaError_t t3_set_attrs(size_t smem) {
@@ -1156,7 +1161,7 @@ int plan_launch(whb_ctx *c) {
         cudaError_t e = t3_set_attrs(c->smem3);
         if (e != cudaSuccess) return fail(WHB_E_CUDA, std::string("cudaFuncSetAttribute(t3): ") + cudaGetErrorString(e));
         int nb = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, t3_fn<K_MID, K_MID, false, 2>(), t3::THREADS, c->smem3);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, t3_fn<K_MID, K_MID, false, 2>(), S3_THREADS, c->smem3);
         if (e != cudaSuccess || nb < 1) return fail(WHB_E_CUDA, "t3 kernel does not fit on an SM");
         c->gx3 = (int)((n2 - 1 + t3::TX - 1) / t3::TX);
         c->JT3 = (int)((n1 - 1 + t3::BY - 1) / t3::BY);
@@ -1473,10 +1478,12 @@ int launch_t3(whb_ctx *c, int s, bool last) {
     const bool zf = c->cur_zf != 0;
     const Member &m0 = c->h_members[0];
     const MemberHost &mh = c->mem[c->order[0]];
-    CUtensorMap tw, tp;
+    CUtensorMap tw, tp, tf;
     std::memset(&tp, 0, sizeof(tp));
+    std::memset(&tf, 0, sizeof(tf));
     WHB_TRY(tensor_map(c, level_ptr(m0, s), t3::RW, t3::WR, &tw));
     WHB_TRY(tensor_map(c, level_ptr(m0, s - 1), t3::LW, t3::NR, &tp));
+    if (m0.f) WHB_TRY(tensor_map(c, m0.f, t3::LW, t3::NR, &tf));
     t3::Scal sc;
     const bool first = (s == 0);
     sc.h1 = first ? mh.half_dt2 : mh.dt2;
@@ -1493,8 +1500,8 @@ int launch_t3(whb_ctx *c, int s, bool last) {
     const int gm = geom_mode(c);
     auto go = [&](auto k1, auto k2, auto zft, auto gmt) {
         t3_fn<decltype(k1)::value, decltype(k2)::value, decltype(zft)::value, decltype(gmt)::value>()
-            <<<grid, t3::THREADS, c->smem3, c->stream>>>(c->geom, c->d_members, s, c->upd_lo, c->upd_hi, c->chunk3,
-                                                         c->JT3, sc, tw, tp);
+            <<<grid, S3_THREADS, c->smem3, c->stream>>>(c->geom, c->d_members, s, c->upd_lo, c->upd_hi, c->chunk3,
+                                                         c->JT3, sc, tw, tp, tf);
     };
     using KF = std::integral_constant<int, K_FIRST>;
     using KM = std::integral_constant<int, K_MID>;
