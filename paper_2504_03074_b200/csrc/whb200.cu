@@ -459,6 +459,106 @@ __global__ void step_general_kernel(GeomG g, const Member *__restrict__ members,
     }
 }
 
+// One leapfrog step of the general operator, marching: thread = one (j, k) column of a chunk of
+// axis-0 planes.  The 2h+1 axis-0 taps of the column come from a register window that takes one
+// new (boundary-imaged) value per plane; axis-1/-2 taps are loads of neighbouring columns (L1 /
+// L2 hits).  No 64-bit div/mod per point (the grid-stride kernel above decodes t -> (plane, j, k)).
+// Whole-grid contexts only (plane_begin == 0), as the general plan.  Same arithmetic and order as
+// general_lap / step_general_kernel.
+template <int H>
+__global__ void __launch_bounds__(128) step_general_march_kernel(GeomG g, const Member *__restrict__ members, int s,
+                                                                 int nloc, int chunk, int JY) {
+    const Member m = members[blockIdx.z];
+    const int kind = (s == 0) ? K_FIRST : ((s == m.n_total - 1) ? K_LAST : K_MID);
+    const double *wcur = level_ptr(m, s);
+    const double *wprv = level_ptr(m, s - 1);
+    double *wnxt = level_ptr(m, s + 1);
+    const double cosn = (kind == K_FIRST) ? 1.0 : m.cos_f[s];
+    const double h = (kind == K_FIRST) ? m.half_dt2 : m.dt2;
+    const double acc0 = m.acc_c[0], accn = m.acc_c[s + 1];
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y % JY;
+    const int pl0 = (blockIdx.y / JY) * chunk;
+    const int pl1 = min(nloc, pl0 + chunk);
+    double rsum = 0.0;
+    const bool col_ok = k < g.n[2];
+    const long long cbase = (long long)j * g.P + k;  // column offset inside a plane
+    // axis-0 window: win[q] = w at plane gi - H + q (imaged)
+    double win[2 * H + 1];
+    auto z_at = [&](int gi) -> double {  // w at global plane gi of this column, boundary-imaged
+        int idx = gi;
+        const int n = g.n[0];
+        double sign = 1.0;
+        if (g.per[0]) {
+            idx = (idx % n + n) % n;
+        } else if (idx < 0) {
+            idx = -idx;
+            sign = -1.0;
+        } else if (idx > n - 1) {
+            idx = 2 * (n - 1) - idx;
+            sign = -1.0;
+        }
+        const double v = __ldg(wcur + (long long)(idx - g.plane_begin + GH) * g.S0 + cbase);
+        return sign < 0.0 ? -v : v;
+    };
+    if (col_ok && pl0 < pl1 && g.act[0]) {
+#pragma unroll
+        for (int q = 0; q < 2 * H; ++q) win[q + 1] = z_at(g.plane_begin + pl0 - H + q);
+    }
+    for (int pl = pl0; pl < pl1 && col_ok; ++pl) {
+        const int gi = g.plane_begin + pl;
+        if (g.act[0]) {
+#pragma unroll
+            for (int q = 0; q < 2 * H; ++q) win[q] = win[q + 1];
+            win[2 * H] = z_at(gi + H);
+        }
+        if (!general_updates(g, gi, j, k)) continue;
+        const long long p = (pl + GH) * g.S0 + cbase;
+        const double wc = wcur[p];
+        double lap = 0.0;
+        if (g.act[0]) {
+#pragma unroll
+            for (int q = 0; q <= 2 * H; ++q) lap = whb_add(lap, whb_mul(g.taps[0][q], win[q]));
+        }
+#pragma unroll
+        for (int a = 1; a < 3; ++a) {
+            if (!g.act[a]) continue;
+#pragma unroll
+            for (int q = 0; q <= 2 * H; ++q) lap = whb_add(lap, whb_mul(g.taps[a][q], gfetch(g, wcur, p, gi, j, k, a, q - H)));
+        }
+        if (g.use_c2) lap = whb_mul(lap, g.c2);
+        double wn;
+        if (kind == K_FIRST) {
+            const double d = m.f ? whb_sub(lap, m.f[p]) : lap;
+            wn = whb_add(wc, whb_mul(h, d));
+            wnxt[p] = wn;
+            m.acc[p] = whb_add(whb_mul(acc0, wc), whb_mul(accn, wn));
+        } else {
+            const double d = m.f ? whb_sub(lap, whb_mul(m.f[p], cosn)) : lap;
+            wn = whb_add(whb_sub(whb_mul(2.0, wc), wprv[p]), whb_mul(h, d));
+            if (kind == K_MID) {
+                wnxt[p] = wn;
+                m.acc[p] = whb_add(m.acc[p], whb_mul(accn, wn));
+            } else {
+                const double out = whb_mul(m.out_scale, whb_add(m.acc[p], whb_mul(accn, wn)));
+                if (m.out_mode == WHB_OUT_FPI) {
+                    const double dd = out - m.v[p];
+                    rsum += dd * dd;
+                    m.v[p] = out;
+                } else if (m.out_mode == WHB_OUT_AV) {
+                    m.dst[p] = whb_sub(m.v[p], out);
+                } else {
+                    m.dst[p] = out;
+                }
+            }
+        }
+    }
+    if (kind == K_LAST && m.out_mode == WHB_OUT_FPI) {
+        const double b = block_sum(rsum);
+        if (threadIdx.x == 0) m.partials[blockIdx.y * gridDim.x + blockIdx.x] = b;
+    }
+}
+
 __global__ void apply_general_kernel(GeomG g, const double *__restrict__ x, double *__restrict__ y, int nloc) {
     const int n1 = g.act[1] ? g.n[1] : 1, n2 = g.n[2];
     const long long total = (long long)nloc * n1 * n2;
@@ -690,6 +790,7 @@ struct whb_ctx {
     long long flush_elems = 0;
     double *stage = nullptr;         // contiguous staging buffer for host transfers
     GeomG geomg{};                   // general operator (kern == 3)
+    int gm_gx = 0, gm_jy = 1, gm_chunk = 1, gm_nch = 0;  // its marching launch plan (0: grid-stride kernel)
     // TMA tensor maps keyed by (buffer, box kind)
     std::map<std::tuple<const double *, int, int>, CUtensorMap> tmaps;
     // implicit-mode solvers (whb_mg_setup / whb_tri_setup)
@@ -1314,8 +1415,18 @@ int launch_step_members(whb_ctx *c, int s, int moff, int nact, int i_begin, int 
     if (nact <= 0 || i_begin >= i_end) return 0;
     if (c->kern == 3) {
         if (moff != 0) return fail(WHB_E_STATE, "general kernel launches start at member 0");
-        step_general_kernel<<<dim3(kGenBlocks, nact, 1), 256, 0, c->stream>>>(c->geomg, c->d_members, s, (int)c->nloc,
-                                                                          part_off);
+        if (c->gm_nch > 0) {
+            dim3 grid(c->gm_gx, c->gm_jy * c->gm_nch, nact);
+            if (c->geomg.order == 4)
+                step_general_march_kernel<2><<<grid, 128, 0, c->stream>>>(c->geomg, c->d_members, s, (int)c->nloc,
+                                                                         c->gm_chunk, c->gm_jy);
+            else
+                step_general_march_kernel<1><<<grid, 128, 0, c->stream>>>(c->geomg, c->d_members, s, (int)c->nloc,
+                                                                         c->gm_chunk, c->gm_jy);
+        } else {
+            step_general_kernel<<<dim3(kGenBlocks, nact, 1), 256, 0, c->stream>>>(c->geomg, c->d_members, s,
+                                                                              (int)c->nloc, part_off);
+        }
         c->launches++;
         WHB_CUDA(cudaGetLastError());
         return 0;
@@ -1758,7 +1869,8 @@ int enqueue_solve(whb_ctx *c, int out_mode) {
             WHB_TRY(launch_step(c, s, active_members(c, s), c->upd_lo, c->upd_hi, c->chunk_len, 0));
     }
     if (out_mode == WHB_OUT_FPI) {
-        int np = c->kern == 3 ? kGenBlocks : c->gx * c->JT * c->nchunks;
+        int np = c->kern == 3 ? (c->gm_nch > 0 ? c->gm_gx * c->gm_jy * c->gm_nch : kGenBlocks)
+                              : c->gx * c->JT * c->nchunks;
         if (c->tb2) np = std::max(np, c->gx2 * c->JT2 * c->nch2);
         if (c->t3) np = std::max(np, c->gx3 * c->JT3 * c->nch3);
         if (c->wfT) np = std::max(np, std::max(c->gxw[2] * c->nchw[2], c->wfT == 4 ? c->gxw[4] * c->nchw[4] : 0));
@@ -2384,11 +2496,28 @@ int whb_set_operator_general(whb_ctx *c, int order, const int *periodic, const d
     c->cres = false;
     c->tb2 = false;
     c->wfT = 0;
+    // marching plan (WHB_GEN_MARCH=0: the grid-stride kernel): 128 columns per CTA along axis 2,
+    // one CTA row per axis-1 index, axis-0 chunks so that ~4 waves of 16 CTAs per SM exist
+    {
+        const char *ge = getenv("WHB_GEN_MARCH");
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+        c->gm_gx = (int)((c->gshape[2] + 127) / 128);
+        c->gm_jy = g.act[1] ? (int)c->gshape[1] : 1;
+        const long long cols = (long long)c->gm_gx * c->gm_jy;
+        const int nl = (int)c->nloc;
+        long long nch = std::max<long long>(1, (4LL * sms * 16 + cols - 1) / cols);
+        nch = std::min<long long>(nch, std::max(1, nl / 8));  // chunks of >= 8 planes
+        c->gm_chunk = (int)((nl + nch - 1) / nch);
+        c->gm_nch = (nl + c->gm_chunk - 1) / c->gm_chunk;
+        if ((ge && std::string(ge) == "0") || (long long)c->gm_jy * c->gm_nch > 65535) c->gm_nch = 0;
+    }
     for (auto &kv : c->graphs) cudaGraphExecDestroy(kv.second);
     c->graphs.clear();
     c->graph_kernels.clear();
-    if (c->nparts < kGenBlocks) {
-        c->nparts = kGenBlocks;
+    const int np_gen = std::max(kGenBlocks, c->gm_gx * c->gm_jy * c->gm_nch);
+    if (c->nparts < np_gen) {
+        c->nparts = np_gen;
         for (auto &m : c->mem) {
             cudaFree(m.partials);
             WHB_CUDA(cudaMalloc(&m.partials, (size_t)c->nparts * sizeof(double)));

@@ -22,8 +22,19 @@ def grid_of(case):
     return wh.build_grid(case["dim"], [tuple(b) for b in case["bounds"]], case["cells"], case["bcs"])
 
 
+@pytest.fixture(params=["march", "grid-stride"])
+def general_kernel(request, monkeypatch):
+    """Both general-operator kernels: the marching one (default) and the grid-stride one
+    (WHB_GEN_MARCH=0); the plan is made when a context gets the operator, so fresh contexts."""
+    wh.release_device_cache()
+    if request.param == "grid-stride":
+        monkeypatch.setenv("WHB_GEN_MARCH", "0")
+    yield request.param
+    wh.release_device_cache()
+
+
 @pytest.mark.parametrize("key", EXT)
-def test_general_operator_wave_solve_bitwise(gpu_available, key):
+def test_general_operator_wave_solve_bitwise(gpu_available, general_kernel, key):
     meta, A = load_golden("ext")
     case = meta["cases"][key]
     g = grid_of(case)
@@ -43,7 +54,7 @@ def test_general_operator_wave_solve_bitwise(gpu_available, key):
     assert sha(wh.waveholtz_operator(prob, cfg, corr=corr)(A[key + "__v"])) == case["av_sha256"]
 
 
-def test_fpi_periodic_order4_bitwise(gpu_available):
+def test_fpi_periodic_order4_bitwise(gpu_available, general_kernel):
     meta, A = load_golden("ext")
     case = meta["cases"]["fpi_per_p4"]
     g = wh.build_grid(2, [(0.0, 1.0)] * 2, [24, 24], "periodic")
@@ -96,3 +107,22 @@ def test_general_operator_larger_grids_vs_oracle(gpu_available, cells, bcs, p):
     sc = O.step_scalars(corr.steps_per_period, corr.dt, corr.omega_tilde)
     ref = O.wave_solve_filtered(np.array(v.values), np.array(f.values), g.spacing, sc, 1.0, names, p)
     assert np.array_equal(out.values, ref)
+
+
+@pytest.mark.parametrize("dim,cells,bcs,order", [(3, (40, 33, 70), "periodic", 4), (2, (300, 257), "dirichlet", 4),
+                                                 (3, (24, 30, 36), ["periodic", "dirichlet", "periodic"], 2)])
+def test_general_kernels_larger_grids_against_oracle(gpu_available, general_kernel, dim, cells, bcs, order):
+    """Beyond the fixture sizes (several axis-0 chunks and axis-2 tiles of the marching kernel):
+    one W(v, f) bitwise against the numpy restatement (oracle/waveholtz_oracle.py)."""
+    g = wh.build_grid(dim, [(0.0, 1.0)] * dim, cells, bcs)
+    bl = [bcs] * dim if isinstance(bcs, str) else list(bcs)
+    f = np.array(O.multi_gaussian(g.shape, g.bounds, g.spacing, 3, seed=11))
+    v = O.zero_dirichlet(np.random.default_rng(2).standard_normal(g.shape) * 1e-2, bl)
+    f = O.zero_dirichlet(f, bl)
+    corr = wh.correct_explicit(8.5, g, order, 1.0)
+    cfg = wh.FilterConfig(omega=8.5, periods=1, steps_per_period=corr.steps_per_period, mode="explicit")
+    out = wh.wave_solve_filtered(wh.GridField.from_values(g, v), wh.GridField.from_values(g, f), cfg, corr,
+                                 wh.DiscreteOperator(g, order, 1.0)).values
+    sc = O.step_scalars(corr.steps_per_period, corr.dt, corr.omega_tilde)
+    ref = O.wave_solve_filtered(v, f, g.spacing, sc, 1.0, bl, order)
+    assert np.array_equal(out, ref)
