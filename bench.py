@@ -69,7 +69,11 @@ WORKLOADS = {
     "cfg2": (2, 2048, 100.5, ("multi", 8), 50),
     "cfg3": (3, 256, 40.7, ("single", 100.0, 300.0, (0.45, 0.5, 0.55)), 30),
     "cfg4": (3, 1024, 150.3, ("multi", 16), 10),
+    # SURVEY 8(f) rank 2 (not a BASELINE config): config 2 with the order-4 stencil, on the
+    # general-operator kernel
+    "p4": (2, 2048, 100.5, ("multi", 8), 20),
 }
+ORDER = {"p4": 4}  # stencil order per workload (default 2)
 
 
 def peaks():
@@ -195,7 +199,7 @@ def build_workload(name):
         f = wh.gaussian_source(g, omega, forcing[1], forcing[2], forcing[3])
     else:
         f = wh.multi_gaussian_source(g, omega, forcing[1], seed=0, slab_planes=16 if dim == 3 else 64)
-    corr = wh.correct_explicit(omega, g, 2, 1.0)
+    corr = wh.correct_explicit(omega, g, ORDER.get(name, 2), 1.0)
     cfg = wh.FilterConfig(omega=omega, periods=1, steps_per_period=corr.steps_per_period, mode="explicit")
     return g, f, corr, cfg, iters
 
@@ -233,7 +237,7 @@ def config_for(name, iterations, ws, decomp="slab", halo="nccl", g=None, cfg=Non
     l2 = ("working set (7 fields x 8.6 GB) far above L2; flushed before every timed iteration anyway"
           if name == "cfg4" else "flushed before every timed iteration (256 MiB write, outside the timed span)")
     return {"workload": name, "grid": [n + 1] * dim, "omega": omega, "N_t": n_t, "iterations": iterations,
-            "cfl": 0.9, "forcing": forcing_desc(name), "parallelism": par, "l2": l2}
+            "cfl": 0.9, "order": ORDER.get(name, 2), "forcing": forcing_desc(name), "parallelism": par, "l2": l2}
 
 
 def lib_sha16():
@@ -251,7 +255,7 @@ def lib_sha16():
 # CPU baseline (numpy restatement = the reference's own numpy call sequence, 1 core)
 
 
-def cpu_baseline_numpy(g, f, corr, target_s=12.0):
+def cpu_baseline_numpy(g, f, corr, target_s=12.0, order=2):
     from oracle import waveholtz_oracle as O
 
     sc = O.step_scalars(corr.steps_per_period, corr.dt, corr.omega_tilde)
@@ -264,7 +268,7 @@ def cpu_baseline_numpy(g, f, corr, target_s=12.0):
         s = dict(sc)
         s["n_total"] = nsteps
         t0 = time.perf_counter()
-        O.wave_solve_filtered(v, fv, g.spacing, s)
+        O.wave_solve_filtered(v, fv, g.spacing, s, 1.0, ["dirichlet"] * g.dim, order)
         return time.perf_counter() - t0
 
     t3 = run(3)
@@ -304,9 +308,10 @@ class SingleRun:
 
         g, f, corr, cfg, _ = build_workload(args.workload)
         self.g, self.f, self.corr, self.cfg = g, f, corr, cfg
-        self.prob = wh.HelmholtzProblem(g, 2, 1.0, cfg.omega, f)
+        self.order = ORDER.get(args.workload, 2)
+        self.prob = wh.HelmholtzProblem(g, self.order, 1.0, cfg.omega, f)
         sched = wh.time_schedule(corr, cfg)
-        self.dp = DeviceProblem(g, c=1.0, device=local)
+        self.dp = DeviceProblem(g, c=1.0, order=self.order, device=local)
         self.dp.set_schedule(sched)
         self.dp.set_forcing(f.values)
         self.ctx = self.dp.ctx
@@ -820,7 +825,7 @@ def run_ours(args, dist, ws, rank, local):
             f = wh.multi_gaussian_source(wl.g, 150.3, 4, seed=0)
             cpu = cpu_baseline_numpy(wl.g, f, corr)
         else:
-            cpu = cpu_baseline_numpy(wl.g, wl.f, wl.corr)
+            cpu = cpu_baseline_numpy(wl.g, wl.f, wl.corr, order=ORDER.get(args.workload, 2))
 
     if rank == 0:
         line = {
@@ -851,6 +856,19 @@ def run_reference(args, ws, rank):
 
     if args.workload == "cfg5":
         return run_reference_cfg5(args, ws)
+    if ORDER.get(args.workload, 2) != 2:  # the C restatement is order 2: the numpy one (1 core)
+        g, f, corr, cfg, _ = build_workload(args.workload)
+        cpu = cpu_baseline_numpy(g, f, corr, target_s=20.0, order=ORDER[args.workload])
+        line = {"metric": METRIC, "value": cpu["value"], "unit": "Gpts/s", "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (BASELINE forcing recipe, SURVEY 8(d)); f sha256 "
+                        + hashlib.sha256(np.ascontiguousarray(f.values).data).hexdigest()[:16],
+                "config": config_for(args.workload, args.steps, ws, args.decomp, args.halo, n_t=corr.steps_per_period),
+                "impl": "reference", "cpu_baseline": cpu,
+                "e2e": {"value": cpu["value"], "unit": "Gpts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
     g, f, corr, cfg, _ = build_workload(args.workload)
     sc = O.step_scalars(corr.steps_per_period, corr.dt, corr.omega_tilde)
     fv = np.array(f.values)

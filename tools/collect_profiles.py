@@ -38,19 +38,18 @@ def main(rnd, src=None, dst_root=None):
     dst_root = os.path.abspath(dst_root) if dst_root else ROOT
     dst = os.path.join(dst_root, "profiles", rnd)
     os.makedirs(dst, exist_ok=True)
-    for w in ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "imp2"):
+    W = ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "p4", "imp2")
+    for w in W:
         for arm in ("bench", "bench_reference"):
             d = last_json(os.path.join(SRC, f"{arm}_{w}.json"))
             if d is not None:
                 json.dump(d, open(os.path.join(dst, f"{arm}_{w}.json"), "w"))
-    cmds = {"cfg1": "--workload cfg1 --steps 2 --warmup 1", "cfg2": "--workload cfg2 --steps 2 --warmup 1",
-            "cfg3": "--workload cfg3 --steps 2 --warmup 1", "cfg4": "--workload cfg4 --steps 1 --warmup 1",
-            "cfg5": "--workload cfg5 --steps 1 --warmup 1"}
-    for w, a in cmds.items():
+    for w in W:
         p = os.path.join(SRC, f"launches_{w}.csv")
         if os.path.exists(p):
-            out = summarise(p, f"ncu --metrics gpu__time_duration.sum --clock-control none python bench.py {a} "
-                               "--no-e2e --no-cpu-baseline")
+            steps = "--steps 1" if w in ("cfg4", "cfg5", "p4", "imp2") else "--steps 2"
+            out = summarise(p, f"ncu --metrics gpu__time_duration.sum --clock-control none python bench.py --workload "
+                               f"{w} {steps} --warmup 1 --no-e2e --no-cpu-baseline")
             json.dump(out, open(os.path.join(dst, f"launches_{w}.json"), "w"), indent=1)
     traffic_path = os.path.join(dst_root, "profiles", "traffic.json")
     if not os.path.exists(traffic_path) and os.path.exists(os.path.join(ROOT, "profiles", "traffic.json")):
@@ -58,8 +57,13 @@ def main(rnd, src=None, dst_root=None):
         os.makedirs(os.path.dirname(traffic_path), exist_ok=True)
         open(traffic_path, "w").write(open(traffic_path_src).read())
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
-    for name, w in (("ncu_cfg1_cres", "cfg1"), ("ncu_cfg2_wf", "cfg2"), ("ncu_cfg3_tb2", "cfg3"),
-                    ("ncu_cfg4_tb2", "cfg4"), ("ncu_imp2_gs", "imp2")):
+    lib_sha = None
+    try:
+        lib_sha = open(os.path.join(SRC, "lib.sha")).read().split()[0][:16]
+    except (OSError, IndexError):
+        pass
+    for w in W:
+        name = f"ncu_{w}"
         rep = os.path.join(SRC, name + ".ncu-rep")
         if not os.path.exists(rep):
             continue
@@ -70,7 +74,7 @@ def main(rnd, src=None, dst_root=None):
             k["dram__bytes_read.sum"][1]]
         wr = float(k["dram__bytes_write.sum"][0]) * {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1}[
             k["dram__bytes_write.sum"][1]]
-        traffic[w] = {"bytes_per_launch": rd + wr, "kernel": k["kernel"][:60],
+        traffic[w] = {"bytes_per_launch": rd + wr, "kernel": k["kernel"][:60], "lib_sha16": lib_sha,
                       "source": f"profiles/{rnd}/{name}.json (ncu --set full, cold cache): "
                                 "dram__bytes_read.sum + dram__bytes_write.sum"}
     json.dump(traffic, open(traffic_path, "w"), indent=1)

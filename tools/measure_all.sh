@@ -1,46 +1,48 @@
 #!/usr/bin/env bash
 # Round-end measurement pass on one B200 (run under gpurun from the repo root):
-#   bench lines for every workload (ours + reference arm), ncu launch lists, and one
-#   `ncu --set full` capture of each dominant kernel.  Outputs land in gpurun_out/m/;
-#   tools/collect_profiles.py turns them into profiles/<round>/.
+#   bench lines for every workload (ours + reference arm), ncu launch lists of the same bench
+#   commands, and one `ncu --set full` capture of each dominant kernel.  Outputs land in
+#   gpurun_out/m/; tools/collect_profiles.py turns them into profiles/<round>/ (+ traffic.json
+#   keyed by the library's sha256).  MEASURE_PART = bench | ncu | all; MEASURE_WORKLOADS selects.
 set -u
+RND=${MEASURE_ROUND:-r02}
 OUT=gpurun_out/m
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/gpu.txt 2>&1
+sha256sum paper_2504_03074_b200/lib/libwhb200.so > $OUT/lib.sha 2>&1
 
 PART=${MEASURE_PART:-all}
+WL=${MEASURE_WORKLOADS:-cfg4 cfg2 cfg3 cfg5 cfg1 p4 imp2}
 if [ "$PART" != ncu ]; then
-for w in ${MEASURE_WORKLOADS:-cfg1 cfg2 cfg3 cfg4 cfg5 imp2}; do
-  python bench.py --workload $w > $OUT/bench_$w.json 2> $OUT/bench_$w.err
-  python bench.py --workload $w --impl reference > $OUT/bench_reference_$w.json 2> $OUT/bench_reference_$w.err
+for w in $WL; do
+  timeout 900 python bench.py --workload $w > $OUT/bench_$w.json 2> $OUT/bench_$w.err
+  timeout 900 python bench.py --workload $w --impl reference > $OUT/bench_reference_$w.json 2> $OUT/bench_reference_$w.err
 done
 fi
 if [ "$PART" != bench ]; then
-
-# launch lists (cold-cache, serialised: shares only); each command first runs plainly
 L="--metrics gpu__time_duration.sum --clock-control none --csv"
-C2="python bench.py --workload cfg2 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
-$C2 > $OUT/plain_cfg2.json && ncu $L -c 2000 --log-file $OUT/launches_cfg2.csv $C2 > $OUT/ncu_l_cfg2.log 2>&1
-C3="python bench.py --workload cfg3 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
-$C3 > $OUT/plain_cfg3.json && ncu $L -c 2000 --log-file $OUT/launches_cfg3.csv $C3 > $OUT/ncu_l_cfg3.log 2>&1
-C1="python bench.py --workload cfg1 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
-$C1 > $OUT/plain_cfg1.json && ncu $L -c 2000 --log-file $OUT/launches_cfg1.csv $C1 > $OUT/ncu_l_cfg1.log 2>&1
-C4="python bench.py --workload cfg4 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
-$C4 > $OUT/plain_cfg4.json && ncu $L -c 2000 --log-file $OUT/launches_cfg4.csv $C4 > $OUT/ncu_l_cfg4.log 2>&1
-C5="python bench.py --workload cfg5 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
-$C5 > $OUT/plain_cfg5.json && ncu $L -c 4000 --log-file $OUT/launches_cfg5.csv $C5 > $OUT/ncu_l_cfg5.log 2>&1
-
-# full captures of the dominant kernels (one launch each, after warm-up launches)
 F="--set full --clock-control none --import-source on -c 1"
-$C2 > $OUT/plain_cfg2b.json && ncu $F -k regex:wf2d_kernel -s 20 -o $OUT/ncu_cfg2_wf $C2 > $OUT/ncu_f_cfg2.log 2>&1
-$C3 > $OUT/plain_cfg3b.json && ncu $F -k regex:tb2_kernel -s 20 -o $OUT/ncu_cfg3_tb2 $C3 > $OUT/ncu_f_cfg3.log 2>&1
-$C1 > $OUT/plain_cfg1b.json && ncu $F -k regex:cres2d_kernel -s 1 -o $OUT/ncu_cfg1_cres $C1 > $OUT/ncu_f_cfg1.log 2>&1
-$C4 > $OUT/plain_cfg4b.json && ncu $F -k regex:tb2_kernel -s 10 -o $OUT/ncu_cfg4_tb2 $C4 > $OUT/ncu_f_cfg4.log 2>&1
-CI="python bench.py --workload imp2 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
-$CI > $OUT/plain_imp2.json && ncu $F -k regex:gs_block_kernel -s 200 -o $OUT/ncu_imp2_gs $CI > $OUT/ncu_f_imp2.log 2>&1
+for w in $WL; do
+  case $w in
+    cfg4) C="python bench.py --workload cfg4 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"; K=t3_kernel; S=10;;
+    cfg2) C="python bench.py --workload cfg2 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"; K=wf2d_kernel; S=20;;
+    cfg3) C="python bench.py --workload cfg3 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"; K=tb2_kernel; S=20;;
+    cfg5) C="python bench.py --workload cfg5 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"; K=wf2d_kernel; S=40;;
+    cfg1) C="python bench.py --workload cfg1 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"; K=cres2d_kernel; S=1;;
+    p4)   C="python bench.py --workload p4 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"; K=step_general_march; S=40;;
+    imp2) C="python bench.py --workload imp2 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"; K=gs_block_kernel; S=200;;
+  esac
+  # each command first runs plainly (exit 0), then under ncu
+  if timeout 900 $C > $OUT/plain_$w.json 2>&1; then
+    timeout 1500 ncu $L -c 4000 --log-file $OUT/launches_$w.csv $C > $OUT/ncu_l_$w.log 2>&1
+    if [ "${MEASURE_FULL:-1}" = 1 ]; then
+      timeout 2400 ncu $F -k regex:$K -s $S -o $OUT/ncu_$w $C > $OUT/ncu_f_$w.log 2>&1
+    fi
+  fi
+done
 fi
 # summarise on the box (ncu -i) and drop the reports: gpurun copies back at most 64 MiB
-python tools/collect_profiles.py r01 $OUT $OUT/collected > $OUT/collect.log 2>&1
+python tools/collect_profiles.py $RND $OUT $OUT/collected > $OUT/collect.log 2>&1
 for r in $OUT/*.ncu-rep; do
   [ -e "$r" ] || continue
   ncu -i "$r" --page raw --csv > "${r%.ncu-rep}_raw.csv" 2>/dev/null
