@@ -59,5 +59,7 @@ def test_converge_matches_reference_runner(gpu_available, name, tmp_path):
                 continue
             if col in ("method", "iterations", "converged", "predicted_mu"):
                 assert x == y, (name, col, x, y)
+            elif col == "relative_gap":  # |cr - mu| / mu of two nearly equal rates: absolute
+                assert x == y == "nan" or abs(float(x) - float(y)) <= max(rtol, 1e-8), (name, col, x, y)
             else:
                 assert close(x, y, max(rtol, 1e-8)) or (x == y == "nan"), (name, col, x, y)
