@@ -220,13 +220,15 @@ int who_fpi_lean(int nd, const int64_t *shape, const double *clo, const double *
             wm = (n == 1) ? wa : t;
             wn = wm;
         }
-        /* acc now holds v_new (boundary points: acc is 0 there) */
-        double ss = 0.0;
+        /* acc now holds v_new (boundary points: acc is 0 there).  The residual (a tolerance
+         * quantity, not bitwise) is summed in long double: a sequential fp64 sum of 1e9 squares
+         * drifts by ~1e-10 relative, more than the 1e-12 the GPU tests hold residuals to. */
+        long double ss = 0.0L;
         for (int64_t p = 0; p < N; ++p) {
             const double d = acc[p] - v[p];
-            ss += d * d;
+            ss += (long double)d * d;
         }
-        resid[k] = sqrt(ss) / sqrt((double)N);
+        resid[k] = sqrt((double)ss) / sqrt((double)N);
         memcpy(v, acc, (size_t)N * sizeof(double));
     }
     free(wa); free(wb); free(acc);

@@ -141,12 +141,41 @@ def field_from_device(ftype, grid, ghost, ctx, field_id):
     points are 0 by invariant, so the field is in the state set_values would leave it in."""
     try:
         fld = ftype(grid, ghost=ghost)
+        _pin_storage(fld)
         buf = fld._writable()
     except (AttributeError, TypeError):
         return ftype.from_values(grid, ctx.download(field_id), ghost=ghost)
     ctx.download_into(field_id, buf)
     fld._touch()
     return fld
+
+
+def _pin_storage(fld):
+    """Back a freshly made field by a recycled page-locked buffer (_native.PinnedPool), so its D2H
+    copy -- and its H2D copy when it is the next call's input -- run at full PCIe rate.  Our
+    GridField keeps its values unpadded (``_vals``); the reference's keeps a ghost-padded ``_buf``
+    (grid.py:197-206), whose ghost frame is zeroed here as its constructor would have left it.
+    Fields of other layouts keep their own storage."""
+    pool = _native.pinned_pool()
+    try:
+        if isinstance(getattr(fld, "_vals", None), np.ndarray) and not hasattr(fld, "_buf"):
+            fld._vals = pool.empty(fld._vals.shape)
+            return
+        if not isinstance(getattr(fld, "_buf", None), np.ndarray):
+            return
+        old = fld._buf
+        new = pool.empty(old.shape)
+    except RuntimeError:  # no page-locked memory (e.g. no CUDA driver): keep pageable storage
+        return
+    g = int(getattr(fld, "ghost", 0))
+    if g > 0:  # ghost frame := 0 (the interior is overwritten by the download)
+        for ax in range(new.ndim):
+            lo = [slice(None)] * new.ndim
+            lo[ax] = slice(0, g)
+            new[tuple(lo)] = 0.0
+            lo[ax] = slice(new.shape[ax] - g, None)
+            new[tuple(lo)] = 0.0
+    fld._buf = new
 
 
 def wave_solve_filtered(v, f, config, corr, op, linear_solver=None, implicit_first_step=True):
