@@ -200,16 +200,25 @@ class PinnedPool:
     replacing one field by a new one cycles between two pinned buffers instead of paying
     cudaHostAlloc (seconds at 8.6 GB) or pageable transfers (staged by the driver) per call."""
 
-    def __init__(self, keep_per_shape: int = 2):
+    def __init__(self, keep_per_shape: int = 2, limit_bytes: int = 40 << 30):
         self.keep = keep_per_shape
+        self.limit = limit_bytes  # page-locked bytes handed out + pooled (beyond: MemoryError)
         self.free = {}
+        self.held = 0
 
     def empty(self, shape) -> np.ndarray:
         import weakref
 
         key = tuple(int(x) for x in shape)
         stack = self.free.setdefault(key, [])
-        buf = stack.pop() if stack else PinnedBuffer(key)
+        if stack:
+            buf = stack.pop()
+        else:
+            nbytes = int(np.prod(key)) * 8
+            if self.held + nbytes > self.limit:
+                raise MemoryError("page-locked pool limit reached")
+            buf = PinnedBuffer(key)
+            self.held += nbytes
         arr = buf.array.view()
         weakref.finalize(arr, self._release, key, buf)
         return arr
@@ -219,6 +228,7 @@ class PinnedPool:
         if len(stack) < self.keep:
             stack.append(buf)
         else:
+            self.held -= int(np.prod(key)) * 8
             buf.free()
 
 

@@ -165,7 +165,7 @@ def _pin_storage(fld):
             return
         old = fld._buf
         new = pool.empty(old.shape)
-    except RuntimeError:  # no page-locked memory (e.g. no CUDA driver): keep pageable storage
+    except (RuntimeError, MemoryError):  # no page-locked memory / pool full: keep pageable storage
         return
     g = int(getattr(fld, "ghost", 0))
     if g > 0:  # ghost frame := 0 (the interior is overwritten by the download)
