@@ -241,12 +241,12 @@ def config_for(name, iterations, ws, decomp="slab", halo="nccl", g=None, cfg=Non
 
 
 def lib_sha16():
-    """sha256 (16 hex digits) of the CUDA library this process runs (the build being measured)."""
+    """The build being measured: sha256 (16 hex digits) of the library's build inputs (CUDA
+    sources, header, nvcc flags; _build.source_sha16 -- nvcc output itself is not byte-stable)."""
     from paper_2504_03074_b200 import _build
 
     try:
-        with open(_build.LIB, "rb") as fh:
-            return hashlib.sha256(fh.read()).hexdigest()[:16]
+        return _build.source_sha16()
     except OSError:
         return None
 

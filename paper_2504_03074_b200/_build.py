@@ -43,6 +43,22 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
+def source_sha16() -> str:
+    """sha256 (16 hex digits) of everything the library is built from: the CUDA sources, the
+    public header and the nvcc flags.  nvcc's output is not byte-reproducible (it embeds
+    per-compile module ids), so measurements are tied to the build inputs instead."""
+    import hashlib
+
+    h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
+    csrc = os.path.join(PKG, "csrc")
+    for fn in sorted(os.listdir(csrc)):
+        if fn.endswith((".cu", ".cuh", ".h")):
+            h.update(fn.encode())
+            h.update(open(os.path.join(csrc, fn), "rb").read())
+    h.update(open(os.path.join(ROOT, "include", "whb200.h"), "rb").read())
+    return h.hexdigest()[:16]
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB

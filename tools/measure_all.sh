@@ -9,7 +9,7 @@ RND=${MEASURE_ROUND:-r02}
 OUT=gpurun_out/m
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/gpu.txt 2>&1
-sha256sum paper_2504_03074_b200/lib/libwhb200.so > $OUT/lib.sha 2>&1
+python -c "from paper_2504_03074_b200 import _build; print(_build.source_sha16())" > $OUT/lib.sha 2>&1
 
 PART=${MEASURE_PART:-all}
 WL=${MEASURE_WORKLOADS:-cfg4 cfg2 cfg3 cfg5 cfg1 p4 imp2}
