@@ -360,7 +360,7 @@ class SingleRun:
         import paper_2504_03074_b200 as wh
         from paper_2504_03074_b200 import timestep as ts
 
-        op = wh.DiscreteOperator(self.g, 2, 1.0)
+        op = wh.DiscreteOperator(self.g, self.order, 1.0)
         v = wh.GridField.zeros(self.g)
         wh.wave_solve_filtered(v, self.f, self.cfg, self.corr, op)  # warm (forcing cached by generation)
         barrier(dist)
