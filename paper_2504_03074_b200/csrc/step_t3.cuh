@@ -12,8 +12,8 @@
 // Iteration i computes level 1 at plane i, level 2 at plane i-2 and level 3 at plane i-4.  Every
 // input of an iteration was produced by an EARLIER iteration (level 2 at i-2 reads level 1 at
 // planes i-3..i-1; level 3 at i-4 reads level 2 at i-5..i-3), so the three level updates of an
-// iteration are independent (3-way ILP per thread) and one __syncthreads per plane publishes
-// them.  Axis-0 neighbours and the pointwise terms (W^{s-1}, f, the previous level, the filter
+// iteration are independent (3-way ILP per thread) and one split barrier per plane (an mbarrier:
+// arrive after the level-1/2 stores, wait at the top of the next iteration) publishes them.  Axis-0 neighbours and the pointwise terms (W^{s-1}, f, the previous level, the filter
 // sum) come from per-thread register queues; the axis-1/axis-2 neighbours of the level being
 // stepped come from shared memory (W^s: the TMA stage; levels 1 and 2: 3-plane rings), axis-2
 // neighbours inside a warp by shuffles.
@@ -56,10 +56,15 @@ constexpr int P_EL = NR * LW;                    // 1024: W^{s-1} / f box (the l
 constexpr int STAGE = W_EL + 2 * P_EL;           // 3280 doubles = 26.2 KB
 constexpr int L1_EL = NR * LW;                   // level-1 plane
 constexpr int L2_EL = (NR - 2) * LW;             // level-2 plane (rows j0-1 .. j0+BY)
+constexpr int N2 = 4;                            // level-2 ring: planes i-5 .. i-2 (see the split barrier)
+
+__device__ __forceinline__ void arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bulk::smem_u32(bar)) : "memory");
+}
 
 template <int ST>
 constexpr size_t smem_bytes() {
-    return (size_t)(ST * STAGE + 3 * L1_EL + 3 * L2_EL) * sizeof(double) + ST * sizeof(uint64_t);
+    return (size_t)(ST * STAGE + 3 * L1_EL + N2 * L2_EL) * sizeof(double) + (ST + 1) * sizeof(uint64_t);
 }
 
 // Per-pass scalars (the reference's host expressions), passed as a kernel parameter.
@@ -93,7 +98,8 @@ __global__ void __launch_bounds__(threads<R>(), 1)
     extern __shared__ __align__(128) double smem[];
     double *l1buf = smem + (size_t)ST * STAGE;
     double *l2buf = l1buf + 3 * L1_EL;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(l2buf + 3 * L2_EL);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(l2buf + N2 * L2_EL);
+    uint64_t *itbar = bars + ST;  // per-plane split barrier: every thread arrives after its level 1/2 stores
 
     const Member m = members[0];
     const int w = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // warp-uniform
@@ -130,6 +136,7 @@ __global__ void __launch_bounds__(threads<R>(), 1)
 
     if (threadIdx.x == 0) {
         for (int t = 0; t < ST; ++t) mbar_init(bars + t, 1);
+        mbar_init(itbar, 32 * NR / R);  // every thread of the CTA
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int p = pfirst; p <= plast && p < pfirst + ST; ++p) issue(p);
     }
@@ -223,9 +230,23 @@ __global__ void __launch_bounds__(threads<R>(), 1)
     // measured slower: 4-7K instructions of loop body thrash the instruction cache).  Stage and
     // ring slots advance incrementally: plane p <-> stage slot (p - pfirst) % ST.
     int sl_i = 1 % ST, sl_n = 2 % ST, ph_n = 0;  // stages of planes i and i+1, phase of the latter
-    int r1w = 0, r12 = 1, r24 = 2;                // level-1 slot of plane i, level-1/-2 slot of i-2, level-2 of i-4
+    int r1w = 0, r12 = 1;  // level-1 ring (3 planes): slots of planes i and i-2
+    int w2 = N2 - 2;       // level-2 ring (4 planes): slot of plane i-2 ((i - 2 - ibeg) mod 4)
+    // Split per-plane barrier: a thread arrives on itbar right after its level-1 and level-2
+    // stores of iteration i and waits for everybody's arrival only at the top of iteration i+1,
+    // so the level-3 work of iteration i overlaps the barrier skew.  Safe because level 3 reads
+    // only the level-2 ring, at plane i-4, and a thread can run at most the level-3 part ahead:
+    // the level-2 store of iteration i+1 (plane i-1) lands in a different slot of the 4-plane ring;
+    // the level-1 / stage slots rewritten at i+1 were last read before the arrivals of iteration i.
     for (int i = ibeg; i <= iend; ++i) {
-        const int SL_I = sl_i, SL_N = sl_n, R1W = r1w, R12 = r12, R24 = r24;
+        if (i > ibeg) {
+            mbar_wait(itbar, (i - ibeg - 1) & 1);
+            if (threadIdx.x == 0 && i - 1 + ST <= plast) {  // stage of plane i-1 is free
+                fence_proxy_async();
+                issue(i - 1 + ST);
+            }
+        }
+        const int SL_I = sl_i, SL_N = sl_n, R1W = r1w, R12 = r12, W2 = w2, R24 = (w2 + 2) % N2;
         // shift the queues: plane i+1 of W^s enters
         // Every queue entry is assigned unconditionally in every copy (values outside a level's
         // plane range are computed from stale data and never stored or consumed), so the
@@ -289,9 +310,10 @@ __global__ void __launch_bounds__(threads<R>(), 1)
                                                                       q12[r].x, xh, fq2[r].y, ws3[r].y, sc.dt2,
                                                                       sc.cos2);
                 q20[r] = mask(pin && yin[r], a, b);
-                *reinterpret_cast<double2 *>(l2buf + R12 * L2_EL + prow0 + r * LW - LW) = q20[r];
+                *reinterpret_cast<double2 *>(l2buf + W2 * L2_EL + prow0 + r * LW - LW) = q20[r];
             }
         }
+        arrive(itbar);  // this thread's level-1 (plane i) and level-2 (plane i-2) stores are done
 
         // ---- level 3 at plane i-4 (step s+2) on the tile, then the filter sum and the outputs
         const int p3 = i - 4;
@@ -364,17 +386,12 @@ __global__ void __launch_bounds__(threads<R>(), 1)
             }
         }
 
-        __syncthreads();  // level 1 (plane i) and level 2 (plane i-2) published; stage of plane i free
-        if (threadIdx.x == 0 && i + ST <= plast) {
-            fence_proxy_async();
-            issue(i + ST);
-        }
         sl_i = sl_n;
         sl_n = sl_n + 1 == ST ? 0 : sl_n + 1;
         ph_n ^= (sl_n == 0);
-        r1w = r12;  // (i+1) % 3 == ((i-2) % 3 + 0) ... rotate all three ring indices by one
-        r12 = r24;
-        r24 = R1W;
+        r1w = r12;  // (i+1) % 3 == (i-2) % 3
+        r12 = (r12 + 1) % 3;
+        w2 = w2 + 1 == N2 ? 0 : w2 + 1;
     }
     (void)any_ok;
     if (K2 == K_LAST && m.out_mode == WHB_OUT_FPI) {
