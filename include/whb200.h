@@ -37,7 +37,7 @@ extern "C" {
 #define WHB_ABI_VERSION 2
 
 /* Ghost planes allocated on each side of a context's owned axis-0 planes. */
-#define WHB_GHOST_PLANES 2
+#define WHB_GHOST_PLANES 3
 
 enum whb_status {
     WHB_OK = 0,
@@ -188,7 +188,12 @@ int whb_matvec(whb_ctx *ctx, int x, int y);
  * devices.  Step s of a solve advances W^s -> W^{s+1}.  A solve is
  *   whb_solve_begin; for s: whb_step(s, region); ...; whb_solve_end
  * or, with two leapfrog steps per HBM pass (whb_plan steps_per_pass == 2),
- *   whb_solve_begin; for s = 0, 2, ...: whb_pair(s, region); [whb_step(N-1, 0)]; whb_solve_end.
+ *   whb_solve_begin; for s = 0, 2, ...: whb_pair(s, region); [whb_step(N-1, 0)]; whb_solve_end,
+ * and with three (steps_per_pass == 3, n_total > 3; n_total <= 3 runs the two-step schedule)
+ *   whb_solve_begin; for s = 0, 3, ... while N - s >= 3: whb_triple(s, region);
+ *   [whb_pair(s, 0) if 2 steps remain | whb_step(s, 0) if 1]; whb_solve_end.
+ * Before a pass of k steps the ghosts hold k planes of W^s and k - 1 of W^{s-1}, so after a
+ * pass the exchange carries what the NEXT pass needs; F is read k - 1 planes deep.
  * whb_step: region 0 = all owned planes, 1 = the first and last owned update
  * planes only (the planes neighbours need), 2 = the remaining interior planes;
  * W^s needs 1 exchanged ghost plane per side.
@@ -204,6 +209,11 @@ int whb_matvec(whb_ctx *ctx, int x, int y);
 int whb_solve_begin(whb_ctx *ctx, int out_mode, int zero_forcing);
 int whb_step(whb_ctx *ctx, int s, int region);
 int whb_pair(whb_ctx *ctx, int s, int region);
+/* Three-step pass (s, s+1, s+2) of a context whose plan runs the three-step kernel (whb_plan:
+ * 3 steps per pass), with the same regions as whb_pair: 0 = every update plane, 1 = the three
+ * first and three last update planes (W^{s+3} there feeds the neighbours' 3 ghost planes, W^{s+2}
+ * their 2), 2 = the rest.  Not for a pass that is both the first and the last (N_t = 3). */
+int whb_triple(whb_ctx *ctx, int s, int region);
 int whb_solve_end(whb_ctx *ctx, double *resid_sq);
 int whb_ghost_planes(whb_ctx *ctx, int *ghost);
 int whb_level_plane_ptr(whb_ctx *ctx, int level, int64_t plane, uint64_t *dev_ptr, int64_t *plane_elems);

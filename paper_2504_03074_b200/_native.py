@@ -34,7 +34,7 @@ EXPORTS = (
     "whb_step", "whb_solve_end", "whb_level_plane_ptr", "whb_stream_ptr", "whb_synchronize",
     "whb_copy_plane", "whb_launch_count", "whb_set_timing", "whb_last_timing", "whb_host_alloc",
     "whb_host_free", "whb_geometry", "whb_set_l2_flush", "whb_apply_operator", "whb_plan", "whb_set_operator_general",
-    "whb_pair", "whb_ghost_planes", "whb_field_plane_ptr", "whb_copy_device",
+    "whb_pair", "whb_triple", "whb_ghost_planes", "whb_field_plane_ptr", "whb_copy_device",
     "whb_imp_apply", "whb_imp_rhs", "whb_vec_xpay", "whb_mg_setup", "whb_mg_vcycle", "whb_tri_setup", "whb_tri_solve",
     "whb_cg_begin", "whb_cg_iterate", "whb_vec_mgs",
     "whb_comm_begin", "whb_comm_end", "whb_comm_join", "whb_nccl_unique_id", "whb_nccl_init", "whb_nccl_exchange",
@@ -126,6 +126,7 @@ def load():
         "whb_plan": ([vp, ctypes.POINTER(c_int), ctypes.POINTER(c_int)], c_int),
         "whb_set_operator_general": ([vp, c_int, ctypes.POINTER(c_int), dp, c_double], c_int),
         "whb_pair": ([vp, c_int, c_int], c_int),
+        "whb_triple": ([vp, c_int, c_int], c_int),
         "whb_ghost_planes": ([vp, ctypes.POINTER(c_int)], c_int),
         "whb_field_plane_ptr": ([vp, c_int, c_int, c_i64, ctypes.POINTER(c_u64), ip64], c_int),
         "whb_copy_device": ([vp, c_u64, vp, c_u64, c_i64], c_int),
@@ -512,6 +513,9 @@ class Context:
 
     def pair(self, s, region=0):
         check(load().whb_pair(self._h, int(s), int(region)), "whb_pair")
+
+    def triple(self, s, region=0):
+        check(load().whb_triple(self._h, int(s), int(region)), "whb_triple")
 
     def ghost_planes(self) -> int:
         g = ctypes.c_int(0)

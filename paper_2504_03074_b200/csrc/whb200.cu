@@ -1257,7 +1257,7 @@ int plan_launch(whb_ctx *c) {
     // planes); small grids whose tiles cannot fill the GPU with chunks of >= 48 planes keep tb2
     const char *t3env = getenv("WHB_T3");
     c->t3 = false;
-    if (c->tb2 && whole && c->act1 && c->kern == 2 && c->nbatch == 1 && !(t3env && std::string(t3env) == "0")) {
+    if (c->tb2 && c->act1 && c->kern == 2 && c->nbatch == 1 && !(t3env && std::string(t3env) == "0")) {
         c->smem3 = t3::smem_bytes<S3_ST>();
         cudaError_t e = t3_set_attrs(c->smem3);
         if (e != cudaSuccess) return fail(WHB_E_CUDA, std::string("cudaFuncSetAttribute(t3): ") + cudaGetErrorString(e));
@@ -1585,7 +1585,8 @@ int launch_pair_range(whb_ctx *c, int s, int ib, int ie, int cl, int po) {
 int launch_pair(whb_ctx *c, int s) { return launch_pair_range(c, s, c->upd_lo, c->upd_hi, c->chunk2, 0); }
 
 // Steps (s, s+1, s+2) of the single member in one pass (step_t3.cuh); `last` when they end the solve.
-int launch_t3(whb_ctx *c, int s, bool last) {
+int launch_t3(whb_ctx *c, int s, bool last, int ib, int ie, int cl) {
+    if (ib >= ie) return 0;
     const bool zf = c->cur_zf != 0;
     const Member &m0 = c->h_members[0];
     const MemberHost &mh = c->mem[c->order[0]];
@@ -1607,11 +1608,12 @@ int launch_t3(whb_ctx *c, int s, bool last) {
     sc.c2 = mh.h_acc[s + 2];
     sc.c3 = mh.h_acc[s + 3];
     sc.osc = mh.out_scale;
-    dim3 grid(c->gx3, c->JT3 * c->nch3, 1);
+    const int nch = (ie - ib + cl - 1) / cl;
+    dim3 grid(c->gx3, c->JT3 * nch, 1);
     const int gm = geom_mode(c);
     auto go = [&](auto k1, auto k2, auto zft, auto gmt) {
         t3_fn<decltype(k1)::value, decltype(k2)::value, decltype(zft)::value, decltype(gmt)::value>()
-            <<<grid, S3_THREADS, c->smem3, c->stream>>>(c->geom, c->d_members, s, c->upd_lo, c->upd_hi, c->chunk3,
+            <<<grid, S3_THREADS, c->smem3, c->stream>>>(c->geom, c->d_members, s, ib, ie, cl,
                                                          c->JT3, sc, tw, tp, tf);
     };
     using KF = std::integral_constant<int, K_FIRST>;
@@ -1847,7 +1849,7 @@ int enqueue_solve(whb_ctx *c, int out_mode) {
         // passes of 3 steps; a remainder of 2 is one two-step pass, of 1 a single step
         int s = 0;
         while (ns - s >= 3) {
-            WHB_TRY(launch_t3(c, s, ns - s == 3));
+            WHB_TRY(launch_t3(c, s, ns - s == 3, c->upd_lo, c->upd_hi, c->chunk3));
             s += 3;
         }
         if (ns - s == 2) WHB_TRY(launch_pair(c, s));
@@ -2935,6 +2937,35 @@ int whb_pair(whb_ctx *c, int s, int region) {
             const int cl = std::min(n, c->chunk2);
             WHB_TRY(launch_pair_range(c, s, lo + 2, hi - 2, cl, 0));
         }
+    } else
+        return fail(WHB_E_ARG, "region must be 0, 1 or 2");
+    return 0;
+}
+
+int whb_triple(whb_ctx *c, int s, int region) {
+    if (!c || c->cur_mode < 0) return fail(WHB_E_STATE, "whb_triple outside whb_solve_begin/end");
+    if (!c->t3) return fail(WHB_E_STATE, "context has no three-step plan (whb_plan)");
+    const int N = c->mem[0].n_total;
+    if (s < 0 || s + 2 >= N) return fail(WHB_E_ARG, "steps (s, s+1, s+2) out of range");
+    if (s == 0 && N == 3) return fail(WHB_E_ARG, "a three-step pass may not be both the first and the last");
+    WHB_TRY(set_dev(c));
+    const int lo = c->upd_lo, hi = c->upd_hi;
+    const bool last = s + 3 == N;
+    if (region == 0) {
+        WHB_TRY(launch_t3(c, s, last, lo, hi, c->chunk3));
+        if (last) c->cur_parts = c->gx3 * c->JT3 * ((hi - lo + c->chunk3 - 1) / c->chunk3);
+    } else if (region == 1) {
+        if (last) return fail(WHB_E_ARG, "the last pass runs as region 0 (nothing needs its halo)");
+        // the three first and three last update planes: W^{s+3} there feeds the neighbours' 3 ghost planes
+        if (hi - lo <= 6) {
+            WHB_TRY(launch_t3(c, s, false, lo, hi, hi - lo));
+        } else {
+            WHB_TRY(launch_t3(c, s, false, lo, lo + 3, 3));
+            WHB_TRY(launch_t3(c, s, false, hi - 3, hi, 3));
+        }
+    } else if (region == 2) {
+        if (last) return fail(WHB_E_ARG, "the last pass runs as region 0 (nothing needs its halo)");
+        if (hi - lo > 6) WHB_TRY(launch_t3(c, s, false, lo + 3, hi - 3, std::min(hi - lo - 6, c->chunk3)));
     } else
         return fail(WHB_E_ARG, "region must be 0, 1 or 2");
     return 0;

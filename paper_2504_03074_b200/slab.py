@@ -3,21 +3,24 @@ GPUs — SURVEY §8(e).
 
 Each rank owns a contiguous range of axis-0 planes (``slab_ranges``) in one
 whb context (include/whb200.h: plane_begin/plane_end) whose allocation carries
-G = 2 ghost planes on each side.  The stencil radius is 1, so a single
-leapfrog step needs one ghost plane of W^s; the two-step pass the 2D/3D
-kernels run (temporal blocking, steps s and s+1 per HBM sweep) needs two
-planes of W^s and one of W^{s-1} and f.  Per pass (s, s+1):
+G = 3 ghost planes on each side.  The stencil radius is 1, so a single
+leapfrog step needs one ghost plane of W^s; a pass of k fused steps (temporal
+blocking: the two-step 2D/3D kernels, the three-step 3D kernel) needs k planes
+of W^s and k - 1 of W^{s-1} and f.  Per pass (s, ..., s+k-1):
 
-    1. compute the two first and two last owned update planes   (whb_pair region 1)
-    2. post the exchange of W^{s+2} (2 planes) and W^{s+1} (1 plane) per side
-    3. compute the remaining interior planes                     (whb_pair region 2)
-    4. join the exchange before the next pass                    (stream wait)
+    1. compute the k first and k last owned update planes     (region 1 of whb_step/pair/triple)
+    2. post the exchange of what the NEXT pass (k' steps) reads: k' planes of
+       W^{s+k} and k' - 1 of W^{s+k-1} per side                 (``halo_items``)
+    3. compute the remaining interior planes                   (region 2)
+    4. join the exchange before the next pass                  (stream wait)
 
-so the halo traffic, 3 x (n1 x n2 x 8 B) per side per TWO steps, overlaps the
-interior update; the one-step schedule (``whb_step`` regions, one plane of
-W^{s+1} per side per step) is used when the context plans one step per pass
-(general operator, 1D).  f is exchanged once (it is static).  Per FPI pass the
-residual sum of squares is all-reduced (one fp64).
+so the halo traffic, (2k - 1) x (n1 x n2 x 8 B) per side per k steps, overlaps
+the interior update.  ``pass_plan`` orders the passes like the whole-grid solve
+(three-step passes then a 2/1-step remainder; pairs then a single step; single
+steps for the general operator and 1D), with k agreed over all slabs
+(``agreed_pass_steps``: the smallest plan, capped by the smallest slab).  f is
+exchanged once (it is static).  Per FPI pass the residual sum of squares is
+all-reduced (one fp64).
 
 The exchange goes through ``torch.distributed`` (NCCL on GPUs, gloo on CPUs)
 on the context's own CUDA stream (``torch.cuda.ExternalStream``); device
@@ -39,7 +42,7 @@ from .filters import mode_name
 from .grid import operator_coefficients
 from .timestep import time_schedule
 
-__all__ = ["slab_ranges", "DeviceShard", "TorchHalo", "NcclHalo", "LocalHalo", "PeerHalo", "PeerSlabGraphs", "run_peer_local_solve", "SlabFPI", "SlabKrylov", "ShardedVectors",
+__all__ = ["slab_ranges", "pass_plan", "run_pass", "agreed_pass_steps", "DeviceShard", "TorchHalo", "NcclHalo", "LocalHalo", "PeerHalo", "PeerSlabGraphs", "run_peer_local_solve", "SlabFPI", "SlabKrylov", "ShardedVectors",
            "run_filtered_solve", "run_local_solve", "halo_items", "exchange_forcing"]
 
 
@@ -82,11 +85,64 @@ def halo_planes(shard, side: str, depth: int):
     return g + n - depth, g + n
 
 
-def halo_items(s: int, two_step: bool):
-    """What the next step/pass needs from the neighbours after step s (one-step) or pass (s, s+1)."""
-    if two_step:
-        return [(level(s + 2), 2), (level(s + 1), 1)]
-    return [(level(s + 1), 1)]
+def pass_plan(n_total: int, steps_per_pass: int):
+    """The passes [(s, k), ...] of a solve, k leapfrog steps each, in the order the whole-grid
+    solve runs them (whb200.cu enqueue_solve): with 3 steps per pass (and n_total > 3) three-step
+    passes while >= 3 steps remain, then one pass of the remaining 2 or 1; with 2, passes
+    (0, 1), (2, 3), ... and a last single step when n_total is odd; else single steps."""
+    if steps_per_pass >= 3 and n_total > 3:
+        out, s = [], 0
+        while n_total - s >= 3:
+            out.append((s, 3))
+            s += 3
+        if s < n_total:
+            out.append((s, n_total - s))
+        return out
+    if steps_per_pass >= 2:
+        return [(s, min(2, n_total - s)) for s in range(0, n_total, 2)]
+    return [(s, 1) for s in range(n_total)]
+
+
+def halo_items(s: int, k: int, k_next: int):
+    """What a pass of k_next steps needs from the neighbours after the pass (s, k): k_next ghost
+    planes of W^{s+k} and k_next - 1 of W^{s+k-1} per side (the pass reads W^{s-1} one plane less
+    deep than W^s)."""
+    e = s + k
+    items = [(level(e), k_next)]
+    if k_next > 1:
+        items.append((level(e - 1), k_next - 1))
+    return items
+
+
+def run_pass(shard, s: int, k: int, region: int):
+    """Region 0/1/2 of the k-step pass starting at step s (whb_step / whb_pair / whb_triple)."""
+    (shard.step, shard.pair, shard.triple)[k - 1](s, region)
+
+
+def agreed_pass_steps(shards, halo=None) -> int:
+    """Steps per pass every slab of the decomposition runs: the smallest plan (whb_plan: 1, 2
+    or 3) over the slabs, capped by the smallest slab (a pass of k steps takes k ghost planes
+    from ONE neighbour).  Across processes this is an all-reduce (MIN) over the halo's process
+    group, done once per shard and cached (every rank reaches it in the same solve)."""
+    k = min(min(sh.steps_per_pass, sh.nloc) for sh in shards)
+    dist = getattr(halo, "dist", None)
+    if dist is not None and halo is not None and halo.nranks > 1:
+        import torch
+
+        dev = "cpu" if dist.get_backend() == "gloo" else f"cuda:{shards[0].device}"
+        t = torch.tensor([k], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        k = int(t.item())
+    return max(1, k)
+
+
+def _pass_steps(shards, halo):
+    k = getattr(shards[0], "pass_steps", None)
+    if k is None:
+        k = agreed_pass_steps(shards, halo)
+        for sh in shards:
+            sh.pass_steps = k
+    return k
 
 
 class DeviceShard:
@@ -126,6 +182,9 @@ class DeviceShard:
 
     def pair(self, s, region):
         self.ctx.pair(s, region)
+
+    def triple(self, s, region):
+        self.ctx.triple(s, region)
 
     def solve_end(self) -> float:
         return self.ctx.solve_end()
@@ -229,6 +288,7 @@ class NcclHalo:
 
     def __init__(self, shard, dist, rank: int, world: int):
         self.shard, self.rank, self.world = shard, rank, world
+        self.dist = dist
         uid = [_native.nccl_unique_id() if rank == 0 else None]
         if world > 1:
             dist.broadcast_object_list(uid, src=0)
@@ -435,8 +495,7 @@ def run_peer_local_solve(shards, halos, out_mode=_native.OUT_FPI, zero_forcing=F
     slab always follow the neighbour's enqueued flag writes).  Returns the residual sums."""
     for sh in shards:
         sh.solve_begin(out_mode, zero_forcing)
-    n_total = shards[0].n_total
-    two = all(sh.steps_per_pass == 2 for sh in shards)
+    plan = pass_plan(shards[0].n_total, _pass_steps(shards, None))
 
     def exchange_both(items, between=None):
         hs = [h.start(sh, items) for sh, h in zip(shards, halos)]
@@ -445,31 +504,15 @@ def run_peer_local_solve(shards, halos, out_mode=_native.OUT_FPI, zero_forcing=F
         for h, q in zip(halos, hs):
             h.finish(q)
 
-    if two:
-        exchange_both([(level(0), 2)])
-        s = 0
-        while s + 1 < n_total:
-            if s + 2 == n_total:
-                for sh in shards:
-                    sh.pair(s, 0)
-            else:
-                for sh in shards:
-                    sh.pair(s, 1)
-                exchange_both(halo_items(s, True), lambda: [sh.pair(s, 2) for sh in shards])
-            s += 2
-        if s < n_total:
+    exchange_both([(level(0), plan[0][1])])  # W^0 = v, as deep as the first pass reads it
+    for n, (s, k) in enumerate(plan):
+        if n + 1 == len(plan):
             for sh in shards:
-                sh.step(s, 0)
-        return [sh.solve_end() for sh in shards]
-    exchange_both([(level(0), 1)])
-    for s in range(n_total):
-        if s == n_total - 1:
-            for sh in shards:
-                sh.step(s, 0)
+                run_pass(sh, s, k, 0)
             continue
         for sh in shards:
-            sh.step(s, 1)
-        exchange_both(halo_items(s, False), lambda: [sh.step(s, 2) for sh in shards])
+            run_pass(sh, s, k, 1)
+        exchange_both(halo_items(s, k, plan[n + 1][1]), lambda: [run_pass(sh, s, k, 2) for sh in shards])
     return [sh.solve_end() for sh in shards]
 
 
@@ -514,87 +557,60 @@ def _exchange_now(halo, shard, items):
 
 
 def run_filtered_solve(shard, halo, out_mode=_native.OUT_FPI, zero_forcing=False) -> float:
-    """One W(v, f) pass of a slab with halo exchange (the schedules above).
-    Returns this rank's residual sum of squares (FPI mode)."""
+    """One W(v, f) pass of a slab with halo exchange (the schedule in the module docstring, with
+    ``pass_plan``'s passes).  Returns this rank's residual sum of squares (FPI mode)."""
     shard.solve_begin(out_mode, zero_forcing)
     multi = halo.nranks > 1
-    n_total = shard.n_total
-    if shard.steps_per_pass == 2:
-        _exchange_now(halo, shard, [(level(0), 2)])  # two ghost planes of W^0 = v
-        s = 0
-        while s + 1 < n_total:
-            if not multi or s + 2 == n_total:
-                shard.pair(s, 0)  # the last pass writes the output; no later step needs its halo
-            else:
-                shard.pair(s, 1)
-                h = halo.start(shard, halo_items(s, True))
-                shard.pair(s, 2)
-                halo.finish(h)
-            s += 2
-        if s < n_total:  # odd step count: the last step alone (its W^s ghosts came with the last pass)
-            shard.step(s, 0)
-        return shard.solve_end()
-    _exchange_now(halo, shard, [(level(0), 1)])  # ghost plane of W^0 = v
-    for s in range(n_total):
-        if not multi or s == n_total - 1:
-            shard.step(s, 0)
+    plan = pass_plan(shard.n_total, _pass_steps([shard], halo))
+    _exchange_now(halo, shard, [(level(0), plan[0][1])])  # W^0 = v, as deep as the first pass reads it
+    for n, (s, k) in enumerate(plan):
+        if not multi or n + 1 == len(plan):
+            run_pass(shard, s, k, 0)  # the last pass writes the output; no later step needs its halo
             continue
-        shard.step(s, 1)
-        h = halo.start(shard, halo_items(s, False))
-        shard.step(s, 2)
+        run_pass(shard, s, k, 1)
+        h = halo.start(shard, halo_items(s, k, plan[n + 1][1]))
+        run_pass(shard, s, k, 2)
         halo.finish(h)
     return shard.solve_end()
 
 
 def run_local_solve(shards, halo: LocalHalo, out_mode=_native.OUT_FPI, zero_forcing=False):
-    """The same schedules for in-process slabs (each step/pass: boundary planes of every
-    slab, plane copies, interior planes)."""
+    """The same schedule for in-process slabs (each pass: boundary planes of every slab, plane
+    copies, interior planes)."""
     for sh in shards:
         sh.solve_begin(out_mode, zero_forcing)
-    n_total = shards[0].n_total
-    two = all(sh.steps_per_pass == 2 for sh in shards)
-    if two:
-        halo.exchange([(level(0), 2)])
-        s = 0
-        while s + 1 < n_total:
-            if s + 2 == n_total:
-                for sh in shards:
-                    sh.pair(s, 0)
-            else:
-                for sh in shards:
-                    sh.pair(s, 1)
-                halo.exchange(halo_items(s, True))
-                for sh in shards:
-                    sh.pair(s, 2)
-            s += 2
-        if s < n_total:
+    plan = pass_plan(shards[0].n_total, _pass_steps(shards, None))
+    halo.exchange([(level(0), plan[0][1])])
+    for n, (s, k) in enumerate(plan):
+        if n + 1 == len(plan):
             for sh in shards:
-                sh.step(s, 0)
-        return [sh.solve_end() for sh in shards]
-    halo.exchange([(level(0), 1)])
-    for s in range(n_total):
-        if s == n_total - 1:
-            for sh in shards:
-                sh.step(s, 0)
+                run_pass(sh, s, k, 0)
             continue
         for sh in shards:
-            sh.step(s, 1)
-        halo.exchange(halo_items(s, False))
+            run_pass(sh, s, k, 1)
+        halo.exchange(halo_items(s, k, plan[n + 1][1]))
         for sh in shards:
-            sh.step(s, 2)
+            run_pass(sh, s, k, 2)
     return [sh.solve_end() for sh in shards]
 
 
+def forcing_depth(shards, halo=None) -> int:
+    """Ghost planes of f a k-step pass reads: k - 1 (at least 1), k agreed over the slabs."""
+    return max(1, _pass_steps(list(shards), halo) - 1)
+
+
 def exchange_forcing(shards_or_shard, halo):
-    """f is read one plane beyond the owned range by the two-step pass: exchange it once."""
+    """f is read k - 1 planes beyond the owned range by a k-step pass: exchange it once (f is
+    static)."""
     if isinstance(halo, LocalHalo):
-        halo.exchange([(field(_native.F), 1)])
+        halo.exchange([(field(_native.F), forcing_depth(halo.shards))])
     elif isinstance(halo, (list, tuple)):  # PeerHalo.local_group
-        hs = [h.start(sh, [(field(_native.F), 1)]) for sh, h in zip(shards_or_shard, halo)]
+        items = [(field(_native.F), forcing_depth(shards_or_shard))]
+        hs = [h.start(sh, items) for sh, h in zip(shards_or_shard, halo)]
         for h, q in zip(halo, hs):
             h.finish(q)
     else:
-        _exchange_now(halo, shards_or_shard, [(field(_native.F), 1)])
+        _exchange_now(halo, shards_or_shard, [(field(_native.F), forcing_depth([shards_or_shard], halo))])
 
 
 class ShardedVectors:

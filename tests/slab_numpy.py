@@ -12,13 +12,13 @@ from paper_2504_03074_b200.grid import operator_coefficients
 
 
 class NumpyShard:
-    """Test double with DeviceShard's interface: the same plane layout (G = 2
-    ghost planes per side, time level L >= 1 in ring slot L mod 4) and the
-    same one-step / two-step region semantics as the device contexts
-    (include/whb200.h whb_step / whb_pair); arithmetic in reference order
-    (the restatement of oracle/waveholtz_oracle.py, per plane)."""
+    """Test double with DeviceShard's interface: the same plane layout (G = 3
+    ghost planes per side, time level L in buffer L mod 6) and the same
+    one-/two-/three-step region semantics as the device contexts
+    (include/whb200.h whb_step / whb_pair / whb_triple); arithmetic in
+    reference order (the restatement of oracle/waveholtz_oracle.py, per plane)."""
 
-    gh = 2
+    gh = 3
 
     def __init__(self, grid, plane_range, c=1.0, steps_per_pass=2):
         self.grid = grid
@@ -27,7 +27,7 @@ class NumpyShard:
         self.steps_per_pass = steps_per_pass
         self.clo, self.cmid, self.c2 = operator_coefficients(grid, 2, c)
         shp = (self.nloc + 2 * self.gh,) + tuple(grid.shape[1:])
-        self.buf = {k: np.zeros(shp) for k in ("v", "f", "acc", "out", 0, 1, 2, 3)}
+        self.buf = {k: np.zeros(shp) for k in ("v", "f", "acc", "out", 0, 1, 2, 3, 4, 5)}
         self.ctx = NumpyVecs(self)
         self.zf = False
         self.device = 0
@@ -64,7 +64,7 @@ class NumpyShard:
         self.buf[self._field(field)][...] = 0.0
 
     def level(self, L):
-        return self.buf["v"] if L == 0 else self.buf[L % 4]
+        return self.buf["v"] if L == 0 else self.buf[L % 6]
 
     def solve_begin(self, out_mode, zero_forcing=False):
         self.mode = out_mode
@@ -163,6 +163,40 @@ class NumpyShard:
                 self._pair_range(s, hi - 2, hi)
         elif hi - lo > 4:
             self._pair_range(s, lo + 2, hi - 2)
+
+    def _triple_range(self, s, a, b):
+        """steps s, s+1, s+2 on update planes [a, b): W^{s+1} on [a-2, b+2) and W^{s+2} on
+        [a-1, b+1) (zero outside the global interior, kept aside), then W^{s+3} on [a, b); W^{s+2}
+        and W^{s+3} of [a, b) are stored (what the next pass reads) — one chunk of the device pass"""
+        w, wp = self.level(s), self.level(s - 1)
+        inner = self._inner()
+        w1, w2 = np.zeros_like(w), np.zeros_like(w)
+        for i in range(a - 2, b + 2):
+            if self.i_lo <= i < self.i_hi:
+                w1[i][inner] = self._advance(s, w, wp, i)
+        for i in range(a - 1, b + 1):
+            if self.i_lo <= i < self.i_hi:
+                w2[i][inner] = self._advance(s + 1, w1, w, i)
+        for i in range(a, b):
+            self._finish(s, i, w, w1[i][inner])
+            self._finish(s + 1, i, w1, w2[i][inner])
+            self.level(s + 2)[i][inner] = w2[i][inner]
+            new = self._advance(s + 2, w2, w1, i)
+            if self._finish(s + 2, i, w2, new):
+                self.level(s + 3)[i][inner] = new
+
+    def triple(self, s, region):
+        lo, hi = self.lo, self.hi
+        if region == 0:
+            self._triple_range(s, lo, hi)
+        elif region == 1:
+            if hi - lo <= 6:
+                self._triple_range(s, lo, hi)
+            else:
+                self._triple_range(s, lo, lo + 3)
+                self._triple_range(s, hi - 3, hi)
+        elif hi - lo > 6:
+            self._triple_range(s, lo + 3, hi - 3)
 
     def solve_end(self):
         return self.rs

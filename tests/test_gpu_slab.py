@@ -55,6 +55,46 @@ def test_local_slabs_match_single_domain_bitwise(gpu_available, monkeypatch, cel
     np.testing.assert_allclose(np.sqrt(sums) / np.sqrt(g.size), rref, rtol=1e-12)
 
 
+@pytest.mark.parametrize("cells,nslabs,omega,chunk3,k", [((32, 19, 23), 3, 9.0, 0, 3), ((24, 20, 36), 3, 7.0, 0, 3),
+                                                        ((64, 64, 64), 2, 20.0, 9, 3), ((40, 70, 61), 4, 8.0, 4, 3),
+                                                        ((8, 12, 10), 4, 5.0, 0, 2), ((30, 13, 17), 1, 6.25, 7, 3)])
+def test_local_slabs_three_step_bitwise(gpu_available, monkeypatch, cells, nslabs, omega, chunk3, k):
+    """The three-step kernel on slabs (whb_triple regions, 3-plane halos of W^{s+3} + 2 of
+    W^{s+2}, f exchanged 2 deep; 2- or 1-step remainder pass) equals the single-domain iterates.
+    WHB_T3=1 forces the plan on grids this small; chunk3 > 0 splits region 2 into axis-0 chunks.
+    (8, 12, 10) over 4 slabs leaves slabs of 2 planes: the slabs agree on two-step passes."""
+    monkeypatch.setenv("WHB_T3", "1")
+    if chunk3:
+        monkeypatch.setenv("WHB_CHUNK3", str(chunk3))
+    d = len(cells)
+    g = wh.build_grid(d, [(0.0, 1.0)] * d, cells, "dirichlet")
+    f = O.multi_gaussian(g.shape, g.bounds, g.spacing, 3, seed=2)
+    corr = wh.correct_explicit(omega, g, 2, 1.0)
+    cfg = wh.FilterConfig(omega=omega, periods=1, steps_per_period=corr.steps_per_period, mode="explicit")
+    shards, halo = _shards(g, f, wh.time_schedule(corr, cfg), nslabs)
+    assert all(sh.steps_per_pass == 3 for sh in shards)
+    assert all(sh.pass_steps == k for sh in shards)
+    iters = 3
+    sums = [sum(run_local_solve(shards, halo)) for _ in range(iters)]
+    for sh in shards:
+        sh.synchronize()
+    v = np.concatenate([sh.download(_native.V) for sh in shards], axis=0)
+    sc = O.step_scalars(corr.steps_per_period, corr.dt, corr.omega_tilde)
+    vref, rref = ON.fpi(f, g.spacing, sc, iters)
+    assert np.array_equal(v, vref), (corr.steps_per_period, k)
+    np.testing.assert_allclose(np.sqrt(sums) / np.sqrt(g.size), rref, rtol=1e-12)
+    # PLAIN and AV outputs through the same three-step slab schedule
+    v0 = O.zero_dirichlet(np.random.default_rng(3).standard_normal(g.shape) * 1e-2, ["dirichlet"] * d)
+    for sh, (p0, p1) in zip(shards, slab_ranges(g.shape[0], nslabs)):
+        sh.upload(_native.V, np.ascontiguousarray(v0[p0:p1]))
+    run_local_solve(shards, halo, _native.OUT_PLAIN)
+    w = np.concatenate([sh.download(_native.OUT) for sh in shards], axis=0)
+    assert np.array_equal(w, ON.wave_solve(v0, f, g.spacing, sc))
+    run_local_solve(shards, halo, _native.OUT_AV, zero_forcing=True)
+    av = np.concatenate([sh.download(_native.OUT) for sh in shards], axis=0)
+    assert np.array_equal(av, v0 - ON.wave_solve(v0, f, g.spacing, sc, zero_f=True))
+
+
 @pytest.mark.parametrize("cells,nslabs,omega", [((50, 41), 3, 11.0), ((20, 18, 22), 2, 7.5)])
 def test_local_slabs_plain_and_matvec_modes(gpu_available, cells, nslabs, omega):
     """PLAIN (W(v, f)) and AV (v - W(v, 0)) outputs of a slab-decomposed two-step solve"""

@@ -88,13 +88,14 @@ class PeerNumpyShard(NumpyShard):
 
     def plane_ptr(self, item, plane):
         kind, ident = item
-        key = ("v" if ident == 0 else ident % 4) if kind == "level" else self._field(ident)
+        key = ("v" if ident == 0 else ident % 6) if kind == "level" else self._field(ident)
         return self.base[key] + plane * self.plane_bytes, self.plane_bytes // 8
 
 
 @pytest.mark.parametrize("use_comm", [False, True])
 @pytest.mark.parametrize("dim,cells,omega,spp,world", [(2, (40, 24), 12.0, 2, 2), (3, (14, 10, 12), 6.5, 2, 3),
-                                                       (2, (9, 30), 8.0, 2, 3), (2, (40, 24), 12.0, 1, 3)])
+                                                       (2, (9, 30), 8.0, 2, 3), (2, (40, 24), 12.0, 1, 3),
+                                                       (3, (20, 10, 12), 7.0, 3, 3), (2, (9, 30), 8.0, 3, 3)])
 def test_peer_halo_lockstep_matches_single_domain(dim, cells, omega, spp, world, use_comm):
     """use_comm: the exchange-stream protocol of the one-process-per-GPU halos (begin / end around
     each exchange, join before the next begins) is followed on every exchange."""

@@ -40,7 +40,7 @@ def _worker(rank, world, port, dim, cells, omega, iters, q, spp):
         corr = correct_explicit(omega, g, 2, 1.0)
         cfg = FilterConfig(omega=omega, periods=1, steps_per_period=corr.steps_per_period, mode="explicit")
         rng = slab_ranges(g.shape[0], world)[rank]
-        shard = NumpyShard(g, rng, steps_per_pass=spp)
+        shard = NumpyShard(g, rng, steps_per_pass=spp[rank] if isinstance(spp, tuple) else spp)
         solver = SlabFPI(shard, TorchHalo(dist, rank, world), corr, cfg, f)
         res = [solver.iterate() for _ in range(iters)]
         q.put((rank, rng, solver.local_iterate(), res))
@@ -50,10 +50,14 @@ def _worker(rank, world, port, dim, cells, omega, iters, q, spp):
 
 @pytest.mark.parametrize("dim,cells,omega,spp,world", [(2, (40, 24), 12.0, 1, 2), (3, (14, 10, 12), 6.5, 1, 2),
                                                        (2, (40, 24), 12.0, 2, 2), (3, (14, 10, 12), 6.5, 2, 2),
-                                                       (3, (14, 10, 12), 6.5, 2, 3), (2, (9, 30), 8.0, 2, 3)])
+                                                       (3, (14, 10, 12), 6.5, 2, 3), (2, (9, 30), 8.0, 2, 3),
+                                                       (3, (20, 10, 12), 6.5, 3, 2), (3, (20, 10, 12), 7.0, 3, 3), (3, (20, 10, 12), 6.75, 3, 2),
+                                                       (2, (9, 30), 8.0, 3, 3), (3, (20, 10, 12), 6.5, (3, 2, 3), 3)])
 def test_slab_fpi_gloo_matches_single_domain(dim, cells, omega, spp, world):
     """world 2 and 3 (a middle slab exchanges both sides; (9, 30) over 3 ranks leaves
-    slabs of 3 and 4 planes, so the two-step boundary regions cover whole slabs)"""
+    slabs of 3 and 4 planes, so the two-/three-step boundary regions cover whole slabs).
+    spp 3: three-step passes with a 2- or 1-step remainder; (3, 2, 3): ranks whose plans
+    differ agree on the smallest (all-reduce MIN) and run two-step passes."""
     iters = 3
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -76,6 +80,22 @@ def test_slab_fpi_gloo_matches_single_domain(dim, cells, omega, spp, world):
     assert np.array_equal(v, vref)
     np.testing.assert_allclose(got[0][3], rref, rtol=1e-12)
     assert all(t[3] == got[0][3] for t in got)
+
+
+@pytest.mark.parametrize("n_total,spp,plan", [
+    (10, 3, [(0, 3), (3, 3), (6, 3), (9, 1)]), (11, 3, [(0, 3), (3, 3), (6, 3), (9, 2)]),
+    (9, 3, [(0, 3), (3, 3), (6, 3)]), (3, 3, [(0, 2), (2, 1)]), (2, 3, [(0, 2)]),
+    (5, 2, [(0, 2), (2, 2), (4, 1)]), (4, 2, [(0, 2), (2, 2)]), (3, 1, [(0, 1), (1, 1), (2, 1)])])
+def test_pass_plan_matches_whole_grid_order(n_total, spp, plan):
+    """slab.pass_plan orders passes like whb200.cu enqueue_solve (a three-step pass is never both
+    the first and the last: n_total <= 3 runs the two-step schedule)."""
+    from paper_2504_03074_b200.slab import halo_items, level, pass_plan
+
+    assert pass_plan(n_total, spp) == plan
+    assert sum(k for _, k in plan) == n_total
+    assert halo_items(0, 3, 3) == [(level(3), 3), (level(2), 2)]
+    assert halo_items(3, 3, 1) == [(level(6), 1)]
+    assert halo_items(0, 2, 2) == [(level(2), 2), (level(1), 1)]
 
 
 def test_slab_ranges():
