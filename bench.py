@@ -538,7 +538,8 @@ def run_slab(args, dist, ws, rank, local):
                "api": "slab.SlabFPI with per-rank whb_upload / whb_download of the owned planes (pinned)"}
         host.free()
     if rank == 0:
-        own_bpu = 56.0 / shard.steps_per_pass if shard.steps_per_pass > 1 else float(BYTES_PER_UPDATE)
+        kp = getattr(shard, "pass_steps", None) or shard.steps_per_pass  # steps per pass all slabs agreed on
+        own_bpu = 56.0 / kp if kp > 1 else float(BYTES_PER_UPDATE)
         per_gpu = units / ws / dev_s
         line = {
             "metric": METRIC, "value": value, "unit": "Gpts/s", "n_gpus": ws, "steps": K, "warmup": W,
@@ -549,7 +550,7 @@ def run_slab(args, dist, ws, rank, local):
             "iters_per_s": K / dev_s,
             "roofline": {"bound": "hbm", "achieved": own_bpu * per_gpu / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": own_bpu * per_gpu / 1e9 / peak, "traffic": None, "peak_source": peak_src,
-                         "bytes_per_update": own_bpu,
+                         "bytes_per_update": own_bpu, "steps_per_pass": kp,
                          "frac_48B": BYTES_PER_UPDATE * per_gpu / 1e9 / peak,
                          "frac_source": "compulsory bytes of the slab's multi-step passes per GPU / device wall "
                                         "time of the timed iterations (exchange and region split included)"},

@@ -99,7 +99,7 @@ def main():
             sh.synchronize()
         dt = time.perf_counter() - t0
         launches = sum(sh.ctx.launch_count() for sh in shards) - l0
-        row = {"slabs": k, "halo": a.halo + ("+graph" if a.graph else ""), "two_step": shards[0].steps_per_pass == 2, "gpts": g.size * n_t * a.iters / dt / 1e9,
+        row = {"slabs": k, "halo": a.halo + ("+graph" if a.graph else ""), "steps_per_pass": shards[0].pass_steps, "gpts": g.size * n_t * a.iters / dt / 1e9,
                "launches_per_iter": launches / a.iters, "resid_sq_last": sums[-1]}
         if not a.no_whole:
             v = np.concatenate([sh.download(_native.V) for sh in shards], axis=0)
