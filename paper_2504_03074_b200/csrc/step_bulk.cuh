@@ -88,10 +88,15 @@ template <int KIND, bool ZF, bool A1, bool SQ = false, int C2 = -1>
 __device__ __forceinline__ double update_point(const Geom &g, double wm, double wc, double wp, double yl,
                                                double yh, double xl, double xh, double fv, double wpv,
                                                double h, double cosn) {
-    double lap = 0.0;
+    // The reference sums into np.zeros (0.0 + first product); that add only turns a -0.0 first
+    // product into +0.0, and it is dropped here because the returned update cannot see it: the
+    // sums differ only when EVERY product is -0.0, which includes cmid*wc (cmid < 0), so wc == +0.0;
+    // then 2*wc - wpv (or wc itself on the first step) is +0.0 or nonzero, never -0.0, and adding
+    // h*d = +-0.0 to it gives the same bits either way.
+    double lap;
     if constexpr (SQ) {
         const double mc = whb_mul(g.cmid0, wc);
-        lap = whb_add(lap, whb_mul(g.clo0, wm));
+        lap = whb_mul(g.clo0, wm);
         lap = whb_add(lap, mc);
         lap = whb_add(lap, whb_mul(g.clo0, wp));
         if (A1) {
@@ -103,7 +108,7 @@ __device__ __forceinline__ double update_point(const Geom &g, double wm, double 
         lap = whb_add(lap, mc);
         lap = whb_add(lap, whb_mul(g.clo0, xh));
     } else {
-        lap = whb_add(lap, whb_mul(g.clo0, wm));
+        lap = whb_mul(g.clo0, wm);
         lap = whb_add(lap, whb_mul(g.cmid0, wc));
         lap = whb_add(lap, whb_mul(g.clo0, wp));
         if (A1) {

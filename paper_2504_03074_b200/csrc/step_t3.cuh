@@ -32,6 +32,13 @@
 // (short-scoreboard stalls 24 % of samples vs barrier 19 %).
 #pragma once
 
+#include <type_traits>
+
+// 1: the three level updates of an iteration interleaved (default); 0: one level after the other
+#ifndef WHB_T3_ILP
+#define WHB_T3_ILP 1
+#endif
+
 namespace t3 {
 
 __device__ __forceinline__ void prefetch_l2(const void *p) {
@@ -147,7 +154,7 @@ __global__ void __launch_bounds__(threads<R>(), 1)
     const bool xin0 = (x >= 1) && (x < g.n2 - 1);
     const bool xin1 = (x + 1 >= 1) && (x + 1 < g.n2 - 1);
     const int rho0 = w * R;
-    bool yin[R], ok0[R], ok1[R];
+    bool yin[R], ok0[R], ok1[R], yx0[R], yx1[R];
     long long pbase[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -156,6 +163,8 @@ __global__ void __launch_bounds__(threads<R>(), 1)
         const bool own = (rho0 + r >= 2) && (rho0 + r <= NR - 3) && lane >= 1 && lane <= 30;
         ok0[r] = own && yin[r] && xin0;
         ok1[r] = own && yin[r] && xin1;
+        yx0[r] = yin[r] && xin0;  // level value kept (not a Dirichlet / out-of-domain point)
+        yx1[r] = yin[r] && xin1;
         pbase[r] = (long long)y * P + x;
     }
     bool any_ok = false;
@@ -226,6 +235,195 @@ __global__ void __launch_bounds__(threads<R>(), 1)
 
     const int ibeg = i0 - 2;  // iteration i: level 1 at i, level 2 at i-2, level 3 at i-4
     const int iend = i1 + 3;
+#if WHB_T3_ILP
+    // Plane loop with the three level updates interleaved: every shared-memory operand of the
+    // iteration (all written by earlier iterations) is loaded first, then the 3 x 2 x R update
+    // chains are formed in one block (no memory operation between them, so the compiler
+    // interleaves them: 6 independent fp64 chains per thread at R = 1 instead of 2), then levels 1
+    // and 2 are published and the split barrier is arrived on, then the level-3 outputs.  The loop
+    // is instantiated per warp role (warp-uniform): level 1 only (the outer two level-1 rows), levels
+    // 1-2 (the next two), all three levels.
+    auto run = [&](auto d2c, auto d3c) {
+        constexpr bool D2 = decltype(d2c)::value;
+        constexpr bool D3 = decltype(d3c)::value;
+        int sl_i = 1 % ST, sl_n = 2 % ST, ph_n = 0;
+        int r1w = 0, r12 = 1;
+        int w2 = N2 - 2;
+        for (int i = ibeg; i <= iend; ++i) {
+            if (i > ibeg) {
+                mbar_wait(itbar, (i - ibeg - 1) & 1);
+                if (threadIdx.x == 0 && i - 1 + ST <= plast) {
+                    fence_proxy_async();
+                    issue(i - 1 + ST);
+                }
+            }
+            const int SL_I = sl_i, SL_N = sl_n, R1W = r1w, R12 = r12, W2 = w2, R24 = (w2 + 2) % N2;
+            if (i + 1 <= plast) mbar_wait(bars + SL_N, ph_n);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                ws5[r] = ws4[r]; ws4[r] = ws3[r]; ws3[r] = ws2[r]; ws2[r] = ws1[r]; ws1[r] = ws0[r];
+                ws0[r] = lds2(smem + SL_N * STAGE + wrow0 + r * RW);
+                q14[r] = q13[r]; q13[r] = q12[r]; q12[r] = q11[r]; q11[r] = q10[r];
+                q23[r] = q22[r]; q22[r] = q21[r]; q21[r] = q20[r];
+                fq4[r] = fq3[r]; fq3[r] = fq2[r]; fq2[r] = fq1[r]; fq1[r] = fq0[r];
+            }
+            // ---- operands: level 1 (W^s stage of plane i), level 2 (level-1 ring, plane i-2),
+            //      level 3 (level-2 ring, plane i-4); x neighbours of levels 2 / 3 by shuffles
+            const double *st = smem + SL_I * STAGE;
+            const double2 y1lo = lds2(st + wrow0 - RW);
+            const double2 y1hi = lds2(st + wrow0 + R * RW);
+            double x1l[R], x1h[R];
+            double2 pv[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int wrow = wrow0 + r * RW;
+                x1l[r] = st[wrow - 1];
+                x1h[r] = st[wrow + 2];
+                const int prow = prow0 + r * LW;
+                pv[r] = LOAD_P ? lds2(st + W_EL + prow) : z2;
+                if (!ZF) fq0[r] = lds2(st + W_EL + P_EL + prow);
+            }
+            double2 y2lo = z2, y2hi = z2, y3lo = z2, y3hi = z2;
+            double x2l[R], x2h[R], x3l[R], x3h[R];
+            if (D2) {
+                const double *l1 = l1buf + R12 * L1_EL;
+                y2lo = lds2(l1 + (row2(0) ? prow0 - LW : prow0));
+                y2hi = lds2(l1 + (row2(R - 1) ? prow0 + R * LW : prow0));
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    x2l[r] = shl(q12[r].y);
+                    x2h[r] = shr(q12[r].x);
+                }
+            }
+            if (D3) {
+                const double *l2 = l2buf + R24 * L2_EL;
+                y3lo = lds2(l2 + (row3(0) ? prow0 - 2 * LW : 2 * lane));
+                y3hi = lds2(l2 + (row3(R - 1) ? prow0 + (R - 1) * LW : 2 * lane));
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    x3l[r] = shl(q22[r].y);
+                    x3h[r] = shr(q22[r].x);
+                }
+            }
+            // ---- the three level updates (independent chains)
+            double a1[R], b1[R], a2[R], b2[R], a3[R], b3[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const double2 yl = r == 0 ? y1lo : ws1[r - 1];
+                const double2 yh = r == R - 1 ? y1hi : ws1[r + 1];
+                a1[r] = update_point<K1, ZF, true, SQ, C2M>(g, ws2[r].x, ws1[r].x, ws0[r].x, yl.x, yh.x, x1l[r],
+                                                         ws1[r].y, fq0[r].x, pv[r].x, sc.h1, sc.cos1);
+                b1[r] = update_point<K1, ZF, true, SQ, C2M>(g, ws2[r].y, ws1[r].y, ws0[r].y, yl.y, yh.y, ws1[r].x,
+                                                         x1h[r], fq0[r].y, pv[r].y, sc.h1, sc.cos1);
+                if (D2) {
+                    const double2 yl2 = r == 0 ? y2lo : q12[r - 1];
+                    const double2 yh2 = r == R - 1 ? y2hi : q12[r + 1];
+                    a2[r] = update_point<K_MID, ZF, true, SQ, C2M>(g, q13[r].x, q12[r].x, q11[r].x, yl2.x, yh2.x,
+                                                                x2l[r], q12[r].y, fq2[r].x, ws3[r].x, sc.dt2, sc.cos2);
+                    b2[r] = update_point<K_MID, ZF, true, SQ, C2M>(g, q13[r].y, q12[r].y, q11[r].y, yl2.y, yh2.y,
+                                                                q12[r].x, x2h[r], fq2[r].y, ws3[r].y, sc.dt2, sc.cos2);
+                }
+                if (D3) {
+                    const double2 yl3 = r == 0 ? y3lo : q22[r - 1];
+                    const double2 yh3 = r == R - 1 ? y3hi : q22[r + 1];
+                    a3[r] = update_point<K_MID, ZF, true, SQ, C2M>(g, q23[r].x, q22[r].x, q21[r].x, yl3.x, yh3.x,
+                                                                x3l[r], q22[r].y, fq4[r].x, q14[r].x, sc.dt2, sc.cos3);
+                    b3[r] = update_point<K_MID, ZF, true, SQ, C2M>(g, q23[r].y, q22[r].y, q21[r].y, yl3.y, yh3.y,
+                                                                q22[r].x, x3h[r], fq4[r].y, q14[r].y, sc.dt2, sc.cos3);
+                }
+            }
+            // ---- publish level 1 (plane i) and level 2 (plane i-2), then arrive
+            const bool pin1 = plane_in(i);
+            const bool pin2 = plane_in(i - 2);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int prow = prow0 + r * LW;
+                const bool c0 = pin1 & yx0[r], c1 = pin1 & yx1[r];
+                q10[r] = make_double2(c0 ? a1[r] : 0.0, c1 ? b1[r] : 0.0);
+                *reinterpret_cast<double2 *>(l1buf + R1W * L1_EL + prow) = q10[r];
+                if (D2 && row2(r)) {
+                    const bool e0 = pin2 & yx0[r], e1 = pin2 & yx1[r];
+                    q20[r] = make_double2(e0 ? a2[r] : 0.0, e1 ? b2[r] : 0.0);
+                    *reinterpret_cast<double2 *>(l2buf + W2 * L2_EL + prow - LW) = q20[r];
+                } else {
+                    q20[r] = z2;
+                }
+            }
+            arrive(itbar);
+
+            // ---- level-3 outputs at plane i-4: the filter sum, W^{s+2}, W^{s+3}, acc (or v / dst)
+            const int p3 = i - 4;
+            const bool out3 = p3 >= i0 && p3 < i1;
+            if (D3) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    if (!row3(r)) continue;
+                    if (out3 && (ok0[r] || ok1[r])) {
+                        // HBM -> L2 four planes ahead, so the one-plane-ahead register loads hit L2
+                        if (p3 + 4 < i1) {
+                            if (K1 != K_FIRST) prefetch_l2(m.acc + (long long)(p3 + 4) * S0 + pbase[r]);
+                            if (want_v) prefetch_l2(m.v + (long long)(p3 + 4) * S0 + pbase[r]);
+                        }
+                        const double2 acc_c = acc_n[r], v_c = v_n[r];
+                        double s0, s1;
+                        if (K1 == K_FIRST) {  // timestep.py:284 then :298 per step
+                            s0 = whb_add(whb_mul(sc.c0, ws5[r].x), whb_mul(sc.c1, q14[r].x));
+                            s1 = whb_add(whb_mul(sc.c0, ws5[r].y), whb_mul(sc.c1, q14[r].y));
+                        } else {
+                            s0 = whb_add(acc_c.x, whb_mul(sc.c1, q14[r].x));
+                            s1 = whb_add(acc_c.y, whb_mul(sc.c1, q14[r].y));
+                        }
+                        s0 = whb_add(whb_add(s0, whb_mul(sc.c2, q22[r].x)), whb_mul(sc.c3, a3[r]));
+                        s1 = whb_add(whb_add(s1, whb_mul(sc.c2, q22[r].y)), whb_mul(sc.c3, b3[r]));
+                        const long long p = (long long)p3 * S0 + pbase[r];
+                        if (K2 == K_MID) {
+                            if (ok0[r] && ok1[r]) {
+                                *reinterpret_cast<double2 *>(w2g + p) = q22[r];
+                                *reinterpret_cast<double2 *>(w3g + p) = make_double2(a3[r], b3[r]);
+                                *reinterpret_cast<double2 *>(m.acc + p) = make_double2(s0, s1);
+                            } else {
+                                if (ok0[r]) { w2g[p] = q22[r].x; w3g[p] = a3[r]; m.acc[p] = s0; }
+                                if (ok1[r]) { w2g[p + 1] = q22[r].y; w3g[p + 1] = b3[r]; m.acc[p + 1] = s1; }
+                            }
+                        } else {
+                            const double o0 = whb_mul(sc.osc, s0);
+                            const double o1 = whb_mul(sc.osc, s1);
+                            if (m.out_mode == WHB_OUT_FPI) {
+                                if (ok0[r]) { const double d = o0 - v_c.x; rsum += d * d; m.v[p] = o0; }
+                                if (ok1[r]) { const double d = o1 - v_c.y; rsum += d * d; m.v[p + 1] = o1; }
+                            } else if (m.out_mode == WHB_OUT_AV) {
+                                if (ok0[r]) m.dst[p] = whb_sub(v_c.x, o0);
+                                if (ok1[r]) m.dst[p + 1] = whb_sub(v_c.y, o1);
+                            } else {
+                                if (ok0[r]) m.dst[p] = o0;
+                                if (ok1[r]) m.dst[p + 1] = o1;
+                            }
+                        }
+                    }
+                    // the next output plane's acc / v, after the last use of this plane's (so the
+                    // load lands in the loop-carried registers), unconditionally and from an
+                    // in-bounds plane (a predicated load merged with the old value made the compiler
+                    // copy the loaded register right away, i.e. wait for the load)
+                    const int pn = min(max(p3 + 1, i0), i1 - 1);
+                    const long long o = (long long)pn * S0 + pbase[r];
+                    if (K1 != K_FIRST) acc_n[r] = __ldcg(reinterpret_cast<const double2 *>(m.acc + o));
+                    if (K2 == K_LAST) v_n[r] = __ldcg(reinterpret_cast<const double2 *>((want_v ? m.v : m.acc) + o));
+                }
+            }
+            sl_i = sl_n;
+            sl_n = sl_n + 1 == ST ? 0 : sl_n + 1;
+            ph_n ^= (sl_n == 0);
+            r1w = r12;
+            r12 = (r12 + 1) % 3;
+            w2 = w2 + 1 == N2 ? 0 : w2 + 1;
+        }
+    };
+    using T_ = std::true_type;
+    using F_ = std::false_type;
+    if (any3) run(T_{}, T_{});
+    else if (any2) run(T_{}, F_{});
+    else run(F_{}, F_{});
+#else
     // Plane loop, one copy of the body (a 6-way unrolled version with compile-time slots was
     // measured slower: 4-7K instructions of loop body thrash the instruction cache).  Stage and
     // ring slots advance incrementally: plane p <-> stage slot (p - pfirst) % ST.
@@ -393,6 +591,7 @@ __global__ void __launch_bounds__(threads<R>(), 1)
         r12 = (r12 + 1) % 3;
         w2 = w2 + 1 == N2 ? 0 : w2 + 1;
     }
+#endif
     (void)any_ok;
     if (K2 == K_LAST && m.out_mode == WHB_OUT_FPI) {
         const double t = block_sum(rsum);
