@@ -2,42 +2,48 @@
 // skewed so that ONE block barrier per plane orders everything (sm_100a).
 //
 // A CTA owns a BY x TX output tile (axis 1 x axis 2) and marches it through a chunk of axis-0
-// planes [i0, i1).  Its 16 warps cover the level-1 region: warp w <-> row j0 - 2 + w, lane l <->
-// the column pair k0 - 2 + 2l, +1 (64 columns).  Levels (time level s+t = "level t"):
+// planes [i0, i1).  Its 512 threads cover the level-1 region, one column pair per thread.  Tile
+// shape (Shape<LX>, LX = lanes of a warp along axis 2; a warp covers 32 / LX rows):
 //
-//     level 1 on rows j0-2 .. j0+BY+1, columns k0-2 .. k0+TX+1   (16 x 64, halo 2)
-//     level 2 on rows j0-1 .. j0+BY,   columns k0-1 .. k0+TX     (14 x 62, halo 1)
-//     level 3 on rows j0   .. j0+BY-1, columns k0   .. k0+TX-1   (12 x 60, the tile)
+//     LX = 32 (main): level-1 region 16 x 64, tile BY x TX = 12 x 60 (warp w <-> row j0 - 2 + w)
+//     LX = 16 / 8 / 4 (ragged right edge): 32 x 32 / 64 x 16 / 128 x 8, tiles 28 x 28 / 60 x 12 / 124 x 4
+//
+// The last column of tiles of a grid whose interior width is not a multiple of 60 uses the
+// narrowest shape that covers the remainder: on 1025^3 the remainder is 4 columns, which the main
+// shape would serve with 86 x nch CTAs computing 64 columns each (5.5 % of the pass); the 124 x 4
+// shape does it with 9 x nch.  Both shapes are bodies of the same kernel (one launch; the CTA
+// picks by blockIdx.x), with the same arithmetic per point.  Levels (time level s+t = "level t"):
+//
+//     level 1 on rows j0-2 .. j0+BY+1, columns k0-2 .. k0+TX+1   (halo 2)
+//     level 2 on rows j0-1 .. j0+BY,   columns k0-1 .. k0+TX     (halo 1)
+//     level 3 on rows j0   .. j0+BY-1, columns k0   .. k0+TX-1   (the tile)
 //
 // Iteration i computes level 1 at plane i, level 2 at plane i-2 and level 3 at plane i-4.  Every
 // input of an iteration was produced by an EARLIER iteration (level 2 at i-2 reads level 1 at
 // planes i-3..i-1; level 3 at i-4 reads level 2 at i-5..i-3), so the three level updates of an
 // iteration are independent (3-way ILP per thread) and one split barrier per plane (an mbarrier:
-// arrive after the level-1/2 stores, wait at the top of the next iteration) publishes them.  Axis-0 neighbours and the pointwise terms (W^{s-1}, f, the previous level, the filter
-// sum) come from per-thread register queues; the axis-1/axis-2 neighbours of the level being
-// stepped come from shared memory (W^s: the TMA stage; levels 1 and 2: 3-plane rings), axis-2
-// neighbours inside a warp by shuffles.
+// arrive after the level-1/2 stores, wait at the top of the next iteration) publishes them.
+// Axis-0 neighbours and the pointwise terms (W^{s-1}, f, the previous level, the filter sum) come
+// from per-thread register queues; the axis-1 neighbours of the level being stepped come from
+// shared memory (W^s: the TMA stage; levels 1 and 2: 3- / 4-plane rings), axis-2 neighbours of
+// level 1 from the stage, of levels 2 / 3 by shuffles (a lane at the edge of its row receives a
+// value of another row: it only feeds halo columns, which no output depends on).
 //
 // HBM traffic per output point per pass: read W^s, W^{s-1}, f, acc; write W^{s+2}, W^{s+3}, acc:
 // 56 B for 3 updates = 18.7 B/update (28 for two steps per pass, 48 for one).  Halo boxes are
-// re-read by the neighbouring tiles, mostly from L2.  Redundant level-1/2 work on the halo:
-// (16*64 + 14*64) / (2*12*60) - 1 = 33 % of those two levels (the level-3 tile carries none).
+// re-read by the neighbouring tiles, mostly from L2.  Redundant level-1/2 work on the halo (main
+// shape): (16*64 + 14*64) / (2*12*60) - 1 = 33 % of those two levels (the level-3 tile carries none).
 //
 // Arithmetic and its order are exactly three consecutive reference steps (update_point, the
 // filter sum in step order), so the iterates stay bitwise equal to the reference's.
 //
-// Measured alternative (round 2): every stencil operand re-read from shared-memory level rings
-// (5- / 4-plane rings, no register queues, f / acc / v from global one plane ahead) -- 164.5 vs
-// 202.6 Gpts/s on config 4: the queue moves it saves cost less than the LDS->DMUL latency it adds
-// (short-scoreboard stalls 24 % of samples vs barrier 19 %).
+// Measured alternatives (round 2, config 4): every stencil operand re-read from shared-memory
+// level rings (no register queues) 164.5 vs 202.6 Gpts/s; two rows per lane (8 warps) 120-160 vs
+// 169-202; a 6-way unrolled plane loop 123-168 (instruction cache); the three level updates one
+// after the other instead of interleaved 225.0 vs 236.7.
 #pragma once
 
 #include <type_traits>
-
-// 1: the three level updates of an iteration interleaved (default); 0: one level after the other
-#ifndef WHB_T3_ILP
-#define WHB_T3_ILP 1
-#endif
 
 namespace t3 {
 
@@ -52,26 +58,40 @@ using bulk::mbar_wait;
 using bulk::tma_load_3d;
 using bulk::update_point;
 
-constexpr int TX = 60;                 // output columns per tile
-constexpr int BY = 12;                 // output rows per tile
-constexpr int NR = BY + 4;             // level-1 rows (16): NR / R warps of R rows each
-constexpr int LW = 64;                 // level-1 row width (columns k0-2 .. k0+61)
-constexpr int RW = 68;                 // staged W^s row: columns k0-4 .. k0+63
-constexpr int WR = BY + 6;             // staged W^s rows: j0-3 .. j0+BY+2
-constexpr int W_EL = (WR * RW + 15) / 16 * 16;   // 1232 (128-B aligned sub-buffers for TMA)
-constexpr int P_EL = NR * LW;                    // 1024: W^{s-1} / f box (the level-1 region)
-constexpr int STAGE = W_EL + 2 * P_EL;           // 3280 doubles = 26.2 KB
-constexpr int L1_EL = NR * LW;                   // level-1 plane
-constexpr int L2_EL = (NR - 2) * LW;             // level-2 plane (rows j0-1 .. j0+BY)
-constexpr int N2 = 4;                            // level-2 ring: planes i-5 .. i-2 (see the split barrier)
+constexpr int NTHREADS = 512;          // 16 warps, one level-1 point pair per thread
+constexpr int N2 = 4;                  // level-2 ring: planes i-5 .. i-2 (see the split barrier)
+
+template <int LX>
+struct Shape {
+    static_assert(LX == 32 || LX == 16 || LX == 8 || LX == 4, "lanes along axis 2");
+    static constexpr int RPW = 32 / LX;              // level-1 rows per warp
+    static constexpr int NR = 16 * RPW;              // level-1 rows
+    static constexpr int LW = 2 * LX;                // level-1 row width (columns k0-2 .. k0+TX+1)
+    static constexpr int TX = LW - 4;                // output columns per tile
+    static constexpr int BY = NR - 4;                // output rows per tile
+    static constexpr int RW = LW + 4;                // staged W^s row: columns k0-4 .. k0+TX+3
+    static constexpr int WR = NR + 2;                // staged W^s rows: j0-3 .. j0+BY+2
+    static constexpr int W_EL = (WR * RW + 15) / 16 * 16;  // 128-B aligned sub-buffers for TMA
+    static constexpr int P_EL = NR * LW;             // W^{s-1} / f box (the level-1 region): 1024
+    static constexpr int STAGE = W_EL + 2 * P_EL;    // main: 3280 doubles = 26.2 KB
+    static constexpr int L1_EL = NR * LW;            // level-1 plane
+    static constexpr int L2_EL = (NR - 2) * LW;      // level-2 plane (rows j0-1 .. j0+BY)
+    template <int ST>
+    static constexpr size_t smem_bytes() {
+        return (size_t)(ST * STAGE + 3 * L1_EL + N2 * L2_EL) * sizeof(double) + (ST + 1) * sizeof(uint64_t);
+    }
+};
+using Main = Shape<32>;
+constexpr int TX = Main::TX;           // main tile: 12 x 60
+constexpr int BY = Main::BY;
+
+// Shape of the last tile column for `rem` remaining interior columns (0: none left; 32: main).
+constexpr int edge_lx(int rem) {
+    return rem <= 0 ? 0 : rem <= Shape<4>::TX ? 4 : rem <= Shape<8>::TX ? 8 : rem <= Shape<16>::TX ? 16 : 32;
+}
 
 __device__ __forceinline__ void arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bulk::smem_u32(bar)) : "memory");
-}
-
-template <int ST>
-constexpr size_t smem_bytes() {
-    return (size_t)(ST * STAGE + 3 * L1_EL + N2 * L2_EL) * sizeof(double) + (ST + 1) * sizeof(uint64_t);
 }
 
 // Per-pass scalars (the reference's host expressions), passed as a kernel parameter.
@@ -82,27 +102,21 @@ struct Scal {
     double osc;                 // (2/T) dt (last pass)
 };
 
-// K1: kind of step s (FIRST when s == 0); K2: MID, or LAST when step s+2 ends the solve.
-// GM: geometry mode as in tb2 / wf2d (0 generic, 1 equal taps, 2 equal taps and c^2 == 1).
-template <int R>
-constexpr int threads() {
-    return 32 * NR / R;
-}
-
-// K1: kind of step s (FIRST when s == 0); K2: MID, or LAST when step s+2 ends the solve.
-// GM: geometry mode as in tb2 / wf2d (0 generic, 1 equal taps, 2 equal taps and c^2 == 1).
-// R: level-1 rows per warp (each lane: R rows x 2 columns); the axis-1 neighbours between a
-// thread's own rows come from its registers, only the outer two from shared memory.
-template <int ST, int K1, int K2, bool ZF, int GM, int R>
-__global__ void __launch_bounds__(threads<R>(), 1)
-    t3_kernel(Geom g, const Member *__restrict__ members, int s, int i_begin, int i_end, int chunk_len, int JT,
-              const Scal sc, const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_p,
-              const __grid_constant__ CUtensorMap tm_f) {
+// One CTA's march.  K1: kind of step s (FIRST when s == 0); K2: MID, or LAST when step s+2 ends
+// the solve.  GM: geometry mode as in tb2 / wf2d (0 generic, 1 equal taps, 2 equal taps and
+// c^2 == 1).  JT: row tiles of this shape; blockIdx.y = chunk * JTY + row tile (JTY = row tiles of
+// the main shape, the grid's), k0: first output column.
+template <int ST, int K1, int K2, bool ZF, int GM, int LX>
+__device__ __forceinline__ void body(double *smem, const Geom &g, const Member *__restrict__ members, int s,
+                                     int i_begin, int i_end, int chunk_len, int JTY, int JT, int k0, const Scal &sc,
+                                     const CUtensorMap *tm_w, const CUtensorMap *tm_p, const CUtensorMap *tm_f) {
+    using S = Shape<LX>;
+    constexpr int LW = S::LW, RW = S::RW, NR = S::NR, W_EL = S::W_EL, P_EL = S::P_EL, STAGE = S::STAGE;
+    constexpr int L1_EL = S::L1_EL, L2_EL = S::L2_EL;
+    constexpr bool UNI = (LX == 32);  // a warp is one row: the level roles are warp-uniform
     constexpr bool SQ = GM >= 1;
     constexpr int C2M = GM == 2 ? 0 : -1;
     constexpr bool LOAD_P = (K1 != K_FIRST);
-    static_assert(NR % R == 0, "rows per warp must divide the level-1 rows");
-    extern __shared__ __align__(128) double smem[];
     double *l1buf = smem + (size_t)ST * STAGE;
     double *l2buf = l1buf + 3 * L1_EL;
     uint64_t *bars = reinterpret_cast<uint64_t *>(l2buf + N2 * L2_EL);
@@ -111,13 +125,14 @@ __global__ void __launch_bounds__(threads<R>(), 1)
     const Member m = members[0];
     const int w = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // warp-uniform
     const int lane = threadIdx.x & 31;
-    const int jt = blockIdx.y % JT;
-    const int ch = blockIdx.y / JT;
-    const int k0 = blockIdx.x * TX;
-    const int j0 = jt * BY;
+    const int cl = lane % LX;                  // column pair within the row
+    const int rho = w * S::RPW + lane / LX;    // level-1 region row (y = j0 - 2 + rho)
+    const int jt = blockIdx.y % JTY;
+    const int ch = blockIdx.y / JTY;
+    const int j0 = jt * S::BY;
     const int i0 = i_begin + ch * chunk_len;
     const int i1 = min(i_end, i0 + chunk_len);
-    if (i0 >= i1) {
+    if (i0 >= i1 || jt >= JT) {
         if (K2 == K_LAST && m.out_mode == WHB_OUT_FPI && threadIdx.x == 0)
             m.partials[blockIdx.y * gridDim.x + blockIdx.x] = 0.0;
         return;
@@ -127,7 +142,7 @@ __global__ void __launch_bounds__(threads<R>(), 1)
     const long long S0 = g.S0;
     const int P = g.P;
 
-    constexpr uint32_t stage_bytes = (uint32_t)((RW * WR + (LOAD_P ? P_EL : 0) + (ZF ? 0 : P_EL)) * 8);
+    constexpr uint32_t stage_bytes = (uint32_t)((RW * S::WR + (LOAD_P ? P_EL : 0) + (ZF ? 0 : P_EL)) * 8);
     // staged planes i0-3 .. i1+2; stage slot of plane p: (p - (i0 - 3)) % ST
     const int pfirst = i0 - 3;
     const int plast = i1 + 2;
@@ -136,71 +151,54 @@ __global__ void __launch_bounds__(threads<R>(), 1)
         double *st = smem + (size_t)slot * STAGE;
         uint64_t *bar = bars + slot;
         mbar_expect_tx(bar, stage_bytes);
-        tma_load_3d(st, &tm_w, k0 - 4, j0 - 3, plane, bar);
-        if (LOAD_P) tma_load_3d(st + W_EL, &tm_p, k0 - 2, j0 - 2, plane, bar);
-        if (!ZF) tma_load_3d(st + W_EL + P_EL, &tm_f, k0 - 2, j0 - 2, plane, bar);
+        tma_load_3d(st, tm_w, k0 - 4, j0 - 3, plane, bar);
+        if (LOAD_P) tma_load_3d(st + W_EL, tm_p, k0 - 2, j0 - 2, plane, bar);
+        if (!ZF) tma_load_3d(st + W_EL + P_EL, tm_f, k0 - 2, j0 - 2, plane, bar);
     };
 
     if (threadIdx.x == 0) {
         for (int t = 0; t < ST; ++t) mbar_init(bars + t, 1);
-        mbar_init(itbar, 32 * NR / R);  // every thread of the CTA
+        mbar_init(itbar, NTHREADS);  // every thread of the CTA
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int p = pfirst; p <= plast && p < pfirst + ST; ++p) issue(p);
     }
     __syncthreads();
 
-    // this thread's rows rho = w*R + r (level-1 region rows; y = j0 - 2 + rho) and column pair
-    const int x = k0 - 2 + 2 * lane;
+    // this thread's point pair
+    const int x = k0 - 2 + 2 * cl;
+    const int y = j0 - 2 + rho;
     const bool xin0 = (x >= 1) && (x < g.n2 - 1);
     const bool xin1 = (x + 1 >= 1) && (x + 1 < g.n2 - 1);
-    const int rho0 = w * R;
-    bool yin[R], ok0[R], ok1[R], yx0[R], yx1[R];
-    long long pbase[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const int y = j0 - 2 + rho0 + r;
-        yin[r] = (y >= g.j_lo) && (y < g.j_hi);
-        const bool own = (rho0 + r >= 2) && (rho0 + r <= NR - 3) && lane >= 1 && lane <= 30;
-        ok0[r] = own && yin[r] && xin0;
-        ok1[r] = own && yin[r] && xin1;
-        yx0[r] = yin[r] && xin0;  // level value kept (not a Dirichlet / out-of-domain point)
-        yx1[r] = yin[r] && xin1;
-        pbase[r] = (long long)y * P + x;
-    }
-    bool any_ok = false;
-#pragma unroll
-    for (int r = 0; r < R; ++r) any_ok = any_ok || ok0[r] || ok1[r];
-    // warp-uniform row ranges: level 2 on rows 1 .. NR-2, level 3 on rows 2 .. NR-3
-    auto row2 = [&](int r) { return rho0 + r >= 1 && rho0 + r <= NR - 2; };
-    auto row3 = [&](int r) { return rho0 + r >= 2 && rho0 + r <= NR - 3; };
-    bool any2 = false, any3 = false;
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        any2 = any2 || row2(r);
-        any3 = any3 || row3(r);
-    }
-    const int wrow0 = (rho0 + 1) * RW + 2 + 2 * lane;  // first own row in a W^s stage
-    const int prow0 = rho0 * LW + 2 * lane;            // first own row in a W^{s-1} / f box, level-1 plane
+    const bool yin = (y >= g.j_lo) && (y < g.j_hi);
+    const bool own = (rho >= 2) && (rho <= NR - 3) && cl >= 1 && cl <= LX - 2;
+    const bool ok0 = own && yin && xin0;
+    const bool ok1 = own && yin && xin1;
+    const bool okk = ok0 || ok1;
+    const bool yx0 = yin && xin0;  // level value kept (not a Dirichlet / out-of-domain point)
+    const bool yx1 = yin && xin1;
+    const long long pbase = (long long)y * P + x;
+    // level 2 on region rows 1 .. NR-2, level 3 on rows 2 .. NR-3
+    const bool r2 = rho >= 1 && rho <= NR - 2;
+    const bool r3 = rho >= 2 && rho <= NR - 3;
+    const int wlo = w * S::RPW, whi = wlo + S::RPW - 1;  // the warp's rows
+    const bool any2 = whi >= 1 && wlo <= NR - 2;
+    const bool any3 = whi >= 2 && wlo <= NR - 3;
+    const int wrow0 = (rho + 1) * RW + 2 + 2 * cl;  // own row in a W^s stage
+    const int prow0 = rho * LW + 2 * cl;            // own row in a W^{s-1} / f box, level-1 plane
 
     auto plane_in = [&](int p) { return p >= g.i_lo && p < g.i_hi; };
     auto shl = [&](double v) { return __shfl_up_sync(0xffffffffu, v, 1); };
     auto shr = [&](double v) { return __shfl_down_sync(0xffffffffu, v, 1); };
-    // Dirichlet / out-of-domain points of a level are 0 (one select per value)
-    auto mask = [&](bool pin, double a, double b) -> double2 {
-        return make_double2((pin && xin0) ? a : 0.0, (pin && xin1) ? b : 0.0);
-    };
     auto lds2 = [&](const double *p) { return *reinterpret_cast<const double2 *>(p); };
 
-    // register queues per own row (column pair): W^s at planes i+1 .. i-4, level 1 at i .. i-4,
-    // level 2 at i-2 .. i-5, f at i .. i-4.  The plane loop is unrolled by ST = 6 (a multiple of
-    // the level-ring period 3), so the queue shifts are register renames and every stage / ring
-    // slot below is a compile-time constant.
+    // register queues of the own column pair: W^s at planes i+1 .. i-4, level 1 at i .. i-4,
+    // level 2 at i-2 .. i-5, f at i .. i-4
     const double2 z2 = make_double2(0.0, 0.0);
-    double2 ws0[R], ws1[R], ws2[R], ws3[R], ws4[R], ws5[R];  // ws0 = W^s(i+1), ws1 = W^s(i), ...
-    double2 q10[R], q11[R], q12[R], q13[R], q14[R];          // q1k = level 1 at plane i-k
-    double2 q20[R], q21[R], q22[R], q23[R];                  // q2k = level 2 at plane i-2-k
-    double2 fq0[R], fq1[R], fq2[R], fq3[R], fq4[R];          // fqk = f at plane i-k
-    double2 acc_n[R], v_n[R];
+    double2 ws0, ws1, ws2, ws3, ws4, ws5;  // ws0 = W^s(i+1), ws1 = W^s(i), ...
+    double2 q10, q11, q12, q13, q14;       // q1k = level 1 at plane i-k
+    double2 q20, q21, q22, q23;            // q2k = level 2 at plane i-2-k
+    double2 fq0, fq1, fq2, fq3, fq4;       // fqk = f at plane i-k
+    double2 acc_n, v_n;
     double rsum = 0.0;
 
     // W^s centres of planes i0-3 and i0-2 (the first iteration, i = i0-2, adds plane i0-1); the
@@ -208,25 +206,22 @@ __global__ void __launch_bounds__(threads<R>(), 1)
     mbar_wait(bars + 0, 0);
     mbar_wait(bars + 1, 0);
     const bool want_v = (K2 == K_LAST) && m.out_mode != WHB_OUT_PLAIN;
-    auto ld2 = [&](const double *base, int p, int r) -> double2 {
-        return *reinterpret_cast<const double2 *>(base + (long long)p * S0 + pbase[r]);
+    auto ld2 = [&](const double *base, int p) -> double2 {
+        return *reinterpret_cast<const double2 *>(base + (long long)p * S0 + pbase);
     };
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        ws1[r] = lds2(smem + 0 * STAGE + wrow0 + r * RW);  // becomes W^s(i-1) below
-        ws0[r] = lds2(smem + 1 * STAGE + wrow0 + r * RW);
-        ws2[r] = ws3[r] = ws4[r] = ws5[r] = z2;
-        q10[r] = q11[r] = q12[r] = q13[r] = q14[r] = z2;
-        q20[r] = q21[r] = q22[r] = q23[r] = z2;
-        fq0[r] = fq1[r] = fq2[r] = fq3[r] = fq4[r] = z2;
-        acc_n[r] = (K1 != K_FIRST && (ok0[r] || ok1[r])) ? ld2(m.acc, i0, r) : z2;
-        v_n[r] = (want_v && (ok0[r] || ok1[r])) ? ld2(m.v, i0, r) : z2;
-        if (ok0[r] || ok1[r])
-            for (int q = 1; q < 4 && i0 + q < i1; ++q) {
-                if (K1 != K_FIRST) prefetch_l2(m.acc + (long long)(i0 + q) * S0 + pbase[r]);
-                if (want_v) prefetch_l2(m.v + (long long)(i0 + q) * S0 + pbase[r]);
-            }
-    }
+    ws1 = lds2(smem + 0 * STAGE + wrow0);  // becomes W^s(i-1) below
+    ws0 = lds2(smem + 1 * STAGE + wrow0);
+    ws2 = ws3 = ws4 = ws5 = z2;
+    q10 = q11 = q12 = q13 = q14 = z2;
+    q20 = q21 = q22 = q23 = z2;
+    fq0 = fq1 = fq2 = fq3 = fq4 = z2;
+    acc_n = (K1 != K_FIRST && okk) ? ld2(m.acc, i0) : z2;
+    v_n = (want_v && okk) ? ld2(m.v, i0) : z2;
+    if (okk)
+        for (int q = 1; q < 4 && i0 + q < i1; ++q) {
+            if (K1 != K_FIRST) prefetch_l2(m.acc + (long long)(i0 + q) * S0 + pbase);
+            if (want_v) prefetch_l2(m.v + (long long)(i0 + q) * S0 + pbase);
+        }
     __syncthreads();  // every thread has read plane pfirst: its slot takes plane pfirst + ST
     if (threadIdx.x == 0 && pfirst + ST <= plast) {
         fence_proxy_async();
@@ -235,118 +230,97 @@ __global__ void __launch_bounds__(threads<R>(), 1)
 
     const int ibeg = i0 - 2;  // iteration i: level 1 at i, level 2 at i-2, level 3 at i-4
     const int iend = i1 + 3;
-#if WHB_T3_ILP
     // Plane loop with the three level updates interleaved: every shared-memory operand of the
-    // iteration (all written by earlier iterations) is loaded first, then the 3 x 2 x R update
-    // chains are formed in one block (no memory operation between them, so the compiler
-    // interleaves them: 6 independent fp64 chains per thread at R = 1 instead of 2), then levels 1
-    // and 2 are published and the split barrier is arrived on, then the level-3 outputs.  The loop
-    // is instantiated per warp role (warp-uniform): level 1 only (the outer two level-1 rows), levels
-    // 1-2 (the next two), all three levels.
+    // iteration (all written by earlier iterations) is loaded first, then the 3 x 2 update chains
+    // are formed in one block (no memory operation between them, so the compiler interleaves
+    // them: 6 independent fp64 chains per thread), then levels 1 and 2 are published and the
+    // split barrier is arrived on, then the level-3 outputs.  Split barrier: a thread arrives
+    // right after its level-1 and level-2 stores of iteration i and waits for everybody's arrival
+    // only at the top of iteration i+1, so the level-3 work of iteration i overlaps the barrier
+    // skew.  Safe because level 3 reads only the level-2 ring, at plane i-4, and a thread can run
+    // at most the level-3 part ahead: the level-2 store of iteration i+1 (plane i-1) lands in a
+    // different slot of the 4-plane ring; the level-1 / stage slots rewritten at i+1 were last
+    // read before the arrivals of iteration i.  The loop is instantiated per warp role
+    // (warp-uniform): level 1 only (a warp of only outer level-1 rows), levels 1-2, all three.
     auto run = [&](auto d2c, auto d3c) {
         constexpr bool D2 = decltype(d2c)::value;
         constexpr bool D3 = decltype(d3c)::value;
-        int sl_i = 1 % ST, sl_n = 2 % ST, ph_n = 0;
-        int r1w = 0, r12 = 1;
-        int w2 = N2 - 2;
+        int sl_i = 1 % ST, sl_n = 2 % ST, ph_n = 0;  // stages of planes i and i+1, phase of the latter
+        int r1w = 0, r12 = 1;                        // level-1 ring (3 planes): slots of planes i and i-2
+        int w2 = N2 - 2;                             // level-2 ring (4 planes): slot of plane i-2
         for (int i = ibeg; i <= iend; ++i) {
             if (i > ibeg) {
                 mbar_wait(itbar, (i - ibeg - 1) & 1);
-                if (threadIdx.x == 0 && i - 1 + ST <= plast) {
+                if (threadIdx.x == 0 && i - 1 + ST <= plast) {  // stage of plane i-1 is free
                     fence_proxy_async();
                     issue(i - 1 + ST);
                 }
             }
             const int SL_I = sl_i, SL_N = sl_n, R1W = r1w, R12 = r12, W2 = w2, R24 = (w2 + 2) % N2;
             if (i + 1 <= plast) mbar_wait(bars + SL_N, ph_n);
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                ws5[r] = ws4[r]; ws4[r] = ws3[r]; ws3[r] = ws2[r]; ws2[r] = ws1[r]; ws1[r] = ws0[r];
-                ws0[r] = lds2(smem + SL_N * STAGE + wrow0 + r * RW);
-                q14[r] = q13[r]; q13[r] = q12[r]; q12[r] = q11[r]; q11[r] = q10[r];
-                q23[r] = q22[r]; q22[r] = q21[r]; q21[r] = q20[r];
-                fq4[r] = fq3[r]; fq3[r] = fq2[r]; fq2[r] = fq1[r]; fq1[r] = fq0[r];
-            }
+            // shift the queues (every entry is assigned unconditionally, so the shifts rename)
+            ws5 = ws4; ws4 = ws3; ws3 = ws2; ws2 = ws1; ws1 = ws0;
+            ws0 = lds2(smem + SL_N * STAGE + wrow0);
+            q14 = q13; q13 = q12; q12 = q11; q11 = q10;
+            q23 = q22; q22 = q21; q21 = q20;
+            fq4 = fq3; fq3 = fq2; fq2 = fq1; fq1 = fq0;
             // ---- operands: level 1 (W^s stage of plane i), level 2 (level-1 ring, plane i-2),
             //      level 3 (level-2 ring, plane i-4); x neighbours of levels 2 / 3 by shuffles
             const double *st = smem + SL_I * STAGE;
             const double2 y1lo = lds2(st + wrow0 - RW);
-            const double2 y1hi = lds2(st + wrow0 + R * RW);
-            double x1l[R], x1h[R];
-            double2 pv[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int wrow = wrow0 + r * RW;
-                x1l[r] = st[wrow - 1];
-                x1h[r] = st[wrow + 2];
-                const int prow = prow0 + r * LW;
-                pv[r] = LOAD_P ? lds2(st + W_EL + prow) : z2;
-                if (!ZF) fq0[r] = lds2(st + W_EL + P_EL + prow);
-            }
+            const double2 y1hi = lds2(st + wrow0 + RW);
+            const double x1l = st[wrow0 - 1];
+            const double x1h = st[wrow0 + 2];
+            const double2 pv = LOAD_P ? lds2(st + W_EL + prow0) : z2;
+            if (!ZF) fq0 = lds2(st + W_EL + P_EL + prow0);
             double2 y2lo = z2, y2hi = z2, y3lo = z2, y3hi = z2;
-            double x2l[R], x2h[R], x3l[R], x3h[R];
+            double x2l = 0.0, x2h = 0.0, x3l = 0.0, x3h = 0.0;
             if (D2) {
+                // (rows outside the level-2 region read in-bounds ring rows and are not used)
                 const double *l1 = l1buf + R12 * L1_EL;
-                y2lo = lds2(l1 + (row2(0) ? prow0 - LW : prow0));
-                y2hi = lds2(l1 + (row2(R - 1) ? prow0 + R * LW : prow0));
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    x2l[r] = shl(q12[r].y);
-                    x2h[r] = shr(q12[r].x);
-                }
+                y2lo = lds2(l1 + ((UNI || r2) ? prow0 - LW : prow0));
+                y2hi = lds2(l1 + ((UNI || r2) ? prow0 + LW : prow0));
+                x2l = shl(q12.y);
+                x2h = shr(q12.x);
             }
             if (D3) {
                 const double *l2 = l2buf + R24 * L2_EL;
-                y3lo = lds2(l2 + (row3(0) ? prow0 - 2 * LW : 2 * lane));
-                y3hi = lds2(l2 + (row3(R - 1) ? prow0 + (R - 1) * LW : 2 * lane));
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    x3l[r] = shl(q22[r].y);
-                    x3h[r] = shr(q22[r].x);
-                }
+                y3lo = lds2(l2 + ((UNI || r3) ? prow0 - 2 * LW : 2 * cl));  // level-2 row rho - 1
+                y3hi = lds2(l2 + ((UNI || r3) ? prow0 : 2 * cl));           // level-2 row rho + 1
+                x3l = shl(q22.y);
+                x3h = shr(q22.x);
             }
             // ---- the three level updates (independent chains)
-            double a1[R], b1[R], a2[R], b2[R], a3[R], b3[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const double2 yl = r == 0 ? y1lo : ws1[r - 1];
-                const double2 yh = r == R - 1 ? y1hi : ws1[r + 1];
-                a1[r] = update_point<K1, ZF, true, SQ, C2M>(g, ws2[r].x, ws1[r].x, ws0[r].x, yl.x, yh.x, x1l[r],
-                                                         ws1[r].y, fq0[r].x, pv[r].x, sc.h1, sc.cos1);
-                b1[r] = update_point<K1, ZF, true, SQ, C2M>(g, ws2[r].y, ws1[r].y, ws0[r].y, yl.y, yh.y, ws1[r].x,
-                                                         x1h[r], fq0[r].y, pv[r].y, sc.h1, sc.cos1);
-                if (D2) {
-                    const double2 yl2 = r == 0 ? y2lo : q12[r - 1];
-                    const double2 yh2 = r == R - 1 ? y2hi : q12[r + 1];
-                    a2[r] = update_point<K_MID, ZF, true, SQ, C2M>(g, q13[r].x, q12[r].x, q11[r].x, yl2.x, yh2.x,
-                                                                x2l[r], q12[r].y, fq2[r].x, ws3[r].x, sc.dt2, sc.cos2);
-                    b2[r] = update_point<K_MID, ZF, true, SQ, C2M>(g, q13[r].y, q12[r].y, q11[r].y, yl2.y, yh2.y,
-                                                                q12[r].x, x2h[r], fq2[r].y, ws3[r].y, sc.dt2, sc.cos2);
-                }
-                if (D3) {
-                    const double2 yl3 = r == 0 ? y3lo : q22[r - 1];
-                    const double2 yh3 = r == R - 1 ? y3hi : q22[r + 1];
-                    a3[r] = update_point<K_MID, ZF, true, SQ, C2M>(g, q23[r].x, q22[r].x, q21[r].x, yl3.x, yh3.x,
-                                                                x3l[r], q22[r].y, fq4[r].x, q14[r].x, sc.dt2, sc.cos3);
-                    b3[r] = update_point<K_MID, ZF, true, SQ, C2M>(g, q23[r].y, q22[r].y, q21[r].y, yl3.y, yh3.y,
-                                                                q22[r].x, x3h[r], fq4[r].y, q14[r].y, sc.dt2, sc.cos3);
-                }
+            double a2 = 0.0, b2 = 0.0, a3 = 0.0, b3 = 0.0;
+            const double a1 = update_point<K1, ZF, true, SQ, C2M>(g, ws2.x, ws1.x, ws0.x, y1lo.x, y1hi.x, x1l, ws1.y,
+                                                                fq0.x, pv.x, sc.h1, sc.cos1);
+            const double b1 = update_point<K1, ZF, true, SQ, C2M>(g, ws2.y, ws1.y, ws0.y, y1lo.y, y1hi.y, ws1.x, x1h,
+                                                                fq0.y, pv.y, sc.h1, sc.cos1);
+            if (D2) {  // prev of step s+1 = W^s at plane i-2 (ws3), f at plane i-2 (fq2)
+                a2 = update_point<K_MID, ZF, true, SQ, C2M>(g, q13.x, q12.x, q11.x, y2lo.x, y2hi.x, x2l, q12.y, fq2.x,
+                                                          ws3.x, sc.dt2, sc.cos2);
+                b2 = update_point<K_MID, ZF, true, SQ, C2M>(g, q13.y, q12.y, q11.y, y2lo.y, y2hi.y, q12.x, x2h, fq2.y,
+                                                          ws3.y, sc.dt2, sc.cos2);
+            }
+            if (D3) {  // level 2 at i-5, i-4, i-3 = q23, q22, q21; prev = level 1 at i-4 (q14); f at i-4 (fq4)
+                a3 = update_point<K_MID, ZF, true, SQ, C2M>(g, q23.x, q22.x, q21.x, y3lo.x, y3hi.x, x3l, q22.y, fq4.x,
+                                                          q14.x, sc.dt2, sc.cos3);
+                b3 = update_point<K_MID, ZF, true, SQ, C2M>(g, q23.y, q22.y, q21.y, y3lo.y, y3hi.y, q22.x, x3h, fq4.y,
+                                                          q14.y, sc.dt2, sc.cos3);
             }
             // ---- publish level 1 (plane i) and level 2 (plane i-2), then arrive
             const bool pin1 = plane_in(i);
             const bool pin2 = plane_in(i - 2);
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int prow = prow0 + r * LW;
-                const bool c0 = pin1 & yx0[r], c1 = pin1 & yx1[r];
-                q10[r] = make_double2(c0 ? a1[r] : 0.0, c1 ? b1[r] : 0.0);
-                *reinterpret_cast<double2 *>(l1buf + R1W * L1_EL + prow) = q10[r];
-                if (D2 && row2(r)) {
-                    const bool e0 = pin2 & yx0[r], e1 = pin2 & yx1[r];
-                    q20[r] = make_double2(e0 ? a2[r] : 0.0, e1 ? b2[r] : 0.0);
-                    *reinterpret_cast<double2 *>(l2buf + W2 * L2_EL + prow - LW) = q20[r];
+            {
+                const bool c0 = pin1 & yx0, c1 = pin1 & yx1;
+                q10 = make_double2(c0 ? a1 : 0.0, c1 ? b1 : 0.0);
+                *reinterpret_cast<double2 *>(l1buf + R1W * L1_EL + prow0) = q10;
+                if (D2 && (UNI || r2)) {
+                    const bool e0 = pin2 & yx0, e1 = pin2 & yx1;
+                    q20 = make_double2(e0 ? a2 : 0.0, e1 ? b2 : 0.0);
+                    *reinterpret_cast<double2 *>(l2buf + W2 * L2_EL + prow0 - LW) = q20;
                 } else {
-                    q20[r] = z2;
+                    q20 = z2;
                 }
             }
             arrive(itbar);
@@ -354,66 +328,64 @@ __global__ void __launch_bounds__(threads<R>(), 1)
             // ---- level-3 outputs at plane i-4: the filter sum, W^{s+2}, W^{s+3}, acc (or v / dst)
             const int p3 = i - 4;
             const bool out3 = p3 >= i0 && p3 < i1;
-            if (D3) {
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    if (!row3(r)) continue;
-                    if (out3 && (ok0[r] || ok1[r])) {
-                        // HBM -> L2 four planes ahead, so the one-plane-ahead register loads hit L2
-                        if (p3 + 4 < i1) {
-                            if (K1 != K_FIRST) prefetch_l2(m.acc + (long long)(p3 + 4) * S0 + pbase[r]);
-                            if (want_v) prefetch_l2(m.v + (long long)(p3 + 4) * S0 + pbase[r]);
-                        }
-                        const double2 acc_c = acc_n[r], v_c = v_n[r];
-                        double s0, s1;
-                        if (K1 == K_FIRST) {  // timestep.py:284 then :298 per step
-                            s0 = whb_add(whb_mul(sc.c0, ws5[r].x), whb_mul(sc.c1, q14[r].x));
-                            s1 = whb_add(whb_mul(sc.c0, ws5[r].y), whb_mul(sc.c1, q14[r].y));
+            if (D3 && (UNI || r3)) {
+                if (out3 && okk) {
+                    // HBM -> L2 four planes ahead, so the one-plane-ahead register loads hit L2
+                    // (measured: without it 20 % of the warp samples waited on them)
+                    if (p3 + 4 < i1) {
+                        if (K1 != K_FIRST) prefetch_l2(m.acc + (long long)(p3 + 4) * S0 + pbase);
+                        if (want_v) prefetch_l2(m.v + (long long)(p3 + 4) * S0 + pbase);
+                    }
+                    const double2 acc_c = acc_n, v_c = v_n;
+                    // acc (+ c0 W^0 on the first pass) + c1 W^{s+1} + c2 W^{s+2} + c3 W^{s+3}, in step order
+                    double s0, s1;
+                    if (K1 == K_FIRST) {  // timestep.py:284 then :298 per step
+                        s0 = whb_add(whb_mul(sc.c0, ws5.x), whb_mul(sc.c1, q14.x));
+                        s1 = whb_add(whb_mul(sc.c0, ws5.y), whb_mul(sc.c1, q14.y));
+                    } else {
+                        s0 = whb_add(acc_c.x, whb_mul(sc.c1, q14.x));
+                        s1 = whb_add(acc_c.y, whb_mul(sc.c1, q14.y));
+                    }
+                    s0 = whb_add(whb_add(s0, whb_mul(sc.c2, q22.x)), whb_mul(sc.c3, a3));
+                    s1 = whb_add(whb_add(s1, whb_mul(sc.c2, q22.y)), whb_mul(sc.c3, b3));
+                    const long long p = (long long)p3 * S0 + pbase;
+                    if (K2 == K_MID) {
+                        if (ok0 && ok1) {
+                            *reinterpret_cast<double2 *>(w2g + p) = q22;
+                            *reinterpret_cast<double2 *>(w3g + p) = make_double2(a3, b3);
+                            *reinterpret_cast<double2 *>(m.acc + p) = make_double2(s0, s1);
                         } else {
-                            s0 = whb_add(acc_c.x, whb_mul(sc.c1, q14[r].x));
-                            s1 = whb_add(acc_c.y, whb_mul(sc.c1, q14[r].y));
+                            if (ok0) { w2g[p] = q22.x; w3g[p] = a3; m.acc[p] = s0; }
+                            if (ok1) { w2g[p + 1] = q22.y; w3g[p + 1] = b3; m.acc[p + 1] = s1; }
                         }
-                        s0 = whb_add(whb_add(s0, whb_mul(sc.c2, q22[r].x)), whb_mul(sc.c3, a3[r]));
-                        s1 = whb_add(whb_add(s1, whb_mul(sc.c2, q22[r].y)), whb_mul(sc.c3, b3[r]));
-                        const long long p = (long long)p3 * S0 + pbase[r];
-                        if (K2 == K_MID) {
-                            if (ok0[r] && ok1[r]) {
-                                *reinterpret_cast<double2 *>(w2g + p) = q22[r];
-                                *reinterpret_cast<double2 *>(w3g + p) = make_double2(a3[r], b3[r]);
-                                *reinterpret_cast<double2 *>(m.acc + p) = make_double2(s0, s1);
-                            } else {
-                                if (ok0[r]) { w2g[p] = q22[r].x; w3g[p] = a3[r]; m.acc[p] = s0; }
-                                if (ok1[r]) { w2g[p + 1] = q22[r].y; w3g[p + 1] = b3[r]; m.acc[p + 1] = s1; }
-                            }
+                    } else {
+                        const double o0 = whb_mul(sc.osc, s0);
+                        const double o1 = whb_mul(sc.osc, s1);
+                        if (m.out_mode == WHB_OUT_FPI) {
+                            if (ok0) { const double d = o0 - v_c.x; rsum += d * d; m.v[p] = o0; }
+                            if (ok1) { const double d = o1 - v_c.y; rsum += d * d; m.v[p + 1] = o1; }
+                        } else if (m.out_mode == WHB_OUT_AV) {
+                            if (ok0) m.dst[p] = whb_sub(v_c.x, o0);
+                            if (ok1) m.dst[p + 1] = whb_sub(v_c.y, o1);
                         } else {
-                            const double o0 = whb_mul(sc.osc, s0);
-                            const double o1 = whb_mul(sc.osc, s1);
-                            if (m.out_mode == WHB_OUT_FPI) {
-                                if (ok0[r]) { const double d = o0 - v_c.x; rsum += d * d; m.v[p] = o0; }
-                                if (ok1[r]) { const double d = o1 - v_c.y; rsum += d * d; m.v[p + 1] = o1; }
-                            } else if (m.out_mode == WHB_OUT_AV) {
-                                if (ok0[r]) m.dst[p] = whb_sub(v_c.x, o0);
-                                if (ok1[r]) m.dst[p + 1] = whb_sub(v_c.y, o1);
-                            } else {
-                                if (ok0[r]) m.dst[p] = o0;
-                                if (ok1[r]) m.dst[p + 1] = o1;
-                            }
+                            if (ok0) m.dst[p] = o0;
+                            if (ok1) m.dst[p + 1] = o1;
                         }
                     }
-                    // the next output plane's acc / v, after the last use of this plane's (so the
-                    // load lands in the loop-carried registers), unconditionally and from an
-                    // in-bounds plane (a predicated load merged with the old value made the compiler
-                    // copy the loaded register right away, i.e. wait for the load)
-                    const int pn = min(max(p3 + 1, i0), i1 - 1);
-                    const long long o = (long long)pn * S0 + pbase[r];
-                    if (K1 != K_FIRST) acc_n[r] = __ldcg(reinterpret_cast<const double2 *>(m.acc + o));
-                    if (K2 == K_LAST) v_n[r] = __ldcg(reinterpret_cast<const double2 *>((want_v ? m.v : m.acc) + o));
                 }
+                // the next output plane's acc / v, after the last use of this plane's (so the
+                // load lands in the loop-carried registers), unconditionally and from an
+                // in-bounds plane (a predicated load merged with the old value made the compiler
+                // copy the loaded register right away, i.e. wait for the load)
+                const int pn = min(max(p3 + 1, i0), i1 - 1);
+                const long long o = (long long)pn * S0 + pbase;
+                if (K1 != K_FIRST) acc_n = __ldcg(reinterpret_cast<const double2 *>(m.acc + o));
+                if (K2 == K_LAST) v_n = __ldcg(reinterpret_cast<const double2 *>((want_v ? m.v : m.acc) + o));
             }
             sl_i = sl_n;
             sl_n = sl_n + 1 == ST ? 0 : sl_n + 1;
             ph_n ^= (sl_n == 0);
-            r1w = r12;
+            r1w = r12;  // (i+1) % 3 == (i-2) % 3
             r12 = (r12 + 1) % 3;
             w2 = w2 + 1 == N2 ? 0 : w2 + 1;
         }
@@ -423,180 +395,33 @@ __global__ void __launch_bounds__(threads<R>(), 1)
     if (any3) run(T_{}, T_{});
     else if (any2) run(T_{}, F_{});
     else run(F_{}, F_{});
-#else
-    // Plane loop, one copy of the body (a 6-way unrolled version with compile-time slots was
-    // measured slower: 4-7K instructions of loop body thrash the instruction cache).  Stage and
-    // ring slots advance incrementally: plane p <-> stage slot (p - pfirst) % ST.
-    int sl_i = 1 % ST, sl_n = 2 % ST, ph_n = 0;  // stages of planes i and i+1, phase of the latter
-    int r1w = 0, r12 = 1;  // level-1 ring (3 planes): slots of planes i and i-2
-    int w2 = N2 - 2;       // level-2 ring (4 planes): slot of plane i-2 ((i - 2 - ibeg) mod 4)
-    // Split per-plane barrier: a thread arrives on itbar right after its level-1 and level-2
-    // stores of iteration i and waits for everybody's arrival only at the top of iteration i+1,
-    // so the level-3 work of iteration i overlaps the barrier skew.  Safe because level 3 reads
-    // only the level-2 ring, at plane i-4, and a thread can run at most the level-3 part ahead:
-    // the level-2 store of iteration i+1 (plane i-1) lands in a different slot of the 4-plane ring;
-    // the level-1 / stage slots rewritten at i+1 were last read before the arrivals of iteration i.
-    for (int i = ibeg; i <= iend; ++i) {
-        if (i > ibeg) {
-            mbar_wait(itbar, (i - ibeg - 1) & 1);
-            if (threadIdx.x == 0 && i - 1 + ST <= plast) {  // stage of plane i-1 is free
-                fence_proxy_async();
-                issue(i - 1 + ST);
-            }
-        }
-        const int SL_I = sl_i, SL_N = sl_n, R1W = r1w, R12 = r12, W2 = w2, R24 = (w2 + 2) % N2;
-        // shift the queues: plane i+1 of W^s enters
-        // Every queue entry is assigned unconditionally in every copy (values outside a level's
-        // plane range are computed from stale data and never stored or consumed), so the
-        // compiler can rename the shifts instead of moving registers.
-        if (i + 1 <= plast) mbar_wait(bars + SL_N, ph_n);
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            ws5[r] = ws4[r]; ws4[r] = ws3[r]; ws3[r] = ws2[r]; ws2[r] = ws1[r]; ws1[r] = ws0[r];
-            ws0[r] = lds2(smem + SL_N * STAGE + wrow0 + r * RW);
-            q14[r] = q13[r]; q13[r] = q12[r]; q12[r] = q11[r]; q11[r] = q10[r];
-            q23[r] = q22[r]; q22[r] = q21[r]; q21[r] = q20[r];
-            fq4[r] = fq3[r]; fq3[r] = fq2[r]; fq2[r] = fq1[r]; fq1[r] = fq0[r];
-        }
-
-        // ---- level 1 at plane i (step s) on every row (needed for i <= i1 + 1)
-        {
-            const double *st = smem + SL_I * STAGE;
-            const double2 ylo = lds2(st + wrow0 - RW);             // row rho0 - 1
-            const double2 yhi = lds2(st + wrow0 + R * RW);         // row rho0 + R
-            const bool pin = plane_in(i);
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const double2 yl = r == 0 ? ylo : ws1[r - 1];
-                const double2 yh = r == R - 1 ? yhi : ws1[r + 1];
-                const int wrow = wrow0 + r * RW;
-                const double xl = st[wrow - 1], xh = st[wrow + 2];  // the stage has the halo columns
-                const int prow = prow0 + r * LW;
-                const double2 pv = LOAD_P ? lds2(st + W_EL + prow) : z2;
-                if (!ZF) fq0[r] = lds2(st + W_EL + P_EL + prow);
-                const double a = update_point<K1, ZF, true, SQ, C2M>(g, ws2[r].x, ws1[r].x, ws0[r].x, yl.x, yh.x, xl,
-                                                                   ws1[r].y, fq0[r].x, pv.x, sc.h1, sc.cos1);
-                const double b = update_point<K1, ZF, true, SQ, C2M>(g, ws2[r].y, ws1[r].y, ws0[r].y, yl.y, yh.y,
-                                                                   ws1[r].x, xh, fq0[r].y, pv.y, sc.h1, sc.cos1);
-                q10[r] = mask(pin && yin[r], a, b);
-                *reinterpret_cast<double2 *>(l1buf + R1W * L1_EL + prow) = q10[r];
-            }
-        }
-
-        // ---- level 2 at plane i-2 (step s+1): level 1 at i-3, i-2, i-1 (queues), rows rho-1, rho+1
-        const int p2 = i - 2;  // needed for i0 - 1 <= p2 <= i1
-        if (any2) {
-            const double *l1 = l1buf + R12 * L1_EL;
-            // (rows outside the level-2 region read in-bounds ring rows and are not used)
-            const double2 ylo = lds2(l1 + (row2(0) ? prow0 - LW : prow0));
-            const double2 yhi = lds2(l1 + (row2(R - 1) ? prow0 + R * LW : prow0));
-            const bool pin = plane_in(p2);
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                if (!row2(r)) {
-                    q20[r] = z2;
-                    continue;
-                }
-                const double2 yl = r == 0 ? ylo : q12[r - 1];
-                const double2 yh = r == R - 1 ? yhi : q12[r + 1];
-                const double xl = shl(q12[r].y), xh = shr(q12[r].x);
-                // prev of step s+1 = W^s at plane i-2 (ws3), f at plane i-2 (fq2)
-                const double a = update_point<K_MID, ZF, true, SQ, C2M>(g, q13[r].x, q12[r].x, q11[r].x, yl.x, yh.x,
-                                                                      xl, q12[r].y, fq2[r].x, ws3[r].x, sc.dt2,
-                                                                      sc.cos2);
-                const double b = update_point<K_MID, ZF, true, SQ, C2M>(g, q13[r].y, q12[r].y, q11[r].y, yl.y, yh.y,
-                                                                      q12[r].x, xh, fq2[r].y, ws3[r].y, sc.dt2,
-                                                                      sc.cos2);
-                q20[r] = mask(pin && yin[r], a, b);
-                *reinterpret_cast<double2 *>(l2buf + W2 * L2_EL + prow0 + r * LW - LW) = q20[r];
-            }
-        }
-        arrive(itbar);  // this thread's level-1 (plane i) and level-2 (plane i-2) stores are done
-
-        // ---- level 3 at plane i-4 (step s+2) on the tile, then the filter sum and the outputs
-        const int p3 = i - 4;
-        const bool out3 = p3 >= i0 && p3 < i1;  // outputs (stores, residual, prefetch) only then
-        if (any3) {
-            const double *l2 = l2buf + R24 * L2_EL;
-            const double2 ylo = lds2(l2 + (row3(0) ? prow0 - 2 * LW : 2 * lane));          // level-2 row rho0 - 1
-            const double2 yhi = lds2(l2 + (row3(R - 1) ? prow0 + (R - 1) * LW : 2 * lane));  // row rho0 + R
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                if (!row3(r)) continue;
-                const double2 yl = r == 0 ? ylo : q22[r - 1];
-                const double2 yh = r == R - 1 ? yhi : q22[r + 1];
-                const double xl = shl(q22[r].y), xh = shr(q22[r].x);
-                // level 2 at i-5, i-4, i-3 = q23, q22, q21; prev = level 1 at i-4 (q14); f at i-4 (fq4)
-                const double a3 = update_point<K_MID, ZF, true, SQ, C2M>(g, q23[r].x, q22[r].x, q21[r].x, yl.x, yh.x,
-                                                                       xl, q22[r].y, fq4[r].x, q14[r].x, sc.dt2,
-                                                                       sc.cos3);
-                const double b3 = update_point<K_MID, ZF, true, SQ, C2M>(g, q23[r].y, q22[r].y, q21[r].y, yl.y, yh.y,
-                                                                       q22[r].x, xh, fq4[r].y, q14[r].y, sc.dt2,
-                                                                       sc.cos3);
-                // next output plane's acc / v (one iteration ahead: hides the HBM latency)
-                const double2 acc_c = acc_n[r], v_c = v_n[r];
-                if (!out3 || !(ok0[r] || ok1[r])) continue;
-                if (p3 + 1 < i1) {
-                    if (K1 != K_FIRST) acc_n[r] = ld2(m.acc, p3 + 1, r);
-                    if (want_v) v_n[r] = ld2(m.v, p3 + 1, r);
-                }
-                // HBM -> L2 four planes ahead, so the one-plane-ahead register loads above hit L2
-                // (measured: without it 20 % of the warp samples waited on them)
-                if (p3 + 4 < i1) {
-                    if (K1 != K_FIRST) prefetch_l2(m.acc + (long long)(p3 + 4) * S0 + pbase[r]);
-                    if (want_v) prefetch_l2(m.v + (long long)(p3 + 4) * S0 + pbase[r]);
-                }
-                // acc (+ c0 W^0 on the first pass) + c1 W^{s+1} + c2 W^{s+2} + c3 W^{s+3}, in step order
-                double s0, s1;
-                if (K1 == K_FIRST) {  // timestep.py:284 then :298 per step
-                    s0 = whb_add(whb_mul(sc.c0, ws5[r].x), whb_mul(sc.c1, q14[r].x));
-                    s1 = whb_add(whb_mul(sc.c0, ws5[r].y), whb_mul(sc.c1, q14[r].y));
-                } else {
-                    s0 = whb_add(acc_c.x, whb_mul(sc.c1, q14[r].x));
-                    s1 = whb_add(acc_c.y, whb_mul(sc.c1, q14[r].y));
-                }
-                s0 = whb_add(whb_add(s0, whb_mul(sc.c2, q22[r].x)), whb_mul(sc.c3, a3));
-                s1 = whb_add(whb_add(s1, whb_mul(sc.c2, q22[r].y)), whb_mul(sc.c3, b3));
-                const long long p = (long long)p3 * S0 + pbase[r];
-                if (K2 == K_MID) {
-                    if (ok0[r] && ok1[r]) {
-                        *reinterpret_cast<double2 *>(w2g + p) = q22[r];
-                        *reinterpret_cast<double2 *>(w3g + p) = make_double2(a3, b3);
-                        *reinterpret_cast<double2 *>(m.acc + p) = make_double2(s0, s1);
-                    } else {
-                        if (ok0[r]) { w2g[p] = q22[r].x; w3g[p] = a3; m.acc[p] = s0; }
-                        if (ok1[r]) { w2g[p + 1] = q22[r].y; w3g[p + 1] = b3; m.acc[p + 1] = s1; }
-                    }
-                } else {
-                    const double o0 = whb_mul(sc.osc, s0);
-                    const double o1 = whb_mul(sc.osc, s1);
-                    if (m.out_mode == WHB_OUT_FPI) {
-                        if (ok0[r]) { const double d = o0 - v_c.x; rsum += d * d; m.v[p] = o0; }
-                        if (ok1[r]) { const double d = o1 - v_c.y; rsum += d * d; m.v[p + 1] = o1; }
-                    } else if (m.out_mode == WHB_OUT_AV) {
-                        if (ok0[r]) m.dst[p] = whb_sub(v_c.x, o0);
-                        if (ok1[r]) m.dst[p + 1] = whb_sub(v_c.y, o1);
-                    } else {
-                        if (ok0[r]) m.dst[p] = o0;
-                        if (ok1[r]) m.dst[p + 1] = o1;
-                    }
-                }
-            }
-        }
-
-        sl_i = sl_n;
-        sl_n = sl_n + 1 == ST ? 0 : sl_n + 1;
-        ph_n ^= (sl_n == 0);
-        r1w = r12;  // (i+1) % 3 == (i-2) % 3
-        r12 = (r12 + 1) % 3;
-        w2 = w2 + 1 == N2 ? 0 : w2 + 1;
-    }
-#endif
-    (void)any_ok;
     if (K2 == K_LAST && m.out_mode == WHB_OUT_FPI) {
         const double t = block_sum(rsum);
         if (threadIdx.x == 0) m.partials[blockIdx.y * gridDim.x + blockIdx.x] = t;
     }
+}
+
+// LXE: shape of the last column of tiles (blockIdx.x == gridDim.x - 1); 32 = the main shape everywhere.
+template <int ST, int LXE>
+constexpr size_t smem_bytes() {
+    return Main::smem_bytes<ST>() > Shape<LXE>::template smem_bytes<ST>() ? Main::smem_bytes<ST>()
+                                                                           : Shape<LXE>::template smem_bytes<ST>();
+}
+
+template <int ST, int K1, int K2, bool ZF, int GM, int LXE>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    t3_kernel(Geom g, const Member *__restrict__ members, int s, int i_begin, int i_end, int chunk_len, int JT,
+              int JTE, const Scal sc, const __grid_constant__ CUtensorMap tm_w,
+              const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_f,
+              const __grid_constant__ CUtensorMap te_w, const __grid_constant__ CUtensorMap te_p,
+              const __grid_constant__ CUtensorMap te_f) {
+    extern __shared__ __align__(128) double smem[];
+    if (LXE != 32 && blockIdx.x == gridDim.x - 1)
+        body<ST, K1, K2, ZF, GM, LXE>(smem, g, members, s, i_begin, i_end, chunk_len, JT, JTE,
+                                      (int)blockIdx.x * Main::TX, sc, &te_w, &te_p, &te_f);
+    else
+        body<ST, K1, K2, ZF, GM, 32>(smem, g, members, s, i_begin, i_end, chunk_len, JT, JT,
+                                     (int)blockIdx.x * Main::TX, sc, &tm_w, &tm_p, &tm_f);
 }
 
 }  // namespace t3

@@ -761,7 +761,7 @@ struct whb_ctx {
     // three-step (T = 3) plan: whole-grid single-problem 3D contexts (step_t3.cuh)
     bool t3 = false;
     size_t smem3 = 0;
-    int gx3 = 1, JT3 = 1, chunk3 = 1, nch3 = 1;
+    int gx3 = 1, JT3 = 1, JTE3 = 1, lxe3 = 32, chunk3 = 1, nch3 = 1;
     // cluster-resident small-grid 2D plan (whole grid in one cluster's shared memory)
     bool cres = false;
     int cres_cl = 0, cres_r = 0, cres_ppt = 1;
@@ -952,39 +952,52 @@ cudaError_t tb2_set_attrs(size_t smem) {
     return e;
 }
 
-// Three-step 3D kernel (step_t3.cuh): 6 TMA stages of 26 KB + the level-1/2 rings (202 KB), 1 CTA/SM.
+// Three-step 3D kernel (step_t3.cuh): 6 TMA stages of 26 KB + the level-1/2 rings (206-225 KB), 1 CTA/SM.
 #ifndef WHB_S3_ST
 #define WHB_S3_ST 6
 #endif
 constexpr int S3_ST = WHB_S3_ST;
-// level-1 rows per warp (1: 16 warps, measured fastest; 2: 8 warps, each lane 2 rows x 2 columns)
-#ifndef WHB_S3_R
-#define WHB_S3_R 1
-#endif
-constexpr int S3_R = WHB_S3_R;
-constexpr int S3_THREADS = t3::threads<S3_R>();
+constexpr int S3_THREADS = t3::NTHREADS;
 
-template <int K1, int K2, bool ZF, int GM>
+// LXE: tile shape of the last (ragged) column of tiles, t3::edge_lx(remaining columns)
+template <int K1, int K2, bool ZF, int GM, int LXE>
 auto t3_fn() {
-    return t3::t3_kernel<S3_ST, K1, K2, ZF, GM, S3_R>;
+    return t3::t3_kernel<S3_ST, K1, K2, ZF, GM, LXE>;
 }
 
-cudaError_t t3_set_attrs(size_t smem) {
+size_t t3_smem(int lxe) {
+    return lxe == 4 ? t3::smem_bytes<S3_ST, 4>() : lxe == 8 ? t3::smem_bytes<S3_ST, 8>()
+         : lxe == 16 ? t3::smem_bytes<S3_ST, 16>() : t3::smem_bytes<S3_ST, 32>();
+}
+
+// calls fn(integral_constant<int, LXE>) for the runtime shape
+template <class F>
+void t3_by_lxe(int lxe, F &&fn) {
+    if (lxe == 4) fn(std::integral_constant<int, 4>{});
+    else if (lxe == 8) fn(std::integral_constant<int, 8>{});
+    else if (lxe == 16) fn(std::integral_constant<int, 16>{});
+    else fn(std::integral_constant<int, 32>{});
+}
+
+cudaError_t t3_set_attrs(int lxe, size_t smem) {
     cudaError_t e = cudaSuccess;
     auto set = [&](auto fn) {
         cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (r != cudaSuccess) e = r;
     };
-    auto set_gm = [&](auto gm) {
-        constexpr int GM = decltype(gm)::value;
-        // (K_FIRST, K_LAST) is never launched: a 3-step solve would write v while reading it as W^0
-        set(t3_fn<K_FIRST, K_MID, false, GM>()); set(t3_fn<K_FIRST, K_MID, true, GM>());
-        set(t3_fn<K_MID, K_MID, false, GM>());   set(t3_fn<K_MID, K_MID, true, GM>());
-        set(t3_fn<K_MID, K_LAST, false, GM>());  set(t3_fn<K_MID, K_LAST, true, GM>());
-    };
-    set_gm(std::integral_constant<int, 0>{});
-    set_gm(std::integral_constant<int, 1>{});
-    set_gm(std::integral_constant<int, 2>{});
+    t3_by_lxe(lxe, [&](auto lx) {
+        constexpr int LXE = decltype(lx)::value;
+        auto set_gm = [&](auto gm) {
+            constexpr int GM = decltype(gm)::value;
+            // (K_FIRST, K_LAST) is never launched: a 3-step solve would write v while reading it as W^0
+            set(t3_fn<K_FIRST, K_MID, false, GM, LXE>()); set(t3_fn<K_FIRST, K_MID, true, GM, LXE>());
+            set(t3_fn<K_MID, K_MID, false, GM, LXE>());   set(t3_fn<K_MID, K_MID, true, GM, LXE>());
+            set(t3_fn<K_MID, K_LAST, false, GM, LXE>());  set(t3_fn<K_MID, K_LAST, true, GM, LXE>());
+        };
+        set_gm(std::integral_constant<int, 0>{});
+        set_gm(std::integral_constant<int, 1>{});
+        set_gm(std::integral_constant<int, 2>{});
+    });
     return e;
 }
 
@@ -1258,14 +1271,25 @@ int plan_launch(whb_ctx *c) {
     const char *t3env = getenv("WHB_T3");
     c->t3 = false;
     if (c->tb2 && c->act1 && c->kern == 2 && c->nbatch == 1 && !(t3env && std::string(t3env) == "0")) {
-        c->smem3 = t3::smem_bytes<S3_ST>();
-        cudaError_t e = t3_set_attrs(c->smem3);
+        // column tiles: full main tiles, then one tile of the narrowest shape covering the rest
+        const int gfull = (int)((n2 - 1) / t3::TX);
+        const int rem = (int)(n2 - 1) - gfull * t3::TX;
+        const char *e3 = getenv("WHB_T3_EDGE");  // 0: main shape on the ragged edge too (A/B)
+        c->lxe3 = (rem == 0 || (e3 && std::string(e3) == "0")) ? 32 : t3::edge_lx(rem);
+        c->smem3 = t3_smem(c->lxe3);
+        cudaError_t e = t3_set_attrs(c->lxe3, c->smem3);
         if (e != cudaSuccess) return fail(WHB_E_CUDA, std::string("cudaFuncSetAttribute(t3): ") + cudaGetErrorString(e));
         int nb = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, t3_fn<K_MID, K_MID, false, 2>(), S3_THREADS, c->smem3);
+        t3_by_lxe(c->lxe3, [&](auto lx) {
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, t3_fn<K_MID, K_MID, false, 2, decltype(lx)::value>(),
+                                                              S3_THREADS, c->smem3);
+        });
         if (e != cudaSuccess || nb < 1) return fail(WHB_E_CUDA, "t3 kernel does not fit on an SM");
-        c->gx3 = (int)((n2 - 1 + t3::TX - 1) / t3::TX);
+        c->gx3 = gfull + (rem > 0 ? 1 : 0);
         c->JT3 = (int)((n1 - 1 + t3::BY - 1) / t3::BY);
+        const int bye = c->lxe3 == 4 ? t3::Shape<4>::BY : c->lxe3 == 8 ? t3::Shape<8>::BY
+                      : c->lxe3 == 16 ? t3::Shape<16>::BY : t3::BY;
+        c->JTE3 = (int)((n1 - 1 + bye - 1) / bye);
         const long long tiles3 = (long long)c->gx3 * c->JT3;
         const long long res3 = (long long)sms * nb;
         // chunks: ~256 planes, but at least 4 waves of CTAs
@@ -1590,12 +1614,20 @@ int launch_t3(whb_ctx *c, int s, bool last, int ib, int ie, int cl) {
     const bool zf = c->cur_zf != 0;
     const Member &m0 = c->h_members[0];
     const MemberHost &mh = c->mem[c->order[0]];
-    CUtensorMap tw, tp, tf;
+    CUtensorMap tw, tp, tf, ew, ep, ef;
     std::memset(&tp, 0, sizeof(tp));
     std::memset(&tf, 0, sizeof(tf));
-    WHB_TRY(tensor_map(c, level_ptr(m0, s), t3::RW, t3::WR, &tw));
-    WHB_TRY(tensor_map(c, level_ptr(m0, s - 1), t3::LW, t3::NR, &tp));
-    if (m0.f) WHB_TRY(tensor_map(c, m0.f, t3::LW, t3::NR, &tf));
+    using SM = t3::Main;
+    WHB_TRY(tensor_map(c, level_ptr(m0, s), SM::RW, SM::WR, &tw));
+    WHB_TRY(tensor_map(c, level_ptr(m0, s - 1), SM::LW, SM::NR, &tp));
+    if (m0.f) WHB_TRY(tensor_map(c, m0.f, SM::LW, SM::NR, &tf));
+    ew = tw, ep = tp, ef = tf;
+    if (c->lxe3 != 32) {  // boxes of the ragged-edge shape
+        const int lw = 2 * c->lxe3, nr = 16 * (32 / c->lxe3);
+        WHB_TRY(tensor_map(c, level_ptr(m0, s), lw + 4, nr + 2, &ew));
+        WHB_TRY(tensor_map(c, level_ptr(m0, s - 1), lw, nr, &ep));
+        if (m0.f) WHB_TRY(tensor_map(c, m0.f, lw, nr, &ef));
+    }
     t3::Scal sc;
     const bool first = (s == 0);
     sc.h1 = first ? mh.half_dt2 : mh.dt2;
@@ -1612,9 +1644,11 @@ int launch_t3(whb_ctx *c, int s, bool last, int ib, int ie, int cl) {
     dim3 grid(c->gx3, c->JT3 * nch, 1);
     const int gm = geom_mode(c);
     auto go = [&](auto k1, auto k2, auto zft, auto gmt) {
-        t3_fn<decltype(k1)::value, decltype(k2)::value, decltype(zft)::value, decltype(gmt)::value>()
-            <<<grid, S3_THREADS, c->smem3, c->stream>>>(c->geom, c->d_members, s, ib, ie, cl,
-                                                         c->JT3, sc, tw, tp, tf);
+        t3_by_lxe(c->lxe3, [&](auto lx) {
+            t3_fn<decltype(k1)::value, decltype(k2)::value, decltype(zft)::value, decltype(gmt)::value,
+                  decltype(lx)::value>()<<<grid, S3_THREADS, c->smem3, c->stream>>>(
+                c->geom, c->d_members, s, ib, ie, cl, c->JT3, c->JTE3, sc, tw, tp, tf, ew, ep, ef);
+        });
     };
     using KF = std::integral_constant<int, K_FIRST>;
     using KM = std::integral_constant<int, K_MID>;

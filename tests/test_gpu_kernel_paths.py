@@ -52,6 +52,7 @@ print(json.dumps(out))
 @pytest.mark.parametrize("env", [{}, {"WHB_CRES": "0"}, {"WHB_CRES_CL": "8"}, {"WHB_CRES_CL": "3"}, {"WHB_WF": "2"}, {"WHB_WF": "0"}, {"WHB_TB2": "0"}, {"WHB_KERNEL": "bulk"},
                                  {"WHB_T3": "1", "WHB_CHUNK3": "7"}, {"WHB_T3": "1", "WHB_CHUNK3": "1"},
                                  {"WHB_T3": "1", "WHB_CHUNK3": "500"}, {"WHB_T3": "0"},
+                                 {"WHB_T3": "1", "WHB_T3_EDGE": "0"},
                                  {"WHB_KERNEL": "simple"}, {"WHB_NO_GRAPHS": "1"}])
 def test_every_kernel_path_bitwise(gpu_available, env):
     e = dict(os.environ, **env)
