@@ -45,6 +45,14 @@
 
 #include <type_traits>
 
+// plane-loop unroll (measured on config 4: 1 -> 239.7, 2 -> 246.3, 3 -> 240.1 Gpts/s; 6 thrashes the instruction cache)
+#ifndef WHB_T3_UNROLL
+#define WHB_T3_UNROLL 2
+#endif
+#define T3_PRAGMA_(x) _Pragma(#x)
+#define T3_UNROLL_(n) T3_PRAGMA_(unroll n)
+#define T3_UNROLL(n) T3_UNROLL_(n)
+
 namespace t3 {
 
 __device__ __forceinline__ void prefetch_l2(const void *p) {
@@ -102,14 +110,22 @@ struct Scal {
     double osc;                 // (2/T) dt (last pass)
 };
 
+// Row window of a launch: tile row jt starts at row j_off + jt * BY and only rows below j_end are
+// written (whole grid: 0 and INT_MAX; the banded host iteration launches one band of rows per
+// pass); part_off: first residual-partial slot of the launch.
+struct RowWin {
+    int j_off, j_end, part_off;
+};
+
 // One CTA's march.  K1: kind of step s (FIRST when s == 0); K2: MID, or LAST when step s+2 ends
 // the solve.  GM: geometry mode as in tb2 / wf2d (0 generic, 1 equal taps, 2 equal taps and
 // c^2 == 1).  JT: row tiles of this shape; blockIdx.y = chunk * JTY + row tile (JTY = row tiles of
 // the main shape, the grid's), k0: first output column.
 template <int ST, int K1, int K2, bool ZF, int GM, int LX>
 __device__ __forceinline__ void body(double *smem, const Geom &g, const Member *__restrict__ members, int s,
-                                     int i_begin, int i_end, int chunk_len, int JTY, int JT, int k0, const Scal &sc,
-                                     const CUtensorMap *tm_w, const CUtensorMap *tm_p, const CUtensorMap *tm_f) {
+                                     int i_begin, int i_end, int chunk_len, int JTY, int JT, int k0, const RowWin rw,
+                                     const Scal &sc, const CUtensorMap *tm_w, const CUtensorMap *tm_p,
+                                     const CUtensorMap *tm_f) {
     using S = Shape<LX>;
     constexpr int LW = S::LW, RW = S::RW, NR = S::NR, W_EL = S::W_EL, P_EL = S::P_EL, STAGE = S::STAGE;
     constexpr int L1_EL = S::L1_EL, L2_EL = S::L2_EL;
@@ -129,12 +145,12 @@ __device__ __forceinline__ void body(double *smem, const Geom &g, const Member *
     const int rho = w * S::RPW + lane / LX;    // level-1 region row (y = j0 - 2 + rho)
     const int jt = blockIdx.y % JTY;
     const int ch = blockIdx.y / JTY;
-    const int j0 = jt * S::BY;
+    const int j0 = rw.j_off + jt * S::BY;
     const int i0 = i_begin + ch * chunk_len;
     const int i1 = min(i_end, i0 + chunk_len);
     if (i0 >= i1 || jt >= JT) {
         if (K2 == K_LAST && m.out_mode == WHB_OUT_FPI && threadIdx.x == 0)
-            m.partials[blockIdx.y * gridDim.x + blockIdx.x] = 0.0;
+            m.partials[rw.part_off + blockIdx.y * gridDim.x + blockIdx.x] = 0.0;
         return;
     }
     double *w2g = level_ptr(m, s + 2);
@@ -170,7 +186,7 @@ __device__ __forceinline__ void body(double *smem, const Geom &g, const Member *
     const bool xin0 = (x >= 1) && (x < g.n2 - 1);
     const bool xin1 = (x + 1 >= 1) && (x + 1 < g.n2 - 1);
     const bool yin = (y >= g.j_lo) && (y < g.j_hi);
-    const bool own = (rho >= 2) && (rho <= NR - 3) && cl >= 1 && cl <= LX - 2;
+    const bool own = (rho >= 2) && (rho <= NR - 3) && cl >= 1 && cl <= LX - 2 && y < rw.j_end;
     const bool ok0 = own && yin && xin0;
     const bool ok1 = own && yin && xin1;
     const bool okk = ok0 || ok1;
@@ -248,6 +264,7 @@ __device__ __forceinline__ void body(double *smem, const Geom &g, const Member *
         int sl_i = 1 % ST, sl_n = 2 % ST, ph_n = 0;  // stages of planes i and i+1, phase of the latter
         int r1w = 0, r12 = 1;                        // level-1 ring (3 planes): slots of planes i and i-2
         int w2 = N2 - 2;                             // level-2 ring (4 planes): slot of plane i-2
+        T3_UNROLL(WHB_T3_UNROLL)
         for (int i = ibeg; i <= iend; ++i) {
             if (i > ibeg) {
                 mbar_wait(itbar, (i - ibeg - 1) & 1);
@@ -397,7 +414,7 @@ __device__ __forceinline__ void body(double *smem, const Geom &g, const Member *
     else run(F_{}, F_{});
     if (K2 == K_LAST && m.out_mode == WHB_OUT_FPI) {
         const double t = block_sum(rsum);
-        if (threadIdx.x == 0) m.partials[blockIdx.y * gridDim.x + blockIdx.x] = t;
+        if (threadIdx.x == 0) m.partials[rw.part_off + blockIdx.y * gridDim.x + blockIdx.x] = t;
     }
 }
 
@@ -411,17 +428,17 @@ constexpr size_t smem_bytes() {
 template <int ST, int K1, int K2, bool ZF, int GM, int LXE>
 __global__ void __launch_bounds__(NTHREADS, 1)
     t3_kernel(Geom g, const Member *__restrict__ members, int s, int i_begin, int i_end, int chunk_len, int JT,
-              int JTE, const Scal sc, const __grid_constant__ CUtensorMap tm_w,
+              int JTE, const RowWin rw, const Scal sc, const __grid_constant__ CUtensorMap tm_w,
               const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_f,
               const __grid_constant__ CUtensorMap te_w, const __grid_constant__ CUtensorMap te_p,
               const __grid_constant__ CUtensorMap te_f) {
     extern __shared__ __align__(128) double smem[];
     if (LXE != 32 && blockIdx.x == gridDim.x - 1)
         body<ST, K1, K2, ZF, GM, LXE>(smem, g, members, s, i_begin, i_end, chunk_len, JT, JTE,
-                                      (int)blockIdx.x * Main::TX, sc, &te_w, &te_p, &te_f);
+                                      (int)blockIdx.x * Main::TX, rw, sc, &te_w, &te_p, &te_f);
     else
         body<ST, K1, K2, ZF, GM, 32>(smem, g, members, s, i_begin, i_end, chunk_len, JT, JT,
-                                     (int)blockIdx.x * Main::TX, sc, &tm_w, &tm_p, &tm_f);
+                                     (int)blockIdx.x * Main::TX, rw, sc, &tm_w, &tm_p, &tm_f);
 }
 
 }  // namespace t3

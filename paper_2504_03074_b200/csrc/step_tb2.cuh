@@ -57,7 +57,8 @@ constexpr size_t tb2_smem_bytes() {
 template <int TX, int BY, int ST, bool A1, int K1, int K2, bool ZF, bool TENSOR, int GM = 0>
 __global__ void __launch_bounds__(Lay<TX, BY, A1>::THREADS)
     tb2_kernel(Geom g, const Member *__restrict__ members, int member_off, int s, int i_begin, int i_end,
-               int chunk_len, int JT, int part_off, const __grid_constant__ CUtensorMap tm_w,
+               int chunk_len, int JT, int part_off, int j_off, int j_end,
+               const __grid_constant__ CUtensorMap tm_w,
                const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_f,
                const __grid_constant__ CUtensorMap tm_a) {
     using L = Lay<TX, BY, A1>;
@@ -74,7 +75,7 @@ __global__ void __launch_bounds__(Lay<TX, BY, A1>::THREADS)
     const int jt = blockIdx.y % JT;
     const int ch = blockIdx.y / JT;
     const int k0 = blockIdx.x * TX;
-    const int j0 = A1 ? jt * BY : 0;
+    const int j0 = A1 ? j_off + jt * BY : 0;  // (j_off, j_end): row window of the launch, see t3::RowWin
     const int i0 = i_begin + ch * chunk_len;
     const int i1 = min(i_end, i0 + chunk_len);
     if (i0 >= i1) {
@@ -143,6 +144,8 @@ __global__ void __launch_bounds__(Lay<TX, BY, A1>::THREADS)
     const bool row_ok = !A1 || (j >= g.j_lo && j < g.j_hi);
     const bool ok0 = row_ok && (k >= 1) && (k < g.n2 - 1);
     const bool ok1 = row_ok && (k + 1 < g.n2 - 1);
+    const bool st0 = ok0 && (j < j_end);  // stored (ok0 / ok1 also keep W^{s+1} on rows past the window)
+    const bool st1 = ok1 && (j < j_end);
     // ext-ring item of this thread (3D: top/bottom row pairs, then left/right singles; 2D: 2 singles)
     int r_ey = 0, r_ex = 0;
     bool r_pair = false, r_any = false;
@@ -186,7 +189,7 @@ __global__ void __launch_bounds__(Lay<TX, BY, A1>::THREADS)
     };
 
     // last pass: v of the next output plane is loaded one iteration ahead (hides its HBM latency)
-    const bool want_v = (K2 == K_LAST) && m.out_mode != WHB_OUT_PLAIN && row_ok && (ok0 || ok1);
+    const bool want_v = (K2 == K_LAST) && m.out_mode != WHB_OUT_PLAIN && row_ok && (st0 || st1);
     const long long pbase = (long long)j * P + k;
     double2 vcur = make_double2(0.0, 0.0);
     // register queues along axis 0 for the main pair: W^s at planes i-1, i and W^{s+1} at
@@ -288,34 +291,34 @@ __global__ void __launch_bounds__(Lay<TX, BY, A1>::THREADS)
             }
             const long long p = (long long)ip * S0 + (long long)j * P + k;
             if (K2 == K_MID) {
-                if (ok0 && ok1) {
+                if (st0 && st1) {
                     *reinterpret_cast<double2 *>(w1g + p) = e_c;
                     *reinterpret_cast<double2 *>(w2g + p) = make_double2(n0, n1);
                     *reinterpret_cast<double2 *>(m.acc + p) = make_double2(a0, a1);
                 } else {
-                    if (ok0) { w1g[p] = e_c.x; w2g[p] = n0; m.acc[p] = a0; }
-                    if (ok1) { w1g[p + 1] = e_c.y; w2g[p + 1] = n1; m.acc[p + 1] = a1; }
+                    if (st0) { w1g[p] = e_c.x; w2g[p] = n0; m.acc[p] = a0; }
+                    if (st1) { w1g[p + 1] = e_c.y; w2g[p + 1] = n1; m.acc[p + 1] = a1; }
                 }
             } else {
                 const double o0 = whb_mul(m.out_scale, a0);
                 const double o1 = whb_mul(m.out_scale, a1);
                 if (m.out_mode == WHB_OUT_FPI) {
-                    if (ok0) {
+                    if (st0) {
                         const double d0 = o0 - vcur.x;
                         rsum += d0 * d0;
                         m.v[p] = o0;
                     }
-                    if (ok1) {
+                    if (st1) {
                         const double d1 = o1 - vcur.y;
                         rsum += d1 * d1;
                         m.v[p + 1] = o1;
                     }
                 } else if (m.out_mode == WHB_OUT_AV) {
-                    if (ok0) m.dst[p] = whb_sub(vcur.x, o0);
-                    if (ok1) m.dst[p + 1] = whb_sub(vcur.y, o1);
+                    if (st0) m.dst[p] = whb_sub(vcur.x, o0);
+                    if (st1) m.dst[p + 1] = whb_sub(vcur.y, o1);
                 } else {
-                    if (ok0) m.dst[p] = o0;
-                    if (ok1) m.dst[p + 1] = o1;
+                    if (st0) m.dst[p] = o0;
+                    if (st1) m.dst[p + 1] = o1;
                 }
             }
         }

@@ -29,6 +29,8 @@
 #include "nccl.h"
 
 #include <algorithm>
+#include <chrono>
+#include <climits>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -595,6 +597,47 @@ __global__ void repitch_kernel(double *stage, int n, double *field, int P, long 
     }
 }
 
+// Rows [ja, jb) of every owned plane between the contiguous staging copy of a host field
+// (planes, n1, n2) and the pitched device field.  dir 1: stage -> field, Dirichlet boundary points
+// and the row padding written as 0 (what zero_boundary_kernel does after a whole-field upload);
+// dir 0: field -> stage.
+__global__ void band_repitch_kernel(double *stage, double *field, int n0, int n1, int n2, int P, long long S0,
+                                    int ja, int jb, int dir) {
+    const int w = dir ? P : n2;
+    const long long per_plane = (long long)(jb - ja) * w;
+    const long long total = per_plane * n0;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long pl = t / per_plane;
+        const long long r = t - pl * per_plane;
+        const int j = ja + (int)(r / w);
+        const int k = (int)(r - (long long)(j - ja) * w);
+        const long long fo = pl * S0 + (long long)j * P + k;
+        const long long so = (pl * n1 + j) * n2 + k;
+        if (dir) {
+            const bool in = k >= 1 && k < n2 - 1 && j >= 1 && j < n1 - 1 && pl >= 1 && pl < n0 - 1;
+            field[fo] = in ? stage[so] : 0.0;
+        } else {
+            stage[so] = field[fo];
+        }
+    }
+}
+
+// Dirichlet boundary points and row padding of rows [ja, jb) of every owned plane := 0 (one thread
+// per row: the two end segments, or the whole row on a boundary row / plane).
+__global__ void band_zero_kernel(double *field, int n0, int n1, int n2, int P, long long S0, int ja, int jb) {
+    const long long total = (long long)(jb - ja) * n0;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int pl = (int)(t / (jb - ja));
+        const int j = ja + (int)(t - (long long)pl * (jb - ja));
+        double *row = field + pl * S0 + (long long)j * P;
+        const bool whole = j == 0 || j == n1 - 1 || pl == 0 || pl == n0 - 1;
+        row[0] = 0.0;
+        for (int k = whole ? 1 : n2 - 1; k < P; ++k) row[k] = 0.0;
+    }
+}
+
 // Write a scratch buffer larger than L2 so the next timed pass starts cold.
 __global__ void l2_flush_kernel(double *buf, long long n, double val) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -762,6 +805,9 @@ struct whb_ctx {
     bool t3 = false;
     size_t smem3 = 0;
     int gx3 = 1, JT3 = 1, JTE3 = 1, lxe3 = 32, chunk3 = 1, nch3 = 1;
+    // row window of the next t3 / tb2 launches (the banded host iteration; whole grid: 0, INT_MAX, 0)
+    int win_j0 = 0, win_j1 = INT_MAX, win_po = 0;
+    int win_lxe = 0;  // edge tile shape of the windowed launches (0: lxe3)
     // cluster-resident small-grid 2D plan (whole grid in one cluster's shared memory)
     bool cres = false;
     int cres_cl = 0, cres_r = 0, cres_ppt = 1;
@@ -780,6 +826,9 @@ struct whb_ctx {
     // timing
     bool timing = false;
     std::vector<cudaEvent_t> ev;
+    // banded host iteration (whb_iterate_host on the three-step plan): copy-in / copy-out streams
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    std::vector<cudaEvent_t> ev_band;
     double t_step_ms = 0.0;
     int64_t t_step_launches = 0;
     double t_solve_ms = 0.0;
@@ -1278,6 +1327,8 @@ int plan_launch(whb_ctx *c) {
         c->lxe3 = (rem == 0 || (e3 && std::string(e3) == "0")) ? 32 : t3::edge_lx(rem);
         c->smem3 = t3_smem(c->lxe3);
         cudaError_t e = t3_set_attrs(c->lxe3, c->smem3);
+        // (the banded host iteration picks a wider, shorter edge shape per band height)
+        for (int lx = c->lxe3 * 2; lx <= 16 && c->lxe3 != 32 && e == cudaSuccess; lx *= 2) e = t3_set_attrs(lx, t3_smem(lx));
         if (e != cudaSuccess) return fail(WHB_E_CUDA, std::string("cudaFuncSetAttribute(t3): ") + cudaGetErrorString(e));
         int nb = 0;
         t3_by_lxe(c->lxe3, [&](auto lx) {
@@ -1301,7 +1352,8 @@ int plan_launch(whb_ctx *c) {
         c->nch3 = (nplanes + c->chunk3 - 1) / c->chunk3;
         c->t3 = ((long long)c->JT3 * c->nch3 <= 65535) &&
                 (c->chunk3 >= 48 || (t3env && std::string(t3env) == "1"));
-        if (c->t3) c->nparts = std::max(c->nparts, c->gx3 * c->JT3 * c->nch3);
+        // (the banded host iteration launches one wave of CTAs per band of 12 rows and pass)
+        if (c->t3) c->nparts = std::max(c->nparts, std::max(c->gx3 * c->JT3 * c->nch3, c->JT3 * 2 * sms));
     }
     c->nring = (c->wfT == 4 || c->t3) ? 6 : 4;
     // cluster-resident plan (whole-grid 2D with the fields in one cluster's shared memory; the
@@ -1545,7 +1597,8 @@ void launch_tb2(whb_ctx *c, dim3 grid, int off, int s, int ib, int ie, int cl, i
     constexpr int threads = A1 ? T3_TX * T3_BY / 2 : T2_TX * T2_BY / 2;
     auto go = [&](auto gm) {
         tb2_fn<A1, K1, K2, ZF, decltype(gm)::value>()<<<grid, threads, c->smem2, c->stream>>>(
-            c->geom, c->d_members, off, s, ib, ie, cl, c->JT2, po, mp.w, mp.p, mp.f, mp.a);
+            c->geom, c->d_members, off, s, ib, ie, cl, (int)(grid.y / ((ie - ib + cl - 1) / cl)), po, c->win_j0,
+            c->win_j1, mp.w, mp.p, mp.f, mp.a);
     };
     const int gm = geom_mode(c);
     if (gm == 2) go(std::integral_constant<int, 2>{});
@@ -1595,7 +1648,12 @@ int launch_pair_range(whb_ctx *c, int s, int ib, int ie, int cl, int po) {
     const int k1 = (s == 0) ? K_FIRST : K_MID;
     auto go = [&](int k2, int off, int cnt) {
         if (cnt <= 0) return;
-        dim3 grid(c->gx2, c->JT2 * nch, cnt);
+        int jt2 = c->JT2;
+        if (c->win_j1 != INT_MAX && c->act1) {  // row window (banded host iteration)
+            const int rows = std::min(c->win_j1, (int)c->gshape[1] - 1) - c->win_j0;
+            jt2 = (std::max(rows, 1) + T3_BY - 1) / T3_BY;
+        }
+        dim3 grid(c->gx2, jt2 * nch, cnt);
         if (c->act1) launch_tb2_kinds<true>(c, k1, k2, zf, grid, off, s, ib, ie, cl, po, mp);
         else launch_tb2_kinds<false>(c, k1, k2, zf, grid, off, s, ib, ie, cl, po, mp);
         c->launches++;
@@ -1622,8 +1680,9 @@ int launch_t3(whb_ctx *c, int s, bool last, int ib, int ie, int cl) {
     WHB_TRY(tensor_map(c, level_ptr(m0, s - 1), SM::LW, SM::NR, &tp));
     if (m0.f) WHB_TRY(tensor_map(c, m0.f, SM::LW, SM::NR, &tf));
     ew = tw, ep = tp, ef = tf;
-    if (c->lxe3 != 32) {  // boxes of the ragged-edge shape
-        const int lw = 2 * c->lxe3, nr = 16 * (32 / c->lxe3);
+    const int lxe_ = (c->win_j1 != INT_MAX && c->win_lxe) ? c->win_lxe : c->lxe3;
+    if (lxe_ != 32) {  // boxes of the ragged-edge shape
+        const int lw = 2 * lxe_, nr = 16 * (32 / lxe_);
         WHB_TRY(tensor_map(c, level_ptr(m0, s), lw + 4, nr + 2, &ew));
         WHB_TRY(tensor_map(c, level_ptr(m0, s - 1), lw, nr, &ep));
         if (m0.f) WHB_TRY(tensor_map(c, m0.f, lw, nr, &ef));
@@ -1641,13 +1700,24 @@ int launch_t3(whb_ctx *c, int s, bool last, int ib, int ie, int cl) {
     sc.c3 = mh.h_acc[s + 3];
     sc.osc = mh.out_scale;
     const int nch = (ie - ib + cl - 1) / cl;
-    dim3 grid(c->gx3, c->JT3 * nch, 1);
+    // row tiles of the launch: the whole grid, or the row window [win_j0, win_j1)
+    int jt = c->JT3, jte = c->JTE3;
+    const int lxe = (c->win_j1 != INT_MAX && c->win_lxe) ? c->win_lxe : c->lxe3;
+    if (c->win_j1 != INT_MAX) {
+        const int rows = std::min(c->win_j1, (int)c->gshape[1] - 1) - c->win_j0;
+        if (rows <= 0) return 0;
+        const int bye = 16 * (32 / lxe) - 4;
+        jt = (rows + t3::BY - 1) / t3::BY;
+        jte = (rows + bye - 1) / bye;
+    }
+    dim3 grid(c->gx3, jt * nch, 1);
+    const t3::RowWin rw{c->win_j0, c->win_j1, c->win_po};
     const int gm = geom_mode(c);
     auto go = [&](auto k1, auto k2, auto zft, auto gmt) {
-        t3_by_lxe(c->lxe3, [&](auto lx) {
+        t3_by_lxe(lxe, [&](auto lx) {
             t3_fn<decltype(k1)::value, decltype(k2)::value, decltype(zft)::value, decltype(gmt)::value,
-                  decltype(lx)::value>()<<<grid, S3_THREADS, c->smem3, c->stream>>>(
-                c->geom, c->d_members, s, ib, ie, cl, c->JT3, c->JTE3, sc, tw, tp, tf, ew, ep, ef);
+                  decltype(lx)::value>()<<<grid, S3_THREADS, t3_smem(lxe), c->stream>>>(
+                c->geom, c->d_members, s, ib, ie, cl, jt, jte, rw, sc, tw, tp, tf, ew, ep, ef);
         });
     };
     using KF = std::integral_constant<int, K_FIRST>;
@@ -2452,6 +2522,9 @@ int whb_destroy(whb_ctx *c) {
     cudaFree(c->d_mgs);
     if (c->h_mgs) cudaFreeHost(c->h_mgs);
     for (auto e : c->ev) cudaEventDestroy(e);
+    for (auto e : c->ev_band) cudaEventDestroy(e);
+    if (c->s_in) cudaStreamDestroy(c->s_in);
+    if (c->s_out) cudaStreamDestroy(c->s_out);
     if (c->nccl) nccl_comm_destroy(c->nccl);
     cudaFree(c->d_nccl);
     if (c->comm) {
@@ -2721,11 +2794,207 @@ int whb_fpi_scaled(whb_ctx *c, int iters, double tol, double root_n, double *res
     return fpi_impl(c, iters, -1.0, resid_sq_out, iters_done, tol, root_n);
 }
 
+// whb_iterate_host on the three-step plan (whole-grid 3D, Dirichlet): the host transfers are hidden
+// behind the passes.  The grid is cut into bands of rows (axis 1; a multiple of the 12-row tiles).
+// Band b of v is uploaded on a copy-in stream (one strided copy + a re-pitch kernel that also
+// zeroes the boundary); on the context stream the (pass p, band b) launches are enqueued by
+// diagonals d = p + b, passes ascending inside a diagonal.  Pass p on band b reads what pass p-1
+// wrote on bands b-1, b, b+1 (a k-step pass reaches k <= 3 rows past its band) -- diagonals
+// d-2, d-1 and, earlier in the same diagonal, (p-1, b+1); a level-ring slot written by (q, b) was
+// last read by (q-2, b+1) at most, an earlier diagonal.  Band b of the new v leaves on a copy-out
+// stream as soon as the last pass has run on it.  Per launch: one wave of CTAs (17 x 1 x nch main
+// tiles + the edge tiles <= 148 SMs), axis-0 chunks chosen for that.  The passes are the plan's
+// (three-step passes, then one or two two-step passes for the remainder); every step is the same
+// arithmetic as in the whole-grid launches, so the iterate is bitwise the same, and the residual
+// sums the same squares in another order.  WHB_PIPE=0 keeps the serial path (upload, solve graph,
+// download); WHB_PIPE_ROWS sets the band height in tiles.
+int iterate_host_banded(whb_ctx *c, const double *v_host, double *v_out_host, double *resid_sq, bool *done) {
+    *done = false;
+    static const bool off = getenv("WHB_PIPE") && std::string(getenv("WHB_PIPE")) == "0";
+    const int ns = max_steps(c);
+    const int n0 = (int)c->gshape[0], n1 = (int)c->gshape[1], n2 = (int)c->gshape[2];
+    if (off || !c->t3 || !c->tb2 || c->kern != 2 || c->nbatch != 1 || !c->act0 || !c->act1 || ns < 9 ||
+        c->plane_begin != 0 || c->plane_end != c->gshape[0] || (int)c->nloc != n0 || cres_smem(c) || c->wfT)
+        return 0;
+    // passes: three steps while the remainder stays 0, 2 or 4; then two-step passes
+    struct Pass { int s, k; };
+    std::vector<Pass> passes;
+    int s = 0;
+    while (ns - s >= 3 && (ns - s - 3) != 1) { passes.push_back({s, 3}); s += 3; }
+    while (ns - s >= 2) { passes.push_back({s, 2}); s += 2; }
+    if (s != ns) return 0;
+    const int NP = (int)passes.size();
+    // bands of `bt` tile rows; axis-0 chunks so that a launch is one wave of CTAs
+    int bt = 2;  // measured on config 4 (e2e Gpts/s): 1 -> 154, 2 -> 180, 4 -> 164, 8 -> 125; serial path 129
+    if (const char *e = getenv("WHB_PIPE_ROWS")) bt = std::max(1, atoi(e));
+    const int rows_total = n1 - 1;  // rows 0 .. n1-2 carry tiles (row 0 and n1-1 are Dirichlet)
+    const int NB = (rows_total + bt * t3::BY - 1) / (bt * t3::BY);
+    if (NB < 2) return 0;
+    int sms = 0;
+    WHB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+    // edge tile shape of a band: a one-wave launch lasts as long as its slowest CTA, and the 124 x 4
+    // shape stages 386 box rows per plane (the main shape 50): take the widest shape that still covers
+    // the band's rows with one tile (28 x 28, 60 x 12, 124 x 4); WHB_PIPE_LXE forces one
+    int lxb = c->lxe3;
+    if (lxb != 32) {
+        const int rows = bt * t3::BY;
+        lxb = rows <= t3::Shape<16>::BY ? 16 : rows <= t3::Shape<8>::BY ? 8 : 4;
+        lxb = std::max(lxb, c->lxe3);  // not narrower than the remainder needs
+        if (const char *e = getenv("WHB_PIPE_LXE")) {
+            const int v = atoi(e);
+            if ((v == 4 || v == 8 || v == 16) && v >= c->lxe3) lxb = v;
+        }
+    }
+    const int edge_by = lxb == 32 ? t3::BY : 16 * (32 / lxb) - 4;
+    const int per3 = (c->gx3 - (lxb != 32 ? 1 : 0)) * bt + (lxb != 32 ? (bt * t3::BY + edge_by - 1) / edge_by : 0);
+    const int nch3 = std::max(1, sms / std::max(1, per3));
+    const int nch2 = std::max(1, sms / std::max(1, c->gx2 * ((bt * t3::BY + T3_BY - 1) / T3_BY)));
+    const int npl = c->upd_hi - c->upd_lo;
+    const int cl3 = (npl + nch3 - 1) / nch3, cl2 = (npl + nch2 - 1) / nch2;
+    // residual partial slots: the last pass writes one per CTA and band
+    const Pass &lastp = passes.back();
+    const int per_band_parts = lastp.k == 3 ? c->gx3 * bt * ((npl + cl3 - 1) / cl3)
+                                            : c->gx2 * ((bt * t3::BY + T3_BY - 1) / T3_BY) * ((npl + cl2 - 1) / cl2);
+    if ((long long)per_band_parts * NB > c->nparts) return 0;
+    if (!c->s_in) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);  // the small copy kernels go first when an SM frees up
+        WHB_CUDA(cudaStreamCreateWithPriority(&c->s_in, cudaStreamNonBlocking, hi));
+        WHB_CUDA(cudaStreamCreateWithPriority(&c->s_out, cudaStreamNonBlocking, hi));
+    }
+    while ((int)c->ev_band.size() < 2 * NB + 1) {
+        cudaEvent_t e;
+        WHB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->ev_band.push_back(e);
+    }
+    WHB_TRY(ensure_hist(c, 1));
+    WHB_TRY(upload_members(c, WHB_OUT_FPI, 0));
+    WHB_CUDA(cudaMemsetAsync(c->d_counter, 0, sizeof(int), c->stream));
+    c->cur_zf = 0;
+    double *v = c->mem[0].v;
+    const size_t hpitch = (size_t)n1 * n2 * sizeof(double);
+    auto band = [&](int b, int &ja, int &jb) {
+        ja = b * bt * t3::BY;
+        jb = b == NB - 1 ? n1 : std::min(n1, (b + 1) * bt * t3::BY);  // copies: the last band takes row n1-1 too
+    };
+    // host <-> pitched device rows: one 3D copy per band (copy engines only), or WHB_PIPE_COPY=stage:
+    // a contiguous copy into the staging field + a re-pitch kernel
+    static const bool direct = !(getenv("WHB_PIPE_COPY") && std::string(getenv("WHB_PIPE_COPY")) == "stage");
+    auto copy_band = [&](double *host, int ja, int jb, bool h2d, cudaStream_t st) -> int {
+        cudaMemcpy3DParms q = {};
+        cudaPitchedPtr hp = make_cudaPitchedPtr(host, (size_t)n2 * sizeof(double), (size_t)n2, (size_t)n1);
+        cudaPitchedPtr dp = make_cudaPitchedPtr(owned(v, c), (size_t)c->P * sizeof(double), (size_t)n2, (size_t)n1);
+        q.srcPtr = h2d ? hp : dp;
+        q.dstPtr = h2d ? dp : hp;
+        q.srcPos = make_cudaPos(0, (size_t)ja, 0);
+        q.dstPos = make_cudaPos(0, (size_t)ja, 0);
+        q.extent = make_cudaExtent((size_t)n2 * sizeof(double), (size_t)(jb - ja), (size_t)n0);
+        q.kind = h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+        WHB_CUDA(cudaMemcpy3DAsync(&q, st));
+        return 0;
+    };
+    if (!direct) WHB_TRY(ensure_stage(c));
+    cudaEvent_t ev0 = c->ev_band[2 * NB];
+    static const bool trace = getenv("WHB_PIPE_TRACE") != nullptr;  // stderr: upload / compute / download end times
+    cudaEvent_t tev[4] = {};
+    if (trace) {
+        for (auto &e : tev) WHB_CUDA(cudaEventCreate(&e));
+        WHB_CUDA(cudaEventRecord(tev[0], c->stream));
+    }
+    WHB_CUDA(cudaEventRecord(ev0, c->stream));
+    WHB_CUDA(cudaStreamWaitEvent(c->s_in, ev0, 0));
+    WHB_CUDA(cudaStreamWaitEvent(c->s_out, ev0, 0));
+    for (int b = 0; b < NB; ++b) {
+        int ja, jb;
+        band(b, ja, jb);
+        if (direct) {
+            WHB_TRY(copy_band(const_cast<double *>(v_host), ja, jb, true, c->s_in));
+            band_zero_kernel<<<74, 256, 0, c->s_in>>>(owned(v, c), n0, n1, n2, c->P, c->S0, ja, jb);
+        } else {
+            WHB_CUDA(cudaMemcpy2DAsync(c->stage + (size_t)ja * n2, hpitch, v_host + (size_t)ja * n2, hpitch,
+                                       (size_t)(jb - ja) * n2 * sizeof(double), n0, cudaMemcpyHostToDevice, c->s_in));
+            band_repitch_kernel<<<296, 256, 0, c->s_in>>>(c->stage, owned(v, c), n0, n1, n2, c->P, c->S0, ja, jb, 1);
+        }
+        c->launches++;
+        WHB_CUDA(cudaGetLastError());
+        WHB_CUDA(cudaEventRecord(c->ev_band[b], c->s_in));
+    }
+    if (trace) WHB_CUDA(cudaEventRecord(tev[1], c->s_in));
+    const auto h0 = std::chrono::steady_clock::now();
+    int rc = 0;
+    for (int d = 0; d < NB + NP - 1 && !rc; ++d) {
+        for (int p = 0; p < NP && !rc; ++p) {
+            const int b = d - p;
+            if (b < 0 || b >= NB) continue;
+            if (p == 0) WHB_CUDA(cudaStreamWaitEvent(c->stream, c->ev_band[std::min(b + 1, NB - 1)], 0));
+            const bool last = (p == NP - 1);
+            c->win_j0 = b * bt * t3::BY;
+            c->win_j1 = b == NB - 1 ? n1 : (b + 1) * bt * t3::BY;
+            c->win_po = last ? b * per_band_parts : 0;
+            c->win_lxe = lxb;
+            if (passes[p].k == 3) rc = launch_t3(c, passes[p].s, last, c->upd_lo, c->upd_hi, cl3);
+            else rc = launch_pair_range(c, passes[p].s, c->upd_lo, c->upd_hi, cl2, c->win_po);
+            if (last && !rc) {
+                int ja, jb;
+                band(b, ja, jb);
+                WHB_CUDA(cudaEventRecord(c->ev_band[NB + b], c->stream));
+                WHB_CUDA(cudaStreamWaitEvent(c->s_out, c->ev_band[NB + b], 0));
+                if (direct) {
+                    WHB_TRY(copy_band(v_out_host, ja, jb, false, c->s_out));
+                } else {
+                    band_repitch_kernel<<<296, 256, 0, c->s_out>>>(c->stage, owned(v, c), n0, n1, n2, c->P, c->S0, ja,
+                                                                   jb, 0);
+                    c->launches++;
+                    WHB_CUDA(cudaGetLastError());
+                    WHB_CUDA(cudaMemcpy2DAsync(v_out_host + (size_t)ja * n2, hpitch, c->stage + (size_t)ja * n2,
+                                               hpitch, (size_t)(jb - ja) * n2 * sizeof(double), n0,
+                                               cudaMemcpyDeviceToHost, c->s_out));
+                }
+            }
+        }
+    }
+    c->win_j0 = 0;
+    c->win_j1 = INT_MAX;
+    c->win_po = 0;
+    c->win_lxe = 0;
+    if (rc) {
+        cudaStreamSynchronize(c->s_in);
+        cudaStreamSynchronize(c->stream);
+        cudaStreamSynchronize(c->s_out);
+        return rc;
+    }
+    reduce_partials_kernel<<<1, 1024, 0, c->stream>>>(c->d_members, 1, per_band_parts * NB, c->d_hist, c->d_counter);
+    c->launches++;
+    WHB_CUDA(cudaGetLastError());
+    if (resid_sq) WHB_CUDA(cudaMemcpyAsync(resid_sq, c->d_hist, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    const double host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+    if (trace) {
+        WHB_CUDA(cudaEventRecord(tev[2], c->stream));
+        WHB_CUDA(cudaEventRecord(tev[3], c->s_out));
+    }
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
+    WHB_CUDA(cudaStreamSynchronize(c->s_out));
+    if (trace) {
+        float up = 0.f, comp = 0.f, down = 0.f;
+        cudaEventElapsedTime(&up, tev[0], tev[1]);
+        cudaEventElapsedTime(&comp, tev[0], tev[2]);
+        cudaEventElapsedTime(&down, tev[0], tev[3]);
+        fprintf(stderr, "[whb banded] bands %d x passes %d: upload done %.1f ms, passes done %.1f ms, download done %.1f ms; "
+                "host enqueue of the passes %.1f ms (chunks of %d planes)\n", NB, NP, up, comp, down, host_ms, cl3);
+        for (auto &e : tev) cudaEventDestroy(e);
+    }
+    *done = true;
+    return 0;
+}
+
 int whb_iterate_host(whb_ctx *c, const double *v_host, double *v_out_host, double *resid_sq) {
     if (!c || !v_host || !v_out_host) return fail(WHB_E_ARG, "NULL argument");
     if (c->nbatch != 1) return fail(WHB_E_ARG, "whb_iterate_host needs nbatch == 1");
     WHB_TRY(set_dev(c));
     WHB_TRY(check_ready(c));
+    bool banded = false;
+    WHB_TRY(iterate_host_banded(c, v_host, v_out_host, resid_sq, &banded));
+    if (banded) return 0;
     WHB_TRY(ensure_hist(c, 1));
     WHB_TRY(upload_members(c, WHB_OUT_FPI, 0));
     WHB_TRY(copy_field_h2d(c, c->mem[0].v, v_host));

@@ -116,3 +116,67 @@ def test_three_step_kernel_fpi_matvec_geometry_modes(gpu_available):
     for cells, c, nt, vmis, rerr, avmis, plan in json.loads(r.stdout.strip().splitlines()[-1]):
         assert plan[1] == 3, plan
         assert vmis == 0 and avmis == 0 and rerr <= 1e-12, (cells, c, nt, vmis, avmis, rerr)
+
+
+BAND_SCRIPT = r"""
+import json, sys, numpy as np
+sys.path.insert(0, %(root)r)
+import paper_2504_03074_b200 as wh
+from paper_2504_03074_b200 import timestep as ts
+from oracle import native as ON, waveholtz_oracle as O
+ts._COURANT[2] = 0.9
+out = []
+# N_t mod 3 = 0 / 1 / 2 (last pass: three-step kernel / two two-step passes / one two-step pass)
+for cells, omega in [((40, 100, 130), 12.0), ((48, 30, 200), 8.0), ((64, 64, 64), 11.0), ((33, 50, 33), 13.0),
+                     ((36, 61, 70), 11.0)]:
+    g = wh.build_grid(3, [(0.0, 1.0)] * 3, list(cells), "dirichlet")
+    f = wh.multi_gaussian_source(g, omega, 3, seed=4)
+    corr = wh.correct_explicit(omega, g, 2, 1.0)
+    sc = O.step_scalars(corr.steps_per_period, corr.dt, corr.omega_tilde)
+    prob = wh.HelmholtzProblem(g, 2, 1.0, omega, f)
+    cfg = wh.FilterConfig(omega=omega, periods=1, steps_per_period=corr.steps_per_period, mode="explicit")
+    step = wh.HostFPIStep(prob, cfg)
+    rng = np.random.default_rng(5)
+    a = rng.standard_normal(g.shape) * 1e-3      # nonzero boundary values: the upload must zero them
+    b = np.full(g.shape, np.nan)
+    ref = np.array(wh.GridField.from_values(g, a).values)
+    mis, rerr, launches = 0, 0.0, []
+    for it in range(3):
+        l0 = step.dp.ctx.launch_count()
+        d = step(a, b)
+        launches.append(step.dp.ctx.launch_count() - l0)
+        new = ON.wave_solve(ref, np.array(f.values), g.spacing, sc)
+        dref = float(np.sqrt(np.sum((new - ref) ** 2)) / np.sqrt(g.size))
+        mis += int(np.sum(b != new))
+        rerr = max(rerr, abs(d - dref) / dref)
+        ref = new
+        a, b = b, a      # feed the iterate back (the reference's _iterate loop)
+    out.append([list(cells), corr.steps_per_period, mis, rerr, launches, list(step.dp.ctx.plan())])
+    wh.release_device_cache()
+print(json.dumps(out))
+"""
+
+
+@pytest.mark.parametrize("env", [{}, {"WHB_PIPE_ROWS": "3"}, {"WHB_PIPE": "0"}, {"WHB_T3_EDGE": "0"}])
+def test_banded_host_iteration_bitwise(gpu_available, env):
+    """whb_iterate_host on the three-step plan hides the host transfers behind (pass, row band)
+    launches enqueued by diagonals: v_new bitwise equal to the C restatement for 3 chained
+    iterations (every remainder of N_t mod 3, ragged bands, every edge tile shape), the residual
+    to 1e-12; WHB_PIPE=0 is the serial path."""
+    e = dict(os.environ, WHB_T3="1", **env)
+    r = subprocess.run([sys.executable, "-c", BAND_SCRIPT % {"root": ROOT}], capture_output=True, text=True, env=e,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    assert {nt % 3 for _, nt, *_ in res} == {0, 1, 2}, res
+    banded = 0
+    for cells, nt, mis, rerr, launches, plan in res:
+        assert plan[1] == 3, plan
+        assert mis == 0, (env, cells, nt, launches)
+        assert rerr < 1e-12, (env, cells, rerr)
+        passes = (nt + 2) // 3
+        if env.get("WHB_PIPE") == "0":
+            assert max(launches) < 2 * passes, launches
+        banded += min(launches) >= 2 * passes  # one launch per pass and band (>= 2 bands)
+    if env.get("WHB_PIPE") != "0":  # the banded path really ran (grids of one band keep the serial path)
+        assert banded >= (3 if "WHB_PIPE_ROWS" in env else 5), res
