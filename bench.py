@@ -349,7 +349,8 @@ class SingleRun:
         for b in bufs:
             b.free()
         return te, {"h2d_bytes_per_step": self.npts * 8, "d2h_bytes_per_step": self.npts * 8 + 8,
-                    "api": "paper_2504_03074_b200.HostFPIStep (C ABI whb_iterate_host), pinned host buffers"}
+                    "api": "paper_2504_03074_b200.HostFPIStep (C ABI whb_iterate_host), pinned host buffers; on the "
+                           "three-step plan v moves in bands of rows on copy streams behind the (pass, band) launches"}
 
     def e2e_seam(self, K, dist):
         """The reference-facing Python seam: v = wave_solve_filtered(v, f, cfg, corr, op) with host
@@ -362,7 +363,8 @@ class SingleRun:
 
         op = wh.DiscreteOperator(self.g, self.order, 1.0)
         v = wh.GridField.zeros(self.g)
-        wh.wave_solve_filtered(v, self.f, self.cfg, self.corr, op)  # warm (forcing cached by generation)
+        for _ in range(2):  # warm: forcing cached by generation, two page-locked fields in the pool
+            v = wh.wave_solve_filtered(v, self.f, self.cfg, self.corr, op)
         barrier(dist)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -371,7 +373,8 @@ class SingleRun:
         te = time.perf_counter() - t0
         return te, {"h2d_bytes_per_step": self.npts * 8, "d2h_bytes_per_step": self.npts * 8,
                     "api": "paper_2504_03074_b200.wave_solve_filtered(GridField v, GridField f, ...) -> new "
-                           "GridField (pageable host fields, strided copies straight into the new field)"}
+                           "GridField (C ABI whb_solve_host; the fields' buffers are recycled page-locked memory, "
+                           "copied in bands of rows behind the passes on the three-step plan)"}
 
     def e2e_solve(self, K, dist):
         """The fpi_solve call through the C ABI with host buffers: f copied in from pinned memory,

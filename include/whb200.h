@@ -156,6 +156,19 @@ int whb_fpi_scaled(whb_ctx *ctx, int iters, double tol, double root_n, double *r
  * (driver.py:222-225) with host GridFields. */
 int whb_iterate_host(whb_ctx *ctx, const double *v_host, double *v_out_host, double *resid_sq);
 
+/* wave_solve_filtered (timestep.py:250-301) with host fields on both sides, member 0: v_host ->
+ * device, one filtered solve in `out_mode` (WHB_OUT_PLAIN: W(v, f); WHB_OUT_AV: v - W(v, 0), the
+ * mat-vec of driver.py:262-267; WHB_OUT_FPI: as whb_iterate_host), result -> out_host.  Both host
+ * fields are strided views as in whb_upload_strided (element strides of planes and rows; a
+ * reference GridField's ghost-padded buffer is such a view).  v_host is not modified unless it
+ * aliases out_host.  On whole-grid 3D problems that run the three-step plan the transfers are
+ * hidden behind the passes: v moves in bands of rows on copy streams while the (pass, band)
+ * launches follow diagonal by diagonal (same arithmetic per point as the whole-grid launches:
+ * the result is bitwise the same); otherwise upload, solve, download in sequence. */
+int whb_solve_host(whb_ctx *ctx, const double *v_host, int64_t v_plane_stride, int64_t v_row_stride,
+                   double *out_host, int64_t out_plane_stride, int64_t out_row_stride, int out_mode,
+                   int zero_forcing, double *resid_sq);
+
 /* ---- Krylov vectors (gmres_solve, linalg.py:102-183; member 0 only) ------
  * Vector ids >= 0 name full-grid device vectors with the field layout.
  * Slots: ids WHB_V..WHB_WD alias the member-0 fields; ids >= 8 are extra

@@ -38,7 +38,7 @@ EXPORTS = (
     "whb_imp_apply", "whb_imp_rhs", "whb_vec_xpay", "whb_mg_setup", "whb_mg_vcycle", "whb_tri_setup", "whb_tri_solve",
     "whb_cg_begin", "whb_cg_iterate", "whb_vec_mgs",
     "whb_comm_begin", "whb_comm_end", "whb_comm_join", "whb_nccl_unique_id", "whb_nccl_init", "whb_nccl_exchange",
-    "whb_nccl_allreduce_sum", "whb_upload_strided", "whb_download_strided",
+    "whb_nccl_allreduce_sum", "whb_upload_strided", "whb_download_strided", "whb_solve_host",
 )
 
 _lib = None
@@ -97,6 +97,7 @@ def load():
                                ctypes.POINTER(c_int)], c_int),
         "whb_nccl_allreduce_sum": ([vp, dp], c_int),
         "whb_iterate_host": ([vp, dp, dp, dp], c_int),
+        "whb_solve_host": ([vp, dp, c_i64, c_i64, dp, c_i64, c_i64, c_int, c_int, dp], c_int),
         "whb_vec_reserve": ([vp, c_int, ctypes.POINTER(c_int)], c_int),
         "whb_vec_upload": ([vp, c_int, dp], c_int),
         "whb_vec_download": ([vp, c_int, dp], c_int),
@@ -408,6 +409,19 @@ class Context:
         v_out = self._out(v_out, "iterate_host v_out")
         r = np.zeros(1)
         check(load().whb_iterate_host(self._h, _dp(v_in), _dp(v_out), _dp(r)), "whb_iterate_host")
+        return float(r[0])
+
+    def solve_host(self, v, out, out_mode=OUT_PLAIN, zero_forcing=False):
+        """One filtered solve with host fields on both sides (whb_solve_host): ``v`` and ``out``
+        are float64 views of the local shape whose last axis is contiguous (e.g. GridField.values
+        and a new field's interior).  Returns resid^2 in FPI mode, else 0."""
+        sv, so = self._strides(v), self._strides(out)
+        if sv is None or so is None or not out.flags.writeable:
+            raise ValueError("solve_host: v / out must be float64 views of the local shape with a contiguous "
+                             "last axis (out writeable)")
+        r = np.zeros(1)
+        check(load().whb_solve_host(self._h, _dp(v), sv[0], sv[1], _dp(out), so[0], so[1], int(out_mode),
+                                    int(bool(zero_forcing)), _dp(r)), "whb_solve_host")
         return float(r[0])
 
     # -- vectors -------------------------------------------------------------------

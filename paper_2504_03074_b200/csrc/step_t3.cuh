@@ -419,6 +419,8 @@ __device__ __forceinline__ void body(double *smem, const Geom &g, const Member *
 }
 
 // LXE: shape of the last column of tiles (blockIdx.x == gridDim.x - 1); 32 = the main shape everywhere.
+// The edge column has its own chunk length: in a one-wave launch (banded host iteration) its spare
+// CTAs take shorter chunks, so the narrow tiles (more box rows per plane) are never the last to end.
 template <int ST, int LXE>
 constexpr size_t smem_bytes() {
     return Main::smem_bytes<ST>() > Shape<LXE>::template smem_bytes<ST>() ? Main::smem_bytes<ST>()
@@ -428,13 +430,14 @@ constexpr size_t smem_bytes() {
 template <int ST, int K1, int K2, bool ZF, int GM, int LXE>
 __global__ void __launch_bounds__(NTHREADS, 1)
     t3_kernel(Geom g, const Member *__restrict__ members, int s, int i_begin, int i_end, int chunk_len, int JT,
-              int JTE, const RowWin rw, const Scal sc, const __grid_constant__ CUtensorMap tm_w,
+              int JTE, int chunk_len_e, const RowWin rw, const Scal sc, const __grid_constant__ CUtensorMap tm_w,
               const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_f,
               const __grid_constant__ CUtensorMap te_w, const __grid_constant__ CUtensorMap te_p,
               const __grid_constant__ CUtensorMap te_f) {
     extern __shared__ __align__(128) double smem[];
     if (LXE != 32 && blockIdx.x == gridDim.x - 1)
-        body<ST, K1, K2, ZF, GM, LXE>(smem, g, members, s, i_begin, i_end, chunk_len, JT, JTE,
+        // the edge column's gridDim.y CTAs: JTE row tiles x chunks of chunk_len_e planes (the rest exit)
+        body<ST, K1, K2, ZF, GM, LXE>(smem, g, members, s, i_begin, i_end, chunk_len_e, JTE, JTE,
                                       (int)blockIdx.x * Main::TX, rw, sc, &te_w, &te_p, &te_f);
     else
         body<ST, K1, K2, ZF, GM, 32>(smem, g, members, s, i_begin, i_end, chunk_len, JT, JT,

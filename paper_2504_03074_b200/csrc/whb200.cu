@@ -597,32 +597,6 @@ __global__ void repitch_kernel(double *stage, int n, double *field, int P, long 
     }
 }
 
-// Rows [ja, jb) of every owned plane between the contiguous staging copy of a host field
-// (planes, n1, n2) and the pitched device field.  dir 1: stage -> field, Dirichlet boundary points
-// and the row padding written as 0 (what zero_boundary_kernel does after a whole-field upload);
-// dir 0: field -> stage.
-__global__ void band_repitch_kernel(double *stage, double *field, int n0, int n1, int n2, int P, long long S0,
-                                    int ja, int jb, int dir) {
-    const int w = dir ? P : n2;
-    const long long per_plane = (long long)(jb - ja) * w;
-    const long long total = per_plane * n0;
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-         t += (long long)gridDim.x * blockDim.x) {
-        const long long pl = t / per_plane;
-        const long long r = t - pl * per_plane;
-        const int j = ja + (int)(r / w);
-        const int k = (int)(r - (long long)(j - ja) * w);
-        const long long fo = pl * S0 + (long long)j * P + k;
-        const long long so = (pl * n1 + j) * n2 + k;
-        if (dir) {
-            const bool in = k >= 1 && k < n2 - 1 && j >= 1 && j < n1 - 1 && pl >= 1 && pl < n0 - 1;
-            field[fo] = in ? stage[so] : 0.0;
-        } else {
-            stage[so] = field[fo];
-        }
-    }
-}
-
 // Dirichlet boundary points and row padding of rows [ja, jb) of every owned plane := 0 (one thread
 // per row: the two end segments, or the whole row on a boundary row / plane).
 __global__ void band_zero_kernel(double *field, int n0, int n1, int n2, int P, long long S0, int ja, int jb) {
@@ -828,6 +802,7 @@ struct whb_ctx {
     std::vector<cudaEvent_t> ev;
     // banded host iteration (whb_iterate_host on the three-step plan): copy-in / copy-out streams
     cudaStream_t s_in = nullptr, s_out = nullptr;
+    std::vector<cudaStream_t> s_band;  // pass launches of band b go to s_band[b % size]
     std::vector<cudaEvent_t> ev_band;
     double t_step_ms = 0.0;
     int64_t t_step_launches = 0;
@@ -1711,13 +1686,19 @@ int launch_t3(whb_ctx *c, int s, bool last, int ib, int ie, int cl) {
         jte = (rows + bye - 1) / bye;
     }
     dim3 grid(c->gx3, jt * nch, 1);
+    // edge column: its jt * nch CTAs as jte row tiles x as many chunks as fit (whole grid: the same chunks)
+    int cle = cl;
+    if (c->win_j1 != INT_MAX && lxe != 32) {
+        const int nche = std::max(1, (jt * nch) / std::max(1, jte));
+        cle = std::max(1, (ie - ib + nche - 1) / nche);
+    }
     const t3::RowWin rw{c->win_j0, c->win_j1, c->win_po};
     const int gm = geom_mode(c);
     auto go = [&](auto k1, auto k2, auto zft, auto gmt) {
         t3_by_lxe(lxe, [&](auto lx) {
             t3_fn<decltype(k1)::value, decltype(k2)::value, decltype(zft)::value, decltype(gmt)::value,
                   decltype(lx)::value>()<<<grid, S3_THREADS, t3_smem(lxe), c->stream>>>(
-                c->geom, c->d_members, s, ib, ie, cl, jt, jte, rw, sc, tw, tp, tf, ew, ep, ef);
+                c->geom, c->d_members, s, ib, ie, cl, jt, jte, cle, rw, sc, tw, tp, tf, ew, ep, ef);
         });
     };
     using KF = std::integral_constant<int, K_FIRST>;
@@ -2525,6 +2506,7 @@ int whb_destroy(whb_ctx *c) {
     for (auto e : c->ev_band) cudaEventDestroy(e);
     if (c->s_in) cudaStreamDestroy(c->s_in);
     if (c->s_out) cudaStreamDestroy(c->s_out);
+    for (auto st : c->s_band) cudaStreamDestroy(st);
     if (c->nccl) nccl_comm_destroy(c->nccl);
     cudaFree(c->d_nccl);
     if (c->comm) {
@@ -2808,7 +2790,12 @@ int whb_fpi_scaled(whb_ctx *c, int iters, double tol, double root_n, double *res
 // arithmetic as in the whole-grid launches, so the iterate is bitwise the same, and the residual
 // sums the same squares in another order.  WHB_PIPE=0 keeps the serial path (upload, solve graph,
 // download); WHB_PIPE_ROWS sets the band height in tiles.
-int iterate_host_banded(whb_ctx *c, const double *v_host, double *v_out_host, double *resid_sq, bool *done) {
+struct HostView {  // a host field as (planes, rows, n2) with element strides (C-contiguous: n1 * n2, n2)
+    double *p;
+    int64_t plane_stride, row_stride;
+};
+
+int solve_host_banded(whb_ctx *c, HostView vin, HostView vout, int out_mode, int zf, double *resid_sq, bool *done) {
     *done = false;
     static const bool off = getenv("WHB_PIPE") && std::string(getenv("WHB_PIPE")) == "0";
     const int ns = max_steps(c);
@@ -2816,6 +2803,8 @@ int iterate_host_banded(whb_ctx *c, const double *v_host, double *v_out_host, do
     if (off || !c->t3 || !c->tb2 || c->kern != 2 || c->nbatch != 1 || !c->act0 || !c->act1 || ns < 9 ||
         c->plane_begin != 0 || c->plane_end != c->gshape[0] || (int)c->nloc != n0 || cres_smem(c) || c->wfT)
         return 0;
+    for (const HostView &h : {vin, vout})  // rows of n2 elements, planes of whole rows (cudaMemcpy3D pitched view)
+        if (h.row_stride < n2 || h.plane_stride % h.row_stride || h.plane_stride < (int64_t)n1 * h.row_stride) return 0;
     // passes: three steps while the remainder stays 0, 2 or 4; then two-step passes
     struct Pass { int s, k; };
     std::vector<Pass> passes;
@@ -2824,66 +2813,108 @@ int iterate_host_banded(whb_ctx *c, const double *v_host, double *v_out_host, do
     while (ns - s >= 2) { passes.push_back({s, 2}); s += 2; }
     if (s != ns) return 0;
     const int NP = (int)passes.size();
-    // bands of `bt` tile rows; axis-0 chunks so that a launch is one wave of CTAs
+    // bands of tile rows: `bt` tiles high, ramping up from one tile at both ends (the pipeline fills
+    // and drains in units of the band height: the first launches wait for the uploads, the last
+    // downloads for the last launches); per band, axis-0 chunks so that a launch is one wave of CTAs
     int bt = 2;  // measured on config 4 (e2e Gpts/s): 1 -> 154, 2 -> 180, 4 -> 164, 8 -> 125; serial path 129
     if (const char *e = getenv("WHB_PIPE_ROWS")) bt = std::max(1, atoi(e));
+    int ramp = 8;  // one-tile bands at each end (then doubling up to bt)
+    if (const char *e = getenv("WHB_PIPE_RAMP")) ramp = std::max(0, atoi(e));
     const int rows_total = n1 - 1;  // rows 0 .. n1-2 carry tiles (row 0 and n1-1 are Dirichlet)
-    const int NB = (rows_total + bt * t3::BY - 1) / (bt * t3::BY);
+    const int tiles_total = (rows_total + t3::BY - 1) / t3::BY;
+    struct Band { int t0, t1, cl3, cl2, lx, po; };
+    std::vector<Band> bands;
+    {
+        std::vector<int> front;  // heights from one end: `ramp` bands of 1, then 2, 4, .. (`ramp` / 2 each) below bt
+        for (int h = 1, n = ramp; h < bt && n > 0; h *= 2, n = std::max(1, n / 2))
+            for (int q = 0; q < n; ++q) front.push_back(h);
+        int fsum = 0;
+        for (int h : front) fsum += h;
+        if (2 * fsum > tiles_total) front.clear(), fsum = 0;
+        std::vector<int> hs(front);
+        int mid = tiles_total - 2 * fsum;
+        while (mid > 0) { hs.push_back(std::min(bt, mid)); mid -= std::min(bt, mid); }
+        hs.insert(hs.end(), front.rbegin(), front.rend());
+        int t = 0;
+        for (int h : hs) { bands.push_back({t, t + h, 0, 0, 0, 0}); t += h; }
+    }
+    const int NB = (int)bands.size();
     if (NB < 2) return 0;
     int sms = 0;
     WHB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
-    // edge tile shape of a band: a one-wave launch lasts as long as its slowest CTA, and the 124 x 4
-    // shape stages 386 box rows per plane (the main shape 50): take the widest shape that still covers
-    // the band's rows with one tile (28 x 28, 60 x 12, 124 x 4); WHB_PIPE_LXE forces one
-    int lxb = c->lxe3;
-    if (lxb != 32) {
-        const int rows = bt * t3::BY;
-        lxb = rows <= t3::Shape<16>::BY ? 16 : rows <= t3::Shape<8>::BY ? 8 : 4;
-        lxb = std::max(lxb, c->lxe3);  // not narrower than the remainder needs
-        if (const char *e = getenv("WHB_PIPE_LXE")) {
-            const int v = atoi(e);
-            if ((v == 4 || v == 8 || v == 16) && v >= c->lxe3) lxb = v;
-        }
-    }
-    const int edge_by = lxb == 32 ? t3::BY : 16 * (32 / lxb) - 4;
-    const int per3 = (c->gx3 - (lxb != 32 ? 1 : 0)) * bt + (lxb != 32 ? (bt * t3::BY + edge_by - 1) / edge_by : 0);
-    const int nch3 = std::max(1, sms / std::max(1, per3));
-    const int nch2 = std::max(1, sms / std::max(1, c->gx2 * ((bt * t3::BY + T3_BY - 1) / T3_BY)));
     const int npl = c->upd_hi - c->upd_lo;
-    const int cl3 = (npl + nch3 - 1) / nch3, cl2 = (npl + nch2 - 1) / nch2;
-    // residual partial slots: the last pass writes one per CTA and band
     const Pass &lastp = passes.back();
-    const int per_band_parts = lastp.k == 3 ? c->gx3 * bt * ((npl + cl3 - 1) / cl3)
-                                            : c->gx2 * ((bt * t3::BY + T3_BY - 1) / T3_BY) * ((npl + cl2 - 1) / cl2);
-    if ((long long)per_band_parts * NB > c->nparts) return 0;
+    int parts = 0;
+    for (Band &B : bands) {
+        const int h = B.t1 - B.t0;
+        // edge tile shape of a band: a one-wave launch lasts as long as its slowest CTA, and the 124 x 4
+        // shape stages 386 box rows per plane (the main shape 50): take the widest shape that still
+        // covers the band's rows with one tile (28 x 28, 60 x 12, 124 x 4); WHB_PIPE_LXE forces one
+        B.lx = c->lxe3;
+        if (B.lx != 32) {
+            const int rows = h * t3::BY;
+            B.lx = rows <= t3::Shape<16>::BY ? 16 : rows <= t3::Shape<8>::BY ? 8 : 4;
+            B.lx = std::max(B.lx, c->lxe3);  // not narrower than the remainder needs
+            if (const char *e = getenv("WHB_PIPE_LXE")) {
+                const int v = atoi(e);
+                if ((v == 4 || v == 8 || v == 16) && v >= c->lxe3) B.lx = v;
+            }
+        }
+        // (the edge column's h slots per chunk all run, as shorter chunks)
+        const int nch3 = std::max(1, sms / std::max(1, c->gx3 * h));
+        const int jt2 = (h * t3::BY + T3_BY - 1) / T3_BY;
+        const int nch2 = std::max(1, sms / std::max(1, c->gx2 * jt2));
+        B.cl3 = (npl + nch3 - 1) / nch3;
+        B.cl2 = (npl + nch2 - 1) / nch2;
+        B.po = parts;  // residual partial slots: the last pass writes one per CTA
+        parts += lastp.k == 3 ? c->gx3 * h * ((npl + B.cl3 - 1) / B.cl3) : c->gx2 * jt2 * ((npl + B.cl2 - 1) / B.cl2);
+    }
+    if (parts > c->nparts) return 0;
     if (!c->s_in) {
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);  // the small copy kernels go first when an SM frees up
         WHB_CUDA(cudaStreamCreateWithPriority(&c->s_in, cudaStreamNonBlocking, hi));
         WHB_CUDA(cudaStreamCreateWithPriority(&c->s_out, cudaStreamNonBlocking, hi));
     }
-    while ((int)c->ev_band.size() < 2 * NB + 1) {
+    // pass launches run as a dataflow over NS streams, diagonal d on stream d % NS (a diagonal is a
+    // chain: (p, b) needs (p-1, b+1), the launch before it): a launch also waits for the events of
+    // (p-1, b) and (p-1, b-1) on the two previous diagonals, so neighbouring diagonals overlap and
+    // the drain / fill gap between the dependent one-wave launches of one diagonal is covered by the
+    // next diagonal's work.  WHB_PIPE_STREAMS=1: one stream.
+    int NS = 4;
+    if (const char *e = getenv("WHB_PIPE_STREAMS")) NS = std::max(1, std::min(16, atoi(e)));
+    while ((int)c->s_band.size() < NS) {
+        cudaStream_t st;
+        WHB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        c->s_band.push_back(st);
+    }
+    // events: [0, NB) uploads, [NB, 3 NB) pass launches (p % 2, b), then one per stream, then the start
+    const int EV_PASS = NB, EV_STREAM = 3 * NB, EV_START = 3 * NB + NS;
+    while ((int)c->ev_band.size() < EV_START + 1) {
         cudaEvent_t e;
         WHB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         c->ev_band.push_back(e);
     }
+    const bool fpi = out_mode == WHB_OUT_FPI;
     WHB_TRY(ensure_hist(c, 1));
-    WHB_TRY(upload_members(c, WHB_OUT_FPI, 0));
-    WHB_CUDA(cudaMemsetAsync(c->d_counter, 0, sizeof(int), c->stream));
-    c->cur_zf = 0;
+    WHB_TRY(upload_members(c, out_mode, zf));
+    if (fpi) WHB_CUDA(cudaMemsetAsync(c->d_counter, 0, sizeof(int), c->stream));
+    c->cur_zf = zf;
     double *v = c->mem[0].v;
-    const size_t hpitch = (size_t)n1 * n2 * sizeof(double);
+    double *result = fpi ? v : c->mem[0].out;  // W(v, f) replaces v, or goes to the output field
     auto band = [&](int b, int &ja, int &jb) {
-        ja = b * bt * t3::BY;
-        jb = b == NB - 1 ? n1 : std::min(n1, (b + 1) * bt * t3::BY);  // copies: the last band takes row n1-1 too
+        ja = bands[b].t0 * t3::BY;
+        jb = b == NB - 1 ? n1 : std::min(n1, bands[b].t1 * t3::BY);  // copies: the last band takes row n1-1 too
     };
-    // host <-> pitched device rows: one 3D copy per band (copy engines only), or WHB_PIPE_COPY=stage:
-    // a contiguous copy into the staging field + a re-pitch kernel
-    static const bool direct = !(getenv("WHB_PIPE_COPY") && std::string(getenv("WHB_PIPE_COPY")) == "stage");
-    auto copy_band = [&](double *host, int ja, int jb, bool h2d, cudaStream_t st) -> int {
+    // host <-> pitched device rows: one 3D copy per band (copy engines only; measured equal to a
+    // contiguous copy into a staging field + a re-pitch kernel, which needs SMs the passes occupy)
+    static const bool nocopy = getenv("WHB_PIPE_NOCOPY") != nullptr;  // timing experiments: passes only
+    auto copy_band = [&](const HostView &h, double *dev, int ja, int jb, bool h2d, cudaStream_t st) -> int {
+        if (nocopy) return 0;
         cudaMemcpy3DParms q = {};
-        cudaPitchedPtr hp = make_cudaPitchedPtr(host, (size_t)n2 * sizeof(double), (size_t)n2, (size_t)n1);
-        cudaPitchedPtr dp = make_cudaPitchedPtr(owned(v, c), (size_t)c->P * sizeof(double), (size_t)n2, (size_t)n1);
+        cudaPitchedPtr hp = make_cudaPitchedPtr(h.p, (size_t)h.row_stride * sizeof(double), (size_t)n2,
+                                                (size_t)(h.plane_stride / h.row_stride));
+        cudaPitchedPtr dp = make_cudaPitchedPtr(owned(dev, c), (size_t)c->P * sizeof(double), (size_t)n2, (size_t)n1);
         q.srcPtr = h2d ? hp : dp;
         q.dstPtr = h2d ? dp : hp;
         q.srcPos = make_cudaPos(0, (size_t)ja, 0);
@@ -2893,8 +2924,7 @@ int iterate_host_banded(whb_ctx *c, const double *v_host, double *v_out_host, do
         WHB_CUDA(cudaMemcpy3DAsync(&q, st));
         return 0;
     };
-    if (!direct) WHB_TRY(ensure_stage(c));
-    cudaEvent_t ev0 = c->ev_band[2 * NB];
+    cudaEvent_t ev0 = c->ev_band[EV_START];
     static const bool trace = getenv("WHB_PIPE_TRACE") != nullptr;  // stderr: upload / compute / download end times
     cudaEvent_t tev[4] = {};
     if (trace) {
@@ -2904,17 +2934,13 @@ int iterate_host_banded(whb_ctx *c, const double *v_host, double *v_out_host, do
     WHB_CUDA(cudaEventRecord(ev0, c->stream));
     WHB_CUDA(cudaStreamWaitEvent(c->s_in, ev0, 0));
     WHB_CUDA(cudaStreamWaitEvent(c->s_out, ev0, 0));
+    for (int q = 0; q < NS; ++q) WHB_CUDA(cudaStreamWaitEvent(c->s_band[q], ev0, 0));
+    cudaStream_t main_stream = c->stream;
     for (int b = 0; b < NB; ++b) {
         int ja, jb;
         band(b, ja, jb);
-        if (direct) {
-            WHB_TRY(copy_band(const_cast<double *>(v_host), ja, jb, true, c->s_in));
-            band_zero_kernel<<<74, 256, 0, c->s_in>>>(owned(v, c), n0, n1, n2, c->P, c->S0, ja, jb);
-        } else {
-            WHB_CUDA(cudaMemcpy2DAsync(c->stage + (size_t)ja * n2, hpitch, v_host + (size_t)ja * n2, hpitch,
-                                       (size_t)(jb - ja) * n2 * sizeof(double), n0, cudaMemcpyHostToDevice, c->s_in));
-            band_repitch_kernel<<<296, 256, 0, c->s_in>>>(c->stage, owned(v, c), n0, n1, n2, c->P, c->S0, ja, jb, 1);
-        }
+        WHB_TRY(copy_band(vin, v, ja, jb, true, c->s_in));
+        band_zero_kernel<<<74, 256, 0, c->s_in>>>(owned(v, c), n0, n1, n2, c->P, c->S0, ja, jb);
         c->launches++;
         WHB_CUDA(cudaGetLastError());
         WHB_CUDA(cudaEventRecord(c->ev_band[b], c->s_in));
@@ -2922,34 +2948,40 @@ int iterate_host_banded(whb_ctx *c, const double *v_host, double *v_out_host, do
     if (trace) WHB_CUDA(cudaEventRecord(tev[1], c->s_in));
     const auto h0 = std::chrono::steady_clock::now();
     int rc = 0;
+    static const bool trace2 = trace && std::string(getenv("WHB_PIPE_TRACE")) == "2";
     for (int d = 0; d < NB + NP - 1 && !rc; ++d) {
+        if (trace2 && d % 8 == 0)
+            fprintf(stderr, "[whb banded] diagonal %d enqueued at host %.2f ms (%lld launches)\n", d,
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count(),
+                    (long long)c->launches);
         for (int p = 0; p < NP && !rc; ++p) {
             const int b = d - p;
             if (b < 0 || b >= NB) continue;
-            if (p == 0) WHB_CUDA(cudaStreamWaitEvent(c->stream, c->ev_band[std::min(b + 1, NB - 1)], 0));
+            cudaStream_t st = c->s_band[d % NS];
+            if (p == 0) {
+                WHB_CUDA(cudaStreamWaitEvent(st, c->ev_band[std::min(b + 1, NB - 1)], 0));
+            } else if (NS > 1) {  // (p-1, b+1) is the launch before this one on the diagonal's stream
+                const int base = EV_PASS + ((p - 1) & 1) * NB;
+                WHB_CUDA(cudaStreamWaitEvent(st, c->ev_band[base + b], 0));
+                if (b > 0) WHB_CUDA(cudaStreamWaitEvent(st, c->ev_band[base + b - 1], 0));
+            }
+            c->stream = st;  // the launchers enqueue on the context stream
             const bool last = (p == NP - 1);
-            c->win_j0 = b * bt * t3::BY;
-            c->win_j1 = b == NB - 1 ? n1 : (b + 1) * bt * t3::BY;
-            c->win_po = last ? b * per_band_parts : 0;
-            c->win_lxe = lxb;
-            if (passes[p].k == 3) rc = launch_t3(c, passes[p].s, last, c->upd_lo, c->upd_hi, cl3);
-            else rc = launch_pair_range(c, passes[p].s, c->upd_lo, c->upd_hi, cl2, c->win_po);
+            const Band &B = bands[b];
+            c->win_j0 = B.t0 * t3::BY;
+            c->win_j1 = b == NB - 1 ? n1 : B.t1 * t3::BY;
+            c->win_po = last ? B.po : 0;
+            c->win_lxe = B.lx;
+            if (passes[p].k == 3) rc = launch_t3(c, passes[p].s, last, c->upd_lo, c->upd_hi, B.cl3);
+            else rc = launch_pair_range(c, passes[p].s, c->upd_lo, c->upd_hi, B.cl2, c->win_po);
+            c->stream = main_stream;
+            cudaEvent_t evp = c->ev_band[EV_PASS + (p & 1) * NB + b];
+            if (!rc) WHB_CUDA(cudaEventRecord(evp, st));
             if (last && !rc) {
                 int ja, jb;
                 band(b, ja, jb);
-                WHB_CUDA(cudaEventRecord(c->ev_band[NB + b], c->stream));
-                WHB_CUDA(cudaStreamWaitEvent(c->s_out, c->ev_band[NB + b], 0));
-                if (direct) {
-                    WHB_TRY(copy_band(v_out_host, ja, jb, false, c->s_out));
-                } else {
-                    band_repitch_kernel<<<296, 256, 0, c->s_out>>>(c->stage, owned(v, c), n0, n1, n2, c->P, c->S0, ja,
-                                                                   jb, 0);
-                    c->launches++;
-                    WHB_CUDA(cudaGetLastError());
-                    WHB_CUDA(cudaMemcpy2DAsync(v_out_host + (size_t)ja * n2, hpitch, c->stage + (size_t)ja * n2,
-                                               hpitch, (size_t)(jb - ja) * n2 * sizeof(double), n0,
-                                               cudaMemcpyDeviceToHost, c->s_out));
-                }
+                WHB_CUDA(cudaStreamWaitEvent(c->s_out, evp, 0));
+                WHB_TRY(copy_band(vout, result, ja, jb, false, c->s_out));
             }
         }
     }
@@ -2957,16 +2989,22 @@ int iterate_host_banded(whb_ctx *c, const double *v_host, double *v_out_host, do
     c->win_j1 = INT_MAX;
     c->win_po = 0;
     c->win_lxe = 0;
+    for (int q = 0; q < NS; ++q) {  // the context stream continues after every band stream
+        cudaEventRecord(c->ev_band[EV_STREAM + q], c->s_band[q]);
+        cudaStreamWaitEvent(c->stream, c->ev_band[EV_STREAM + q], 0);
+    }
     if (rc) {
         cudaStreamSynchronize(c->s_in);
         cudaStreamSynchronize(c->stream);
         cudaStreamSynchronize(c->s_out);
         return rc;
     }
-    reduce_partials_kernel<<<1, 1024, 0, c->stream>>>(c->d_members, 1, per_band_parts * NB, c->d_hist, c->d_counter);
-    c->launches++;
-    WHB_CUDA(cudaGetLastError());
-    if (resid_sq) WHB_CUDA(cudaMemcpyAsync(resid_sq, c->d_hist, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (fpi) {
+        reduce_partials_kernel<<<1, 1024, 0, c->stream>>>(c->d_members, 1, parts, c->d_hist, c->d_counter);
+        c->launches++;
+        WHB_CUDA(cudaGetLastError());
+        if (resid_sq) WHB_CUDA(cudaMemcpyAsync(resid_sq, c->d_hist, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    }
     const double host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
     if (trace) {
         WHB_CUDA(cudaEventRecord(tev[2], c->stream));
@@ -2980,7 +3018,8 @@ int iterate_host_banded(whb_ctx *c, const double *v_host, double *v_out_host, do
         cudaEventElapsedTime(&comp, tev[0], tev[2]);
         cudaEventElapsedTime(&down, tev[0], tev[3]);
         fprintf(stderr, "[whb banded] bands %d x passes %d: upload done %.1f ms, passes done %.1f ms, download done %.1f ms; "
-                "host enqueue of the passes %.1f ms (chunks of %d planes)\n", NB, NP, up, comp, down, host_ms, cl3);
+                "host enqueue of the passes %.1f ms (chunks of %d planes)\n", NB, NP, up, comp, down, host_ms,
+                bands[NB / 2].cl3);
         for (auto &e : tev) cudaEventDestroy(e);
     }
     *done = true;
@@ -2993,7 +3032,9 @@ int whb_iterate_host(whb_ctx *c, const double *v_host, double *v_out_host, doubl
     WHB_TRY(set_dev(c));
     WHB_TRY(check_ready(c));
     bool banded = false;
-    WHB_TRY(iterate_host_banded(c, v_host, v_out_host, resid_sq, &banded));
+    const int64_t hp = c->gshape[1] * c->gshape[2], hr = c->gshape[2];
+    WHB_TRY(solve_host_banded(c, HostView{const_cast<double *>(v_host), hp, hr}, HostView{v_out_host, hp, hr},
+                              WHB_OUT_FPI, 0, resid_sq, &banded));
     if (banded) return 0;
     WHB_TRY(ensure_hist(c, 1));
     WHB_TRY(upload_members(c, WHB_OUT_FPI, 0));
@@ -3003,6 +3044,34 @@ int whb_iterate_host(whb_ctx *c, const double *v_host, double *v_out_host, doubl
     WHB_TRY(run_solve(c, WHB_OUT_FPI, 0));
     WHB_TRY(copy_field_d2h(c, c->mem[0].v, v_out_host));
     if (resid_sq) WHB_CUDA(cudaMemcpyAsync(resid_sq, c->d_hist, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    WHB_CUDA(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int whb_solve_host(whb_ctx *c, const double *v_host, int64_t v_plane_stride, int64_t v_row_stride, double *out_host,
+                   int64_t out_plane_stride, int64_t out_row_stride, int out_mode, int zero_forcing, double *resid_sq) {
+    if (!c || !v_host || !out_host) return fail(WHB_E_ARG, "NULL argument");
+    if (out_mode < 0 || out_mode > 2) return fail(WHB_E_ARG, "bad out_mode");
+    if (c->nbatch != 1) return fail(WHB_E_ARG, "whb_solve_host needs nbatch == 1");
+    WHB_TRY(set_dev(c));
+    WHB_TRY(check_ready(c));
+    const int zf = (zero_forcing || out_mode == WHB_OUT_AV) ? 1 : 0;
+    bool banded = false;
+    WHB_TRY(solve_host_banded(c, HostView{const_cast<double *>(v_host), v_plane_stride, v_row_stride},
+                              HostView{out_host, out_plane_stride, out_row_stride}, out_mode, zf, resid_sq, &banded));
+    if (banded) return 0;
+    // serial path: upload, the solve graph, download
+    double *v = c->mem[0].v;
+    WHB_TRY(copy_field_strided(c, v, const_cast<double *>(v_host), v_plane_stride, v_row_stride, true));
+    WHB_TRY(zero_bnd(c, v));
+    WHB_TRY(ensure_hist(c, 1));
+    WHB_TRY(upload_members(c, out_mode, zf));
+    if (out_mode == WHB_OUT_FPI) WHB_CUDA(cudaMemsetAsync(c->d_counter, 0, sizeof(int), c->stream));
+    WHB_TRY(run_solve(c, out_mode, zf));
+    WHB_TRY(copy_field_strided(c, out_mode == WHB_OUT_FPI ? v : c->mem[0].out, out_host, out_plane_stride,
+                               out_row_stride, false));
+    if (out_mode == WHB_OUT_FPI && resid_sq)
+        WHB_CUDA(cudaMemcpyAsync(resid_sq, c->d_hist, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     WHB_CUDA(cudaStreamSynchronize(c->stream));
     return 0;
 }

@@ -134,17 +134,27 @@ def _field_type(v):
     return type(v) if hasattr(type(v), "from_values") else GridField
 
 
+def new_field(ftype, grid, ghost):
+    """(field, writable interior view) of a freshly allocated field of type ``ftype`` (ours or the
+    reference's GridField) backed by a recycled page-locked buffer, or None when the type does not
+    expose its buffer."""
+    try:
+        fld = ftype(grid, ghost=ghost)
+        _pin_storage(fld)
+        return fld, fld._writable()
+    except (AttributeError, TypeError):
+        return None
+
+
 def field_from_device(ftype, grid, ghost, ctx, field_id):
     """A freshly allocated field of type ``ftype`` (ours or the reference's GridField) holding
     device field ``field_id``: copied straight into the new field's (possibly ghost-padded)
     buffer with one strided D2H copy, no host-side repacking.  The device field's Dirichlet
     points are 0 by invariant, so the field is in the state set_values would leave it in."""
-    try:
-        fld = ftype(grid, ghost=ghost)
-        _pin_storage(fld)
-        buf = fld._writable()
-    except (AttributeError, TypeError):
+    made = new_field(ftype, grid, ghost)
+    if made is None:
         return ftype.from_values(grid, ctx.download(field_id), ghost=ghost)
+    fld, buf = made
     ctx.download_into(field_id, buf)
     fld._touch()
     return fld
@@ -202,9 +212,19 @@ def wave_solve_filtered(v, f, config, corr, op, linear_solver=None, implicit_fir
         return field_from_device(_field_type(v), grid, max(2, op.ghost_width), dp.ctx, _native.OUT)
     dp.set_schedule(time_schedule(corr, config))
     zero_f = dp.set_forcing_field(f)
-    dp.ctx.upload_view(_native.V, v.values)
-    dp.ctx.filtered_solve(_native.OUT_PLAIN, zero_forcing=zero_f)
-    return field_from_device(_field_type(v), grid, max(2, op.ghost_width), dp.ctx, _native.OUT)
+    ctx = dp.ctx
+    vals = v.values
+    made = new_field(_field_type(v), grid, max(2, op.ghost_width))
+    if made is not None and ctx.nbatch == 1 and ctx._strides(vals) is not None and ctx._strides(made[1]) is not None:
+        # host field in, host field out in one call (whb_solve_host): on the three-step plan the
+        # transfers of v and W(v, f) move in bands of rows behind the passes
+        fld, buf = made
+        ctx.solve_host(vals, buf, _native.OUT_PLAIN, zero_forcing=zero_f)
+        fld._touch()
+        return fld
+    ctx.upload_view(_native.V, vals)
+    ctx.filtered_solve(_native.OUT_PLAIN, zero_forcing=zero_f)
+    return field_from_device(_field_type(v), grid, max(2, op.ghost_width), ctx, _native.OUT)
 
 
 @dataclass

@@ -151,6 +151,15 @@ for cells, omega in [((40, 100, 130), 12.0), ((48, 30, 200), 8.0), ((64, 64, 64)
         rerr = max(rerr, abs(d - dref) / dref)
         ref = new
         a, b = b, a      # feed the iterate back (the reference's _iterate loop)
+    # the Python seam (host GridField in, new GridField out: whb_solve_host, plain output), twice
+    op = wh.DiscreteOperator(g, 2, 1.0)
+    vf = wh.GridField.from_values(g, rng.standard_normal(g.shape) * 1e-3)
+    for it in range(2):
+        l0 = step.dp.ctx.launch_count()
+        wf = wh.wave_solve_filtered(vf, f, cfg, corr, op)
+        launches.append(step.dp.ctx.launch_count() - l0)
+        mis += int(np.sum(wf.values != ON.wave_solve(np.array(vf.values), np.array(f.values), g.spacing, sc)))
+        vf = wf
     out.append([list(cells), corr.steps_per_period, mis, rerr, launches, list(step.dp.ctx.plan())])
     wh.release_device_cache()
 print(json.dumps(out))

@@ -25,10 +25,26 @@ pytestmark = pytest.mark.skipif(not RH.available(), reason="reference not presen
 class FakeCtx:
     """Test double of _native.Context (oracle arithmetic, host memory)."""
 
+    nbatch = 1
+
     def __init__(self, grid):
         self.grid = grid
         self.fields = {}
         self.sched = None
+        self.host_solves = 0
+
+    def _strides(self, a):  # as _native.Context._strides: views with a contiguous last axis
+        if not isinstance(a, np.ndarray) or a.dtype != np.float64 or a.ndim not in (2, 3) or a.strides[-1] != 8:
+            return None
+        return a.strides[0] // 8, a.strides[-2] // 8
+
+    def solve_host(self, v, out, out_mode=_native.OUT_PLAIN, zero_forcing=False):
+        assert self._strides(v) is not None and self._strides(out) is not None and out.flags.writeable
+        self.upload(_native.V, v)
+        self.filtered_solve(out_mode, zero_forcing)
+        out[...] = self.fields[_native.OUT]
+        self.host_solves += 1
+        return 0.0
 
     def set_schedule(self, member, sched):
         self.sched = sched
@@ -91,6 +107,8 @@ def test_rebinding_reroutes_the_reference_drivers(monkeypatch):
     assert krun.iterations == krun_ref.iterations
     assert np.array_equal(x.values, x_ref.values)
     assert probs, "the device layer was used"
+    # 2D fields go in and out through the one-call host solve (strided reference buffers)
+    assert all(p.ctx.host_solves > 0 for p in probs.values())
 
 
 def test_reference_objects_accepted_directly(monkeypatch):
