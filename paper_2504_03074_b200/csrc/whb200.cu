@@ -1729,12 +1729,28 @@ void launch_wf(whb_ctx *c, int off, int cnt, int s) {
     // Row chunks per strip: one wave of CTAs for a single member (nchw); with cnt members
     // per launch, longer chunks — every chunk re-streams T + lag warm-up rows (8 at T = 4),
     // which at the single-member chunk length of a 1025^2 grid (12 rows) is 67 % extra.
+    // The chunk count of a batched launch maximises (fill of the CTA waves) x (useful rows per
+    // chunk): the kernel is latency-bound, so an SM holding 2 of its 3 CTAs runs at 2/3 -- 64
+    // members x 5 strips as one chunk each are 320 CTAs on 444 slots (72 %), as 4 chunks each 1280
+    // CTAs on 3 waves (96 %, x 256 / 264 useful rows).  WHB_WF_BATCH=wave: the old rule (one wave).
     int nch = c->nchw[T], cl = c->chw[T];
     if (cnt > 1) {
-        const long long want = c->wf_res[T] / ((long long)c->gxw[T] * cnt);  // one wave of CTAs
-        nch = (int)std::max<long long>(1, std::min<long long>(nch, want));
+        static const bool one_wave = getenv("WHB_WF_BATCH") && std::string(getenv("WHB_WF_BATCH")) == "wave";
         const int nplanes = c->upd_hi - c->upd_lo;
-        cl = (nplanes + nch - 1) / nch;
+        const long long res = std::max<long long>(1, c->wf_res[T]);
+        int best = 1;
+        if (one_wave) {
+            best = (int)std::max<long long>(1, std::min<long long>(nch, res / ((long long)c->gxw[T] * cnt)));
+        } else {
+            double best_eff = 0.0;
+            for (int n = 1; n <= c->nchw[T]; ++n) {
+                const int l = (nplanes + n - 1) / n;
+                const long long ctas = (long long)c->gxw[T] * ((nplanes + l - 1) / l) * cnt;
+                const double eff = (double)ctas / (double)((ctas + res - 1) / res * res) * l / (l + 2.0 * T);
+                if (eff > best_eff + 1e-9) best_eff = eff, best = n;
+            }
+        }
+        cl = (nplanes + best - 1) / best;
         nch = (nplanes + cl - 1) / cl;
     }
     dim3 grid(c->gxw[T], nch, cnt);
@@ -2816,9 +2832,9 @@ int solve_host_banded(whb_ctx *c, HostView vin, HostView vout, int out_mode, int
     // bands of tile rows: `bt` tiles high, ramping up from one tile at both ends (the pipeline fills
     // and drains in units of the band height: the first launches wait for the uploads, the last
     // downloads for the last launches); per band, axis-0 chunks so that a launch is one wave of CTAs
-    int bt = 2;  // measured on config 4 (e2e Gpts/s): 1 -> 154, 2 -> 180, 4 -> 164, 8 -> 125; serial path 129
+    int bt = 2;  // measured on config 4 (ms per call, 4 streams): 1 -> 495, 2 -> 436, 4 -> 511; serial path ~690
     if (const char *e = getenv("WHB_PIPE_ROWS")) bt = std::max(1, atoi(e));
-    int ramp = 8;  // one-tile bands at each end (then doubling up to bt)
+    int ramp = 0;  // one-tile bands at each end, then doubling up to bt (measured: 0 -> 427 ms per call, 8 -> 443, 16 -> 468)
     if (const char *e = getenv("WHB_PIPE_RAMP")) ramp = std::max(0, atoi(e));
     const int rows_total = n1 - 1;  // rows 0 .. n1-2 carry tiles (row 0 and n1-1 are Dirichlet)
     const int tiles_total = (rows_total + t3::BY - 1) / t3::BY;
@@ -2881,7 +2897,7 @@ int solve_host_banded(whb_ctx *c, HostView vin, HostView vout, int out_mode, int
     // (p-1, b) and (p-1, b-1) on the two previous diagonals, so neighbouring diagonals overlap and
     // the drain / fill gap between the dependent one-wave launches of one diagonal is covered by the
     // next diagonal's work.  WHB_PIPE_STREAMS=1: one stream.
-    int NS = 4;
+    int NS = 2;  // measured on config 4 (ms per call): 1 -> 484, 2 -> 427, 4 -> 436
     if (const char *e = getenv("WHB_PIPE_STREAMS")) NS = std::max(1, std::min(16, atoi(e)));
     while ((int)c->s_band.size() < NS) {
         cudaStream_t st;
