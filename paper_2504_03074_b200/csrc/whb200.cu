@@ -461,6 +461,9 @@ __global__ void step_general_kernel(GeomG g, const Member *__restrict__ members,
     }
 }
 
+#ifndef WHB_GM_MINB
+#define WHB_GM_MINB 6  // resident blocks per SM the register allocation aims at
+#endif
 // One leapfrog step of the general operator, marching: thread = one (j, k) column of a chunk of
 // axis-0 planes.  The 2h+1 axis-0 taps of the column come from a register window that takes one
 // new (boundary-imaged) value per plane; axis-1/-2 taps are loads of neighbouring columns (L1 /
@@ -468,9 +471,11 @@ __global__ void step_general_kernel(GeomG g, const Member *__restrict__ members,
 // Whole-grid contexts only (plane_begin == 0), as the general plan.  Same arithmetic and order as
 // general_lap / step_general_kernel.
 template <int H>
-__global__ void __launch_bounds__(128) step_general_march_kernel(GeomG g, const Member *__restrict__ members, int s,
-                                                                 int nloc, int chunk, int JY) {
-    const Member m = members[blockIdx.z];
+__global__ void __launch_bounds__(128, WHB_GM_MINB) step_general_march_kernel(GeomG g, const Member *__restrict__ members,
+                                                                              int s, int nloc, int chunk, int JY) {
+    // (a reference, not a copy: level_ptr indexes the ring dynamically, which would put a copy of the
+    // entry into every thread's local memory -- 160 B of stores per thread in blocks of 9 planes)
+    const Member &m = members[blockIdx.z];
     const int kind = (s == 0) ? K_FIRST : ((s == m.n_total - 1) ? K_LAST : K_MID);
     const double *wcur = level_ptr(m, s);
     const double *wprv = level_ptr(m, s - 1);
@@ -507,50 +512,114 @@ __global__ void __launch_bounds__(128) step_general_march_kernel(GeomG g, const 
 #pragma unroll
         for (int q = 0; q < 2 * H; ++q) win[q + 1] = z_at(g.plane_begin + pl0 - H + q);
     }
+    // The operands of a plane that do not depend on the previous one -- the entering window value,
+    // f, W^{n-1}, acc, v -- are loaded one iteration ahead: the stores of an iteration may alias the
+    // next one's loads as far as the compiler knows, so without this every plane paid its DRAM round
+    // trips in sequence (40.8 Gpts/s on the order-4 2049^2 workload, 0.28 of HBM).
+    const double *const mf = m.f;
+    double *const macc = m.acc, *const mv = m.v, *const mdst = m.dst;
+    const int omode = m.out_mode;
+    const double oscale = m.out_scale;
+    const bool need_v = (kind == K_LAST) && omode != WHB_OUT_PLAIN;
+    // (two planes ahead was measured slower: 40.0 vs 45.7 Gpts/s, one resident block less per SM)
+    double zN = 0.0, fN = 0.0, pN = 0.0, aN = 0.0, vN = 0.0;
+    // a chunk whose window stays inside the grid reads the entering value directly
+    const bool zfast = g.per[0] == 0 && g.plane_begin + pl0 - H >= 0 && g.plane_begin + pl1 - 1 + H <= g.n[0] - 1;
+    auto load_plane = [&](int pl) {
+        if (g.act[0])
+            zN = zfast ? __ldg(wcur + (long long)(pl + H + GH) * g.S0 + cbase) : z_at(g.plane_begin + pl + H);
+        const long long p = (pl + GH) * g.S0 + cbase;
+        if (mf) fN = mf[p];
+        if (kind != K_FIRST) {
+            pN = wprv[p];
+            aN = macc[p];
+        }
+        if (need_v) vN = mv[p];
+    };
+    if (col_ok && pl0 < pl1) load_plane(pl0);
+    // The axis-1 / axis-2 taps of a column sit at fixed offsets from the point (j and k do not change
+    // along the march): boundary images (odd reflection / periodic wrap, as gfetch) are resolved
+    // once per thread into an element offset and a sign per tap.
+    long long off1[2 * H + 1], off2[2 * H + 1];
+    bool neg1[2 * H + 1], neg2[2 * H + 1];
+#pragma unroll
+    for (int q = 0; q <= 2 * H; ++q) {
+        auto image = [&](int axis, int c, long long stride, long long &off, bool &neg) {
+            int idx = c + q - H;
+            const int n = g.n[axis];
+            neg = false;
+            if (g.per[axis]) {
+                idx = (idx % n + n) % n;
+            } else if (idx < 0) {
+                idx = -idx;
+                neg = true;
+            } else if (idx > n - 1) {
+                idx = 2 * (n - 1) - idx;
+                neg = true;
+            }
+            off = (long long)(idx - c) * stride;
+        };
+        image(1, j, g.P, off1[q], neg1[q]);
+        image(2, k, 1, off2[q], neg2[q]);
+    }
+    // points of this column that are updated at all (axis-1 / axis-2 part of general_updates)
+    const bool col_upd = col_ok && !(g.act[1] && !g.per[1] && (j < 1 || j > g.n[1] - 2)) &&
+                         !(!g.per[2] && (k < 1 || k > g.n[2] - 2));
+    const bool a0_bnd = g.act[0] && !g.per[0];
     for (int pl = pl0; pl < pl1 && col_ok; ++pl) {
         const int gi = g.plane_begin + pl;
+        const double zc = zN, fc = fN, pc = pN, ac = aN, vc = vN;
+        if (pl + 1 < pl1) load_plane(pl + 1);
         if (g.act[0]) {
 #pragma unroll
             for (int q = 0; q < 2 * H; ++q) win[q] = win[q + 1];
-            win[2 * H] = z_at(gi + H);
+            win[2 * H] = zc;
         }
-        if (!general_updates(g, gi, j, k)) continue;
+        if (!col_upd || (a0_bnd && (gi < 1 || gi > g.n[0] - 2))) continue;
         const long long p = (pl + GH) * g.S0 + cbase;
-        const double wc = wcur[p];
+        const double wc = g.act[0] ? win[H] : wcur[p];  // (an updated point is not a boundary image)
         double lap = 0.0;
         if (g.act[0]) {
 #pragma unroll
             for (int q = 0; q <= 2 * H; ++q) lap = whb_add(lap, whb_mul(g.taps[0][q], win[q]));
         }
+        if (g.act[1]) {
 #pragma unroll
-        for (int a = 1; a < 3; ++a) {
-            if (!g.act[a]) continue;
+            for (int q = 0; q <= 2 * H; ++q) {
+                const double v = wcur[p + off1[q]];
+                lap = whb_add(lap, whb_mul(g.taps[1][q], neg1[q] ? -v : v));
+            }
+        }
+        if (g.act[2]) {
 #pragma unroll
-            for (int q = 0; q <= 2 * H; ++q) lap = whb_add(lap, whb_mul(g.taps[a][q], gfetch(g, wcur, p, gi, j, k, a, q - H)));
+            for (int q = 0; q <= 2 * H; ++q) {
+                const double v = wcur[p + off2[q]];
+                lap = whb_add(lap, whb_mul(g.taps[2][q], neg2[q] ? -v : v));
+            }
         }
         if (g.use_c2) lap = whb_mul(lap, g.c2);
         double wn;
         if (kind == K_FIRST) {
-            const double d = m.f ? whb_sub(lap, m.f[p]) : lap;
+            const double d = mf ? whb_sub(lap, fc) : lap;
             wn = whb_add(wc, whb_mul(h, d));
             wnxt[p] = wn;
-            m.acc[p] = whb_add(whb_mul(acc0, wc), whb_mul(accn, wn));
+            macc[p] = whb_add(whb_mul(acc0, wc), whb_mul(accn, wn));
         } else {
-            const double d = m.f ? whb_sub(lap, whb_mul(m.f[p], cosn)) : lap;
-            wn = whb_add(whb_sub(whb_mul(2.0, wc), wprv[p]), whb_mul(h, d));
+            const double d = mf ? whb_sub(lap, whb_mul(fc, cosn)) : lap;
+            wn = whb_add(whb_sub(whb_mul(2.0, wc), pc), whb_mul(h, d));
             if (kind == K_MID) {
                 wnxt[p] = wn;
-                m.acc[p] = whb_add(m.acc[p], whb_mul(accn, wn));
+                macc[p] = whb_add(ac, whb_mul(accn, wn));
             } else {
-                const double out = whb_mul(m.out_scale, whb_add(m.acc[p], whb_mul(accn, wn)));
-                if (m.out_mode == WHB_OUT_FPI) {
-                    const double dd = out - m.v[p];
+                const double out = whb_mul(oscale, whb_add(ac, whb_mul(accn, wn)));
+                if (omode == WHB_OUT_FPI) {
+                    const double dd = out - vc;
                     rsum += dd * dd;
-                    m.v[p] = out;
-                } else if (m.out_mode == WHB_OUT_AV) {
-                    m.dst[p] = whb_sub(m.v[p], out);
+                    mv[p] = out;
+                } else if (omode == WHB_OUT_AV) {
+                    mdst[p] = whb_sub(vc, out);
                 } else {
-                    m.dst[p] = out;
+                    mdst[p] = out;
                 }
             }
         }
@@ -1318,8 +1387,10 @@ int plan_launch(whb_ctx *c) {
         c->JTE3 = (int)((n1 - 1 + bye - 1) / bye);
         const long long tiles3 = (long long)c->gx3 * c->JT3;
         const long long res3 = (long long)sms * nb;
-        // chunks: ~256 planes, but at least 4 waves of CTAs
-        long long nch = std::max<long long>((nplanes + 255) / 256, (4 * res3 + tiles3 - 1) / tiles3);
+        // chunks: ~256 planes, but at least 2 waves of CTAs (measured, Gpts/s -- 257^3: chunks of 52 / 64 /
+        // 86 / 128 / 255 planes 212 / 220 / 226 / 199 / 184, the two-step kernel 182; 1025^3: 256 / 342 /
+        // 512 / 1023 planes 250 / 249 / 242 / 225)
+        long long nch = std::max<long long>((nplanes + 255) / 256, (2 * res3 + tiles3 - 1) / tiles3);
         int cl3 = (int)((nplanes + nch - 1) / nch);
         const char *env3 = getenv("WHB_CHUNK3");
         if (env3 && atoi(env3) > 0) cl3 = atoi(env3);
@@ -2616,6 +2687,7 @@ int whb_set_operator_general(whb_ctx *c, int order, const int *periodic, const d
         long long nch = std::max<long long>(1, (4LL * sms * 16 + cols - 1) / cols);
         nch = std::min<long long>(nch, std::max(1, nl / 8));  // chunks of >= 8 planes
         c->gm_chunk = (int)((nl + nch - 1) / nch);
+        if (const char *gc = getenv("WHB_GM_CHUNK")) c->gm_chunk = std::max(1, atoi(gc));
         c->gm_nch = (nl + c->gm_chunk - 1) / c->gm_chunk;
         if ((ge && std::string(ge) == "0") || (long long)c->gm_jy * c->gm_nch > 65535) c->gm_nch = 0;
     }
@@ -2886,6 +2958,10 @@ int solve_host_banded(whb_ctx *c, HostView vin, HostView vout, int out_mode, int
         parts += lastp.k == 3 ? c->gx3 * h * ((npl + B.cl3 - 1) / B.cl3) : c->gx2 * jt2 * ((npl + B.cl2 - 1) / B.cl2);
     }
     if (parts > c->nparts) return 0;
+    // small grids: a band's one-wave launch would cut the march into chunks too short to amortise a
+    // CTA's start-up (~20 planes' worth); they keep the serial path unless WHB_PIPE=1 forces bands
+    static const bool force = getenv("WHB_PIPE") && std::string(getenv("WHB_PIPE")) == "1";
+    if (!force && bands[NB / 2].cl3 < 64) return 0;
     if (!c->s_in) {
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);  // the small copy kernels go first when an SM frees up

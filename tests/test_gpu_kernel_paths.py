@@ -172,7 +172,7 @@ def test_banded_host_iteration_bitwise(gpu_available, env):
     launches enqueued by diagonals: v_new bitwise equal to the C restatement for 3 chained
     iterations (every remainder of N_t mod 3, ragged bands, every edge tile shape), the residual
     to 1e-12; WHB_PIPE=0 is the serial path."""
-    e = dict(os.environ, WHB_T3="1", **env)
+    e = dict(os.environ, WHB_T3="1", **{"WHB_PIPE": "1", **env})  # WHB_PIPE=1: bands on small grids too
     r = subprocess.run([sys.executable, "-c", BAND_SCRIPT % {"root": ROOT}], capture_output=True, text=True, env=e,
                        timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]

@@ -26,7 +26,7 @@ for w in $WL; do
   case $w in
     cfg4) C="python bench.py --workload cfg4 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"; K=t3_kernel; S=10;;
     cfg2) C="python bench.py --workload cfg2 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"; K=wf2d_kernel; S=20;;
-    cfg3) C="python bench.py --workload cfg3 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"; K=tb2_kernel; S=20;;
+    cfg3) C="python bench.py --workload cfg3 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"; K=t3_kernel; S=20;;
     cfg5) C="python bench.py --workload cfg5 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"; K=wf2d_kernel; S=40;;
     cfg1) C="python bench.py --workload cfg1 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"; K=cres2d_kernel; S=1;;
     p4)   C="python bench.py --workload p4 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"; K=step_general_march; S=40;;
