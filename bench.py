@@ -17,8 +17,11 @@ value      = grid-point updates / s (N stored points x N_t x K / device time), G
 e2e        = the same through the reference-facing C-ABI call with HOST buffers:
              whb_iterate_host (paper_2504_03074_b200.HostFPIStep), v copied in from pinned
              host memory and v_new copied out every step (the reference's _iterate loop body,
-             driver.py:222-226); e2e_solve = whb_upload(f) + whb_fpi(K) + whb_download(v)
-             (the fpi_solve call: f in once, residual out every step, v out once)
+             driver.py:222-226; on the three-step plan the copies move in bands of rows behind
+             the passes); e2e_solve = whb_upload(f) + whb_fpi(K) +
+             whb_download(v) (the fpi_solve call: f in once, residual out every step, v out
+             once); e2e_seam = wave_solve_filtered(GridField, ...) -> GridField, the Python seam
+             the reference's drivers call (C ABI whb_solve_host)
 roofline   = the dominant (multi-step) kernel: bytes per launch / average launch duration
              (CUDA events on the launching stream) against the measured HBM peak.  ``frac``
              uses the kernel's DRAM bytes per launch from the ncu capture of THIS build

@@ -49,7 +49,8 @@ def source_sha16() -> str:
     per-compile module ids), so measurements are tied to the build inputs instead."""
     import hashlib
 
-    h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
+    # (flags without the checkout's absolute include path: the same sources hash the same anywhere)
+    h = hashlib.sha256(" ".join(f for f in NVCC_FLAGS if not f.startswith(ROOT)).encode())
     csrc = os.path.join(PKG, "csrc")
     for fn in sorted(os.listdir(csrc)):
         if fn.endswith((".cu", ".cuh", ".h")):

@@ -53,10 +53,59 @@
 #define T3_UNROLL_(n) T3_PRAGMA_(unroll n)
 #define T3_UNROLL(n) T3_UNROLL_(n)
 
+// L2 policy experiments (config 4 is DRAM-bound at 6.0 TB/s on 77.6 GB per pass, 29 % above the
+// compulsory bytes: the halo boxes of neighbouring tiles miss L2): WHB_T3_STCS streaming output
+// stores, WHB_T3_LDCS streaming acc / v loads, WHB_T3_HINT evict-last TMA loads
+#ifndef WHB_T3_STCS
+#define WHB_T3_STCS 0
+#endif
+#ifndef WHB_T3_LDCS
+#define WHB_T3_LDCS 0
+#endif
+#ifndef WHB_T3_HINT
+#define WHB_T3_HINT 0
+#endif
+// L2 prefetch distance of the acc / v loads in planes (0: none)
+#ifndef WHB_T3_PF
+#define WHB_T3_PF 4
+#endif
+
 namespace t3 {
 
 __device__ __forceinline__ void prefetch_l2(const void *p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+// tma_load_3d with an L2 cache-policy operand
+__device__ __forceinline__ void tma_load_3d_hint(void *sdst, const CUtensorMap *map, int c0, int c1, int c2,
+                                                 uint64_t *bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(bulk::smem_u32(sdst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bulk::smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+__device__ __forceinline__ void store2(double *p, double2 v) {
+#if WHB_T3_STCS
+    __stcs(reinterpret_cast<double2 *>(p), v);
+#else
+    *reinterpret_cast<double2 *>(p) = v;
+#endif
+}
+
+__device__ __forceinline__ double2 load2_once(const double *p) {
+#if WHB_T3_LDCS
+    return __ldcs(reinterpret_cast<const double2 *>(p));
+#else
+    return __ldcg(reinterpret_cast<const double2 *>(p));
+#endif
 }
 
 using bulk::fence_proxy_async;
@@ -115,6 +164,7 @@ struct Scal {
 // pass); part_off: first residual-partial slot of the launch.
 struct RowWin {
     int j_off, j_end, part_off;
+    int jt_fast;  // CTA -> tile order: row tiles fastest (1) or column tiles fastest (0, as launched)
 };
 
 // One CTA's march.  K1: kind of step s (FIRST when s == 0); K2: MID, or LAST when step s+2 ends
@@ -123,7 +173,8 @@ struct RowWin {
 // the main shape, the grid's), k0: first output column.
 template <int ST, int K1, int K2, bool ZF, int GM, int LX>
 __device__ __forceinline__ void body(double *smem, const Geom &g, const Member *__restrict__ members, int s,
-                                     int i_begin, int i_end, int chunk_len, int JTY, int JT, int k0, const RowWin rw,
+                                     int i_begin, int i_end, int chunk_len, int JTY, int JT, int yidx, int lin, int k0,
+                                     const RowWin rw,
                                      const Scal &sc, const CUtensorMap *tm_w, const CUtensorMap *tm_p,
                                      const CUtensorMap *tm_f) {
     using S = Shape<LX>;
@@ -143,14 +194,14 @@ __device__ __forceinline__ void body(double *smem, const Geom &g, const Member *
     const int lane = threadIdx.x & 31;
     const int cl = lane % LX;                  // column pair within the row
     const int rho = w * S::RPW + lane / LX;    // level-1 region row (y = j0 - 2 + rho)
-    const int jt = blockIdx.y % JTY;
-    const int ch = blockIdx.y / JTY;
+    const int jt = yidx % JTY;  // yidx = chunk * JTY + row tile
+    const int ch = yidx / JTY;
     const int j0 = rw.j_off + jt * S::BY;
     const int i0 = i_begin + ch * chunk_len;
     const int i1 = min(i_end, i0 + chunk_len);
     if (i0 >= i1 || jt >= JT) {
         if (K2 == K_LAST && m.out_mode == WHB_OUT_FPI && threadIdx.x == 0)
-            m.partials[rw.part_off + blockIdx.y * gridDim.x + blockIdx.x] = 0.0;
+            m.partials[rw.part_off + lin] = 0.0;
         return;
     }
     double *w2g = level_ptr(m, s + 2);
@@ -162,14 +213,23 @@ __device__ __forceinline__ void body(double *smem, const Geom &g, const Member *
     // staged planes i0-3 .. i1+2; stage slot of plane p: (p - (i0 - 3)) % ST
     const int pfirst = i0 - 3;
     const int plast = i1 + 2;
+#if WHB_T3_HINT
+    const uint64_t pol = policy_evict_last();
+#endif
     auto issue = [&](int plane) {
         const int slot = (plane - pfirst) % ST;
         double *st = smem + (size_t)slot * STAGE;
         uint64_t *bar = bars + slot;
         mbar_expect_tx(bar, stage_bytes);
+#if WHB_T3_HINT
+        tma_load_3d_hint(st, tm_w, k0 - 4, j0 - 3, plane, bar, pol);
+        if (LOAD_P) tma_load_3d_hint(st + W_EL, tm_p, k0 - 2, j0 - 2, plane, bar, pol);
+        if (!ZF) tma_load_3d_hint(st + W_EL + P_EL, tm_f, k0 - 2, j0 - 2, plane, bar, pol);
+#else
         tma_load_3d(st, tm_w, k0 - 4, j0 - 3, plane, bar);
         if (LOAD_P) tma_load_3d(st + W_EL, tm_p, k0 - 2, j0 - 2, plane, bar);
         if (!ZF) tma_load_3d(st + W_EL + P_EL, tm_f, k0 - 2, j0 - 2, plane, bar);
+#endif
     };
 
     if (threadIdx.x == 0) {
@@ -234,7 +294,7 @@ __device__ __forceinline__ void body(double *smem, const Geom &g, const Member *
     acc_n = (K1 != K_FIRST && okk) ? ld2(m.acc, i0) : z2;
     v_n = (want_v && okk) ? ld2(m.v, i0) : z2;
     if (okk)
-        for (int q = 1; q < 4 && i0 + q < i1; ++q) {
+        for (int q = 1; q < WHB_T3_PF && i0 + q < i1; ++q) {
             if (K1 != K_FIRST) prefetch_l2(m.acc + (long long)(i0 + q) * S0 + pbase);
             if (want_v) prefetch_l2(m.v + (long long)(i0 + q) * S0 + pbase);
         }
@@ -349,9 +409,9 @@ __device__ __forceinline__ void body(double *smem, const Geom &g, const Member *
                 if (out3 && okk) {
                     // HBM -> L2 four planes ahead, so the one-plane-ahead register loads hit L2
                     // (measured: without it 20 % of the warp samples waited on them)
-                    if (p3 + 4 < i1) {
-                        if (K1 != K_FIRST) prefetch_l2(m.acc + (long long)(p3 + 4) * S0 + pbase);
-                        if (want_v) prefetch_l2(m.v + (long long)(p3 + 4) * S0 + pbase);
+                    if (WHB_T3_PF > 0 && p3 + WHB_T3_PF < i1) {
+                        if (K1 != K_FIRST) prefetch_l2(m.acc + (long long)(p3 + WHB_T3_PF) * S0 + pbase);
+                        if (want_v) prefetch_l2(m.v + (long long)(p3 + WHB_T3_PF) * S0 + pbase);
                     }
                     const double2 acc_c = acc_n, v_c = v_n;
                     // acc (+ c0 W^0 on the first pass) + c1 W^{s+1} + c2 W^{s+2} + c3 W^{s+3}, in step order
@@ -368,9 +428,9 @@ __device__ __forceinline__ void body(double *smem, const Geom &g, const Member *
                     const long long p = (long long)p3 * S0 + pbase;
                     if (K2 == K_MID) {
                         if (ok0 && ok1) {
-                            *reinterpret_cast<double2 *>(w2g + p) = q22;
-                            *reinterpret_cast<double2 *>(w3g + p) = make_double2(a3, b3);
-                            *reinterpret_cast<double2 *>(m.acc + p) = make_double2(s0, s1);
+                            store2(w2g + p, q22);
+                            store2(w3g + p, make_double2(a3, b3));
+                            store2(m.acc + p, make_double2(s0, s1));
                         } else {
                             if (ok0) { w2g[p] = q22.x; w3g[p] = a3; m.acc[p] = s0; }
                             if (ok1) { w2g[p + 1] = q22.y; w3g[p + 1] = b3; m.acc[p + 1] = s1; }
@@ -396,8 +456,8 @@ __device__ __forceinline__ void body(double *smem, const Geom &g, const Member *
                 // copy the loaded register right away, i.e. wait for the load)
                 const int pn = min(max(p3 + 1, i0), i1 - 1);
                 const long long o = (long long)pn * S0 + pbase;
-                if (K1 != K_FIRST) acc_n = __ldcg(reinterpret_cast<const double2 *>(m.acc + o));
-                if (K2 == K_LAST) v_n = __ldcg(reinterpret_cast<const double2 *>((want_v ? m.v : m.acc) + o));
+                if (K1 != K_FIRST) acc_n = load2_once(m.acc + o);
+                if (K2 == K_LAST) v_n = load2_once((want_v ? m.v : m.acc) + o);
             }
             sl_i = sl_n;
             sl_n = sl_n + 1 == ST ? 0 : sl_n + 1;
@@ -414,7 +474,7 @@ __device__ __forceinline__ void body(double *smem, const Geom &g, const Member *
     else run(F_{}, F_{});
     if (K2 == K_LAST && m.out_mode == WHB_OUT_FPI) {
         const double t = block_sum(rsum);
-        if (threadIdx.x == 0) m.partials[rw.part_off + blockIdx.y * gridDim.x + blockIdx.x] = t;
+        if (threadIdx.x == 0) m.partials[rw.part_off + lin] = t;
     }
 }
 
@@ -435,13 +495,26 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               const __grid_constant__ CUtensorMap te_w, const __grid_constant__ CUtensorMap te_p,
               const __grid_constant__ CUtensorMap te_f) {
     extern __shared__ __align__(128) double smem[];
-    if (LXE != 32 && blockIdx.x == gridDim.x - 1)
-        // the edge column's gridDim.y CTAs: JTE row tiles x chunks of chunk_len_e planes (the rest exit)
-        body<ST, K1, K2, ZF, GM, LXE>(smem, g, members, s, i_begin, i_end, chunk_len_e, JTE, JTE,
-                                      (int)blockIdx.x * Main::TX, rw, sc, &te_w, &te_p, &te_f);
+    // CTA -> tile: the hardware starts CTAs in linear order (blockIdx.x fastest).  Column tiles
+    // fastest (as launched) keeps the CTAs that run at the same time on whole grid rows: 262 vs 240
+    // Gpts/s on 1025^3 against row tiles fastest (same DRAM bytes: CTAs 12 rows apart in one 480-B
+    // column camp on the same channels); when a chunk's tiles all fit in one wave (257^3: 110) row
+    // tiles fastest is ahead, 237 vs 227.
+    const int lin = blockIdx.y * gridDim.x + blockIdx.x;
+    int bx = blockIdx.x, yidx = blockIdx.y;
+    if (rw.jt_fast) {
+        const int per = gridDim.x * JT;
+        const int chl = lin / per, r = lin - chl * per;
+        bx = r / JT;
+        yidx = chl * JT + (r - bx * JT);
+    }
+    if (LXE != 32 && bx == (int)gridDim.x - 1)
+        // the edge column's JT * chunks CTAs: JTE row tiles x chunks of chunk_len_e planes (the rest exit)
+        body<ST, K1, K2, ZF, GM, LXE>(smem, g, members, s, i_begin, i_end, chunk_len_e, JTE, JTE, yidx, lin,
+                                      bx * Main::TX, rw, sc, &te_w, &te_p, &te_f);
     else
-        body<ST, K1, K2, ZF, GM, 32>(smem, g, members, s, i_begin, i_end, chunk_len, JT, JT,
-                                     (int)blockIdx.x * Main::TX, rw, sc, &tm_w, &tm_p, &tm_f);
+        body<ST, K1, K2, ZF, GM, 32>(smem, g, members, s, i_begin, i_end, chunk_len, JT, JT, yidx, lin,
+                                     bx * Main::TX, rw, sc, &tm_w, &tm_p, &tm_f);
 }
 
 }  // namespace t3

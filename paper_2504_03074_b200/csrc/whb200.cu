@@ -1620,9 +1620,18 @@ int tensor_map(whb_ctx *c, const double *base, int box_w, int box_h, CUtensorMap
     cuuint64_t strides[2] = {(cuuint64_t)c->P * sizeof(double), (cuuint64_t)c->S0 * sizeof(double)};
     cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
     cuuint32_t estr[3] = {1, 1, 1};
+    // L2 promotion (the granularity a box row is fetched into L2 with): WHB_TMA_PROMO=0|64|128|256.
+    // Measured on config 4 (DRAM read per three-step pass, pass time): 256 B 51.1 GB 12.92 ms, 128 B
+    // 48.4 GB 12.57 ms, none 48.3 GB 12.54 ms, 64 B 46.7 GB 12.34 ms.
+    static const CUtensorMapL2promotion promo = [] {
+        const char *e = getenv("WHB_TMA_PROMO");
+        const int v = e ? atoi(e) : 64;
+        return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+             : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    }();
     CUresult r = g_encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(base), dims, strides, box,
-                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(WHB_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
     c->tmaps.emplace(key, m);
     *out = m;
@@ -1763,7 +1772,11 @@ int launch_t3(whb_ctx *c, int s, bool last, int ib, int ie, int cl) {
         const int nche = std::max(1, (jt * nch) / std::max(1, jte));
         cle = std::max(1, (ie - ib + nche - 1) / nche);
     }
-    const t3::RowWin rw{c->win_j0, c->win_j1, c->win_po};
+    int sms3 = 148;
+    cudaDeviceGetAttribute(&sms3, cudaDevAttrMultiProcessorCount, c->device);
+    static const char *ord = getenv("WHB_T3_ORDER");  // jt | x: force a CTA -> tile order (A/B)
+    const int jt_fast = ord ? (std::string(ord) == "jt") : (c->gx3 * jt <= sms3);
+    const t3::RowWin rw{c->win_j0, c->win_j1, c->win_po, jt_fast};
     const int gm = geom_mode(c);
     auto go = [&](auto k1, auto k2, auto zft, auto gmt) {
         t3_by_lxe(lxe, [&](auto lx) {

@@ -1,7 +1,7 @@
 #!/usr/bin/env bash
 # Round-end measurement pass on one B200 (run under gpurun from the repo root):
-#   bench lines for every workload (ours + reference arm), ncu launch lists of the same bench
-#   commands, and one `ncu --set full` capture of each dominant kernel.  Outputs land in
+#   ncu launch lists of the bench commands and one `ncu --set full` capture of each dominant kernel
+#   (each command first runs plainly), then the bench lines of every workload (ours + reference arm).  Outputs land in
 #   gpurun_out/m/; tools/collect_profiles.py turns them into profiles/<round>/ (+ traffic.json
 #   keyed by the library's sha256).  MEASURE_PART = bench | ncu | all; MEASURE_WORKLOADS selects.
 set -u
@@ -13,12 +13,6 @@ python -c "from paper_2504_03074_b200 import _build; print(_build.source_sha16()
 
 PART=${MEASURE_PART:-all}
 WL=${MEASURE_WORKLOADS:-cfg4 cfg2 cfg3 cfg5 cfg1 p4 imp2}
-if [ "$PART" != ncu ]; then
-for w in $WL; do
-  timeout 900 python bench.py --workload $w > $OUT/bench_$w.json 2> $OUT/bench_$w.err
-  timeout 900 python bench.py --workload $w --impl reference > $OUT/bench_reference_$w.json 2> $OUT/bench_reference_$w.err
-done
-fi
 if [ "$PART" != bench ]; then
 L="--metrics gpu__time_duration.sum --clock-control none --csv"
 F="--set full --clock-control none --import-source on -c 1"
@@ -39,6 +33,17 @@ for w in $WL; do
       timeout 2400 ncu $F -k regex:$K -s $S -o $OUT/ncu_$w $C > $OUT/ncu_f_$w.log 2>&1
     fi
   fi
+done
+fi
+# the ncu summaries first: the bench lines below then read this build's DRAM bytes per launch
+if [ "$PART" != bench ]; then
+  python tools/collect_profiles.py $RND $OUT $OUT/collected > $OUT/collect.log 2>&1
+  cp $OUT/collected/profiles/traffic.json profiles/traffic.json
+fi
+if [ "$PART" != ncu ]; then
+for w in $WL; do
+  timeout 900 python bench.py --workload $w > $OUT/bench_$w.json 2> $OUT/bench_$w.err
+  timeout 900 python bench.py --workload $w --impl reference > $OUT/bench_reference_$w.json 2> $OUT/bench_reference_$w.err
 done
 fi
 # summarise on the box (ncu -i) and drop the reports: gpurun copies back at most 64 MiB
