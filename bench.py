@@ -781,6 +781,10 @@ def run_ours(args, dist, ws, rank, local):
     avg_launch_s = step_s / max(1, step_launches)
     bytes_per_launch_comp = own_bpu * units_rank / max(1, step_launches)
     traffic, traffic_src = load_traffic(args.workload)
+    if traffic and getattr(wl, "members", 1) > 1:
+        # a batched run's launches carry the members still active (64 down to 1): the capture, one
+        # launch of all members, is not the average launch
+        traffic, traffic_src = None, "batched launches differ in member count; the ncu capture is one launch of all members"
     if traffic:
         achieved, frac_source = traffic / avg_launch_s / 1e9, (
             "ncu DRAM bytes per launch of this build (profiles/traffic.json: " + str(traffic_src) + ")")
