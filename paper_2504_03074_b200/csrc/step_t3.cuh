@@ -130,7 +130,8 @@ struct Shape {
     static constexpr int WR = NR + 2;                // staged W^s rows: j0-3 .. j0+BY+2
     static constexpr int W_EL = (WR * RW + 15) / 16 * 16;  // 128-B aligned sub-buffers for TMA
     static constexpr int P_EL = NR * LW;             // W^{s-1} / f box (the level-1 region): 1024
-    static constexpr int STAGE = W_EL + 2 * P_EL;    // main: 3280 doubles = 26.2 KB
+    static constexpr int A_EL = (BY * TX + 15) / 16 * 16;  // filter-sum box (the tile), of the plane 4 behind
+    static constexpr int STAGE = W_EL + 2 * P_EL + A_EL;   // main: 4000 doubles = 32 KB
     static constexpr int L1_EL = NR * LW;            // level-1 plane
     static constexpr int L2_EL = (NR - 2) * LW;      // level-2 plane (rows j0-1 .. j0+BY)
     template <int ST>
@@ -176,7 +177,7 @@ __device__ __forceinline__ void body(double *smem, const Geom &g, const Member *
                                      int i_begin, int i_end, int chunk_len, int JTY, int JT, int yidx, int lin, int k0,
                                      const RowWin rw,
                                      const Scal &sc, const CUtensorMap *tm_w, const CUtensorMap *tm_p,
-                                     const CUtensorMap *tm_f) {
+                                     const CUtensorMap *tm_f, const CUtensorMap *tm_a) {
     using S = Shape<LX>;
     constexpr int LW = S::LW, RW = S::RW, NR = S::NR, W_EL = S::W_EL, P_EL = S::P_EL, STAGE = S::STAGE;
     constexpr int L1_EL = S::L1_EL, L2_EL = S::L2_EL;
@@ -209,10 +210,13 @@ __device__ __forceinline__ void body(double *smem, const Geom &g, const Member *
     const long long S0 = g.S0;
     const int P = g.P;
 
-    constexpr uint32_t stage_bytes = (uint32_t)((RW * S::WR + (LOAD_P ? P_EL : 0) + (ZF ? 0 : P_EL)) * 8);
-    // staged planes i0-3 .. i1+2; stage slot of plane p: (p - (i0 - 3)) % ST
+    constexpr int A_OFF = W_EL + 2 * P_EL;  // the filter sum of plane p - 4 rides in the stage of plane p
+    constexpr uint32_t stage_bytes =
+        (uint32_t)((RW * S::WR + (LOAD_P ? P_EL : 0) + (ZF ? 0 : P_EL) + (LOAD_P ? S::BY * S::TX : 0)) * 8);
+    // staged planes i0-3 .. i1+2 (.. i1+3 when acc rides along: the last output plane's acc comes with
+    // the stage of plane i1+3); stage slot of plane p: (p - (i0 - 3)) % ST
     const int pfirst = i0 - 3;
-    const int plast = i1 + 2;
+    const int plast = i1 + (LOAD_P ? 3 : 2);
 #if WHB_T3_HINT
     const uint64_t pol = policy_evict_last();
 #endif
@@ -230,6 +234,8 @@ __device__ __forceinline__ void body(double *smem, const Geom &g, const Member *
         if (LOAD_P) tma_load_3d(st + W_EL, tm_p, k0 - 2, j0 - 2, plane, bar);
         if (!ZF) tma_load_3d(st + W_EL + P_EL, tm_f, k0 - 2, j0 - 2, plane, bar);
 #endif
+        // acc of the plane whose outputs are formed while this stage is current (iteration `plane`)
+        if (LOAD_P) tma_load_3d(st + A_OFF, tm_a, k0, j0, plane - 4, bar);
     };
 
     if (threadIdx.x == 0) {
@@ -274,7 +280,7 @@ __device__ __forceinline__ void body(double *smem, const Geom &g, const Member *
     double2 q10, q11, q12, q13, q14;       // q1k = level 1 at plane i-k
     double2 q20, q21, q22, q23;            // q2k = level 2 at plane i-2-k
     double2 fq0, fq1, fq2, fq3, fq4;       // fqk = f at plane i-k
-    double2 acc_n, v_n;
+    double2 v_n;
     double rsum = 0.0;
 
     // W^s centres of planes i0-3 and i0-2 (the first iteration, i = i0-2, adds plane i0-1); the
@@ -291,13 +297,10 @@ __device__ __forceinline__ void body(double *smem, const Geom &g, const Member *
     q10 = q11 = q12 = q13 = q14 = z2;
     q20 = q21 = q22 = q23 = z2;
     fq0 = fq1 = fq2 = fq3 = fq4 = z2;
-    acc_n = (K1 != K_FIRST && okk) ? ld2(m.acc, i0) : z2;
     v_n = (want_v && okk) ? ld2(m.v, i0) : z2;
-    if (okk)
-        for (int q = 1; q < WHB_T3_PF && i0 + q < i1; ++q) {
-            if (K1 != K_FIRST) prefetch_l2(m.acc + (long long)(i0 + q) * S0 + pbase);
-            if (want_v) prefetch_l2(m.v + (long long)(i0 + q) * S0 + pbase);
-        }
+    if (okk && want_v)
+        for (int q = 1; q < WHB_T3_PF && i0 + q < i1; ++q) prefetch_l2(m.v + (long long)(i0 + q) * S0 + pbase);
+    const int arow = (rho - 2) * S::TX + 2 * (cl - 1);  // own pair in the staged acc box (own threads only)
     __syncthreads();  // every thread has read plane pfirst: its slot takes plane pfirst + ST
     if (threadIdx.x == 0 && pfirst + ST <= plast) {
         fence_proxy_async();
@@ -350,6 +353,8 @@ __device__ __forceinline__ void body(double *smem, const Geom &g, const Member *
             const double x1h = st[wrow0 + 2];
             const double2 pv = LOAD_P ? lds2(st + W_EL + prow0) : z2;
             if (!ZF) fq0 = lds2(st + W_EL + P_EL + prow0);
+            // (read before the arrive: the stage is refilled once every thread has arrived)
+            const double2 acc_c = (LOAD_P && D3 && own) ? lds2(st + A_OFF + arow) : z2;
             double2 y2lo = z2, y2hi = z2, y3lo = z2, y3hi = z2;
             double x2l = 0.0, x2h = 0.0, x3l = 0.0, x3h = 0.0;
             if (D2) {
@@ -409,11 +414,9 @@ __device__ __forceinline__ void body(double *smem, const Geom &g, const Member *
                 if (out3 && okk) {
                     // HBM -> L2 four planes ahead, so the one-plane-ahead register loads hit L2
                     // (measured: without it 20 % of the warp samples waited on them)
-                    if (WHB_T3_PF > 0 && p3 + WHB_T3_PF < i1) {
-                        if (K1 != K_FIRST) prefetch_l2(m.acc + (long long)(p3 + WHB_T3_PF) * S0 + pbase);
-                        if (want_v) prefetch_l2(m.v + (long long)(p3 + WHB_T3_PF) * S0 + pbase);
-                    }
-                    const double2 acc_c = acc_n, v_c = v_n;
+                    if (WHB_T3_PF > 0 && want_v && p3 + WHB_T3_PF < i1)
+                        prefetch_l2(m.v + (long long)(p3 + WHB_T3_PF) * S0 + pbase);
+                    const double2 v_c = v_n;
                     // acc (+ c0 W^0 on the first pass) + c1 W^{s+1} + c2 W^{s+2} + c3 W^{s+3}, in step order
                     double s0, s1;
                     if (K1 == K_FIRST) {  // timestep.py:284 then :298 per step
@@ -454,10 +457,10 @@ __device__ __forceinline__ void body(double *smem, const Geom &g, const Member *
                 // load lands in the loop-carried registers), unconditionally and from an
                 // in-bounds plane (a predicated load merged with the old value made the compiler
                 // copy the loaded register right away, i.e. wait for the load)
-                const int pn = min(max(p3 + 1, i0), i1 - 1);
-                const long long o = (long long)pn * S0 + pbase;
-                if (K1 != K_FIRST) acc_n = load2_once(m.acc + o);
-                if (K2 == K_LAST) v_n = load2_once((want_v ? m.v : m.acc) + o);
+                if (K2 == K_LAST) {
+                    const int pn = min(max(p3 + 1, i0), i1 - 1);
+                    v_n = load2_once((want_v ? m.v : m.acc) + (long long)pn * S0 + pbase);
+                }
             }
             sl_i = sl_n;
             sl_n = sl_n + 1 == ST ? 0 : sl_n + 1;
@@ -492,8 +495,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     t3_kernel(Geom g, const Member *__restrict__ members, int s, int i_begin, int i_end, int chunk_len, int JT,
               int JTE, int chunk_len_e, const RowWin rw, const Scal sc, const __grid_constant__ CUtensorMap tm_w,
               const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_f,
-              const __grid_constant__ CUtensorMap te_w, const __grid_constant__ CUtensorMap te_p,
-              const __grid_constant__ CUtensorMap te_f) {
+              const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap te_w,
+              const __grid_constant__ CUtensorMap te_p, const __grid_constant__ CUtensorMap te_f,
+              const __grid_constant__ CUtensorMap te_a) {
     extern __shared__ __align__(128) double smem[];
     // CTA -> tile: the hardware starts CTAs in linear order (blockIdx.x fastest).  Column tiles
     // fastest (as launched) keeps the CTAs that run at the same time on whole grid rows: 262 vs 240
@@ -511,10 +515,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (LXE != 32 && bx == (int)gridDim.x - 1)
         // the edge column's JT * chunks CTAs: JTE row tiles x chunks of chunk_len_e planes (the rest exit)
         body<ST, K1, K2, ZF, GM, LXE>(smem, g, members, s, i_begin, i_end, chunk_len_e, JTE, JTE, yidx, lin,
-                                      bx * Main::TX, rw, sc, &te_w, &te_p, &te_f);
+                                      bx * Main::TX, rw, sc, &te_w, &te_p, &te_f, &te_a);
     else
         body<ST, K1, K2, ZF, GM, 32>(smem, g, members, s, i_begin, i_end, chunk_len, JT, JT, yidx, lin,
-                                     bx * Main::TX, rw, sc, &tm_w, &tm_p, &tm_f);
+                                     bx * Main::TX, rw, sc, &tm_w, &tm_p, &tm_f, &tm_a);
 }
 
 }  // namespace t3

@@ -1047,7 +1047,7 @@ cudaError_t tb2_set_attrs(size_t smem) {
 
 // Three-step 3D kernel (step_t3.cuh): 6 TMA stages of 26 KB + the level-1/2 rings (206-225 KB), 1 CTA/SM.
 #ifndef WHB_S3_ST
-#define WHB_S3_ST 6
+#define WHB_S3_ST 5
 #endif
 constexpr int S3_ST = WHB_S3_ST;
 constexpr int S3_THREADS = t3::NTHREADS;
@@ -1727,20 +1727,22 @@ int launch_t3(whb_ctx *c, int s, bool last, int ib, int ie, int cl) {
     const bool zf = c->cur_zf != 0;
     const Member &m0 = c->h_members[0];
     const MemberHost &mh = c->mem[c->order[0]];
-    CUtensorMap tw, tp, tf, ew, ep, ef;
+    CUtensorMap tw, tp, tf, ta, ew, ep, ef, ea;
     std::memset(&tp, 0, sizeof(tp));
     std::memset(&tf, 0, sizeof(tf));
     using SM = t3::Main;
     WHB_TRY(tensor_map(c, level_ptr(m0, s), SM::RW, SM::WR, &tw));
     WHB_TRY(tensor_map(c, level_ptr(m0, s - 1), SM::LW, SM::NR, &tp));
     if (m0.f) WHB_TRY(tensor_map(c, m0.f, SM::LW, SM::NR, &tf));
-    ew = tw, ep = tp, ef = tf;
+    WHB_TRY(tensor_map(c, m0.acc, SM::TX, SM::BY, &ta));
+    ew = tw, ep = tp, ef = tf, ea = ta;
     const int lxe_ = (c->win_j1 != INT_MAX && c->win_lxe) ? c->win_lxe : c->lxe3;
     if (lxe_ != 32) {  // boxes of the ragged-edge shape
         const int lw = 2 * lxe_, nr = 16 * (32 / lxe_);
         WHB_TRY(tensor_map(c, level_ptr(m0, s), lw + 4, nr + 2, &ew));
         WHB_TRY(tensor_map(c, level_ptr(m0, s - 1), lw, nr, &ep));
         if (m0.f) WHB_TRY(tensor_map(c, m0.f, lw, nr, &ef));
+        WHB_TRY(tensor_map(c, m0.acc, lw - 4, nr - 4, &ea));
     }
     t3::Scal sc;
     const bool first = (s == 0);
@@ -1782,7 +1784,7 @@ int launch_t3(whb_ctx *c, int s, bool last, int ib, int ie, int cl) {
         t3_by_lxe(lxe, [&](auto lx) {
             t3_fn<decltype(k1)::value, decltype(k2)::value, decltype(zft)::value, decltype(gmt)::value,
                   decltype(lx)::value>()<<<grid, S3_THREADS, t3_smem(lxe), c->stream>>>(
-                c->geom, c->d_members, s, ib, ie, cl, jt, jte, cle, rw, sc, tw, tp, tf, ew, ep, ef);
+                c->geom, c->d_members, s, ib, ie, cl, jt, jte, cle, rw, sc, tw, tp, tf, ta, ew, ep, ef, ea);
         });
     };
     using KF = std::integral_constant<int, K_FIRST>;
